@@ -1,0 +1,206 @@
+/*
+ * tdpg.h — C-ABI of the B200-native timing-driven global placement engine.
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes, returns
+ * an int status (TDPG_OK == 0) and never lets a C++ exception cross the ABI.
+ * On failure the thread-local message from tdpg_last_error() carries the
+ * reference's exception text (proj/include/tdp/errors.hpp:9-42, e.g.
+ * "non-finite value: ... at iteration N", "combinational cycle: ...") and
+ * tdpg_last_error_kind() the exception class.
+ *
+ * One session = one design resident in HBM (structure-of-arrays netlist,
+ * levelized timing-graph CSR, density grid, pin-pair ledger, optimizer
+ * state).  Host pointers are read/written synchronously; functions named
+ * *_dev operate on device-resident state only and are stream-ordered.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   tdpg_session_create      Netlist::finalize + build_timing_graph   src/netlist.cpp:5-21, src/timing_graph.cpp:49-138
+ *   tdpg_pin_positions       pin_positions                            src/netlist.cpp:23-32
+ *   tdpg_wirelength          wa_wirelength per net + hpwl_total       src/wirelength.cpp:49-58, :74-85
+ *   tdpg_density             DensityGrid::evaluate                    src/density.cpp:66-158
+ *   tdpg_pp_loss             pin_pair_loss                            src/pin_pairs.cpp:17-49
+ *   tdpg_pp_set/get/update   PinPairWeights + update_pair_weights     include/tdp/pin_pairs.hpp:16, src/pin_pairs.cpp:7-15
+ *   tdpg_objective           objective_and_gradient                   src/placer.cpp:275-343
+ *   tdpg_adam_step           AdamState::step                          src/placer.cpp:345-356
+ *   tdpg_sta                 run_sta (arrival/required/slack/tns/wns) src/sta.cpp:33-143
+ *   tdpg_extract_endpoint    report_timing_endpoint (k = 1)           src/paths.cpp:167-189
+ *   tdpg_paths_hits          collect_pin_pairs                        src/paths.cpp:191-203
+ *   tdpg_place               run_placement                            src/placer.cpp:358-484
+ *   tdpg_generate            generate_synthetic                       src/generator.cpp:60-263
+ */
+#ifndef TDPG_H
+#define TDPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    TDPG_OK = 0,
+    TDPG_ERR_PARSE = 1,       /* tdp::ParseError                       */
+    TDPG_ERR_VALIDATION = 2,  /* tdp::ValidationError                  */
+    TDPG_ERR_CYCLE = 3,       /* tdp::CycleError (a ValidationError)   */
+    TDPG_ERR_ENDPOINT = 4,    /* tdp::EndpointError (a ValidationError) */
+    TDPG_ERR_GRAPH = 5,       /* tdp::GraphError                       */
+    TDPG_ERR_NONFINITE = 6,   /* tdp::NonFiniteError                   */
+    TDPG_ERR_CUDA = 7,        /* CUDA runtime failure / no device      */
+    TDPG_ERR_INTERNAL = 9
+};
+
+/* Flat structure-of-arrays view of tdp::Design (include/tdp/netlist.hpp:11-93).
+ * Pin ids, cell ids and net ids are array indices, as in the reference.  */
+typedef struct tdpg_netlist {
+    int32_t n_cells;
+    int32_t n_pins;
+    int32_t n_nets;
+    int32_t n_sources;
+    int32_t n_endpoints;
+    const double* cell_w;      /* [n_cells]   Cell::width                     */
+    const double* cell_h;      /* [n_cells]   Cell::height                    */
+    const double* cell_delay;  /* [n_cells]   Cell::delay                     */
+    const uint8_t* cell_fixed; /* [n_cells]   Cell::is_fixed                  */
+    const int32_t* pin_cell;   /* [n_pins]    owner cell id or -1 (terminal)  */
+    const double* pin_term;    /* [2*n_pins]  terminal_pos (x, y)             */
+    const double* pin_off;     /* [2*n_pins]  offset (x, y)                   */
+    const uint8_t* pin_dir;    /* [n_pins]    0 = Input, 1 = Output           */
+    const double* pin_cap;     /* [n_pins]    load_cap                        */
+    const int32_t* net_start;  /* [n_nets+1]  CSR into net_pins               */
+    const int32_t* net_pins;   /* [net_start[n_nets]] driver, then sinks      */
+    const int32_t* sources;    /* [n_sources]                                 */
+    const int32_t* endpoints;  /* [n_endpoints]                               */
+    double clock_period;
+    double r_unit;
+    double c_unit;
+    double core[4];            /* x_lo, y_lo, x_hi, y_hi                      */
+    const char* const* pin_names; /* optional [n_pins], only for error text  */
+} tdpg_netlist;
+
+/* OptimizerConfig (include/tdp/placer.hpp:22-57), same field meaning. */
+typedef struct tdpg_config {
+    double gamma_frac;
+    int32_t grid_nx, grid_ny;
+    double target_density;
+    double beta;
+    int32_t pp_loss;           /* 0 quadratic, 1 linear                       */
+    int32_t net_weighting;     /* bool                                        */
+    int32_t m;
+    double w0, w1;
+    int32_t timing_start_iter;
+    int32_t extraction;        /* 0 endpoint (the only policy on device yet)  */
+    int32_t k;
+    int32_t max_iters;
+    double stop_overflow;
+    double mu;
+    double lambda0;            /* <= 0 selects gradient-norm balancing        */
+    double lambda_max;
+    double step0_frac;
+    double step_decay;
+    double adam_beta1, adam_beta2, adam_eps;
+    uint64_t seed;
+    double init_jitter_frac;
+    int32_t threads;           /* accepted for drop-in parity; ignored        */
+} tdpg_config;
+
+void tdpg_config_default(tdpg_config* cfg);
+
+/* One TraceRow (include/tdp/placer.hpp:67-79). */
+typedef struct tdpg_trace_row {
+    int32_t iter;
+    int32_t has_timing;
+    double hpwl, overflow, tns, wns, wl_term, density_term, pp_term, lambda, beta_pp;
+} tdpg_trace_row;
+
+typedef struct tdpg_session tdpg_session;
+
+const char* tdpg_last_error(void);
+int tdpg_last_error_kind(void);
+const char* tdpg_version(void);
+int tdpg_device_count(void);
+
+/* ---- session -------------------------------------------------------- */
+int tdpg_session_create(const tdpg_netlist* nl, tdpg_session** out);
+int tdpg_session_destroy(tdpg_session* s);
+/* Timing graph facts: counts[0..3] = n_net_arcs, n_cell_arcs, n_levels, max_level;
+ * level may be NULL, else [n_pins] level per pin (timing_graph.hpp:33). */
+int tdpg_graph_info(tdpg_session* s, int32_t counts[4], int32_t* level);
+/* arcs in reference id order: from/to/kind(0 net, 1 cell)/owner, each [n_arcs] (any may be NULL) */
+int tdpg_graph_arcs(tdpg_session* s, int32_t* from, int32_t* to, int32_t* kind, int32_t* owner);
+
+/* ---- positions ------------------------------------------------------ */
+int tdpg_set_positions(tdpg_session* s, const double* cell_xy);   /* [2*n_cells] host */
+int tdpg_get_positions(tdpg_session* s, double* cell_xy);
+int tdpg_pin_positions(tdpg_session* s, double* pin_xy);          /* [2*n_pins] out    */
+
+/* ---- objective terms (at the session's current positions) ----------- */
+/* wl = sum_e w_e * WA_e, hpwl exact; pin_grad [2*n_pins] (w_e-scaled) may be NULL. */
+int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* wl, double* hpwl,
+                    double* pin_grad);
+/* DensityGrid(nx, ny, target_density) then evaluate; d_cell [2*n_cells] may be NULL. */
+int tdpg_set_grid(tdpg_session* s, int32_t nx, int32_t ny, double target_density);
+int tdpg_density(tdpg_session* s, double* value, double* overflow, double* d_cell);
+
+/* ---- pin-pair ledger (PinPairWeights) ------------------------------- */
+int tdpg_pp_set(tdpg_session* s, int64_t q, const int32_t* a, const int32_t* b, const double* w);
+int tdpg_pp_size(tdpg_session* s, int64_t* q);
+int tdpg_pp_get(tdpg_session* s, int32_t* a, int32_t* b, double* w);
+/* update_pair_weights: hits in order; a <= b canonical. */
+int tdpg_pp_update(tdpg_session* s, int64_t n_hits, const int32_t* a, const int32_t* b,
+                   const double* path_slack, double wns, double w0, double w1);
+int tdpg_pp_loss(tdpg_session* s, int32_t kind, double* value, double* d_pin /* [2*n_pins] or NULL */);
+
+/* ---- full objective: objective_and_gradient ------------------------- */
+/* terms[6] = value, wl_term, density_term, pp_term, hpwl, overflow. */
+int tdpg_objective(tdpg_session* s, double gamma, double lambda, double beta, int32_t pp_kind,
+                   const double* net_w, double terms[6], double* d_cell /* [2*n_cells] or NULL */);
+
+/* AdamState::step on a host flat vector (exposed for the reference-shaped API/tests). */
+int tdpg_adam_step(int64_t n, double* x, const double* grad, double* m, double* v, int32_t* t, double lr,
+                   double beta1, double beta2, double eps);
+
+/* ---- timing ----------------------------------------------------------- */
+/* run_sta at current positions.  Any output pointer may be NULL. */
+int tdpg_sta(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* arr_known, uint8_t* req_known,
+             double* tns, double* wns);
+/* report_timing_endpoint(n, k=1) on the last STA; counts[0..3] = n_paths, total_pins,
+ * unique_endpoints, unique_pin_pairs; candidates_generated = n_paths. */
+int tdpg_extract_endpoint(tdpg_session* s, int32_t n, int32_t k, int64_t counts[4]);
+int tdpg_paths_get(tdpg_session* s, int32_t* path_start /* [n_paths+1] */, int32_t* pins, double* slack);
+/* collect_pin_pairs of the last extraction: number of hits, then fetch */
+int tdpg_paths_hits(tdpg_session* s, int64_t* n_hits, int32_t* a, int32_t* b, double* slack);
+/* Device-timed duration (ms) of the last STA / extraction call, CUDA events. */
+int tdpg_last_timing_ms(tdpg_session* s, double* sta_ms, double* extract_ms);
+
+/* ---- the placement loop: run_placement ------------------------------ */
+/* pos_explicit [n_cells] (bool) marks cells whose coordinates came from the file;
+ * positions are the session's current positions on entry and the result on exit.
+ * trace may be NULL; else capacity max_iters rows.  final[3] = tns, wns, hpwl. */
+int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit, tdpg_trace_row* trace,
+               int32_t* n_rows, int32_t* stop_overflow, double final_[3]);
+
+/* ---- bench/driver hooks (device-resident, no host copies) ------------ */
+/* Prepare an iteration engine (grid, gamma, lambda schedule) for tdpg_iterate_dev. */
+int tdpg_engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit);
+/* Run n GP iterations (timing refresh per schedule) fully on device; optional device time. */
+int tdpg_iterate_dev(tdpg_session* s, int32_t n_iters, double* device_ms);
+int tdpg_engine_stats(tdpg_session* s, int32_t* iter, int32_t* refreshes, int64_t* launches);
+/* Per-kernel device time (ms) of one iteration of each kind, measured with events. */
+int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_t n_out, char* names, int32_t name_len);
+
+/* ---- synthetic designs (generate_synthetic semantics) ---------------- */
+typedef struct tdpg_design tdpg_design;
+/* Builds the netlist exactly as the reference generator (same mt19937_64 stream);
+ * calibrate != 0 runs the 300-iteration coarse placement on the GPU to set the clock. */
+int tdpg_generate(uint64_t seed, int32_t n_cells, int32_t n_registers, double avg_fanout, double fail_frac,
+                  double r_unit, double c_unit, int32_t calibrate, tdpg_design** out);
+int tdpg_design_view(tdpg_design* d, tdpg_netlist* view, const double** positions);
+int tdpg_design_set_clock(tdpg_design* d, double clock_period);
+int tdpg_design_destroy(tdpg_design* d);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TDPG_H */

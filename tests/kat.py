@@ -1,0 +1,144 @@
+"""Known-answer checks restated from the reference's own test suite.
+
+Each check takes a backend class with the oracle interface (``Oracle``,
+``RefOracle``, or the GPU engine's ``Session``) and asserts the numbers the
+reference tests pin (citations: /root/reference/proj/tests/...).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from fixtures import make_diamond, make_t1, make_t2, make_trunk16
+
+
+def _pin(d, name):
+    return d.pin_names.index(name)
+
+
+def check_t1_sta(B):
+    """test_sta.cpp:55-77 — T1 arr/req/slack/tns/wns exact."""
+    d = make_t1()
+    t = B(d).sta()
+    assert np.allclose(t["arr"], [0, 0, 1, 10, 11, 27, 28, 28], rtol=0, atol=1e-12)
+    assert np.allclose(t["req"], [-18, -18, -17, -8, -7, 9, 10, 10], rtol=0, atol=1e-12)
+    assert np.allclose(t["slack"], -18.0, rtol=0, atol=1e-12)
+    assert t["arr_known"].all() and t["req_known"].all()
+    assert t["tns"] == -18.0 and t["wns"] == -18.0
+
+
+def check_t2_sta(B):
+    """test_sta.cpp:79-103."""
+    d = make_t2()
+    t = B(d).sta()
+    p = lambda n: _pin(d, n)  # noqa: E731
+    assert t["arr"][p("M.out")] == 15.0 and t["arr"][p("EP1")] == 15.0 and t["arr"][p("EP2")] == 13.0
+    assert t["req"][p("X.in")] == -5.0 and t["req"][p("Y.in")] == -4.0 and t["req"][p("S")] == -5.0
+    assert t["slack"][p("M.a")] == -5.0 and t["slack"][p("M.b")] == -4.0 and t["slack"][p("Z.out")] == -3.0
+    assert t["tns"] == -8.0 and t["wns"] == -5.0
+
+
+def check_t1_graph(B):
+    """test_netlist.cpp:252-269 — 4 net arcs then 3 cell arcs, level[0]=0, level[7]=7."""
+    g = B(make_t1()).graph()
+    assert g["n_net_arcs"] == 4 and g["n_cell_arcs"] == 3
+    assert list(g["arc_kind"]) == [0, 0, 0, 0, 1, 1, 1]
+    assert g["level"][0] == 0 and g["level"][7] == 7
+    assert list(g["level"]) == list(range(8))
+
+
+def _paths(r):
+    return [r["pins"][r["start"][i]:r["start"][i + 1]].tolist() for i in range(r["n_paths"])]
+
+
+def check_diamond_paths(B):
+    """test_paths.cpp:42-74 — diamond(7,5) and the equal-delay tie diamond(7,7)."""
+    r = B(make_diamond(7.0, 5.0)).extract(n=0)  # clock 10, path delay 8: not violated
+    assert r["n_paths"] == 0
+    d = make_diamond(7.0, 5.0)
+    d.clock_period = 5.0  # violate so the endpoint policy reports it
+    r = B(d).extract(n=0)
+    assert _paths(r) == [[0, 1, 2, 5, 7, 8]] and r["slack"][0] == 5.0 - 8.0
+    d = make_diamond(7.0, 7.0)
+    d.clock_period = 5.0
+    r = B(d).extract(n=0)
+    assert _paths(r) == [[0, 1, 2, 5, 7, 8]]  # smallest pin sequence wins the tie
+
+
+def check_t2_endpoint(B):
+    """test_paths.cpp:105-139 — endpoint(n=2, k=1): slacks -5, -3; counters."""
+    r = B(make_t2()).extract(n=2)
+    assert r["n_paths"] == 2
+    assert list(r["slack"]) == [-5.0, -3.0]
+    assert r["unique_endpoints"] == 2 and r["candidates_generated"] == 2 and r["unique_pin_pairs"] == 5
+
+
+def check_trunk16(B):
+    """test_paths.cpp:141-166 — endpoint(16, 1): 16 paths / 16 endpoints / 40 pairs."""
+    r = B(make_trunk16()).extract(n=16)
+    assert r["n_paths"] == 16 and r["unique_endpoints"] == 16 and r["unique_pin_pairs"] == 40
+
+
+def check_t1_pairs(B):
+    """test_paths.cpp:197-211 — T1 hits {(0,1),(2,3),(4,5),(6,7)} @ -18."""
+    r = B(make_t1()).extract(n=1)
+    a, b, s = r["hits"]
+    assert list(zip(a.tolist(), b.tolist())) == [(0, 1), (2, 3), (4, 5), (6, 7)]
+    assert np.all(s == -18.0)
+
+
+def check_t1_hpwl(B):
+    """test_placer.cpp:151-156."""
+    assert B(make_t1()).hpwl() == 7.0
+
+
+def check_wa_closed_form(B):
+    """test_placer.cpp:56-65 — {(0,0),(10,0)}, gamma 1 -> 10 tanh 5."""
+    v, g = B.wa(np.array([[0.0, 0.0], [10.0, 0.0]]), 1.0)
+    assert abs(v - 10.0 * math.tanh(5.0)) <= 1e-14 * 10.0
+    assert abs(g[0, 0] + g[1, 0]) <= 1e-14 * abs(g[0, 0]) and g[0, 0] < 0.0 and g[0, 1] == 0.0
+    v, g = B.wa(np.array([[5.0, 5.0]] * 3), 1.0)
+    assert v == 0.0 and np.all(g == 0.0)
+
+
+def check_pp_hand_values(B):
+    """test_placer.cpp:283-299."""
+    led = ([0], [1], [10.0])
+    pins = np.array([[0.0, 0.0], [3.0, 4.0]])
+    v, d = B.pp_loss(led, pins, 0)
+    assert v == 250.0 and d[0, 0] == -60.0 and d[0, 1] == -80.0 and d[1, 0] == 60.0
+    v, d = B.pp_loss(led, pins, 1)
+    assert v == 50.0 and d[0, 0] == -6.0 and d[0, 1] == -8.0
+    v, d = B.pp_loss(([0], [1], [5.0]), np.array([[1.0, 1.0], [1.0, 1.0]]), 1)
+    assert v == 0.0 and d[0, 0] == 0.0 and np.isfinite(d).all()
+
+
+def check_ledger(B):
+    """test_placer.cpp:346-378 — 10 -> 10.16; double hit -> 10.04; guards."""
+    s = B(make_t1())
+    w = s.pp_update(None, ([1], [2], [-400.0]), -500.0, 10.0, 0.2)
+    assert list(w[2]) == [10.0]
+    w = s.pp_update(w, ([1], [2], [-400.0]), -500.0, 10.0, 0.2)
+    assert abs(w[2][0] - 10.16) <= 1e-12 * 10.16
+    w2 = s.pp_update(None, ([3, 3], [4, 4], [-400.0, -100.0]), -500.0, 10.0, 0.2)
+    assert abs(w2[2][0] - (10.0 + 0.2 * 0.2)) <= 1e-12 * 10.04
+    base = ([0], [1], [10.0])
+    for wns in (0.0, 3.0):
+        w3 = s.pp_update(base, ([0], [1], [-1.0]), wns, 10.0, 0.2)
+        assert list(w3[2]) == [10.0]
+    w4 = s.pp_update(base, ([0, 5], [1, 6], [0.0, 2.5]), -4.0, 10.0, 0.2)
+    assert list(w4[0]) == [0] and list(w4[2]) == [10.0]
+
+
+def check_adam(B):
+    """test_placer.cpp:509-520 — 5 -> 4.9 -> 4.8."""
+    x, g, m, v = np.array([5.0]), np.array([3.0]), np.zeros(1), np.zeros(1)
+    t = B.adam_step(x, g, m, v, 0, 0.1)
+    assert abs(x[0] - 4.9) <= 1e-8 * 4.9
+    t = B.adam_step(x, g, m, v, t, 0.1)
+    assert abs(x[0] - 4.8) <= 1e-7 * 4.8 and t == 2
+
+
+ALL = [check_t1_sta, check_t2_sta, check_t1_graph, check_diamond_paths, check_t2_endpoint, check_trunk16,
+       check_t1_pairs, check_t1_hpwl, check_wa_closed_form, check_pp_hand_values, check_ledger, check_adam]
