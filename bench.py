@@ -1,0 +1,374 @@
+"""bench.py — timing-driven GP on a 1M-cell synthetic netlist (BASELINE.json configs[2]).
+
+One step = one GP iteration of run_placement (placer.cpp:412-478): WA wirelength +
+pin-pair attraction + bin density, value and gradient, Adam step, clamp; a timing
+refresh (STA + endpoint-policy extraction of every violated endpoint + ledger
+update, placer.cpp:415-435) runs every m=15 steps and is included in the timed
+region.  fp64 throughout, like the reference.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value` = GP iterations/s over the whole job (N independent replicas when N > 1,
+"replicas only").  `e2e` = the same iterations through the C-ABI with
+host buffers (positions H2D + new positions/trace row D2H every step).  Extra keys
+report the STA + top-k extraction sweep on the same 1M timing graph, the dominant
+kernel's roofline and the reference CPU baseline.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "GP iters/s & top-k path-extraction ms at 1M cells; TNS/WNS/HPWL parity"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=15)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, default=1_000_000, help="generator spec n_cells (1.1x cells)")
+    ap.add_argument("--grid", type=int, default=1024)
+    ap.add_argument("--m", type=int, default=15)
+    ap.add_argument("--fail-frac", type=float, default=0.8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-evals", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 2 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 2 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def bench_config(args, iters):
+    return {"grid_nx": args.grid, "grid_ny": args.grid, "m": args.m, "timing_start_iter": 0, "max_iters": iters,
+            "seed": 1}
+
+
+def peaks():
+    try:
+        return json.load(open(PEAKS))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def kernel_bytes(d, grid, E_tot):
+    """Algorithmic (compulsory) bytes per launch of each GP kernel, fp64.  DESIGN.md §4."""
+    C, P, N, E = d.n_cells, d.n_pins, d.n_nets, d.n_net_pins
+    B = grid * grid
+    return {
+        # net CSR + entry record (cell id, offset) + cell positions once + per-entry gradient write
+        "wirelength": 4 * (N + 1) + E * (4 + 16) + 16 * C + 16 * E,
+        # positions + sizes + fixed flags once, grid accumulators written once
+        "density_scatter": C * (16 + 16 + 1) + 8 * B,
+        # accumulators read + reset, excess written
+        "density_bins": 3 * 8 * B,
+        # fold CSR + entry gradients + positions/sizes + excess once + Adam m,v r/w + positions written
+        "cells": 4 * (C + 1) + 4 * E_tot + 16 * E + C * (1 + 16 + 16) + 8 * B + C * (32 + 32) + 16 * C,
+    }
+
+
+def iteration_bytes(d, grid, Q=0):
+    """SURVEY.md §8(d) bytes_iter with p = 8 (fp64), plus the Adam step 2C*p*7."""
+    C, N, E = d.n_cells, d.n_nets, d.n_net_pins
+    p = 8
+    B = grid * grid
+    return 2 * C * p + 2 * C * p + E * (4 + 2 * p) + 4 * (N + 1) + 4 * E + Q * (8 + p) + 2 * C * p + 2 * B * p + 2 * C * p * 7
+
+
+def make_design(args, rank):
+    from paper_2503_11674_b200.engine import generate
+    t0 = time.time()
+    d = generate(seed=1 + rank, cells=args.cells, fail_frac=args.fail_frac, calibrate=True)
+    return d, time.time() - t0
+
+
+def extraction_sweep(d, ns=(1000, 10000, 100000)):
+    """STA + report_timing_endpoint(n, 1) on a spread snapshot of the 1M graph, clock set so
+    80% of endpoints fail (configs[3]); device time per n (CUDA events)."""
+    from paper_2503_11674_b200.engine import Session
+    rng = np.random.default_rng(1)
+    xy = d.positions.copy()
+    x0, y0, x1, y1 = d.core
+    xy[:, 0] = x0 + rng.random(d.n_cells) * (x1 - x0 - d.cell_w)
+    xy[:, 1] = y0 + rng.random(d.n_cells) * (y1 - y0 - d.cell_h)
+    s = Session(d)
+    t = s.sta(xy)
+    clock0 = d.clock_period
+    arr = t["arr"][d.endpoints]
+    d.clock_period = float(np.quantile(arr, 0.2))
+    s2 = Session(d)
+    out = {}
+    s2.set_positions(xy)
+    for n in ns:
+        best = None
+        for _ in range(3):
+            r = s2.extract(None, n=n, run_sta=True)
+            tot = r["sta_ms"] + r["extract_ms"]
+            if best is None or tot < best[0]:
+                best = (tot, r["sta_ms"], r["extract_ms"], r["n_paths"])
+        out[str(n)] = {"total_ms": round(best[0], 3), "sta_ms": round(best[1], 3), "extract_ms": round(best[2], 3),
+                       "paths": best[3]}
+    d.clock_period = clock0
+    return out, xy
+
+
+def cpu_baseline(d, args, xy_snapshot):
+    """Reference CPU implementation (oracle/_ref: the reference's own sources) on a bounded
+    sample of the same workload: objective_and_gradient on the 1M design (1 and nproc threads,
+    the better quoted) + one STA / top-10K extraction."""
+    from oracle.oracle import Oracle, RefOracle
+    kind = "reference" if RefOracle.available() else "port"
+    B = RefOracle if kind == "reference" else Oracle
+    t0 = time.time()
+    o = B(d)
+    setup_s = time.time() - t0
+    nproc = os.cpu_count() or 1
+    gamma = 0.01 * d.span
+    res = {}
+    for th in sorted({1, nproc}):
+        ts = []
+        for _ in range(max(1, args.cpu_sample_evals)):
+            t1 = time.perf_counter()
+            if kind == "reference":
+                o.objective(d.positions, args.grid, args.grid, 0.6, gamma, 1e-4, 2.5e-5, threads=th)
+            else:
+                o.objective(d.positions, args.grid, args.grid, 0.6, gamma, 1e-4, 2.5e-5)
+            ts.append(time.perf_counter() - t1)
+        res[th] = min(ts)
+        if kind != "reference":
+            break
+    best_th = min(res, key=res.get)
+    ex = {}
+    if kind == "reference":
+        r = o.extract(xy_snapshot, n=10000, threads=1)
+        ex = {"sta_ms": round(r["sta_ms"], 1), "extract_top10k_ms": round(r["extract_ms"], 1)}
+    return {"value": round(1.0 / res[best_th], 4), "unit": "iters/s", "cores": best_th, "kind": kind,
+            "sample": f"objective_and_gradient on the {d.n_cells}-cell design, grid {args.grid}^2, "
+                      f"{args.cpu_sample_evals} evals per thread count, best of threads {sorted(res)} "
+                      f"(s/eval: {', '.join(f'{k}T {v:.2f}' for k, v in res.items())}); Adam + refresh excluded",
+            "threads_tried": {str(k): round(v, 3) for k, v in res.items()}, "setup_s": round(setup_s, 1), **ex}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.oracle import Oracle, RefOracle
+    from paper_2503_11674_b200.engine import generate
+    kind = "reference" if RefOracle.available() else "port"
+    try:
+        d = generate(seed=1, cells=args.cells, fail_frac=args.fail_frac, calibrate=False)
+    except Exception:
+        # no GPU for the generator's calibration is fine: the netlist is host-built
+        raise
+    d.clock_period = 1.0
+    o = (RefOracle if kind == "reference" else Oracle)(d)
+    nproc = os.cpu_count() or 1
+    gamma = 0.01 * d.span
+    xy = d.positions.copy()
+    x = xy.reshape(-1).copy()
+    m = np.zeros_like(x)
+    v = np.zeros_like(x)
+    t = 0
+    times = []
+    total_steps = args.warmup + args.steps
+    for it in range(total_steps):
+        t1 = time.perf_counter()
+        if kind == "reference":
+            _, g = o.objective(x.reshape(-1, 2), args.grid, args.grid, 0.6, gamma, 1e-4, 2.5e-5, threads=nproc)
+        else:
+            _, g = o.objective(x.reshape(-1, 2), args.grid, args.grid, 0.6, gamma, 1e-4, 2.5e-5)
+        t = (RefOracle if kind == "reference" else Oracle).adam_step(x, g.reshape(-1), m, v, t,
+                                                                     0.01 * d.span * 0.999 ** it)
+        dt = time.perf_counter() - t1
+        if it >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    val = len(times) / tot
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "iters/s",
+                      "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": round(1000 * tot / len(times), 1), "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": f"synthetic {args.cells}-spec-cell netlist ({d.n_cells} cells, "
+                                             f"{d.n_nets} nets), GP iteration (objective_and_gradient + Adam), "
+                                             f"grid {args.grid}^2", "cells": d.n_cells, "nets": d.n_nets},
+                      "cpu_baseline": {"value": round(val, 4), "unit": "iters/s", "cores": nproc, "kind": kind,
+                                       "sample": "every step one full-size GP iteration (timing refresh excluded)"},
+                      "e2e": {"value": round(val, 4), "unit": "iters/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2503_11674_b200.engine import Session
+
+    d, gen_s = make_design(args, rank)
+    total_iters = args.warmup + args.steps + 64
+    cfg = bench_config(args, total_iters)
+    s = Session(d)
+    t0 = time.time()
+    s.engine_init(cfg)
+    init_s = time.time() - t0
+    s.iterate(args.warmup)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    barrier()
+    st0 = s.engine_stats()
+    with Clocks(local) as clk:
+        dev_ms = s.iterate(args.steps)
+    st1 = s.engine_stats()
+    barrier()
+    ms = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dev_ms_max = float(ms.item())
+    value = world * args.steps / (dev_ms_max / 1000.0)
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+    refreshes = st1["refreshes"] - st0["refreshes"]
+
+    # per-kernel profile of loop iterations (roofline of the dominant kernel)
+    prof = s.profile_iteration(5)
+
+    # e2e: the same iterations through host buffers (pinned), positions in/out every step
+    C = d.n_cells
+    hin = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
+    hout = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
+    hin.numpy()[:] = s.positions().reshape(-1)
+    e2e_steps = min(args.steps, 20)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        s.step_host(hin.data_ptr(), hout.data_ptr())
+        hin, hout = hout, hin
+    e2e_s = time.perf_counter() - t0
+    e2e_val = world * e2e_steps / e2e_s
+    sweep, xy_snap = (extraction_sweep(d) if rank == 0 else ({}, None))
+
+    if rank != 0:
+        return
+    pk = peaks()
+    E_tot = d.n_net_pins + int(np.sum(np.isin(np.arange(d.n_pins), d.net_pins, invert=True) & (d.pin_cell >= 0)))
+    kb = kernel_bytes(d, args.grid, E_tot)
+    dom = max((k for k in prof if k in kb), key=lambda k: prof[k])
+    dom_ms = prof[dom]
+    achieved = kb[dom] / (dom_ms / 1000.0) / 1e9
+    iter_ms = sum(prof.values())
+    ib = iteration_bytes(d, args.grid)
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(d, args, xy_snap)
+        except Exception as e:  # reported, never fatal
+            cpu = {"error": str(e)[:200]}
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(dom)
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"configs[2]: synthetic {d.n_cells}-cell / {d.n_nets}-net netlist "
+                               f"(generator spec {args.cells}, fail_frac {args.fail_frac}), full timing-driven GP "
+                               f"iteration, grid {args.grid}^2, timing refresh every {args.m} iterations "
+                               f"(STA + endpoint extraction of all violated endpoints + ledger) inside the timed region",
+                   "cells": d.n_cells, "pins": d.n_pins, "nets": d.n_nets, "net_pins": d.n_net_pins,
+                   "endpoints": int(d.endpoints.size), "grid": args.grid, "m": args.m,
+                   "l2": "working set per iteration > L2 (positions+netlist+gradients+grid ~ 2x 126 MB)",
+                   "parallelism": "replicas only" if world > 1 else "single GPU", "refreshes_timed": refreshes},
+        "e2e": {"value": round(e2e_val, 3), "unit": "iters/s", "h2d_bytes_per_step": 16 * C,
+                "d2h_bytes_per_step": 16 * C + 88, "path": "tdpg_step_host (C-ABI, pinned host positions)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk.get("hbm_gbs"),
+                     "unit": "GB/s", "frac": round(achieved / pk.get("hbm_gbs", 6650.0), 4), "traffic": traffic,
+                     "algorithmic_bytes": kb[dom], "kernel_ms": round(dom_ms, 4),
+                     "peak_source": "measured" if "fallback" not in pk else "fallback"},
+        "iteration": {"kernels_ms": {k: round(v, 4) for k, v in prof.items()}, "sum_ms": round(iter_ms, 4),
+                      "bytes_iter_survey": ib,
+                      "frac_of_hbm": round(ib / (iter_ms / 1000.0) / 1e9 / pk.get("hbm_gbs", 6650.0), 4)},
+        "extraction_sweep_ms": sweep,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "setup_s": {"generate_and_calibrate": round(gen_s, 2), "engine_init": round(init_s, 2)},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -34,6 +34,10 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -186,6 +190,8 @@ int tdpg_engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos
 /* Run n GP iterations (timing refresh per schedule) fully on device; optional device time. */
 int tdpg_iterate_dev(tdpg_session* s, int32_t n_iters, double* device_ms);
 int tdpg_engine_stats(tdpg_session* s, int32_t* iter, int32_t* refreshes, int64_t* launches);
+/* One iteration through host buffers (positions in, positions + trace row out) — the e2e path. */
+int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_trace_row* row);
 /* Per-kernel device time (ms) of one iteration of each kind, measured with events. */
 int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_t n_out, char* names, int32_t name_len);
 
@@ -201,6 +207,10 @@ int tdpg_design_destroy(tdpg_design* d);
 
 #ifdef __cplusplus
 }
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
 #endif
 
 #endif /* TDPG_H */

@@ -1054,7 +1054,7 @@ int orc_place(void* h, const double* init_xy, const uint8_t* pos_explicit, const
                            cfg->pp_loss, net_w, s->q, s->la, s->lb, s->lw, terms, g);
         if (rc) {
             if (rc == TDPG_ERR_NONFINITE) {
-                char tmp[512];
+                char tmp[640];
                 snprintf(tmp, sizeof tmp, "%s at iteration %d", g_err, iter);
                 fail(rc, "%s", tmp);
             }

@@ -1,0 +1,164 @@
+// engine.cuh — the device-resident session behind the tdpg C-ABI.
+//
+// HBM layout (all structure-of-arrays, fp64 like the reference):
+//   cells     : xy double2[C] (lower-left origin), wh double2[C], delay[C], fixed u8[C]
+//   pins      : cell int[P] (-1 terminal), off double2[P], anchor double2[P]
+//               (terminal_pos), dir u8[P], cap[P]
+//   net CSR   : net_start[N+1]; per net-pin entry e (driver first, then sinks):
+//               e_cell int[E] (owner cell, or -1-pin for terminals), e_off double2[E]
+//   fold CSR  : per cell, the entry ids of its pins in ascending pin id
+//               (reference fold order, placer.cpp:318-325)
+//   timing    : pins grouped by level (ascending id inside a level), per-pin in-arc
+//               CSR (from-pin, ascending arc id) and out-arc CSR (to-pin)
+//   grid      : int64 fixed-point occupancy accumulators (deterministic scatter),
+//               excess double[B]
+//   ledger    : sorted 64-bit pair keys (a<<32|b) + weights; per-pin incidence CSR
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct tdpg_session;
+
+namespace tdpg {
+
+struct Grid {
+    int nx = 0, ny = 0;
+    double td = 0.0;
+    double x0 = 0, y0 = 0, bw = 0, bh = 0, cap = 0, total_movable = 0;
+    double scale = 1.0, inv_scale = 1.0; // fixed-point occupancy: q = rint(w * scale)
+    bool has_fixed = false;
+    DBuf<long long> acc;
+    DBuf<double> excess;
+    DBuf<double> base; // fixed-cell exact overlap (density.cpp:75-93), when any fixed cell
+    bool valid() const { return nx > 0; }
+    long long bins() const { return static_cast<long long>(nx) * ny; }
+};
+
+// Per-iteration schedule entry (host-computed with the reference's std::pow).
+struct Sched {
+    double lr, c1, c2, lambda;
+};
+
+// Device scalars of one objective evaluation.
+struct Terms {
+    double value, wl, density, pp, hpwl, overflow;
+};
+
+// Device-side control block for the iteration loop.
+struct Ctrl {
+    int iter;          // next iteration index
+    int stopped;       // stop_overflow reached (placer.cpp:459-462)
+    int nonfinite_at;  // first iteration with a non-finite term/gradient, INT_MAX if none
+    int engaged;       // timing rounds have started
+    int rows;          // trace rows written
+    int pad[3];
+};
+
+struct TraceRowDev {
+    int iter, has_timing;
+    double hpwl, overflow, tns, wns, wl_term, density_term, pp_term, lambda, beta_pp;
+};
+
+struct Engine; // placement loop state (gp.cu)
+
+} // namespace tdpg
+
+struct tdpg_session {
+    // sizes
+    int C = 0, P = 0, N = 0, E = 0, E_tot = 0, S = 0, EP = 0, A = 0, A_net = 0, A_cell = 0, L = 0;
+    double clock = 0, r_unit = 0, c_unit = 0, core[4] = {0, 0, 0, 0};
+    cudaStream_t st = nullptr;
+    int device = 0;
+
+    // host copies
+    std::vector<double> h_cell_w, h_cell_h, h_cell_delay, h_pin_cap, h_pin_off, h_pin_term;
+    std::vector<uint8_t> h_cell_fixed, h_pin_dir, h_is_source, h_is_endpoint;
+    std::vector<int> h_pin_cell, h_net_start, h_net_pins, h_sources, h_endpoints, h_pin_net, h_pin_entry;
+    std::vector<std::string> pin_names;
+    std::vector<int> h_level, h_lvl_start, h_lvl_pins, h_arc_from, h_arc_to, h_arc_kind, h_arc_owner;
+    std::vector<double> h_cell_xy; // last uploaded positions (for fixed-cell baseline)
+
+    // device netlist
+    tdpg::DBuf<double2> cell_xy, cell_wh, anchor, pin_off, e_off;
+    tdpg::DBuf<double> cell_delay, pin_cap;
+    tdpg::DBuf<uint8_t> cell_fixed, pin_dir, is_source, is_endpoint;
+    tdpg::DBuf<int> pin_cell, net_start, net_pins, e_cell, pin_entry, cell_ent_start, cell_ent;
+
+    // device timing graph
+    tdpg::DBuf<int> lvl_pins, in_start, in_from, out_start, out_to, ep_sorted;
+
+    // STA state
+    tdpg::DBuf<double2> pin_xy;
+    tdpg::DBuf<double> arr, req, slack;
+    tdpg::DBuf<uint8_t> ak, rk, tie;
+    tdpg::DBuf<int> pred, tie_list, counters; // counters: [0] tie count
+    double tns = 0, wns = 0;
+    bool sta_valid = false;
+
+    // GP scratch
+    tdpg::DBuf<double2> grad_e, d_cell, adam_m, adam_v;
+    tdpg::DBuf<double> part; // per-block partial sums
+    tdpg::Grid grid;
+    tdpg::DBuf<double> net_w;
+    bool has_net_w = false;
+
+    // ledger + PP incidence
+    tdpg::DBuf<unsigned long long> led_key, led_key2;
+    tdpg::DBuf<double> led_w, led_w2;
+    long long Q = 0;
+    tdpg::DBuf<int> pp_pins, pp_start, pp_entry, pp_inc;
+    int n_pp_pins = 0;
+    bool pp_dirty = true;
+
+    // extraction results
+    tdpg::DBuf<int> ex_ep, ex_len, ex_hops, ex_off, ex_hoff, ex_pins;
+    tdpg::DBuf<double> ex_slack;
+    tdpg::DBuf<unsigned long long> hit_key, hit_key_s;
+    tdpg::DBuf<int> hit_idx, hit_idx_s;
+    tdpg::DBuf<double> hit_slack;
+    int n_paths = 0;
+    long long n_path_pins = 0, n_hits = 0, uniq_pairs = 0;
+    bool hits_sorted = false;
+    double last_sta_ms = 0, last_extract_ms = 0;
+
+    // sort / scan scratch
+    tdpg::DBuf<unsigned char> cub_tmp;
+    tdpg::DBuf<unsigned long long> sort_k0, sort_k1;
+    tdpg::DBuf<int> sort_v0, sort_v1;
+    tdpg::HBuf<long long> h_small;
+
+    // placement engine
+    tdpg::Engine* eng = nullptr; // owned; deleted in ~tdpg_session (place.cu)
+
+    ~tdpg_session();
+};
+
+namespace tdpg {
+
+// session.cu
+void upload_positions(tdpg_session* s, const double* xy);
+void ensure_grid(tdpg_session* s, int nx, int ny, double td);
+void* cub_scratch(tdpg_session* s, size_t bytes);
+
+// gp.cu
+void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk);
+int wa_blocks(const tdpg_session* s);
+void rebuild_pp_incidence(tdpg_session* s);
+void launch_pp(tdpg_session* s, int kind, double beta, double* part_pp, int nblk);
+int pp_blocks(const tdpg_session* s);
+void launch_density(tdpg_session* s, double* part_d, int nblk);
+int bins_blocks(const tdpg_session* s);
+Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double beta, int kind, bool use_net_w,
+                         double* d_cell_host);
+
+// timing.cu
+void run_sta_dev(tdpg_session* s);
+void extract_endpoint_dev(tdpg_session* s, int n);
+void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool hits_all_violated);
+void net_weights_dev(tdpg_session* s);
+
+} // namespace tdpg

@@ -1,0 +1,826 @@
+// gp.cu — objective_and_gradient on the device (placer.cpp:275-343) and its kernels.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+
+#include "gp_kernels.cuh"
+
+namespace tdpg {
+
+int api_fail(int kind, const std::string& msg);
+
+// =====================================================================================
+// WA wirelength + exact HPWL, one thread per net (wirelength.cpp:12-85).
+// Writes the net-weighted per-entry gradient w_e * dWA/dpin into grad_e (placer.cpp:298-309:
+// each pin is on <= 1 net, so pin_grad[pin] = 0 + w * g), and per-block partial sums of
+// w_e * WA_e and HPWL_e.
+// =====================================================================================
+template <int K>
+__device__ __forceinline__ double wa_dim_reg(int n, const double (&x)[K], double gamma, double (&g)[K])
+{
+    double hi = x[0], lo = x[0];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+        if (i < n) hi = smax(hi, x[i]), lo = smin(lo, x[i]);
+    double eu[K], el[K];
+    double s_max = 0.0, t_max = 0.0, s_min = 0.0, t_min = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+        if (i < n) {
+            eu[i] = exp((x[i] - hi) / gamma);
+            s_max += eu[i];
+            t_max += (x[i] - hi) * eu[i];
+            el[i] = exp(-(x[i] - lo) / gamma);
+            s_min += el[i];
+            t_min += (x[i] - lo) * el[i];
+        }
+    const double max_term = t_max / s_max;
+    const double min_term = t_min / s_min;
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+        if (i < n) {
+            const double d_max = (eu[i] / s_max) * (1.0 + ((x[i] - hi) - max_term) / gamma);
+            const double d_min = (el[i] / s_min) * (1.0 - ((x[i] - lo) - min_term) / gamma);
+            g[i] = d_max - d_min;
+        }
+    return (hi - lo) + (max_term - min_term);
+}
+
+// Large nets: three passes over the pins, exps recomputed in the gradient pass like the reference.
+__device__ double wa_dim_mem(int s0, int n, int axis, const int* __restrict__ e_cell,
+                             const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
+                             const double2* __restrict__ anchor, double gamma, double w, double2* __restrict__ grad_e,
+                             double& hp)
+{
+    auto X = [&](int i) {
+        const double2 p = entry_pos(e_cell[s0 + i], e_off[s0 + i], cell_xy, anchor);
+        return axis ? p.y : p.x;
+    };
+    double hi = X(0), lo = hi;
+    for (int i = 0; i < n; ++i) {
+        const double x = X(i);
+        hi = smax(hi, x), lo = smin(lo, x);
+    }
+    double s_max = 0.0, t_max = 0.0, s_min = 0.0, t_min = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double x = X(i);
+        const double eu = exp((x - hi) / gamma);
+        s_max += eu;
+        t_max += (x - hi) * eu;
+        const double el = exp(-(x - lo) / gamma);
+        s_min += el;
+        t_min += (x - lo) * el;
+    }
+    const double max_term = t_max / s_max;
+    const double min_term = t_min / s_min;
+    for (int i = 0; i < n; ++i) {
+        const double xi = X(i);
+        const double eu = exp((xi - hi) / gamma);
+        const double el = exp(-(xi - lo) / gamma);
+        const double d_max = (eu / s_max) * (1.0 + ((xi - hi) - max_term) / gamma);
+        const double d_min = (el / s_min) * (1.0 - ((xi - lo) - min_term) / gamma);
+        const double gi = w * (d_max - d_min);
+        if (axis) grad_e[s0 + i].y = gi;
+        else grad_e[s0 + i].x = gi;
+    }
+    hp = hi - lo;
+    return (hi - lo) + (max_term - min_term);
+}
+
+__global__ void __launch_bounds__(kBlock) k_wirelength(int N, const int* __restrict__ net_start,
+                                                       const int* __restrict__ e_cell,
+                                                       const double2* __restrict__ e_off,
+                                                       const double2* __restrict__ cell_xy,
+                                                       const double2* __restrict__ anchor,
+                                                       const double* __restrict__ net_w, double gamma,
+                                                       double2* __restrict__ grad_e, double* __restrict__ part_wl,
+                                                       double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
+{
+    __shared__ double sh[kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    const int e = blockIdx.x * kBlock + threadIdx.x;
+    double wl = 0.0, hp = 0.0;
+    if (e < N) {
+        const int s0 = net_start[e], n = net_start[e + 1] - s0;
+        const double w = net_w ? net_w[e] : 1.0;
+        if (n < 2) {
+            for (int i = 0; i < n; ++i) grad_e[s0 + i] = make_double2(0.0, 0.0);
+        } else if (n <= kWaRegPins) {
+            double x[kWaRegPins], y[kWaRegPins], gx[kWaRegPins], gy[kWaRegPins];
+#pragma unroll
+            for (int i = 0; i < kWaRegPins; ++i) {
+                if (i < n) {
+                    const double2 p = entry_pos(e_cell[s0 + i], e_off[s0 + i], cell_xy, anchor);
+                    x[i] = p.x, y[i] = p.y;
+                } else {
+                    x[i] = 0.0, y[i] = 0.0;
+                }
+            }
+            const double vx = wa_dim_reg<kWaRegPins>(n, x, gamma, gx);
+            const double vy = wa_dim_reg<kWaRegPins>(n, y, gamma, gy);
+            double xl = x[0], xh = x[0], yl = y[0], yh = y[0];
+#pragma unroll
+            for (int i = 0; i < kWaRegPins; ++i)
+                if (i < n) {
+                    xl = smin(xl, x[i]), xh = smax(xh, x[i]), yl = smin(yl, y[i]), yh = smax(yh, y[i]);
+                    grad_e[s0 + i] = make_double2(w * gx[i], w * gy[i]);
+                }
+            wl = w * (vx + vy);
+            hp = (xh - xl) + (yh - yl);
+        } else {
+            double hx, hy;
+            const double vx = wa_dim_mem(s0, n, 0, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hx);
+            const double vy = wa_dim_mem(s0, n, 1, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hy);
+            wl = w * (vx + vy);
+            hp = hx + hy;
+        }
+    }
+    const double bw = block_sum<kBlock>(wl, sh);
+    const double bh = block_sum<kBlock>(hp, sh);
+    if (threadIdx.x == 0) part_wl[blockIdx.x] = bw, part_hp[blockIdx.x] = bh;
+}
+
+// =====================================================================================
+// Pin-pair attraction (pin_pairs.cpp:17-49).  One thread per pin that appears in the
+// ledger; its incidences are in ledger (map-key) order, so the per-pin sum has the
+// reference's accumulation order.  beta * sum is added onto the pin's WA entry gradient,
+// which is exactly the reference fold term pin_grad + beta * pp.d_pin (placer.cpp:323).
+// Pair values are summed once per pair (on the lower pin's side).
+// =====================================================================================
+__global__ void __launch_bounds__(kBlock) k_pin_pairs(const int* __restrict__ n_pins_dev, const int* __restrict__ pp_start,
+                                                      const int* __restrict__ pp_entry, const int* __restrict__ pp_inc,
+                                                      const unsigned long long* __restrict__ led_key,
+                                                      const double* __restrict__ led_w,
+                                                      const int* __restrict__ pin_cell,
+                                                      const double2* __restrict__ pin_off,
+                                                      const double2* __restrict__ cell_xy,
+                                                      const double2* __restrict__ anchor, int kind, double beta,
+                                                      int n_net_entries, double2* __restrict__ grad_e,
+                                                      double* __restrict__ part_pp,
+                                                      const Ctrl* __restrict__ ctrl)
+{
+    __shared__ double sh[kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    const int n_pins = *n_pins_dev;
+    double val = 0.0;
+    for (int i = blockIdx.x * kBlock + threadIdx.x; i < n_pins; i += gridDim.x * kBlock) {
+        double sx = 0.0, sy = 0.0;
+        for (int j = pp_start[i]; j < pp_start[i + 1]; ++j) {
+            const int inc = pp_inc[j];
+            const int q = inc >> 1;
+            const bool second = inc & 1;
+            const unsigned long long key = led_key[q];
+            const int a = static_cast<int>(key >> 32), b = static_cast<int>(key & 0xFFFFFFFFull);
+            const double w = led_w[q];
+            const double2 pa = pin_pos(a, pin_cell, pin_off, cell_xy, anchor);
+            const double2 pb = pin_pos(b, pin_cell, pin_off, cell_xy, anchor);
+            const double dx = pa.x - pb.x;
+            const double dy = pa.y - pb.y;
+            double gx, gy;
+            if (kind == 0) {
+                if (!second) val += w * (dx * dx + dy * dy);
+                gx = 2.0 * w * dx;
+                gy = 2.0 * w * dy;
+            } else {
+                const double dist = sqrt(dx * dx + dy * dy);
+                if (!second) val += w * dist;
+                if (!(dist > 0.0)) continue;
+                gx = w * dx / dist;
+                gy = w * dy / dist;
+            }
+            if (second) sx -= gx, sy -= gy;
+            else sx += gx, sy += gy;
+        }
+        const int e = pp_entry[i];
+        if (e >= n_net_entries) { // off-net pin: pin_grad is 0, slot holds 0 + beta * pp
+            grad_e[e] = make_double2(0.0 + beta * sx, 0.0 + beta * sy);
+        } else if (e >= 0) {
+            double2 g = grad_e[e];
+            g.x = g.x + beta * sx;
+            g.y = g.y + beta * sy;
+            grad_e[e] = g;
+        }
+    }
+    const double bv = block_sum<kBlock>(val, sh);
+    if (threadIdx.x == 0) part_pp[blockIdx.x] = bv;
+}
+
+// =====================================================================================
+// Density (density.cpp:66-158).  Scatter: one thread per movable cell rasterises its
+// quadratic B-spline footprint into int64 fixed-point accumulators (order-independent,
+// hence run-to-run deterministic).  Bins: excess = max(0, occ - cap), value / overflow
+// partial sums, accumulators reset for the next evaluation.
+// =====================================================================================
+constexpr int kFootCache = 16;
+
+__global__ void __launch_bounds__(kBlock) k_density_scatter(int C, const double2* __restrict__ cell_xy,
+                                                            const double2* __restrict__ cell_wh,
+                                                            const uint8_t* __restrict__ fixed, GridDev g,
+                                                            unsigned long long* __restrict__ acc,
+                                                            const Ctrl* __restrict__ ctrl)
+{
+    if (ctrl && ctrl->stopped) return;
+    const int c = blockIdx.x * kBlock + threadIdx.x;
+    if (c >= C || fixed[c]) return;
+    const double2 p = cell_xy[c], s = cell_wh[c];
+    const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
+    int bx0, bx1, by0, by1;
+    footprint_range(g, xl, xh, yl, yh, bx0, bx1, by0, by1);
+    const double area = s.x * s.y;
+    const int nby = by1 - by0 + 1;
+    double wyc[kFootCache], dwyc[kFootCache];
+    const bool cached = nby <= kFootCache;
+    if (cached)
+        for (int j = 0; j < nby; ++j) {
+            const double cy = g.y0 + (by0 + j + 0.5) * g.bh;
+            wyc[j] = extent_weight(yl, yh, cy, g.bh);
+            dwyc[j] = extent_weight_grad(yl, yh, cy, g.bh);
+        }
+    for (int bx = bx0; bx <= bx1; ++bx) {
+        const double cx = g.x0 + (bx + 0.5) * g.bw;
+        const double wx = extent_weight(xl, xh, cx, g.bw);
+        const double dwx = extent_weight_grad(xl, xh, cx, g.bw);
+        if (wx == 0.0 && dwx == 0.0) continue;
+        for (int by = by0; by <= by1; ++by) {
+            double wy, dwy;
+            if (cached) {
+                wy = wyc[by - by0], dwy = dwyc[by - by0];
+            } else {
+                const double cy = g.y0 + (by + 0.5) * g.bh;
+                wy = extent_weight(yl, yh, cy, g.bh);
+                dwy = extent_weight_grad(yl, yh, cy, g.bh);
+            }
+            if (wy == 0.0 && dwy == 0.0) continue;
+            const double w = area * wx * wy;
+            const long long q = __double2ll_rn(w * g.scale);
+            if (q) atomicAdd(&acc[static_cast<long long>(bx) * g.ny + by], static_cast<unsigned long long>(q));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g, long long* __restrict__ acc,
+                                                         const double* __restrict__ base,
+                                                         double* __restrict__ excess, double* __restrict__ part_d,
+                                                         const Ctrl* __restrict__ ctrl)
+{
+    __shared__ double sh[kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    double v2 = 0.0, v1 = 0.0;
+    for (long long b = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; b < B;
+         b += static_cast<long long>(gridDim.x) * kBlock) {
+        const long long q = acc[b];
+        acc[b] = 0;
+        const double mov = static_cast<double>(q) * g.inv_scale;
+        const double occ = base ? base[b] + mov : mov;
+        const double ex = smax(0.0, occ - g.cap);
+        excess[b] = ex;
+        v2 += ex * ex;
+        v1 += ex;
+    }
+    const double s2 = block_sum<kBlock>(v2, sh);
+    const double s1 = block_sum<kBlock>(v1, sh);
+    if (threadIdx.x == 0) part_d[2 * blockIdx.x] = s2, part_d[2 * blockIdx.x + 1] = s1;
+}
+
+// =====================================================================================
+// Finalize: deterministic fixed-order sums of all partials -> objective terms, trace
+// row, stop / non-finite flags, and the schedule values of this iteration.
+// =====================================================================================
+
+
+__global__ void k_finalize(FinArgs a, Ctrl* ctrl, IterCur* cur)
+{
+    __shared__ double sh[kBlock / 32];
+    __shared__ int skip;
+    if (threadIdx.x == 0) skip = ctrl ? ctrl->stopped : 0;
+    __syncthreads();
+    if (skip) {
+        if (threadIdx.x == 0) cur->do_adam = 0;
+        return;
+    }
+    double wl = 0, hp = 0, pp = 0, d2 = 0, d1 = 0;
+    for (int i = threadIdx.x; i < a.nb_wa; i += kBlock) wl += a.part_wl[i], hp += a.part_hp[i];
+    for (int i = threadIdx.x; i < a.nb_pp; i += kBlock) pp += a.part_pp[i];
+    for (int i = threadIdx.x; i < a.nb_d; i += kBlock) d2 += a.part_d[2 * i], d1 += a.part_d[2 * i + 1];
+    wl = block_sum<kBlock>(wl, sh);
+    hp = block_sum<kBlock>(hp, sh);
+    pp = block_sum<kBlock>(pp, sh);
+    d2 = block_sum<kBlock>(d2, sh);
+    d1 = block_sum<kBlock>(d1, sh);
+    if (threadIdx.x != 0) return;
+    const int it = ctrl ? ctrl->iter : 0;
+    const double lambda = a.sched ? a.sched[it].lambda : a.lambda_single;
+    Terms t;
+    t.wl = wl, t.hpwl = hp, t.pp = a.nb_pp ? pp : 0.0, t.density = d2;
+    t.overflow = a.total_movable > 0.0 ? d1 / a.total_movable : 0.0;
+    t.value = t.wl + lambda * t.density + a.beta * t.pp;
+    *a.terms = t;
+    const bool finite = isfinite(t.value) && isfinite(t.wl) && isfinite(t.density) && isfinite(t.pp);
+    cur->lambda = lambda;
+    cur->iter = it;
+    cur->do_adam = 0;
+    if (!ctrl) return;
+    if (!finite) atomicMin(&ctrl->nonfinite_at, it);
+    if (a.trace) {
+        TraceRowDev r;
+        r.iter = it;
+        r.has_timing = a.timing_row && a.timing_row[0] != 0.0;
+        r.tns = r.has_timing ? a.timing_row[1] : 0.0;
+        r.wns = r.has_timing ? a.timing_row[2] : 0.0;
+        r.hpwl = t.hpwl, r.overflow = t.overflow, r.wl_term = t.wl, r.density_term = t.density;
+        r.pp_term = t.pp, r.lambda = lambda, r.beta_pp = a.beta * t.pp;
+        a.trace[it] = r;
+    }
+    if (a.timing_row_clear) a.timing_row_clear[0] = 0.0;
+    ctrl->rows = it + 1;
+    if (ctrl->engaged && t.overflow <= a.stop_overflow) { // placer.cpp:459-462
+        ctrl->stopped = 1;
+        return;
+    }
+    if (a.sched) {
+        cur->lr = a.sched[it].lr, cur->c1 = a.sched[it].c1, cur->c2 = a.sched[it].c2;
+        cur->do_adam = 1;
+    }
+    ctrl->iter = it + 1;
+}
+
+// =====================================================================================
+// Cell kernel: gradient fold (placer.cpp:318-333) + density gradient (density.cpp:148-156)
+// + Adam (placer.cpp:345-356) + write-back/clamp (placer.cpp:472-476), one thread per cell.
+// =====================================================================================
+struct CellArgs {
+    int C;
+    const int* ent_start;
+    const int* ent;
+    const double2* grad_e;
+    const uint8_t* fixed;
+    double2* xy;
+    const double2* wh;
+    GridDev g;
+    const double* excess;
+    double2* d_cell;    // optional gradient output
+    double2* m;         // Adam state (iteration mode)
+    double2* v;
+    double b1, b2, eps;
+    double core_x0, core_y0, core_x1, core_y1;
+};
+
+__global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __restrict__ cur, Ctrl* ctrl)
+{
+    const int c = blockIdx.x * kBlock + threadIdx.x;
+    if (c >= a.C) return;
+    const bool adam = cur->do_adam;
+    if (ctrl && !adam && !a.d_cell) return; // stopped: nothing to do
+    double gx = 0.0, gy = 0.0;
+    for (int j = a.ent_start[c]; j < a.ent_start[c + 1]; ++j) {
+        const double2 ge = a.grad_e[a.ent[j]];
+        gx += ge.x;
+        gy += ge.y;
+    }
+    if (a.fixed[c]) {
+        if (a.d_cell) a.d_cell[c] = make_double2(0.0, 0.0);
+        return;
+    }
+    const double2 p = a.xy[c], s = a.wh[c];
+    const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
+    int bx0, bx1, by0, by1;
+    footprint_range(a.g, xl, xh, yl, yh, bx0, bx1, by0, by1);
+    const double area = s.x * s.y;
+    double dgx = 0.0, dgy = 0.0;
+    for (int bx = bx0; bx <= bx1; ++bx) {
+        const double cx = a.g.x0 + (bx + 0.5) * a.g.bw;
+        const double wx = extent_weight(xl, xh, cx, a.g.bw);
+        const double dwx = extent_weight_grad(xl, xh, cx, a.g.bw);
+        if (wx == 0.0 && dwx == 0.0) continue;
+        for (int by = by0; by <= by1; ++by) {
+            const double cy = a.g.y0 + (by + 0.5) * a.g.bh;
+            const double wy = extent_weight(yl, yh, cy, a.g.bh);
+            const double dwy = extent_weight_grad(yl, yh, cy, a.g.bh);
+            if (wy == 0.0 && dwy == 0.0) continue;
+            const double f = 2.0 * a.excess[static_cast<long long>(bx) * a.g.ny + by];
+            dgx += f * (area * dwx * wy);
+            dgy += f * (area * wx * dwy);
+        }
+    }
+    const double lambda = cur->lambda;
+    gx += lambda * dgx;
+    gy += lambda * dgy;
+    if (ctrl && !(isfinite(gx) && isfinite(gy))) atomicMin(&ctrl->nonfinite_at, cur->iter);
+    if (a.d_cell) a.d_cell[c] = make_double2(gx, gy);
+    if (!adam) return;
+    double2 m = a.m[c], v = a.v[c];
+    const double lr = cur->lr, c1 = cur->c1, c2 = cur->c2;
+    m.x = a.b1 * m.x + (1.0 - a.b1) * gx;
+    m.y = a.b1 * m.y + (1.0 - a.b1) * gy;
+    v.x = a.b2 * v.x + (1.0 - a.b2) * gx * gx;
+    v.y = a.b2 * v.y + (1.0 - a.b2) * gy * gy;
+    double x = p.x - lr * (m.x / c1) / (sqrt(v.x / c2) + a.eps);
+    double y = p.y - lr * (m.y / c1) / (sqrt(v.y / c2) + a.eps);
+    const double xhi = a.core_x1 - s.x, yhi = a.core_y1 - s.y; // clamp_to_core, placer.cpp:99-103
+    x = x < a.core_x0 ? a.core_x0 : (xhi < x ? xhi : x);
+    y = y < a.core_y0 ? a.core_y0 : (yhi < y ? yhi : y);
+    a.m[c] = m, a.v[c] = v;
+    a.xy[c] = make_double2(x, y);
+}
+
+// Adam on a flat device vector (AdamState::step for the reference-shaped host API).
+__global__ void k_adam_flat(long long n, double* x, const double* g, double* m, double* v, double lr, double b1,
+                            double b2, double eps, double c1, double c2)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= n) return;
+    m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+    v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+    x[i] -= lr * (m[i] / c1) / (sqrt(v[i] / c2) + eps);
+}
+
+// =====================================================================================
+// host side
+// =====================================================================================
+GridDev grid_dev(const tdpg_session* s)
+{
+    const Grid& g = s->grid;
+    return GridDev{g.nx, g.ny, g.x0, g.y0, g.bw, g.bh, g.cap, g.scale, g.inv_scale, g.total_movable};
+}
+
+int wa_blocks(const tdpg_session* s) { return std::max(1, static_cast<int>(blocks_for(s->N, kBlock))); }
+int pp_blocks(const tdpg_session*) { return 148 * 4; }
+int bins_blocks(const tdpg_session* s)
+{
+    return std::max(1, std::min(148 * 8, static_cast<int>(blocks_for(s->grid.bins(), kBlock))));
+}
+
+// Per-pin incidence CSR of the ledger (rebuilt when the ledger changes).
+__global__ void k_pp_inc_keys(long long Q, const unsigned long long* key, unsigned long long* out)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= Q) return;
+    const unsigned long long k = key[i];
+    out[2 * i] = (k >> 32 << 32) | static_cast<unsigned long long>(2 * i);
+    out[2 * i + 1] = (k << 32) | static_cast<unsigned long long>(2 * i + 1);
+}
+
+__global__ void k_pp_csr(long long n, const unsigned long long* sorted, int* pp_inc, int* pin_of, int* head)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long k = sorted[i];
+    pp_inc[i] = static_cast<int>(k & 0xFFFFFFFFull);
+    pin_of[i] = static_cast<int>(k >> 32);
+    head[i] = (i == 0 || (sorted[i - 1] >> 32) != (k >> 32)) ? 1 : 0;
+}
+
+__global__ void k_pp_heads(long long n, const int* head, const int* head_pos, const int* pin_of, const int* pin_entry,
+                           int* pp_start, int* pp_entry, int* n_pins_out)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= n) return;
+    if (head[i]) {
+        const int h = head_pos[i];
+        pp_start[h] = static_cast<int>(i);
+        pp_entry[h] = pin_entry[pin_of[i]];
+    }
+    if (i == n - 1) {
+        const int total = head_pos[i] + head[i];
+        pp_start[total] = static_cast<int>(n);
+        *n_pins_out = total;
+    }
+}
+
+void rebuild_pp_incidence(tdpg_session* s)
+{
+    if (!s->pp_dirty) return;
+    s->pp_dirty = false;
+    const long long Q = s->Q, n = 2 * Q;
+    // capacity: every pair is a net arc, so Q <= A_net
+    const size_t cap = static_cast<size_t>(std::max<long long>(n, 2LL * s->A_net)) + 2;
+    s->pp_inc.reserve(cap);
+    s->pp_start.reserve(cap + 1);
+    s->pp_entry.reserve(cap);
+    s->pp_pins.reserve(4); // pp_pins[0] = number of distinct pins (device)
+    if (Q == 0) {
+        s->pp_pins.zero(s->st, 1);
+        s->n_pp_pins = 0;
+        return;
+    }
+    s->sort_k0.reserve(cap), s->sort_k1.reserve(cap), s->sort_v0.reserve(cap), s->sort_v1.reserve(cap);
+    k_pp_inc_keys<<<blocks_for(Q, kBlock), kBlock, 0, s->st>>>(Q, s->led_key, s->sort_k0);
+    CK_LAUNCH();
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, s->sort_k0.p, s->sort_k1.p, static_cast<int>(n), 0, 64, s->st);
+    void* tmp = cub_scratch(s, bytes);
+    CK(cub::DeviceRadixSort::SortKeys(tmp, bytes, s->sort_k0.p, s->sort_k1.p, static_cast<int>(n), 0, 64, s->st));
+    int* pin_of = s->sort_v0.p;
+    int* head = s->sort_v1.p;
+    int* head_pos = reinterpret_cast<int*>(s->sort_k0.p); // k0 free now (cap >= n ints)
+    k_pp_csr<<<blocks_for(n, kBlock), kBlock, 0, s->st>>>(n, s->sort_k1, s->pp_inc, pin_of, head);
+    CK_LAUNCH();
+    bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, head, head_pos, static_cast<int>(n), s->st);
+    tmp = cub_scratch(s, bytes);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, head, head_pos, static_cast<int>(n), s->st));
+    k_pp_heads<<<blocks_for(n, kBlock), kBlock, 0, s->st>>>(n, head, head_pos, pin_of, s->pin_entry, s->pp_start,
+                                                            s->pp_entry, s->pp_pins);
+    CK_LAUNCH();
+}
+
+void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk,
+                       const Ctrl* ctrl)
+{
+    k_wirelength<<<nblk, kBlock, 0, s->st>>>(s->N, s->net_start, s->e_cell, s->e_off, s->cell_xy, s->anchor,
+                                             use_net_w ? s->net_w.p : nullptr, gamma, s->grad_e, part_wl, part_hp,
+                                             ctrl);
+    CK_LAUNCH();
+}
+
+void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk)
+{
+    launch_wirelength(s, gamma, use_net_w, part_wl, part_hp, nblk, nullptr);
+}
+
+void launch_pp(tdpg_session* s, int kind, double beta, double* part_pp, int nblk, const Ctrl* ctrl)
+{
+    k_pin_pairs<<<nblk, kBlock, 0, s->st>>>(s->pp_pins, s->pp_start, s->pp_entry, s->pp_inc, s->led_key, s->led_w,
+                                            s->pin_cell, s->pin_off, s->cell_xy, s->anchor, kind, beta, s->E,
+                                            s->grad_e, part_pp, ctrl);
+    CK_LAUNCH();
+}
+
+void launch_pp(tdpg_session* s, int kind, double beta, double* part_pp, int nblk)
+{
+    launch_pp(s, kind, beta, part_pp, nblk, nullptr);
+}
+
+void launch_density(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl)
+{
+    const GridDev g = grid_dev(s);
+    k_density_scatter<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(
+        s->C, s->cell_xy, s->cell_wh, s->cell_fixed, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
+    CK_LAUNCH();
+    k_density_bins<<<nblk, kBlock, 0, s->st>>>(s->grid.bins(), g, s->grid.acc, s->grid.has_fixed ? s->grid.base.p : nullptr,
+                                               s->grid.excess, part_d, ctrl);
+    CK_LAUNCH();
+}
+
+void launch_density(tdpg_session* s, double* part_d, int nblk) { launch_density(s, part_d, nblk, nullptr); }
+
+void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl)
+{
+    const GridDev g = grid_dev(s);
+    k_density_scatter<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(
+        s->C, s->cell_xy, s->cell_wh, s->cell_fixed, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
+    CK_LAUNCH();
+}
+
+void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl)
+{
+    const GridDev g = grid_dev(s);
+    k_density_bins<<<nblk, kBlock, 0, s->st>>>(s->grid.bins(), g, s->grid.acc, s->grid.has_fixed ? s->grid.base.p : nullptr,
+                                               s->grid.excess, part_d, ctrl);
+    CK_LAUNCH();
+}
+
+CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps)
+{
+    CellArgs a;
+    a.C = s->C;
+    a.ent_start = s->cell_ent_start;
+    a.ent = s->cell_ent;
+    a.grad_e = s->grad_e;
+    a.fixed = s->cell_fixed;
+    a.xy = s->cell_xy;
+    a.wh = s->cell_wh;
+    a.g = grid_dev(s);
+    a.excess = s->grid.excess;
+    a.d_cell = d_cell;
+    a.m = m, a.v = v;
+    a.b1 = b1, a.b2 = b2, a.eps = eps;
+    a.core_x0 = s->core[0], a.core_y0 = s->core[1], a.core_x1 = s->core[2], a.core_y1 = s->core[3];
+    return a;
+}
+
+// One full objective_and_gradient evaluation at the session's positions.
+Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double beta, int kind, bool use_net_w,
+                         double* d_cell_host)
+{
+    if (!s->grid.valid()) throw Error(TDPG_ERR_VALIDATION, "validation error: density grid not set");
+    const int nb_wa = wa_blocks(s), nb_pp = pp_blocks(s), nb_d = bins_blocks(s);
+    s->part.reserve(2 * nb_wa + nb_pp + 2 * nb_d + 64);
+    double* part_wl = s->part.p;
+    double* part_hp = part_wl + nb_wa;
+    double* part_pp = part_hp + nb_wa;
+    double* part_d = part_pp + nb_pp;
+    Terms* terms = reinterpret_cast<Terms*>(part_d + 2 * nb_d);
+    IterCur* cur = reinterpret_cast<IterCur*>(terms + 1);
+    launch_wirelength(s, gamma, use_net_w, part_wl, part_hp, nb_wa);
+    const bool pp = s->Q > 0;
+    if (pp) {
+        rebuild_pp_incidence(s);
+        launch_pp(s, kind, beta, part_pp, nb_pp);
+    }
+    launch_density(s, part_d, nb_d);
+    FinArgs fa{};
+    fa.part_wl = part_wl, fa.part_hp = part_hp, fa.part_pp = part_pp, fa.part_d = part_d;
+    fa.nb_wa = nb_wa, fa.nb_pp = pp ? nb_pp : 0, fa.nb_d = nb_d;
+    fa.total_movable = s->grid.total_movable, fa.beta = beta, fa.sched = nullptr, fa.lambda_single = lambda;
+    fa.terms = terms;
+    k_finalize<<<1, kBlock, 0, s->st>>>(fa, nullptr, cur);
+    CK_LAUNCH();
+    const CellArgs ca = cell_args(s, s->d_cell, nullptr, nullptr, 0, 0, 0);
+    k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, nullptr);
+    CK_LAUNCH();
+    Terms t;
+    CK(cudaMemcpyAsync(&t, terms, sizeof(Terms), cudaMemcpyDeviceToHost, s->st));
+    if (d_cell_host) s->d_cell.download(reinterpret_cast<double2*>(d_cell_host), s->C, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    return t;
+}
+
+} // namespace tdpg
+
+using namespace tdpg;
+
+#define API_BEGIN try {
+#define API_END                                                                   \
+    return TDPG_OK;                                                               \
+    }                                                                             \
+    catch (const ::tdpg::Error& e) { return ::tdpg::api_fail(e.kind, e.what()); } \
+    catch (const std::exception& e) { return ::tdpg::api_fail(TDPG_ERR_INTERNAL, e.what()); }
+
+namespace {
+
+void check_finite_terms(const Terms& t, const double* d_cell, int C)
+{
+    bool ok = std::isfinite(t.value) && std::isfinite(t.wl) && std::isfinite(t.density) && std::isfinite(t.pp);
+    for (int i = 0; ok && d_cell && i < 2 * C; ++i) ok = std::isfinite(d_cell[i]);
+    if (!ok) throw Error(TDPG_ERR_NONFINITE, "non-finite value: non-finite objective or gradient");
+}
+
+void set_net_w(tdpg_session* s, const double* net_w)
+{
+    if (!net_w) return;
+    s->net_w.upload(net_w, static_cast<size_t>(s->N), s->st);
+}
+
+} // namespace
+
+extern "C" {
+
+int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* wl, double* hpwl, double* pin_grad)
+{
+    API_BEGIN
+    set_net_w(s, net_w);
+    const int nb = wa_blocks(s);
+    s->part.reserve(2 * nb + 8);
+    launch_wirelength(s, gamma, net_w != nullptr, s->part.p, s->part.p + nb, nb);
+    std::vector<double> part(2 * nb);
+    s->part.download(part.data(), part.size(), s->st);
+    std::vector<double2> ge;
+    if (pin_grad) {
+        ge.resize(s->E);
+        s->grad_e.download(ge.data(), ge.size(), s->st);
+    }
+    CK(cudaStreamSynchronize(s->st));
+    double a = 0, b = 0;
+    for (int i = 0; i < nb; ++i) a += part[i], b += part[nb + i];
+    if (wl) *wl = a;
+    if (hpwl) *hpwl = b;
+    if (pin_grad) {
+        std::fill(pin_grad, pin_grad + 2 * static_cast<size_t>(s->P), 0.0);
+        for (int e = 0; e < s->E; ++e) {
+            const int p = s->h_net_pins[e];
+            pin_grad[2 * p] = ge[e].x, pin_grad[2 * p + 1] = ge[e].y;
+        }
+    }
+    API_END
+}
+
+int tdpg_density(tdpg_session* s, double* value, double* overflow, double* d_cell)
+{
+    API_BEGIN
+    if (!s->grid.valid()) throw Error(TDPG_ERR_VALIDATION, "validation error: density grid not set");
+    // Density alone = objective with the WA/PP contributions removed: run the density
+    // kernels and the cell kernel with zero entry gradients and lambda = 1.
+    const int nb_d = bins_blocks(s);
+    s->part.reserve(2 * nb_d + 64);
+    double* part_d = s->part.p;
+    Terms* terms = reinterpret_cast<Terms*>(part_d + 2 * nb_d);
+    IterCur* cur = reinterpret_cast<IterCur*>(terms + 1);
+    launch_density(s, part_d, nb_d);
+    FinArgs fa{};
+    fa.part_d = part_d, fa.nb_d = nb_d, fa.total_movable = s->grid.total_movable, fa.lambda_single = 1.0;
+    fa.terms = terms;
+    k_finalize<<<1, kBlock, 0, s->st>>>(fa, nullptr, cur);
+    CK_LAUNCH();
+    if (d_cell) {
+        s->grad_e.zero(s->st, s->E_tot);
+        const CellArgs ca = cell_args(s, s->d_cell, nullptr, nullptr, 0, 0, 0);
+        k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, nullptr);
+        CK_LAUNCH();
+        s->d_cell.download(reinterpret_cast<double2*>(d_cell), s->C, s->st);
+    }
+    Terms t;
+    CK(cudaMemcpyAsync(&t, terms, sizeof(Terms), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    *value = t.density;
+    *overflow = t.overflow;
+    API_END
+}
+
+int tdpg_pp_loss(tdpg_session* s, int32_t kind, double* value, double* d_pin)
+{
+    API_BEGIN
+    const int nb = pp_blocks(s);
+    s->part.reserve(nb + 8);
+    double v = 0.0;
+    if (d_pin) std::fill(d_pin, d_pin + 2 * static_cast<size_t>(s->P), 0.0);
+    if (s->Q > 0) {
+        rebuild_pp_incidence(s);
+        s->grad_e.zero(s->st, s->E_tot);
+        launch_pp(s, kind, 1.0, s->part.p, nb);
+        std::vector<double> part(nb);
+        s->part.download(part.data(), nb, s->st);
+        std::vector<double2> ge;
+        if (d_pin) {
+            ge.resize(s->E_tot);
+            s->grad_e.download(ge.data(), ge.size(), s->st);
+        }
+        CK(cudaStreamSynchronize(s->st));
+        for (double x : part) v += x;
+        if (d_pin)
+            for (int p = 0; p < s->P; ++p) {
+                const int e = s->h_pin_entry[p];
+                if (e >= 0) d_pin[2 * p] = ge[e].x, d_pin[2 * p + 1] = ge[e].y;
+            }
+    }
+    *value = v;
+    API_END
+}
+
+int tdpg_objective(tdpg_session* s, double gamma, double lambda, double beta, int32_t pp_kind, const double* net_w,
+                   double terms[6], double* d_cell)
+{
+    API_BEGIN
+    if (net_w) set_net_w(s, net_w);
+    std::vector<double> tmp;
+    double* g = d_cell;
+    if (!g) {
+        tmp.resize(2 * static_cast<size_t>(s->C));
+        g = tmp.data();
+    }
+    const Terms t = evaluate_objective(s, gamma, lambda, beta, pp_kind, net_w != nullptr, g);
+    terms[0] = t.value, terms[1] = t.wl, terms[2] = t.density, terms[3] = t.pp, terms[4] = t.hpwl,
+    terms[5] = t.overflow;
+    check_finite_terms(t, g, s->C);
+    API_END
+}
+
+int tdpg_adam_step(int64_t n, double* x, const double* g, double* m, double* v, int32_t* t, double lr, double b1,
+                   double b2, double eps)
+{
+    API_BEGIN
+    if (tdpg_device_count() == 0) throw Error(TDPG_ERR_CUDA, "cuda error: no CUDA device available");
+    ++*t;
+    const double c1 = 1.0 - std::pow(b1, *t); // host-side scalars, bitwise std::pow like the reference
+    const double c2 = 1.0 - std::pow(b2, *t);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DBuf<double> dx(n), dg(n), dm(n), dv(n);
+    dx.upload(x, n, st), dg.upload(g, n, st), dm.upload(m, n, st), dv.upload(v, n, st);
+    k_adam_flat<<<blocks_for(n, kBlock), kBlock, 0, st>>>(n, dx, dg, dm, dv, lr, b1, b2, eps, c1, c2);
+    CK_LAUNCH();
+    dx.download(x, n, st), dm.download(m, n, st), dv.download(v, n, st);
+    CK(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    API_END
+}
+
+} // extern "C"
+
+// Placement-loop internals used by place.cu
+namespace tdpg {
+void launch_wirelength_ctrl(tdpg_session* s, double gamma, bool use_net_w, double* pw, double* ph, int nb,
+                            const Ctrl* ctrl)
+{
+    launch_wirelength(s, gamma, use_net_w, pw, ph, nb, ctrl);
+}
+void launch_pp_ctrl(tdpg_session* s, int kind, double beta, double* pp, int nb, const Ctrl* ctrl)
+{
+    launch_pp(s, kind, beta, pp, nb, ctrl);
+}
+void launch_density_ctrl(tdpg_session* s, double* pd, int nb, const Ctrl* ctrl) { launch_density(s, pd, nb, ctrl); }
+void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur)
+{
+    k_finalize<<<1, kBlock, 0, s->st>>>(fa, ctrl, cur);
+    CK_LAUNCH();
+}
+void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
+                  const IterCur* cur, Ctrl* ctrl)
+{
+    const CellArgs ca = cell_args(s, d_cell, m, v, b1, b2, eps);
+    k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, ctrl);
+    CK_LAUNCH();
+}
+} // namespace tdpg

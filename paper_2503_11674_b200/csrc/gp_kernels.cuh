@@ -1,0 +1,109 @@
+// gp_kernels.cuh — per-iteration GP kernels (WA wirelength, pin-pair attraction,
+// bin density, fused gradient fold + Adam).  fp64, compiled with -fmad=false so
+// every expression rounds exactly like the reference's x86-64 build.
+#pragma once
+
+#include "engine.cuh"
+
+namespace tdpg {
+
+constexpr int kBlock = 256;
+constexpr int kWaRegPins = 8; // nets up to this size keep pins/exps in registers
+
+__device__ __forceinline__ double2 entry_pos(int ec, double2 off, const double2* __restrict__ cell_xy,
+                                             const double2* __restrict__ anchor)
+{
+    const double2 a = ec >= 0 ? cell_xy[ec] : anchor[-1 - ec];
+    return make_double2(a.x + off.x, a.y + off.y); // netlist.cpp:28-29
+}
+
+__device__ __forceinline__ double2 pin_pos(int p, const int* __restrict__ pin_cell, const double2* __restrict__ off,
+                                           const double2* __restrict__ cell_xy, const double2* __restrict__ anchor)
+{
+    const int c = pin_cell[p];
+    const double2 a = c >= 0 ? cell_xy[c] : anchor[p];
+    const double2 o = off[p];
+    return make_double2(a.x + o.x, a.y + o.y);
+}
+
+// ---- bspline footprint (density.cpp:13-49) ---------------------------------------
+__device__ __forceinline__ double bspline2(double u)
+{
+    const double a = fabs(u);
+    if (a >= 1.5) return 0.0;
+    if (a <= 0.5) return 0.75 - a * a;
+    const double t = 1.5 - a;
+    return 0.5 * t * t;
+}
+
+__device__ __forceinline__ double bspline2_integral(double u)
+{
+    if (u <= -1.5) return 0.0;
+    if (u >= 1.5) return 1.0;
+    if (u <= -0.5) {
+        const double t = u + 1.5;
+        return t * t * t / 6.0;
+    }
+    if (u <= 0.5) return 0.5 + 0.75 * u - u * u * u / 3.0;
+    const double t = 1.5 - u;
+    return 1.0 - t * t * t / 6.0;
+}
+
+__device__ __forceinline__ double extent_weight(double lo, double hi, double c, double h)
+{
+    return (bspline2_integral((hi - c) / h) - bspline2_integral((lo - c) / h)) * h / (hi - lo);
+}
+
+__device__ __forceinline__ double extent_weight_grad(double lo, double hi, double c, double h)
+{
+    return (bspline2((hi - c) / h) - bspline2((lo - c) / h)) / (hi - lo);
+}
+
+struct GridDev {
+    int nx, ny;
+    double x0, y0, bw, bh, cap, scale, inv_scale, total_movable;
+};
+
+// Footprint bin range of a movable cell (density.cpp:109-112).
+__device__ __forceinline__ void footprint_range(const GridDev& g, double xl, double xh, double yl, double yh, int& bx0,
+                                                int& bx1, int& by0, int& by1)
+{
+    bx0 = max(0, static_cast<int>(floor((xl - 1.5 * g.bw - g.x0) / g.bw - 0.5)));
+    bx1 = min(g.nx - 1, static_cast<int>(ceil((xh + 1.5 * g.bw - g.x0) / g.bw - 0.5)));
+    by0 = max(0, static_cast<int>(floor((yl - 1.5 * g.bh - g.y0) / g.bh - 0.5)));
+    by1 = min(g.ny - 1, static_cast<int>(ceil((yh + 1.5 * g.bh - g.y0) / g.bh - 0.5)));
+}
+
+struct IterCur { // schedule values of the iteration being executed
+    double lr, c1, c2, lambda;
+    int iter, do_adam, pad0, pad1;
+};
+
+struct FinArgs {
+    const double *part_wl, *part_hp, *part_pp, *part_d;
+    int nb_wa, nb_pp, nb_d;
+    double total_movable, beta;
+    const Sched* sched;      // per-iteration schedule, or null (single evaluation)
+    double lambda_single;    // lambda when sched == null
+    double stop_overflow;
+    Terms* terms;
+    TraceRowDev* trace;      // may be null
+    const double* timing_row; // [has_timing, tns, wns] written by the timing refresh
+    double* timing_row_clear;
+};
+
+// launchers shared by gp.cu / place.cu
+void launch_wirelength_ctrl(tdpg_session* s, double gamma, bool use_net_w, double* pw, double* ph, int nb,
+                            const Ctrl* ctrl);
+void launch_pp_ctrl(tdpg_session* s, int kind, double beta, double* pp, int nb, const Ctrl* ctrl);
+void launch_density_ctrl(tdpg_session* s, double* pd, int nb, const Ctrl* ctrl);
+void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl);
+void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl);
+void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur);
+void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
+                  const IterCur* cur, Ctrl* ctrl);
+void run_sta_async(tdpg_session* s, double* out3);
+void ledger_apply_sorted(tdpg_session* s, long long H, double wns, double w0, double w1);
+int api_fail(int kind, const std::string& msg);
+
+} // namespace tdpg

@@ -1,0 +1,471 @@
+// place.cu — run_placement (placer.cpp:358-484) as a device-resident loop.
+//
+// One GP iteration = WA -> pin pairs -> density scatter -> density bins -> finalize ->
+// cells (fold + density gradient + Adam + clamp), captured once as a CUDA graph and
+// replayed; per-iteration scalars (lr, Adam bias corrections, lambda) come from a
+// schedule table computed on the host with the reference's own std::pow sequence, so the
+// graph is identical every iteration.  The timing refresh (STA + extraction + ledger
+// update, placer.cpp:415-435) runs on the same stream before the scheduled iterations.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <random>
+
+#include "gp_kernels.cuh"
+
+namespace tdpg {
+
+GridDev grid_dev(const tdpg_session* s);
+
+struct Engine {
+    tdpg_config cfg{};
+    double span = 0, gamma = 0, lambda = 0, lambda_cap = 0;
+    DBuf<Sched> sched;
+    DBuf<Ctrl> ctrl;
+    DBuf<TraceRowDev> trace;
+    DBuf<double> timing_row; // has_timing, tns, wns
+    DBuf<IterCur> cur;
+    DBuf<Terms> terms;
+    DBuf<double2> m, v;
+    DBuf<double> part;
+    int nb_wa = 0, nb_pp = 0, nb_d = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    int launched = 0, refreshes = 0;
+    long long kernel_launches = 0;
+    int kernels_per_iter = 6;
+    double last_refresh_ms = 0, total_refresh_ms = 0;
+    ~Engine()
+    {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+    }
+};
+
+namespace {
+
+void validate_config(const tdpg_config& c)
+{ // placer.cpp:68-90, same messages
+    auto bad = [](const char* m) { throw Error(TDPG_ERR_VALIDATION, std::string("validation error: config: ") + m); };
+    if (c.grid_nx < 1 || c.grid_ny < 1) bad("density grid must be at least 1x1");
+    if (!(c.target_density > 0.0)) bad("target_density must be > 0");
+    if (!(c.gamma_frac > 0.0)) bad("gamma_frac must be > 0");
+    if (c.beta < 0.0) bad("beta must be >= 0");
+    if (c.m < 1) bad("m must be >= 1");
+    if (!(c.w0 > 0.0)) bad("w0 must be > 0");
+    if (c.w1 < 0.0) bad("w1 must be >= 0");
+    if (c.timing_start_iter < 0) bad("timing_start_iter must be >= 0");
+    if (c.k < 1) bad("k must be >= 1");
+    if (c.max_iters < 0) bad("max_iters must be >= 0");
+    if (c.stop_overflow < 0.0) bad("stop_overflow must be >= 0");
+    if (!(c.mu > 0.0)) bad("mu must be > 0");
+    if (!(c.lambda_max > 0.0)) bad("lambda_max must be > 0");
+    if (!(c.step0_frac > 0.0)) bad("step0_frac must be > 0");
+    if (!(c.step_decay > 0.0 && c.step_decay <= 1.0)) bad("step_decay must be in (0, 1]");
+    if (!(c.adam_beta1 >= 0.0 && c.adam_beta1 < 1.0) || !(c.adam_beta2 >= 0.0 && c.adam_beta2 < 1.0))
+        bad("adam betas must be in [0, 1)");
+    if (!(c.adam_eps > 0.0)) bad("adam_eps must be > 0");
+    if (c.init_jitter_frac < 0.0) bad("init_jitter_frac must be >= 0");
+    if (c.threads < 1) bad("threads must be >= 1");
+    if (c.extraction != 0) throw Error(TDPG_ERR_INTERNAL, "the topn extraction policy is not implemented on the device yet");
+    if (c.k != 1) throw Error(TDPG_ERR_INTERNAL, "k > 1 per endpoint is not implemented on the device yet");
+}
+
+__global__ void k_l1_pair(int C, const double2* __restrict__ a, const double2* __restrict__ b,
+                          const uint8_t* __restrict__ fixed, double* __restrict__ part)
+{
+    __shared__ double sh[kBlock / 32];
+    double sa = 0.0, sb = 0.0;
+    for (int c = blockIdx.x * kBlock + threadIdx.x; c < C; c += gridDim.x * kBlock) {
+        if (fixed[c]) continue;
+        sa += fabs(a[c].x) + fabs(a[c].y);
+        sb += fabs(b[c].x) + fabs(b[c].y);
+    }
+    sa = block_sum<kBlock>(sa, sh);
+    sb = block_sum<kBlock>(sb, sh);
+    if (threadIdx.x == 0) part[2 * blockIdx.x] = sa, part[2 * blockIdx.x + 1] = sb;
+}
+
+// lambda0 "auto": |grad WL|_1 / |grad D|_1 over movable cells (placer.cpp:388-402).
+double lambda_auto(tdpg_session* s, double gamma, int kind)
+{
+    evaluate_objective(s, gamma, 0.0, 0.0, kind, false, nullptr);
+    DBuf<double2> wl(s->C);
+    CK(cudaMemcpyAsync(wl.p, s->d_cell.p, sizeof(double2) * s->C, cudaMemcpyDeviceToDevice, s->st));
+    // density-only gradient: zero entry gradients, lambda = 1
+    const int nb_d = bins_blocks(s);
+    DBuf<double> part(2 * nb_d + 64);
+    Terms* terms = reinterpret_cast<Terms*>(part.p + 2 * nb_d);
+    IterCur* cur = reinterpret_cast<IterCur*>(terms + 1);
+    launch_density(s, part.p, nb_d);
+    FinArgs fa{};
+    fa.part_d = part.p, fa.nb_d = nb_d, fa.total_movable = s->grid.total_movable, fa.lambda_single = 1.0;
+    fa.terms = terms;
+    launch_finalize(s, fa, nullptr, cur);
+    s->grad_e.zero(s->st, s->E_tot);
+    launch_cells(s, s->d_cell, nullptr, nullptr, 0, 0, 0, cur, nullptr);
+    const int nb = 148 * 2;
+    DBuf<double> p2(2 * nb);
+    k_l1_pair<<<nb, kBlock, 0, s->st>>>(s->C, wl, s->d_cell, s->cell_fixed, p2);
+    CK_LAUNCH();
+    std::vector<double> h(2 * nb);
+    p2.download(h.data(), h.size(), s->st);
+    CK(cudaStreamSynchronize(s->st));
+    double wl1 = 0.0, d1 = 0.0;
+    for (int i = 0; i < nb; ++i) wl1 += h[2 * i], d1 += h[2 * i + 1];
+    return (wl1 > 0.0 && d1 > 0.0) ? wl1 / d1 : 1.0;
+}
+
+void capture_iteration(tdpg_session* s, Engine& E)
+{
+    if (E.gexec) cudaGraphExecDestroy(E.gexec), E.gexec = nullptr;
+    if (E.graph) cudaGraphDestroy(E.graph), E.graph = nullptr;
+    double* part_wl = E.part.p;
+    double* part_hp = part_wl + E.nb_wa;
+    double* part_pp = part_hp + E.nb_wa;
+    double* part_d = part_pp + E.nb_pp;
+    FinArgs fa{};
+    fa.part_wl = part_wl, fa.part_hp = part_hp, fa.part_pp = part_pp, fa.part_d = part_d;
+    fa.nb_wa = E.nb_wa, fa.nb_pp = E.nb_pp, fa.nb_d = E.nb_d;
+    fa.total_movable = s->grid.total_movable, fa.beta = E.cfg.beta;
+    fa.sched = E.sched, fa.stop_overflow = E.cfg.stop_overflow, fa.terms = E.terms, fa.trace = E.trace;
+    fa.timing_row = E.timing_row, fa.timing_row_clear = E.timing_row;
+    CK(cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
+    launch_wirelength_ctrl(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, E.nb_wa, E.ctrl);
+    launch_pp_ctrl(s, E.cfg.pp_loss, E.cfg.beta, part_pp, E.nb_pp, E.ctrl);
+    launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
+    launch_finalize(s, fa, E.ctrl, E.cur);
+    launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl);
+    CK(cudaStreamEndCapture(s->st, &E.graph));
+    CK(cudaGraphInstantiate(&E.gexec, E.graph, 0));
+}
+
+} // namespace
+
+void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit)
+{
+    validate_config(*cfg);
+    auto E = std::make_unique<Engine>();
+    E->cfg = *cfg;
+    const double cw = s->core[2] - s->core[0], ch = s->core[3] - s->core[1];
+    E->span = cw > ch ? cw : ch; // Rect::span (geometry.hpp:34)
+    E->gamma = cfg->gamma_frac * E->span;
+
+    // implicit starts get a seeded jitter (placer.cpp:375-382): mt19937_64 + rng_uniform
+    std::vector<double> xy(2 * static_cast<size_t>(s->C));
+    s->cell_xy.download(reinterpret_cast<double2*>(xy.data()), s->C, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    std::mt19937_64 rng(cfg->seed);
+    auto unit = [&] { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
+    for (int c = 0; c < s->C; ++c) {
+        if (s->h_cell_fixed[c] || (pos_explicit && pos_explicit[c])) continue;
+        xy[2 * c] += (-1.0 + (1.0 - -1.0) * unit()) * cfg->init_jitter_frac * cw;
+        xy[2 * c + 1] += (-1.0 + (1.0 - -1.0) * unit()) * cfg->init_jitter_frac * ch;
+        const double xh = s->core[2] - s->h_cell_w[c], yh = s->core[3] - s->h_cell_h[c];
+        double& x = xy[2 * c];
+        double& y = xy[2 * c + 1];
+        x = std::clamp(x, s->core[0], xh);
+        y = std::clamp(y, s->core[1], yh);
+    }
+    upload_positions(s, xy.data());
+    ensure_grid(s, cfg->grid_nx, cfg->grid_ny, cfg->target_density);
+
+    // fresh ledger; buffers sized for the bound Q <= A_net so graph pointers stay valid
+    const size_t qcap = static_cast<size_t>(std::max(s->A_net, 1)) + 1;
+    s->Q = 0;
+    s->led_key.reserve(qcap), s->led_w.reserve(qcap), s->led_key2.reserve(qcap), s->led_w2.reserve(qcap);
+    s->pp_inc.reserve(2 * qcap), s->pp_start.reserve(2 * qcap + 1), s->pp_entry.reserve(2 * qcap);
+    s->pp_pins.reserve(4);
+    s->pp_dirty = true;
+    rebuild_pp_incidence(s);
+    s->net_w.reserve(std::max(s->N, 1));
+    if (cfg->net_weighting) {
+        std::vector<double> ones(s->N, 1.0);
+        s->net_w.upload(ones, s->st);
+    }
+
+    E->lambda = cfg->lambda0 > 0.0 ? cfg->lambda0 : lambda_auto(s, E->gamma, cfg->pp_loss);
+    E->lambda_cap = E->lambda * cfg->lambda_max;
+
+    // per-iteration schedule (placer.cpp:470-471, :349-350, :477)
+    const int T = std::max(cfg->max_iters, 1);
+    std::vector<Sched> sch(T);
+    double lam = E->lambda;
+    for (int it = 0; it < T; ++it) {
+        sch[it].lr = cfg->step0_frac * E->span * std::pow(cfg->step_decay, it);
+        sch[it].c1 = 1.0 - std::pow(cfg->adam_beta1, it + 1);
+        sch[it].c2 = 1.0 - std::pow(cfg->adam_beta2, it + 1);
+        sch[it].lambda = lam;
+        lam = std::min(lam * cfg->mu, E->lambda_cap);
+    }
+    E->sched.upload(sch, s->st);
+    Ctrl c0{};
+    c0.nonfinite_at = INT_MAX;
+    E->ctrl.alloc(1);
+    CK(cudaMemcpyAsync(E->ctrl.p, &c0, sizeof c0, cudaMemcpyHostToDevice, s->st));
+    E->trace.alloc(T);
+    E->timing_row.alloc(3);
+    E->timing_row.zero(s->st);
+    E->cur.alloc(1);
+    E->terms.alloc(1);
+    E->m.alloc(s->C), E->v.alloc(s->C);
+    E->m.zero(s->st), E->v.zero(s->st);
+    E->nb_wa = wa_blocks(s), E->nb_pp = pp_blocks(s), E->nb_d = bins_blocks(s);
+    E->part.alloc(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
+    E->part.zero(s->st);
+    delete s->eng;
+    s->eng = E.release();
+    capture_iteration(s, *s->eng);
+    CK(cudaStreamSynchronize(s->st));
+}
+
+Ctrl read_ctrl(tdpg_session* s)
+{
+    Ctrl c;
+    CK(cudaMemcpyAsync(&c, s->eng->ctrl.p, sizeof c, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    return c;
+}
+
+// Timing round (placer.cpp:415-435).  Returns false when the loop already stopped.
+bool timing_refresh(tdpg_session* s)
+{
+    Engine& E = *s->eng;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s->st));
+    const Ctrl c = read_ctrl(s);
+    if (c.stopped) {
+        cudaEventDestroy(e0), cudaEventDestroy(e1);
+        return false;
+    }
+    run_sta_dev(s);
+    const double row[3] = {1.0, s->tns, s->wns};
+    CK(cudaMemcpyAsync(E.timing_row.p, row, sizeof row, cudaMemcpyHostToDevice, s->st));
+    const int one = 1;
+    CK(cudaMemcpyAsync(&E.ctrl.p->engaged, &one, sizeof one, cudaMemcpyHostToDevice, s->st));
+    if (s->wns < 0.0) {
+        extract_endpoint_dev(s, 0); // n = number of violated endpoints (placer.cpp:424-428)
+        ledger_apply_sorted(s, s->n_hits, s->wns, E.cfg.w0, E.cfg.w1);
+        rebuild_pp_incidence(s);
+    }
+    if (E.cfg.net_weighting) net_weights_dev(s);
+    // our kernels in this round: pin_xy + 2 per level + slack/final; extraction (slack/final,
+    // ties, two backtrace passes, head count), ledger groups, incidence (3), net weights
+    E.kernel_launches += 1 + 2LL * s->L + 2 + (s->wns < 0.0 ? 6 + 1 + 3 : 0) + (E.cfg.net_weighting ? 1 : 0);
+    CK(cudaEventRecord(e1, s->st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    E.last_refresh_ms = ms;
+    E.total_refresh_ms += ms;
+    cudaEventDestroy(e0), cudaEventDestroy(e1);
+    ++E.refreshes;
+    return true;
+}
+
+// Run up to n iterations of the loop (refreshes per schedule).  Returns iterations launched.
+int engine_run(tdpg_session* s, int n)
+{
+    Engine& E = *s->eng;
+    int done = 0;
+    for (; done < n && E.launched < E.cfg.max_iters; ++done) {
+        const int it = E.launched;
+        if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0)
+            if (!timing_refresh(s)) {
+                E.launched = E.cfg.max_iters; // loop ended (stop_overflow)
+                break;
+            }
+        CK(cudaGraphLaunch(E.gexec, s->st));
+        E.kernel_launches += E.kernels_per_iter;
+        ++E.launched;
+    }
+    return done;
+}
+
+} // namespace tdpg
+
+tdpg_session::~tdpg_session()
+{
+    delete eng; // Engine is complete here
+    if (st) cudaStreamDestroy(st);
+}
+
+using namespace tdpg;
+
+#define API_BEGIN try {
+#define API_END                                                                   \
+    return TDPG_OK;                                                               \
+    }                                                                             \
+    catch (const ::tdpg::Error& e) { return ::tdpg::api_fail(e.kind, e.what()); } \
+    catch (const std::exception& e) { return ::tdpg::api_fail(TDPG_ERR_INTERNAL, e.what()); }
+
+extern "C" {
+
+int tdpg_engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit)
+{
+    API_BEGIN
+    engine_init(s, cfg, pos_explicit);
+    API_END
+}
+
+int tdpg_iterate_dev(tdpg_session* s, int32_t n, double* device_ms)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s->st));
+    engine_run(s, n);
+    CK(cudaEventRecord(e1, s->st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (device_ms) *device_ms = ms;
+    cudaEventDestroy(e0), cudaEventDestroy(e1);
+    const Ctrl c = read_ctrl(s);
+    if (c.nonfinite_at != INT_MAX)
+        throw Error(TDPG_ERR_NONFINITE, "non-finite value: non-finite objective or gradient at iteration " +
+                                            std::to_string(c.nonfinite_at));
+    API_END
+}
+
+// Per-kernel device time of `reps` loop iterations (no refresh), CUDA events between launches.
+int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_t n_out, char* names, int32_t name_len)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
+    Engine& E = *s->eng;
+    static const char* kNames[6] = {"wirelength", "pin_pairs", "density_scatter", "density_bins", "finalize", "cells"};
+    double* part_wl = E.part.p;
+    double* part_hp = part_wl + E.nb_wa;
+    double* part_pp = part_hp + E.nb_wa;
+    double* part_d = part_pp + E.nb_pp;
+    FinArgs fa{};
+    fa.part_wl = part_wl, fa.part_hp = part_hp, fa.part_pp = part_pp, fa.part_d = part_d;
+    fa.nb_wa = E.nb_wa, fa.nb_pp = E.nb_pp, fa.nb_d = E.nb_d;
+    fa.total_movable = s->grid.total_movable, fa.beta = E.cfg.beta;
+    fa.sched = E.sched, fa.stop_overflow = E.cfg.stop_overflow, fa.terms = E.terms, fa.trace = E.trace;
+    fa.timing_row = E.timing_row, fa.timing_row_clear = E.timing_row;
+    cudaEvent_t ev[7];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (int r = 0; r < reps && E.launched < E.cfg.max_iters; ++r) {
+        CK(cudaEventRecord(ev[0], s->st));
+        launch_wirelength_ctrl(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, E.nb_wa, E.ctrl);
+        CK(cudaEventRecord(ev[1], s->st));
+        launch_pp_ctrl(s, E.cfg.pp_loss, E.cfg.beta, part_pp, E.nb_pp, E.ctrl);
+        CK(cudaEventRecord(ev[2], s->st));
+        launch_density_scatter_ctrl(s, E.ctrl);
+        CK(cudaEventRecord(ev[3], s->st));
+        launch_density_bins_ctrl(s, part_d, E.nb_d, E.ctrl);
+        CK(cudaEventRecord(ev[4], s->st));
+        launch_finalize(s, fa, E.ctrl, E.cur);
+        CK(cudaEventRecord(ev[5], s->st));
+        launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl);
+        CK(cudaEventRecord(ev[6], s->st));
+        CK(cudaEventSynchronize(ev[6]));
+        for (int k = 0; k < 6; ++k) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+            acc[k] += ms;
+        }
+        ++E.launched;
+        E.kernel_launches += E.kernels_per_iter;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < 6 && k < n_out; ++k) {
+        out_ms[k] = acc[k] / std::max(reps, 1);
+        if (names && name_len > 0) {
+            std::strncpy(names + static_cast<size_t>(k) * name_len, kNames[k], name_len - 1);
+            names[static_cast<size_t>(k) * name_len + name_len - 1] = 0;
+        }
+    }
+    API_END
+}
+
+// One loop iteration through host buffers: positions in (pinned host -> device), the
+// iteration (with its scheduled timing refresh), positions + trace row out.  This is the
+// reference-shaped objective_and_gradient + AdamState::step call with host vectors.
+int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_trace_row* row)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
+    Engine& E = *s->eng;
+    if (xy_in) {
+        CK(cudaMemcpyAsync(s->cell_xy.p, xy_in, sizeof(double2) * s->C, cudaMemcpyHostToDevice, s->st));
+        s->sta_valid = false;
+    }
+    const int it = E.launched;
+    engine_run(s, 1);
+    if (xy_out) CK(cudaMemcpyAsync(xy_out, s->cell_xy.p, sizeof(double2) * s->C, cudaMemcpyDeviceToHost, s->st));
+    TraceRowDev r{};
+    if (row && it < E.cfg.max_iters)
+        CK(cudaMemcpyAsync(&r, E.trace.p + it, sizeof r, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (row) {
+        row->iter = r.iter, row->has_timing = r.has_timing, row->hpwl = r.hpwl, row->overflow = r.overflow;
+        row->tns = r.tns, row->wns = r.wns, row->wl_term = r.wl_term, row->density_term = r.density_term;
+        row->pp_term = r.pp_term, row->lambda = r.lambda, row->beta_pp = r.beta_pp;
+    }
+    API_END
+}
+
+int tdpg_engine_stats(tdpg_session* s, int32_t* iter, int32_t* refreshes, int64_t* launches)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised");
+    if (iter) *iter = s->eng->launched;
+    if (refreshes) *refreshes = s->eng->refreshes;
+    if (launches) *launches = s->eng->kernel_launches;
+    API_END
+}
+
+int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit, tdpg_trace_row* trace,
+               int32_t* n_rows, int32_t* stop_overflow, double final_[3])
+{
+    API_BEGIN
+    engine_init(s, cfg, pos_explicit);
+    engine_run(s, cfg->max_iters);
+    const Ctrl c = read_ctrl(s);
+    if (c.nonfinite_at != INT_MAX)
+        throw Error(TDPG_ERR_NONFINITE, "non-finite value: non-finite objective or gradient at iteration " +
+                                            std::to_string(c.nonfinite_at));
+    const int rows = c.rows;
+    if (trace && rows > 0) {
+        std::vector<TraceRowDev> tr(rows);
+        s->eng->trace.download(tr.data(), rows, s->st);
+        CK(cudaStreamSynchronize(s->st));
+        for (int i = 0; i < rows; ++i) {
+            tdpg_trace_row& r = trace[i];
+            r.iter = tr[i].iter, r.has_timing = tr[i].has_timing, r.hpwl = tr[i].hpwl, r.overflow = tr[i].overflow;
+            r.tns = tr[i].tns, r.wns = tr[i].wns, r.wl_term = tr[i].wl_term, r.density_term = tr[i].density_term;
+            r.pp_term = tr[i].pp_term, r.lambda = tr[i].lambda, r.beta_pp = tr[i].beta_pp;
+        }
+    }
+    if (n_rows) *n_rows = rows;
+    if (stop_overflow) *stop_overflow = c.stopped;
+    // final STA + exact HPWL at the returned positions (placer.cpp:482, bindings.cpp:381-382)
+    run_sta_dev(s);
+    double hp = 0.0;
+    {
+        const int nb = wa_blocks(s);
+        s->part.reserve(2 * nb + 8);
+        launch_wirelength(s, s->eng->gamma, false, s->part.p, s->part.p + nb, nb);
+        std::vector<double> h(nb);
+        s->part.download(h.data(), nb, s->st);
+        // part.p + nb holds hpwl partials
+        s->part.download(h.data(), 0, s->st);
+        std::vector<double> hh(nb);
+        CK(cudaMemcpyAsync(hh.data(), s->part.p + nb, nb * sizeof(double), cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        for (double x : hh) hp += x;
+    }
+    if (final_) final_[0] = s->tns, final_[1] = s->wns, final_[2] = hp;
+    API_END
+}
+
+} // extern "C"

@@ -1,0 +1,510 @@
+// session.cu — session lifetime, netlist upload, timing-graph build, C-ABI plumbing.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "engine.cuh"
+
+using namespace tdpg;
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_kind = 0;
+} // namespace
+
+namespace tdpg {
+
+int api_fail(int kind, const std::string& msg)
+{
+    g_err = msg;
+    g_kind = kind;
+    return kind;
+}
+
+} // namespace tdpg
+
+#define API_BEGIN try {
+#define API_END                                                     \
+    return TDPG_OK;                                                 \
+    }                                                               \
+    catch (const ::tdpg::Error& e) { return ::tdpg::api_fail(e.kind, e.what()); } \
+    catch (const std::bad_alloc&) { return ::tdpg::api_fail(TDPG_ERR_INTERNAL, "out of host memory"); } \
+    catch (const std::exception& e) { return ::tdpg::api_fail(TDPG_ERR_INTERNAL, e.what()); }
+
+
+namespace tdpg {
+
+void* cub_scratch(tdpg_session* s, size_t bytes)
+{
+    s->cub_tmp.reserve(bytes);
+    return s->cub_tmp.p;
+}
+
+// Kernel: pin positions (netlist.cpp:23-32): anchor + offset, two IEEE adds.
+__global__ void k_fixed_baseline(int C, const double2* xy, const double2* wh, const uint8_t* fixed, double x0,
+                                 double y0, double bw, double bh, int nx, int ny, double* base)
+{
+    // Fixed cells are few; one thread per fixed cell, fp64 atomics into the baseline.
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C || !fixed[c]) return;
+    const double xl = xy[c].x, xh = xl + wh[c].x, yl = xy[c].y, yh = yl + wh[c].y;
+    const int bx0 = max(0, static_cast<int>(floor((xl - x0) / bw)));
+    const int bx1 = min(nx - 1, static_cast<int>(floor((xh - x0) / bw)));
+    const int by0 = max(0, static_cast<int>(floor((yl - y0) / bh)));
+    const int by1 = min(ny - 1, static_cast<int>(floor((yh - y0) / bh)));
+    for (int bx = bx0; bx <= bx1; ++bx)
+        for (int by = by0; by <= by1; ++by) {
+            const double ox = smin(xh, x0 + (bx + 1) * bw) - smax(xl, x0 + bx * bw);
+            const double oy = smin(yh, y0 + (by + 1) * bh) - smax(yl, y0 + by * bh);
+            if (ox > 0.0 && oy > 0.0) atomicAdd(&base[static_cast<long long>(bx) * ny + by], ox * oy);
+        }
+}
+
+void refresh_fixed_baseline(tdpg_session* s)
+{
+    Grid& g = s->grid;
+    if (!g.valid() || !g.has_fixed) return;
+    g.base.zero(s->st);
+    k_fixed_baseline<<<blocks_for(s->C, 256), 256, 0, s->st>>>(s->C, s->cell_xy, s->cell_wh, s->cell_fixed, g.x0,
+                                                                g.y0, g.bw, g.bh, g.nx, g.ny, g.base);
+    CK_LAUNCH();
+}
+
+void upload_positions(tdpg_session* s, const double* xy)
+{
+    s->h_cell_xy.assign(xy, xy + 2 * static_cast<size_t>(s->C));
+    s->cell_xy.upload(reinterpret_cast<const double2*>(xy), s->C, s->st);
+    s->sta_valid = false;
+    refresh_fixed_baseline(s);
+}
+
+// DensityGrid ctor (density.cpp:53-64).
+void ensure_grid(tdpg_session* s, int nx, int ny, double td)
+{
+    if (nx < 1 || ny < 1) throw Error(TDPG_ERR_VALIDATION, "validation error: density grid must be at least 1x1");
+    Grid& g = s->grid;
+    if (g.nx == nx && g.ny == ny && g.td == td) return;
+    g.nx = nx, g.ny = ny, g.td = td;
+    g.x0 = s->core[0], g.y0 = s->core[1];
+    g.bw = (s->core[2] - s->core[0]) / nx;
+    g.bh = (s->core[3] - s->core[1]) / ny;
+    g.cap = td * g.bw * g.bh;
+    double mov = 0.0, all = 0.0;
+    bool fixed = false;
+    for (int c = 0; c < s->C; ++c) {
+        const double a = s->h_cell_w[c] * s->h_cell_h[c];
+        all += a;
+        if (!s->h_cell_fixed[c]) mov += a;
+        else fixed = true;
+    }
+    g.total_movable = mov;
+    g.has_fixed = fixed;
+    // Fixed point: every bin's movable occupancy is <= total area, keep 2 bits of headroom.
+    int ex = 0;
+    std::frexp(std::max(all, 1e-300), &ex);
+    const int k = std::min(60 - ex, 1000);
+    g.scale = std::ldexp(1.0, k);
+    g.inv_scale = std::ldexp(1.0, -k);
+    const long long B = g.bins();
+    g.acc.alloc(B);
+    g.acc.zero(s->st);
+    g.excess.alloc(B);
+    if (fixed) {
+        g.base.alloc(B);
+        refresh_fixed_baseline(s);
+    } else {
+        g.base.release();
+    }
+}
+
+} // namespace tdpg
+
+namespace {
+
+void build_graph(tdpg_session* s)
+{
+    const int P = s->P, C = s->C;
+    s->h_is_source.assign(P, 0);
+    s->h_is_endpoint.assign(P, 0);
+    for (int v : s->h_sources) s->h_is_source[v] = 1;
+    for (int v : s->h_endpoints) s->h_is_endpoint[v] = 1;
+    // cell_pins, ascending (netlist.cpp:12-14)
+    std::vector<int> cps(C + 1, 0), cp;
+    for (int p = 0; p < P; ++p)
+        if (s->h_pin_cell[p] >= 0) cps[s->h_pin_cell[p] + 1]++;
+    for (int c = 0; c < C; ++c) cps[c + 1] += cps[c];
+    cp.resize(cps[C]);
+    {
+        std::vector<int> f(cps.begin(), cps.end() - 1);
+        for (int p = 0; p < P; ++p)
+            if (s->h_pin_cell[p] >= 0) cp[f[s->h_pin_cell[p]]++] = p;
+    }
+    // arcs: net arcs in (net, sink) order, then cell arcs (cell, input, output) (timing_graph.cpp:60-77)
+    auto& af = s->h_arc_from;
+    auto& at = s->h_arc_to;
+    auto& ak = s->h_arc_kind;
+    auto& ao = s->h_arc_owner;
+    af.clear(), at.clear(), ak.clear(), ao.clear();
+    const size_t reserve = static_cast<size_t>(s->E) * 2 + 16;
+    af.reserve(reserve), at.reserve(reserve), ak.reserve(reserve), ao.reserve(reserve);
+    for (int n = 0; n < s->N; ++n)
+        for (int e = s->h_net_start[n] + 1; e < s->h_net_start[n + 1]; ++e) {
+            af.push_back(s->h_net_pins[s->h_net_start[n]]), at.push_back(s->h_net_pins[e]), ak.push_back(0),
+                ao.push_back(n);
+        }
+    s->A_net = static_cast<int>(af.size());
+    for (int c = 0; c < C; ++c)
+        for (int i = cps[c]; i < cps[c + 1]; ++i) {
+            const int in = cp[i];
+            if (s->h_pin_dir[in] != 0 || s->h_is_endpoint[in]) continue;
+            for (int j = cps[c]; j < cps[c + 1]; ++j) {
+                const int out = cp[j];
+                if (s->h_pin_dir[out] != 1 || s->h_is_source[out]) continue;
+                af.push_back(in), at.push_back(out), ak.push_back(1), ao.push_back(c);
+            }
+        }
+    s->A = static_cast<int>(af.size());
+    s->A_cell = s->A - s->A_net;
+    const int A = s->A;
+    std::vector<int> in_s(P + 1, 0), out_s(P + 1, 0), in_a(A), out_a(A);
+    for (int a = 0; a < A; ++a) in_s[at[a] + 1]++, out_s[af[a] + 1]++;
+    for (int p = 0; p < P; ++p) in_s[p + 1] += in_s[p], out_s[p + 1] += out_s[p];
+    {
+        std::vector<int> fi(in_s.begin(), in_s.end() - 1), fo(out_s.begin(), out_s.end() - 1);
+        for (int a = 0; a < A; ++a) in_a[fi[at[a]]++] = a, out_a[fo[af[a]]++] = a;
+    }
+    // Kahn levelization, level = longest path from an in-degree-0 pin (timing_graph.cpp:87-104)
+    std::vector<int> indeg(P), order;
+    order.reserve(P);
+    s->h_level.assign(P, 0);
+    for (int p = 0; p < P; ++p) {
+        indeg[p] = in_s[p + 1] - in_s[p];
+        if (indeg[p] == 0) order.push_back(p);
+    }
+    for (size_t h = 0; h < order.size(); ++h) {
+        const int u = order[h];
+        for (int i = out_s[u]; i < out_s[u + 1]; ++i) {
+            const int v = at[out_a[i]];
+            s->h_level[v] = std::max(s->h_level[v], s->h_level[u] + 1);
+            if (--indeg[v] == 0) order.push_back(v);
+        }
+    }
+    auto name = [&](int p) { return s->pin_names.empty() ? "p" + std::to_string(p) : s->pin_names[p]; };
+    if (static_cast<int>(order.size()) != P) { // report_cycle (timing_graph.cpp:12-45)
+        std::vector<uint8_t> rem(P, 0);
+        int start = -1;
+        for (int p = 0; p < P; ++p)
+            if (indeg[p] > 0) rem[p] = 1, start = p;
+        std::vector<int> seen(P, -1), walk;
+        int cur = start;
+        while (seen[cur] < 0) {
+            seen[cur] = static_cast<int>(walk.size());
+            walk.push_back(cur);
+            for (int i = in_s[cur]; i < in_s[cur + 1]; ++i) {
+                const int u = af[in_a[i]];
+                if (rem[u]) {
+                    cur = u;
+                    break;
+                }
+            }
+        }
+        std::string msg;
+        for (size_t i = static_cast<size_t>(seen[cur]); i < walk.size(); ++i) {
+            if (!msg.empty()) msg += " <- ";
+            msg += name(walk[i]);
+        }
+        throw Error(TDPG_ERR_CYCLE, "validation error: combinational cycle: " + msg);
+    }
+    int max_level = 0;
+    for (int p = 0; p < P; ++p) max_level = std::max(max_level, s->h_level[p]);
+    s->L = max_level + 1;
+    s->h_lvl_start.assign(s->L + 1, 0);
+    for (int p = 0; p < P; ++p) s->h_lvl_start[s->h_level[p] + 1]++;
+    for (int l = 0; l < s->L; ++l) s->h_lvl_start[l + 1] += s->h_lvl_start[l];
+    s->h_lvl_pins.resize(P);
+    {
+        std::vector<int> f(s->h_lvl_start.begin(), s->h_lvl_start.end() - 1);
+        for (int p = 0; p < P; ++p) s->h_lvl_pins[f[s->h_level[p]]++] = p;
+    }
+    // endpoint reachability (timing_graph.cpp:112-135)
+    std::vector<uint8_t> reach(P, 0);
+    std::vector<int> stack;
+    for (int v : s->h_sources)
+        if (!reach[v]) reach[v] = 1, stack.push_back(v);
+    while (!stack.empty()) {
+        const int u = stack.back();
+        stack.pop_back();
+        for (int i = out_s[u]; i < out_s[u + 1]; ++i) {
+            const int v = at[out_a[i]];
+            if (!reach[v]) reach[v] = 1, stack.push_back(v);
+        }
+    }
+    for (int e : s->h_endpoints)
+        if (!reach[e])
+            throw Error(TDPG_ERR_VALIDATION, "validation error: endpoint \"" + name(e) + "\" unreachable from every source");
+
+    // device CSR: from-pins of in-arcs / to-pins of out-arcs, ascending arc id
+    std::vector<int> in_from(A), out_to(A);
+    for (int i = 0; i < A; ++i) in_from[i] = af[in_a[i]], out_to[i] = at[out_a[i]];
+    s->in_start.upload(in_s, s->st);
+    s->in_from.upload(in_from, s->st);
+    s->out_start.upload(out_s, s->st);
+    s->out_to.upload(out_to, s->st);
+    s->lvl_pins.upload(s->h_lvl_pins, s->st);
+    std::vector<int> eps(s->h_endpoints);
+    std::sort(eps.begin(), eps.end());
+    s->ep_sorted.upload(eps, s->st);
+}
+
+void check_netlist(const tdpg_netlist* d)
+{
+    auto bad = [](const std::string& m) { throw Error(TDPG_ERR_VALIDATION, "validation error: " + m); };
+    if (d->n_cells < 0 || d->n_pins < 0 || d->n_nets < 0) bad("negative sizes");
+    for (int p = 0; p < d->n_pins; ++p)
+        if (d->pin_cell[p] < -1 || d->pin_cell[p] >= d->n_cells) bad("pin cell id out of range");
+    if (d->net_start[0] != 0) bad("net_start[0] must be 0");
+    std::vector<int> owner(d->n_pins, -1);
+    for (int n = 0; n < d->n_nets; ++n) {
+        if (d->net_start[n + 1] - d->net_start[n] < 2) bad("net needs at least one sink");
+        for (int e = d->net_start[n]; e < d->net_start[n + 1]; ++e) {
+            const int p = d->net_pins[e];
+            if (p < 0 || p >= d->n_pins) bad("net pin id out of range");
+            if (owner[p] >= 0) bad("pin used by two nets");
+            owner[p] = n;
+        }
+    }
+    for (int i = 0; i < d->n_sources; ++i)
+        if (d->sources[i] < 0 || d->sources[i] >= d->n_pins) bad("source pin id out of range");
+    for (int i = 0; i < d->n_endpoints; ++i)
+        if (d->endpoints[i] < 0 || d->endpoints[i] >= d->n_pins) bad("endpoint pin id out of range");
+}
+
+} // namespace
+
+extern "C" {
+
+const char* tdpg_last_error(void) { return g_err.c_str(); }
+int tdpg_last_error_kind(void) { return g_kind; }
+const char* tdpg_version(void) { return "tdpg 0.1 (sm_100a, fp64)"; }
+
+int tdpg_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void tdpg_config_default(tdpg_config* c)
+{
+    std::memset(c, 0, sizeof *c); // placer.hpp:22-57
+    c->gamma_frac = 0.01, c->grid_nx = 16, c->grid_ny = 16, c->target_density = 0.6, c->beta = 2.5e-5;
+    c->m = 15, c->w0 = 10.0, c->w1 = 0.2, c->timing_start_iter = 500, c->k = 1, c->max_iters = 1500;
+    c->mu = 1.05, c->lambda_max = 1e8, c->step0_frac = 0.01, c->step_decay = 0.999, c->adam_beta1 = 0.9;
+    c->adam_beta2 = 0.999, c->adam_eps = 1e-8, c->seed = 1, c->init_jitter_frac = 0.02, c->threads = 1;
+}
+
+int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
+{
+    API_BEGIN
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw Error(TDPG_ERR_CUDA, "cuda error: no CUDA device available (the tdpg engine has no CPU fallback)");
+    }
+    check_netlist(d);
+    auto s = std::make_unique<tdpg_session>();
+    CK(cudaGetDevice(&s->device));
+    CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    s->C = d->n_cells, s->P = d->n_pins, s->N = d->n_nets, s->S = d->n_sources, s->EP = d->n_endpoints;
+    s->E = d->net_start[d->n_nets];
+    s->clock = d->clock_period, s->r_unit = d->r_unit, s->c_unit = d->c_unit;
+    std::memcpy(s->core, d->core, sizeof s->core);
+    const int C = s->C, P = s->P, N = s->N, E = s->E;
+    s->h_cell_w.assign(d->cell_w, d->cell_w + C);
+    s->h_cell_h.assign(d->cell_h, d->cell_h + C);
+    s->h_cell_delay.assign(d->cell_delay, d->cell_delay + C);
+    s->h_cell_fixed.assign(d->cell_fixed, d->cell_fixed + C);
+    s->h_pin_cell.assign(d->pin_cell, d->pin_cell + P);
+    s->h_pin_term.assign(d->pin_term, d->pin_term + 2 * static_cast<size_t>(P));
+    s->h_pin_off.assign(d->pin_off, d->pin_off + 2 * static_cast<size_t>(P));
+    s->h_pin_dir.assign(d->pin_dir, d->pin_dir + P);
+    s->h_pin_cap.assign(d->pin_cap, d->pin_cap + P);
+    s->h_net_start.assign(d->net_start, d->net_start + N + 1);
+    s->h_net_pins.assign(d->net_pins, d->net_pins + E);
+    s->h_sources.assign(d->sources, d->sources + s->S);
+    s->h_endpoints.assign(d->endpoints, d->endpoints + s->EP);
+    if (d->pin_names) {
+        s->pin_names.resize(P);
+        for (int p = 0; p < P; ++p) s->pin_names[p] = d->pin_names[p] ? d->pin_names[p] : "";
+    }
+    build_graph(s.get());
+
+    // device netlist
+    std::vector<double2> wh(C);
+    for (int c = 0; c < C; ++c) wh[c] = make_double2(s->h_cell_w[c], s->h_cell_h[c]);
+    s->cell_wh.upload(wh, s->st);
+    s->cell_delay.upload(s->h_cell_delay, s->st);
+    s->cell_fixed.upload(s->h_cell_fixed, s->st);
+    s->pin_cell.upload(s->h_pin_cell, s->st);
+    s->pin_off.upload(reinterpret_cast<const double2*>(s->h_pin_off.data()), P, s->st);
+    s->anchor.upload(reinterpret_cast<const double2*>(s->h_pin_term.data()), P, s->st);
+    s->pin_dir.upload(s->h_pin_dir, s->st);
+    s->pin_cap.upload(s->h_pin_cap, s->st);
+    s->is_source.upload(s->h_is_source, s->st);
+    s->is_endpoint.upload(s->h_is_endpoint, s->st);
+    s->net_start.upload(s->h_net_start, s->st);
+    s->net_pins.upload(s->h_net_pins, s->st);
+    std::vector<int> e_cell(E), pin_entry(P, -1);
+    std::vector<double2> e_off(E);
+    s->h_pin_net.assign(P, -1);
+    for (int n = 0; n < N; ++n)
+        for (int e = s->h_net_start[n]; e < s->h_net_start[n + 1]; ++e) {
+            const int p = s->h_net_pins[e];
+            e_cell[e] = s->h_pin_cell[p] >= 0 ? s->h_pin_cell[p] : -1 - p;
+            e_off[e] = make_double2(s->h_pin_off[2 * p], s->h_pin_off[2 * p + 1]);
+            pin_entry[p] = e;
+            s->h_pin_net[p] = n;
+        }
+    s->e_cell.upload(e_cell, s->st);
+    s->e_off.upload(e_off, s->st);
+    // Cell pins on no net still take pin-pair gradient (pin_pairs.cpp:31-34 writes any pin):
+    // they get extra slots after the E net entries, written only by the pin-pair kernel.
+    int extra = 0;
+    for (int p = 0; p < P; ++p)
+        if (pin_entry[p] < 0 && s->h_pin_cell[p] >= 0) pin_entry[p] = E + extra++;
+    s->E_tot = E + extra;
+    s->h_pin_entry = pin_entry;
+    s->pin_entry.upload(pin_entry, s->st);
+    // fold CSR: per cell, the entries of its pins in ascending pin id
+    std::vector<int> ces(C + 1, 0), ce;
+    for (int p = 0; p < P; ++p)
+        if (s->h_pin_cell[p] >= 0 && pin_entry[p] >= 0) ces[s->h_pin_cell[p] + 1]++;
+    for (int c = 0; c < C; ++c) ces[c + 1] += ces[c];
+    ce.resize(ces[C]);
+    {
+        std::vector<int> f(ces.begin(), ces.end() - 1);
+        for (int p = 0; p < P; ++p)
+            if (s->h_pin_cell[p] >= 0 && pin_entry[p] >= 0) ce[f[s->h_pin_cell[p]]++] = pin_entry[p];
+    }
+    s->cell_ent_start.upload(ces, s->st);
+    s->cell_ent.upload(ce, s->st);
+
+    // state buffers
+    s->cell_xy.alloc(C);
+    s->d_cell.alloc(C);
+    s->grad_e.alloc(std::max(s->E_tot, 1));
+    s->grad_e.zero(s->st);
+    s->pin_xy.alloc(P);
+    s->arr.alloc(P), s->req.alloc(P), s->slack.alloc(P);
+    s->ak.alloc(P), s->rk.alloc(P), s->tie.alloc(P);
+    s->pred.alloc(P), s->tie_list.alloc(std::max(P, 1));
+    s->counters.alloc(16);
+    s->h_small.reserve(64);
+    CK(cudaStreamSynchronize(s->st));
+    *out = s.release();
+    API_END
+}
+
+int tdpg_session_destroy(tdpg_session* s)
+{
+    API_BEGIN
+    delete s;
+    API_END
+}
+
+int tdpg_graph_info(tdpg_session* s, int32_t counts[4], int32_t* level)
+{
+    API_BEGIN
+    counts[0] = s->A_net, counts[1] = s->A_cell, counts[2] = s->L, counts[3] = s->L - 1;
+    if (level) std::memcpy(level, s->h_level.data(), s->h_level.size() * sizeof(int32_t));
+    API_END
+}
+
+int tdpg_graph_arcs(tdpg_session* s, int32_t* from, int32_t* to, int32_t* kind, int32_t* owner)
+{
+    API_BEGIN
+    const size_t A = static_cast<size_t>(s->A);
+    if (from) std::memcpy(from, s->h_arc_from.data(), A * sizeof(int32_t));
+    if (to) std::memcpy(to, s->h_arc_to.data(), A * sizeof(int32_t));
+    if (kind) std::memcpy(kind, s->h_arc_kind.data(), A * sizeof(int32_t));
+    if (owner) std::memcpy(owner, s->h_arc_owner.data(), A * sizeof(int32_t));
+    API_END
+}
+
+int tdpg_set_positions(tdpg_session* s, const double* xy)
+{
+    API_BEGIN
+    upload_positions(s, xy);
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_get_positions(tdpg_session* s, double* xy)
+{
+    API_BEGIN
+    s->cell_xy.download(reinterpret_cast<double2*>(xy), s->C, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_set_grid(tdpg_session* s, int32_t nx, int32_t ny, double td)
+{
+    API_BEGIN
+    ensure_grid(s, nx, ny, td);
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_pp_set(tdpg_session* s, int64_t q, const int32_t* a, const int32_t* b, const double* w)
+{
+    API_BEGIN
+    std::vector<std::pair<unsigned long long, double>> v(static_cast<size_t>(q));
+    for (int64_t i = 0; i < q; ++i) {
+        if (a[i] < 0 || b[i] < 0 || a[i] >= s->P || b[i] >= s->P)
+            throw Error(TDPG_ERR_VALIDATION, "validation error: pin pair id out of range");
+        v[static_cast<size_t>(i)] = {(static_cast<unsigned long long>(static_cast<uint32_t>(a[i])) << 32) |
+                                         static_cast<uint32_t>(b[i]),
+                                     w[i]};
+    }
+    std::sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    std::vector<unsigned long long> k(v.size());
+    std::vector<double> ww(v.size());
+    for (size_t i = 0; i < v.size(); ++i) k[i] = v[i].first, ww[i] = v[i].second;
+    s->led_key.upload(k, s->st);
+    s->led_w.upload(ww, s->st);
+    s->Q = q;
+    s->pp_dirty = true;
+    if (s->E_tot > s->E) CK(cudaMemsetAsync(s->grad_e.p + s->E, 0, sizeof(double2) * (s->E_tot - s->E), s->st));
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_pp_size(tdpg_session* s, int64_t* q)
+{
+    API_BEGIN
+    *q = s->Q;
+    API_END
+}
+
+int tdpg_pp_get(tdpg_session* s, int32_t* a, int32_t* b, double* w)
+{
+    API_BEGIN
+    std::vector<unsigned long long> k(static_cast<size_t>(s->Q));
+    s->led_key.download(k.data(), k.size(), s->st);
+    if (w) s->led_w.download(w, static_cast<size_t>(s->Q), s->st);
+    CK(cudaStreamSynchronize(s->st));
+    for (size_t i = 0; i < k.size(); ++i) {
+        if (a) a[i] = static_cast<int32_t>(k[i] >> 32);
+        if (b) b[i] = static_cast<int32_t>(k[i] & 0xFFFFFFFFull);
+    }
+    API_END
+}
+
+} // extern "C"

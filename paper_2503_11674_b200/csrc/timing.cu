@@ -1,0 +1,677 @@
+// timing.cu — levelized STA (sta.cpp:33-143), rank-0 critical-path extraction with the
+// enumerator's lexicographic tie rule (paths.cpp:12-189), collect_pin_pairs
+// (paths.cpp:191-203) and the pin-pair weight ledger (pin_pairs.cpp:7-15), on the device.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+
+#include "gp_kernels.cuh"
+
+namespace tdpg {
+
+int api_fail(int kind, const std::string& msg);
+
+constexpr unsigned long long kNoKey = ~0ull;
+
+// net_delay (sta.cpp:10-14): (r * L) * (c * L + cap), L = Manhattan(driver, sink).
+__device__ __forceinline__ double net_delay(double2 a, double2 b, double cap, double r, double c)
+{
+    const double len = fabs(a.x - b.x) + fabs(a.y - b.y);
+    return (r * len) * (c * len + cap);
+}
+
+__global__ void k_pin_xy(int P, const int* __restrict__ pin_cell, const double2* __restrict__ off,
+                         const double2* __restrict__ cell_xy, const double2* __restrict__ anchor,
+                         double2* __restrict__ pin_xy)
+{
+    const int p = blockIdx.x * kBlock + threadIdx.x;
+    if (p < P) pin_xy[p] = pin_pos(p, pin_cell, off, cell_xy, anchor);
+}
+
+struct StaArgs {
+    const int *lvl_pins, *in_start, *in_from, *out_start, *out_to, *pin_cell;
+    const uint8_t *is_source, *is_endpoint, *pin_dir;
+    const double *cell_delay, *pin_cap;
+    const double2* pin_xy;
+    double r, c, clock;
+    double *arr, *req;
+    uint8_t *ak, *rk, *tie;
+    int *pred, *tie_list, *counters;
+};
+
+// propagate_arrival for one level (sta.cpp:41-62): max over known fan-in, strict '>' in
+// ascending arc id; records the winning fan-in pin and whether another arc tied it exactly.
+__global__ void __launch_bounds__(kBlock) k_arrival(int lo, int hi, StaArgs a)
+{
+    const int i = lo + blockIdx.x * kBlock + threadIdx.x;
+    if (i >= hi) return;
+    const int v = a.lvl_pins[i];
+    if (a.is_source[v]) {
+        a.arr[v] = 0.0, a.ak[v] = 1, a.pred[v] = -1, a.tie[v] = 0;
+        return;
+    }
+    const bool sink = a.pin_dir[v] == 0;
+    const int j0 = a.in_start[v], j1 = a.in_start[v + 1];
+    double best = -INFINITY;
+    bool found = false;
+    int bu = -1, ntie = 0;
+    if (j1 > j0) {
+        const double2 pv = a.pin_xy[v];
+        const double cap = a.pin_cap[v];
+        const double dcell = sink ? 0.0 : a.cell_delay[a.pin_cell[v]];
+        for (int j = j0; j < j1; ++j) {
+            const int u = a.in_from[j];
+            if (!a.ak[u]) continue;
+            const double d = sink ? net_delay(a.pin_xy[u], pv, cap, a.r, a.c) : dcell;
+            const double cand = a.arr[u] + d;
+            if (!found || cand > best) {
+                best = cand, found = true, bu = u, ntie = 1;
+            } else if (cand == best) {
+                ++ntie;
+            }
+        }
+    }
+    a.arr[v] = found ? best : 0.0;
+    a.ak[v] = found ? 1 : 0;
+    a.pred[v] = found ? bu : -1;
+    a.tie[v] = ntie > 1;
+    if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = v;
+}
+
+// propagate_required for one level (sta.cpp:77-97): min over known fan-out, strict '<'.
+__global__ void __launch_bounds__(kBlock) k_required(int lo, int hi, StaArgs a)
+{
+    const int i = lo + blockIdx.x * kBlock + threadIdx.x;
+    if (i >= hi) return;
+    const int u = a.lvl_pins[i];
+    double best = INFINITY;
+    bool found = false;
+    if (a.is_endpoint[u]) best = a.clock, found = true;
+    const int j0 = a.out_start[u], j1 = a.out_start[u + 1];
+    if (j1 > j0) {
+        const bool driver = a.pin_dir[u] == 1;
+        const double2 pu = a.pin_xy[u];
+        const double dcell = driver ? 0.0 : a.cell_delay[a.pin_cell[u]];
+        for (int j = j0; j < j1; ++j) {
+            const int t = a.out_to[j];
+            if (!a.rk[t]) continue;
+            const double d = driver ? net_delay(pu, a.pin_xy[t], a.pin_cap[t], a.r, a.c) : dcell;
+            const double cand = a.req[t] - d;
+            if (!found || cand < best) best = cand, found = true;
+        }
+    }
+    a.req[u] = found ? best : a.clock;
+    a.rk[u] = found ? 1 : 0;
+}
+
+// compute_slacks + endpoint keys (sta.cpp:104-133, paths.cpp:77-87): orderable slack keys
+// over the pin-sorted endpoint list so a stable radix sort yields (slack, pin) order.
+__global__ void __launch_bounds__(kBlock) k_slack_keys(int P, int EP, const double* __restrict__ arr,
+                                                       const double* __restrict__ req, double* __restrict__ slack,
+                                                       const int* __restrict__ ep_sorted,
+                                                       unsigned long long* __restrict__ keys, int* __restrict__ vals,
+                                                       double* __restrict__ part)
+{
+    __shared__ double sh[kBlock / 32];
+    __shared__ double shm[kBlock / 32];
+    __shared__ int shc[kBlock / 32];
+    const int n = max(P, EP);
+    double tns = 0.0, wns = 0.0;
+    int nv = 0;
+    for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
+        if (i < P) slack[i] = req[i] - arr[i];
+        if (i < EP) {
+            const int e = ep_sorted[i];
+            const double s = req[e] - arr[e];
+            const bool viol = s < 0.0;
+            keys[i] = viol ? double_key(s) : kNoKey;
+            vals[i] = e;
+            if (viol) tns += s, wns = fmin(wns, s), ++nv;
+        }
+    }
+    const double bt = block_sum<kBlock>(tns, sh);
+    // block min / count
+    double m = wns;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int c = nv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) shm[w] = m, shc[w] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = 0.0;
+        int cc = 0;
+        for (int k = 0; k < kBlock / 32; ++k) mm = fmin(mm, shm[k]), cc += shc[k];
+        part[3 * blockIdx.x] = bt, part[3 * blockIdx.x + 1] = mm, part[3 * blockIdx.x + 2] = cc;
+    }
+}
+
+__global__ void k_sta_final(int nb, const double* part, double* out3)
+{
+    __shared__ double sh[kBlock / 32];
+    double t = 0.0, m = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < nb; i += kBlock) t += part[3 * i], m = fmin(m, part[3 * i + 1]), c += part[3 * i + 2];
+    t = block_sum<kBlock>(t, sh);
+    c = block_sum<kBlock>(c, sh);
+    __shared__ double mins[kBlock];
+    mins[threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = 0.0;
+        for (int k = 0; k < kBlock; ++k) mm = fmin(mm, mins[k]);
+        out3[0] = t, out3[1] = mm, out3[2] = c;
+    }
+}
+
+// Exact delay ties: the enumerator prefers the lexicographically smallest full pin
+// sequence (paths.hpp:63-69).  Tie pins are resolved in level order so every
+// predecessor path is final when compared.  One block; tie pins are rare.
+__device__ int materialize(const int* pred, int v, int* buf)
+{
+    int n = 0;
+    for (int u = v; u >= 0; u = pred[u]) ++n;
+    int k = n;
+    for (int u = v; u >= 0; u = pred[u]) buf[--k] = u;
+    return n;
+}
+
+__global__ void k_resolve_ties(StaArgs a, const int* __restrict__ level, int L, int* scratch, int stride)
+{
+    const int ntie = a.counters[0];
+    if (ntie == 0) return;
+    int* b1 = scratch + static_cast<long long>(threadIdx.x) * 2 * stride;
+    int* b2 = b1 + stride;
+    for (int l = 1; l < L; ++l) {
+        for (int t = threadIdx.x; t < ntie; t += blockDim.x) {
+            const int v = a.tie_list[t];
+            if (level[v] != l) continue;
+            const bool sink = a.pin_dir[v] == 0;
+            const double2 pv = a.pin_xy[v];
+            int bu = -1, nb = 0;
+            for (int j = a.in_start[v]; j < a.in_start[v + 1]; ++j) {
+                const int u = a.in_from[j];
+                if (!a.ak[u]) continue;
+                const double d = sink ? net_delay(a.pin_xy[u], pv, a.pin_cap[v], a.r, a.c)
+                                      : a.cell_delay[a.pin_cell[v]];
+                if (a.arr[u] + d != a.arr[v]) continue;
+                const int n1 = materialize(a.pred, u, b1);
+                b1[n1] = v;
+                if (bu < 0) {
+                    for (int k = 0; k <= n1; ++k) b2[k] = b1[k];
+                    nb = n1 + 1, bu = u;
+                    continue;
+                }
+                // lexicographic compare of b1[0..n1] vs b2[0..nb)
+                const int m = min(n1 + 1, nb);
+                int k = 0;
+                while (k < m && b1[k] == b2[k]) ++k;
+                const bool less = (k < m) ? (b1[k] < b2[k]) : (n1 + 1 < nb);
+                if (less) {
+                    for (int q = 0; q <= n1; ++q) b2[q] = b1[q];
+                    nb = n1 + 1, bu = u;
+                }
+            }
+            if (bu >= 0) a.pred[v] = bu;
+        }
+        __syncthreads();
+    }
+}
+
+// Backtrace of the rank-0 path of each selected endpoint: pass 1 counts pins and
+// net hops (hops leaving an Output pin, paths.cpp:195-200), pass 2 writes them.
+__global__ void k_bt_count(int n, const int* __restrict__ ep, const int* __restrict__ pred,
+                           const uint8_t* __restrict__ pin_dir, int* __restrict__ len, int* __restrict__ hops)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    int v = ep[i], l = 1, h = 0;
+    for (int u = pred[v]; u >= 0; v = u, u = pred[v]) {
+        ++l;
+        h += pin_dir[u] == 1;
+    }
+    len[i] = l, hops[i] = h;
+}
+
+__global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restrict__ pred,
+                           const uint8_t* __restrict__ pin_dir, const int* __restrict__ len,
+                           const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
+                           const double* __restrict__ arr, double clock, int* __restrict__ pins,
+                           double* __restrict__ pslack, unsigned long long* __restrict__ hkey,
+                           double* __restrict__ hslack, int* __restrict__ hidx)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    int v = ep[i];
+    const double sl = clock - arr[v]; // path slack = clock - rank-0 delay (paths.cpp:123)
+    pslack[i] = sl;
+    int k = off[i] + len[i] - 1;
+    int h = hoff[i] + hops[i] - 1;
+    pins[k] = v;
+    for (int u = pred[v]; u >= 0; v = u, u = pred[v]) {
+        pins[--k] = u;
+        if (pin_dir[u] == 1) {
+            const unsigned lo = static_cast<unsigned>(min(u, v)), hi = static_cast<unsigned>(max(u, v));
+            hkey[h] = (static_cast<unsigned long long>(lo) << 32) | hi;
+            hslack[h] = sl;
+            hidx[h] = h;
+            --h;
+        }
+    }
+}
+
+__global__ void k_count_heads(long long n, const unsigned long long* __restrict__ k, int* __restrict__ out)
+{
+    int c = 0;
+    for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * kBlock)
+        c += (k[i] != kNoKey) && (i == 0 || k[i - 1] != k[i]);
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// update_pair_weights (pin_pairs.cpp:7-15) over hits sorted stably by pair: one thread per
+// group of equal pairs applies the group's additions in hit order; new pairs enter at w0.
+__global__ void k_ledger_groups(long long H, const unsigned long long* __restrict__ hk, const int* __restrict__ hidx,
+                                const double* __restrict__ hslack, const unsigned long long* __restrict__ led_key,
+                                double* __restrict__ led_w, long long Q, double wns, double w0, double w1,
+                                uint8_t* __restrict__ new_flag, double* __restrict__ new_w)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= H) return;
+    const unsigned long long key = hk[i];
+    new_flag[i] = 0;
+    if (key == kNoKey || (i > 0 && hk[i - 1] == key)) return;
+    long long lo = 0, hi = Q;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (led_key[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    const bool found = lo < Q && led_key[lo] == key;
+    double w = found ? led_w[lo] : w0;
+    long long j = found ? i : i + 1;
+    for (; j < H && hk[j] == key; ++j) w += w1 * (hslack[hidx[j]] / wns);
+    if (found) led_w[lo] = w;
+    else new_flag[i] = 1, new_w[i] = w;
+}
+
+__global__ void k_iota(long long n, int* out)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i < n) out[i] = static_cast<int>(i);
+}
+
+__global__ void k_host_hit_keys(long long n, const int* a, const int* b, const double* s, unsigned long long* key,
+                                int* idx)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= n) return;
+    key[i] = s[i] < 0.0 ? (static_cast<unsigned long long>(static_cast<unsigned>(a[i])) << 32) | static_cast<unsigned>(b[i])
+                        : kNoKey;
+    idx[i] = static_cast<int>(i);
+}
+
+// apply_net_weights (placer.cpp:262-273)
+__global__ void k_net_weights(int N, const int* __restrict__ net_start, const int* __restrict__ net_pins,
+                              const double* __restrict__ slack, double wns, double* __restrict__ w)
+{
+    const int e = blockIdx.x * kBlock + threadIdx.x;
+    if (e >= N) return;
+    double r = 1.0;
+    if (wns < 0.0) {
+        double worst = slack[net_pins[net_start[e]]];
+        for (int j = net_start[e] + 1; j < net_start[e + 1]; ++j) worst = smin(worst, slack[net_pins[j]]);
+        if (worst < 0.0) r = 1.0 + (-worst) / (-wns);
+    }
+    w[e] = r;
+}
+
+// ---------------------------------------------------------------------------------------
+StaArgs sta_args(tdpg_session* s)
+{
+    StaArgs a;
+    a.lvl_pins = s->lvl_pins, a.in_start = s->in_start, a.in_from = s->in_from, a.out_start = s->out_start;
+    a.out_to = s->out_to, a.pin_cell = s->pin_cell, a.is_source = s->is_source, a.is_endpoint = s->is_endpoint;
+    a.pin_dir = s->pin_dir, a.cell_delay = s->cell_delay, a.pin_cap = s->pin_cap, a.pin_xy = s->pin_xy;
+    a.r = s->r_unit, a.c = s->c_unit, a.clock = s->clock, a.arr = s->arr, a.req = s->req, a.ak = s->ak, a.rk = s->rk;
+    a.tie = s->tie, a.pred = s->pred, a.tie_list = s->tie_list, a.counters = s->counters;
+    return a;
+}
+
+// Full STA at the current positions; leaves endpoint keys in sort_k0/sort_v0 and
+// [tns, wns, n_violated] in counters-adjacent scratch. Stream-ordered, no host sync.
+void run_sta_async(tdpg_session* s, double* out3)
+{
+    const int P = s->P;
+    k_pin_xy<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor,
+                                                          s->pin_xy);
+    CK_LAUNCH();
+    CK(cudaMemsetAsync(s->counters.p, 0, sizeof(int) * 4, s->st));
+    const StaArgs a = sta_args(s);
+    for (int l = 0; l < s->L; ++l) {
+        const int lo = s->h_lvl_start[l], hi = s->h_lvl_start[l + 1];
+        if (hi > lo) k_arrival<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, a);
+    }
+    CK_LAUNCH();
+    for (int l = s->L - 1; l >= 0; --l) {
+        const int lo = s->h_lvl_start[l], hi = s->h_lvl_start[l + 1];
+        if (hi > lo) k_required<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, a);
+    }
+    CK_LAUNCH();
+    const size_t ep = static_cast<size_t>(std::max(s->EP, 1));
+    s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
+    const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
+    s->part.reserve(3 * nb + 8);
+    k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0, s->sort_v0,
+                                           s->part);
+    CK_LAUNCH();
+    k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
+    CK_LAUNCH();
+}
+
+void run_sta_dev(tdpg_session* s)
+{
+    s->part.reserve(16);
+    DBuf<double> out3(3);
+    run_sta_async(s, out3);
+    double h[3];
+    out3.download(h, 3, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    s->tns = h[0], s->wns = h[1];
+    s->sta_valid = true;
+}
+
+// report_timing_endpoint(n, k = 1) on the current STA (paths.cpp:167-189).
+void extract_endpoint_dev(tdpg_session* s, int n)
+{
+    if (!s->sta_valid) run_sta_dev(s);
+    // recompute keys (run_sta_async left them; recompute cheaply to be self-contained)
+    DBuf<double> out3(3);
+    {
+        const int P = s->P;
+        const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
+        s->part.reserve(3 * nb + 8);
+        const size_t ep = static_cast<size_t>(std::max(s->EP, 1));
+        s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
+        k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0,
+                                               s->sort_v0, s->part);
+        CK_LAUNCH();
+        k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
+        CK_LAUNCH();
+    }
+    const int EP = s->EP;
+    if (EP > 0) {
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP, 0,
+                                        64, s->st);
+        void* tmp = cub_scratch(s, bytes);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP, 0, 64,
+                                           s->st));
+    }
+    // ties: resolve before any backtrace
+    {
+        const int stride = s->L + 2;
+        DBuf<int> scratch(static_cast<size_t>(kBlock) * 2 * stride);
+        DBuf<int> level(s->P);
+        level.upload(s->h_level, s->st);
+        k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), level, s->L, scratch, stride);
+        CK_LAUNCH();
+        double h[3];
+        out3.download(h, 3, s->st);
+        CK(cudaStreamSynchronize(s->st));
+        const int nv = static_cast<int>(h[2]);
+        s->n_paths = (n <= 0) ? nv : std::min(n, nv);
+    }
+    const int np = s->n_paths;
+    s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0;
+    if (np == 0) return;
+    s->ex_len.reserve(np), s->ex_hops.reserve(np), s->ex_off.reserve(np), s->ex_hoff.reserve(np);
+    s->ex_slack.reserve(np);
+    k_bt_count<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
+                                                             s->ex_hops);
+    CK_LAUNCH();
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->ex_len.p, s->ex_off.p, np, s->st);
+    void* tmp = cub_scratch(s, bytes);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_len.p, s->ex_off.p, np, s->st));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_hops.p, s->ex_hoff.p, np, s->st));
+    int tail[4];
+    CK(cudaMemcpyAsync(&tail[0], s->ex_off.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[1], s->ex_len.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[2], s->ex_hoff.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[3], s->ex_hops.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    s->n_path_pins = static_cast<long long>(tail[0]) + tail[1];
+    s->n_hits = static_cast<long long>(tail[2]) + tail[3];
+    const long long H = s->n_hits;
+    s->ex_pins.reserve(s->n_path_pins + 1);
+    s->hit_key.reserve(H + 1), s->hit_slack.reserve(H + 1), s->hit_idx.reserve(H + 1);
+    s->hit_key_s.reserve(H + 1), s->hit_idx_s.reserve(H + 1);
+    k_bt_write<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
+                                                             s->ex_off, s->ex_hops, s->ex_hoff, s->arr, s->clock,
+                                                             s->ex_pins, s->ex_slack, s->hit_key, s->hit_slack,
+                                                             s->hit_idx);
+    CK_LAUNCH();
+    if (H > 0) {
+        bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
+                                        static_cast<int>(H), 0, 64, s->st);
+        tmp = cub_scratch(s, bytes);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
+                                           static_cast<int>(H), 0, 64, s->st));
+        CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
+        k_count_heads<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 4), kBlock, 0, s->st>>>(H, s->hit_key_s,
+                                                                                                 s->counters.p + 1);
+        CK_LAUNCH();
+        int u = 0;
+        CK(cudaMemcpyAsync(&u, s->counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        s->uniq_pairs = u;
+    }
+    s->hits_sorted = true;
+}
+
+// Apply the last sorted hits (hit_key_s / hit_idx_s / hit_slack) to the ledger.
+void ledger_apply_sorted(tdpg_session* s, long long H, double wns, double w0, double w1)
+{
+    if (!(wns < 0.0) || H == 0) return;
+    DBuf<uint8_t> flag(H);
+    DBuf<double> nw(H);
+    const long long Q = s->Q;
+    k_ledger_groups<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(H, s->hit_key_s, s->hit_idx_s, s->hit_slack,
+                                                                 s->led_key, s->led_w, Q, wns, w0, w1, flag, nw);
+    CK_LAUNCH();
+    DBuf<unsigned long long> new_k(H);
+    DBuf<double> new_w(H);
+    DBuf<int> n_sel(1);
+    size_t bytes = 0;
+    cub::DeviceSelect::Flagged(nullptr, bytes, s->hit_key_s.p, flag.p, new_k.p, n_sel.p, static_cast<int>(H), s->st);
+    void* tmp = cub_scratch(s, bytes);
+    CK(cub::DeviceSelect::Flagged(tmp, bytes, s->hit_key_s.p, flag.p, new_k.p, n_sel.p, static_cast<int>(H), s->st));
+    CK(cub::DeviceSelect::Flagged(tmp, bytes, nw.p, flag.p, new_w.p, n_sel.p, static_cast<int>(H), s->st));
+    int M = 0;
+    CK(cudaMemcpyAsync(&M, n_sel.p, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (M == 0) return;
+    const long long nq = Q + M;
+    s->led_key2.reserve(nq), s->led_w2.reserve(nq);
+    if (Q == 0) {
+        CK(cudaMemcpyAsync(s->led_key2.p, new_k.p, M * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s->st));
+        CK(cudaMemcpyAsync(s->led_w2.p, new_w.p, M * sizeof(double), cudaMemcpyDeviceToDevice, s->st));
+    } else {
+        bytes = 0;
+        cub::DeviceMerge::MergePairs(nullptr, bytes, s->led_key.p, s->led_w.p, static_cast<int>(Q), new_k.p, new_w.p,
+                                     M, s->led_key2.p, s->led_w2.p, ::cuda::std::less<>{}, s->st);
+        tmp = cub_scratch(s, bytes);
+        CK(cub::DeviceMerge::MergePairs(tmp, bytes, s->led_key.p, s->led_w.p, static_cast<int>(Q), new_k.p, new_w.p, M,
+                                        s->led_key2.p, s->led_w2.p, ::cuda::std::less<>{}, s->st));
+    }
+    // copy back (not swap): the iteration graph holds the ledger pointers
+    s->led_key.reserve(nq), s->led_w.reserve(nq);
+    CK(cudaMemcpyAsync(s->led_key.p, s->led_key2.p, nq * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s->st));
+    CK(cudaMemcpyAsync(s->led_w.p, s->led_w2.p, nq * sizeof(double), cudaMemcpyDeviceToDevice, s->st));
+    s->Q = nq;
+    s->pp_dirty = true;
+}
+
+void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool)
+{
+    ledger_apply_sorted(s, s->n_hits, wns, w0, w1);
+}
+
+void net_weights_dev(tdpg_session* s)
+{
+    s->net_w.reserve(std::max(s->N, 1));
+    k_net_weights<<<blocks_for(s->N, kBlock), kBlock, 0, s->st>>>(s->N, s->net_start, s->net_pins.p,
+                                                                  s->slack, s->wns, s->net_w);
+    CK_LAUNCH();
+}
+
+} // namespace tdpg
+
+using namespace tdpg;
+
+#define API_BEGIN try {
+#define API_END                                                                   \
+    return TDPG_OK;                                                               \
+    }                                                                             \
+    catch (const ::tdpg::Error& e) { return ::tdpg::api_fail(e.kind, e.what()); } \
+    catch (const std::exception& e) { return ::tdpg::api_fail(TDPG_ERR_INTERNAL, e.what()); }
+
+extern "C" {
+
+int tdpg_pin_positions(tdpg_session* s, double* pin_xy)
+{
+    API_BEGIN
+    k_pin_xy<<<blocks_for(s->P, kBlock), kBlock, 0, s->st>>>(s->P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor,
+                                                             s->pin_xy);
+    CK_LAUNCH();
+    s->pin_xy.download(reinterpret_cast<double2*>(pin_xy), s->P, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_sta(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* ak, uint8_t* rk, double* tns,
+             double* wns)
+{
+    API_BEGIN
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s->st));
+    run_sta_dev(s);
+    CK(cudaEventRecord(e1, s->st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    s->last_sta_ms = ms;
+    cudaEventDestroy(e0), cudaEventDestroy(e1);
+    const size_t P = static_cast<size_t>(s->P);
+    if (arr) s->arr.download(arr, P, s->st);
+    if (req) s->req.download(req, P, s->st);
+    if (slack) s->slack.download(slack, P, s->st);
+    if (ak) s->ak.download(ak, P, s->st);
+    if (rk) s->rk.download(rk, P, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    if (tns) *tns = s->tns;
+    if (wns) *wns = s->wns;
+    API_END
+}
+
+int tdpg_extract_endpoint(tdpg_session* s, int32_t n, int32_t k, int64_t counts[4])
+{
+    API_BEGIN
+    if (k != 1) throw Error(TDPG_ERR_INTERNAL, "k > 1 per endpoint is not implemented on the device yet");
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s->st));
+    extract_endpoint_dev(s, n);
+    CK(cudaEventRecord(e1, s->st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    s->last_extract_ms = ms;
+    cudaEventDestroy(e0), cudaEventDestroy(e1);
+    counts[0] = s->n_paths;
+    counts[1] = s->n_path_pins;
+    counts[2] = s->n_paths; // k = 1: every selected endpoint is covered once
+    counts[3] = s->uniq_pairs;
+    API_END
+}
+
+int tdpg_paths_get(tdpg_session* s, int32_t* start, int32_t* pins, double* slack)
+{
+    API_BEGIN
+    const int np = s->n_paths;
+    if (np > 0) {
+        if (start) {
+            s->ex_off.download(start, np, s->st);
+            CK(cudaStreamSynchronize(s->st));
+            start[np] = static_cast<int32_t>(s->n_path_pins);
+        }
+        if (pins) s->ex_pins.download(pins, s->n_path_pins, s->st);
+        if (slack) s->ex_slack.download(slack, np, s->st);
+    } else if (start) {
+        start[0] = 0;
+    }
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_paths_hits(tdpg_session* s, int64_t* n_hits, int32_t* a, int32_t* b, double* slack)
+{
+    API_BEGIN
+    *n_hits = s->n_hits;
+    if (s->n_hits > 0 && (a || b || slack)) {
+        std::vector<unsigned long long> k(s->n_hits);
+        s->hit_key.download(k.data(), k.size(), s->st);
+        if (slack) s->hit_slack.download(slack, s->n_hits, s->st);
+        CK(cudaStreamSynchronize(s->st));
+        for (size_t i = 0; i < k.size(); ++i) {
+            if (a) a[i] = static_cast<int32_t>(k[i] >> 32);
+            if (b) b[i] = static_cast<int32_t>(k[i] & 0xFFFFFFFFull);
+        }
+    }
+    API_END
+}
+
+int tdpg_pp_update(tdpg_session* s, int64_t n, const int32_t* a, const int32_t* b, const double* sl, double wns,
+                   double w0, double w1)
+{
+    API_BEGIN
+    if (!(wns < 0.0) || n == 0) return TDPG_OK; // pin_pairs.cpp:9
+    DBuf<int> da(n), db(n);
+    DBuf<double> ds(n);
+    da.upload(a, n, s->st), db.upload(b, n, s->st), ds.upload(sl, n, s->st);
+    s->hit_key.reserve(n + 1), s->hit_idx.reserve(n + 1), s->hit_key_s.reserve(n + 1), s->hit_idx_s.reserve(n + 1);
+    s->hit_slack.reserve(n + 1);
+    k_host_hit_keys<<<blocks_for(n, kBlock), kBlock, 0, s->st>>>(n, da, db, ds, s->hit_key, s->hit_idx);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(s->hit_slack.p, ds.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s->st));
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
+                                    static_cast<int>(n), 0, 64, s->st);
+    void* tmp = cub_scratch(s, bytes);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
+                                       static_cast<int>(n), 0, 64, s->st));
+    ledger_apply_sorted(s, n, wns, w0, w1);
+    s->n_hits = 0; // host-provided hits are not an extraction result
+    s->n_paths = 0;
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_last_timing_ms(tdpg_session* s, double* sta_ms, double* extract_ms)
+{
+    API_BEGIN
+    if (sta_ms) *sta_ms = s->last_sta_ms;
+    if (extract_ms) *extract_ms = s->last_extract_ms;
+    API_END
+}
+
+} // extern "C"

@@ -1,0 +1,395 @@
+"""ctypes binding of the sm_100a engine (``libtdpgpu.so``, C-ABI in ``include/tdpg.h``).
+
+``Session`` mirrors the reference's operator API on one device-resident design:
+``sta`` = run_sta, ``extract`` = report_timing_endpoint + collect_pin_pairs,
+``objective`` = objective_and_gradient, ``density`` = DensityGrid::evaluate,
+``pp_update`` = update_pair_weights, ``place`` = run_placement
+(/root/reference/proj/include/tdp/*.hpp).  There is no CPU fallback: without
+the built library or a CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .design import Design, TdpgConfig, TdpgNetlist, TdpgTraceRow, make_config
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtdpgpu.so")
+
+_P = C.c_void_p
+_I32P = C.POINTER(C.c_int32)
+_I64P = C.POINTER(C.c_int64)
+_F64P = C.POINTER(C.c_double)
+
+ERR_NAMES = {1: "ParseError", 2: "ValidationError", 3: "CycleError", 4: "EndpointError", 5: "GraphError",
+             6: "NonFiniteError", 7: "CudaError", 9: "InternalError"}
+
+
+class TdpgError(RuntimeError):
+    def __init__(self, kind, msg):
+        super().__init__(msg)
+        self.kind = kind
+        self.kind_name = ERR_NAMES.get(kind, "Error")
+
+
+class ValidationError(TdpgError, ValueError):
+    pass
+
+
+class NonFiniteError(TdpgError):
+    pass
+
+
+def _raise(kind, msg):
+    if kind in (1, 2, 3, 4):
+        raise ValidationError(kind, msg)
+    if kind == 6:
+        raise NonFiniteError(kind, msg)
+    raise TdpgError(kind, msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+_lib = None
+
+# exported symbol -> (restype, argtypes)
+_SIGS = {
+    "tdpg_last_error": (C.c_char_p, []),
+    "tdpg_last_error_kind": (C.c_int, []),
+    "tdpg_version": (C.c_char_p, []),
+    "tdpg_device_count": (C.c_int, []),
+    "tdpg_config_default": (None, [_P]),
+    "tdpg_session_create": (C.c_int, [_P, C.POINTER(_P)]),
+    "tdpg_session_destroy": (C.c_int, [_P]),
+    "tdpg_graph_info": (C.c_int, [_P, _I32P, _P]),
+    "tdpg_graph_arcs": (C.c_int, [_P, _P, _P, _P, _P]),
+    "tdpg_set_positions": (C.c_int, [_P, _P]),
+    "tdpg_get_positions": (C.c_int, [_P, _P]),
+    "tdpg_pin_positions": (C.c_int, [_P, _P]),
+    "tdpg_wirelength": (C.c_int, [_P, C.c_double, _P, _F64P, _F64P, _P]),
+    "tdpg_set_grid": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double]),
+    "tdpg_density": (C.c_int, [_P, _F64P, _F64P, _P]),
+    "tdpg_pp_set": (C.c_int, [_P, C.c_int64, _P, _P, _P]),
+    "tdpg_pp_size": (C.c_int, [_P, _I64P]),
+    "tdpg_pp_get": (C.c_int, [_P, _P, _P, _P]),
+    "tdpg_pp_update": (C.c_int, [_P, C.c_int64, _P, _P, _P, C.c_double, C.c_double, C.c_double]),
+    "tdpg_pp_loss": (C.c_int, [_P, C.c_int32, _F64P, _P]),
+    "tdpg_objective": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.c_int32, _P, _P, _P]),
+    "tdpg_adam_step": (C.c_int, [C.c_int64, _P, _P, _P, _P, _I32P, C.c_double, C.c_double, C.c_double,
+                                 C.c_double]),
+    "tdpg_sta": (C.c_int, [_P, _P, _P, _P, _P, _P, _F64P, _F64P]),
+    "tdpg_extract_endpoint": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P]),
+    "tdpg_paths_get": (C.c_int, [_P, _P, _P, _P]),
+    "tdpg_paths_hits": (C.c_int, [_P, _I64P, _P, _P, _P]),
+    "tdpg_last_timing_ms": (C.c_int, [_P, _F64P, _F64P]),
+    "tdpg_place": (C.c_int, [_P, _P, _P, _P, _I32P, _I32P, _F64P]),
+    "tdpg_engine_init": (C.c_int, [_P, _P, _P]),
+    "tdpg_iterate_dev": (C.c_int, [_P, C.c_int32, _F64P]),
+    "tdpg_engine_stats": (C.c_int, [_P, _I32P, _I32P, _I64P]),
+    "tdpg_step_host": (C.c_int, [_P, _P, _P, _P]),
+    "tdpg_profile_iteration": (C.c_int, [_P, C.c_int32, _F64P, C.c_int32, C.c_char_p, C.c_int32]),
+    "tdpg_generate": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                C.c_double, C.c_int32, C.POINTER(_P)]),
+    "tdpg_design_view": (C.c_int, [_P, _P, C.POINTER(_P)]),
+    "tdpg_design_set_clock": (C.c_int, [_P, C.c_double]),
+    "tdpg_design_destroy": (C.c_int, [_P]),
+}
+
+
+def lib():
+    """Load the engine library; fails loudly when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `make -C paper_2503_11674_b200/csrc` "
+                              "(the engine has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc:
+        L = lib()
+        _raise(rc, L.tdpg_last_error().decode())
+
+
+def device_count():
+    return lib().tdpg_device_count()
+
+
+class Session:
+    """One design resident on the GPU (the reference operator API, drop-in)."""
+
+    def __init__(self, design: Design):
+        self.lib = lib()
+        self.d = design
+        self._view = design.view()
+        h = _P()
+        _check(self.lib.tdpg_session_create(C.byref(self._view), C.byref(h)))
+        self.h = h.value
+        self.set_positions(design.positions)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tdpg_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # positions -----------------------------------------------------------
+    def set_positions(self, xy):
+        xy = np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
+        _check(self.lib.tdpg_set_positions(self.h, xy.ctypes.data))
+
+    def positions(self):
+        out = np.zeros((self.d.n_cells, 2))
+        _check(self.lib.tdpg_get_positions(self.h, out.ctypes.data))
+        return out
+
+    def _pos(self, xy):
+        if xy is not None:
+            self.set_positions(xy)
+
+    def pin_positions(self, xy=None):
+        self._pos(xy)
+        out = np.zeros((self.d.n_pins, 2))
+        _check(self.lib.tdpg_pin_positions(self.h, out.ctypes.data))
+        return out
+
+    # graph ---------------------------------------------------------------
+    def graph(self):
+        cnt = (C.c_int32 * 4)()
+        level = np.zeros(self.d.n_pins, np.int32)
+        _check(self.lib.tdpg_graph_info(self.h, cnt, level.ctypes.data))
+        A = cnt[0] + cnt[1]
+        arcs = [np.zeros(A, np.int32) for _ in range(4)]
+        _check(self.lib.tdpg_graph_arcs(self.h, *[_p(a) for a in arcs]))
+        return dict(n_net_arcs=cnt[0], n_cell_arcs=cnt[1], n_levels=cnt[2], level=level, arc_from=arcs[0],
+                    arc_to=arcs[1], arc_kind=arcs[2], arc_owner=arcs[3])
+
+    # objective terms -----------------------------------------------------
+    def wirelength(self, gamma, xy=None, net_w=None, grad=True):
+        self._pos(xy)
+        wl, hp = C.c_double(), C.c_double()
+        g = np.zeros((self.d.n_pins, 2)) if grad else None
+        nw = None if net_w is None else np.ascontiguousarray(net_w, np.float64)
+        _check(self.lib.tdpg_wirelength(self.h, gamma, _p(nw), C.byref(wl), C.byref(hp), _p(g)))
+        return wl.value, hp.value, g
+
+    def hpwl(self, xy=None):
+        return self.wirelength(1.0, xy, grad=False)[1]
+
+    def density(self, xy=None, nx=16, ny=16, td=0.6):
+        self._pos(xy)
+        _check(self.lib.tdpg_set_grid(self.h, nx, ny, td))
+        v, o = C.c_double(), C.c_double()
+        d = np.zeros((self.d.n_cells, 2))
+        _check(self.lib.tdpg_density(self.h, C.byref(v), C.byref(o), d.ctypes.data))
+        return v.value, o.value, d
+
+    def set_ledger(self, ledger):
+        if ledger is None or len(ledger[0]) == 0:
+            _check(self.lib.tdpg_pp_set(self.h, 0, None, None, None))
+            return
+        a, b, w = (np.ascontiguousarray(ledger[0], np.int32), np.ascontiguousarray(ledger[1], np.int32),
+                   np.ascontiguousarray(ledger[2], np.float64))
+        _check(self.lib.tdpg_pp_set(self.h, a.size, _p(a), _p(b), _p(w)))
+
+    def ledger(self):
+        q = C.c_int64()
+        _check(self.lib.tdpg_pp_size(self.h, C.byref(q)))
+        out = (np.zeros(q.value, np.int32), np.zeros(q.value, np.int32), np.zeros(q.value))
+        if q.value:
+            _check(self.lib.tdpg_pp_get(self.h, *[_p(x) for x in out]))
+        return out
+
+    def pp_update(self, ledger, hits, wns, w0=10.0, w1=0.2):
+        self.set_ledger(ledger)
+        ha, hb, hs = (np.ascontiguousarray(hits[0], np.int32), np.ascontiguousarray(hits[1], np.int32),
+                      np.ascontiguousarray(hits[2], np.float64))
+        _check(self.lib.tdpg_pp_update(self.h, ha.size, _p(ha), _p(hb), _p(hs), wns, w0, w1))
+        return self.ledger()
+
+    def pp_loss_session(self, kind=0, ledger=None, xy=None):
+        self._pos(xy)
+        if ledger is not None:
+            self.set_ledger(ledger)
+        v = C.c_double()
+        d = np.zeros((self.d.n_pins, 2))
+        _check(self.lib.tdpg_pp_loss(self.h, kind, C.byref(v), d.ctypes.data))
+        return v.value, d
+
+    def objective(self, xy=None, nx=16, ny=16, td=0.6, gamma=1.0, lam=1.0, beta=0.0, kind=0, net_w=None,
+                  ledger=None):
+        self._pos(xy)
+        _check(self.lib.tdpg_set_grid(self.h, nx, ny, td))
+        self.set_ledger(ledger)
+        nw = None if net_w is None else np.ascontiguousarray(net_w, np.float64)
+        terms = np.zeros(6)
+        d = np.zeros((self.d.n_cells, 2))
+        _check(self.lib.tdpg_objective(self.h, gamma, lam, beta, kind, _p(nw), terms.ctypes.data, d.ctypes.data))
+        return terms, d
+
+    # timing ----------------------------------------------------------------
+    def sta(self, xy=None):
+        self._pos(xy)
+        P = self.d.n_pins
+        arr, req, slack = np.zeros(P), np.zeros(P), np.zeros(P)
+        ak, rk = np.zeros(P, np.uint8), np.zeros(P, np.uint8)
+        tns, wns = C.c_double(), C.c_double()
+        _check(self.lib.tdpg_sta(self.h, arr.ctypes.data, req.ctypes.data, slack.ctypes.data, ak.ctypes.data,
+                                 rk.ctypes.data, C.byref(tns), C.byref(wns)))
+        return dict(arr=arr, req=req, slack=slack, arr_known=ak, req_known=rk, tns=tns.value, wns=wns.value)
+
+    def extract(self, xy=None, n=0, k=1, run_sta=True):
+        if run_sta or xy is not None:
+            self._pos(xy)
+            tns, wns = C.c_double(), C.c_double()
+            _check(self.lib.tdpg_sta(self.h, None, None, None, None, None, C.byref(tns), C.byref(wns)))
+        cnt = (C.c_int64 * 4)()
+        _check(self.lib.tdpg_extract_endpoint(self.h, n, k, cnt))
+        npath, total = cnt[0], cnt[1]
+        start = np.zeros(npath + 1, np.int32)
+        pins = np.zeros(max(total, 1), np.int32)
+        slack = np.zeros(max(npath, 1))
+        _check(self.lib.tdpg_paths_get(self.h, start.ctypes.data, pins.ctypes.data, slack.ctypes.data))
+        nh = C.c_int64()
+        _check(self.lib.tdpg_paths_hits(self.h, C.byref(nh), None, None, None))
+        m = max(nh.value, 1)
+        ha, hb, hs = np.zeros(m, np.int32), np.zeros(m, np.int32), np.zeros(m)
+        _check(self.lib.tdpg_paths_hits(self.h, C.byref(nh), ha.ctypes.data, hb.ctypes.data, hs.ctypes.data))
+        sta_ms, ex_ms = C.c_double(), C.c_double()
+        _check(self.lib.tdpg_last_timing_ms(self.h, C.byref(sta_ms), C.byref(ex_ms)))
+        return dict(start=start, pins=pins[:total], slack=slack[:npath], n_paths=npath, unique_endpoints=cnt[2],
+                    unique_pin_pairs=cnt[3], candidates_generated=npath,
+                    hits=(ha[:nh.value], hb[:nh.value], hs[:nh.value]), sta_ms=sta_ms.value, extract_ms=ex_ms.value)
+
+    # placement -------------------------------------------------------------
+    def place(self, cfg: dict | None = None, xy=None):
+        c = make_config(cfg)
+        self._pos(xy if xy is not None else self.d.positions)
+        rows = (TdpgTraceRow * max(c.max_iters, 1))()
+        nr, so = C.c_int32(), C.c_int32()
+        fin = (C.c_double * 3)()
+        _check(self.lib.tdpg_place(self.h, C.byref(c), self.d.pos_explicit.ctypes.data, rows, C.byref(nr),
+                                   C.byref(so), fin))
+        return dict(positions=self.positions(), trace=[rows[i] for i in range(nr.value)], iterations=nr.value,
+                    stop_reason="overflow" if so.value else "max_iters", tns=fin[0], wns=fin[1], hpwl=fin[2],
+                    ledger=self.ledger())
+
+    def engine_init(self, cfg: dict | None = None, xy=None):
+        c = make_config(cfg)
+        self._pos(xy if xy is not None else self.d.positions)
+        self._cfg = c
+        _check(self.lib.tdpg_engine_init(self.h, C.byref(c), self.d.pos_explicit.ctypes.data))
+
+    def iterate(self, n):
+        ms = C.c_double()
+        _check(self.lib.tdpg_iterate_dev(self.h, n, C.byref(ms)))
+        return ms.value
+
+    def step_host(self, xy_in_ptr, xy_out_ptr):
+        """One iteration through host buffers (raw pointers, e.g. pinned memory)."""
+        row = TdpgTraceRow()
+        _check(self.lib.tdpg_step_host(self.h, xy_in_ptr, xy_out_ptr, C.byref(row)))
+        return row
+
+    def engine_stats(self):
+        it, rf, ln = C.c_int32(), C.c_int32(), C.c_int64()
+        _check(self.lib.tdpg_engine_stats(self.h, C.byref(it), C.byref(rf), C.byref(ln)))
+        return dict(iterations=it.value, refreshes=rf.value, kernel_launches=ln.value)
+
+    def profile_iteration(self, reps=5):
+        n = 16
+        out = (C.c_double * n)()
+        names = C.create_string_buffer(n * 32)
+        _check(self.lib.tdpg_profile_iteration(self.h, reps, out, n, names, 32))
+        res = {}
+        for i in range(n):
+            nm = names.raw[i * 32:(i + 1) * 32].split(b"\0")[0].decode()
+            if nm:
+                res[nm] = out[i]
+        return res
+
+    # stateless helpers (tiny one-net designs on the device) ---------------------
+    @staticmethod
+    def _one_net_design(xy):
+        xy = np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
+        n = xy.shape[0]
+        return Design(cell_w=np.zeros(0), cell_h=np.zeros(0), cell_delay=np.zeros(0), cell_fixed=np.zeros(0),
+                      pin_cell=-np.ones(n), pin_term=xy, pin_off=np.zeros((n, 2)),
+                      pin_dir=[1] + [0] * (n - 1), pin_cap=np.zeros(n), net_start=[0, n] if n >= 2 else [0],
+                      net_pins=list(range(n)) if n >= 2 else [], sources=[], endpoints=[], clock_period=1.0,
+                      r_unit=1.0, c_unit=1.0, core=(0.0, 0.0, 1.0, 1.0), positions=np.zeros((0, 2)),
+                      pos_explicit=np.zeros(0))
+
+    @classmethod
+    def wa(cls, xy, gamma):
+        """wa_wirelength on one net (wirelength.cpp:49-58), computed by the device kernel."""
+        xy = np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
+        if xy.shape[0] < 2:
+            return 0.0, np.zeros_like(xy)
+        s = cls(cls._one_net_design(xy))
+        v, _, g = s.wirelength(gamma)
+        return v, g
+
+    @classmethod
+    def pp_loss(cls, ledger, pin_xy, kind=0):
+        """pin_pair_loss (pin_pairs.cpp:17-49), computed by the device kernel."""
+        s = cls(cls._one_net_design(pin_xy))
+        return s.pp_loss_session(kind, ledger)
+
+    @classmethod
+    def adam_step(cls, x, g, m, v, t, lr, b1=0.9, b2=0.999, eps=1e-8):
+        tt = C.c_int32(t)
+        _check(lib().tdpg_adam_step(x.size, x.ctypes.data, g.ctypes.data, m.ctypes.data, v.ctypes.data, C.byref(tt),
+                                    lr, b1, b2, eps))
+        return tt.value
+
+
+def generate(seed=1, cells=100, registers=-1, fanout=2.0, fail_frac=0.2, r_unit=1e-4, c_unit=1e-4,
+             calibrate=True) -> Design:
+    """generate_synthetic (generator.cpp:60-263): same netlist as the reference, O(N log N);
+    the clock calibration's coarse placement runs on the GPU (calibrate=False keeps clock 1.0)."""
+    L = lib()
+    h = _P()
+    _check(L.tdpg_generate(seed, cells, registers, fanout, fail_frac, r_unit, c_unit, int(calibrate), C.byref(h)))
+    try:
+        v = TdpgNetlist()
+        pos = _P()
+        _check(L.tdpg_design_view(h, C.byref(v), C.byref(pos)))
+
+        def arr(ptr, n, ct, shape=None):
+            if n == 0:
+                return np.zeros(shape or (0,), dtype=np.dtype(ct))
+            a = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
+            return a.reshape(shape) if shape else a
+
+        Cn, P, N = v.n_cells, v.n_pins, v.n_nets
+        E = arr(v.net_start, N + 1, C.c_int32)[-1]
+        d = Design(cell_w=arr(v.cell_w, Cn, C.c_double), cell_h=arr(v.cell_h, Cn, C.c_double),
+                   cell_delay=arr(v.cell_delay, Cn, C.c_double), cell_fixed=arr(v.cell_fixed, Cn, C.c_uint8),
+                   pin_cell=arr(v.pin_cell, P, C.c_int32), pin_term=arr(v.pin_term, 2 * P, C.c_double, (P, 2)),
+                   pin_off=arr(v.pin_off, 2 * P, C.c_double, (P, 2)), pin_dir=arr(v.pin_dir, P, C.c_uint8),
+                   pin_cap=arr(v.pin_cap, P, C.c_double), net_start=arr(v.net_start, N + 1, C.c_int32),
+                   net_pins=arr(v.net_pins, int(E), C.c_int32), sources=arr(v.sources, v.n_sources, C.c_int32),
+                   endpoints=arr(v.endpoints, v.n_endpoints, C.c_int32), clock_period=v.clock_period,
+                   r_unit=v.r_unit, c_unit=v.c_unit, core=tuple(v.core),
+                   positions=arr(pos.value, 2 * Cn, C.c_double, (Cn, 2)), pos_explicit=np.zeros(Cn, np.uint8))
+        return d
+    finally:
+        L.tdpg_design_destroy(h)

@@ -1,0 +1,211 @@
+"""Parity of the sm_100a engine (through the C-ABI) against the oracle.
+
+Tolerances (stated per north_star):
+  * levelization, arcs, extracted paths, pair hits, ledger keys: bit-exact;
+  * STA arrival / required / slack: bit-exact (fp64, FMA-free, same op order);
+  * per-net WA values and pin gradients: 1e-12 relative to the field scale
+    (CUDA's exp differs from glibc's by <= 1 ulp);
+  * objective terms / density / cell gradients: 1e-9 relative to the field
+    scale (density occupancy is accumulated in 2^-k fixed point for run-to-run
+    determinism, reductions are tree-ordered);
+  * final TNS / WNS / HPWL after a fixed iteration count: within 1%.
+"""
+import numpy as np
+import pytest
+
+import kat
+from fixtures import make_t1, make_trunk16, random_design, spread_positions
+from oracle.oracle import Oracle, RefOracle
+
+pytestmark = pytest.mark.gpu
+
+from paper_2503_11674_b200.engine import Session, generate  # noqa: E402
+
+
+def _paths(r):
+    return [r["pins"][r["start"][i]:r["start"][i + 1]].tolist() for i in range(r["n_paths"])]
+
+
+def field_err(a, b):
+    scale = max(np.max(np.abs(b)), 1e-300)
+    return float(np.max(np.abs(a - b)) / scale) if a.size else 0.0
+
+
+@pytest.mark.parametrize("check", kat.ALL, ids=lambda f: f.__name__)
+def test_known_answers_on_device(check):
+    check(Session)
+
+
+@pytest.mark.parametrize("seed", range(1, 81))
+def test_random_designs_bitwise_timing(seed):
+    d = random_design(seed)
+    s, o = Session(d), Oracle(d)
+    gs, go = s.graph(), o.graph()
+    for k in ("n_net_arcs", "n_cell_arcs", "n_levels"):
+        assert gs[k] == go[k]
+    for k in ("level", "arc_from", "arc_to", "arc_kind", "arc_owner"):
+        assert np.array_equal(gs[k], go[k]), k
+    ts, to = s.sta(), o.sta()
+    for k in ("arr", "req", "slack", "arr_known", "req_known"):
+        assert np.array_equal(ts[k], to[k]), k
+    assert ts["wns"] == to["wns"]
+    assert abs(ts["tns"] - to["tns"]) <= 1e-12 * max(1.0, abs(to["tns"]))
+    es, eo = s.extract(n=0), o.extract(n=0)
+    assert _paths(es) == _paths(eo)
+    assert np.array_equal(es["slack"], eo["slack"])
+    for k in ("unique_endpoints", "unique_pin_pairs", "candidates_generated"):
+        assert es[k] == eo[k], k
+    for x, y in zip(es["hits"], eo["hits"]):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("seed", range(1, 41))
+def test_random_designs_objective(seed):
+    d = random_design(seed)
+    s, o = Session(d), Oracle(d)
+    hits, wns = o.extract(n=0)["hits"], o.sta()["wns"]
+    led = o.pp_update(None, hits, wns) if wns < 0 else None
+    if led is not None:
+        led2 = s.pp_update(None, hits, wns)
+        for x, y in zip(led, led2):
+            assert np.array_equal(x, y)
+    for kind in (0, 1):
+        ts, gs = s.objective(nx=8, ny=8, td=0.05, gamma=0.3, lam=0.7, beta=0.2, kind=kind, ledger=led)
+        to, go = o.objective(nx=8, ny=8, td=0.05, gamma=0.3, lam=0.7, beta=0.2, kind=kind, ledger=led)
+        assert np.allclose(ts, to, rtol=1e-9, atol=1e-12), (ts, to)
+        assert field_err(gs, go) <= 1e-9
+    vs, os_, ds = s.density(nx=5, ny=7, td=0.1)
+    vo, oo, do = o.density(nx=5, ny=7, td=0.1)
+    assert abs(vs - vo) <= 1e-9 * max(vo, 1e-300) and abs(os_ - oo) <= 1e-9 * max(oo, 1e-300)
+    assert field_err(ds, do) <= 1e-9
+
+
+def test_wa_per_net_against_reference():
+    rng = np.random.default_rng(5)
+    for n in [2, 3, 5, 8, 9, 17, 40]:
+        xy = rng.uniform(0, 100, (n, 2))
+        vs, gs = Session.wa(xy, 3.7)
+        vr, gr = (RefOracle if RefOracle.available() else Oracle).wa(xy, 3.7)
+        assert abs(vs - vr) <= 1e-12 * abs(vr)
+        assert field_err(gs, gr) <= 1e-12
+
+
+def test_chain_pairs_off_net_pins():
+    """Pin pairs between pins on no net (the reference chain fixture, test_placer.cpp:839-871)."""
+    d = make_t1()
+    led = ([1, 3], [5, 7], [4.0, 2.5])  # A.in-C.in (on nets), B.in-PO
+    ts, gs = Session(d).objective(nx=4, ny=4, td=0.9, gamma=0.5, lam=0.3, beta=0.7, ledger=led)
+    to, go = Oracle(d).objective(nx=4, ny=4, td=0.9, gamma=0.5, lam=0.3, beta=0.7, ledger=led)
+    assert np.allclose(ts, to, rtol=1e-12) and field_err(gs, go) <= 1e-12
+
+
+@pytest.fixture(scope="module")
+def design_10k():
+    return generate(seed=1, cells=10000, fail_frac=0.7, calibrate=True)
+
+
+def test_generated_10k_snapshot_parity(design_10k):
+    d = design_10k
+    xy = spread_positions(d, 3)
+    s, o = Session(d), Oracle(d)
+    ts, to = s.sta(xy), o.sta(xy)
+    assert np.array_equal(ts["arr"], to["arr"]) and np.array_equal(ts["slack"], to["slack"])
+    es, eo = s.extract(xy, n=1000), o.extract(xy, n=1000)
+    assert es["n_paths"] == eo["n_paths"] == 1000
+    assert np.array_equal(es["pins"], eo["pins"]) and np.array_equal(es["start"], eo["start"])
+    assert np.array_equal(es["slack"], eo["slack"])
+    assert es["unique_pin_pairs"] == eo["unique_pin_pairs"]
+    led = o.pp_update(None, eo["hits"], to["wns"])
+    led2 = s.pp_update(None, es["hits"], ts["wns"])
+    for x, y in zip(led, led2):
+        assert np.array_equal(x, y)
+    args = dict(nx=64, ny=64, td=0.6, gamma=0.01 * d.span, lam=1e-4, beta=2.5e-5, ledger=led)
+    tsv, gs = s.objective(xy, **args)
+    tov, go = o.objective(xy, **args)
+    assert np.allclose(tsv, tov, rtol=1e-9)
+    assert field_err(gs, go) <= 1e-9
+
+
+def test_generated_10k_clock_matches_reference_calibration():
+    """Clock calibration runs the coarse placement on the GPU; against the reference's
+    own generate_synthetic the netlist is identical and the clock agrees to 1e-6."""
+    if not RefOracle.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefOracle.generate(seed=2, cells=2000, fail_frac=0.4)
+    ours = generate(seed=2, cells=2000, fail_frac=0.4, calibrate=True)
+    assert np.array_equal(ours.net_pins, ref.net_pins)
+    assert abs(ours.clock_period - ref.clock_period) <= 1e-6 * ref.clock_period
+
+
+def test_place_10k_config_parity(design_10k):
+    """configs[0]: 10K cells, 200 GP iterations, timing from iter 100 every 15, grid 64^2.
+    Final TNS / WNS / HPWL within 1% of the oracle's run_placement."""
+    cfg = {"max_iters": 200, "timing_start_iter": 100, "m": 15, "grid_nx": 64, "grid_ny": 64, "seed": 1}
+    ps = Session(design_10k).place(cfg)
+    po = Oracle(design_10k).place(cfg)
+    assert ps["iterations"] == po["iterations"] == 200
+    for k in ("tns", "wns", "hpwl"):
+        assert abs(ps[k] - po[k]) <= 0.01 * abs(po[k]), (k, ps[k], po[k])
+    # trace rows: every row's hpwl / overflow track the oracle
+    for rs, ro in zip(ps["trace"], po["trace"]):
+        assert rs.has_timing == ro.has_timing
+        assert abs(rs.hpwl - ro.hpwl) <= 0.01 * ro.hpwl
+
+
+def test_place_small_trace_tight():
+    """A short run keeps the trajectory within 1e-6 of the oracle row by row."""
+    d = generate(seed=4, cells=300, fail_frac=0.5, calibrate=True)
+    cfg = {"max_iters": 40, "timing_start_iter": 10, "m": 5, "grid_nx": 8, "grid_ny": 8, "seed": 4}
+    ps, po = Session(d).place(cfg), Oracle(d).place(cfg)
+    assert len(ps["trace"]) == len(po["trace"])
+    for rs, ro in zip(ps["trace"], po["trace"]):
+        assert abs(rs.hpwl - ro.hpwl) <= 1e-6 * ro.hpwl
+        assert abs(rs.overflow - ro.overflow) <= 1e-6 * max(ro.overflow, 1e-12)
+        if ro.has_timing:
+            assert abs(rs.tns - ro.tns) <= 1e-6 * max(1.0, abs(ro.tns))
+
+
+def test_determinism_run_to_run(design_10k):
+    cfg = {"max_iters": 60, "timing_start_iter": 20, "m": 10, "grid_nx": 64, "grid_ny": 64, "seed": 1}
+    a = Session(design_10k).place(cfg)
+    b = Session(design_10k).place(cfg)
+    assert np.array_equal(a["positions"], b["positions"])
+    assert (a["tns"], a["wns"], a["hpwl"]) == (b["tns"], b["wns"], b["hpwl"])
+
+
+def test_trunk16_and_ties():
+    d = make_trunk16()
+    assert _paths(Session(d).extract(n=16)) == _paths(Oracle(d).extract(n=16))
+
+
+def test_nonfinite_raises_with_iteration():
+    """NonFiniteError carries the iteration, like run_placement (placer.cpp:441-443)."""
+    from oracle.oracle import OracleError
+    from paper_2503_11674_b200.engine import NonFiniteError
+    d = make_t1()
+    cfg = {"max_iters": 5, "lambda0": 1e308, "grid_nx": 4, "grid_ny": 4, "target_density": 0.01}
+    with pytest.raises(OracleError) as eo:
+        Oracle(d).place(cfg)
+    with pytest.raises(NonFiniteError) as es:
+        Session(d).place(cfg)
+    assert str(es.value) == str(eo.value)
+
+
+@pytest.mark.parametrize("cells", [200000])
+def test_large_sta_and_extraction_bitwise(cells):
+    """200K-cell design: STA + top-10K extraction bit-exact against the C oracle."""
+    d = generate(seed=1, cells=cells, fail_frac=0.4, calibrate=False)
+    d.clock_period = 1.0
+    xy = spread_positions(d, 1)
+    s, o = Session(d), Oracle(d)
+    to = o.sta(xy)
+    d_clock = float(np.quantile(to["arr"][d.endpoints], 0.6))
+    d.clock_period = d_clock
+    s, o = Session(d), Oracle(d)
+    ts, to = s.sta(xy), o.sta(xy)
+    assert np.array_equal(ts["arr"], to["arr"]) and np.array_equal(ts["req"], to["req"])
+    es, eo = s.extract(xy, n=10000), o.extract(xy, n=10000)
+    assert es["n_paths"] == eo["n_paths"] == 10000
+    assert np.array_equal(es["pins"], eo["pins"]) and np.array_equal(es["slack"], eo["slack"])
+    for x, y in zip(es["hits"], eo["hits"]):
+        assert np.array_equal(x, y)
