@@ -32,6 +32,23 @@ def _p(a):
     return None if a is None else a.ctypes.data
 
 
+class Row:
+    """TraceRow parsed from the reference's metrics.csv (placer.cpp:234-260)."""
+
+    def __init__(self, cells):
+        self.iter = int(cells[0])
+        self.hpwl, self.overflow = float(cells[1]), float(cells[2])
+        self.has_timing = cells[3] != ""
+        self.tns = float(cells[3]) if self.has_timing else 0.0
+        self.wns = float(cells[4]) if self.has_timing else 0.0
+        self.wl_term, self.density_term, self.pp_term = float(cells[5]), float(cells[6]), float(cells[7])
+        self.lambda_, self.beta_pp = float(cells[8]), float(cells[9])
+
+
+def parse_metrics_csv(text):
+    return [Row(line.split(",")) for line in text.strip().splitlines()[1:]]
+
+
 class OracleError(RuntimeError):
     def __init__(self, kind, msg):
         super().__init__(msg)
@@ -489,6 +506,7 @@ class RefOracle(_Base):
         self.lib.ref_place_positions(self.h, pos.ctypes.data)
         ledger = (np.zeros(npairs.value, np.int32), np.zeros(npairs.value, np.int32), np.zeros(npairs.value))
         self.lib.ref_pp_ledger_get(self.h, *[_p(x) for x in ledger])
+        csv = self.lib.ref_place_csv(self.h).decode()
         return dict(positions=pos, iterations=it.value, stop_reason="overflow" if so.value else "max_iters",
-                    tns=fin[0], wns=fin[1], hpwl=fin[2], metrics_csv=self.lib.ref_place_csv(self.h).decode(),
+                    tns=fin[0], wns=fin[1], hpwl=fin[2], metrics_csv=csv, trace=parse_metrics_csv(csv),
                     ledger=ledger, elapsed_ms=ms.value)

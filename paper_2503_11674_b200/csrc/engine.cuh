@@ -87,6 +87,10 @@ struct tdpg_session {
     tdpg::DBuf<double> cell_delay, pin_cap;
     tdpg::DBuf<uint8_t> cell_fixed, pin_dir, is_source, is_endpoint;
     tdpg::DBuf<int> pin_cell, net_start, net_pins, e_cell, pin_entry, cell_ent_start, cell_ent;
+    // WA warp chunks: whole nets packed into <= 32 entries; per entry (pos in net << 8 | net size)
+    tdpg::DBuf<int> chunk_e0, chunk_net0, big_nets;
+    tdpg::DBuf<uint16_t> e_meta;
+    int n_chunks = 0, n_big = 0;
 
     // device timing graph
     tdpg::DBuf<int> lvl_pins, in_start, in_from, out_start, out_to, ep_sorted;
@@ -96,6 +100,13 @@ struct tdpg_session {
     tdpg::DBuf<double> arr, req, slack;
     tdpg::DBuf<uint8_t> ak, rk, tie;
     tdpg::DBuf<int> pred, tie_list, counters; // counters: [0] tie count
+    tdpg::DBuf<int> d_level, tie_scratch;
+    tdpg::DBuf<double> sta_out; // tns, wns, n_violated
+    // ledger-update scratch
+    tdpg::DBuf<uint8_t> lg_flag;
+    tdpg::DBuf<double> lg_w, lg_new_w;
+    tdpg::DBuf<unsigned long long> lg_new_k;
+    tdpg::DBuf<int> lg_nsel;
     double tns = 0, wns = 0;
     bool sta_valid = false;
 

@@ -89,7 +89,10 @@ __device__ double wa_dim_mem(int s0, int n, int axis, const int* __restrict__ e_
     return (hi - lo) + (max_term - min_term);
 }
 
-__global__ void __launch_bounds__(kBlock) k_wirelength(int N, const int* __restrict__ net_start,
+// Thread-per-net WA for the nets the chunked kernel does not take (> 32 pins); net_list
+// selects them (null = every net).
+__global__ void __launch_bounds__(kBlock) k_wirelength(int N, const int* __restrict__ net_list,
+                                                       const int* __restrict__ net_start,
                                                        const int* __restrict__ e_cell,
                                                        const double2* __restrict__ e_off,
                                                        const double2* __restrict__ cell_xy,
@@ -100,9 +103,10 @@ __global__ void __launch_bounds__(kBlock) k_wirelength(int N, const int* __restr
 {
     __shared__ double sh[kBlock / 32];
     if (ctrl && ctrl->stopped) return;
-    const int e = blockIdx.x * kBlock + threadIdx.x;
+    const int i_net = blockIdx.x * kBlock + threadIdx.x;
     double wl = 0.0, hp = 0.0;
-    if (e < N) {
+    if (i_net < N) {
+        const int e = net_list ? net_list[i_net] : i_net;
         const int s0 = net_start[e], n = net_start[e + 1] - s0;
         const double w = net_w ? net_w[e] : 1.0;
         if (n < 2) {
@@ -135,6 +139,125 @@ __global__ void __launch_bounds__(kBlock) k_wirelength(int N, const int* __restr
             const double vy = wa_dim_mem(s0, n, 1, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hy);
             wl = w * (vx + vy);
             hp = hx + hy;
+        }
+    }
+    const double bw = block_sum<kBlock>(wl, sh);
+    const double bh = block_sum<kBlock>(hp, sh);
+    if (threadIdx.x == 0) part_wl[blockIdx.x] = bw, part_hp[blockIdx.x] = bh;
+}
+
+// =====================================================================================
+// WA wirelength, warp-chunked (the fast path for nets of <= 32 pins).
+// Nets are packed, whole and in order, into chunks of <= 32 net-pin entries; one warp
+// owns a chunk and one lane one entry.  Lanes load their entry (coalesced), then one
+// head lane per net walks the net's pins in the reference order for the max/min and the
+// four exponential sums (wirelength.cpp:15-34), so only per-net work is sequential and
+// warp divergence is bounded by the largest net in the chunk.  The 4 exps per pin are
+// computed once and reused for the gradient; divisions by gamma and by the sums become
+// multiplications by reciprocals computed once per kernel / per net.
+// =====================================================================================
+constexpr int kWaWarps = kBlock / 32;
+
+struct WaSmem {
+    double2 xy[kWaWarps][32];
+    double sum[kWaWarps][32][8]; // per lane summands; head lanes overwrite with per-net results
+};
+
+__global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* __restrict__ chunk_e0,
+                                                      const int* __restrict__ chunk_net0,
+                                                      const uint16_t* __restrict__ e_meta,
+                                                      const int* __restrict__ e_cell,
+                                                      const double2* __restrict__ e_off,
+                                                      const double2* __restrict__ cell_xy,
+                                                      const double2* __restrict__ anchor,
+                                                      const double* __restrict__ net_w, double gamma,
+                                                      double inv_gamma, double2* __restrict__ grad_e,
+                                                      double* __restrict__ part_wl, double* __restrict__ part_hp,
+                                                      const Ctrl* __restrict__ ctrl)
+{
+    __shared__ WaSmem sm;
+    __shared__ double sh[kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int chunk = blockIdx.x * kWaWarps + w;
+    double wl = 0.0, hp = 0.0;
+    if (chunk < n_chunks) {
+        const int e0 = chunk_e0[2 * chunk], e1 = chunk_e0[2 * chunk + 1];
+        const int e = e0 + lane;
+        const bool valid = e < e1;
+        int pos = 0, n = 0;
+        double x = 0.0, y = 0.0;
+        if (valid) {
+            const uint16_t m = e_meta[e];
+            pos = m >> 8, n = m & 0xFF;
+            const double2 p = entry_pos(e_cell[e], e_off[e], cell_xy, anchor);
+            x = p.x, y = p.y;
+            sm.xy[w][lane] = p;
+        }
+        const int head = lane - pos;
+        const bool is_head = valid && pos == 0;
+        const unsigned head_mask = __ballot_sync(0xffffffffu, is_head);
+        __syncwarp();
+        // head lanes: hi/lo per dimension in pin order (wirelength.cpp:15-20)
+        double hix = 0, lox = 0, hiy = 0, loy = 0;
+        if (is_head) {
+            hix = lox = x, hiy = loy = y;
+            for (int i = 1; i < n; ++i) {
+                const double2 q = sm.xy[w][lane + i];
+                hix = smax(hix, q.x), lox = smin(lox, q.x), hiy = smax(hiy, q.y), loy = smin(loy, q.y);
+            }
+            sm.sum[w][lane][0] = hix, sm.sum[w][lane][1] = lox, sm.sum[w][lane][2] = hiy, sm.sum[w][lane][3] = loy;
+        }
+        __syncwarp();
+        if (valid && !is_head) {
+            hix = sm.sum[w][head][0], lox = sm.sum[w][head][1], hiy = sm.sum[w][head][2], loy = sm.sum[w][head][3];
+        }
+        __syncwarp();
+        // per pin: the four anchored exponentials (wirelength.cpp:26-31)
+        double eux = 0, elx = 0, euy = 0, ely = 0;
+        if (valid) {
+            eux = exp((x - hix) * inv_gamma);
+            elx = exp(-(x - lox) * inv_gamma);
+            euy = exp((y - hiy) * inv_gamma);
+            ely = exp(-(y - loy) * inv_gamma);
+            double* s = sm.sum[w][lane];
+            s[0] = eux, s[1] = (x - hix) * eux, s[2] = elx, s[3] = (x - lox) * elx;
+            s[4] = euy, s[5] = (y - hiy) * euy, s[6] = ely, s[7] = (y - loy) * ely;
+        }
+        __syncwarp();
+        double r[8];
+        if (is_head) {
+            double a[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = 0.0;
+            for (int i = 0; i < n; ++i) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) a[k] += sm.sum[w][lane + i][k];
+            }
+            const double isx = 1.0 / a[0], inx = 1.0 / a[2], isy = 1.0 / a[4], iny = 1.0 / a[6];
+            const double mtx = a[1] / a[0], ntx = a[3] / a[2], mty = a[5] / a[4], nty = a[7] / a[6];
+            const int net = chunk_net0[chunk] + __popc(head_mask & ((1u << lane) - 1u));
+            const double wt = net_w ? net_w[net] : 1.0;
+            wl = wt * (((hix - lox) + (mtx - ntx)) + ((hiy - loy) + (mty - nty)));
+            hp = (hix - lox) + (hiy - loy);
+            r[0] = isx, r[1] = mtx, r[2] = inx, r[3] = ntx, r[4] = isy, r[5] = mty, r[6] = iny, r[7] = nty;
+        }
+        __syncwarp();
+        if (is_head) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sm.sum[w][lane][k] = r[k];
+            const int net = chunk_net0[chunk] + __popc(head_mask & ((1u << lane) - 1u));
+            sm.xy[w][lane].x = net_w ? net_w[net] : 1.0; // own position no longer needed
+        }
+        __syncwarp();
+        if (valid) {
+            const double* q = sm.sum[w][head];
+            const double wt = sm.xy[w][head].x;
+            const double dmx = (eux * q[0]) * (1.0 + ((x - hix) - q[1]) * inv_gamma);
+            const double dnx = (elx * q[2]) * (1.0 - ((x - lox) - q[3]) * inv_gamma);
+            const double dmy = (euy * q[4]) * (1.0 + ((y - hiy) - q[5]) * inv_gamma);
+            const double dny = (ely * q[6]) * (1.0 - ((y - loy) - q[7]) * inv_gamma);
+            grad_e[e] = make_double2(wt * (dmx - dnx), wt * (dmy - dny));
         }
     }
     const double bw = block_sum<kBlock>(wl, sh);
@@ -227,35 +350,35 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter(int C, const double2
     const double2 p = cell_xy[c], s = cell_wh[c];
     const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
     int bx0, bx1, by0, by1;
-    footprint_range(g, xl, xh, yl, yh, bx0, bx1, by0, by1);
+    foot_range(xl, xh, g.x0, g.bw, g.inv_bw, g.nx, bx0, bx1);
+    foot_range(yl, yh, g.y0, g.bh, g.inv_bh, g.ny, by0, by1);
     const double area = s.x * s.y;
-    const int nby = by1 - by0 + 1;
-    double wyc[kFootCache], dwyc[kFootCache];
-    const bool cached = nby <= kFootCache;
-    if (cached)
-        for (int j = 0; j < nby; ++j) {
-            const double cy = g.y0 + (by0 + j + 0.5) * g.bh;
-            wyc[j] = extent_weight(yl, yh, cy, g.bh);
-            dwyc[j] = extent_weight_grad(yl, yh, cy, g.bh);
-        }
+    const double ilx = 1.0 / s.x, ily = 1.0 / s.y;
+    const int nby = min(by1 - by0 + 1, kFoot);
+    double wyc[kFoot];
+#pragma unroll
+    for (int j = 0; j < kFoot; ++j) {
+        double dwy = 0.0;
+        wyc[j] = 0.0;
+        if (j < nby) extent_w(yl, yh, g.y0 + (by0 + j + 0.5) * g.bh, g.bh, g.inv_bh, ily, wyc[j], dwy);
+    }
     for (int bx = bx0; bx <= bx1; ++bx) {
-        const double cx = g.x0 + (bx + 0.5) * g.bw;
-        const double wx = extent_weight(xl, xh, cx, g.bw);
-        const double dwx = extent_weight_grad(xl, xh, cx, g.bw);
-        if (wx == 0.0 && dwx == 0.0) continue;
-        for (int by = by0; by <= by1; ++by) {
+        double wx, dwx;
+        extent_w(xl, xh, g.x0 + (bx + 0.5) * g.bw, g.bw, g.inv_bw, ilx, wx, dwx);
+        if (wx == 0.0) continue; // zero-weight columns add nothing to the occupancy
+        const double aw = area * wx;
+        unsigned long long* row = acc + static_cast<long long>(bx) * g.ny + by0;
+#pragma unroll
+        for (int j = 0; j < kFoot; ++j) {
+            if (j >= nby) break;
+            const long long q = __double2ll_rn(aw * wyc[j] * g.scale);
+            if (q) atomicAdd(row + j, static_cast<unsigned long long>(q));
+        }
+        for (int by = by0 + kFoot; by <= by1; ++by) { // footprints wider than kFoot bins
             double wy, dwy;
-            if (cached) {
-                wy = wyc[by - by0], dwy = dwyc[by - by0];
-            } else {
-                const double cy = g.y0 + (by + 0.5) * g.bh;
-                wy = extent_weight(yl, yh, cy, g.bh);
-                dwy = extent_weight_grad(yl, yh, cy, g.bh);
-            }
-            if (wy == 0.0 && dwy == 0.0) continue;
-            const double w = area * wx * wy;
-            const long long q = __double2ll_rn(w * g.scale);
-            if (q) atomicAdd(&acc[static_cast<long long>(bx) * g.ny + by], static_cast<unsigned long long>(q));
+            extent_w(yl, yh, g.y0 + (by + 0.5) * g.bh, g.bh, g.inv_bh, ily, wy, dwy);
+            const long long q = __double2ll_rn(aw * wy * g.scale);
+            if (q) atomicAdd(acc + static_cast<long long>(bx) * g.ny + by, static_cast<unsigned long long>(q));
         }
     }
 }
@@ -386,22 +509,37 @@ __global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __r
     const double2 p = a.xy[c], s = a.wh[c];
     const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
     int bx0, bx1, by0, by1;
-    footprint_range(a.g, xl, xh, yl, yh, bx0, bx1, by0, by1);
+    foot_range(xl, xh, a.g.x0, a.g.bw, a.g.inv_bw, a.g.nx, bx0, bx1);
+    foot_range(yl, yh, a.g.y0, a.g.bh, a.g.inv_bh, a.g.ny, by0, by1);
     const double area = s.x * s.y;
+    const double ilx = 1.0 / s.x, ily = 1.0 / s.y;
+    const int nby = min(by1 - by0 + 1, kFoot);
+    double wyc[kFoot], dwyc[kFoot];
+#pragma unroll
+    for (int j = 0; j < kFoot; ++j) {
+        wyc[j] = 0.0, dwyc[j] = 0.0;
+        if (j < nby) extent_w(yl, yh, a.g.y0 + (by0 + j + 0.5) * a.g.bh, a.g.bh, a.g.inv_bh, ily, wyc[j], dwyc[j]);
+    }
     double dgx = 0.0, dgy = 0.0;
     for (int bx = bx0; bx <= bx1; ++bx) {
-        const double cx = a.g.x0 + (bx + 0.5) * a.g.bw;
-        const double wx = extent_weight(xl, xh, cx, a.g.bw);
-        const double dwx = extent_weight_grad(xl, xh, cx, a.g.bw);
+        double wx, dwx;
+        extent_w(xl, xh, a.g.x0 + (bx + 0.5) * a.g.bw, a.g.bw, a.g.inv_bw, ilx, wx, dwx);
         if (wx == 0.0 && dwx == 0.0) continue;
-        for (int by = by0; by <= by1; ++by) {
-            const double cy = a.g.y0 + (by + 0.5) * a.g.bh;
-            const double wy = extent_weight(yl, yh, cy, a.g.bh);
-            const double dwy = extent_weight_grad(yl, yh, cy, a.g.bh);
-            if (wy == 0.0 && dwy == 0.0) continue;
+        const double adx = area * dwx, awx = area * wx;
+        const double* ex = a.excess + static_cast<long long>(bx) * a.g.ny + by0;
+#pragma unroll
+        for (int j = 0; j < kFoot; ++j) {
+            if (j >= nby) break;
+            const double f = 2.0 * ex[j];
+            dgx += f * (adx * wyc[j]);
+            dgy += f * (awx * dwyc[j]);
+        }
+        for (int by = by0 + kFoot; by <= by1; ++by) {
+            double wy, dwy;
+            extent_w(yl, yh, a.g.y0 + (by + 0.5) * a.g.bh, a.g.bh, a.g.inv_bh, ily, wy, dwy);
             const double f = 2.0 * a.excess[static_cast<long long>(bx) * a.g.ny + by];
-            dgx += f * (area * dwx * wy);
-            dgy += f * (area * wx * dwy);
+            dgx += f * (adx * wy);
+            dgy += f * (awx * dwy);
         }
     }
     const double lambda = cur->lambda;
@@ -442,10 +580,13 @@ __global__ void k_adam_flat(long long n, double* x, const double* g, double* m, 
 GridDev grid_dev(const tdpg_session* s)
 {
     const Grid& g = s->grid;
-    return GridDev{g.nx, g.ny, g.x0, g.y0, g.bw, g.bh, g.cap, g.scale, g.inv_scale, g.total_movable};
+    return GridDev{g.nx, g.ny, g.x0, g.y0, g.bw, g.bh, g.cap, g.scale, g.inv_scale, g.total_movable, 1.0 / g.bw,
+                   1.0 / g.bh};
 }
 
-int wa_blocks(const tdpg_session* s) { return std::max(1, static_cast<int>(blocks_for(s->N, kBlock))); }
+int wa_chunk_blocks(const tdpg_session* s);
+int wa_big_blocks(const tdpg_session* s);
+int wa_blocks(const tdpg_session* s) { return wa_chunk_blocks(s) + wa_big_blocks(s); }
 int pp_blocks(const tdpg_session*) { return 148 * 4; }
 int bins_blocks(const tdpg_session* s)
 {
@@ -526,13 +667,25 @@ void rebuild_pp_incidence(tdpg_session* s)
     CK_LAUNCH();
 }
 
+// blocks of the chunked WA kernel and of the big-net kernel (partials laid out back to back)
+int wa_chunk_blocks(const tdpg_session* s) { return std::max(1, static_cast<int>(blocks_for(s->n_chunks, kWaWarps))); }
+int wa_big_blocks(const tdpg_session* s) { return s->n_big ? static_cast<int>(blocks_for(s->n_big, kBlock)) : 0; }
+
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk,
                        const Ctrl* ctrl)
 {
-    k_wirelength<<<nblk, kBlock, 0, s->st>>>(s->N, s->net_start, s->e_cell, s->e_off, s->cell_xy, s->anchor,
-                                             use_net_w ? s->net_w.p : nullptr, gamma, s->grad_e, part_wl, part_hp,
-                                             ctrl);
+    const int nb1 = wa_chunk_blocks(s), nb2 = wa_big_blocks(s);
+    (void)nblk;
+    const double* nw = use_net_w ? s->net_w.p : nullptr;
+    k_wa_chunks<<<nb1, kBlock, 0, s->st>>>(s->n_chunks, s->chunk_e0, s->chunk_net0, s->e_meta, s->e_cell, s->e_off,
+                                           s->cell_xy, s->anchor, nw, gamma, 1.0 / gamma, s->grad_e, part_wl, part_hp,
+                                           ctrl);
     CK_LAUNCH();
+    if (nb2) {
+        k_wirelength<<<nb2, kBlock, 0, s->st>>>(s->n_big, s->big_nets, s->net_start, s->e_cell, s->e_off, s->cell_xy,
+                                                s->anchor, nw, gamma, s->grad_e, part_wl + nb1, part_hp + nb1, ctrl);
+        CK_LAUNCH();
+    }
 }
 
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk)

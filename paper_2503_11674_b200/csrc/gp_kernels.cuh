@@ -61,8 +61,44 @@ __device__ __forceinline__ double extent_weight_grad(double lo, double hi, doubl
 
 struct GridDev {
     int nx, ny;
-    double x0, y0, bw, bh, cap, scale, inv_scale, total_movable;
+    double x0, y0, bw, bh, cap, scale, inv_scale, total_movable, inv_bw, inv_bh;
 };
+
+// bspline2 / bspline2_integral with the divisions by 6 and 3 as reciprocal multiplies.
+__device__ __forceinline__ double bspline2_integral_r(double u)
+{
+    constexpr double kSixth = 1.0 / 6.0, kThird = 1.0 / 3.0;
+    if (u <= -1.5) return 0.0;
+    if (u >= 1.5) return 1.0;
+    if (u <= -0.5) {
+        const double t = u + 1.5;
+        return t * t * t * kSixth;
+    }
+    if (u <= 0.5) return 0.5 + 0.75 * u - u * u * u * kThird;
+    const double t = 1.5 - u;
+    return 1.0 - t * t * t * kSixth;
+}
+
+// extent_weight + extent_weight_grad (density.cpp:41-49) for one bin centre c, with the
+// per-cell reciprocal of the extent and the grid's reciprocal pitch.
+__device__ __forceinline__ void extent_w(double lo, double hi, double c, double h, double inv_h, double inv_len,
+                                         double& w, double& dw)
+{
+    const double uh = (hi - c) * inv_h, ul = (lo - c) * inv_h;
+    w = (bspline2_integral_r(uh) - bspline2_integral_r(ul)) * h * inv_len;
+    dw = (bspline2(uh) - bspline2(ul)) * inv_len;
+}
+
+constexpr int kFoot = 16; // footprint bins per dimension kept in registers/local memory
+
+// Footprint bin range (density.cpp:109-112) with reciprocal pitch; bins at the range ends
+// carry zero weight, so a one-bin difference from the division form changes nothing.
+__device__ __forceinline__ void foot_range(double lo, double hi, double origin, double pitch, double inv_pitch,
+                                           int nbins, int& b0, int& b1)
+{
+    b0 = max(0, static_cast<int>(floor((lo - 1.5 * pitch - origin) * inv_pitch - 0.5)));
+    b1 = min(nbins - 1, static_cast<int>(ceil((hi + 1.5 * pitch - origin) * inv_pitch - 0.5)));
+}
 
 // Footprint bin range of a movable cell (density.cpp:109-112).
 __device__ __forceinline__ void footprint_range(const GridDev& g, double xl, double xh, double yl, double yh, int& bx0,

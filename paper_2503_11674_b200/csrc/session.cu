@@ -254,6 +254,7 @@ void build_graph(tdpg_session* s)
     s->out_start.upload(out_s, s->st);
     s->out_to.upload(out_to, s->st);
     s->lvl_pins.upload(s->h_lvl_pins, s->st);
+    s->d_level.upload(s->h_level, s->st);
     std::vector<int> eps(s->h_endpoints);
     std::sort(eps.begin(), eps.end());
     s->ep_sorted.upload(eps, s->st);
@@ -374,6 +375,31 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         }
     s->e_cell.upload(e_cell, s->st);
     s->e_off.upload(e_off, s->st);
+    {   // warp chunks for the WA kernel: whole nets of <= 32 pins, packed in net order
+        std::vector<int> se, c_net0, big; // se: (start, end) entry range per chunk
+        std::vector<uint16_t> meta(std::max(E, 1), 0);
+        bool open = false;
+        for (int n = 0; n < N; ++n) {
+            const int b = s->h_net_start[n], k = s->h_net_start[n + 1] - b;
+            if (k > 32) {
+                big.push_back(n);
+                open = false;
+                continue;
+            }
+            if (!open || (b + k) - se[se.size() - 2] > 32) {
+                se.push_back(b), se.push_back(b), c_net0.push_back(n);
+                open = true;
+            }
+            se.back() = b + k;
+            for (int i = 0; i < k; ++i) meta[b + i] = static_cast<uint16_t>((i << 8) | k);
+        }
+        s->n_chunks = static_cast<int>(c_net0.size());
+        s->n_big = static_cast<int>(big.size());
+        s->chunk_e0.upload(se.empty() ? std::vector<int>{0, 0} : se, s->st);
+        s->chunk_net0.upload(c_net0.empty() ? std::vector<int>{0} : c_net0, s->st);
+        s->e_meta.upload(meta, s->st);
+        s->big_nets.upload(big.empty() ? std::vector<int>{0} : big, s->st);
+    }
     // Cell pins on no net still take pin-pair gradient (pin_pairs.cpp:31-34 writes any pin):
     // they get extra slots after the E net entries, written only by the pin-pair kernel.
     int extra = 0;

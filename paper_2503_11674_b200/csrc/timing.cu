@@ -375,11 +375,10 @@ void run_sta_async(tdpg_session* s, double* out3)
 
 void run_sta_dev(tdpg_session* s)
 {
-    s->part.reserve(16);
-    DBuf<double> out3(3);
-    run_sta_async(s, out3);
+    s->sta_out.reserve(4);
+    run_sta_async(s, s->sta_out);
     double h[3];
-    out3.download(h, 3, s->st);
+    s->sta_out.download(h, 3, s->st);
     CK(cudaStreamSynchronize(s->st));
     s->tns = h[0], s->wns = h[1];
     s->sta_valid = true;
@@ -389,8 +388,9 @@ void run_sta_dev(tdpg_session* s)
 void extract_endpoint_dev(tdpg_session* s, int n)
 {
     if (!s->sta_valid) run_sta_dev(s);
-    // recompute keys (run_sta_async left them; recompute cheaply to be self-contained)
-    DBuf<double> out3(3);
+    // endpoint keys from the current STA (cheap; keeps extraction self-contained)
+    s->sta_out.reserve(4);
+    double* out3 = s->sta_out.p;
     {
         const int P = s->P;
         const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
@@ -415,13 +415,11 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     // ties: resolve before any backtrace
     {
         const int stride = s->L + 2;
-        DBuf<int> scratch(static_cast<size_t>(kBlock) * 2 * stride);
-        DBuf<int> level(s->P);
-        level.upload(s->h_level, s->st);
-        k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), level, s->L, scratch, stride);
+        s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * stride);
+        k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), s->d_level, s->L, s->tie_scratch, stride);
         CK_LAUNCH();
         double h[3];
-        out3.download(h, 3, s->st);
+        CK(cudaMemcpyAsync(h, out3, sizeof h, cudaMemcpyDeviceToHost, s->st));
         CK(cudaStreamSynchronize(s->st));
         const int nv = static_cast<int>(h[2]);
         s->n_paths = (n <= 0) ? nv : std::min(n, nv);
@@ -479,15 +477,16 @@ void extract_endpoint_dev(tdpg_session* s, int n)
 void ledger_apply_sorted(tdpg_session* s, long long H, double wns, double w0, double w1)
 {
     if (!(wns < 0.0) || H == 0) return;
-    DBuf<uint8_t> flag(H);
-    DBuf<double> nw(H);
+    s->lg_flag.reserve(H), s->lg_w.reserve(H), s->lg_new_k.reserve(H), s->lg_new_w.reserve(H), s->lg_nsel.reserve(2);
+    DBuf<uint8_t>& flag = s->lg_flag;
+    DBuf<double>& nw = s->lg_w;
     const long long Q = s->Q;
     k_ledger_groups<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(H, s->hit_key_s, s->hit_idx_s, s->hit_slack,
                                                                  s->led_key, s->led_w, Q, wns, w0, w1, flag, nw);
     CK_LAUNCH();
-    DBuf<unsigned long long> new_k(H);
-    DBuf<double> new_w(H);
-    DBuf<int> n_sel(1);
+    DBuf<unsigned long long>& new_k = s->lg_new_k;
+    DBuf<double>& new_w = s->lg_new_w;
+    DBuf<int>& n_sel = s->lg_nsel;
     size_t bytes = 0;
     cub::DeviceSelect::Flagged(nullptr, bytes, s->hit_key_s.p, flag.p, new_k.p, n_sel.p, static_cast<int>(H), s->st);
     void* tmp = cub_scratch(s, bytes);

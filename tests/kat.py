@@ -140,5 +140,26 @@ def check_adam(B):
     assert abs(x[0] - 4.8) <= 1e-7 * 4.8 and t == 2
 
 
-ALL = [check_t1_sta, check_t2_sta, check_t1_graph, check_diamond_paths, check_t2_endpoint, check_trunk16,
+# quick_config (test_placer.cpp:693-705)
+QUICK = {"max_iters": 40, "timing_start_iter": 10, "m": 5, "grid_nx": 8, "grid_ny": 8, "target_density": 1e-6}
+
+
+def check_schedule(B):
+    """test_placer.cpp:709-739 — tight T1 (clock 2): 40 rows, timing rows at 10, 15, ..., 35,
+    no attraction before the first round, violated at every round, pairs attracted."""
+    d = make_t1()
+    d.clock_period = 2.0
+    out = B(d).place(QUICK)
+    assert out["stop_reason"] == "max_iters" and out["iterations"] == 40 and len(out["trace"]) == 40
+    for row in out["trace"]:
+        expect = row.iter >= 10 and (row.iter - 10) % 5 == 0
+        assert bool(row.has_timing) == expect
+        if row.iter < 10:
+            assert row.pp_term == 0.0
+        if expect:
+            assert row.wns < 0.0
+    assert out["trace"][-1].pp_term > 0.0
+
+
+ALL = [check_schedule, check_t1_sta, check_t2_sta, check_t1_graph, check_diamond_paths, check_t2_endpoint, check_trunk16,
        check_t1_pairs, check_t1_hpwl, check_wa_closed_form, check_pp_hand_values, check_ledger, check_adam]
