@@ -36,8 +36,8 @@ METRIC = "GP iters/s & top-k path-extraction ms at 1M cells; TNS/WNS/HPWL parity
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=15)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cells", type=int, default=1_000_000, help="generator spec n_cells (1.1x cells)")
     ap.add_argument("--grid", type=int, default=1024)
@@ -272,7 +272,6 @@ def run_ours(args):
     t0 = time.time()
     s.engine_init(cfg)
     init_s = time.time() - t0
-    s.iterate(args.warmup)
 
     def barrier():
         torch.cuda.synchronize()
@@ -280,12 +279,16 @@ def run_ours(args):
             import torch.distributed as dist
             dist.barrier()
 
-    barrier()
-    st0 = s.engine_stats()
+    # the sampler runs from before the warm-up until after the timed region
     with Clocks(local) as clk:
+        time.sleep(0.5)
+        s.iterate(args.warmup)
+        barrier()
+        st0 = s.engine_stats()
         dev_ms = s.iterate(args.steps)
-    st1 = s.engine_stats()
-    barrier()
+        st1 = s.engine_stats()
+        barrier()
+        time.sleep(0.3)
     ms = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         import torch.distributed as dist
