@@ -34,6 +34,9 @@ struct Grid {
     DBuf<long long> acc;
     DBuf<double> excess;
     DBuf<double> base; // fixed-cell exact overlap (density.cpp:75-93), when any fixed cell
+    DBuf<int> perm, perm_tmp;  // movable cells in spatial (tile) order, for the windowed scatter
+    DBuf<unsigned> perm_keys;
+    int n_movable = 0;
     bool valid() const { return nx > 0; }
     long long bins() const { return static_cast<long long>(nx) * ny; }
 };
@@ -154,6 +157,7 @@ namespace tdpg {
 void upload_positions(tdpg_session* s, const double* xy);
 void ensure_grid(tdpg_session* s, int nx, int ny, double td);
 void* cub_scratch(tdpg_session* s, size_t bytes);
+void sort_cells_spatial(tdpg_session* s);
 
 // gp.cu
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk);

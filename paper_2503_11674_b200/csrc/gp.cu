@@ -158,9 +158,9 @@ __global__ void __launch_bounds__(kBlock) k_wirelength(int N, const int* __restr
 // =====================================================================================
 constexpr int kWaWarps = kBlock / 32;
 
-struct WaSmem {
-    double2 xy[kWaWarps][32];
-    double sum[kWaWarps][32][8]; // per lane summands; head lanes overwrite with per-net results
+struct WaSmem { // [k][lane] layout: head lanes walking their net read consecutive words
+    double x[kWaWarps][32], y[kWaWarps][32];
+    double sum[kWaWarps][8][32]; // per lane summands; head lanes overwrite with per-net results
 };
 
 __global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* __restrict__ chunk_e0,
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* _
             pos = m >> 8, n = m & 0xFF;
             const double2 p = entry_pos(e_cell[e], e_off[e], cell_xy, anchor);
             x = p.x, y = p.y;
-            sm.xy[w][lane] = p;
+            sm.x[w][lane] = x, sm.y[w][lane] = y;
         }
         const int head = lane - pos;
         const bool is_head = valid && pos == 0;
@@ -203,14 +203,14 @@ __global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* _
         if (is_head) {
             hix = lox = x, hiy = loy = y;
             for (int i = 1; i < n; ++i) {
-                const double2 q = sm.xy[w][lane + i];
-                hix = smax(hix, q.x), lox = smin(lox, q.x), hiy = smax(hiy, q.y), loy = smin(loy, q.y);
+                const double qx = sm.x[w][lane + i], qy = sm.y[w][lane + i];
+                hix = smax(hix, qx), lox = smin(lox, qx), hiy = smax(hiy, qy), loy = smin(loy, qy);
             }
-            sm.sum[w][lane][0] = hix, sm.sum[w][lane][1] = lox, sm.sum[w][lane][2] = hiy, sm.sum[w][lane][3] = loy;
+            sm.sum[w][0][lane] = hix, sm.sum[w][1][lane] = lox, sm.sum[w][2][lane] = hiy, sm.sum[w][3][lane] = loy;
         }
         __syncwarp();
         if (valid && !is_head) {
-            hix = sm.sum[w][head][0], lox = sm.sum[w][head][1], hiy = sm.sum[w][head][2], loy = sm.sum[w][head][3];
+            hix = sm.sum[w][0][head], lox = sm.sum[w][1][head], hiy = sm.sum[w][2][head], loy = sm.sum[w][3][head];
         }
         __syncwarp();
         // per pin: the four anchored exponentials (wirelength.cpp:26-31)
@@ -220,9 +220,10 @@ __global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* _
             elx = exp(-(x - lox) * inv_gamma);
             euy = exp((y - hiy) * inv_gamma);
             ely = exp(-(y - loy) * inv_gamma);
-            double* s = sm.sum[w][lane];
-            s[0] = eux, s[1] = (x - hix) * eux, s[2] = elx, s[3] = (x - lox) * elx;
-            s[4] = euy, s[5] = (y - hiy) * euy, s[6] = ely, s[7] = (y - loy) * ely;
+            sm.sum[w][0][lane] = eux, sm.sum[w][1][lane] = (x - hix) * eux;
+            sm.sum[w][2][lane] = elx, sm.sum[w][3][lane] = (x - lox) * elx;
+            sm.sum[w][4][lane] = euy, sm.sum[w][5][lane] = (y - hiy) * euy;
+            sm.sum[w][6][lane] = ely, sm.sum[w][7][lane] = (y - loy) * ely;
         }
         __syncwarp();
         double r[8];
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* _
             for (int k = 0; k < 8; ++k) a[k] = 0.0;
             for (int i = 0; i < n; ++i) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) a[k] += sm.sum[w][lane + i][k];
+                for (int k = 0; k < 8; ++k) a[k] += sm.sum[w][k][lane + i];
             }
             const double isx = 1.0 / a[0], inx = 1.0 / a[2], isy = 1.0 / a[4], iny = 1.0 / a[6];
             const double mtx = a[1] / a[0], ntx = a[3] / a[2], mty = a[5] / a[4], nty = a[7] / a[6];
@@ -245,14 +246,16 @@ __global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* _
         __syncwarp();
         if (is_head) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) sm.sum[w][lane][k] = r[k];
+            for (int k = 0; k < 8; ++k) sm.sum[w][k][lane] = r[k];
             const int net = chunk_net0[chunk] + __popc(head_mask & ((1u << lane) - 1u));
-            sm.xy[w][lane].x = net_w ? net_w[net] : 1.0; // own position no longer needed
+            sm.x[w][lane] = net_w ? net_w[net] : 1.0; // own position no longer needed
         }
         __syncwarp();
         if (valid) {
-            const double* q = sm.sum[w][head];
-            const double wt = sm.xy[w][head].x;
+            double q[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) q[k] = sm.sum[w][k][head];
+            const double wt = sm.x[w][head];
             const double dmx = (eux * q[0]) * (1.0 + ((x - hix) - q[1]) * inv_gamma);
             const double dnx = (elx * q[2]) * (1.0 - ((x - lox) - q[3]) * inv_gamma);
             const double dmy = (euy * q[4]) * (1.0 + ((y - hiy) - q[5]) * inv_gamma);
@@ -338,20 +341,18 @@ __global__ void __launch_bounds__(kBlock) k_pin_pairs(const int* __restrict__ n_
 // =====================================================================================
 constexpr int kFootCache = 16;
 
-__global__ void __launch_bounds__(kBlock) k_density_scatter(int C, const double2* __restrict__ cell_xy,
-                                                            const double2* __restrict__ cell_wh,
-                                                            const uint8_t* __restrict__ fixed, GridDev g,
-                                                            unsigned long long* __restrict__ acc,
-                                                            const Ctrl* __restrict__ ctrl)
+// Scatter over cells in spatial order (perm, refreshed by sort_cells_spatial): the block's
+// footprints usually cover a small window of bins, which is accumulated in shared memory
+// with shared int64 atomics and flushed once per bin; blocks whose window does not fit
+// fall back to global atomics.  Integer adds commute, so the result is bitwise the same
+// whatever the order or the path.
+constexpr int kWinBins = 4096; // 32 KB of int64 accumulators
+
+__device__ __forceinline__ void scatter_cell(const double2 p, const double2 s, const GridDev& g, int bx0, int bx1,
+                                             int by0, int by1, unsigned long long* base, long long row_stride,
+                                             int col0, int row0)
 {
-    if (ctrl && ctrl->stopped) return;
-    const int c = blockIdx.x * kBlock + threadIdx.x;
-    if (c >= C || fixed[c]) return;
-    const double2 p = cell_xy[c], s = cell_wh[c];
     const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
-    int bx0, bx1, by0, by1;
-    foot_range(xl, xh, g.x0, g.bw, g.inv_bw, g.nx, bx0, bx1);
-    foot_range(yl, yh, g.y0, g.bh, g.inv_bh, g.ny, by0, by1);
     const double area = s.x * s.y;
     const double ilx = 1.0 / s.x, ily = 1.0 / s.y;
     const int nby = min(by1 - by0 + 1, kFoot);
@@ -365,22 +366,83 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter(int C, const double2
     for (int bx = bx0; bx <= bx1; ++bx) {
         double wx, dwx;
         extent_w(xl, xh, g.x0 + (bx + 0.5) * g.bw, g.bw, g.inv_bw, ilx, wx, dwx);
-        if (wx == 0.0) continue; // zero-weight columns add nothing to the occupancy
+        if (wx == 0.0) continue;
         const double aw = area * wx;
-        unsigned long long* row = acc + static_cast<long long>(bx) * g.ny + by0;
+        unsigned long long* row = base + static_cast<long long>(bx - row0) * row_stride + (by0 - col0);
 #pragma unroll
         for (int j = 0; j < kFoot; ++j) {
             if (j >= nby) break;
             const long long q = __double2ll_rn(aw * wyc[j] * g.scale);
             if (q) atomicAdd(row + j, static_cast<unsigned long long>(q));
         }
-        for (int by = by0 + kFoot; by <= by1; ++by) { // footprints wider than kFoot bins
+        for (int by = by0 + kFoot; by <= by1; ++by) {
             double wy, dwy;
             extent_w(yl, yh, g.y0 + (by + 0.5) * g.bh, g.bh, g.inv_bh, ily, wy, dwy);
             const long long q = __double2ll_rn(aw * wy * g.scale);
-            if (q) atomicAdd(acc + static_cast<long long>(bx) * g.ny + by, static_cast<unsigned long long>(q));
+            if (q) atomicAdd(row + (by - by0), static_cast<unsigned long long>(q));
         }
     }
+}
+
+__global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const int* __restrict__ perm,
+                                                                const double2* __restrict__ cell_xy,
+                                                                const double2* __restrict__ cell_wh, GridDev g,
+                                                                unsigned long long* __restrict__ acc,
+                                                                const Ctrl* __restrict__ ctrl)
+{
+    __shared__ unsigned long long win[kWinBins];
+    __shared__ int bb[4];
+    if (ctrl && ctrl->stopped) return;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    const bool valid = i < n_mov;
+    double2 p = make_double2(0, 0), s = make_double2(1, 1);
+    int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+    if (valid) {
+        const int c = perm[i];
+        p = cell_xy[c], s = cell_wh[c];
+        foot_range(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx0, bx1);
+        foot_range(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by0, by1);
+    }
+    if (threadIdx.x == 0) bb[0] = INT_MAX, bb[1] = INT_MIN, bb[2] = INT_MAX, bb[3] = INT_MIN;
+    int a0 = bx0, a1 = bx1, c0 = by0, c1 = by1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 = min(a0, __shfl_xor_sync(0xffffffffu, a0, o)), a1 = max(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+        c0 = min(c0, __shfl_xor_sync(0xffffffffu, c0, o)), c1 = max(c1, __shfl_xor_sync(0xffffffffu, c1, o));
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && a0 <= a1) {
+        atomicMin(&bb[0], a0), atomicMax(&bb[1], a1), atomicMin(&bb[2], c0), atomicMax(&bb[3], c1);
+    }
+    __syncthreads();
+    const int X0 = bb[0], Y0 = bb[2];
+    const long long W = static_cast<long long>(bb[1]) - X0 + 1, H = static_cast<long long>(bb[3]) - Y0 + 1;
+    if (X0 > bb[1]) return; // no movable cell in this block
+    if (W * H <= kWinBins) {
+        for (int k = threadIdx.x; k < W * H; k += kBlock) win[k] = 0ull;
+        __syncthreads();
+        if (valid) scatter_cell(p, s, g, bx0, bx1, by0, by1, win, H, Y0, X0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < W * H; k += kBlock) {
+            const unsigned long long v = win[k];
+            if (v) atomicAdd(&acc[static_cast<long long>(X0 + k / H) * g.ny + (Y0 + k % H)], v);
+        }
+    } else if (valid) {
+        scatter_cell(p, s, g, bx0, bx1, by0, by1, acc, g.ny, 0, 0);
+    }
+}
+
+// Spatial order of the movable cells: key = 8x8-bin tile of the cell's lower-left corner.
+__global__ void k_spatial_keys(int C, const double2* __restrict__ cell_xy, const uint8_t* __restrict__ fixed,
+                               GridDev g, int tiles_y, unsigned* __restrict__ keys, int* __restrict__ vals)
+{
+    const int c = blockIdx.x * kBlock + threadIdx.x;
+    if (c >= C) return;
+    const double2 p = cell_xy[c];
+    const int bx = min(g.nx - 1, max(0, static_cast<int>((p.x - g.x0) * g.inv_bw)));
+    const int by = min(g.ny - 1, max(0, static_cast<int>((p.y - g.y0) * g.inv_bh)));
+    keys[c] = fixed[c] ? 0xFFFFFFFFu : static_cast<unsigned>((bx >> 3) * tiles_y + (by >> 3));
+    vals[c] = c;
 }
 
 __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g, long long* __restrict__ acc,
@@ -706,12 +768,37 @@ void launch_pp(tdpg_session* s, int kind, double beta, double* part_pp, int nblk
     launch_pp(s, kind, beta, part_pp, nblk, nullptr);
 }
 
+// Refresh the spatial permutation of the movable cells (radix sort by 8x8-bin tile).
+void sort_cells_spatial(tdpg_session* s)
+{
+    Grid& gr = s->grid;
+    const int C = s->C;
+    if (C == 0) return;
+    gr.perm.reserve(C), gr.perm_keys.reserve(2 * static_cast<size_t>(C)), gr.perm_tmp.reserve(C);
+    const GridDev g = grid_dev(s);
+    const int tiles_y = (g.ny + 7) / 8, tiles_x = (g.nx + 7) / 8;
+    unsigned* k0 = gr.perm_keys.p;
+    unsigned* k1 = gr.perm_keys.p + C;
+    k_spatial_keys<<<blocks_for(C, kBlock), kBlock, 0, s->st>>>(C, s->cell_xy, s->cell_fixed, g, tiles_y, k0,
+                                                                gr.perm_tmp);
+    CK_LAUNCH();
+    int bits = 1;
+    while ((1ll << bits) < static_cast<long long>(tiles_x) * tiles_y + 1) ++bits;
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0, k1, gr.perm_tmp.p, gr.perm.p, C, 0, 32, s->st);
+    void* tmp = cub_scratch(s, bytes);
+    // fixed cells carry key 0xFFFFFFFF: sort all 32 bits only when any exist
+    CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, gr.perm_tmp.p, gr.perm.p, C, 0,
+                                       gr.has_fixed ? 32 : bits, s->st));
+}
+
+void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl);
+
 void launch_density(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl)
 {
     const GridDev g = grid_dev(s);
-    k_density_scatter<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(
-        s->C, s->cell_xy, s->cell_wh, s->cell_fixed, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
-    CK_LAUNCH();
+    if (!ctrl) sort_cells_spatial(s); // one-off evaluations sort first; the loop sorts on its own schedule
+    launch_density_scatter_ctrl(s, ctrl);
     k_density_bins<<<nblk, kBlock, 0, s->st>>>(s->grid.bins(), g, s->grid.acc, s->grid.has_fixed ? s->grid.base.p : nullptr,
                                                s->grid.excess, part_d, ctrl);
     CK_LAUNCH();
@@ -722,8 +809,10 @@ void launch_density(tdpg_session* s, double* part_d, int nblk) { launch_density(
 void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl)
 {
     const GridDev g = grid_dev(s);
-    k_density_scatter<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(
-        s->C, s->cell_xy, s->cell_wh, s->cell_fixed, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
+    const int n_mov = s->grid.n_movable;
+    if (n_mov == 0) return;
+    k_density_scatter_win<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(
+        n_mov, s->grid.perm, s->cell_xy, s->cell_wh, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
     CK_LAUNCH();
 }
 

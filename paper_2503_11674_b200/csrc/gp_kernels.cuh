@@ -89,7 +89,7 @@ __device__ __forceinline__ void extent_w(double lo, double hi, double c, double 
     dw = (bspline2(uh) - bspline2(ul)) * inv_len;
 }
 
-constexpr int kFoot = 16; // footprint bins per dimension kept in registers/local memory
+constexpr int kFoot = 8; // footprint bins per dimension kept in registers (wider footprints loop)
 
 // Footprint bin range (density.cpp:109-112) with reciprocal pitch; bins at the range ends
 // carry zero weight, so a one-bin difference from the division form changes nothing.

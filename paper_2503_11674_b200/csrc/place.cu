@@ -35,6 +35,7 @@ struct Engine {
     int launched = 0, refreshes = 0;
     long long kernel_launches = 0;
     int kernels_per_iter = 6;
+    int sort_every = 2; // iterations between spatial re-sorts of the cells
     double last_refresh_ms = 0, total_refresh_ms = 0;
     ~Engine()
     {
@@ -214,6 +215,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->nb_wa = wa_blocks(s), E->nb_pp = pp_blocks(s), E->nb_d = bins_blocks(s);
     E->part.alloc(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
+    sort_cells_spatial(s); // allocates the permutation before the graph captures its pointer
     delete s->eng;
     s->eng = E.release();
     capture_iteration(s, *s->eng);
@@ -278,6 +280,10 @@ int engine_run(tdpg_session* s, int n)
                 E.launched = E.cfg.max_iters; // loop ended (stop_overflow)
                 break;
             }
+        if (it % E.sort_every == 0) {
+            sort_cells_spatial(s); // refresh the scatter's spatial cell order
+            E.kernel_launches += 1;
+        }
         CK(cudaGraphLaunch(E.gexec, s->st));
         E.kernel_launches += E.kernels_per_iter;
         ++E.launched;
@@ -359,6 +365,7 @@ int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_
         CK(cudaEventRecord(ev[1], s->st));
         launch_pp_ctrl(s, E.cfg.pp_loss, E.cfg.beta, part_pp, E.nb_pp, E.ctrl);
         CK(cudaEventRecord(ev[2], s->st));
+        if (r % E.sort_every == 0) sort_cells_spatial(s);
         launch_density_scatter_ctrl(s, E.ctrl);
         CK(cudaEventRecord(ev[3], s->st));
         launch_density_bins_ctrl(s, part_d, E.nb_d, E.ctrl);

@@ -102,6 +102,8 @@ void ensure_grid(tdpg_session* s, int nx, int ny, double td)
     }
     g.total_movable = mov;
     g.has_fixed = fixed;
+    g.n_movable = 0;
+    for (int c = 0; c < s->C; ++c) g.n_movable += s->h_cell_fixed[c] ? 0 : 1;
     // Fixed point: every bin's movable occupancy is <= total area, keep 2 bits of headroom.
     int ex = 0;
     std::frexp(std::max(all, 1e-300), &ex);
