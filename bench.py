@@ -297,6 +297,7 @@ def run_ours(args):
     value = world * args.steps / (dev_ms_max / 1000.0)
     launches = st1["kernel_launches"] - st0["kernel_launches"]
     refreshes = st1["refreshes"] - st0["refreshes"]
+    refresh_ms = st1["refresh_ms"] - st0["refresh_ms"]
 
     # per-kernel profile of loop iterations (roofline of the dominant kernel)
     prof = s.profile_iteration(5)
@@ -346,7 +347,8 @@ def run_ours(args):
                    "cells": d.n_cells, "pins": d.n_pins, "nets": d.n_nets, "net_pins": d.n_net_pins,
                    "endpoints": int(d.endpoints.size), "grid": args.grid, "m": args.m,
                    "l2": "working set per iteration > L2 (positions+netlist+gradients+grid ~ 2x 126 MB)",
-                   "parallelism": "replicas only" if world > 1 else "single GPU", "refreshes_timed": refreshes},
+                   "parallelism": "replicas only" if world > 1 else "single GPU", "refreshes_timed": refreshes,
+                   "refresh_ms_timed": round(refresh_ms, 3), "ledger_pairs_end": st1["ledger_pairs"]},
         "e2e": {"value": round(e2e_val, 3), "unit": "iters/s", "h2d_bytes_per_step": 16 * C,
                 "d2h_bytes_per_step": 16 * C + 88, "path": "tdpg_step_host (C-ABI, pinned host positions)"},
         "gpu_launches": int(launches),

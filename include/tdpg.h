@@ -190,6 +190,8 @@ int tdpg_engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos
 /* Run n GP iterations (timing refresh per schedule) fully on device; optional device time. */
 int tdpg_iterate_dev(tdpg_session* s, int32_t n_iters, double* device_ms);
 int tdpg_engine_stats(tdpg_session* s, int32_t* iter, int32_t* refreshes, int64_t* launches);
+/* Device time spent in timing refreshes so far (CUDA events), the last one, and the ledger size. */
+int tdpg_engine_times(tdpg_session* s, double* refresh_ms_total, double* last_refresh_ms, int64_t* ledger_pairs);
 /* One iteration through host buffers (positions in, positions + trace row out) — the e2e path. */
 int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_trace_row* row);
 /* Per-kernel device time (ms) of one iteration of each kind, measured with events. */

@@ -10,6 +10,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <random>
 
 #include "gp_kernels.cuh"
@@ -215,6 +216,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->nb_wa = wa_blocks(s), E->nb_pp = pp_blocks(s), E->nb_d = bins_blocks(s);
     E->part.alloc(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
+    if (const char* se = std::getenv("TDPG_SORT_EVERY")) E->sort_every = std::max(1, std::atoi(se));
     sort_cells_spatial(s); // allocates the permutation before the graph captures its pointer
     delete s->eng;
     s->eng = E.release();
@@ -428,6 +430,16 @@ int tdpg_engine_stats(tdpg_session* s, int32_t* iter, int32_t* refreshes, int64_
     if (iter) *iter = s->eng->launched;
     if (refreshes) *refreshes = s->eng->refreshes;
     if (launches) *launches = s->eng->kernel_launches;
+    API_END
+}
+
+int tdpg_engine_times(tdpg_session* s, double* refresh_ms_total, double* last_refresh_ms, int64_t* ledger_pairs)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised");
+    if (refresh_ms_total) *refresh_ms_total = s->eng->total_refresh_ms;
+    if (last_refresh_ms) *last_refresh_ms = s->eng->last_refresh_ms;
+    if (ledger_pairs) *ledger_pairs = s->Q;
     API_END
 }
 

@@ -92,6 +92,7 @@ _SIGS = {
     "tdpg_iterate_dev": (C.c_int, [_P, C.c_int32, _F64P]),
     "tdpg_engine_stats": (C.c_int, [_P, _I32P, _I32P, _I64P]),
     "tdpg_step_host": (C.c_int, [_P, _P, _P, _P]),
+    "tdpg_engine_times": (C.c_int, [_P, _F64P, _F64P, _I64P]),
     "tdpg_profile_iteration": (C.c_int, [_P, C.c_int32, _F64P, C.c_int32, C.c_char_p, C.c_int32]),
     "tdpg_generate": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
                                 C.c_double, C.c_int32, C.POINTER(_P)]),
@@ -311,7 +312,10 @@ class Session:
     def engine_stats(self):
         it, rf, ln = C.c_int32(), C.c_int32(), C.c_int64()
         _check(self.lib.tdpg_engine_stats(self.h, C.byref(it), C.byref(rf), C.byref(ln)))
-        return dict(iterations=it.value, refreshes=rf.value, kernel_launches=ln.value)
+        tot, last, q = C.c_double(), C.c_double(), C.c_int64()
+        _check(self.lib.tdpg_engine_times(self.h, C.byref(tot), C.byref(last), C.byref(q)))
+        return dict(iterations=it.value, refreshes=rf.value, kernel_launches=ln.value, refresh_ms=tot.value,
+                    last_refresh_ms=last.value, ledger_pairs=q.value)
 
     def profile_iteration(self, reps=5):
         n = 16
