@@ -90,10 +90,10 @@ struct tdpg_session {
     tdpg::DBuf<double> cell_delay, pin_cap;
     tdpg::DBuf<uint8_t> cell_fixed, pin_dir, is_source, is_endpoint;
     tdpg::DBuf<int> pin_cell, net_start, net_pins, e_cell, pin_entry, cell_ent_start, cell_ent;
-    // WA warp chunks: whole nets packed into <= 32 entries; per entry (pos in net << 8 | net size)
-    tdpg::DBuf<int> chunk_e0, chunk_net0, big_nets;
-    tdpg::DBuf<uint16_t> e_meta;
-    int n_chunks = 0, n_big = 0;
+    // WA size classes: nets sorted by pin count, per block (pin count, first, count)
+    tdpg::DBuf<int> net_by_size;
+    tdpg::DBuf<int4> wa_blk;
+    int n_wa_blocks = 0;
 
     // device timing graph
     tdpg::DBuf<int> lvl_pins, in_start, in_from, out_start, out_to, ep_sorted;

@@ -17,37 +17,6 @@ int api_fail(int kind, const std::string& msg);
 // each pin is on <= 1 net, so pin_grad[pin] = 0 + w * g), and per-block partial sums of
 // w_e * WA_e and HPWL_e.
 // =====================================================================================
-template <int K>
-__device__ __forceinline__ double wa_dim_reg(int n, const double (&x)[K], double gamma, double (&g)[K])
-{
-    double hi = x[0], lo = x[0];
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-        if (i < n) hi = smax(hi, x[i]), lo = smin(lo, x[i]);
-    double eu[K], el[K];
-    double s_max = 0.0, t_max = 0.0, s_min = 0.0, t_min = 0.0;
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-        if (i < n) {
-            eu[i] = exp((x[i] - hi) / gamma);
-            s_max += eu[i];
-            t_max += (x[i] - hi) * eu[i];
-            el[i] = exp(-(x[i] - lo) / gamma);
-            s_min += el[i];
-            t_min += (x[i] - lo) * el[i];
-        }
-    const double max_term = t_max / s_max;
-    const double min_term = t_min / s_min;
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-        if (i < n) {
-            const double d_max = (eu[i] / s_max) * (1.0 + ((x[i] - hi) - max_term) / gamma);
-            const double d_min = (el[i] / s_min) * (1.0 - ((x[i] - lo) - min_term) / gamma);
-            g[i] = d_max - d_min;
-        }
-    return (hi - lo) + (max_term - min_term);
-}
-
 // Large nets: three passes over the pins, exps recomputed in the gradient pass like the reference.
 __device__ double wa_dim_mem(int s0, int n, int axis, const int* __restrict__ e_cell,
                              const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
@@ -89,178 +58,109 @@ __device__ double wa_dim_mem(int s0, int n, int axis, const int* __restrict__ e_
     return (hi - lo) + (max_term - min_term);
 }
 
-// Thread-per-net WA for the nets the chunked kernel does not take (> 32 pins); net_list
-// selects them (null = every net).
-__global__ void __launch_bounds__(kBlock) k_wirelength(int N, const int* __restrict__ net_list,
-                                                       const int* __restrict__ net_start,
-                                                       const int* __restrict__ e_cell,
-                                                       const double2* __restrict__ e_off,
-                                                       const double2* __restrict__ cell_xy,
-                                                       const double2* __restrict__ anchor,
-                                                       const double* __restrict__ net_w, double gamma,
-                                                       double2* __restrict__ grad_e, double* __restrict__ part_wl,
-                                                       double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
+// =====================================================================================
+// WA wirelength, size-classed (the fast path).  Nets are sorted once by pin count; every
+// block holds nets of one pin count N (2..kWaMaxN), so one thread per net runs a fully
+// unrolled body with N known at compile time: pins in registers, no divergence, the
+// max/min and the four exponential sums accumulated in the reference's pin order
+// (wirelength.cpp:15-34), the 4 exps per pin computed once and reused for the gradient.
+// Divisions by gamma and by the per-net sums become multiplications by reciprocals.
+// Blocks with N == 0 take the nets outside the classes (more pins) through the generic
+// three-pass code (wa_dim_mem).
+// =====================================================================================
+template <int N>
+__device__ __forceinline__ void wa_axis(const double (&x)[N], double inv_gamma, double (&g)[N], double& value,
+                                        double& extent)
 {
-    __shared__ double sh[kBlock / 32];
-    if (ctrl && ctrl->stopped) return;
-    const int i_net = blockIdx.x * kBlock + threadIdx.x;
-    double wl = 0.0, hp = 0.0;
-    if (i_net < N) {
-        const int e = net_list ? net_list[i_net] : i_net;
-        const int s0 = net_start[e], n = net_start[e + 1] - s0;
-        const double w = net_w ? net_w[e] : 1.0;
-        if (n < 2) {
-            for (int i = 0; i < n; ++i) grad_e[s0 + i] = make_double2(0.0, 0.0);
-        } else if (n <= kWaRegPins) {
-            double x[kWaRegPins], y[kWaRegPins], gx[kWaRegPins], gy[kWaRegPins];
+    double hi = x[0], lo = x[0];
 #pragma unroll
-            for (int i = 0; i < kWaRegPins; ++i) {
-                if (i < n) {
-                    const double2 p = entry_pos(e_cell[s0 + i], e_off[s0 + i], cell_xy, anchor);
-                    x[i] = p.x, y[i] = p.y;
-                } else {
-                    x[i] = 0.0, y[i] = 0.0;
-                }
-            }
-            const double vx = wa_dim_reg<kWaRegPins>(n, x, gamma, gx);
-            const double vy = wa_dim_reg<kWaRegPins>(n, y, gamma, gy);
-            double xl = x[0], xh = x[0], yl = y[0], yh = y[0];
+    for (int i = 0; i < N; ++i) hi = smax(hi, x[i]), lo = smin(lo, x[i]);
+    double eu[N], el[N];
+    double s_max = 0.0, t_max = 0.0, s_min = 0.0, t_min = 0.0;
 #pragma unroll
-            for (int i = 0; i < kWaRegPins; ++i)
-                if (i < n) {
-                    xl = smin(xl, x[i]), xh = smax(xh, x[i]), yl = smin(yl, y[i]), yh = smax(yh, y[i]);
-                    grad_e[s0 + i] = make_double2(w * gx[i], w * gy[i]);
-                }
-            wl = w * (vx + vy);
-            hp = (xh - xl) + (yh - yl);
-        } else {
-            double hx, hy;
-            const double vx = wa_dim_mem(s0, n, 0, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hx);
-            const double vy = wa_dim_mem(s0, n, 1, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hy);
-            wl = w * (vx + vy);
-            hp = hx + hy;
-        }
+    for (int i = 0; i < N; ++i) {
+        eu[i] = exp((x[i] - hi) * inv_gamma);
+        el[i] = exp(-(x[i] - lo) * inv_gamma);
     }
-    const double bw = block_sum<kBlock>(wl, sh);
-    const double bh = block_sum<kBlock>(hp, sh);
-    if (threadIdx.x == 0) part_wl[blockIdx.x] = bw, part_hp[blockIdx.x] = bh;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        s_max += eu[i];
+        t_max += (x[i] - hi) * eu[i];
+        s_min += el[i];
+        t_min += (x[i] - lo) * el[i];
+    }
+    const double is_max = 1.0 / s_max, is_min = 1.0 / s_min;
+    const double max_term = t_max * is_max, min_term = t_min * is_min;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double d_max = (eu[i] * is_max) * (1.0 + ((x[i] - hi) - max_term) * inv_gamma);
+        const double d_min = (el[i] * is_min) * (1.0 - ((x[i] - lo) - min_term) * inv_gamma);
+        g[i] = d_max - d_min;
+    }
+    value = (hi - lo) + (max_term - min_term);
+    extent = hi - lo;
 }
 
-// =====================================================================================
-// WA wirelength, warp-chunked (the fast path for nets of <= 32 pins).
-// Nets are packed, whole and in order, into chunks of <= 32 net-pin entries; one warp
-// owns a chunk and one lane one entry.  Lanes load their entry (coalesced), then one
-// head lane per net walks the net's pins in the reference order for the max/min and the
-// four exponential sums (wirelength.cpp:15-34), so only per-net work is sequential and
-// warp divergence is bounded by the largest net in the chunk.  The 4 exps per pin are
-// computed once and reused for the gradient; divisions by gamma and by the sums become
-// multiplications by reciprocals computed once per kernel / per net.
-// =====================================================================================
-constexpr int kWaWarps = kBlock / 32;
-
-struct WaSmem { // [k][lane] layout: head lanes walking their net read consecutive words
-    double x[kWaWarps][32], y[kWaWarps][32];
-    double sum[kWaWarps][8][32]; // per lane summands; head lanes overwrite with per-net results
-};
-
-__global__ void __launch_bounds__(kBlock) k_wa_chunks(int n_chunks, const int* __restrict__ chunk_e0,
-                                                      const int* __restrict__ chunk_net0,
-                                                      const uint16_t* __restrict__ e_meta,
-                                                      const int* __restrict__ e_cell,
-                                                      const double2* __restrict__ e_off,
-                                                      const double2* __restrict__ cell_xy,
-                                                      const double2* __restrict__ anchor,
-                                                      const double* __restrict__ net_w, double gamma,
-                                                      double inv_gamma, double2* __restrict__ grad_e,
-                                                      double* __restrict__ part_wl, double* __restrict__ part_hp,
-                                                      const Ctrl* __restrict__ ctrl)
+template <int N>
+__device__ __forceinline__ void wa_net(int s0, double w, const int* __restrict__ e_cell,
+                                       const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
+                                       const double2* __restrict__ anchor, double inv_gamma,
+                                       double2* __restrict__ grad_e, double& wl, double& hp)
 {
-    __shared__ WaSmem sm;
+    double x[N], y[N], gx[N], gy[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double2 p = entry_pos(e_cell[s0 + i], e_off[s0 + i], cell_xy, anchor);
+        x[i] = p.x, y[i] = p.y;
+    }
+    double vx, vy, hx, hy;
+    wa_axis<N>(x, inv_gamma, gx, vx, hx);
+    wa_axis<N>(y, inv_gamma, gy, vy, hy);
+#pragma unroll
+    for (int i = 0; i < N; ++i) grad_e[s0 + i] = make_double2(w * gx[i], w * gy[i]);
+    wl = w * (vx + vy);
+    hp = hx + hy;
+}
+
+constexpr int kWaMaxN = 8;
+
+__global__ void __launch_bounds__(kBlock) k_wa_sized(const int4* __restrict__ blk, const int* __restrict__ net_by_size,
+                                                     const int* __restrict__ net_start, const int* __restrict__ e_cell,
+                                                     const double2* __restrict__ e_off,
+                                                     const double2* __restrict__ cell_xy,
+                                                     const double2* __restrict__ anchor,
+                                                     const double* __restrict__ net_w, double gamma, double inv_gamma,
+                                                     double2* __restrict__ grad_e, double* __restrict__ part_wl,
+                                                     double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
+{
     __shared__ double sh[kBlock / 32];
     if (ctrl && ctrl->stopped) return;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int chunk = blockIdx.x * kWaWarps + w;
+    const int4 b = blk[blockIdx.x]; // (pin count or 0, first index in net_by_size, count, -)
     double wl = 0.0, hp = 0.0;
-    if (chunk < n_chunks) {
-        const int e0 = chunk_e0[2 * chunk], e1 = chunk_e0[2 * chunk + 1];
-        const int e = e0 + lane;
-        const bool valid = e < e1;
-        int pos = 0, n = 0;
-        double x = 0.0, y = 0.0;
-        if (valid) {
-            const uint16_t m = e_meta[e];
-            pos = m >> 8, n = m & 0xFF;
-            const double2 p = entry_pos(e_cell[e], e_off[e], cell_xy, anchor);
-            x = p.x, y = p.y;
-            sm.x[w][lane] = x, sm.y[w][lane] = y;
-        }
-        const int head = lane - pos;
-        const bool is_head = valid && pos == 0;
-        const unsigned head_mask = __ballot_sync(0xffffffffu, is_head);
-        __syncwarp();
-        // head lanes: hi/lo per dimension in pin order (wirelength.cpp:15-20)
-        double hix = 0, lox = 0, hiy = 0, loy = 0;
-        if (is_head) {
-            hix = lox = x, hiy = loy = y;
-            for (int i = 1; i < n; ++i) {
-                const double qx = sm.x[w][lane + i], qy = sm.y[w][lane + i];
-                hix = smax(hix, qx), lox = smin(lox, qx), hiy = smax(hiy, qy), loy = smin(loy, qy);
+    if (static_cast<int>(threadIdx.x) < b.z) {
+        const int net = net_by_size[b.y + threadIdx.x];
+        const int s0 = net_start[net];
+        const double w = net_w ? net_w[net] : 1.0;
+        switch (b.x) {
+        case 2: wa_net<2>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
+        case 3: wa_net<3>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
+        case 4: wa_net<4>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
+        case 5: wa_net<5>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
+        case 6: wa_net<6>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
+        case 7: wa_net<7>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
+        case 8: wa_net<8>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
+        default: {
+            const int n = net_start[net + 1] - s0;
+            if (n < 2) {
+                for (int i = 0; i < n; ++i) grad_e[s0 + i] = make_double2(0.0, 0.0);
+            } else {
+                double hx, hy;
+                const double vx = wa_dim_mem(s0, n, 0, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hx);
+                const double vy = wa_dim_mem(s0, n, 1, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hy);
+                wl = w * (vx + vy);
+                hp = hx + hy;
             }
-            sm.sum[w][0][lane] = hix, sm.sum[w][1][lane] = lox, sm.sum[w][2][lane] = hiy, sm.sum[w][3][lane] = loy;
         }
-        __syncwarp();
-        if (valid && !is_head) {
-            hix = sm.sum[w][0][head], lox = sm.sum[w][1][head], hiy = sm.sum[w][2][head], loy = sm.sum[w][3][head];
-        }
-        __syncwarp();
-        // per pin: the four anchored exponentials (wirelength.cpp:26-31)
-        double eux = 0, elx = 0, euy = 0, ely = 0;
-        if (valid) {
-            eux = exp((x - hix) * inv_gamma);
-            elx = exp(-(x - lox) * inv_gamma);
-            euy = exp((y - hiy) * inv_gamma);
-            ely = exp(-(y - loy) * inv_gamma);
-            sm.sum[w][0][lane] = eux, sm.sum[w][1][lane] = (x - hix) * eux;
-            sm.sum[w][2][lane] = elx, sm.sum[w][3][lane] = (x - lox) * elx;
-            sm.sum[w][4][lane] = euy, sm.sum[w][5][lane] = (y - hiy) * euy;
-            sm.sum[w][6][lane] = ely, sm.sum[w][7][lane] = (y - loy) * ely;
-        }
-        __syncwarp();
-        double r[8];
-        if (is_head) {
-            double a[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) a[k] = 0.0;
-            for (int i = 0; i < n; ++i) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) a[k] += sm.sum[w][k][lane + i];
-            }
-            const double isx = 1.0 / a[0], inx = 1.0 / a[2], isy = 1.0 / a[4], iny = 1.0 / a[6];
-            const double mtx = a[1] / a[0], ntx = a[3] / a[2], mty = a[5] / a[4], nty = a[7] / a[6];
-            const int net = chunk_net0[chunk] + __popc(head_mask & ((1u << lane) - 1u));
-            const double wt = net_w ? net_w[net] : 1.0;
-            wl = wt * (((hix - lox) + (mtx - ntx)) + ((hiy - loy) + (mty - nty)));
-            hp = (hix - lox) + (hiy - loy);
-            r[0] = isx, r[1] = mtx, r[2] = inx, r[3] = ntx, r[4] = isy, r[5] = mty, r[6] = iny, r[7] = nty;
-        }
-        __syncwarp();
-        if (is_head) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) sm.sum[w][k][lane] = r[k];
-            const int net = chunk_net0[chunk] + __popc(head_mask & ((1u << lane) - 1u));
-            sm.x[w][lane] = net_w ? net_w[net] : 1.0; // own position no longer needed
-        }
-        __syncwarp();
-        if (valid) {
-            double q[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) q[k] = sm.sum[w][k][head];
-            const double wt = sm.x[w][head];
-            const double dmx = (eux * q[0]) * (1.0 + ((x - hix) - q[1]) * inv_gamma);
-            const double dnx = (elx * q[2]) * (1.0 - ((x - lox) - q[3]) * inv_gamma);
-            const double dmy = (euy * q[4]) * (1.0 + ((y - hiy) - q[5]) * inv_gamma);
-            const double dny = (ely * q[6]) * (1.0 - ((y - loy) - q[7]) * inv_gamma);
-            grad_e[e] = make_double2(wt * (dmx - dnx), wt * (dmy - dny));
         }
     }
     const double bw = block_sum<kBlock>(wl, sh);
@@ -559,10 +459,16 @@ __global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __r
     const bool adam = cur->do_adam;
     if (ctrl && !adam && !a.d_cell) return; // stopped: nothing to do
     double gx = 0.0, gy = 0.0;
-    for (int j = a.ent_start[c]; j < a.ent_start[c + 1]; ++j) {
-        const double2 ge = a.grad_e[a.ent[j]];
-        gx += ge.x;
-        gy += ge.y;
+    {   // fold in ascending pin order (placer.cpp:318-325); loads batched 4 at a time
+        const int j0 = a.ent_start[c], j1 = a.ent_start[c + 1];
+        for (int j = j0; j < j1; j += 4) {
+            double2 ge[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ge[k] = (j + k < j1) ? a.grad_e[a.ent[j + k]] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (j + k < j1) gx += ge[k].x, gy += ge[k].y;
+        }
     }
     if (a.fixed[c]) {
         if (a.d_cell) a.d_cell[c] = make_double2(0.0, 0.0);
@@ -582,27 +488,28 @@ __global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __r
         wyc[j] = 0.0, dwyc[j] = 0.0;
         if (j < nby) extent_w(yl, yh, a.g.y0 + (by0 + j + 0.5) * a.g.bh, a.g.bh, a.g.inv_bh, ily, wyc[j], dwyc[j]);
     }
+    // density gradient (density.cpp:148-156), regrouped per bin column:
+    //   dgx = sum_bx area*dwx(bx) * sum_by f(bx,by)*wy(by),  dgy = sum_bx area*wx(bx) * sum_by f*dwy(by)
     double dgx = 0.0, dgy = 0.0;
     for (int bx = bx0; bx <= bx1; ++bx) {
         double wx, dwx;
         extent_w(xl, xh, a.g.x0 + (bx + 0.5) * a.g.bw, a.g.bw, a.g.inv_bw, ilx, wx, dwx);
         if (wx == 0.0 && dwx == 0.0) continue;
-        const double adx = area * dwx, awx = area * wx;
         const double* ex = a.excess + static_cast<long long>(bx) * a.g.ny + by0;
+        double f[kFoot];
 #pragma unroll
-        for (int j = 0; j < kFoot; ++j) {
-            if (j >= nby) break;
-            const double f = 2.0 * ex[j];
-            dgx += f * (adx * wyc[j]);
-            dgy += f * (awx * dwyc[j]);
-        }
+        for (int j = 0; j < kFoot; ++j) f[j] = j < nby ? ex[j] : 0.0;
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int j = 0; j < kFoot; ++j) sx += f[j] * wyc[j], sy += f[j] * dwyc[j];
         for (int by = by0 + kFoot; by <= by1; ++by) {
             double wy, dwy;
             extent_w(yl, yh, a.g.y0 + (by + 0.5) * a.g.bh, a.g.bh, a.g.inv_bh, ily, wy, dwy);
-            const double f = 2.0 * a.excess[static_cast<long long>(bx) * a.g.ny + by];
-            dgx += f * (adx * wy);
-            dgy += f * (awx * dwy);
+            const double fe = a.excess[static_cast<long long>(bx) * a.g.ny + by];
+            sx += fe * wy, sy += fe * dwy;
         }
+        dgx += (area * dwx) * (2.0 * sx);
+        dgy += (area * wx) * (2.0 * sy);
     }
     const double lambda = cur->lambda;
     gx += lambda * dgx;
@@ -646,9 +553,7 @@ GridDev grid_dev(const tdpg_session* s)
                    1.0 / g.bh};
 }
 
-int wa_chunk_blocks(const tdpg_session* s);
-int wa_big_blocks(const tdpg_session* s);
-int wa_blocks(const tdpg_session* s) { return wa_chunk_blocks(s) + wa_big_blocks(s); }
+int wa_blocks(const tdpg_session* s) { return std::max(1, s->n_wa_blocks); }
 int pp_blocks(const tdpg_session*) { return 148 * 4; }
 int bins_blocks(const tdpg_session* s)
 {
@@ -729,25 +634,14 @@ void rebuild_pp_incidence(tdpg_session* s)
     CK_LAUNCH();
 }
 
-// blocks of the chunked WA kernel and of the big-net kernel (partials laid out back to back)
-int wa_chunk_blocks(const tdpg_session* s) { return std::max(1, static_cast<int>(blocks_for(s->n_chunks, kWaWarps))); }
-int wa_big_blocks(const tdpg_session* s) { return s->n_big ? static_cast<int>(blocks_for(s->n_big, kBlock)) : 0; }
-
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk,
                        const Ctrl* ctrl)
 {
-    const int nb1 = wa_chunk_blocks(s), nb2 = wa_big_blocks(s);
     (void)nblk;
-    const double* nw = use_net_w ? s->net_w.p : nullptr;
-    k_wa_chunks<<<nb1, kBlock, 0, s->st>>>(s->n_chunks, s->chunk_e0, s->chunk_net0, s->e_meta, s->e_cell, s->e_off,
-                                           s->cell_xy, s->anchor, nw, gamma, 1.0 / gamma, s->grad_e, part_wl, part_hp,
-                                           ctrl);
+    k_wa_sized<<<s->n_wa_blocks, kBlock, 0, s->st>>>(s->wa_blk, s->net_by_size, s->net_start, s->e_cell, s->e_off,
+                                                     s->cell_xy, s->anchor, use_net_w ? s->net_w.p : nullptr, gamma,
+                                                     1.0 / gamma, s->grad_e, part_wl, part_hp, ctrl);
     CK_LAUNCH();
-    if (nb2) {
-        k_wirelength<<<nb2, kBlock, 0, s->st>>>(s->n_big, s->big_nets, s->net_start, s->e_cell, s->e_off, s->cell_xy,
-                                                s->anchor, nw, gamma, s->grad_e, part_wl + nb1, part_hp + nb1, ctrl);
-        CK_LAUNCH();
-    }
 }
 
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk)

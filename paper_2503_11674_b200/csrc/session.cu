@@ -377,30 +377,22 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         }
     s->e_cell.upload(e_cell, s->st);
     s->e_off.upload(e_off, s->st);
-    {   // warp chunks for the WA kernel: whole nets of <= 32 pins, packed in net order
-        std::vector<int> se, c_net0, big; // se: (start, end) entry range per chunk
-        std::vector<uint16_t> meta(std::max(E, 1), 0);
-        bool open = false;
-        for (int n = 0; n < N; ++n) {
-            const int b = s->h_net_start[n], k = s->h_net_start[n + 1] - b;
-            if (k > 32) {
-                big.push_back(n);
-                open = false;
-                continue;
-            }
-            if (!open || (b + k) - se[se.size() - 2] > 32) {
-                se.push_back(b), se.push_back(b), c_net0.push_back(n);
-                open = true;
-            }
-            se.back() = b + k;
-            for (int i = 0; i < k; ++i) meta[b + i] = static_cast<uint16_t>((i << 8) | k);
-        }
-        s->n_chunks = static_cast<int>(c_net0.size());
-        s->n_big = static_cast<int>(big.size());
-        s->chunk_e0.upload(se.empty() ? std::vector<int>{0, 0} : se, s->st);
-        s->chunk_net0.upload(c_net0.empty() ? std::vector<int>{0} : c_net0, s->st);
-        s->e_meta.upload(meta, s->st);
-        s->big_nets.upload(big.empty() ? std::vector<int>{0} : big, s->st);
+    {   // WA size classes: nets sorted (stably) by pin count; blocks of 256 nets of one count;
+        // counts outside [2, 8] go to class 0 (generic path)
+        constexpr int kMaxN = 8, kB = 256;
+        auto cls = [&](int n) { return (n >= 2 && n <= kMaxN) ? n : 0; };
+        std::vector<int> cnt(kMaxN + 2, 0);
+        for (int n = 0; n < N; ++n) cnt[cls(s->h_net_start[n + 1] - s->h_net_start[n]) + 1]++;
+        for (int k = 0; k <= kMaxN; ++k) cnt[k + 1] += cnt[k];
+        std::vector<int> order(std::max(N, 1)), fill(cnt.begin(), cnt.end() - 1);
+        for (int n = 0; n < N; ++n) order[fill[cls(s->h_net_start[n + 1] - s->h_net_start[n])]++] = n;
+        std::vector<int4> blk;
+        for (int k = 0; k <= kMaxN; ++k)
+            for (int i = cnt[k]; i < cnt[k + 1]; i += kB) blk.push_back(make_int4(k, i, std::min(kB, cnt[k + 1] - i), 0));
+        if (blk.empty()) blk.push_back(make_int4(0, 0, 0, 0));
+        s->n_wa_blocks = static_cast<int>(blk.size());
+        s->net_by_size.upload(order, s->st);
+        s->wa_blk.upload(blk, s->st);
     }
     // Cell pins on no net still take pin-pair gradient (pin_pairs.cpp:31-34 writes any pin):
     // they get extra slots after the E net entries, written only by the pin-pair kernel.
