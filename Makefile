@@ -3,6 +3,7 @@ all: engine oracle
 
 engine:
 	$(MAKE) -C paper_2503_11674_b200/csrc -j8
+	$(MAKE) -C paper_2503_11674_b200/host
 
 oracle:
 	$(MAKE) -C oracle all

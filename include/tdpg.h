@@ -142,6 +142,12 @@ int tdpg_pin_positions(tdpg_session* s, double* pin_xy);          /* [2*n_pins] 
 /* wl = sum_e w_e * WA_e, hpwl exact; pin_grad [2*n_pins] (w_e-scaled) may be NULL. */
 int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* wl, double* hpwl,
                     double* pin_grad);
+/* hpwl_total on caller-provided pin positions ([2*n_pins], wirelength.cpp:74-85). */
+int tdpg_hpwl_pins(tdpg_session* s, const double* pin_xy, double* hpwl);
+/* DesignConstraints::core (the density grid follows it). */
+int tdpg_set_core(tdpg_session* s, const double core[4]);
+/* DesignConstraints timing fields (clock_period, r_unit, c_unit) used by the STA. */
+int tdpg_set_constraints(tdpg_session* s, double clock_period, double r_unit, double c_unit);
 /* DensityGrid(nx, ny, target_density) then evaluate; d_cell [2*n_cells] may be NULL. */
 int tdpg_set_grid(tdpg_session* s, int32_t nx, int32_t ny, double target_density);
 int tdpg_density(tdpg_session* s, double* value, double* overflow, double* d_cell);
@@ -172,12 +178,27 @@ int tdpg_sta(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* 
  * unique_endpoints, unique_pin_pairs; candidates_generated = n_paths. */
 int tdpg_extract_endpoint(tdpg_session* s, int32_t n, int32_t k, int64_t counts[4]);
 int tdpg_paths_get(tdpg_session* s, int32_t* path_start /* [n_paths+1] */, int32_t* pins, double* slack);
+/* Counts of the last extraction (same layout as tdpg_extract_endpoint's counts). */
+int tdpg_paths_counts(tdpg_session* s, int64_t counts[4]);
 /* collect_pin_pairs of the last extraction: number of hits, then fetch */
 int tdpg_paths_hits(tdpg_session* s, int64_t* n_hits, int32_t* a, int32_t* b, double* slack);
+/* STA on caller-provided pin positions ([2*n_pins], e.g. tdp::PinPositions) instead of the
+ * cells' positions; cleared by tdpg_set_positions.  (run_sta takes PinPositions, sta.hpp:50) */
+int tdpg_set_pin_positions(tdpg_session* s, const double* pin_xy);
+/* Download the last STA without recomputing it. */
+int tdpg_sta_fetch(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* arr_known,
+                   uint8_t* req_known, double* tns, double* wns);
+/* PathEnumerator::path_to(pin, rank) (paths.hpp:54), rank 0: *n_pins = 0 when no source reaches pin. */
+int tdpg_path_to(tdpg_session* s, int32_t pin, int32_t rank, int32_t* pins, int32_t cap, int32_t* n_pins,
+                 double* delay);
 /* Device-timed duration (ms) of the last STA / extraction call, CUDA events. */
 int tdpg_last_timing_ms(tdpg_session* s, double* sta_ms, double* extract_ms);
 
 /* ---- the placement loop: run_placement ------------------------------ */
+/* TimingRoundObserver (placer.hpp:134): called after every timing round with the iteration;
+ * tdpg_sta_fetch / tdpg_paths_get / tdpg_paths_hits read that round's annotation and report. */
+typedef void (*tdpg_round_cb)(void* user, int32_t iter);
+int tdpg_set_round_callback(tdpg_session* s, tdpg_round_cb cb, void* user);
 /* pos_explicit [n_cells] (bool) marks cells whose coordinates came from the file;
  * positions are the session's current positions on entry and the result on exit.
  * trace may be NULL; else capacity max_iters rows.  final[3] = tns, wns, hpwl. */

@@ -111,7 +111,8 @@ struct tdpg_session {
     tdpg::DBuf<unsigned long long> lg_new_k;
     tdpg::DBuf<int> lg_nsel;
     double tns = 0, wns = 0;
-    bool sta_valid = false;
+    bool sta_valid = false, ties_resolved = false;
+    bool pin_xy_external = false; // STA uses caller-provided pin positions (tdpg_set_pin_positions)
 
     // GP scratch
     tdpg::DBuf<double2> grad_e, d_cell, adam_m, adam_v;
@@ -146,7 +147,9 @@ struct tdpg_session {
     tdpg::HBuf<long long> h_small;
 
     // placement engine
-    tdpg::Engine* eng = nullptr; // owned; deleted in ~tdpg_session (place.cu)
+    tdpg::Engine* eng = nullptr;
+    tdpg_round_cb round_cb = nullptr; // called after every timing round of tdpg_place
+    void* round_user = nullptr; // owned; deleted in ~tdpg_session (place.cu)
 
     ~tdpg_session();
 };
@@ -173,6 +176,7 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
 // timing.cu
 void run_sta_dev(tdpg_session* s);
 void extract_endpoint_dev(tdpg_session* s, int n);
+void resolve_ties_dev(tdpg_session* s);
 void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool hits_all_violated);
 void net_weights_dev(tdpg_session* s);
 

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstring>
 
 #include "gp_kernels.cuh"
 
@@ -532,6 +533,30 @@ __global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __r
     a.xy[c] = make_double2(x, y);
 }
 
+// hpwl_total on caller-provided pin positions (wirelength.cpp:74-85), one thread per net.
+__global__ void __launch_bounds__(kBlock) k_hpwl_pins(int N, const int* __restrict__ net_start,
+                                                      const int* __restrict__ net_pins,
+                                                      const double2* __restrict__ pin_xy, double* __restrict__ part)
+{
+    __shared__ double sh[kBlock / 32];
+    const int e = blockIdx.x * kBlock + threadIdx.x;
+    double h = 0.0;
+    if (e < N) {
+        const int s0 = net_start[e], s1 = net_start[e + 1];
+        if (s1 - s0 >= 2) {
+            const double2 p0 = pin_xy[net_pins[s0]];
+            double xl = p0.x, xh = p0.x, yl = p0.y, yh = p0.y;
+            for (int j = s0 + 1; j < s1; ++j) {
+                const double2 p = pin_xy[net_pins[j]];
+                xl = smin(xl, p.x), xh = smax(xh, p.x), yl = smin(yl, p.y), yh = smax(yh, p.y);
+            }
+            h = (xh - xl) + (yh - yl);
+        }
+    }
+    h = block_sum<kBlock>(h, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = h;
+}
+
 // Adam on a flat device vector (AdamState::step for the reference-shaped host API).
 __global__ void k_adam_flat(long long n, double* x, const double* g, double* m, double* v, double lr, double b1,
                             double b2, double eps, double c1, double c2)
@@ -910,6 +935,42 @@ int tdpg_objective(tdpg_session* s, double gamma, double lambda, double beta, in
     terms[0] = t.value, terms[1] = t.wl, terms[2] = t.density, terms[3] = t.pp, terms[4] = t.hpwl,
     terms[5] = t.overflow;
     check_finite_terms(t, g, s->C);
+    API_END
+}
+
+int tdpg_hpwl_pins(tdpg_session* s, const double* pin_xy, double* hpwl)
+{
+    API_BEGIN
+    DBuf<double2> pxy(std::max(s->P, 1));
+    pxy.upload(reinterpret_cast<const double2*>(pin_xy), s->P, s->st);
+    const int nb = std::max(1, static_cast<int>(blocks_for(s->N, kBlock)));
+    DBuf<double> part(nb);
+    k_hpwl_pins<<<nb, kBlock, 0, s->st>>>(s->N, s->net_start, s->net_pins, pxy, part);
+    CK_LAUNCH();
+    std::vector<double> h(nb);
+    part.download(h.data(), nb, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    double t = 0.0;
+    for (double x : h) t += x;
+    *hpwl = t;
+    API_END
+}
+
+int tdpg_set_core(tdpg_session* s, const double core[4])
+{
+    API_BEGIN
+    if (std::memcmp(s->core, core, sizeof s->core) != 0) {
+        std::memcpy(s->core, core, sizeof s->core);
+        s->grid.nx = 0; // the grid geometry follows the core; rebuilt by the next tdpg_set_grid
+    }
+    API_END
+}
+
+int tdpg_set_constraints(tdpg_session* s, double clock_period, double r_unit, double c_unit)
+{
+    API_BEGIN
+    if (s->clock != clock_period || s->r_unit != r_unit || s->c_unit != c_unit) s->sta_valid = false;
+    s->clock = clock_period, s->r_unit = r_unit, s->c_unit = c_unit;
     API_END
 }
 

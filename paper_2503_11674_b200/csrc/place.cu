@@ -245,6 +245,7 @@ bool timing_refresh(tdpg_session* s)
         cudaEventDestroy(e0), cudaEventDestroy(e1);
         return false;
     }
+    s->pin_xy_external = false;
     run_sta_dev(s);
     const double row[3] = {1.0, s->tns, s->wns};
     CK(cudaMemcpyAsync(E.timing_row.p, row, sizeof row, cudaMemcpyHostToDevice, s->st));
@@ -254,8 +255,11 @@ bool timing_refresh(tdpg_session* s)
         extract_endpoint_dev(s, 0); // n = number of violated endpoints (placer.cpp:424-428)
         ledger_apply_sorted(s, s->n_hits, s->wns, E.cfg.w0, E.cfg.w1);
         rebuild_pp_incidence(s);
+    } else {
+        s->n_paths = 0, s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0; // empty report
     }
     if (E.cfg.net_weighting) net_weights_dev(s);
+    if (s->round_cb) s->round_cb(s->round_user, E.launched); // TimingRoundObserver (placer.cpp:434)
     // our kernels in this round: pin_xy + 2 per level + slack/final; extraction (slack/final,
     // ties, two backtrace passes, head count), ledger groups, incidence (3), net weights
     E.kernel_launches += 1 + 2LL * s->L + 2 + (s->wns < 0.0 ? 6 + 1 + 3 : 0) + (E.cfg.net_weighting ? 1 : 0);
@@ -311,6 +315,14 @@ using namespace tdpg;
     catch (const std::exception& e) { return ::tdpg::api_fail(TDPG_ERR_INTERNAL, e.what()); }
 
 extern "C" {
+
+int tdpg_set_round_callback(tdpg_session* s, tdpg_round_cb cb, void* user)
+{
+    API_BEGIN
+    s->round_cb = cb;
+    s->round_user = user;
+    API_END
+}
 
 int tdpg_engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit)
 {

@@ -347,9 +347,11 @@ StaArgs sta_args(tdpg_session* s)
 void run_sta_async(tdpg_session* s, double* out3)
 {
     const int P = s->P;
-    k_pin_xy<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor,
-                                                          s->pin_xy);
-    CK_LAUNCH();
+    if (!s->pin_xy_external) { // pin positions from the cells (netlist.cpp:23-32) unless the caller gave them
+        k_pin_xy<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor,
+                                                              s->pin_xy);
+        CK_LAUNCH();
+    }
     CK(cudaMemsetAsync(s->counters.p, 0, sizeof(int) * 4, s->st));
     const StaArgs a = sta_args(s);
     for (int l = 0; l < s->L; ++l) {
@@ -382,6 +384,18 @@ void run_sta_dev(tdpg_session* s)
     CK(cudaStreamSynchronize(s->st));
     s->tns = h[0], s->wns = h[1];
     s->sta_valid = true;
+    s->ties_resolved = false;
+}
+
+// Exact-delay ties of the last STA resolved to the lexicographically smallest path (idempotent).
+void resolve_ties_dev(tdpg_session* s)
+{
+    if (s->ties_resolved) return;
+    const int stride = s->L + 2;
+    s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * stride);
+    k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), s->d_level, s->L, s->tie_scratch, stride);
+    CK_LAUNCH();
+    s->ties_resolved = true;
 }
 
 // report_timing_endpoint(n, k = 1) on the current STA (paths.cpp:167-189).
@@ -414,10 +428,7 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     }
     // ties: resolve before any backtrace
     {
-        const int stride = s->L + 2;
-        s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * stride);
-        k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), s->d_level, s->L, s->tie_scratch, stride);
-        CK_LAUNCH();
+        resolve_ties_dev(s);
         double h[3];
         CK(cudaMemcpyAsync(h, out3, sizeof h, cudaMemcpyDeviceToHost, s->st));
         CK(cudaStreamSynchronize(s->st));
@@ -603,6 +614,13 @@ int tdpg_extract_endpoint(tdpg_session* s, int32_t n, int32_t k, int64_t counts[
     API_END
 }
 
+int tdpg_paths_counts(tdpg_session* s, int64_t counts[4])
+{
+    API_BEGIN
+    counts[0] = s->n_paths, counts[1] = s->n_path_pins, counts[2] = s->n_paths, counts[3] = s->uniq_pairs;
+    API_END
+}
+
 int tdpg_paths_get(tdpg_session* s, int32_t* start, int32_t* pins, double* slack)
 {
     API_BEGIN
@@ -662,6 +680,72 @@ int tdpg_pp_update(tdpg_session* s, int64_t n, const int32_t* a, const int32_t* 
     s->n_hits = 0; // host-provided hits are not an extraction result
     s->n_paths = 0;
     CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_set_pin_positions(tdpg_session* s, const double* pin_xy)
+{
+    API_BEGIN
+    s->pin_xy.upload(reinterpret_cast<const double2*>(pin_xy), s->P, s->st);
+    s->pin_xy_external = true;
+    s->sta_valid = false;
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_sta_fetch(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* ak, uint8_t* rk, double* tns,
+                   double* wns)
+{
+    API_BEGIN
+    if (!s->sta_valid) throw Error(TDPG_ERR_GRAPH, "graph error: no timing annotation (run tdpg_sta first)");
+    const size_t P = static_cast<size_t>(s->P);
+    if (arr) s->arr.download(arr, P, s->st);
+    if (req) s->req.download(req, P, s->st);
+    if (slack) s->slack.download(slack, P, s->st);
+    if (ak) s->ak.download(ak, P, s->st);
+    if (rk) s->rk.download(rk, P, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    if (tns) *tns = s->tns;
+    if (wns) *wns = s->wns;
+    API_END
+}
+
+// PathEnumerator::path_to(pin, rank) for rank 0 (paths.cpp:44-55): the worst source->pin path.
+int tdpg_path_to(tdpg_session* s, int32_t pin, int32_t rank, int32_t* pins, int32_t cap, int32_t* n_pins,
+                 double* delay)
+{
+    API_BEGIN
+    if (pin < 0 || pin >= s->P) throw Error(TDPG_ERR_VALIDATION, "validation error: pin id out of range");
+    if (rank != 0) throw Error(TDPG_ERR_INTERNAL, "path ranks > 0 (k > 1) are not implemented on the device yet");
+    if (!s->sta_valid) run_sta_dev(s);
+    resolve_ties_dev(s);
+    uint8_t known = 0;
+    CK(cudaMemcpyAsync(&known, s->ak.p + pin, 1, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    *n_pins = 0;
+    if (!known) return TDPG_OK; // no source reaches the pin: nullptr in the reference
+    DBuf<int> ep(1), len(1), hops(1), off(1), hoff(1), out(std::max(cap, 1));
+    DBuf<double> sl(1);
+    ep.upload(&pin, 1, s->st);
+    const int z = 0;
+    off.upload(&z, 1, s->st), hoff.upload(&z, 1, s->st);
+    k_bt_count<<<1, kBlock, 0, s->st>>>(1, ep, s->pred, s->pin_dir, len, hops);
+    CK_LAUNCH();
+    int L = 0;
+    len.download(&L, 1, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    if (L > cap) throw Error(TDPG_ERR_VALIDATION, "validation error: path longer than the output buffer");
+    s->hit_key.reserve(L + 1), s->hit_slack.reserve(L + 1), s->hit_idx.reserve(L + 1);
+    k_bt_write<<<1, kBlock, 0, s->st>>>(1, ep, s->pred, s->pin_dir, len, off, hops, hoff, s->arr, s->clock, out, sl,
+                                        s->hit_key, s->hit_slack, s->hit_idx);
+    CK_LAUNCH();
+    out.download(pins, L, s->st);
+    double a = 0.0;
+    CK(cudaMemcpyAsync(&a, s->arr.p + pin, sizeof a, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    *n_pins = L;
+    if (delay) *delay = a;
+    s->n_hits = 0, s->n_paths = 0; // scratch hit buffers were reused
     API_END
 }
 

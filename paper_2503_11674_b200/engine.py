@@ -92,6 +92,14 @@ _SIGS = {
     "tdpg_iterate_dev": (C.c_int, [_P, C.c_int32, _F64P]),
     "tdpg_engine_stats": (C.c_int, [_P, _I32P, _I32P, _I64P]),
     "tdpg_step_host": (C.c_int, [_P, _P, _P, _P]),
+    "tdpg_set_pin_positions": (C.c_int, [_P, _P]),
+    "tdpg_paths_counts": (C.c_int, [_P, _I64P]),
+    "tdpg_set_core": (C.c_int, [_P, _P]),
+    "tdpg_hpwl_pins": (C.c_int, [_P, _P, _F64P]),
+    "tdpg_set_constraints": (C.c_int, [_P, C.c_double, C.c_double, C.c_double]),
+    "tdpg_sta_fetch": (C.c_int, [_P, _P, _P, _P, _P, _P, _F64P, _F64P]),
+    "tdpg_path_to": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int32, _I32P, _F64P]),
+    "tdpg_set_round_callback": (C.c_int, [_P, _P, _P]),
     "tdpg_engine_times": (C.c_int, [_P, _F64P, _F64P, _I64P]),
     "tdpg_profile_iteration": (C.c_int, [_P, C.c_int32, _F64P, C.c_int32, C.c_char_p, C.c_int32]),
     "tdpg_generate": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,

@@ -1,0 +1,705 @@
+// tdp_api.cpp — the reference's tdp:: operator API implemented over the sm_100a engine (include/tdpg.h).
+//
+// A device session is created once per netlist and cached (keyed on the Netlist's address plus a cheap
+// fingerprint), so per-iteration calls such as objective_and_gradient only upload positions.  Exceptions
+// from the C-ABI are re-thrown as the reference's exception classes with the reference's messages.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <memory>
+#include <mutex>
+#include <set>
+
+#include "tdp/tdp_api.hpp"
+#include "tdpg.h"
+
+namespace tdp {
+
+namespace {
+
+std::string strip(const std::string& m, const char* prefix)
+{
+    const std::string p(prefix);
+    return m.compare(0, p.size(), p) == 0 ? m.substr(p.size()) : m;
+}
+
+[[noreturn]] void rethrow(int kind)
+{
+    const std::string m = tdpg_last_error();
+    switch (kind) {
+    case TDPG_ERR_PARSE: throw ParseError(strip(m, "parse error: "));
+    case TDPG_ERR_CYCLE: throw CycleError(strip(m, "validation error: combinational cycle: "));
+    case TDPG_ERR_ENDPOINT: throw EndpointError(strip(m, "validation error: "));
+    case TDPG_ERR_VALIDATION: throw ValidationError(strip(m, "validation error: "));
+    case TDPG_ERR_GRAPH: throw GraphError(strip(m, "graph error: "));
+    case TDPG_ERR_NONFINITE: throw NonFiniteError(strip(m, "non-finite value: "));
+    case TDPG_ERR_INTERNAL: throw std::logic_error(m);
+    default: throw std::runtime_error(m);
+    }
+}
+
+void ck(int rc)
+{
+    if (rc != TDPG_OK) rethrow(rc);
+}
+
+// Flat SoA copy of a Netlist + constraints, owned alongside the session it created.
+struct FlatNetlist {
+    std::vector<double> cw, ch, cd, pt, po, pc;
+    std::vector<uint8_t> cf, pd;
+    std::vector<int32_t> pcell, ns, np, src, ep;
+    std::vector<std::string> names;
+    std::vector<const char*> name_ptrs;
+    tdpg_netlist view{};
+
+    FlatNetlist(const Netlist& nl, const DesignConstraints& c)
+    {
+        const size_t C = nl.cells.size(), P = nl.pins.size();
+        for (const Cell& cell : nl.cells)
+            cw.push_back(cell.width), ch.push_back(cell.height), cd.push_back(cell.delay), cf.push_back(cell.is_fixed);
+        for (const Pin& p : nl.pins) {
+            pcell.push_back(p.cell);
+            pt.push_back(p.terminal_pos.x), pt.push_back(p.terminal_pos.y);
+            po.push_back(p.offset.x), po.push_back(p.offset.y);
+            pd.push_back(p.dir == PinDir::Output ? 1 : 0);
+            pc.push_back(p.load_cap);
+            names.push_back(p.name);
+        }
+        ns.push_back(0);
+        for (const Net& n : nl.nets) {
+            np.push_back(n.driver);
+            for (int s : n.sinks) np.push_back(s);
+            ns.push_back(static_cast<int32_t>(np.size()));
+        }
+        src.assign(nl.sources.begin(), nl.sources.end());
+        ep.assign(nl.endpoints.begin(), nl.endpoints.end());
+        for (const auto& s : names) name_ptrs.push_back(s.c_str());
+        view.n_cells = static_cast<int32_t>(C), view.n_pins = static_cast<int32_t>(P);
+        view.n_nets = static_cast<int32_t>(nl.nets.size());
+        view.n_sources = static_cast<int32_t>(src.size()), view.n_endpoints = static_cast<int32_t>(ep.size());
+        view.cell_w = cw.data(), view.cell_h = ch.data(), view.cell_delay = cd.data(), view.cell_fixed = cf.data();
+        view.pin_cell = pcell.data(), view.pin_term = pt.data(), view.pin_off = po.data(), view.pin_dir = pd.data();
+        view.pin_cap = pc.data(), view.net_start = ns.data(), view.net_pins = np.data(), view.sources = src.data();
+        view.endpoints = ep.data(), view.clock_period = c.clock_period > 0 ? c.clock_period : 1.0;
+        view.r_unit = c.r_unit, view.c_unit = c.c_unit;
+        view.core[0] = c.core.x_lo, view.core[1] = c.core.y_lo, view.core[2] = c.core.x_hi, view.core[3] = c.core.y_hi;
+        view.pin_names = name_ptrs.data();
+    }
+};
+
+struct Sess {
+    std::unique_ptr<FlatNetlist> flat;
+    tdpg_session* s = nullptr;
+    std::vector<std::size_t> fp;
+    ~Sess()
+    {
+        if (s) tdpg_session_destroy(s);
+    }
+};
+
+std::vector<std::size_t> fingerprint(const Netlist& nl)
+{
+    std::vector<std::size_t> f = {nl.cells.size(), nl.pins.size(), nl.nets.size(), nl.sources.size(),
+                                  nl.endpoints.size()};
+    const std::size_t P = nl.pins.size(), N = nl.nets.size();
+    for (std::size_t k = 0; k < 16 && P; ++k) {
+        const Pin& p = nl.pins[k * P / 16];
+        f.push_back(static_cast<std::size_t>(p.cell + 7) * 31 + (p.dir == PinDir::Output));
+    }
+    for (std::size_t k = 0; k < 16 && N; ++k) {
+        const Net& n = nl.nets[k * N / 16];
+        f.push_back(static_cast<std::size_t>(n.driver) * 131 + n.sinks.size());
+    }
+    return f;
+}
+
+std::mutex g_mu;
+std::map<const Netlist*, std::shared_ptr<Sess>> g_cache;
+
+// Device session for this netlist (rebuilt when the netlist or the core changed).
+std::shared_ptr<Sess> session(const Netlist& nl, const DesignConstraints& c)
+{
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto fp = fingerprint(nl);
+    auto it = g_cache.find(&nl);
+    if (it != g_cache.end() && it->second->fp == fp) {
+        ck(tdpg_set_constraints(it->second->s, c.clock_period > 0 ? c.clock_period : 1.0, c.r_unit, c.c_unit));
+        return it->second;
+    }
+    auto S = std::make_shared<Sess>();
+    S->flat = std::make_unique<FlatNetlist>(nl, c);
+    S->fp = std::move(fp);
+    ck(tdpg_session_create(&S->flat->view, &S->s));
+    if (g_cache.size() > 64) g_cache.clear();
+    g_cache[&nl] = S;
+    return S;
+}
+
+// A design core for netlist-only calls: any nondegenerate rect works for STA/WA/PP.
+DesignConstraints core_only(const Rect& core)
+{
+    DesignConstraints c;
+    c.core = core.nondegenerate() ? core : Rect{0.0, 0.0, 1.0, 1.0};
+    c.r_unit = c.c_unit = 1.0;
+    c.clock_period = 1.0;
+    return c;
+}
+
+std::vector<double> flat_points(const std::vector<Point>& p)
+{
+    std::vector<double> v(2 * p.size());
+    for (std::size_t i = 0; i < p.size(); ++i) v[2 * i] = p[i].x, v[2 * i + 1] = p[i].y;
+    return v;
+}
+
+std::vector<Point> points(const std::vector<double>& v)
+{
+    std::vector<Point> p(v.size() / 2);
+    for (std::size_t i = 0; i < p.size(); ++i) p[i] = Point{v[2 * i], v[2 * i + 1]};
+    return p;
+}
+
+// One-net scratch netlist of terminal pins at the given positions (pin 0 drives the rest).
+struct PointNet {
+    Netlist nl;
+    explicit PointNet(std::span<const Point> pts)
+    {
+        for (std::size_t i = 0; i < pts.size(); ++i) {
+            Pin p;
+            p.name = "t" + std::to_string(i);
+            p.terminal_pos = pts[i];
+            p.dir = i == 0 ? PinDir::Output : PinDir::Input;
+            nl.pins.push_back(p);
+        }
+        if (pts.size() >= 2) {
+            Net n;
+            n.name = "n";
+            n.driver = 0;
+            for (std::size_t i = 1; i < pts.size(); ++i) n.sinks.push_back(static_cast<int>(i));
+            nl.nets.push_back(n);
+        }
+        nl.finalize();
+    }
+};
+
+void set_core(tdpg_session* s, const Rect& r)
+{
+    const double core[4] = {r.x_lo, r.y_lo, r.x_hi, r.y_hi};
+    ck(tdpg_set_core(s, core));
+}
+
+void ledger_upload(tdpg_session* s, const PinPairWeights& w)
+{
+    std::vector<int32_t> a, b;
+    std::vector<double> ww;
+    a.reserve(w.size()), b.reserve(w.size()), ww.reserve(w.size());
+    for (const auto& [pr, x] : w) a.push_back(pr.first), b.push_back(pr.second), ww.push_back(x);
+    ck(tdpg_pp_set(s, static_cast<int64_t>(a.size()), a.data(), b.data(), ww.data()));
+}
+
+PinPairWeights ledger_download(tdpg_session* s)
+{
+    int64_t q = 0;
+    ck(tdpg_pp_size(s, &q));
+    std::vector<int32_t> a(q), b(q);
+    std::vector<double> w(q);
+    if (q) ck(tdpg_pp_get(s, a.data(), b.data(), w.data()));
+    PinPairWeights out;
+    for (int64_t i = 0; i < q; ++i) out.emplace(std::make_pair(a[i], b[i]), w[i]);
+    return out;
+}
+
+TimingAnnotation fetch_annotation(tdpg_session* s, const Netlist& nl)
+{
+    const std::size_t P = nl.pins.size();
+    TimingAnnotation ann;
+    ann.arr.resize(P), ann.req.resize(P), ann.slack.resize(P);
+    std::vector<uint8_t> ak(P), rk(P);
+    ck(tdpg_sta_fetch(s, ann.arr.data(), ann.req.data(), ann.slack.data(), ak.data(), rk.data(), &ann.tns, &ann.wns));
+    ann.arr_known.assign(ak.begin(), ak.end());
+    ann.req_known.assign(rk.begin(), rk.end());
+    for (int e : nl.endpoints) ann.endpoint_slacks.emplace_back(e, ann.slack[static_cast<std::size_t>(e)]);
+    return ann;
+}
+
+ExtractionReport fetch_report(tdpg_session* s, const Netlist& nl, int n, int k, const int64_t counts[4], double ms)
+{
+    ExtractionReport r;
+    r.policy = "endpoint", r.n = n, r.k = k;
+    const int np = static_cast<int>(counts[0]);
+    std::vector<int32_t> start(np + 1), pins(std::max<int64_t>(counts[1], 1));
+    std::vector<double> slack(std::max(np, 1));
+    ck(tdpg_paths_get(s, start.data(), pins.data(), slack.data()));
+    for (int i = 0; i < np; ++i)
+        r.paths.push_back(CriticalPath{std::vector<int>(pins.begin() + start[i], pins.begin() + start[i + 1]), slack[i]});
+    r.unique_endpoints = static_cast<int>(counts[2]);
+    r.unique_pin_pairs = static_cast<int>(counts[3]);
+    r.candidates_generated = np;
+    r.elapsed_ms = ms;
+    (void)nl;
+    return r;
+}
+
+// STA on the device at the given pin positions.
+std::shared_ptr<Sess> sta_at(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                             const DesignConstraints& c)
+{
+    if (!graph.levelized || graph.level.size() != static_cast<std::size_t>(graph.num_pins))
+        throw GraphError("timing graph is not levelized");
+    auto S = session(nl, c);
+    const auto xy = flat_points(pos);
+    ck(tdpg_set_pin_positions(S->s, xy.data()));
+    ck(tdpg_sta(S->s, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
+    return S;
+}
+
+} // namespace
+
+// ---- netlist -----------------------------------------------------------------------------------
+void Netlist::finalize()
+{ // netlist.cpp:5-21 semantics: per-cell ascending pin lists, owning net per pin, role flags
+    cell_pins.assign(cells.size(), {});
+    pin_net.assign(pins.size(), -1);
+    pin_is_source.assign(pins.size(), false);
+    pin_is_endpoint.assign(pins.size(), false);
+    for (std::size_t p = 0; p < pins.size(); ++p)
+        if (pins[p].cell >= 0) cell_pins[static_cast<std::size_t>(pins[p].cell)].push_back(static_cast<int>(p));
+    for (std::size_t n = 0; n < nets.size(); ++n) {
+        pin_net[static_cast<std::size_t>(nets[n].driver)] = static_cast<int>(n);
+        for (int s : nets[n].sinks) pin_net[static_cast<std::size_t>(s)] = static_cast<int>(n);
+    }
+    for (int s : sources) pin_is_source[static_cast<std::size_t>(s)] = true;
+    for (int e : endpoints) pin_is_endpoint[static_cast<std::size_t>(e)] = true;
+}
+
+PinPositions pin_positions(const Netlist& nl, const std::vector<Point>& cell_pos)
+{
+    auto S = session(nl, core_only({}));
+    const auto xy = flat_points(cell_pos);
+    ck(tdpg_set_positions(S->s, xy.data()));
+    std::vector<double> out(2 * nl.pins.size());
+    ck(tdpg_pin_positions(S->s, out.data()));
+    return points(out);
+}
+
+// ---- timing graph ----------------------------------------------------------------------------------
+TimingGraph build_timing_graph(const Netlist& nl)
+{
+    auto S = session(nl, core_only({}));
+    TimingGraph g;
+    g.num_pins = static_cast<int>(nl.pins.size());
+    int32_t cnt[4];
+    g.level.resize(nl.pins.size());
+    ck(tdpg_graph_info(S->s, cnt, g.level.data()));
+    g.num_net_arcs = cnt[0], g.num_cell_arcs = cnt[1];
+    const std::size_t A = static_cast<std::size_t>(cnt[0]) + cnt[1];
+    std::vector<int32_t> from(A), to(A), kind(A), owner(A);
+    ck(tdpg_graph_arcs(S->s, from.data(), to.data(), kind.data(), owner.data()));
+    g.arcs.resize(A);
+    g.in_arcs.assign(nl.pins.size(), {});
+    g.out_arcs.assign(nl.pins.size(), {});
+    for (std::size_t a = 0; a < A; ++a) {
+        g.arcs[a] = Arc{from[a], to[a], kind[a] ? ArcKind::CellArc : ArcKind::NetArc, owner[a]};
+        g.out_arcs[static_cast<std::size_t>(from[a])].push_back(static_cast<int>(a));
+        g.in_arcs[static_cast<std::size_t>(to[a])].push_back(static_cast<int>(a));
+    }
+    g.levels.assign(static_cast<std::size_t>(cnt[2]), {});
+    for (std::size_t p = 0; p < nl.pins.size(); ++p) g.levels[static_cast<std::size_t>(g.level[p])].push_back(static_cast<int>(p));
+    g.sources = nl.sources, g.endpoints = nl.endpoints;
+    g.is_source.assign(nl.pins.size(), false);
+    g.is_endpoint.assign(nl.pins.size(), false);
+    for (int s : nl.sources) g.is_source[static_cast<std::size_t>(s)] = true;
+    for (int e : nl.endpoints) g.is_endpoint[static_cast<std::size_t>(e)] = true;
+    g.levelized = true;
+    return g;
+}
+
+// ---- STA -------------------------------------------------------------------------------------------
+double net_delay(const Point& a, const Point& b, double cap, const DesignConstraints& c)
+{ // scalar convenience form of the device's net_delay (sta.cpp:10-14), same expression
+    const double len = manhattan(a, b);
+    return (c.r_unit * len) * (c.c_unit * len + cap);
+}
+
+double arc_delay(const Arc& arc, const Netlist& nl, const PinPositions& pos, const DesignConstraints& c)
+{
+    if (arc.kind == ArcKind::CellArc) return nl.cells[static_cast<std::size_t>(arc.owner)].delay;
+    return net_delay(pos[static_cast<std::size_t>(arc.from)], pos[static_cast<std::size_t>(arc.to)],
+                     nl.pins[static_cast<std::size_t>(arc.to)].load_cap, c);
+}
+
+std::vector<double> propagate_arrival(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                                      const DesignConstraints& c, std::vector<bool>* arr_known, int)
+{
+    auto S = sta_at(graph, nl, pos, c);
+    TimingAnnotation a = fetch_annotation(S->s, nl);
+    if (arr_known) *arr_known = a.arr_known;
+    return a.arr;
+}
+
+std::vector<double> propagate_required(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                                       const DesignConstraints& c, std::vector<bool>* req_known, int)
+{
+    auto S = sta_at(graph, nl, pos, c);
+    TimingAnnotation a = fetch_annotation(S->s, nl);
+    if (req_known) *req_known = a.req_known;
+    return a.req;
+}
+
+TimingAnnotation compute_slacks(const TimingGraph& graph, std::vector<double> arrivals, std::vector<double> required,
+                                std::vector<bool> arr_known, std::vector<bool> req_known)
+{ // glue over caller-supplied vectors (sta.cpp:104-120); the engine computes slacks on the device
+    TimingAnnotation ann;
+    ann.arr = std::move(arrivals), ann.req = std::move(required);
+    ann.arr_known = std::move(arr_known), ann.req_known = std::move(req_known);
+    ann.slack.resize(ann.arr.size());
+    for (std::size_t p = 0; p < ann.arr.size(); ++p) ann.slack[p] = ann.req[p] - ann.arr[p];
+    for (int e : graph.endpoints) ann.endpoint_slacks.emplace_back(e, ann.slack[static_cast<std::size_t>(e)]);
+    std::tie(ann.tns, ann.wns) = tns_wns(ann.endpoint_slacks);
+    return ann;
+}
+
+std::pair<double, double> tns_wns(const std::vector<std::pair<int, double>>& endpoint_slacks)
+{
+    double tns = 0.0, wns = 0.0;
+    for (const auto& [pin, s] : endpoint_slacks)
+        if (s < 0.0) {
+            tns += s;
+            if (s < wns) wns = s;
+        }
+    return {tns, wns};
+}
+
+TimingAnnotation run_sta(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                         const DesignConstraints& c, int)
+{
+    auto S = sta_at(graph, nl, pos, c);
+    return fetch_annotation(S->s, nl);
+}
+
+// ---- paths -----------------------------------------------------------------------------------------
+PathEnumerator::PathEnumerator(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                               const DesignConstraints& c)
+    : graph_(graph), netlist_(nl), pos_(pos), constraints_(c)
+{
+}
+
+const PathEnumerator::Record* PathEnumerator::path_to(int pin, std::size_t rank)
+{
+    if (rank > 0) throw std::logic_error("path ranks > 0 (k > 1) are not implemented on the device yet");
+    if (auto it = found_.find(pin); it != found_.end()) return &it->second;
+    if (none_.count(pin)) return nullptr;
+    auto S = sta_at(graph_, netlist_, pos_, constraints_);
+    std::vector<int32_t> buf(static_cast<std::size_t>(graph_.levels.size()) + 2);
+    int32_t n = 0;
+    double delay = 0.0;
+    ck(tdpg_path_to(S->s, pin, 0, buf.data(), static_cast<int32_t>(buf.size()), &n, &delay));
+    if (n == 0) {
+        none_[pin] = true;
+        return nullptr;
+    }
+    Record r;
+    r.delay = delay;
+    r.pins.assign(buf.begin(), buf.begin() + n);
+    return &found_.emplace(pin, std::move(r)).first->second;
+}
+
+std::vector<CriticalPath> k_worst_paths_to(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                                           const DesignConstraints& c, const TimingAnnotation&, int endpoint, int k)
+{
+    if (endpoint < 0 || endpoint >= graph.num_pins || !graph.is_endpoint[static_cast<std::size_t>(endpoint)])
+        throw EndpointError("pin " + std::to_string(endpoint) + " is not an endpoint");
+    std::vector<CriticalPath> out;
+    if (k <= 0) return out;
+    if (k > 1) throw std::logic_error("k > 1 per endpoint is not implemented on the device yet");
+    PathEnumerator en(graph, nl, pos, c);
+    if (const auto* r = en.path_to(endpoint, 0)) out.push_back(CriticalPath{r->pins, c.clock_period - r->delay});
+    return out;
+}
+
+ExtractionReport report_timing(const TimingGraph&, const Netlist&, const PinPositions&, const DesignConstraints&,
+                               const TimingAnnotation&, int, int)
+{
+    throw std::logic_error("the topn extraction policy is not implemented on the device yet");
+}
+
+ExtractionReport report_timing_endpoint(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                                        const DesignConstraints& c, const TimingAnnotation&, int n, int k, int)
+{
+    if (k != 1) throw std::logic_error("k > 1 per endpoint is not implemented on the device yet");
+    const auto t0 = std::chrono::steady_clock::now();
+    ExtractionReport r;
+    r.policy = "endpoint", r.n = n, r.k = k;
+    if (n <= 0) return r; // violated.resize(0) (paths.cpp:178)
+    auto S = sta_at(graph, nl, pos, c);
+    int64_t counts[4];
+    ck(tdpg_extract_endpoint(S->s, n, 1, counts));
+    r = fetch_report(S->s, nl, n, k, counts, 0.0);
+    r.elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return r;
+}
+
+std::vector<PairHit> collect_pin_pairs(const Netlist& nl, const std::vector<CriticalPath>& paths)
+{ // glue over caller-supplied paths (paths.cpp:191-203); the engine produces hits on the device
+    std::vector<PairHit> hits;
+    for (const auto& path : paths)
+        for (std::size_t i = 0; i + 1 < path.pins.size(); ++i) {
+            if (nl.pins[static_cast<std::size_t>(path.pins[i])].dir != PinDir::Output) continue;
+            hits.push_back(PairHit{std::minmax(path.pins[i], path.pins[i + 1]), path.slack});
+        }
+    return hits;
+}
+
+// ---- pin pairs -------------------------------------------------------------------------------------
+void update_pair_weights(PinPairWeights& weights, const std::vector<PairHit>& hits, double wns, double w0, double w1)
+{
+    if (!(wns < 0.0) || hits.empty()) return;
+    int max_pin = 0;
+    for (const auto& [pr, w] : weights) max_pin = std::max({max_pin, pr.first, pr.second});
+    for (const auto& h : hits) max_pin = std::max({max_pin, h.pair.first, h.pair.second});
+    std::vector<Point> pts(static_cast<std::size_t>(max_pin) + 1);
+    PointNet scratch{std::span<const Point>(pts)};
+    auto S = session(scratch.nl, core_only({}));
+    ledger_upload(S->s, weights);
+    std::vector<int32_t> a, b;
+    std::vector<double> sl;
+    for (const auto& h : hits) a.push_back(h.pair.first), b.push_back(h.pair.second), sl.push_back(h.path_slack);
+    ck(tdpg_pp_update(S->s, static_cast<int64_t>(a.size()), a.data(), b.data(), sl.data(), wns, w0, w1));
+    weights = ledger_download(S->s);
+    std::lock_guard<std::mutex> lock(g_mu);
+    g_cache.erase(&scratch.nl);
+}
+
+PinPairLossResult pin_pair_loss(const PinPairWeights& weights, const PinPositions& pins, std::size_t num_pins,
+                                PairLossKind kind)
+{
+    PinPairLossResult out;
+    out.d_pin.assign(num_pins, Point{});
+    if (weights.empty() || pins.empty()) return out;
+    PointNet scratch{std::span<const Point>(pins.data(), pins.size())};
+    auto S = session(scratch.nl, core_only({}));
+    ledger_upload(S->s, weights);
+    std::vector<double> d(2 * pins.size());
+    ck(tdpg_pp_loss(S->s, kind == PairLossKind::Linear ? 1 : 0, &out.value, d.data()));
+    for (std::size_t p = 0; p < std::min(num_pins, pins.size()); ++p) out.d_pin[p] = Point{d[2 * p], d[2 * p + 1]};
+    std::lock_guard<std::mutex> lock(g_mu);
+    g_cache.erase(&scratch.nl);
+    return out;
+}
+
+// ---- wirelength ------------------------------------------------------------------------------------
+NetTermGrad wa_wirelength(std::span<const Point> pin_pos, double gamma)
+{
+    NetTermGrad out;
+    out.d_pin.assign(pin_pos.size(), Point{});
+    if (pin_pos.size() < 2) return out;
+    PointNet scratch{pin_pos};
+    auto S = session(scratch.nl, core_only({}));
+    double wl = 0.0, hp = 0.0;
+    std::vector<double> g(2 * pin_pos.size());
+    ck(tdpg_wirelength(S->s, gamma, nullptr, &wl, &hp, g.data()));
+    out.value = wl;
+    for (std::size_t i = 0; i < pin_pos.size(); ++i) out.d_pin[i] = Point{g[2 * i], g[2 * i + 1]};
+    std::lock_guard<std::mutex> lock(g_mu);
+    g_cache.erase(&scratch.nl);
+    return out;
+}
+
+double hpwl_net(std::span<const Point> pin_pos)
+{
+    if (pin_pos.size() < 2) return 0.0;
+    PointNet scratch{pin_pos};
+    auto S = session(scratch.nl, core_only({}));
+    double h = 0.0;
+    std::vector<double> xy(2 * pin_pos.size());
+    for (std::size_t i = 0; i < pin_pos.size(); ++i) xy[2 * i] = pin_pos[i].x, xy[2 * i + 1] = pin_pos[i].y;
+    ck(tdpg_hpwl_pins(S->s, xy.data(), &h));
+    std::lock_guard<std::mutex> lock(g_mu);
+    g_cache.erase(&scratch.nl);
+    return h;
+}
+
+double hpwl_total(const Netlist& nl, const PinPositions& pos)
+{
+    auto S = session(nl, core_only({}));
+    const auto xy = flat_points(pos);
+    double h = 0.0;
+    ck(tdpg_hpwl_pins(S->s, xy.data(), &h));
+    return h;
+}
+
+// ---- density ----------------------------------------------------------------------------------------
+DensityGrid::DensityGrid(const Netlist&, const Rect& core, int nx, int ny, double target_density)
+    : core_(core), nx_(nx), ny_(ny), target_density_(target_density)
+{
+    if (nx < 1 || ny < 1) throw ValidationError("density grid must be at least 1x1");
+}
+
+DensityResult DensityGrid::evaluate(const Netlist& nl, const std::vector<Point>& cell_pos, int) const
+{
+    auto S = session(nl, core_only(core_));
+    set_core(S->s, core_);
+    const auto xy = flat_points(cell_pos);
+    ck(tdpg_set_positions(S->s, xy.data()));
+    ck(tdpg_set_grid(S->s, nx_, ny_, target_density_));
+    DensityResult r;
+    std::vector<double> d(2 * nl.cells.size());
+    ck(tdpg_density(S->s, &r.value, &r.overflow, d.data()));
+    r.d_cell = points(d);
+    return r;
+}
+
+// ---- placer -------------------------------------------------------------------------------------------
+namespace {
+std::string fmt17(double v)
+{
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    return buf;
+}
+
+tdpg_config to_c(const OptimizerConfig& c)
+{
+    tdpg_config k;
+    tdpg_config_default(&k);
+    k.gamma_frac = c.gamma_frac, k.grid_nx = c.grid_nx, k.grid_ny = c.grid_ny, k.target_density = c.target_density;
+    k.beta = c.beta, k.pp_loss = c.pp_loss == PairLossKind::Linear, k.net_weighting = c.net_weighting, k.m = c.m;
+    k.w0 = c.w0, k.w1 = c.w1, k.timing_start_iter = c.timing_start_iter;
+    k.extraction = c.extraction == ExtractionPolicy::TopN, k.k = c.k, k.max_iters = c.max_iters;
+    k.stop_overflow = c.stop_overflow, k.mu = c.mu, k.lambda0 = c.lambda0, k.lambda_max = c.lambda_max;
+    k.step0_frac = c.step0_frac, k.step_decay = c.step_decay, k.adam_beta1 = c.adam_beta1;
+    k.adam_beta2 = c.adam_beta2, k.adam_eps = c.adam_eps, k.seed = c.seed, k.init_jitter_frac = c.init_jitter_frac;
+    k.threads = c.threads;
+    return k;
+}
+} // namespace
+
+std::string metrics_to_csv(const MetricTrace& trace)
+{ // placer.cpp:234-260 format
+    std::string out = "iter,hpwl,overflow,tns,wns,wl_term,density_term,pp_term,lambda,beta_pp\n";
+    for (const TraceRow& r : trace) {
+        out += std::to_string(r.iter) + ',' + fmt17(r.hpwl) + ',' + fmt17(r.overflow) + ',';
+        if (r.has_timing) out += fmt17(r.tns);
+        out += ',';
+        if (r.has_timing) out += fmt17(r.wns);
+        out += ',' + fmt17(r.wl_term) + ',' + fmt17(r.density_term) + ',' + fmt17(r.pp_term) + ',' + fmt17(r.lambda) +
+               ',' + fmt17(r.beta_pp) + '\n';
+    }
+    return out;
+}
+
+std::string weights_to_json(const PinPairWeights& weights, const Netlist& nl)
+{
+    std::string out = "{\n  \"pairs\": [";
+    bool first = true;
+    for (const auto& [pr, w] : weights) {
+        out += first ? "\n" : ",\n";
+        first = false;
+        out += "    {\n      \"a\": \"" + nl.pins[static_cast<std::size_t>(pr.first)].name + "\",\n      \"b\": \"" +
+               nl.pins[static_cast<std::size_t>(pr.second)].name + "\",\n      \"weight\": " + fmt17(w) + "\n    }";
+    }
+    out += weights.empty() ? "]\n}\n" : "\n  ]\n}\n";
+    return out;
+}
+
+ObjectiveResult objective_and_gradient(const Netlist& nl, const std::vector<Point>& cell_pos, const DensityGrid& grid,
+                                       const PinPairWeights& weights, const std::vector<double>& net_weights,
+                                       double gamma, double lambda, double beta, PairLossKind kind, int)
+{
+    if (!net_weights.empty() && net_weights.size() != nl.nets.size())
+        throw ValidationError("net weight count does not match net count");
+    auto S = session(nl, core_only(grid.core()));
+    set_core(S->s, grid.core());
+    const auto xy = flat_points(cell_pos);
+    ck(tdpg_set_positions(S->s, xy.data()));
+    ck(tdpg_set_grid(S->s, grid.nx(), grid.ny(), grid.target_density()));
+    ledger_upload(S->s, weights);
+    double terms[6];
+    std::vector<double> d(2 * nl.cells.size());
+    ck(tdpg_objective(S->s, gamma, lambda, beta, kind == PairLossKind::Linear ? 1 : 0,
+                      net_weights.empty() ? nullptr : net_weights.data(), terms, d.data()));
+    ObjectiveResult r;
+    r.value = terms[0], r.wl_term = terms[1], r.density_term = terms[2], r.pp_term = terms[3], r.hpwl = terms[4];
+    r.overflow = terms[5];
+    r.d_cell = points(d);
+    return r;
+}
+
+std::vector<double> apply_net_weights(const TimingAnnotation& ann, const Netlist& nl)
+{ // glue over a caller-supplied annotation (placer.cpp:262-273); the engine applies it on the device
+    std::vector<double> w(nl.nets.size(), 1.0);
+    if (ann.wns >= 0.0) return w;
+    for (std::size_t e = 0; e < nl.nets.size(); ++e) {
+        double worst = ann.slack[static_cast<std::size_t>(nl.nets[e].driver)];
+        for (int s : nl.nets[e].sinks) worst = std::min(worst, ann.slack[static_cast<std::size_t>(s)]);
+        if (worst < 0.0) w[e] = 1.0 + (-worst) / (-ann.wns);
+    }
+    return w;
+}
+
+void AdamState::step(std::vector<double>& x, const std::vector<double>& grad, double lr, double beta1, double beta2,
+                     double eps)
+{
+    int32_t tt = t;
+    ck(tdpg_adam_step(static_cast<int64_t>(x.size()), x.data(), grad.data(), m.data(), v.data(), &tt, lr, beta1, beta2,
+                      eps));
+    t = tt;
+}
+
+namespace {
+struct ObserverCtx {
+    tdpg_session* s;
+    const Netlist* nl;
+    const TimingRoundObserver* obs;
+};
+
+void observer_trampoline(void* user, int32_t iter)
+{
+    auto* c = static_cast<ObserverCtx*>(user);
+    const TimingAnnotation ann = fetch_annotation(c->s, *c->nl);
+    int64_t counts[4];
+    ck(tdpg_paths_counts(c->s, counts));
+    ExtractionReport r = fetch_report(c->s, *c->nl, static_cast<int>(counts[0]), 1, counts, 0.0);
+    if (ann.wns >= 0.0) r = ExtractionReport{}; // the round was skipped (placer.cpp:422-432)
+    (*c->obs)(iter, ann, r);
+}
+} // namespace
+
+PlacementOutcome run_placement(const Design& design, const OptimizerConfig& config, const TimingRoundObserver& observer)
+{
+    const Netlist& nl = design.netlist;
+    auto S = session(nl, design.constraints);
+    set_core(S->s, design.constraints.core);
+    const auto xy = flat_points(design.positions);
+    ck(tdpg_set_positions(S->s, xy.data()));
+    std::vector<uint8_t> expl(design.pos_explicit.begin(), design.pos_explicit.end());
+    expl.resize(nl.cells.size(), 0);
+    const tdpg_config cfg = to_c(config);
+    std::vector<tdpg_trace_row> rows(static_cast<std::size_t>(std::max(config.max_iters, 1)));
+    int32_t n_rows = 0, stop = 0;
+    double fin[3];
+    ObserverCtx ctx{S->s, &nl, &observer};
+    ck(tdpg_set_round_callback(S->s, observer ? observer_trampoline : nullptr, &ctx));
+    const int rc = tdpg_place(S->s, &cfg, expl.data(), rows.data(), &n_rows, &stop, fin);
+    tdpg_set_round_callback(S->s, nullptr, nullptr);
+    ck(rc);
+    PlacementOutcome out;
+    std::vector<double> pos(2 * nl.cells.size());
+    ck(tdpg_get_positions(S->s, pos.data()));
+    out.positions = points(pos);
+    for (int i = 0; i < n_rows; ++i) {
+        const tdpg_trace_row& r = rows[static_cast<std::size_t>(i)];
+        TraceRow t;
+        t.iter = r.iter, t.hpwl = r.hpwl, t.overflow = r.overflow, t.has_timing = r.has_timing != 0, t.tns = r.tns;
+        t.wns = r.wns, t.wl_term = r.wl_term, t.density_term = r.density_term, t.pp_term = r.pp_term;
+        t.lambda = r.lambda, t.beta_pp = r.beta_pp;
+        out.trace.push_back(t);
+    }
+    out.pair_weights = ledger_download(S->s);
+    out.final_timing = fetch_annotation(S->s, nl); // tdpg_place ran STA at the returned positions
+    out.iterations = n_rows;
+    out.stop_reason = stop ? "overflow" : "max_iters";
+    return out;
+}
+
+} // namespace tdp

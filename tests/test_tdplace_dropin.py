@@ -1,0 +1,92 @@
+"""The reference's Python API (tdplace) as a drop-in: the reference's own smoke tests
+(proj/tests/python/test_smoke.py:42-113) restated against paper_2503_11674_b200.tdplace.
+compare_csv / render_svg are not on the device."""
+import pytest
+
+from paper_2503_11674_b200 import tdplace
+
+T1 = {
+    "core": [0, 0, 10, 10], "clock_period": 10, "r_unit": 1, "c_unit": 1,
+    "cells": [{"name": "A", "width": 1, "height": 1, "x": 0, "y": 0, "delay": 1},
+              {"name": "B", "width": 1, "height": 1, "x": 3, "y": 0, "delay": 1},
+              {"name": "C", "width": 1, "height": 1, "x": 3, "y": 4, "delay": 1}],
+    "pins": [{"name": "PI", "terminal": {"x": 0, "y": 0}, "dir": "out"},
+             {"name": "A.in", "cell": "A", "dir": "in"}, {"name": "A.out", "cell": "A", "dir": "out"},
+             {"name": "B.in", "cell": "B", "dir": "in"}, {"name": "B.out", "cell": "B", "dir": "out"},
+             {"name": "C.in", "cell": "C", "dir": "in"}, {"name": "C.out", "cell": "C", "dir": "out"},
+             {"name": "PO", "terminal": {"x": 3, "y": 4}, "dir": "in"}],
+    "nets": [{"name": "n0", "driver": "PI", "sinks": ["A.in"]}, {"name": "n1", "driver": "A.out", "sinks": ["B.in"]},
+             {"name": "n2", "driver": "B.out", "sinks": ["C.in"]}, {"name": "n3", "driver": "C.out", "sinks": ["PO"]}],
+    "sources": ["PI"], "endpoints": ["PO"],
+}
+QUICK = {"max_iters": 40, "timing_start_iter": 10, "m": 5, "grid_nx": 8, "grid_ny": 8, "seed": 3}
+
+
+def test_exceptions_map_to_python_types():
+    with pytest.raises(tdplace.ParseError):
+        tdplace.validate("{not json")
+    with pytest.raises(ValueError):
+        tdplace.validate({"core": [0, 0, 10, 10]})
+    with pytest.raises(tdplace.ValidationError):
+        tdplace.validate(dict(T1, clock_period=-1))
+    with pytest.raises(ValueError):
+        tdplace.report_paths(T1, policy="sideways")
+
+
+def test_default_config():
+    cfg = tdplace.default_config()
+    assert cfg["m"] == 15 and cfg["w0"] == 10.0 and cfg["lambda0"] == "auto"
+
+
+@pytest.mark.gpu
+def test_sta_on_known_design():
+    rep = tdplace.sta(T1)
+    assert rep["tns"] == pytest.approx(-18.0) and rep["wns"] == pytest.approx(-18.0)
+    assert len(rep["endpoints"]) == 1 and len(rep["pins"]) == 8
+    assert tdplace.hpwl(T1) == pytest.approx(7.0)
+
+
+@pytest.mark.gpu
+def test_generate_place_sta_roundtrip():
+    design = tdplace.generate(seed=7, cells=40, fail_frac=0.3)
+    tdplace.validate(design)
+    out = tdplace.place(design, QUICK)
+    assert out["iterations"] >= 1 and out["stop_reason"] in ("max_iters", "overflow")
+    assert len(out["placement"]["cells"]) == len(design["cells"])
+    rep = tdplace.sta(design, out["placement"])
+    assert rep["tns"] == pytest.approx(out["tns"]) and rep["wns"] == pytest.approx(out["wns"])
+    again = tdplace.place(design, QUICK)
+    assert again["metrics_csv"] == out["metrics_csv"] and again["placement"] == out["placement"]
+
+
+@pytest.mark.gpu
+def test_report_paths():
+    rep = tdplace.report_paths(T1, policy="endpoint", n=1, k=1)
+    assert rep["policy"] == "endpoint" and len(rep["paths"]) == 1
+    path = rep["paths"][0]
+    assert path["pins"][0] == "PI" and path["pins"][-1] == "PO" and path["slack"] == pytest.approx(-18.0)
+
+
+@pytest.mark.gpu
+def test_default_config_round_trips_through_place():
+    cfg = tdplace.default_config()
+    cfg.update(QUICK)
+    assert tdplace.place(T1, cfg)["iterations"] >= 1
+
+
+@pytest.mark.gpu
+def test_generated_names_match_reference_json():
+    """Generated designs carry the reference generator's names (pi*, c*.i*, r*.d/q, po*, n*)."""
+    from oracle.oracle import RefOracle
+    if not RefOracle.available():
+        pytest.skip("oracle/_ref not built")
+    import ctypes, json
+    d = tdplace.generate(seed=5, cells=60, fail_frac=0.3)
+    lib = RefOracle.lib_()
+    h = ctypes.c_void_p()
+    assert lib.ref_generate(5, 60, -1, 2.0, 0.3, 1e-4, 1e-4, ctypes.byref(h), None) == 0
+    ref = json.loads(lib.ref_design_to_json(h.value).decode())
+    lib.ref_destroy(h.value)
+    assert [c["name"] for c in d["cells"]] == [c["name"] for c in ref["cells"]]
+    assert [p["name"] for p in d["pins"]] == [p["name"] for p in ref["pins"]]
+    assert d["nets"] == ref["nets"] and d["sources"] == ref["sources"] and d["endpoints"] == ref["endpoints"]
