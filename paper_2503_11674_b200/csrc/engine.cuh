@@ -72,6 +72,7 @@ struct Engine; // placement loop state (gp.cu)
 
 struct tdpg_session {
     // sizes
+    // E: net-pin entries; E_tot: WA-layout slots (E_lay >= E) + off-net pins
     int C = 0, P = 0, N = 0, E = 0, E_tot = 0, S = 0, EP = 0, A = 0, A_net = 0, A_cell = 0, L = 0;
     double clock = 0, r_unit = 0, c_unit = 0, core[4] = {0, 0, 0, 0};
     cudaStream_t st = nullptr;
@@ -90,10 +91,12 @@ struct tdpg_session {
     tdpg::DBuf<double> cell_delay, pin_cap;
     tdpg::DBuf<uint8_t> cell_fixed, pin_dir, is_source, is_endpoint;
     tdpg::DBuf<int> pin_cell, net_start, net_pins, e_cell, pin_entry, cell_ent_start, cell_ent;
-    // WA size classes: nets sorted by pin count, per block (pin count, first, count)
-    tdpg::DBuf<int> net_by_size;
+    // WA layout: nets sorted by pin count; per block (pin count N or 0, first, count, entry base);
+    // entries of N-pin nets slot-major per block, class-0 nets contiguous (wa_gen_start)
+    tdpg::DBuf<int> net_by_size, wa_gen_start;
     tdpg::DBuf<int4> wa_blk;
-    int n_wa_blocks = 0;
+    int n_wa_blocks = 0, E_lay = 0;
+    int wa_cls_blk0[9] = {0}, wa_cls_nblk[9] = {0};
 
     // device timing graph
     tdpg::DBuf<int> lvl_pins, in_start, in_from, out_start, out_to, ep_sorted;

@@ -103,70 +103,88 @@ __device__ __forceinline__ void wa_axis(const double (&x)[N], double inv_gamma, 
 }
 
 template <int N>
-__device__ __forceinline__ void wa_net(int s0, double w, const int* __restrict__ e_cell,
-                                       const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
-                                       const double2* __restrict__ anchor, double inv_gamma,
-                                       double2* __restrict__ grad_e, double& wl, double& hp)
+__device__ __forceinline__ void wa_net_slots(int base, double w, const int* __restrict__ e_cell,
+                                             const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
+                                             const double2* __restrict__ anchor, double inv_gamma,
+                                             double2* __restrict__ grad_e, double& wl, double& hp)
 {
     double x[N], y[N], gx[N], gy[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-        const double2 p = entry_pos(e_cell[s0 + i], e_off[s0 + i], cell_xy, anchor);
+    for (int i = 0; i < N; ++i) { // pin i of this net at base + i * 256 (slot-major block layout)
+        const double2 p = entry_pos(__ldcs(e_cell + base + i * kBlock), __ldcs(e_off + base + i * kBlock), cell_xy,
+                                    anchor);
         x[i] = p.x, y[i] = p.y;
     }
     double vx, vy, hx, hy;
     wa_axis<N>(x, inv_gamma, gx, vx, hx);
     wa_axis<N>(y, inv_gamma, gy, vy, hy);
 #pragma unroll
-    for (int i = 0; i < N; ++i) grad_e[s0 + i] = make_double2(w * gx[i], w * gy[i]);
+    for (int i = 0; i < N; ++i) grad_e[base + i * kBlock] = make_double2(w * gx[i], w * gy[i]);
     wl = w * (vx + vy);
     hp = hx + hy;
 }
 
 constexpr int kWaMaxN = 8;
 
-__global__ void __launch_bounds__(kBlock) k_wa_sized(const int4* __restrict__ blk, const int* __restrict__ net_by_size,
-                                                     const int* __restrict__ net_start, const int* __restrict__ e_cell,
-                                                     const double2* __restrict__ e_off,
+// One launch per pin count N: thread t of block b owns the t-th net of the block.
+template <int N>
+__global__ void __launch_bounds__(kBlock) k_wa_class(int blk0, const int4* __restrict__ blk,
+                                                     const int* __restrict__ net_by_size,
+                                                     const int* __restrict__ e_cell, const double2* __restrict__ e_off,
                                                      const double2* __restrict__ cell_xy,
                                                      const double2* __restrict__ anchor,
-                                                     const double* __restrict__ net_w, double gamma, double inv_gamma,
+                                                     const double* __restrict__ net_w, double inv_gamma,
                                                      double2* __restrict__ grad_e, double* __restrict__ part_wl,
                                                      double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
 {
     __shared__ double sh[kBlock / 32];
     if (ctrl && ctrl->stopped) return;
-    const int4 b = blk[blockIdx.x]; // (pin count or 0, first index in net_by_size, count, -)
+    const int4 b = blk[blk0 + blockIdx.x]; // (N, first in net_by_size, count, entry base)
     double wl = 0.0, hp = 0.0;
     if (static_cast<int>(threadIdx.x) < b.z) {
-        const int net = net_by_size[b.y + threadIdx.x];
-        const int s0 = net_start[net];
+        const double w = net_w ? net_w[net_by_size[b.y + threadIdx.x]] : 1.0;
+        wa_net_slots<N>(b.w + threadIdx.x, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp);
+    }
+    const double bw = block_sum<kBlock>(wl, sh);
+    const double bh = block_sum<kBlock>(hp, sh);
+    if (threadIdx.x == 0) part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
+}
+
+// Nets outside the classes (more than kWaMaxN pins): three-pass generic code per net.
+__global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __restrict__ blk,
+                                                       const int* __restrict__ net_by_size,
+                                                       const int* __restrict__ gen_start,
+                                                       const int* __restrict__ net_start,
+                                                       const int* __restrict__ e_cell,
+                                                       const double2* __restrict__ e_off,
+                                                       const double2* __restrict__ cell_xy,
+                                                       const double2* __restrict__ anchor,
+                                                       const double* __restrict__ net_w, double gamma,
+                                                       double2* __restrict__ grad_e, double* __restrict__ part_wl,
+                                                       double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
+{
+    __shared__ double sh[kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    const int4 b = blk[blk0 + blockIdx.x];
+    double wl = 0.0, hp = 0.0;
+    if (static_cast<int>(threadIdx.x) < b.z) {
+        const int i = b.y + threadIdx.x;
+        const int net = net_by_size[i];
+        const int s0 = gen_start[i], n = net_start[net + 1] - net_start[net];
         const double w = net_w ? net_w[net] : 1.0;
-        switch (b.x) {
-        case 2: wa_net<2>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
-        case 3: wa_net<3>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
-        case 4: wa_net<4>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
-        case 5: wa_net<5>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
-        case 6: wa_net<6>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
-        case 7: wa_net<7>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
-        case 8: wa_net<8>(s0, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp); break;
-        default: {
-            const int n = net_start[net + 1] - s0;
-            if (n < 2) {
-                for (int i = 0; i < n; ++i) grad_e[s0 + i] = make_double2(0.0, 0.0);
-            } else {
-                double hx, hy;
-                const double vx = wa_dim_mem(s0, n, 0, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hx);
-                const double vy = wa_dim_mem(s0, n, 1, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hy);
-                wl = w * (vx + vy);
-                hp = hx + hy;
-            }
-        }
+        if (n < 2) {
+            for (int k = 0; k < n; ++k) grad_e[s0 + k] = make_double2(0.0, 0.0);
+        } else {
+            double hx, hy;
+            const double vx = wa_dim_mem(s0, n, 0, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hx);
+            const double vy = wa_dim_mem(s0, n, 1, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hy);
+            wl = w * (vx + vy);
+            hp = hx + hy;
         }
     }
     const double bw = block_sum<kBlock>(wl, sh);
     const double bh = block_sum<kBlock>(hp, sh);
-    if (threadIdx.x == 0) part_wl[blockIdx.x] = bw, part_hp[blockIdx.x] = bh;
+    if (threadIdx.x == 0) part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
 }
 
 // =====================================================================================
@@ -249,9 +267,29 @@ constexpr int kFootCache = 16;
 // whatever the order or the path.
 constexpr int kWinBins = 4096; // 32 KB of int64 accumulators
 
+// 64-bit fixed-point add into shared memory as two native 32-bit atomics with an explicit carry
+// (a 64-bit shared atomicAdd compiles to a CAS spin loop, ATOMS.CAST.SPIN.64, on sm_100a).
+struct SmemAcc {
+    unsigned* lo;
+    unsigned* hi;
+    __device__ __forceinline__ void add(long long k, unsigned long long v) const
+    {
+        const unsigned vl = static_cast<unsigned>(v), vh = static_cast<unsigned>(v >> 32);
+        const unsigned old = atomicAdd(lo + k, vl);
+        const unsigned carry = (old + vl < old) ? 1u : 0u;
+        if (vh + carry) atomicAdd(hi + k, vh + carry);
+    }
+};
+
+struct GlobalAcc {
+    unsigned long long* p;
+    __device__ __forceinline__ void add(long long k, unsigned long long v) const { atomicAdd(p + k, v); }
+};
+
+template <typename Acc>
 __device__ __forceinline__ void scatter_cell(const double2 p, const double2 s, const GridDev& g, int bx0, int bx1,
-                                             int by0, int by1, unsigned long long* base, long long row_stride,
-                                             int col0, int row0)
+                                             int by0, int by1, const Acc& acc, long long row_stride, int col0,
+                                             int row0)
 {
     const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
     const double area = s.x * s.y;
@@ -269,18 +307,18 @@ __device__ __forceinline__ void scatter_cell(const double2 p, const double2 s, c
         extent_w(xl, xh, g.x0 + (bx + 0.5) * g.bw, g.bw, g.inv_bw, ilx, wx, dwx);
         if (wx == 0.0) continue;
         const double aw = area * wx;
-        unsigned long long* row = base + static_cast<long long>(bx - row0) * row_stride + (by0 - col0);
+        const long long row = static_cast<long long>(bx - row0) * row_stride + (by0 - col0);
 #pragma unroll
         for (int j = 0; j < kFoot; ++j) {
             if (j >= nby) break;
             const long long q = __double2ll_rn(aw * wyc[j] * g.scale);
-            if (q) atomicAdd(row + j, static_cast<unsigned long long>(q));
+            if (q) acc.add(row + j, static_cast<unsigned long long>(q));
         }
         for (int by = by0 + kFoot; by <= by1; ++by) {
             double wy, dwy;
             extent_w(yl, yh, g.y0 + (by + 0.5) * g.bh, g.bh, g.inv_bh, ily, wy, dwy);
             const long long q = __double2ll_rn(aw * wy * g.scale);
-            if (q) atomicAdd(row + (by - by0), static_cast<unsigned long long>(q));
+            if (q) acc.add(row + (by - by0), static_cast<unsigned long long>(q));
         }
     }
 }
@@ -291,7 +329,7 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
                                                                 unsigned long long* __restrict__ acc,
                                                                 const Ctrl* __restrict__ ctrl)
 {
-    __shared__ unsigned long long win[kWinBins];
+    __shared__ unsigned win_lo[kWinBins], win_hi[kWinBins];
     __shared__ int bb[4];
     if (ctrl && ctrl->stopped) return;
     const int i = blockIdx.x * kBlock + threadIdx.x;
@@ -320,16 +358,16 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
     const long long W = static_cast<long long>(bb[1]) - X0 + 1, H = static_cast<long long>(bb[3]) - Y0 + 1;
     if (X0 > bb[1]) return; // no movable cell in this block
     if (W * H <= kWinBins) {
-        for (int k = threadIdx.x; k < W * H; k += kBlock) win[k] = 0ull;
+        for (int k = threadIdx.x; k < W * H; k += kBlock) win_lo[k] = 0u, win_hi[k] = 0u;
         __syncthreads();
-        if (valid) scatter_cell(p, s, g, bx0, bx1, by0, by1, win, H, Y0, X0);
+        if (valid) scatter_cell(p, s, g, bx0, bx1, by0, by1, SmemAcc{win_lo, win_hi}, H, Y0, X0);
         __syncthreads();
         for (int k = threadIdx.x; k < W * H; k += kBlock) {
-            const unsigned long long v = win[k];
+            const unsigned long long v = (static_cast<unsigned long long>(win_hi[k]) << 32) | win_lo[k];
             if (v) atomicAdd(&acc[static_cast<long long>(X0 + k / H) * g.ny + (Y0 + k % H)], v);
         }
     } else if (valid) {
-        scatter_cell(p, s, g, bx0, bx1, by0, by1, acc, g.ny, 0, 0);
+        scatter_cell(p, s, g, bx0, bx1, by0, by1, GlobalAcc{acc}, g.ny, 0, 0);
     }
 }
 
@@ -659,14 +697,36 @@ void rebuild_pp_incidence(tdpg_session* s)
     CK_LAUNCH();
 }
 
+template <int N>
+void launch_wa_class(tdpg_session* s, const double* nw, double inv_gamma, double* pw, double* ph, const Ctrl* ctrl)
+{
+    if (!s->wa_cls_nblk[N]) return;
+    k_wa_class<N><<<s->wa_cls_nblk[N], kBlock, 0, s->st>>>(s->wa_cls_blk0[N], s->wa_blk, s->net_by_size, s->e_cell,
+                                                           s->e_off, s->cell_xy, s->anchor, nw, inv_gamma, s->grad_e,
+                                                           pw, ph, ctrl);
+    CK_LAUNCH();
+}
+
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk,
                        const Ctrl* ctrl)
 {
     (void)nblk;
-    k_wa_sized<<<s->n_wa_blocks, kBlock, 0, s->st>>>(s->wa_blk, s->net_by_size, s->net_start, s->e_cell, s->e_off,
-                                                     s->cell_xy, s->anchor, use_net_w ? s->net_w.p : nullptr, gamma,
-                                                     1.0 / gamma, s->grad_e, part_wl, part_hp, ctrl);
-    CK_LAUNCH();
+    const double* nw = use_net_w ? s->net_w.p : nullptr;
+    const double ig = 1.0 / gamma;
+    launch_wa_class<2>(s, nw, ig, part_wl, part_hp, ctrl);
+    launch_wa_class<3>(s, nw, ig, part_wl, part_hp, ctrl);
+    launch_wa_class<4>(s, nw, ig, part_wl, part_hp, ctrl);
+    launch_wa_class<5>(s, nw, ig, part_wl, part_hp, ctrl);
+    launch_wa_class<6>(s, nw, ig, part_wl, part_hp, ctrl);
+    launch_wa_class<7>(s, nw, ig, part_wl, part_hp, ctrl);
+    launch_wa_class<8>(s, nw, ig, part_wl, part_hp, ctrl);
+    if (s->wa_cls_nblk[0]) {
+        k_wa_generic<<<s->wa_cls_nblk[0], kBlock, 0, s->st>>>(s->wa_cls_blk0[0], s->wa_blk, s->net_by_size,
+                                                              s->wa_gen_start, s->net_start, s->e_cell, s->e_off,
+                                                              s->cell_xy, s->anchor, nw, gamma, s->grad_e, part_wl,
+                                                              part_hp, ctrl);
+        CK_LAUNCH();
+    }
 }
 
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk)
@@ -677,7 +737,7 @@ void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* pa
 void launch_pp(tdpg_session* s, int kind, double beta, double* part_pp, int nblk, const Ctrl* ctrl)
 {
     k_pin_pairs<<<nblk, kBlock, 0, s->st>>>(s->pp_pins, s->pp_start, s->pp_entry, s->pp_inc, s->led_key, s->led_w,
-                                            s->pin_cell, s->pin_off, s->cell_xy, s->anchor, kind, beta, s->E,
+                                            s->pin_cell, s->pin_off, s->cell_xy, s->anchor, kind, beta, s->E_lay,
                                             s->grad_e, part_pp, ctrl);
     CK_LAUNCH();
 }
@@ -840,7 +900,7 @@ int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* 
     s->part.download(part.data(), part.size(), s->st);
     std::vector<double2> ge;
     if (pin_grad) {
-        ge.resize(s->E);
+        ge.resize(s->E_tot);
         s->grad_e.download(ge.data(), ge.size(), s->st);
     }
     CK(cudaStreamSynchronize(s->st));
@@ -850,9 +910,9 @@ int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* 
     if (hpwl) *hpwl = b;
     if (pin_grad) {
         std::fill(pin_grad, pin_grad + 2 * static_cast<size_t>(s->P), 0.0);
-        for (int e = 0; e < s->E; ++e) {
-            const int p = s->h_net_pins[e];
-            pin_grad[2 * p] = ge[e].x, pin_grad[2 * p + 1] = ge[e].y;
+        for (int p = 0; p < s->P; ++p) {
+            const int e = s->h_pin_entry[p];
+            if (e >= 0 && s->h_pin_net[p] >= 0) pin_grad[2 * p] = ge[e].x, pin_grad[2 * p + 1] = ge[e].y;
         }
     }
     API_END

@@ -35,7 +35,7 @@ struct Engine {
     cudaGraphExec_t gexec = nullptr;
     int launched = 0, refreshes = 0;
     long long kernel_launches = 0;
-    int kernels_per_iter = 6;
+    int kernels_per_iter = 13; // 7 WA classes + generic + PP + scatter + bins + finalize + cells (upper bound)
     int sort_every = 2; // iterations between spatial re-sorts of the cells
     double last_refresh_ms = 0, total_refresh_ms = 0;
     ~Engine()
@@ -302,7 +302,11 @@ int engine_run(tdpg_session* s, int n)
 tdpg_session::~tdpg_session()
 {
     delete eng; // Engine is complete here
-    if (st) cudaStreamDestroy(st);
+    if (st) {
+        cudaStreamSynchronize(st);
+        cudaCtxResetPersistingL2Cache(); // release the L2 lines this session pinned
+        cudaStreamDestroy(st);
+    }
 }
 
 using namespace tdpg;

@@ -365,42 +365,64 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     s->is_endpoint.upload(s->h_is_endpoint, s->st);
     s->net_start.upload(s->h_net_start, s->st);
     s->net_pins.upload(s->h_net_pins, s->st);
-    std::vector<int> e_cell(E), pin_entry(P, -1);
-    std::vector<double2> e_off(E);
+    // Net-pin entries in the WA layout: nets sorted (stably) by pin count; nets of N = 2..8 pins in
+    // blocks of 256, slot-major inside a block (pin j of the block's t-th net at base + j*256 + t, so a
+    // warp's loads and stores of one pin slot are contiguous); other nets (class 0) contiguous after.
+    constexpr int kMaxN = 8, kB = 256;
+    auto cls = [&](int n) { return (n >= 2 && n <= kMaxN) ? n : 0; };
+    std::vector<int> cnt(kMaxN + 2, 0);
+    for (int n = 0; n < N; ++n) cnt[cls(s->h_net_start[n + 1] - s->h_net_start[n]) + 1]++;
+    for (int k = 0; k <= kMaxN; ++k) cnt[k + 1] += cnt[k];
+    std::vector<int> order(std::max(N, 1)), fill(cnt.begin(), cnt.end() - 1);
+    for (int n = 0; n < N; ++n) order[fill[cls(s->h_net_start[n + 1] - s->h_net_start[n])]++] = n;
+    std::vector<int> new_id(std::max(E, 1), -1), gen_start(std::max(N, 1), 0);
+    std::vector<int4> blk;
+    int pos = 0;
+    for (int k = 2; k <= kMaxN; ++k) {
+        s->wa_cls_blk0[k] = static_cast<int>(blk.size());
+        for (int i = cnt[k]; i < cnt[k + 1]; i += kB) {
+            const int count = std::min(kB, cnt[k + 1] - i);
+            blk.push_back(make_int4(k, i, count, pos));
+            for (int t = 0; t < count; ++t)
+                for (int j = 0; j < k; ++j) new_id[s->h_net_start[order[i + t]] + j] = pos + j * kB + t;
+            pos += kB * k;
+        }
+        s->wa_cls_nblk[k] = static_cast<int>(blk.size()) - s->wa_cls_blk0[k];
+    }
+    s->wa_cls_blk0[0] = static_cast<int>(blk.size());
+    for (int i = cnt[0]; i < cnt[1]; i += kB) blk.push_back(make_int4(0, i, std::min(kB, cnt[1] - i), 0));
+    s->wa_cls_nblk[0] = static_cast<int>(blk.size()) - s->wa_cls_blk0[0];
+    for (int i = cnt[0]; i < cnt[1]; ++i) {
+        const int n = order[i], b0 = s->h_net_start[n], k = s->h_net_start[n + 1] - b0;
+        gen_start[i] = pos;
+        for (int j = 0; j < k; ++j) new_id[b0 + j] = pos + j;
+        pos += k;
+    }
+    s->n_wa_blocks = static_cast<int>(blk.size());
+    s->E_lay = pos;
+    if (blk.empty()) blk.push_back(make_int4(0, 0, 0, 0));
+    s->net_by_size.upload(order, s->st);
+    s->wa_blk.upload(blk, s->st);
+    s->wa_gen_start.upload(gen_start, s->st);
+    std::vector<int> e_cell(std::max(pos, 1), 0), pin_entry(P, -1);
+    std::vector<double2> e_off(std::max(pos, 1), make_double2(0.0, 0.0));
     s->h_pin_net.assign(P, -1);
     for (int n = 0; n < N; ++n)
         for (int e = s->h_net_start[n]; e < s->h_net_start[n + 1]; ++e) {
-            const int p = s->h_net_pins[e];
-            e_cell[e] = s->h_pin_cell[p] >= 0 ? s->h_pin_cell[p] : -1 - p;
-            e_off[e] = make_double2(s->h_pin_off[2 * p], s->h_pin_off[2 * p + 1]);
-            pin_entry[p] = e;
+            const int p = s->h_net_pins[e], id = new_id[e];
+            e_cell[id] = s->h_pin_cell[p] >= 0 ? s->h_pin_cell[p] : -1 - p;
+            e_off[id] = make_double2(s->h_pin_off[2 * p], s->h_pin_off[2 * p + 1]);
+            pin_entry[p] = id;
             s->h_pin_net[p] = n;
         }
     s->e_cell.upload(e_cell, s->st);
     s->e_off.upload(e_off, s->st);
-    {   // WA size classes: nets sorted (stably) by pin count; blocks of 256 nets of one count;
-        // counts outside [2, 8] go to class 0 (generic path)
-        constexpr int kMaxN = 8, kB = 256;
-        auto cls = [&](int n) { return (n >= 2 && n <= kMaxN) ? n : 0; };
-        std::vector<int> cnt(kMaxN + 2, 0);
-        for (int n = 0; n < N; ++n) cnt[cls(s->h_net_start[n + 1] - s->h_net_start[n]) + 1]++;
-        for (int k = 0; k <= kMaxN; ++k) cnt[k + 1] += cnt[k];
-        std::vector<int> order(std::max(N, 1)), fill(cnt.begin(), cnt.end() - 1);
-        for (int n = 0; n < N; ++n) order[fill[cls(s->h_net_start[n + 1] - s->h_net_start[n])]++] = n;
-        std::vector<int4> blk;
-        for (int k = 0; k <= kMaxN; ++k)
-            for (int i = cnt[k]; i < cnt[k + 1]; i += kB) blk.push_back(make_int4(k, i, std::min(kB, cnt[k + 1] - i), 0));
-        if (blk.empty()) blk.push_back(make_int4(0, 0, 0, 0));
-        s->n_wa_blocks = static_cast<int>(blk.size());
-        s->net_by_size.upload(order, s->st);
-        s->wa_blk.upload(blk, s->st);
-    }
     // Cell pins on no net still take pin-pair gradient (pin_pairs.cpp:31-34 writes any pin):
     // they get extra slots after the E net entries, written only by the pin-pair kernel.
     int extra = 0;
     for (int p = 0; p < P; ++p)
-        if (pin_entry[p] < 0 && s->h_pin_cell[p] >= 0) pin_entry[p] = E + extra++;
-    s->E_tot = E + extra;
+        if (pin_entry[p] < 0 && s->h_pin_cell[p] >= 0) pin_entry[p] = pos + extra++;
+    s->E_tot = pos + extra;
     s->h_pin_entry = pin_entry;
     s->pin_entry.upload(pin_entry, s->st);
     // fold CSR: per cell, the entries of its pins in ascending pin id
@@ -419,6 +441,24 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
 
     // state buffers
     s->cell_xy.alloc(C);
+    {   // keep the cell positions (gathered by WA, PP and the fold every iteration) L2-resident
+        int max_persist = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
+        const size_t bytes = sizeof(double2) * static_cast<size_t>(std::max(C, 1));
+        if (max_persist > 0) {
+            const size_t limit = std::min<size_t>(static_cast<size_t>(max_persist), 2 * bytes);
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit) == cudaSuccess) {
+                cudaStreamAttrValue attr{};
+                attr.accessPolicyWindow.base_ptr = s->cell_xy.p;
+                attr.accessPolicyWindow.num_bytes = bytes;
+                attr.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(limit) / static_cast<float>(bytes));
+                attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cudaStreamSetAttribute(s->st, cudaStreamAttributeAccessPolicyWindow, &attr);
+            }
+            cudaGetLastError();
+        }
+    }
     s->d_cell.alloc(C);
     s->grad_e.alloc(std::max(s->E_tot, 1));
     s->grad_e.zero(s->st);
@@ -502,7 +542,8 @@ int tdpg_pp_set(tdpg_session* s, int64_t q, const int32_t* a, const int32_t* b, 
     s->led_w.upload(ww, s->st);
     s->Q = q;
     s->pp_dirty = true;
-    if (s->E_tot > s->E) CK(cudaMemsetAsync(s->grad_e.p + s->E, 0, sizeof(double2) * (s->E_tot - s->E), s->st));
+    if (s->E_tot > s->E_lay)
+        CK(cudaMemsetAsync(s->grad_e.p + s->E_lay, 0, sizeof(double2) * (s->E_tot - s->E_lay), s->st));
     CK(cudaStreamSynchronize(s->st));
     API_END
 }

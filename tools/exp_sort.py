@@ -2,7 +2,7 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2503_11674_b200.engine import Session, generate
 d = generate(seed=1, cells=1_000_000, fail_frac=0.8, calibrate=True)
-for se in ["1000000", "8", "2", "1"]:
+for se in ["1000000", "4", "2", "1"]:
     os.environ["TDPG_SORT_EVERY"] = se
     s = Session(d)
     cfg = {"grid_nx": 1024, "grid_ny": 1024, "m": 15, "timing_start_iter": 0, "max_iters": 400, "seed": 1}

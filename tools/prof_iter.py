@@ -1,15 +1,16 @@
-"""Small driver for ncu: a 1M design, engine warmed up past two timing refreshes, then a
-few plain GP iterations (the launches ncu should capture)."""
+"""Small driver for ncu: a 1M design, engine warmed up for W iterations (default 17, two timing
+refreshes), then a few plain GP iterations (the launches ncu should capture)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2503_11674_b200.engine import Session, generate
 
 cells = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+warm = int(sys.argv[2]) if len(sys.argv) > 2 else 17
 d = generate(seed=1, cells=cells, fail_frac=0.8, calibrate=True)
 s = Session(d)
-s.engine_init({"grid_nx": 1024, "grid_ny": 1024, "m": 15, "timing_start_iter": 0, "max_iters": 200, "seed": 1})
-s.iterate(17)  # refreshes at 0 and 15
+s.engine_init({"grid_nx": 1024, "grid_ny": 1024, "m": 15, "timing_start_iter": 0, "max_iters": warm + 40, "seed": 1})
+s.iterate(warm)
 print("profile window start", flush=True)
 s.iterate(5)
 print(s.engine_stats(), flush=True)
