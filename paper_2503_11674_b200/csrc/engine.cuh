@@ -118,7 +118,7 @@ struct tdpg_session {
     bool pin_xy_external = false; // STA uses caller-provided pin positions (tdpg_set_pin_positions)
 
     // GP scratch
-    tdpg::DBuf<double2> grad_e, d_cell, adam_m, adam_v;
+    tdpg::DBuf<double2> grad_e, d_cell, dgrad; // per-entry WA(+PP) gradient, cell gradient, density gradient
     tdpg::DBuf<double> part; // per-block partial sums
     tdpg::Grid grid;
     tdpg::DBuf<double> net_w;

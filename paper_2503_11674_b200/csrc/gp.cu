@@ -13,61 +13,14 @@ namespace tdpg {
 int api_fail(int kind, const std::string& msg);
 
 // =====================================================================================
-// WA wirelength + exact HPWL, one thread per net (wirelength.cpp:12-85).
-// Writes the net-weighted per-entry gradient w_e * dWA/dpin into grad_e (placer.cpp:298-309:
-// each pin is on <= 1 net, so pin_grad[pin] = 0 + w * g), and per-block partial sums of
-// w_e * WA_e and HPWL_e.
-// =====================================================================================
-// Large nets: three passes over the pins, exps recomputed in the gradient pass like the reference.
-__device__ double wa_dim_mem(int s0, int n, int axis, const int* __restrict__ e_cell,
-                             const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
-                             const double2* __restrict__ anchor, double gamma, double w, double2* __restrict__ grad_e,
-                             double& hp)
-{
-    auto X = [&](int i) {
-        const double2 p = entry_pos(e_cell[s0 + i], e_off[s0 + i], cell_xy, anchor);
-        return axis ? p.y : p.x;
-    };
-    double hi = X(0), lo = hi;
-    for (int i = 0; i < n; ++i) {
-        const double x = X(i);
-        hi = smax(hi, x), lo = smin(lo, x);
-    }
-    double s_max = 0.0, t_max = 0.0, s_min = 0.0, t_min = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const double x = X(i);
-        const double eu = exp((x - hi) / gamma);
-        s_max += eu;
-        t_max += (x - hi) * eu;
-        const double el = exp(-(x - lo) / gamma);
-        s_min += el;
-        t_min += (x - lo) * el;
-    }
-    const double max_term = t_max / s_max;
-    const double min_term = t_min / s_min;
-    for (int i = 0; i < n; ++i) {
-        const double xi = X(i);
-        const double eu = exp((xi - hi) / gamma);
-        const double el = exp(-(xi - lo) / gamma);
-        const double d_max = (eu / s_max) * (1.0 + ((xi - hi) - max_term) / gamma);
-        const double d_min = (el / s_min) * (1.0 - ((xi - lo) - min_term) / gamma);
-        const double gi = w * (d_max - d_min);
-        if (axis) grad_e[s0 + i].y = gi;
-        else grad_e[s0 + i].x = gi;
-    }
-    hp = hi - lo;
-    return (hi - lo) + (max_term - min_term);
-}
-
-// =====================================================================================
 // WA wirelength, size-classed (the fast path).  Nets are sorted once by pin count; every
 // block holds nets of one pin count N (2..kWaMaxN), so one thread per net runs a fully
 // unrolled body with N known at compile time: pins in registers, no divergence, the
 // max/min and the four exponential sums accumulated in the reference's pin order
 // (wirelength.cpp:15-34), the 4 exps per pin computed once and reused for the gradient.
 // Divisions by gamma and by the per-net sums become multiplications by reciprocals.
-// Blocks with N == 0 take the nets outside the classes (more pins) through the generic
-// three-pass code (wa_dim_mem).
+// Entries are laid out slot-major per block so each pin slot is one coalesced access;
+// nets outside the classes (more pins) take k_wa_generic, one warp per net.
 // =====================================================================================
 template <int N>
 __device__ __forceinline__ void wa_axis(const double (&x)[N], double inv_gamma, double (&g)[N], double& value,
@@ -150,7 +103,56 @@ __global__ void __launch_bounds__(kBlock) k_wa_class(int blk0, const int4* __res
     if (threadIdx.x == 0) part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
 }
 
-// Nets outside the classes (more than kWaMaxN pins): three-pass generic code per net.
+// Nets outside the classes (more than kWaMaxN pins): one warp per net, lanes stride over the
+// pins (contiguous in the layout); max/min and the exponential sums reduced with shuffles.
+__device__ __forceinline__ double wsum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void wa_axis_warp(int s0, int n, int axis, const int* __restrict__ e_cell,
+                                             const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
+                                             const double2* __restrict__ anchor, double inv_gamma, double w,
+                                             double2* __restrict__ grad_e, double& value, double& extent)
+{
+    const int lane = threadIdx.x & 31;
+    auto X = [&](int i) {
+        const double2 p = entry_pos(e_cell[s0 + i], e_off[s0 + i], cell_xy, anchor);
+        return axis ? p.y : p.x;
+    };
+    double hi = X(0), lo = hi;
+    for (int i = lane; i < n; i += 32) {
+        const double x = X(i);
+        hi = smax(hi, x), lo = smin(lo, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        hi = smax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        lo = smin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    }
+    double s_max = 0.0, t_max = 0.0, s_min = 0.0, t_min = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double x = X(i);
+        const double eu = exp((x - hi) * inv_gamma), el = exp(-(x - lo) * inv_gamma);
+        s_max += eu, t_max += (x - hi) * eu, s_min += el, t_min += (x - lo) * el;
+    }
+    s_max = wsum(s_max), t_max = wsum(t_max), s_min = wsum(s_min), t_min = wsum(t_min);
+    const double is_max = 1.0 / s_max, is_min = 1.0 / s_min;
+    const double max_term = t_max * is_max, min_term = t_min * is_min;
+    for (int i = lane; i < n; i += 32) {
+        const double x = X(i);
+        const double eu = exp((x - hi) * inv_gamma), el = exp(-(x - lo) * inv_gamma);
+        const double d = (eu * is_max) * (1.0 + ((x - hi) - max_term) * inv_gamma) -
+                         (el * is_min) * (1.0 - ((x - lo) - min_term) * inv_gamma);
+        if (axis) grad_e[s0 + i].y = w * d;
+        else grad_e[s0 + i].x = w * d;
+    }
+    value = (hi - lo) + (max_term - min_term);
+    extent = hi - lo;
+}
+
 __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __restrict__ blk,
                                                        const int* __restrict__ net_by_size,
                                                        const int* __restrict__ gen_start,
@@ -159,28 +161,28 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
                                                        const double2* __restrict__ e_off,
                                                        const double2* __restrict__ cell_xy,
                                                        const double2* __restrict__ anchor,
-                                                       const double* __restrict__ net_w, double gamma,
+                                                       const double* __restrict__ net_w, double inv_gamma,
                                                        double2* __restrict__ grad_e, double* __restrict__ part_wl,
                                                        double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
 {
     __shared__ double sh[kBlock / 32];
     if (ctrl && ctrl->stopped) return;
     const int4 b = blk[blk0 + blockIdx.x];
+    const int lane = threadIdx.x & 31;
     double wl = 0.0, hp = 0.0;
-    if (static_cast<int>(threadIdx.x) < b.z) {
-        const int i = b.y + threadIdx.x;
+    for (int t = threadIdx.x >> 5; t < b.z; t += kBlock / 32) { // one warp per net
+        const int i = b.y + t;
         const int net = net_by_size[i];
         const int s0 = gen_start[i], n = net_start[net + 1] - net_start[net];
         const double w = net_w ? net_w[net] : 1.0;
         if (n < 2) {
-            for (int k = 0; k < n; ++k) grad_e[s0 + k] = make_double2(0.0, 0.0);
-        } else {
-            double hx, hy;
-            const double vx = wa_dim_mem(s0, n, 0, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hx);
-            const double vy = wa_dim_mem(s0, n, 1, e_cell, e_off, cell_xy, anchor, gamma, w, grad_e, hy);
-            wl = w * (vx + vy);
-            hp = hx + hy;
+            for (int k = lane; k < n; k += 32) grad_e[s0 + k] = make_double2(0.0, 0.0);
+            continue;
         }
+        double vx, vy, hx, hy;
+        wa_axis_warp(s0, n, 0, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vx, hx);
+        wa_axis_warp(s0, n, 1, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vy, hy);
+        if (lane == 0) wl += w * (vx + vy), hp += hx + hy;
     }
     const double bw = block_sum<kBlock>(wl, sh);
     const double bh = block_sum<kBlock>(hp, sh);
@@ -471,8 +473,62 @@ __global__ void k_finalize(FinArgs a, Ctrl* ctrl, IterCur* cur)
 }
 
 // =====================================================================================
-// Cell kernel: gradient fold (placer.cpp:318-333) + density gradient (density.cpp:148-156)
-// + Adam (placer.cpp:345-356) + write-back/clamp (placer.cpp:472-476), one thread per cell.
+// Density gradient (density.cpp:148-156), one thread per movable cell in the scatter's spatial
+// order, so neighbouring threads read neighbouring excess bins (L1 hits).  Regrouped per bin
+// column: dgx = sum_bx area*dwx(bx) * 2*sum_by f(bx,by)*wy(by), dgy = sum_bx area*wx(bx) * 2*sum_by f*dwy.
+// =====================================================================================
+__global__ void __launch_bounds__(kBlock) k_dens_grad(int n_mov, const int* __restrict__ perm,
+                                                      const double2* __restrict__ cell_xy,
+                                                      const double2* __restrict__ cell_wh, GridDev g,
+                                                      const double* __restrict__ excess, double2* __restrict__ dgrad,
+                                                      const Ctrl* __restrict__ ctrl)
+{
+    if (ctrl && ctrl->stopped) return;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n_mov) return;
+    const int c = perm[i];
+    const double2 p = cell_xy[c], s = cell_wh[c];
+    const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
+    int bx0, bx1, by0, by1;
+    foot_range(xl, xh, g.x0, g.bw, g.inv_bw, g.nx, bx0, bx1);
+    foot_range(yl, yh, g.y0, g.bh, g.inv_bh, g.ny, by0, by1);
+    const double area = s.x * s.y;
+    const double ilx = 1.0 / s.x, ily = 1.0 / s.y;
+    const int nby = min(by1 - by0 + 1, kFoot);
+    double wyc[kFoot], dwyc[kFoot];
+#pragma unroll
+    for (int j = 0; j < kFoot; ++j) {
+        wyc[j] = 0.0, dwyc[j] = 0.0;
+        if (j < nby) extent_w(yl, yh, g.y0 + (by0 + j + 0.5) * g.bh, g.bh, g.inv_bh, ily, wyc[j], dwyc[j]);
+    }
+    double dgx = 0.0, dgy = 0.0;
+    for (int bx = bx0; bx <= bx1; ++bx) {
+        double wx, dwx;
+        extent_w(xl, xh, g.x0 + (bx + 0.5) * g.bw, g.bw, g.inv_bw, ilx, wx, dwx);
+        if (wx == 0.0 && dwx == 0.0) continue;
+        const double* ex = excess + static_cast<long long>(bx) * g.ny + by0;
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int j = 0; j < kFoot; ++j)
+            if (j < nby) {
+                const double f = ex[j];
+                sx += f * wyc[j], sy += f * dwyc[j];
+            }
+        for (int by = by0 + kFoot; by <= by1; ++by) {
+            double wy, dwy;
+            extent_w(yl, yh, g.y0 + (by + 0.5) * g.bh, g.bh, g.inv_bh, ily, wy, dwy);
+            const double fe = excess[static_cast<long long>(bx) * g.ny + by];
+            sx += fe * wy, sy += fe * dwy;
+        }
+        dgx += (area * dwx) * (2.0 * sx);
+        dgy += (area * wx) * (2.0 * sy);
+    }
+    dgrad[c] = make_double2(dgx, dgy);
+}
+
+// =====================================================================================
+// Cell kernel: gradient fold (placer.cpp:318-333) + lambda * density gradient + Adam
+// (placer.cpp:345-356) + write-back / clamp (placer.cpp:472-476), one thread per cell.
 // =====================================================================================
 struct CellArgs {
     int C;
@@ -482,8 +538,7 @@ struct CellArgs {
     const uint8_t* fixed;
     double2* xy;
     const double2* wh;
-    GridDev g;
-    const double* excess;
+    const double2* dgrad;
     double2* d_cell;    // optional gradient output
     double2* m;         // Adam state (iteration mode)
     double2* v;
@@ -513,49 +568,14 @@ __global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __r
         if (a.d_cell) a.d_cell[c] = make_double2(0.0, 0.0);
         return;
     }
-    const double2 p = a.xy[c], s = a.wh[c];
-    const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
-    int bx0, bx1, by0, by1;
-    foot_range(xl, xh, a.g.x0, a.g.bw, a.g.inv_bw, a.g.nx, bx0, bx1);
-    foot_range(yl, yh, a.g.y0, a.g.bh, a.g.inv_bh, a.g.ny, by0, by1);
-    const double area = s.x * s.y;
-    const double ilx = 1.0 / s.x, ily = 1.0 / s.y;
-    const int nby = min(by1 - by0 + 1, kFoot);
-    double wyc[kFoot], dwyc[kFoot];
-#pragma unroll
-    for (int j = 0; j < kFoot; ++j) {
-        wyc[j] = 0.0, dwyc[j] = 0.0;
-        if (j < nby) extent_w(yl, yh, a.g.y0 + (by0 + j + 0.5) * a.g.bh, a.g.bh, a.g.inv_bh, ily, wyc[j], dwyc[j]);
-    }
-    // density gradient (density.cpp:148-156), regrouped per bin column:
-    //   dgx = sum_bx area*dwx(bx) * sum_by f(bx,by)*wy(by),  dgy = sum_bx area*wx(bx) * sum_by f*dwy(by)
-    double dgx = 0.0, dgy = 0.0;
-    for (int bx = bx0; bx <= bx1; ++bx) {
-        double wx, dwx;
-        extent_w(xl, xh, a.g.x0 + (bx + 0.5) * a.g.bw, a.g.bw, a.g.inv_bw, ilx, wx, dwx);
-        if (wx == 0.0 && dwx == 0.0) continue;
-        const double* ex = a.excess + static_cast<long long>(bx) * a.g.ny + by0;
-        double f[kFoot];
-#pragma unroll
-        for (int j = 0; j < kFoot; ++j) f[j] = j < nby ? ex[j] : 0.0;
-        double sx = 0.0, sy = 0.0;
-#pragma unroll
-        for (int j = 0; j < kFoot; ++j) sx += f[j] * wyc[j], sy += f[j] * dwyc[j];
-        for (int by = by0 + kFoot; by <= by1; ++by) {
-            double wy, dwy;
-            extent_w(yl, yh, a.g.y0 + (by + 0.5) * a.g.bh, a.g.bh, a.g.inv_bh, ily, wy, dwy);
-            const double fe = a.excess[static_cast<long long>(bx) * a.g.ny + by];
-            sx += fe * wy, sy += fe * dwy;
-        }
-        dgx += (area * dwx) * (2.0 * sx);
-        dgy += (area * wx) * (2.0 * sy);
-    }
+    const double2 dg = a.dgrad[c];
     const double lambda = cur->lambda;
-    gx += lambda * dgx;
-    gy += lambda * dgy;
+    gx += lambda * dg.x;
+    gy += lambda * dg.y;
     if (ctrl && !(isfinite(gx) && isfinite(gy))) atomicMin(&ctrl->nonfinite_at, cur->iter);
     if (a.d_cell) a.d_cell[c] = make_double2(gx, gy);
     if (!adam) return;
+    const double2 p = a.xy[c], s = a.wh[c];
     double2 m = a.m[c], v = a.v[c];
     const double lr = cur->lr, c1 = cur->c1, c2 = cur->c2;
     m.x = a.b1 * m.x + (1.0 - a.b1) * gx;
@@ -723,7 +743,7 @@ void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* pa
     if (s->wa_cls_nblk[0]) {
         k_wa_generic<<<s->wa_cls_nblk[0], kBlock, 0, s->st>>>(s->wa_cls_blk0[0], s->wa_blk, s->net_by_size,
                                                               s->wa_gen_start, s->net_start, s->e_cell, s->e_off,
-                                                              s->cell_xy, s->anchor, nw, gamma, s->grad_e, part_wl,
+                                                              s->cell_xy, s->anchor, nw, ig, s->grad_e, part_wl,
                                                               part_hp, ctrl);
         CK_LAUNCH();
     }
@@ -813,13 +833,25 @@ CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, dou
     a.fixed = s->cell_fixed;
     a.xy = s->cell_xy;
     a.wh = s->cell_wh;
-    a.g = grid_dev(s);
-    a.excess = s->grid.excess;
+    a.dgrad = s->dgrad;
     a.d_cell = d_cell;
     a.m = m, a.v = v;
     a.b1 = b1, a.b2 = b2, a.eps = eps;
     a.core_x0 = s->core[0], a.core_y0 = s->core[1], a.core_x1 = s->core[2], a.core_y1 = s->core[3];
     return a;
+}
+
+// density gradient then the cell kernel
+void launch_cell_pass(tdpg_session* s, const CellArgs& ca, const IterCur* cur, Ctrl* ctrl)
+{
+    const int n_mov = s->grid.n_movable;
+    if (n_mov > 0) {
+        k_dens_grad<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(n_mov, s->grid.perm, s->cell_xy, s->cell_wh,
+                                                                     grid_dev(s), s->grid.excess, s->dgrad, ctrl);
+        CK_LAUNCH();
+    }
+    k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, ctrl);
+    CK_LAUNCH();
 }
 
 // One full objective_and_gradient evaluation at the session's positions.
@@ -850,8 +882,7 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
     k_finalize<<<1, kBlock, 0, s->st>>>(fa, nullptr, cur);
     CK_LAUNCH();
     const CellArgs ca = cell_args(s, s->d_cell, nullptr, nullptr, 0, 0, 0);
-    k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, nullptr);
-    CK_LAUNCH();
+    launch_cell_pass(s, ca, cur, nullptr);
     Terms t;
     CK(cudaMemcpyAsync(&t, terms, sizeof(Terms), cudaMemcpyDeviceToHost, s->st));
     if (d_cell_host) s->d_cell.download(reinterpret_cast<double2*>(d_cell_host), s->C, s->st);
@@ -938,8 +969,7 @@ int tdpg_density(tdpg_session* s, double* value, double* overflow, double* d_cel
     if (d_cell) {
         s->grad_e.zero(s->st, s->E_tot);
         const CellArgs ca = cell_args(s, s->d_cell, nullptr, nullptr, 0, 0, 0);
-        k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, nullptr);
-        CK_LAUNCH();
+        launch_cell_pass(s, ca, cur, nullptr);
         s->d_cell.download(reinterpret_cast<double2*>(d_cell), s->C, s->st);
     }
     Terms t;
@@ -1077,7 +1107,6 @@ void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, doub
                   const IterCur* cur, Ctrl* ctrl)
 {
     const CellArgs ca = cell_args(s, d_cell, m, v, b1, b2, eps);
-    k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, ctrl);
-    CK_LAUNCH();
+    launch_cell_pass(s, ca, cur, ctrl);
 }
 } // namespace tdpg

@@ -390,7 +390,8 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         s->wa_cls_nblk[k] = static_cast<int>(blk.size()) - s->wa_cls_blk0[k];
     }
     s->wa_cls_blk0[0] = static_cast<int>(blk.size());
-    for (int i = cnt[0]; i < cnt[1]; i += kB) blk.push_back(make_int4(0, i, std::min(kB, cnt[1] - i), 0));
+    constexpr int kGenNets = 32; // generic nets per block: one warp per net, 8 warps loop over them
+    for (int i = cnt[0]; i < cnt[1]; i += kGenNets) blk.push_back(make_int4(0, i, std::min(kGenNets, cnt[1] - i), 0));
     s->wa_cls_nblk[0] = static_cast<int>(blk.size()) - s->wa_cls_blk0[0];
     for (int i = cnt[0]; i < cnt[1]; ++i) {
         const int n = order[i], b0 = s->h_net_start[n], k = s->h_net_start[n + 1] - b0;
@@ -460,6 +461,8 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         }
     }
     s->d_cell.alloc(C);
+    s->dgrad.alloc(std::max(C, 1));
+    s->dgrad.zero(s->st);
     s->grad_e.alloc(std::max(s->E_tot, 1));
     s->grad_e.zero(s->st);
     s->pin_xy.alloc(P);
