@@ -15,6 +15,7 @@
 //   ledger    : sorted 64-bit pair keys (a<<32|b) + weights; per-pin incidence CSR
 #pragma once
 
+#include <array>
 #include <memory>
 #include <string>
 #include <vector>
@@ -107,7 +108,10 @@ struct tdpg_session {
     tdpg::DBuf<uint8_t> ak, rk, tie;
     tdpg::DBuf<int> pred, tie_list, counters; // counters: [0] tie count
     tdpg::DBuf<int> d_level, tie_scratch;
-    tdpg::DBuf<double> sta_out; // tns, wns, n_violated
+    tdpg::DBuf<double> sta_out;  // tns, wns, n_violated
+    tdpg::DBuf<double> sta_part; // STA reduction partials
+    cudaGraphExec_t sta_gexec = nullptr; // the per-level STA sweep, captured once
+    std::array<const void*, 6> sta_graph_key{};
     // ledger-update scratch
     tdpg::DBuf<uint8_t> lg_flag;
     tdpg::DBuf<double> lg_w, lg_new_w;

@@ -386,6 +386,7 @@ __global__ void k_spatial_keys(int C, const double2* __restrict__ cell_xy, const
     vals[c] = c;
 }
 
+// Two bins per thread (16-byte loads/stores); one pass: read the accumulator, reset it, write excess.
 __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g, long long* __restrict__ acc,
                                                          const double* __restrict__ base,
                                                          double* __restrict__ excess, double* __restrict__ part_d,
@@ -394,16 +395,27 @@ __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g,
     __shared__ double sh[kBlock / 32];
     if (ctrl && ctrl->stopped) return;
     double v2 = 0.0, v1 = 0.0;
-    for (long long b = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; b < B;
-         b += static_cast<long long>(gridDim.x) * kBlock) {
-        const long long q = acc[b];
-        acc[b] = 0;
+    const long long b = 2 * (blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x);
+    auto one = [&](long long q, long long k, double& ex) {
         const double mov = static_cast<double>(q) * g.inv_scale;
-        const double occ = base ? base[b] + mov : mov;
-        const double ex = smax(0.0, occ - g.cap);
-        excess[b] = ex;
+        const double occ = base ? base[k] + mov : mov;
+        ex = smax(0.0, occ - g.cap);
         v2 += ex * ex;
         v1 += ex;
+    };
+    if (b + 1 < B) {
+        const longlong2 q = *reinterpret_cast<const longlong2*>(acc + b);
+        *reinterpret_cast<longlong2*>(acc + b) = make_longlong2(0, 0);
+        double2 ex;
+        one(q.x, b, ex.x);
+        one(q.y, b + 1, ex.y);
+        *reinterpret_cast<double2*>(excess + b) = ex;
+    } else if (b < B) {
+        const long long q = acc[b];
+        acc[b] = 0;
+        double ex;
+        one(q, b, ex);
+        excess[b] = ex;
     }
     const double s2 = block_sum<kBlock>(v2, sh);
     const double s1 = block_sum<kBlock>(v1, sh);
@@ -416,9 +428,11 @@ __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g,
 // =====================================================================================
 
 
-__global__ void k_finalize(FinArgs a, Ctrl* ctrl, IterCur* cur)
+constexpr int kFinBlock = 1024;
+
+__global__ void __launch_bounds__(kFinBlock) k_finalize(FinArgs a, Ctrl* ctrl, IterCur* cur)
 {
-    __shared__ double sh[kBlock / 32];
+    __shared__ double sh[kFinBlock / 32];
     __shared__ int skip;
     if (threadIdx.x == 0) skip = ctrl ? ctrl->stopped : 0;
     __syncthreads();
@@ -427,14 +441,14 @@ __global__ void k_finalize(FinArgs a, Ctrl* ctrl, IterCur* cur)
         return;
     }
     double wl = 0, hp = 0, pp = 0, d2 = 0, d1 = 0;
-    for (int i = threadIdx.x; i < a.nb_wa; i += kBlock) wl += a.part_wl[i], hp += a.part_hp[i];
-    for (int i = threadIdx.x; i < a.nb_pp; i += kBlock) pp += a.part_pp[i];
-    for (int i = threadIdx.x; i < a.nb_d; i += kBlock) d2 += a.part_d[2 * i], d1 += a.part_d[2 * i + 1];
-    wl = block_sum<kBlock>(wl, sh);
-    hp = block_sum<kBlock>(hp, sh);
-    pp = block_sum<kBlock>(pp, sh);
-    d2 = block_sum<kBlock>(d2, sh);
-    d1 = block_sum<kBlock>(d1, sh);
+    for (int i = threadIdx.x; i < a.nb_wa; i += kFinBlock) wl += a.part_wl[i], hp += a.part_hp[i];
+    for (int i = threadIdx.x; i < a.nb_pp; i += kFinBlock) pp += a.part_pp[i];
+    for (int i = threadIdx.x; i < a.nb_d; i += kFinBlock) d2 += a.part_d[2 * i], d1 += a.part_d[2 * i + 1];
+    wl = block_sum<kFinBlock>(wl, sh);
+    hp = block_sum<kFinBlock>(hp, sh);
+    pp = block_sum<kFinBlock>(pp, sh);
+    d2 = block_sum<kFinBlock>(d2, sh);
+    d1 = block_sum<kFinBlock>(d1, sh);
     if (threadIdx.x != 0) return;
     const int it = ctrl ? ctrl->iter : 0;
     const double lambda = a.sched ? a.sched[it].lambda : a.lambda_single;
@@ -640,7 +654,7 @@ int wa_blocks(const tdpg_session* s) { return std::max(1, s->n_wa_blocks); }
 int pp_blocks(const tdpg_session*) { return 148 * 4; }
 int bins_blocks(const tdpg_session* s)
 {
-    return std::max(1, std::min(148 * 8, static_cast<int>(blocks_for(s->grid.bins(), kBlock))));
+    return std::max(1, static_cast<int>(blocks_for((s->grid.bins() + 1) / 2, kBlock)));
 }
 
 // Per-pin incidence CSR of the ledger (rebuilt when the ledger changes).
@@ -879,7 +893,7 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
     fa.nb_wa = nb_wa, fa.nb_pp = pp ? nb_pp : 0, fa.nb_d = nb_d;
     fa.total_movable = s->grid.total_movable, fa.beta = beta, fa.sched = nullptr, fa.lambda_single = lambda;
     fa.terms = terms;
-    k_finalize<<<1, kBlock, 0, s->st>>>(fa, nullptr, cur);
+    k_finalize<<<1, kFinBlock, 0, s->st>>>(fa, nullptr, cur);
     CK_LAUNCH();
     const CellArgs ca = cell_args(s, s->d_cell, nullptr, nullptr, 0, 0, 0);
     launch_cell_pass(s, ca, cur, nullptr);
@@ -964,7 +978,7 @@ int tdpg_density(tdpg_session* s, double* value, double* overflow, double* d_cel
     FinArgs fa{};
     fa.part_d = part_d, fa.nb_d = nb_d, fa.total_movable = s->grid.total_movable, fa.lambda_single = 1.0;
     fa.terms = terms;
-    k_finalize<<<1, kBlock, 0, s->st>>>(fa, nullptr, cur);
+    k_finalize<<<1, kFinBlock, 0, s->st>>>(fa, nullptr, cur);
     CK_LAUNCH();
     if (d_cell) {
         s->grad_e.zero(s->st, s->E_tot);
@@ -1100,7 +1114,7 @@ void launch_pp_ctrl(tdpg_session* s, int kind, double beta, double* pp, int nb, 
 void launch_density_ctrl(tdpg_session* s, double* pd, int nb, const Ctrl* ctrl) { launch_density(s, pd, nb, ctrl); }
 void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur)
 {
-    k_finalize<<<1, kBlock, 0, s->st>>>(fa, ctrl, cur);
+    k_finalize<<<1, kFinBlock, 0, s->st>>>(fa, ctrl, cur);
     CK_LAUNCH();
 }
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,

@@ -7,7 +7,9 @@
 // graph is identical every iteration.  The timing refresh (STA + extraction + ledger
 // update, placer.cpp:415-435) runs on the same stream before the scheduled iterations.
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
@@ -246,15 +248,29 @@ bool timing_refresh(tdpg_session* s)
         return false;
     }
     s->pin_xy_external = false;
+    static const bool trace = std::getenv("TDPG_TRACE_REFRESH") != nullptr;
+    auto stamp = [&](const char* what) {
+        if (!trace) return;
+        static auto t0 = std::chrono::steady_clock::now();
+        CK(cudaStreamSynchronize(s->st));
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "[refresh %d] %-10s %.3f ms\n", E.launched, what, ms);
+        t0 = std::chrono::steady_clock::now();
+    };
+    stamp("start");
     run_sta_dev(s);
+    stamp("sta");
     const double row[3] = {1.0, s->tns, s->wns};
     CK(cudaMemcpyAsync(E.timing_row.p, row, sizeof row, cudaMemcpyHostToDevice, s->st));
     const int one = 1;
     CK(cudaMemcpyAsync(&E.ctrl.p->engaged, &one, sizeof one, cudaMemcpyHostToDevice, s->st));
     if (s->wns < 0.0) {
         extract_endpoint_dev(s, 0); // n = number of violated endpoints (placer.cpp:424-428)
+        stamp("extract");
         ledger_apply_sorted(s, s->n_hits, s->wns, E.cfg.w0, E.cfg.w1);
+        stamp("ledger");
         rebuild_pp_incidence(s);
+        stamp("incidence");
     } else {
         s->n_paths = 0, s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0; // empty report
     }
@@ -302,6 +318,7 @@ int engine_run(tdpg_session* s, int n)
 tdpg_session::~tdpg_session()
 {
     delete eng; // Engine is complete here
+    if (sta_gexec) cudaGraphExecDestroy(sta_gexec);
     if (st) {
         cudaStreamSynchronize(st);
         cudaCtxResetPersistingL2Cache(); // release the L2 lines this session pinned

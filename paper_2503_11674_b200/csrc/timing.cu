@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cmath>
 
@@ -343,8 +344,9 @@ StaArgs sta_args(tdpg_session* s)
 }
 
 // Full STA at the current positions; leaves endpoint keys in sort_k0/sort_v0 and
-// [tns, wns, n_violated] in counters-adjacent scratch. Stream-ordered, no host sync.
-void run_sta_async(tdpg_session* s, double* out3)
+// [tns, wns, n_violated] in out3. Stream-ordered, no host sync.  The 2L per-level launches are
+// captured once into a CUDA graph (re-captured only if a buffer it uses moved).
+void sta_record(tdpg_session* s, double* out3)
 {
     const int P = s->P;
     if (!s->pin_xy_external) { // pin positions from the cells (netlist.cpp:23-32) unless the caller gave them
@@ -364,15 +366,33 @@ void run_sta_async(tdpg_session* s, double* out3)
         if (hi > lo) k_required<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, a);
     }
     CK_LAUNCH();
+    const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
+    k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0, s->sort_v0,
+                                           s->sta_part);
+    CK_LAUNCH();
+    k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->sta_part, out3);
+    CK_LAUNCH();
+}
+
+void run_sta_async(tdpg_session* s, double* out3)
+{
     const size_t ep = static_cast<size_t>(std::max(s->EP, 1));
     s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
-    const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
-    s->part.reserve(3 * nb + 8);
-    k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0, s->sort_v0,
-                                           s->part);
-    CK_LAUNCH();
-    k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
-    CK_LAUNCH();
+    const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(s->P, s->EP), kBlock))));
+    s->sta_part.reserve(3 * nb + 8);
+    const std::array<const void*, 6> key = {s->pin_xy_external ? s->pin_xy.p : nullptr, s->cell_xy.p, s->sort_k0.p,
+                                            s->sort_v0.p, s->sta_part.p, out3};
+    if (!s->sta_gexec || key != s->sta_graph_key) {
+        if (s->sta_gexec) cudaGraphExecDestroy(s->sta_gexec), s->sta_gexec = nullptr;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
+        sta_record(s, out3);
+        CK(cudaStreamEndCapture(s->st, &g));
+        CK(cudaGraphInstantiate(&s->sta_gexec, g, 0));
+        cudaGraphDestroy(g);
+        s->sta_graph_key = key;
+    }
+    CK(cudaGraphLaunch(s->sta_gexec, s->st));
 }
 
 void run_sta_dev(tdpg_session* s)
