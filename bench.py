@@ -55,16 +55,20 @@ def dist_env():
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=None):
         self.index, self.rows, self.proc = index, [], None
+        self.period_ms = period_ms or int(os.environ.get("TDPG_CLOCK_MS", "100"))
 
     def __enter__(self):
+        if self.period_ms <= 0:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, stdin=subprocess.DEVNULL,
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()

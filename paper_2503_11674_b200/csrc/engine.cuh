@@ -98,6 +98,11 @@ struct tdpg_session {
     tdpg::DBuf<int4> wa_blk;
     int n_wa_blocks = 0, E_lay = 0;
     int wa_cls_blk0[9] = {0}, wa_cls_nblk[9] = {0};
+    // engine-mode pin pairs (dense ledger indexed by sink pin; fused into WA)
+    tdpg::DBuf<uint32_t> pp_mask, pp_ord;   // per class-ordered net
+    tdpg::DBuf<int> wa_gen_ord, pin_loc, pin_driver;
+    tdpg::DBuf<double> ppw_e, dl_w;        // pair weight per WA slot / per sink pin (0 = none)
+    std::vector<int> h_pin_driver;
 
     // device timing graph
     tdpg::DBuf<int> lvl_pins, in_start, in_from, out_start, out_to, ep_sorted;
@@ -147,6 +152,14 @@ struct tdpg_session {
     bool hits_sorted = false;
     double last_sta_ms = 0, last_extract_ms = 0;
 
+    // engine-mode refresh buffers (capacity-sized; hits keyed by sink pin)
+    tdpg::DBuf<unsigned> eh_key, eh_key_s;
+    tdpg::DBuf<int> eh_idx, eh_idx_s;
+    tdpg::DBuf<double> eh_slack;
+    tdpg::DBuf<long long> ex_counts;                 // n_paths, path pins, hits of the last refresh
+    tdpg::DBuf<unsigned long long> q_count;          // pairs in the dense ledger
+    long long hcap = 0;
+
     // sort / scan scratch
     tdpg::DBuf<unsigned char> cub_tmp;
     tdpg::DBuf<unsigned long long> sort_k0, sort_k1;
@@ -182,6 +195,9 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
 
 // timing.cu
 void run_sta_dev(tdpg_session* s);
+void refresh_reserve(tdpg_session* s);
+void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting);
+void dense_ledger_to_sorted(tdpg_session* s);
 void extract_endpoint_dev(tdpg_session* s, int n);
 void resolve_ties_dev(tdpg_session* s);
 void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool hits_all_violated);

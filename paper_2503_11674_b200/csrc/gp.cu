@@ -55,11 +55,57 @@ __device__ __forceinline__ void wa_axis(const double (&x)[N], double inv_gamma, 
     extent = hi - lo;
 }
 
+// Pin-pair attraction fused into WA (engine mode).  Every pair the engine's extraction creates is
+// a net arc (driver, sink) (paths.cpp:195-200), so a net's pairs are exactly its sinks with a ledger
+// weight, and both pins' positions are already in this thread's registers.  Per pin the reference
+// accumulates pp.d_pin in map-key order (pin_pairs.cpp:22-34): a sink has one term, the driver one
+// term per pair in ascending sink pin id (the per-net order word).  Sink term = (2w)(p_s - p_d)
+// (quadratic) or w(p_s - p_d)/dist (linear) whichever pin is `first`; the driver subtracts them.
+struct PPArgs {
+    const uint32_t* mask;  // per class-ordered net: bit j = sink slot j has a pair
+    const uint32_t* ord;   // per class-ordered net: sink slots in ascending pin id, 3 bits each
+    const double* w_e;     // pair weight per WA entry slot (0 = no pair)
+    double beta;
+    int kind;              // 0 quadratic, 1 linear
+};
+
+template <int N>
+__device__ __forceinline__ void pp_net(const PPArgs& pp, uint32_t mask, uint32_t ord, int base, const double (&x)[N],
+                                       const double (&y)[N], double (&px)[N], double (&py)[N], double& val)
+{
+#pragma unroll
+    for (int j = 0; j < N; ++j) px[j] = 0.0, py[j] = 0.0;
+#pragma unroll
+    for (int j = 1; j < N; ++j) {
+        if (!(mask >> j & 1u)) continue;
+        const double w = pp.w_e[base + j * kBlock];
+        const double dx = x[j] - x[0], dy = y[j] - y[0];
+        if (pp.kind == 0) {
+            val += w * (dx * dx + dy * dy);
+            px[j] = 2.0 * w * dx, py[j] = 2.0 * w * dy;
+        } else {
+            const double dist = sqrt(dx * dx + dy * dy);
+            val += w * dist;
+            if (dist > 0.0) px[j] = w * dx / dist, py[j] = w * dy / dist;
+        }
+    }
+    double sx = 0.0, sy = 0.0; // driver: terms in ascending sink pin id
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) {
+        const int j = (ord >> (3 * k)) & 7;
+#pragma unroll
+        for (int q = 1; q < N; ++q)
+            if (q == j && (mask >> q & 1u)) sx -= px[q], sy -= py[q];
+    }
+    px[0] = sx, py[0] = sy;
+}
+
 template <int N>
 __device__ __forceinline__ void wa_net_slots(int base, double w, const int* __restrict__ e_cell,
                                              const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
                                              const double2* __restrict__ anchor, double inv_gamma,
-                                             double2* __restrict__ grad_e, double& wl, double& hp)
+                                             double2* __restrict__ grad_e, double& wl, double& hp,
+                                             const PPArgs* pp, uint32_t mask, uint32_t ord, double& ppv)
 {
     double x[N], y[N], gx[N], gy[N];
 #pragma unroll
@@ -71,8 +117,17 @@ __device__ __forceinline__ void wa_net_slots(int base, double w, const int* __re
     double vx, vy, hx, hy;
     wa_axis<N>(x, inv_gamma, gx, vx, hx);
     wa_axis<N>(y, inv_gamma, gy, vy, hy);
+    if (pp && mask) {
+        double px[N], py[N];
+        pp_net<N>(*pp, mask, ord, base, x, y, px, py, ppv);
+        // fold term pin_grad + beta * pp.d_pin (placer.cpp:323)
 #pragma unroll
-    for (int i = 0; i < N; ++i) grad_e[base + i * kBlock] = make_double2(w * gx[i], w * gy[i]);
+        for (int i = 0; i < N; ++i)
+            grad_e[base + i * kBlock] = make_double2(w * gx[i] + pp->beta * px[i], w * gy[i] + pp->beta * py[i]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) grad_e[base + i * kBlock] = make_double2(w * gx[i], w * gy[i]);
+    }
     wl = w * (vx + vy);
     hp = hx + hy;
 }
@@ -88,19 +143,28 @@ __global__ void __launch_bounds__(kBlock) k_wa_class(int blk0, const int4* __res
                                                      const double2* __restrict__ anchor,
                                                      const double* __restrict__ net_w, double inv_gamma,
                                                      double2* __restrict__ grad_e, double* __restrict__ part_wl,
-                                                     double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
+                                                     double* __restrict__ part_hp, PPArgs pp, double* __restrict__ part_pp,
+                                                     const Ctrl* __restrict__ ctrl)
 {
     __shared__ double sh[kBlock / 32];
     if (ctrl && ctrl->stopped) return;
     const int4 b = blk[blk0 + blockIdx.x]; // (N, first in net_by_size, count, entry base)
-    double wl = 0.0, hp = 0.0;
+    double wl = 0.0, hp = 0.0, ppv = 0.0;
     if (static_cast<int>(threadIdx.x) < b.z) {
-        const double w = net_w ? net_w[net_by_size[b.y + threadIdx.x]] : 1.0;
-        wa_net_slots<N>(b.w + threadIdx.x, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp);
+        const int i = b.y + threadIdx.x;
+        const double w = net_w ? net_w[net_by_size[i]] : 1.0;
+        const uint32_t mask = pp.mask ? pp.mask[i] : 0u;
+        const uint32_t ord = mask ? pp.ord[i] : 0u;
+        wa_net_slots<N>(b.w + threadIdx.x, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, wl, hp,
+                        pp.mask ? &pp : nullptr, mask, ord, ppv);
     }
     const double bw = block_sum<kBlock>(wl, sh);
     const double bh = block_sum<kBlock>(hp, sh);
-    if (threadIdx.x == 0) part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
+    const double bp = part_pp ? block_sum<kBlock>(ppv, sh) : 0.0;
+    if (threadIdx.x == 0) {
+        part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
+        if (part_pp) part_pp[blk0 + blockIdx.x] = bp;
+    }
 }
 
 // Nets outside the classes (more than kWaMaxN pins): one warp per net, lanes stride over the
@@ -163,13 +227,15 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
                                                        const double2* __restrict__ anchor,
                                                        const double* __restrict__ net_w, double inv_gamma,
                                                        double2* __restrict__ grad_e, double* __restrict__ part_wl,
-                                                       double* __restrict__ part_hp, const Ctrl* __restrict__ ctrl)
+                                                       double* __restrict__ part_hp, PPArgs pp,
+                                                       const int* __restrict__ gen_ord, double* __restrict__ part_pp,
+                                                       const Ctrl* __restrict__ ctrl)
 {
     __shared__ double sh[kBlock / 32];
     if (ctrl && ctrl->stopped) return;
     const int4 b = blk[blk0 + blockIdx.x];
     const int lane = threadIdx.x & 31;
-    double wl = 0.0, hp = 0.0;
+    double wl = 0.0, hp = 0.0, ppv = 0.0;
     for (int t = threadIdx.x >> 5; t < b.z; t += kBlock / 32) { // one warp per net
         const int i = b.y + t;
         const int net = net_by_size[i];
@@ -183,10 +249,45 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
         wa_axis_warp(s0, n, 0, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vx, hx);
         wa_axis_warp(s0, n, 1, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vy, hy);
         if (lane == 0) wl += w * (vx + vy), hp += hx + hy;
+        if (pp.w_e) { // rare large nets: lane 0 walks the sinks in ascending pin id
+            __syncwarp();
+            if (lane == 0) {
+                const double2 pd = entry_pos(e_cell[s0], e_off[s0], cell_xy, anchor);
+                double sx = 0.0, sy = 0.0;
+                for (int k = 0; k + 1 < n; ++k) {
+                    const int j = gen_ord[s0 + k];
+                    const double wt = pp.w_e[s0 + j];
+                    if (wt == 0.0) continue;
+                    const double2 ps = entry_pos(e_cell[s0 + j], e_off[s0 + j], cell_xy, anchor);
+                    const double dx = ps.x - pd.x, dy = ps.y - pd.y;
+                    double gx = 0.0, gy = 0.0;
+                    if (pp.kind == 0) {
+                        ppv += wt * (dx * dx + dy * dy);
+                        gx = 2.0 * wt * dx, gy = 2.0 * wt * dy;
+                    } else {
+                        const double dist = sqrt(dx * dx + dy * dy);
+                        ppv += wt * dist;
+                        if (dist > 0.0) gx = wt * dx / dist, gy = wt * dy / dist;
+                    }
+                    double2 ge = grad_e[s0 + j];
+                    ge.x = ge.x + pp.beta * gx, ge.y = ge.y + pp.beta * gy;
+                    grad_e[s0 + j] = ge;
+                    sx -= gx, sy -= gy;
+                }
+                double2 gd = grad_e[s0];
+                gd.x = gd.x + pp.beta * sx, gd.y = gd.y + pp.beta * sy;
+                grad_e[s0] = gd;
+            }
+            __syncwarp();
+        }
     }
     const double bw = block_sum<kBlock>(wl, sh);
     const double bh = block_sum<kBlock>(hp, sh);
-    if (threadIdx.x == 0) part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
+    const double bp = part_pp ? block_sum<kBlock>(ppv, sh) : 0.0;
+    if (threadIdx.x == 0) {
+        part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
+        if (part_pp) part_pp[blk0 + blockIdx.x] = bp;
+    }
 }
 
 // =====================================================================================
@@ -732,35 +833,46 @@ void rebuild_pp_incidence(tdpg_session* s)
 }
 
 template <int N>
-void launch_wa_class(tdpg_session* s, const double* nw, double inv_gamma, double* pw, double* ph, const Ctrl* ctrl)
+void launch_wa_class(tdpg_session* s, const double* nw, double inv_gamma, double* pw, double* ph, const PPArgs& pp,
+                     double* ppart, const Ctrl* ctrl)
 {
     if (!s->wa_cls_nblk[N]) return;
     k_wa_class<N><<<s->wa_cls_nblk[N], kBlock, 0, s->st>>>(s->wa_cls_blk0[N], s->wa_blk, s->net_by_size, s->e_cell,
                                                            s->e_off, s->cell_xy, s->anchor, nw, inv_gamma, s->grad_e,
-                                                           pw, ph, ctrl);
+                                                           pw, ph, pp, ppart, ctrl);
     CK_LAUNCH();
+}
+
+// WA (+ fused pin pairs when pp_fused: the engine's dense ledger) over all size classes.
+void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp,
+                          bool pp_fused, int kind, double beta, double* part_pp, const Ctrl* ctrl)
+{
+    const double* nw = use_net_w ? s->net_w.p : nullptr;
+    const double ig = 1.0 / gamma;
+    PPArgs pp{nullptr, nullptr, nullptr, beta, kind};
+    if (pp_fused) pp = PPArgs{s->pp_mask.p, s->pp_ord.p, s->ppw_e.p, beta, kind};
+    double* ppart = pp_fused ? part_pp : nullptr;
+    launch_wa_class<2>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    launch_wa_class<3>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    launch_wa_class<4>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    launch_wa_class<5>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    launch_wa_class<6>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    launch_wa_class<7>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    launch_wa_class<8>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    if (s->wa_cls_nblk[0]) {
+        k_wa_generic<<<s->wa_cls_nblk[0], kBlock, 0, s->st>>>(s->wa_cls_blk0[0], s->wa_blk, s->net_by_size,
+                                                              s->wa_gen_start, s->net_start, s->e_cell, s->e_off,
+                                                              s->cell_xy, s->anchor, nw, ig, s->grad_e, part_wl,
+                                                              part_hp, pp, s->wa_gen_ord, ppart, ctrl);
+        CK_LAUNCH();
+    }
 }
 
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk,
                        const Ctrl* ctrl)
 {
     (void)nblk;
-    const double* nw = use_net_w ? s->net_w.p : nullptr;
-    const double ig = 1.0 / gamma;
-    launch_wa_class<2>(s, nw, ig, part_wl, part_hp, ctrl);
-    launch_wa_class<3>(s, nw, ig, part_wl, part_hp, ctrl);
-    launch_wa_class<4>(s, nw, ig, part_wl, part_hp, ctrl);
-    launch_wa_class<5>(s, nw, ig, part_wl, part_hp, ctrl);
-    launch_wa_class<6>(s, nw, ig, part_wl, part_hp, ctrl);
-    launch_wa_class<7>(s, nw, ig, part_wl, part_hp, ctrl);
-    launch_wa_class<8>(s, nw, ig, part_wl, part_hp, ctrl);
-    if (s->wa_cls_nblk[0]) {
-        k_wa_generic<<<s->wa_cls_nblk[0], kBlock, 0, s->st>>>(s->wa_cls_blk0[0], s->wa_blk, s->net_by_size,
-                                                              s->wa_gen_start, s->net_start, s->e_cell, s->e_off,
-                                                              s->cell_xy, s->anchor, nw, ig, s->grad_e, part_wl,
-                                                              part_hp, ctrl);
-        CK_LAUNCH();
-    }
+    launch_wirelength_pp(s, gamma, use_net_w, part_wl, part_hp, false, 0, 0.0, nullptr, ctrl);
 }
 
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk)

@@ -132,6 +132,8 @@ struct FinArgs {
 void launch_wirelength_ctrl(tdpg_session* s, double gamma, bool use_net_w, double* pw, double* ph, int nb,
                             const Ctrl* ctrl);
 void launch_pp_ctrl(tdpg_session* s, int kind, double beta, double* pp, int nb, const Ctrl* ctrl);
+void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp,
+                          bool pp_fused, int kind, double beta, double* part_pp, const Ctrl* ctrl);
 void launch_density_ctrl(tdpg_session* s, double* pd, int nb, const Ctrl* ctrl);
 void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl);
 void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl);

@@ -37,13 +37,29 @@ struct Engine {
     cudaGraphExec_t gexec = nullptr;
     int launched = 0, refreshes = 0;
     long long kernel_launches = 0;
-    int kernels_per_iter = 13; // 7 WA classes + generic + PP + scatter + bins + finalize + cells (upper bound)
+    int kernels_per_iter = 13; // 7 WA classes + generic + scatter + bins + finalize + dens_grad + cells (max)
+    cudaGraphExec_t refresh_gexec = nullptr; // the whole timing refresh, captured once
+    cudaGraphExec_t sort_gexec = nullptr;    // spatial re-sort of the cells
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
     int sort_every = 2; // iterations between spatial re-sorts of the cells
     double last_refresh_ms = 0, total_refresh_ms = 0;
     ~Engine()
     {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
+        if (refresh_gexec) cudaGraphExecDestroy(refresh_gexec);
+        if (sort_gexec) cudaGraphExecDestroy(sort_gexec);
+        for (auto& e : refresh_ev) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    }
+    double refresh_ms()
+    {
+        double t = 0.0;
+        for (auto& e : refresh_ev) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(e.second) == cudaSuccess && cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess)
+                t += ms;
+        }
+        return t;
     }
 };
 
@@ -121,10 +137,22 @@ double lambda_auto(tdpg_session* s, double gamma, int kind)
     return (wl1 > 0.0 && d1 > 0.0) ? wl1 / d1 : 1.0;
 }
 
+template <typename F>
+cudaGraphExec_t capture(tdpg_session* s, F&& record)
+{
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    CK(cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
+    record();
+    CK(cudaStreamEndCapture(s->st, &g));
+    CK(cudaGraphInstantiate(&x, g, 0));
+    cudaGraphDestroy(g);
+    return x;
+}
+
 void capture_iteration(tdpg_session* s, Engine& E)
 {
     if (E.gexec) cudaGraphExecDestroy(E.gexec), E.gexec = nullptr;
-    if (E.graph) cudaGraphDestroy(E.graph), E.graph = nullptr;
     double* part_wl = E.part.p;
     double* part_hp = part_wl + E.nb_wa;
     double* part_pp = part_hp + E.nb_wa;
@@ -135,14 +163,14 @@ void capture_iteration(tdpg_session* s, Engine& E)
     fa.total_movable = s->grid.total_movable, fa.beta = E.cfg.beta;
     fa.sched = E.sched, fa.stop_overflow = E.cfg.stop_overflow, fa.terms = E.terms, fa.trace = E.trace;
     fa.timing_row = E.timing_row, fa.timing_row_clear = E.timing_row;
-    CK(cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
-    launch_wirelength_ctrl(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, E.nb_wa, E.ctrl);
-    launch_pp_ctrl(s, E.cfg.pp_loss, E.cfg.beta, part_pp, E.nb_pp, E.ctrl);
-    launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
-    launch_finalize(s, fa, E.ctrl, E.cur);
-    launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl);
-    CK(cudaStreamEndCapture(s->st, &E.graph));
-    CK(cudaGraphInstantiate(&E.gexec, E.graph, 0));
+    E.gexec = capture(s, [&] {
+        // WA + fused pin pairs (dense ledger) -> density -> finalize -> density gradient + cells
+        launch_wirelength_pp(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, true, E.cfg.pp_loss,
+                             E.cfg.beta, part_pp, E.ctrl);
+        launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
+        launch_finalize(s, fa, E.ctrl, E.cur);
+        launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl);
+    });
 }
 
 } // namespace
@@ -175,14 +203,12 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     upload_positions(s, xy.data());
     ensure_grid(s, cfg->grid_nx, cfg->grid_ny, cfg->target_density);
 
-    // fresh ledger; buffers sized for the bound Q <= A_net so graph pointers stay valid
-    const size_t qcap = static_cast<size_t>(std::max(s->A_net, 1)) + 1;
+    // fresh PinPairWeights: the engine keeps it dense (weight per sink pin, fused into WA)
     s->Q = 0;
-    s->led_key.reserve(qcap), s->led_w.reserve(qcap), s->led_key2.reserve(qcap), s->led_w2.reserve(qcap);
-    s->pp_inc.reserve(2 * qcap), s->pp_start.reserve(2 * qcap + 1), s->pp_entry.reserve(2 * qcap);
-    s->pp_pins.reserve(4);
     s->pp_dirty = true;
-    rebuild_pp_incidence(s);
+    s->dl_w.zero(s->st), s->ppw_e.zero(s->st), s->pp_mask.zero(s->st);
+    s->q_count.reserve(2);
+    s->q_count.zero(s->st);
     s->net_w.reserve(std::max(s->N, 1));
     if (cfg->net_weighting) {
         std::vector<double> ones(s->N, 1.0);
@@ -215,14 +241,22 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->terms.alloc(1);
     E->m.alloc(s->C), E->v.alloc(s->C);
     E->m.zero(s->st), E->v.zero(s->st);
-    E->nb_wa = wa_blocks(s), E->nb_pp = pp_blocks(s), E->nb_d = bins_blocks(s);
+    E->nb_wa = wa_blocks(s), E->nb_pp = wa_blocks(s), E->nb_d = bins_blocks(s); // PP partials per WA block
     E->part.alloc(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
     if (const char* se = std::getenv("TDPG_SORT_EVERY")) E->sort_every = std::max(1, std::atoi(se));
-    sort_cells_spatial(s); // allocates the permutation before the graph captures its pointer
+    // every buffer the graphs touch is sized before capture, so their pointers never move
+    refresh_reserve(s);
+    s->pin_xy_external = false;
+    sort_cells_spatial(s);
     delete s->eng;
     s->eng = E.release();
-    capture_iteration(s, *s->eng);
+    Engine& G = *s->eng;
+    capture_iteration(s, G);
+    G.refresh_gexec = capture(s, [&] {
+        refresh_record(s, G.ctrl, G.timing_row, G.cfg.w0, G.cfg.w1, G.cfg.net_weighting != 0);
+    });
+    G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
     CK(cudaStreamSynchronize(s->st));
 }
 
@@ -234,76 +268,63 @@ Ctrl read_ctrl(tdpg_session* s)
     return c;
 }
 
-// Timing round (placer.cpp:415-435).  Returns false when the loop already stopped.
-bool timing_refresh(tdpg_session* s)
+__global__ void k_count_heads32(long long n, const unsigned* __restrict__ k, unsigned long long* __restrict__ out)
 {
-    Engine& E = *s->eng;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, s->st));
-    const Ctrl c = read_ctrl(s);
-    if (c.stopped) {
-        cudaEventDestroy(e0), cudaEventDestroy(e1);
-        return false;
-    }
-    s->pin_xy_external = false;
-    static const bool trace = std::getenv("TDPG_TRACE_REFRESH") != nullptr;
-    auto stamp = [&](const char* what) {
-        if (!trace) return;
-        static auto t0 = std::chrono::steady_clock::now();
-        CK(cudaStreamSynchronize(s->st));
-        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        std::fprintf(stderr, "[refresh %d] %-10s %.3f ms\n", E.launched, what, ms);
-        t0 = std::chrono::steady_clock::now();
-    };
-    stamp("start");
-    run_sta_dev(s);
-    stamp("sta");
-    const double row[3] = {1.0, s->tns, s->wns};
-    CK(cudaMemcpyAsync(E.timing_row.p, row, sizeof row, cudaMemcpyHostToDevice, s->st));
-    const int one = 1;
-    CK(cudaMemcpyAsync(&E.ctrl.p->engaged, &one, sizeof one, cudaMemcpyHostToDevice, s->st));
-    if (s->wns < 0.0) {
-        extract_endpoint_dev(s, 0); // n = number of violated endpoints (placer.cpp:424-428)
-        stamp("extract");
-        ledger_apply_sorted(s, s->n_hits, s->wns, E.cfg.w0, E.cfg.w1);
-        stamp("ledger");
-        rebuild_pp_incidence(s);
-        stamp("incidence");
-    } else {
-        s->n_paths = 0, s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0; // empty report
-    }
-    if (E.cfg.net_weighting) net_weights_dev(s);
-    if (s->round_cb) s->round_cb(s->round_user, E.launched); // TimingRoundObserver (placer.cpp:434)
-    // our kernels in this round: pin_xy + 2 per level + slack/final; extraction (slack/final,
-    // ties, two backtrace passes, head count), ledger groups, incidence (3), net weights
-    E.kernel_launches += 1 + 2LL * s->L + 2 + (s->wns < 0.0 ? 6 + 1 + 3 : 0) + (E.cfg.net_weighting ? 1 : 0);
-    CK(cudaEventRecord(e1, s->st));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    E.last_refresh_ms = ms;
-    E.total_refresh_ms += ms;
-    cudaEventDestroy(e0), cudaEventDestroy(e1);
-    ++E.refreshes;
-    return true;
+    int c = 0;
+    for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * kBlock)
+        c += (k[i] != 0xFFFFFFFFu) && (i == 0 || k[i - 1] != k[i]);
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, static_cast<unsigned long long>(c));
 }
 
-// Run up to n iterations of the loop (refreshes per schedule).  Returns iterations launched.
+// Timing round (placer.cpp:415-435) as one graph launch: STA, extraction of every violated endpoint,
+// ledger update, net weights; nothing comes back to the host unless an observer is registered.
+void timing_refresh(tdpg_session* s)
+{
+    Engine& E = *s->eng;
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    CK(cudaEventCreate(&ev.first));
+    CK(cudaEventCreate(&ev.second));
+    CK(cudaEventRecord(ev.first, s->st));
+    CK(cudaGraphLaunch(E.refresh_gexec, s->st));
+    CK(cudaEventRecord(ev.second, s->st));
+    E.refresh_ev.push_back(ev);
+    // our kernels: pin_xy, 2 per level, slack keys, sta final, begin, ties, bt count, fill, bt write,
+    // counts, ledger (+ net weights)
+    E.kernel_launches += 2LL * s->L + 10 + (E.cfg.net_weighting ? 1 : 0);
+    ++E.refreshes;
+    if (s->round_cb) { // TimingRoundObserver (placer.cpp:434): this round's annotation and report
+        double h[3];
+        long long c[3];
+        CK(cudaMemcpyAsync(h, s->sta_out.p, sizeof h, cudaMemcpyDeviceToHost, s->st));
+        CK(cudaMemcpyAsync(c, s->ex_counts.p, sizeof c, cudaMemcpyDeviceToHost, s->st));
+        DBuf<unsigned long long> u(1);
+        u.zero(s->st);
+        k_count_heads32<<<148 * 4, kBlock, 0, s->st>>>(s->hcap, s->eh_key_s, u);
+        CK_LAUNCH();
+        unsigned long long uq = 0;
+        u.download(&uq, 1, s->st);
+        CK(cudaStreamSynchronize(s->st));
+        s->tns = h[0], s->wns = h[1];
+        s->sta_valid = true, s->ties_resolved = true;
+        s->n_paths = static_cast<int>(c[0]), s->n_path_pins = c[1], s->n_hits = 0;
+        s->uniq_pairs = s->n_paths ? static_cast<long long>(uq) : 0;
+        s->round_cb(s->round_user, E.launched);
+    }
+}
+
+// Run up to n iterations of the loop (refreshes per schedule), all enqueued without host syncs;
+// after a stop (stop_overflow) the kernels see the device flag and do nothing.
 int engine_run(tdpg_session* s, int n)
 {
     Engine& E = *s->eng;
     int done = 0;
     for (; done < n && E.launched < E.cfg.max_iters; ++done) {
         const int it = E.launched;
-        if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0)
-            if (!timing_refresh(s)) {
-                E.launched = E.cfg.max_iters; // loop ended (stop_overflow)
-                break;
-            }
+        if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0) timing_refresh(s);
         if (it % E.sort_every == 0) {
-            sort_cells_spatial(s); // refresh the scatter's spatial cell order
+            CK(cudaGraphLaunch(E.sort_gexec, s->st)); // refresh the scatter's spatial cell order
             E.kernel_launches += 1;
         }
         CK(cudaGraphLaunch(E.gexec, s->st));
@@ -380,7 +401,8 @@ int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_
     API_BEGIN
     if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
     Engine& E = *s->eng;
-    static const char* kNames[6] = {"wirelength", "pin_pairs", "density_scatter", "density_bins", "finalize", "cells"};
+    static const char* kNames[6] = {"wirelength_pp", "spatial_sort", "density_scatter", "density_bins", "finalize",
+                                    "cells"};
     double* part_wl = E.part.p;
     double* part_hp = part_wl + E.nb_wa;
     double* part_pp = part_hp + E.nb_wa;
@@ -396,11 +418,11 @@ int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_
     double acc[6] = {0, 0, 0, 0, 0, 0};
     for (int r = 0; r < reps && E.launched < E.cfg.max_iters; ++r) {
         CK(cudaEventRecord(ev[0], s->st));
-        launch_wirelength_ctrl(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, E.nb_wa, E.ctrl);
+        launch_wirelength_pp(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, true, E.cfg.pp_loss,
+                             E.cfg.beta, part_pp, E.ctrl);
         CK(cudaEventRecord(ev[1], s->st));
-        launch_pp_ctrl(s, E.cfg.pp_loss, E.cfg.beta, part_pp, E.nb_pp, E.ctrl);
+        if (r % E.sort_every == 0) CK(cudaGraphLaunch(E.sort_gexec, s->st));
         CK(cudaEventRecord(ev[2], s->st));
-        if (r % E.sort_every == 0) sort_cells_spatial(s);
         launch_density_scatter_ctrl(s, E.ctrl);
         CK(cudaEventRecord(ev[3], s->st));
         launch_density_bins_ctrl(s, part_d, E.nb_d, E.ctrl);
@@ -470,9 +492,22 @@ int tdpg_engine_times(tdpg_session* s, double* refresh_ms_total, double* last_re
 {
     API_BEGIN
     if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised");
-    if (refresh_ms_total) *refresh_ms_total = s->eng->total_refresh_ms;
-    if (last_refresh_ms) *last_refresh_ms = s->eng->last_refresh_ms;
-    if (ledger_pairs) *ledger_pairs = s->Q;
+    const double tot = s->eng->refresh_ms();
+    if (refresh_ms_total) *refresh_ms_total = tot;
+    if (last_refresh_ms) {
+        *last_refresh_ms = 0.0;
+        if (!s->eng->refresh_ev.empty()) {
+            float ms = 0.f;
+            const auto& e = s->eng->refresh_ev.back();
+            if (cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess) *last_refresh_ms = ms;
+        }
+    }
+    if (ledger_pairs) {
+        unsigned long long q = 0;
+        CK(cudaMemcpyAsync(&q, s->q_count.p, sizeof q, cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        *ledger_pairs = static_cast<int64_t>(q);
+    }
     API_END
 }
 
@@ -500,6 +535,7 @@ int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_expli
     }
     if (n_rows) *n_rows = rows;
     if (stop_overflow) *stop_overflow = c.stopped;
+    dense_ledger_to_sorted(s); // PlacementOutcome::pair_weights as the sorted ledger (tdpg_pp_get)
     // final STA + exact HPWL at the returned positions (placer.cpp:482, bindings.cpp:381-382)
     run_sta_dev(s);
     double hp = 0.0;
@@ -507,10 +543,6 @@ int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_expli
         const int nb = wa_blocks(s);
         s->part.reserve(2 * nb + 8);
         launch_wirelength(s, s->eng->gamma, false, s->part.p, s->part.p + nb, nb);
-        std::vector<double> h(nb);
-        s->part.download(h.data(), nb, s->st);
-        // part.p + nb holds hpwl partials
-        s->part.download(h.data(), 0, s->st);
         std::vector<double> hh(nb);
         CK(cudaMemcpyAsync(hh.data(), s->part.p + nb, nb * sizeof(double), cudaMemcpyDeviceToHost, s->st));
         CK(cudaStreamSynchronize(s->st));

@@ -401,6 +401,38 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     }
     s->n_wa_blocks = static_cast<int>(blk.size());
     s->E_lay = pos;
+    {   // fused pin-pair tables (engine mode): per class-ordered net the sink slots in ascending pin
+        // id (3 bits each), per generic net the same as a list; per sink pin its (net index, slot)
+        std::vector<uint32_t> ord(std::max(N, 1), 0u);
+        std::vector<int> gen_ord(std::max(pos, 1), 0), pin_loc(P, -1), pin_drv(P, -1);
+        std::vector<std::pair<int, int>> sk;
+        for (int i = 0; i < N; ++i) {
+            const int n = order[i], b0 = s->h_net_start[n], k = s->h_net_start[n + 1] - b0;
+            sk.clear();
+            for (int j = 1; j < k; ++j) sk.emplace_back(s->h_net_pins[b0 + j], j);
+            std::sort(sk.begin(), sk.end());
+            for (int j = 1; j < k; ++j) pin_drv[s->h_net_pins[b0 + j]] = s->h_net_pins[b0];
+            if (i < cnt[0] || i >= cnt[1]) { // class net
+                uint32_t w = 0;
+                for (size_t q = 0; q < sk.size(); ++q) w |= static_cast<uint32_t>(sk[q].second) << (3 * q);
+                ord[i] = w;
+                for (int j = 1; j < k; ++j) pin_loc[s->h_net_pins[b0 + j]] = (i << 3) | j;
+            } else {
+                for (size_t q = 0; q < sk.size(); ++q) gen_ord[gen_start[i] + static_cast<int>(q)] = sk[q].second;
+            }
+        }
+        s->pp_ord.upload(ord, s->st);
+        s->wa_gen_ord.upload(gen_ord, s->st);
+        s->pin_loc.upload(pin_loc, s->st);
+        s->pin_driver.upload(pin_drv, s->st);
+        s->h_pin_driver = pin_drv;
+        s->pp_mask.alloc(std::max(N, 1));
+        s->pp_mask.zero(s->st);
+        s->ppw_e.alloc(std::max(pos, 1));
+        s->ppw_e.zero(s->st);
+        s->dl_w.alloc(std::max(P, 1));
+        s->dl_w.zero(s->st);
+    }
     if (blk.empty()) blk.push_back(make_int4(0, 0, 0, 0));
     s->net_by_size.upload(order, s->st);
     s->wa_blk.upload(blk, s->st);

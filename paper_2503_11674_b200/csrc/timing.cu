@@ -561,6 +561,252 @@ void net_weights_dev(tdpg_session* s)
     CK_LAUNCH();
 }
 
+// =====================================================================================
+// Engine-mode timing refresh (placer.cpp:415-435) with no host round trip: every size comes from
+// device memory, every launch is sized for its capacity (endpoints, endpoints x levels), so the
+// whole refresh is captured once as a CUDA graph.  The reference skips extraction and the ledger
+// when wns >= 0; here the kernels read wns (sta_out[1]) and exit.
+// =====================================================================================
+__device__ __forceinline__ bool refresh_active(const double* sta_out, const Ctrl* ctrl)
+{
+    return !(ctrl && ctrl->stopped) && sta_out[1] < 0.0;
+}
+
+__global__ void k_refresh_begin(const double* sta_out, Ctrl* ctrl, double* timing_row)
+{
+    if (ctrl->stopped) return;
+    timing_row[0] = 1.0, timing_row[1] = sta_out[0], timing_row[2] = sta_out[1];
+    ctrl->engaged = 1;
+}
+
+__global__ void k_bt_count_dev(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                               const int* __restrict__ ep, const int* __restrict__ pred,
+                               const uint8_t* __restrict__ pin_dir, int* __restrict__ len, int* __restrict__ hops)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= EP) return;
+    const int n_paths = refresh_active(sta_out, ctrl) ? static_cast<int>(sta_out[2]) : 0;
+    if (i >= n_paths) {
+        len[i] = 0, hops[i] = 0;
+        return;
+    }
+    int v = ep[i], l = 1, h = 0;
+    for (int u = pred[v]; u >= 0; v = u, u = pred[v]) ++l, h += pin_dir[u] == 1;
+    len[i] = l, hops[i] = h;
+}
+
+// Paths into the capacity buffers; one hit per hop leaving an Output pin keyed by the hop's sink
+// pin (each pair is a net arc: the sink identifies it), tagged with the path slack.
+__global__ void k_bt_write_dev(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                               const int* __restrict__ ep, const int* __restrict__ pred,
+                               const uint8_t* __restrict__ pin_dir, const int* __restrict__ len,
+                               const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
+                               const double* __restrict__ arr, double clock, int* __restrict__ pins,
+                               double* __restrict__ pslack, unsigned* __restrict__ hkey,
+                               double* __restrict__ hslack, int* __restrict__ hidx)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= EP || len[i] == 0) return;
+    int v = ep[i];
+    const double sl = clock - arr[v]; // paths.cpp:123
+    pslack[i] = sl;
+    int k = off[i] + len[i] - 1, h = hoff[i] + hops[i] - 1;
+    pins[k] = v;
+    for (int u = pred[v]; u >= 0; v = u, u = pred[v]) {
+        pins[--k] = u;
+        if (pin_dir[u] == 1) {
+            hkey[h] = sl < 0.0 ? static_cast<unsigned>(v) : 0xFFFFFFFFu; // pin_pairs.cpp:11
+            hslack[h] = sl;
+            hidx[h] = h;
+            --h;
+        }
+    }
+}
+
+__global__ void k_fill_u32(long long n, unsigned* p, unsigned v)
+{
+    for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * kBlock)
+        p[i] = v;
+}
+
+// update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin;
+// the head of each group applies the group's additions in hit order.
+__global__ void k_ledger_dense(long long H, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                               const unsigned* __restrict__ hk, const int* __restrict__ hidx,
+                               const double* __restrict__ hslack, double w0, double w1, double* __restrict__ dl_w,
+                               double* __restrict__ ppw_e, const int* __restrict__ pin_entry,
+                               const int* __restrict__ pin_loc, uint32_t* __restrict__ pp_mask,
+                               unsigned long long* __restrict__ q_count)
+{
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= H || !refresh_active(sta_out, ctrl)) return;
+    const unsigned key = hk[i];
+    if (key == 0xFFFFFFFFu || (i > 0 && hk[i - 1] == key)) return;
+    const double wns = sta_out[1];
+    const int v = static_cast<int>(key);
+    double w = dl_w[v];
+    const bool fresh = !(w > 0.0); // weights start at w0 > 0 and never decrease
+    long long j = i;
+    if (fresh) w = w0, ++j;
+    for (; j < H && hk[j] == key; ++j) w += w1 * (hslack[hidx[j]] / wns);
+    dl_w[v] = w;
+    ppw_e[pin_entry[v]] = w;
+    if (fresh) {
+        const int loc = pin_loc[v];
+        if (loc >= 0) atomicOr(&pp_mask[loc >> 3], 1u << (loc & 7));
+        atomicAdd(q_count, 1ull);
+    }
+}
+
+__global__ void k_extract_counts(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                                 const int* __restrict__ len, const int* __restrict__ off,
+                                 const int* __restrict__ hops, const int* __restrict__ hoff,
+                                 long long* __restrict__ counts)
+{
+    const bool on = refresh_active(sta_out, ctrl) && EP > 0;
+    counts[0] = on ? static_cast<long long>(sta_out[2]) : 0;
+    counts[1] = on ? static_cast<long long>(off[EP - 1]) + len[EP - 1] : 0;
+    counts[2] = on ? static_cast<long long>(hoff[EP - 1]) + hops[EP - 1] : 0;
+}
+
+__global__ void k_net_weights_dev(int N, const int* __restrict__ net_start, const int* __restrict__ net_pins,
+                                  const double* __restrict__ slack, const double* __restrict__ sta_out,
+                                  const Ctrl* __restrict__ ctrl, double* __restrict__ w)
+{
+    const int e = blockIdx.x * kBlock + threadIdx.x;
+    if (e >= N || (ctrl && ctrl->stopped)) return;
+    const double wns = sta_out[1];
+    double r = 1.0;
+    if (wns < 0.0) { // apply_net_weights (placer.cpp:262-273)
+        double worst = slack[net_pins[net_start[e]]];
+        for (int j = net_start[e] + 1; j < net_start[e + 1]; ++j) worst = smin(worst, slack[net_pins[j]]);
+        if (worst < 0.0) r = 1.0 + (-worst) / (-wns);
+    }
+    w[e] = r;
+}
+
+static int bits_for(long long n)
+{
+    int b = 1;
+    while ((1ll << b) <= n) ++b;
+    return b;
+}
+
+// Reserve every buffer the engine refresh touches (before capture; pointers never move after).
+void refresh_reserve(tdpg_session* s)
+{
+    const size_t EP = static_cast<size_t>(std::max(s->EP, 1));
+    const size_t L = static_cast<size_t>(std::max(s->L, 1));
+    s->hcap = static_cast<long long>(EP) * static_cast<long long>((L + 1) / 2 + 1);
+    const size_t H = static_cast<size_t>(s->hcap);
+    s->sort_k0.reserve(EP), s->sort_k1.reserve(EP), s->sort_v0.reserve(EP), s->sort_v1.reserve(EP);
+    s->ex_len.reserve(EP), s->ex_hops.reserve(EP), s->ex_off.reserve(EP), s->ex_hoff.reserve(EP);
+    s->ex_slack.reserve(EP), s->ex_pins.reserve(EP * L + 1);
+    s->eh_key.reserve(H), s->eh_key_s.reserve(H), s->eh_idx.reserve(H), s->eh_idx_s.reserve(H);
+    s->eh_slack.reserve(H);
+    s->ex_counts.reserve(4), s->q_count.reserve(2), s->sta_out.reserve(4);
+    const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(s->P, s->EP), kBlock))));
+    s->sta_part.reserve(3 * nb + 8);
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b1, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p,
+                                    static_cast<int>(EP), 0, 64, s->st);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, s->ex_len.p, s->ex_off.p, static_cast<int>(EP), s->st);
+    cub::DeviceRadixSort::SortPairs(nullptr, b3, s->eh_key.p, s->eh_key_s.p, s->eh_idx.p, s->eh_idx_s.p,
+                                    static_cast<int>(H), 0, 32, s->st);
+    cub_scratch(s, std::max({b1, b2, b3}));
+    s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * (s->L + 2));
+    if (s->N) s->net_w.reserve(s->N);
+}
+
+// The whole refresh, stream-ordered and host-sync-free (captured by the engine).
+void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting)
+{
+    sta_record(s, s->sta_out);
+    k_refresh_begin<<<1, 1, 0, s->st>>>(s->sta_out, ctrl, timing_row);
+    CK_LAUNCH();
+    const int EP = s->EP;
+    if (EP == 0) return;
+    size_t bytes = s->cub_tmp.n;
+    CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP,
+                                       0, 64, s->st));
+    k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), s->d_level, s->L, s->tie_scratch, s->L + 2);
+    CK_LAUNCH();
+    k_bt_count_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred,
+                                                                 s->pin_dir, s->ex_len, s->ex_hops);
+    CK_LAUNCH();
+    bytes = s->cub_tmp.n;
+    CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_len.p, s->ex_off.p, EP, s->st));
+    bytes = s->cub_tmp.n;
+    CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_hops.p, s->ex_hoff.p, EP, s->st));
+    const long long H = s->hcap;
+    k_fill_u32<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 8), kBlock, 0, s->st>>>(H, s->eh_key, 0xFFFFFFFFu);
+    CK_LAUNCH();
+    k_bt_write_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred, s->pin_dir,
+                                                                 s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff, s->arr,
+                                                                 s->clock, s->ex_pins, s->ex_slack, s->eh_key,
+                                                                 s->eh_slack, s->eh_idx);
+    CK_LAUNCH();
+    k_extract_counts<<<1, 1, 0, s->st>>>(EP, s->sta_out, ctrl, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff,
+                                         s->ex_counts);
+    CK_LAUNCH();
+    bytes = s->cub_tmp.n;
+    CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->eh_key.p, s->eh_key_s.p, s->eh_idx.p, s->eh_idx_s.p,
+                                       static_cast<int>(H), 0, bits_for(s->P), s->st));
+    k_ledger_dense<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(H, s->sta_out, ctrl, s->eh_key_s, s->eh_idx_s,
+                                                                s->eh_slack, w0, w1, s->dl_w, s->ppw_e, s->pin_entry,
+                                                                s->pin_loc, s->pp_mask, s->q_count);
+    CK_LAUNCH();
+    if (net_weighting && s->N) {
+        k_net_weights_dev<<<blocks_for(s->N, kBlock), kBlock, 0, s->st>>>(s->N, s->net_start, s->net_pins, s->slack,
+                                                                          s->sta_out, ctrl, s->net_w);
+        CK_LAUNCH();
+    }
+}
+
+// Dense ledger -> the sorted (a, b, w) ledger of the session (tdpg_pp_get), after a run.
+__global__ void k_dense_to_pairs(int P, const double* __restrict__ dl_w, const int* __restrict__ pin_driver,
+                                 unsigned long long* __restrict__ key, double* __restrict__ w)
+{
+    const int v = blockIdx.x * kBlock + threadIdx.x;
+    if (v >= P) return;
+    const double x = dl_w[v];
+    const int d = pin_driver[v];
+    if (x > 0.0 && d >= 0) {
+        const unsigned lo = static_cast<unsigned>(min(v, d)), hi = static_cast<unsigned>(max(v, d));
+        key[v] = (static_cast<unsigned long long>(lo) << 32) | hi;
+        w[v] = x;
+    } else {
+        key[v] = kNoKey;
+        w[v] = 0.0;
+    }
+}
+
+void dense_ledger_to_sorted(tdpg_session* s)
+{
+    const int P = s->P;
+    if (P == 0) return;
+    DBuf<unsigned long long> k0(P), k1(P);
+    DBuf<double> w0(P), w1(P);
+    k_dense_to_pairs<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->dl_w, s->pin_driver, k0, w0);
+    CK_LAUNCH();
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0.p, k1.p, w0.p, w1.p, P, 0, 64, s->st);
+    void* tmp = cub_scratch(s, bytes);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0.p, k1.p, w0.p, w1.p, P, 0, 64, s->st));
+    unsigned long long q = 0;
+    CK(cudaMemcpyAsync(&q, s->q_count.p, sizeof q, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    s->led_key.reserve(q + 1), s->led_w.reserve(q + 1);
+    if (q) {
+        CK(cudaMemcpyAsync(s->led_key.p, k1.p, q * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s->st));
+        CK(cudaMemcpyAsync(s->led_w.p, w1.p, q * sizeof(double), cudaMemcpyDeviceToDevice, s->st));
+    }
+    s->Q = static_cast<long long>(q);
+    s->pp_dirty = true;
+    CK(cudaStreamSynchronize(s->st));
+}
+
 } // namespace tdpg
 
 using namespace tdpg;
