@@ -64,19 +64,26 @@ struct GridDev {
     double x0, y0, bw, bh, cap, scale, inv_scale, total_movable, inv_bw, inv_bh;
 };
 
-// bspline2 / bspline2_integral with the divisions by 6 and 3 as reciprocal multiplies.
+// bspline2 / bspline2_integral (density.cpp:15-36), divisions by 6 and 3 as reciprocal multiplies,
+// evaluated branch-free: every piece is computed and the right one selected (same formula per piece,
+// so the selected value is unchanged; lanes of a warp no longer diverge on the bin position).
+__device__ __forceinline__ double bspline2_bf(double u)
+{
+    const double a = fabs(u);
+    const double t = 1.5 - a;
+    const double inner = 0.75 - a * a, outer = 0.5 * t * t;
+    return a >= 1.5 ? 0.0 : (a <= 0.5 ? inner : outer);
+}
+
 __device__ __forceinline__ double bspline2_integral_r(double u)
 {
     constexpr double kSixth = 1.0 / 6.0, kThird = 1.0 / 3.0;
-    if (u <= -1.5) return 0.0;
-    if (u >= 1.5) return 1.0;
-    if (u <= -0.5) {
-        const double t = u + 1.5;
-        return t * t * t * kSixth;
-    }
-    if (u <= 0.5) return 0.5 + 0.75 * u - u * u * u * kThird;
-    const double t = 1.5 - u;
-    return 1.0 - t * t * t * kSixth;
+    const double t1 = u + 1.5, t3 = 1.5 - u;
+    const double left = t1 * t1 * t1 * kSixth;
+    const double mid = 0.5 + 0.75 * u - u * u * u * kThird;
+    const double right = 1.0 - t3 * t3 * t3 * kSixth;
+    const double r = u <= -0.5 ? left : (u <= 0.5 ? mid : right);
+    return u <= -1.5 ? 0.0 : (u >= 1.5 ? 1.0 : r);
 }
 
 // extent_weight + extent_weight_grad (density.cpp:41-49) for one bin centre c, with the
@@ -86,10 +93,10 @@ __device__ __forceinline__ void extent_w(double lo, double hi, double c, double 
 {
     const double uh = (hi - c) * inv_h, ul = (lo - c) * inv_h;
     w = (bspline2_integral_r(uh) - bspline2_integral_r(ul)) * h * inv_len;
-    dw = (bspline2(uh) - bspline2(ul)) * inv_len;
+    dw = (bspline2_bf(uh) - bspline2_bf(ul)) * inv_len;
 }
 
-constexpr int kFoot = 8; // footprint bins per dimension kept in registers (wider footprints loop)
+constexpr int kFoot = 7; // footprint bins per dimension kept in registers (wider footprints loop)
 
 // Footprint bin range (density.cpp:109-112) with reciprocal pitch; bins at the range ends
 // carry zero weight, so a one-bin difference from the division form changes nothing.
