@@ -217,6 +217,29 @@ __device__ __forceinline__ void wa_axis_warp(int s0, int n, int axis, const int*
     extent = hi - lo;
 }
 
+// One axis of a net of <= 32 pins, lane i holding pin i (lanes past the net hold the driver and
+// contribute nothing): max/min and the four exponential sums by warp shuffles; returns the pin's
+// unweighted gradient (wirelength.cpp:15-43).
+__device__ __forceinline__ double wa_lane(double x, bool on, double inv_gamma, double& value, double& extent)
+{
+    double hi = x, lo = x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        hi = smax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        lo = smin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    }
+    const double eu = on ? exp((x - hi) * inv_gamma) : 0.0;
+    const double el = on ? exp(-(x - lo) * inv_gamma) : 0.0;
+    const double s_max = wsum(eu), t_max = wsum((x - hi) * eu);
+    const double s_min = wsum(el), t_min = wsum((x - lo) * el);
+    const double is_max = 1.0 / s_max, is_min = 1.0 / s_min;
+    const double max_term = t_max * is_max, min_term = t_min * is_min;
+    value = (hi - lo) + (max_term - min_term);
+    extent = hi - lo;
+    return (eu * is_max) * (1.0 + ((x - hi) - max_term) * inv_gamma) -
+           (el * is_min) * (1.0 - ((x - lo) - min_term) * inv_gamma);
+}
+
 __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __restrict__ blk,
                                                        const int* __restrict__ net_by_size,
                                                        const int* __restrict__ gen_start,
@@ -246,8 +269,17 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
             continue;
         }
         double vx, vy, hx, hy;
-        wa_axis_warp(s0, n, 0, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vx, hx);
-        wa_axis_warp(s0, n, 1, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vy, hy);
+        if (n <= 32) { // one pin per lane, held in registers: one gather, exps computed once
+            const bool on = lane < n;
+            const double2 p = on ? entry_pos(e_cell[s0 + lane], e_off[s0 + lane], cell_xy, anchor)
+                                 : entry_pos(e_cell[s0], e_off[s0], cell_xy, anchor);
+            const double gx = wa_lane(p.x, on, inv_gamma, vx, hx);
+            const double gy = wa_lane(p.y, on, inv_gamma, vy, hy);
+            if (on) grad_e[s0 + lane] = make_double2(w * gx, w * gy);
+        } else {
+            wa_axis_warp(s0, n, 0, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vx, hx);
+            wa_axis_warp(s0, n, 1, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vy, hy);
+        }
         if (lane == 0) wl += w * (vx + vy), hp += hx + hy;
         if (pp.w_e) { // rare large nets: lane 0 walks the sinks in ascending pin id
             __syncwarp();
@@ -390,38 +422,39 @@ struct GlobalAcc {
 };
 
 template <typename Acc>
-__device__ __forceinline__ void scatter_cell(const double2 p, const double2 s, const GridDev& g, int bx0, int bx1,
-                                             int by0, int by1, const Acc& acc, long long row_stride, int col0,
-                                             int row0)
-{
-    const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
+__device__ __noinline__ void scatter_cell_wide(const double2 p, const double2 s, const GridDev& g, const Acc& acc,
+                                               long long row_stride, int col0, int row0)
+{   // general footprint (cells wider than ~2 bins): any number of bins per axis
+    const Axis ax = make_axis(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx);
+    const Axis ay = make_axis(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny);
     const double area = s.x * s.y;
-    const double ilx = 1.0 / s.x, ily = 1.0 / s.y;
-    const int nby = min(by1 - by0 + 1, kFoot);
-    double wyc[kFoot];
-#pragma unroll
-    for (int j = 0; j < kFoot; ++j) {
-        double dwy = 0.0;
-        wyc[j] = 0.0;
-        if (j < nby) extent_w(yl, yh, g.y0 + (by0 + j + 0.5) * g.bh, g.bh, g.inv_bh, ily, wyc[j], dwy);
-    }
-    for (int bx = bx0; bx <= bx1; ++bx) {
-        double wx, dwx;
-        extent_w(xl, xh, g.x0 + (bx + 0.5) * g.bw, g.bw, g.inv_bw, ilx, wx, dwx);
+    for (int bx = ax.b0; bx <= ax.b1; ++bx) {
+        const double wx = axis_w(ax, bx);
         if (wx == 0.0) continue;
         const double aw = area * wx;
-        const long long row = static_cast<long long>(bx - row0) * row_stride + (by0 - col0);
-#pragma unroll
-        for (int j = 0; j < kFoot; ++j) {
-            if (j >= nby) break;
-            const long long q = __double2ll_rn(aw * wyc[j] * g.scale);
-            if (q) acc.add(row + j, static_cast<unsigned long long>(q));
+        const long long row = static_cast<long long>(bx - row0) * row_stride - col0;
+        for (int by = ay.b0; by <= ay.b1; ++by) {
+            const long long q = __double2ll_rn(aw * axis_w(ay, by) * g.scale);
+            if (q) acc.add(row + by, static_cast<unsigned long long>(q));
         }
-        for (int by = by0 + kFoot; by <= by1; ++by) {
-            double wy, dwy;
-            extent_w(yl, yh, g.y0 + (by + 0.5) * g.bh, g.bh, g.inv_bh, ily, wy, dwy);
-            const long long q = __double2ll_rn(aw * wy * g.scale);
-            if (q) acc.add(row + (by - by0), static_cast<unsigned long long>(q));
+    }
+}
+
+// Five-bin footprint (axis5) scatter: entry (i, j) = area * wx_i * wy_j (density.cpp:127), in fixed point.
+template <typename Acc>
+__device__ __forceinline__ void scatter_cell5(double area, int bx, int by, const double (&wx)[kF5],
+                                              const double (&wy)[kF5], const GridDev& g, const Acc& acc,
+                                              long long row_stride, int col0, int row0)
+{
+#pragma unroll
+    for (int i = 0; i < kF5; ++i) {
+        if (wx[i] == 0.0) continue;
+        const double aw = area * wx[i];
+        const long long row = static_cast<long long>(bx + i - row0) * row_stride + (by - col0);
+#pragma unroll
+        for (int j = 0; j < kF5; ++j) {
+            const long long q = __double2ll_rn(aw * wy[j] * g.scale);
+            if (q) acc.add(row + j, static_cast<unsigned long long>(q));
         }
     }
 }
@@ -439,11 +472,21 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
     const bool valid = i < n_mov;
     double2 p = make_double2(0, 0), s = make_double2(1, 1);
     int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+    double wx[kF5], wy[kF5], dw[kF5];
+    int bx = 0, by = 0;
+    bool fast = false;
     if (valid) {
         const int c = perm[i];
         p = cell_xy[c], s = cell_wh[c];
-        foot_range(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx0, bx1);
-        foot_range(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by0, by1);
+        fast = axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dw) &&
+               axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dw);
+        if (fast) {
+            bx0 = max(bx, 0), bx1 = min(bx + kF5 - 1, g.nx - 1), by0 = max(by, 0), by1 = min(by + kF5 - 1, g.ny - 1);
+        } else {
+            const Axis ax = make_axis(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx);
+            const Axis ay = make_axis(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny);
+            bx0 = ax.b0, bx1 = ax.b1, by0 = ay.b0, by1 = ay.b1;
+        }
     }
     if (threadIdx.x == 0) bb[0] = INT_MAX, bb[1] = INT_MIN, bb[2] = INT_MAX, bb[3] = INT_MIN;
     int a0 = bx0, a1 = bx1, c0 = by0, c1 = by1;
@@ -460,17 +503,24 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
     const int X0 = bb[0], Y0 = bb[2];
     const long long W = static_cast<long long>(bb[1]) - X0 + 1, H = static_cast<long long>(bb[3]) - Y0 + 1;
     if (X0 > bb[1]) return; // no movable cell in this block
+    const double area = s.x * s.y;
     if (W * H <= kWinBins) {
         for (int k = threadIdx.x; k < W * H; k += kBlock) win_lo[k] = 0u, win_hi[k] = 0u;
         __syncthreads();
-        if (valid) scatter_cell(p, s, g, bx0, bx1, by0, by1, SmemAcc{win_lo, win_hi}, H, Y0, X0);
+        if (valid) {
+            const SmemAcc sa{win_lo, win_hi};
+            if (fast) scatter_cell5(area, bx, by, wx, wy, g, sa, H, Y0, X0);
+            else scatter_cell_wide(p, s, g, sa, H, Y0, X0);
+        }
         __syncthreads();
         for (int k = threadIdx.x; k < W * H; k += kBlock) {
             const unsigned long long v = (static_cast<unsigned long long>(win_hi[k]) << 32) | win_lo[k];
             if (v) atomicAdd(&acc[static_cast<long long>(X0 + k / H) * g.ny + (Y0 + k % H)], v);
         }
     } else if (valid) {
-        scatter_cell(p, s, g, bx0, bx1, by0, by1, GlobalAcc{acc}, g.ny, 0, 0);
+        const GlobalAcc ga{acc};
+        if (fast) scatter_cell5(area, bx, by, wx, wy, g, ga, g.ny, 0, 0);
+        else scatter_cell_wide(p, s, g, ga, g.ny, 0, 0);
     }
 }
 
@@ -592,7 +642,32 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(FinArgs a, Ctrl* ctrl, I
 // order, so neighbouring threads read neighbouring excess bins (L1 hits).  Regrouped per bin
 // column: dgx = sum_bx area*dwx(bx) * 2*sum_by f(bx,by)*wy(by), dgy = sum_bx area*wx(bx) * 2*sum_by f*dwy.
 // =====================================================================================
-__global__ void __launch_bounds__(kBlock) k_dens_grad(int n_mov, const int* __restrict__ perm,
+__device__ __noinline__ double2 dens_grad_wide(const double2 p, const double2 s, const GridDev& g,
+                                               const double* __restrict__ excess)
+{   // general footprint (cells wider than ~2 bins)
+    const Axis ax = make_axis(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx);
+    const Axis ay = make_axis(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny);
+    const double area = s.x * s.y;
+    double dgx = 0.0, dgy = 0.0;
+    for (int bx = ax.b0; bx <= ax.b1; ++bx) {
+        double wx, dwx;
+        axis_at(ax, bx, wx, dwx);
+        if (wx == 0.0 && dwx == 0.0) continue;
+        double sx = 0.0, sy = 0.0;
+        for (int by = ay.b0; by <= ay.b1; ++by) {
+            double wy, dwy;
+            axis_at(ay, by, wy, dwy);
+            if (wy == 0.0 && dwy == 0.0) continue;
+            const double f = excess[static_cast<long long>(bx) * g.ny + by];
+            sx += f * wy, sy += f * dwy;
+        }
+        dgx += (area * dwx) * (2.0 * sx);
+        dgy += (area * wx) * (2.0 * sy);
+    }
+    return make_double2(dgx, dgy);
+}
+
+__global__ void __launch_bounds__(kBlock, 3) k_dens_grad(int n_mov, const int* __restrict__ perm,
                                                       const double2* __restrict__ cell_xy,
                                                       const double2* __restrict__ cell_wh, GridDev g,
                                                       const double* __restrict__ excess, double2* __restrict__ dgrad,
@@ -603,40 +678,27 @@ __global__ void __launch_bounds__(kBlock) k_dens_grad(int n_mov, const int* __re
     if (i >= n_mov) return;
     const int c = perm[i];
     const double2 p = cell_xy[c], s = cell_wh[c];
-    const double xl = p.x, xh = xl + s.x, yl = p.y, yh = yl + s.y;
-    int bx0, bx1, by0, by1;
-    foot_range(xl, xh, g.x0, g.bw, g.inv_bw, g.nx, bx0, bx1);
-    foot_range(yl, yh, g.y0, g.bh, g.inv_bh, g.ny, by0, by1);
-    const double area = s.x * s.y;
-    const double ilx = 1.0 / s.x, ily = 1.0 / s.y;
-    const int nby = min(by1 - by0 + 1, kFoot);
-    double wyc[kFoot], dwyc[kFoot];
-#pragma unroll
-    for (int j = 0; j < kFoot; ++j) {
-        wyc[j] = 0.0, dwyc[j] = 0.0;
-        if (j < nby) extent_w(yl, yh, g.y0 + (by0 + j + 0.5) * g.bh, g.bh, g.inv_bh, ily, wyc[j], dwyc[j]);
+    double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
+    int bx, by;
+    if (!(axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx) &&
+          axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy))) {
+        dgrad[c] = dens_grad_wide(p, s, g, excess);
+        return;
     }
+    const double area = s.x * s.y;
     double dgx = 0.0, dgy = 0.0;
-    for (int bx = bx0; bx <= bx1; ++bx) {
-        double wx, dwx;
-        extent_w(xl, xh, g.x0 + (bx + 0.5) * g.bw, g.bw, g.inv_bw, ilx, wx, dwx);
-        if (wx == 0.0 && dwx == 0.0) continue;
-        const double* ex = excess + static_cast<long long>(bx) * g.ny + by0;
+#pragma unroll
+    for (int a = 0; a < kF5; ++a) {
+        if (wx[a] == 0.0 && dwx[a] == 0.0) continue; // (outside the grid, or no support)
+        const double* ex = excess + static_cast<long long>(bx + a) * g.ny + by;
+        double f[kF5];
+#pragma unroll
+        for (int j = 0; j < kF5; ++j) f[j] = (wy[j] != 0.0 || dwy[j] != 0.0) ? ex[j] : 0.0;
         double sx = 0.0, sy = 0.0;
 #pragma unroll
-        for (int j = 0; j < kFoot; ++j)
-            if (j < nby) {
-                const double f = ex[j];
-                sx += f * wyc[j], sy += f * dwyc[j];
-            }
-        for (int by = by0 + kFoot; by <= by1; ++by) {
-            double wy, dwy;
-            extent_w(yl, yh, g.y0 + (by + 0.5) * g.bh, g.bh, g.inv_bh, ily, wy, dwy);
-            const double fe = excess[static_cast<long long>(bx) * g.ny + by];
-            sx += fe * wy, sy += fe * dwy;
-        }
-        dgx += (area * dwx) * (2.0 * sx);
-        dgy += (area * wx) * (2.0 * sy);
+        for (int j = 0; j < kF5; ++j) sx += f[j] * wy[j], sy += f[j] * dwy[j];
+        dgx += (area * dwx[a]) * (2.0 * sx);
+        dgy += (area * wx[a]) * (2.0 * sy);
     }
     dgrad[c] = make_double2(dgx, dgy);
 }
@@ -834,33 +896,37 @@ void rebuild_pp_incidence(tdpg_session* s)
 
 template <int N>
 void launch_wa_class(tdpg_session* s, const double* nw, double inv_gamma, double* pw, double* ph, const PPArgs& pp,
-                     double* ppart, const Ctrl* ctrl)
+                     double* ppart, const Ctrl* ctrl, cudaStream_t st)
 {
     if (!s->wa_cls_nblk[N]) return;
-    k_wa_class<N><<<s->wa_cls_nblk[N], kBlock, 0, s->st>>>(s->wa_cls_blk0[N], s->wa_blk, s->net_by_size, s->e_cell,
+    k_wa_class<N><<<s->wa_cls_nblk[N], kBlock, 0, st>>>(s->wa_cls_blk0[N], s->wa_blk, s->net_by_size, s->e_cell,
                                                            s->e_off, s->cell_xy, s->anchor, nw, inv_gamma, s->grad_e,
                                                            pw, ph, pp, ppart, ctrl);
     CK_LAUNCH();
 }
 
-// WA (+ fused pin pairs when pp_fused: the engine's dense ledger) over all size classes.
+// WA (+ fused pin pairs when pp_fused: the engine's dense ledger) over all size classes.  The class
+// kernels touch disjoint nets; with branch streams (graph capture) each class runs on its own branch
+// so the small per-class grids overlap instead of draining the GPU one after another.
 void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp,
-                          bool pp_fused, int kind, double beta, double* part_pp, const Ctrl* ctrl)
+                          bool pp_fused, int kind, double beta, double* part_pp, const Ctrl* ctrl,
+                          const cudaStream_t* branch, int n_branch)
 {
     const double* nw = use_net_w ? s->net_w.p : nullptr;
     const double ig = 1.0 / gamma;
     PPArgs pp{nullptr, nullptr, nullptr, beta, kind};
     if (pp_fused) pp = PPArgs{s->pp_mask.p, s->pp_ord.p, s->ppw_e.p, beta, kind};
     double* ppart = pp_fused ? part_pp : nullptr;
-    launch_wa_class<2>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
-    launch_wa_class<3>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
-    launch_wa_class<4>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
-    launch_wa_class<5>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
-    launch_wa_class<6>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
-    launch_wa_class<7>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
-    launch_wa_class<8>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl);
+    auto st = [&](int k) { return n_branch > 0 ? branch[k % n_branch] : s->st; };
+    launch_wa_class<2>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(1));
+    launch_wa_class<3>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(2));
+    launch_wa_class<4>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(3));
+    launch_wa_class<5>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(4));
+    launch_wa_class<6>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(5));
+    launch_wa_class<7>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(6));
+    launch_wa_class<8>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(7));
     if (s->wa_cls_nblk[0]) {
-        k_wa_generic<<<s->wa_cls_nblk[0], kBlock, 0, s->st>>>(s->wa_cls_blk0[0], s->wa_blk, s->net_by_size,
+        k_wa_generic<<<s->wa_cls_nblk[0], kBlock, 0, st(0)>>>(s->wa_cls_blk0[0], s->wa_blk, s->net_by_size,
                                                               s->wa_gen_start, s->net_start, s->e_cell, s->e_off,
                                                               s->cell_xy, s->anchor, nw, ig, s->grad_e, part_wl,
                                                               part_hp, pp, s->wa_gen_ord, ppart, ctrl);
@@ -872,7 +938,7 @@ void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* pa
                        const Ctrl* ctrl)
 {
     (void)nblk;
-    launch_wirelength_pp(s, gamma, use_net_w, part_wl, part_hp, false, 0, 0.0, nullptr, ctrl);
+    launch_wirelength_pp(s, gamma, use_net_w, part_wl, part_hp, false, 0, 0.0, nullptr, ctrl, nullptr, 0);
 }
 
 void launch_wirelength(tdpg_session* s, double gamma, bool use_net_w, double* part_wl, double* part_hp, int nblk)
@@ -967,15 +1033,20 @@ CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, dou
     return a;
 }
 
-// density gradient then the cell kernel
-void launch_cell_pass(tdpg_session* s, const CellArgs& ca, const IterCur* cur, Ctrl* ctrl)
+void launch_dens_grad(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st)
 {
     const int n_mov = s->grid.n_movable;
     if (n_mov > 0) {
-        k_dens_grad<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(n_mov, s->grid.perm, s->cell_xy, s->cell_wh,
-                                                                     grid_dev(s), s->grid.excess, s->dgrad, ctrl);
+        k_dens_grad<<<blocks_for(n_mov, kBlock), kBlock, 0, st>>>(n_mov, s->grid.perm, s->cell_xy, s->cell_wh,
+                                                                  grid_dev(s), s->grid.excess, s->dgrad, ctrl);
         CK_LAUNCH();
     }
+}
+
+// density gradient (unless the caller already enqueued it) then the cell kernel
+void launch_cell_pass(tdpg_session* s, const CellArgs& ca, const IterCur* cur, Ctrl* ctrl, bool dens_grad = true)
+{
+    if (dens_grad) launch_dens_grad(s, ctrl, s->st);
     k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, ctrl);
     CK_LAUNCH();
 }
@@ -1230,9 +1301,9 @@ void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cu
     CK_LAUNCH();
 }
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
-                  const IterCur* cur, Ctrl* ctrl)
+                  const IterCur* cur, Ctrl* ctrl, bool dens_grad)
 {
     const CellArgs ca = cell_args(s, d_cell, m, v, b1, b2, eps);
-    launch_cell_pass(s, ca, cur, ctrl);
+    launch_cell_pass(s, ca, cur, ctrl, dens_grad);
 }
 } // namespace tdpg

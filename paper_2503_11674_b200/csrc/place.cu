@@ -43,8 +43,18 @@ struct Engine {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
     int sort_every = 2; // iterations between spatial re-sorts of the cells
     double last_refresh_ms = 0, total_refresh_ms = 0;
+    // branch streams + fork/join events of the captured iteration graph (density chain and the WA
+    // size classes run as parallel graph branches)
+    static constexpr int kBranches = 8;
+    cudaStream_t br[kBranches] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[kBranches] = {};
     ~Engine()
     {
+        for (auto& b : br)
+            if (b) cudaStreamDestroy(b);
+        for (auto& e : ev_join)
+            if (e) cudaEventDestroy(e);
+        if (ev_fork) cudaEventDestroy(ev_fork);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
         if (refresh_gexec) cudaGraphExecDestroy(refresh_gexec);
@@ -163,13 +173,34 @@ void capture_iteration(tdpg_session* s, Engine& E)
     fa.total_movable = s->grid.total_movable, fa.beta = E.cfg.beta;
     fa.sched = E.sched, fa.stop_overflow = E.cfg.stop_overflow, fa.terms = E.terms, fa.trace = E.trace;
     fa.timing_row = E.timing_row, fa.timing_row_clear = E.timing_row;
+    if (!E.ev_fork) {
+        CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
+        for (int k = 0; k < Engine::kBranches; ++k) {
+            CK(cudaStreamCreateWithFlags(&E.br[k], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&E.ev_join[k], cudaEventDisableTiming));
+        }
+    }
     E.gexec = capture(s, [&] {
-        // WA + fused pin pairs (dense ledger) -> density -> finalize -> density gradient + cells
-        launch_wirelength_pp(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, true, E.cfg.pp_loss,
-                             E.cfg.beta, part_pp, E.ctrl);
+        // fork: density chain (scatter -> bins -> density gradient) on branch 0, the WA size classes
+        // (+ fused pin pairs, dense ledger) on the main stream and branches 1..7; join -> finalize -> cells
+        cudaStream_t main = s->st;
+        CK(cudaEventRecord(E.ev_fork, main));
+        for (int k = 0; k < Engine::kBranches; ++k) CK(cudaStreamWaitEvent(E.br[k], E.ev_fork, 0));
+        s->st = E.br[0];
         launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
+        launch_dens_grad(s, E.ctrl, E.br[0]);
+        s->st = main;
+        cudaStream_t wa_st[Engine::kBranches] = {main};
+        for (int k = 1; k < Engine::kBranches; ++k) wa_st[k] = E.br[k];
+        launch_wirelength_pp(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, true, E.cfg.pp_loss,
+                             E.cfg.beta, part_pp, E.ctrl, wa_st, Engine::kBranches);
+        for (int k = 0; k < Engine::kBranches; ++k) {
+            CK(cudaEventRecord(E.ev_join[k], E.br[k]));
+            CK(cudaStreamWaitEvent(main, E.ev_join[k], 0));
+        }
         launch_finalize(s, fa, E.ctrl, E.cur);
-        launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl);
+        launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
+                     false);
     });
 }
 
@@ -401,8 +432,8 @@ int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_
     API_BEGIN
     if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
     Engine& E = *s->eng;
-    static const char* kNames[6] = {"wirelength_pp", "spatial_sort", "density_scatter", "density_bins", "finalize",
-                                    "cells"};
+    static const char* kNames[7] = {"wirelength_pp", "spatial_sort", "density_scatter", "density_bins", "finalize",
+                                    "dens_grad", "cells"};
     double* part_wl = E.part.p;
     double* part_hp = part_wl + E.nb_wa;
     double* part_pp = part_hp + E.nb_wa;
@@ -413,13 +444,13 @@ int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_
     fa.total_movable = s->grid.total_movable, fa.beta = E.cfg.beta;
     fa.sched = E.sched, fa.stop_overflow = E.cfg.stop_overflow, fa.terms = E.terms, fa.trace = E.trace;
     fa.timing_row = E.timing_row, fa.timing_row_clear = E.timing_row;
-    cudaEvent_t ev[7];
+    cudaEvent_t ev[8];
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    double acc[6] = {0, 0, 0, 0, 0, 0};
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
     for (int r = 0; r < reps && E.launched < E.cfg.max_iters; ++r) {
         CK(cudaEventRecord(ev[0], s->st));
         launch_wirelength_pp(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, true, E.cfg.pp_loss,
-                             E.cfg.beta, part_pp, E.ctrl);
+                             E.cfg.beta, part_pp, E.ctrl, nullptr, 0);
         CK(cudaEventRecord(ev[1], s->st));
         if (r % E.sort_every == 0) CK(cudaGraphLaunch(E.sort_gexec, s->st));
         CK(cudaEventRecord(ev[2], s->st));
@@ -429,10 +460,13 @@ int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_
         CK(cudaEventRecord(ev[4], s->st));
         launch_finalize(s, fa, E.ctrl, E.cur);
         CK(cudaEventRecord(ev[5], s->st));
-        launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl);
+        launch_dens_grad(s, E.ctrl, s->st);
         CK(cudaEventRecord(ev[6], s->st));
-        CK(cudaEventSynchronize(ev[6]));
-        for (int k = 0; k < 6; ++k) {
+        launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
+                     false);
+        CK(cudaEventRecord(ev[7], s->st));
+        CK(cudaEventSynchronize(ev[7]));
+        for (int k = 0; k < 7; ++k) {
             float ms = 0;
             cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
             acc[k] += ms;
@@ -441,7 +475,7 @@ int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_
         E.kernel_launches += E.kernels_per_iter;
     }
     for (auto& e : ev) cudaEventDestroy(e);
-    for (int k = 0; k < 6 && k < n_out; ++k) {
+    for (int k = 0; k < 7 && k < n_out; ++k) {
         out_ms[k] = acc[k] / std::max(reps, 1);
         if (names && name_len > 0) {
             std::strncpy(names + static_cast<size_t>(k) * name_len, kNames[k], name_len - 1);

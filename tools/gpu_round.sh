@@ -13,7 +13,7 @@ for w in $WHAT; do
     bench)  timeout 1200 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"; tail -c 3000 gpurun_out/bench_$TAG.json;;
     launches) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv \
                --log-file gpurun_out/launches_$TAG.csv python tools/prof_iter.py > gpurun_out/launches_$TAG.log 2>&1; echo "launches rc=$?";;
-    full)   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_wa|k_cells|k_density|k_pin_pairs' \
-               --profile-from-start off -c 8 -o gpurun_out/full_$TAG python tools/prof_iter.py > gpurun_out/full_$TAG.log 2>&1; echo "full rc=$?";;
+    full)   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-k_wa|k_cells|k_dens}" \
+               --profile-from-start off -c ${NCU_C:-8} -o gpurun_out/full_$TAG python tools/prof_iter.py > gpurun_out/full_$TAG.log 2>&1; echo "full rc=$?";;
   esac
 done
