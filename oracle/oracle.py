@@ -115,6 +115,8 @@ class Oracle(_Base):
             lib.orc_pp_get.argtypes = [_P, _P, _P, _P]
             lib.orc_sta.argtypes = [_P, _P, _P, _P, _P, _P, _P, _F64P, _F64P]
             lib.orc_extract.argtypes = [_P, _P, C.c_int32, _I64P]
+            lib.orc_extract_policy.argtypes = [_P, _P, C.c_int32, C.c_int32, C.c_int32, _I64P]
+            lib.orc_k_worst.argtypes = [_P, _P, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
             lib.orc_paths_get.argtypes = [_P, _P, _P, _P, _I64P]
             lib.orc_hits_get.argtypes = [_P, _P, _P, _P]
             lib.orc_graph_info.argtypes = [_P, _I32P, _P, _P, _P, _P, _P]
@@ -191,18 +193,38 @@ class Oracle(_Base):
                                      ak.ctypes.data, rk.ctypes.data, C.byref(tns), C.byref(wns)))
         return dict(arr=arr, req=req, slack=slack, arr_known=ak, req_known=rk, tns=tns.value, wns=wns.value)
 
-    def extract(self, xy=None, n=0):
+    def extract(self, xy=None, n=0, k=1, policy=0):
+        """n <= 0 with the endpoint policy and k = 1 selects every violated endpoint (the placer's
+        call); otherwise the reference's report_timing_endpoint(n, k) / report_timing(n) (policy 1)
+        through the lazy PathEnumerator restatement."""
         xy = self.d.positions if xy is None else np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
-        cnt = (C.c_int64 * 4)()
-        self._check(self.lib.orc_extract(self.h, xy.ctypes.data, n, cnt))
-        npath, total = cnt[0], cnt[1]
+        cnt = (C.c_int64 * 5)()
+        if policy == 0 and k == 1 and n <= 0:
+            self._check(self.lib.orc_extract(self.h, xy.ctypes.data, n, cnt))
+            cnt[4] = cnt[0]
+        else:
+            self._check(self.lib.orc_extract_policy(self.h, xy.ctypes.data, policy, n, k, cnt))
+        return self._report(cnt)
+
+    def k_worst(self, endpoint, k, xy=None):
+        xy = self.d.positions if xy is None else np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
+        n = C.c_int32()
+        self._check(self.lib.orc_k_worst(self.h, xy.ctypes.data, endpoint, k, C.byref(n)))
+        r = self._report([n.value, 0, 0, 0, n.value])
+        return [r["pins"][r["start"][i]:r["start"][i + 1]].tolist() for i in range(n.value)], r["slack"]
+
+    def _report(self, cnt):
+        npath = cnt[0]
+        start = np.zeros(npath + 1, np.int32)
+        self.lib.orc_paths_get(self.h, start.ctypes.data, None, None, None)
+        total = int(start[-1])
         start, pins, slack = np.zeros(npath + 1, np.int32), np.zeros(max(total, 1), np.int32), np.zeros(max(npath, 1))
         nh = C.c_int64()
         self.lib.orc_paths_get(self.h, start.ctypes.data, pins.ctypes.data, slack.ctypes.data, C.byref(nh))
         ha, hb, hs = np.zeros(max(nh.value, 1), np.int32), np.zeros(max(nh.value, 1), np.int32), np.zeros(max(nh.value, 1))
         self.lib.orc_hits_get(self.h, ha.ctypes.data, hb.ctypes.data, hs.ctypes.data)
         return dict(start=start, pins=pins[:total], slack=slack[:npath], n_paths=npath, unique_endpoints=cnt[2],
-                    unique_pin_pairs=cnt[3], candidates_generated=npath,
+                    unique_pin_pairs=cnt[3], candidates_generated=cnt[4],
                     hits=(ha[:nh.value], hb[:nh.value], hs[:nh.value]))
 
     def pp_update(self, ledger, hits, wns, w0=10.0, w1=0.2):

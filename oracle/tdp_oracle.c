@@ -722,7 +722,53 @@ static int cmp_ep(const void* x, const void* y)
     return (a->pin > b->pin) - (a->pin < b->pin);
 }
 
+int cmp_u64(const void* x, const void* y);
+int cmp_i32(const void* x, const void* y);
+
+/* collect_pin_pairs (paths.cpp:191-203) and finish_report counters (:89-102) over the session's
+ * p_start / p_pins / p_slack.  counts[0..3] = n_paths, total_pins, unique_endpoints, unique_pin_pairs. */
+static void finish_report(orc_session* s, int64_t* counts)
+{
+    const tdpg_netlist* nl = &s->nl;
+    const int32_t nv = s->n_paths, off = s->p_start[nv];
+    free(s->h_a), free(s->h_b), free(s->h_s);
+    s->h_a = malloc(((size_t)off + 1) * sizeof(int32_t));
+    s->h_b = malloc(((size_t)off + 1) * sizeof(int32_t));
+    s->h_s = malloc(((size_t)off + 1) * sizeof(double));
+    int64_t nh = 0;
+    for (int32_t i = 0; i < nv; ++i)
+        for (int32_t j = s->p_start[i]; j + 1 < s->p_start[i + 1]; ++j) {
+            const int32_t p0 = s->p_pins[j], p1 = s->p_pins[j + 1];
+            if (nl->pin_dir[p0] != 1) continue;
+            s->h_a[nh] = p0 < p1 ? p0 : p1, s->h_b[nh] = p0 < p1 ? p1 : p0, s->h_s[nh] = s->p_slack[i];
+            ++nh;
+        }
+    s->n_hits = nh;
+    uint64_t* keys = malloc(((size_t)nh + 1) * sizeof(uint64_t));
+    for (int64_t i = 0; i < nh; ++i) keys[i] = ((uint64_t)(uint32_t)s->h_a[i] << 32) | (uint32_t)s->h_b[i];
+    qsort(keys, (size_t)nh, sizeof(uint64_t), cmp_u64);
+    int64_t uniq = 0;
+    for (int64_t i = 0; i < nh; ++i) uniq += (i == 0 || keys[i] != keys[i - 1]);
+    free(keys);
+    /* unique endpoints: distinct last pins */
+    int32_t* last = malloc(((size_t)nv + 1) * sizeof(int32_t));
+    for (int32_t i = 0; i < nv; ++i) last[i] = s->p_pins[s->p_start[i + 1] - 1];
+    qsort(last, (size_t)nv, sizeof(int32_t), cmp_i32);
+    int64_t ue = 0;
+    for (int32_t i = 0; i < nv; ++i) ue += (i == 0 || last[i] != last[i - 1]);
+    free(last);
+    counts[0] = nv, counts[1] = off, counts[2] = ue, counts[3] = uniq;
+}
+
 int orc_extract(void* h, const double* cell_xy, int32_t n, int64_t counts[4])
+{
+    int64_t c5[5];
+    const int rc = orc_extract5(h, cell_xy, n, c5);
+    memcpy(counts, c5, 4 * sizeof(int64_t));
+    return rc;
+}
+
+int orc_extract5(void* h, const double* cell_xy, int32_t n, int64_t counts[5])
 {
     orc_session* s = h;
     const tdpg_netlist* nl = &s->nl;
@@ -785,36 +831,8 @@ int orc_extract(void* h, const double* cell_xy, int32_t n, int64_t counts[4])
         s->p_slack[i] = nl->clock_period - delay[v[i].pin]; /* paths.cpp:123 */
     }
     s->p_start[nv] = off;
-    /* collect_pin_pairs (paths.cpp:191-203) and finish_report counters (:89-102) */
-    free(s->h_a), free(s->h_b), free(s->h_s);
-    s->h_a = malloc(((size_t)off + 1) * sizeof(int32_t));
-    s->h_b = malloc(((size_t)off + 1) * sizeof(int32_t));
-    s->h_s = malloc(((size_t)off + 1) * sizeof(double));
-    int64_t nh = 0;
-    for (int32_t i = 0; i < nv; ++i)
-        for (int32_t j = s->p_start[i]; j + 1 < s->p_start[i + 1]; ++j) {
-            const int32_t p0 = s->p_pins[j], p1 = s->p_pins[j + 1];
-            if (nl->pin_dir[p0] != 1) continue;
-            s->h_a[nh] = p0 < p1 ? p0 : p1, s->h_b[nh] = p0 < p1 ? p1 : p0, s->h_s[nh] = s->p_slack[i];
-            ++nh;
-        }
-    s->n_hits = nh;
-    uint64_t* keys = malloc(((size_t)nh + 1) * sizeof(uint64_t));
-    for (int64_t i = 0; i < nh; ++i) keys[i] = ((uint64_t)(uint32_t)s->h_a[i] << 32) | (uint32_t)s->h_b[i];
-    int cmp_u64(const void*, const void*);
-    qsort(keys, (size_t)nh, sizeof(uint64_t), cmp_u64);
-    int64_t uniq = 0;
-    for (int64_t i = 0; i < nh; ++i) uniq += (i == 0 || keys[i] != keys[i - 1]);
-    free(keys);
-    /* unique endpoints: distinct last pins */
-    int32_t* last = malloc(((size_t)nv + 1) * sizeof(int32_t));
-    for (int32_t i = 0; i < nv; ++i) last[i] = s->p_pins[s->p_start[i + 1] - 1];
-    int cmp_i32(const void*, const void*);
-    qsort(last, (size_t)nv, sizeof(int32_t), cmp_i32);
-    int64_t ue = 0;
-    for (int32_t i = 0; i < nv; ++i) ue += (i == 0 || last[i] != last[i - 1]);
-    free(last);
-    counts[0] = nv, counts[1] = off, counts[2] = ue, counts[3] = uniq;
+    finish_report(s, counts);
+    counts[4] = nv;
     free(v), free(delay), free(pred), free(ok), free(b1), free(b2), free(pos);
     return 0;
 }
@@ -847,6 +865,241 @@ int orc_hits_get(void* h, int32_t* a, int32_t* b, double* slack)
     memcpy(a, s->h_a, (size_t)s->n_hits * sizeof(int32_t));
     memcpy(b, s->h_b, (size_t)s->n_hits * sizeof(int32_t));
     memcpy(slack, s->h_s, (size_t)s->n_hits * sizeof(double));
+    return 0;
+}
+
+/* ---- PathEnumerator (src/paths.cpp:12-55, include/tdp/paths.hpp:43-93) ----------
+ * Lazy k-best enumeration exactly as the reference: per pin a list of found records and a
+ * candidate heap holding at most one candidate per in-arc (the next unconsumed predecessor
+ * rank, paths.cpp:48-53).  The heap order is a strict total order (delay descending, then the
+ * lexicographically smallest full pin sequence, paths.hpp:63-69), so a linear max search over the
+ * at most fan-in candidates pops the same candidate as std::priority_queue.  Records link to
+ * their predecessor (pin, rank) instead of copying pin vectors. */
+typedef struct { double delay; int32_t pp, pr, len; } rea_rec;  /* pred pin / rank (-1: source) */
+typedef struct { double delay; int32_t arc, pr; } rea_cand;
+typedef struct {
+    orc_session* s;
+    const double* pos;
+    uint8_t* init;
+    rea_rec** found;
+    int32_t *nf, *cf;
+    rea_cand** heap;
+    int32_t *nh, *ch;
+    int32_t *b1, *b2, cap;
+} rea_t;
+
+static void rea_open(rea_t* r, orc_session* s, const double* pos)
+{
+    const size_t P = (size_t)s->nl.n_pins + 1;
+    r->s = s, r->pos = pos;
+    r->init = calloc(P, 1);
+    r->found = calloc(P, sizeof(rea_rec*));
+    r->nf = calloc(P, sizeof(int32_t)), r->cf = calloc(P, sizeof(int32_t));
+    r->heap = calloc(P, sizeof(rea_cand*));
+    r->nh = calloc(P, sizeof(int32_t)), r->ch = calloc(P, sizeof(int32_t));
+    r->cap = s->n_levels + 2;
+    r->b1 = malloc((size_t)r->cap * sizeof(int32_t)), r->b2 = malloc((size_t)r->cap * sizeof(int32_t));
+}
+
+static void rea_close(rea_t* r)
+{
+    const size_t P = (size_t)r->s->nl.n_pins + 1;
+    for (size_t i = 0; i < P; ++i) free(r->found[i]), free(r->heap[i]);
+    free(r->init), free(r->found), free(r->nf), free(r->cf), free(r->heap), free(r->nh), free(r->ch);
+    free(r->b1), free(r->b2);
+}
+
+/* pin sequence of record (v, k), source first; returns its length */
+static int32_t rea_seq(const rea_t* r, int32_t v, int32_t k, int32_t* buf)
+{
+    const int32_t n = r->found[v][k].len;
+    for (int32_t i = n - 1; i >= 0; --i) {
+        buf[i] = v;
+        const rea_rec* e = &r->found[v][k];
+        v = e->pp, k = e->pr;
+    }
+    return n;
+}
+
+/* CandidateOrder (paths.hpp:63-69): does candidate a come out of the heap before b? */
+static int rea_before(rea_t* r, int32_t v, const rea_cand* a, const rea_cand* b)
+{
+    if (a->delay != b->delay) return a->delay > b->delay;
+    const orc_session* s = r->s;
+    const int32_t na = rea_seq(r, s->from[a->arc], a->pr, r->b1);
+    const int32_t nb = rea_seq(r, s->from[b->arc], b->pr, r->b2);
+    r->b1[na] = v, r->b2[nb] = v;
+    return lex_less(r->b1, na + 1, r->b2, nb + 1);
+}
+
+static const rea_rec* rea_path_to(rea_t* r, int32_t v, int32_t rank);
+
+/* push_candidate (paths.cpp:19-31) */
+static void rea_push(rea_t* r, int32_t v, int32_t arc, int32_t pred_rank)
+{
+    const int32_t u = r->s->from[arc];
+    const rea_rec* pred = rea_path_to(r, u, pred_rank);
+    if (!pred) return;
+    rea_cand c;
+    c.delay = pred->delay + arc_delay(r->s, arc, r->pos);
+    c.arc = arc, c.pr = pred_rank;
+    if (r->nh[v] == r->ch[v]) {
+        r->ch[v] = r->ch[v] ? 2 * r->ch[v] : 4;
+        r->heap[v] = realloc(r->heap[v], (size_t)r->ch[v] * sizeof(rea_cand));
+    }
+    r->heap[v][r->nh[v]++] = c;
+}
+
+static void rea_append(rea_t* r, int32_t v, rea_rec e)
+{
+    if (r->nf[v] == r->cf[v]) {
+        r->cf[v] = r->cf[v] ? 2 * r->cf[v] : 2;
+        r->found[v] = realloc(r->found[v], (size_t)r->cf[v] * sizeof(rea_rec));
+    }
+    r->found[v][r->nf[v]++] = e;
+}
+
+/* initialize (paths.cpp:33-42) + path_to (paths.cpp:44-55) */
+static const rea_rec* rea_path_to(rea_t* r, int32_t v, int32_t rank)
+{
+    const orc_session* s = r->s;
+    if (!r->init[v]) {
+        r->init[v] = 1;
+        if (s->is_source[v]) {
+            const rea_rec e = {0.0, -1, -1, 1};
+            rea_append(r, v, e);
+        } else {
+            for (int32_t j = s->in_start[v]; j < s->in_start[v + 1]; ++j) rea_push(r, v, s->in_arcs[j], 0);
+        }
+    }
+    while (r->nf[v] <= rank && r->nh[v] > 0) {
+        int32_t best = 0;
+        for (int32_t i = 1; i < r->nh[v]; ++i)
+            if (rea_before(r, v, &r->heap[v][i], &r->heap[v][best])) best = i;
+        const rea_cand top = r->heap[v][best];
+        r->heap[v][best] = r->heap[v][--r->nh[v]];
+        const int32_t u = s->from[top.arc];
+        const rea_rec e = {top.delay, u, top.pr, r->found[u][top.pr].len + 1};
+        rea_append(r, v, e);
+        rea_push(r, v, top.arc, top.pr + 1);
+    }
+    return rank < r->nf[v] ? &r->found[v][rank] : NULL;
+}
+
+typedef struct {
+    double slack;
+    int32_t off, len;
+    const int32_t* pool;
+} path_ref;
+
+static int cmp_path(const void* x, const void* y)
+{   /* report_timing's order (paths.cpp:155-158): slack ascending, then pin sequence */
+    const path_ref* a = x;
+    const path_ref* b = y;
+    if (a->slack != b->slack) return a->slack < b->slack ? -1 : 1;
+    const int32_t* pa = a->pool + a->off;
+    const int32_t* pb = b->pool + b->off;
+    const int32_t n = a->len < b->len ? a->len : b->len;
+    for (int32_t i = 0; i < n; ++i)
+        if (pa[i] != pb[i]) return pa[i] < pb[i] ? -1 : 1;
+    return (a->len > b->len) - (a->len < b->len);
+}
+
+/* report_timing_endpoint (policy 0, paths.cpp:167-189) / report_timing (policy 1, :136-165) at
+ * cell_xy (run_sta first).  counts[4] = candidates_generated. */
+int orc_extract_policy(void* h, const double* cell_xy, int32_t policy, int32_t n, int32_t k, int64_t counts[5])
+{
+    orc_session* s = h;
+    const tdpg_netlist* nl = &s->nl;
+    const int32_t P = nl->n_pins;
+    double* pos = malloc(((size_t)P + 1) * 2 * sizeof(double));
+    orc_pin_positions(nl, cell_xy, pos);
+    sta_at(s, pos);
+    ep_rank* v = malloc(((size_t)nl->n_endpoints + 1) * sizeof(ep_rank));
+    int32_t nv = 0;
+    for (int32_t i = 0; i < nl->n_endpoints; ++i) {
+        const int32_t e = nl->endpoints[i];
+        if (s->slack[e] < 0.0) v[nv].pin = e, v[nv].slack = s->slack[e], ++nv;
+    }
+    qsort(v, (size_t)nv, sizeof(ep_rank), cmp_ep);
+    if (n <= 0) n = nv; /* the callers' convention: n <= 0 = every violated endpoint (placer.cpp:424-429) */
+    if (nv > n) nv = n;
+    const int32_t per = policy == 1 ? n : k; /* topn: n paths per endpoint (paths.cpp:148-151) */
+    rea_t r;
+    rea_open(&r, s, pos);
+    /* enumerate_per_endpoint (paths.cpp:108-132), single shared enumerator */
+    int64_t np = 0, cap_paths = 16, cap_pins = 1024, used = 0;
+    path_ref* refs = malloc((size_t)cap_paths * sizeof(path_ref));
+    int32_t* pool = malloc((size_t)cap_pins * sizeof(int32_t));
+    for (int32_t i = 0; i < nv; ++i)
+        for (int32_t j = 0; j < per; ++j) {
+            const rea_rec* rec = rea_path_to(&r, v[i].pin, j);
+            if (!rec) break;
+            const int32_t len = rec->len;
+            const double sl = nl->clock_period - rec->delay; /* paths.cpp:123 */
+            if (np == cap_paths) cap_paths *= 2, refs = realloc(refs, (size_t)cap_paths * sizeof(path_ref));
+            while (used + len > cap_pins) cap_pins *= 2, pool = realloc(pool, (size_t)cap_pins * sizeof(int32_t));
+            rea_seq(&r, v[i].pin, j, pool + used);
+            refs[np].slack = sl, refs[np].off = (int32_t)used, refs[np].len = len;
+            used += len, ++np;
+        }
+    rea_close(&r);
+    int64_t cand = np;
+    if (policy == 1) {
+        cand = (int64_t)nv * n; /* paths.cpp:149 */
+        for (int64_t i = 0; i < np; ++i) refs[i].pool = pool;
+        qsort(refs, (size_t)np, sizeof(path_ref), cmp_path);
+        if (np > n) np = n;
+    }
+    free(s->p_start), free(s->p_pins), free(s->p_slack);
+    s->n_paths = (int32_t)np;
+    s->p_start = malloc(((size_t)np + 1) * sizeof(int32_t));
+    s->p_pins = malloc(((size_t)used + 1) * sizeof(int32_t));
+    s->p_slack = malloc(((size_t)np + 1) * sizeof(double));
+    int32_t off = 0;
+    for (int64_t i = 0; i < np; ++i) {
+        s->p_start[i] = off;
+        memcpy(s->p_pins + off, pool + refs[i].off, (size_t)refs[i].len * sizeof(int32_t));
+        s->p_slack[i] = refs[i].slack;
+        off += refs[i].len;
+    }
+    s->p_start[np] = off;
+    finish_report(s, counts);
+    counts[4] = cand;
+    free(refs), free(pool), free(v), free(pos);
+    return 0;
+}
+
+/* k_worst_paths_to (paths.cpp:57-72): EndpointError for a non-endpoint; results into the session's
+ * path buffers (orc_paths_get). */
+int orc_k_worst(void* h, const double* cell_xy, int32_t endpoint, int32_t k, int32_t* n_paths)
+{
+    orc_session* s = h;
+    const tdpg_netlist* nl = &s->nl;
+    if (endpoint < 0 || endpoint >= nl->n_pins || !s->is_endpoint[endpoint])
+        return fail(TDPG_ERR_ENDPOINT, "validation error: pin %d is not an endpoint", endpoint);
+    double* pos = malloc(((size_t)nl->n_pins + 1) * 2 * sizeof(double));
+    orc_pin_positions(nl, cell_xy, pos);
+    rea_t r;
+    rea_open(&r, s, pos);
+    free(s->p_start), free(s->p_pins), free(s->p_slack);
+    s->p_start = malloc(((size_t)k + 1) * sizeof(int32_t));
+    s->p_pins = malloc(((size_t)k * (size_t)r.cap + 1) * sizeof(int32_t));
+    s->p_slack = malloc(((size_t)k + 1) * sizeof(double));
+    int32_t np = 0, off = 0;
+    for (; np < k; ++np) {
+        const rea_rec* rec = rea_path_to(&r, endpoint, np);
+        if (!rec) break;
+        s->p_start[np] = off;
+        off += rea_seq(&r, endpoint, np, s->p_pins + off);
+        s->p_slack[np] = nl->clock_period - rec->delay;
+    }
+    s->p_start[np] = off;
+    s->n_paths = np;
+    s->n_hits = 0;
+    rea_close(&r);
+    free(pos);
+    *n_paths = np;
     return 0;
 }
 

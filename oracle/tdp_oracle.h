@@ -48,6 +48,13 @@ int orc_sta(void* h, const double* cell_xy, double* arr, double* req, double* sl
 /* report_timing_endpoint(n, k = 1) after run_sta at cell_xy; n <= 0 = all violated.
  * counts = n_paths, total_pins, unique_endpoints, unique_pin_pairs */
 int orc_extract(void* h, const double* cell_xy, int32_t n, int64_t counts[4]);
+/* same, counts[4] = candidates_generated */
+int orc_extract5(void* h, const double* cell_xy, int32_t n, int64_t counts[5]);
+/* report_timing_endpoint(n, k) (policy 0) or report_timing(n) (policy 1, "topn") through the
+ * lazy PathEnumerator; n <= 0 is NOT special here (the reference's n). counts[4] = candidates. */
+int orc_extract_policy(void* h, const double* cell_xy, int32_t policy, int32_t n, int32_t k, int64_t counts[5]);
+/* k_worst_paths_to(endpoint, k); results via orc_paths_get. */
+int orc_k_worst(void* h, const double* cell_xy, int32_t endpoint, int32_t k, int32_t* n_paths);
 int orc_paths_get(void* h, int32_t* start, int32_t* pins, double* slack, int64_t* n_hits);
 int orc_hits_get(void* h, int32_t* a, int32_t* b, double* slack);
 int orc_pp_set(void* h, int64_t q, const int32_t* a, const int32_t* b, const double* w);

@@ -161,5 +161,53 @@ def check_schedule(B):
     assert out["trace"][-1].pp_term > 0.0
 
 
-ALL = [check_schedule, check_t1_sta, check_t2_sta, check_t1_graph, check_diamond_paths, check_t2_endpoint, check_trunk16,
+def check_k_worst_diamond(B):
+    """test_paths.cpp:42-74 — k_worst_paths_to on the diamond: via_a (slack 2), via_b (slack 4), only two
+    paths exist; the equal-delay diamond orders the tie by the smaller pin sequence."""
+    d = make_diamond(7.0, 5.0)
+    ep = _pin(d, "EP")
+    s = B(d)
+    p1, s1 = s.k_worst(ep, 1)
+    assert p1 == [[0, 1, 2, 5, 7, 8]] and s1[0] == 2.0
+    p2, s2 = s.k_worst(ep, 2)
+    assert p2 == [[0, 1, 2, 5, 7, 8], [0, 3, 4, 6, 7, 8]] and s2[1] == 4.0
+    p3, _ = s.k_worst(ep, 3)
+    assert len(p3) == 2
+    d = make_diamond(7.0, 7.0)
+    p2, s2 = B(d).k_worst(_pin(d, "EP"), 2)
+    assert len(p2) == 2 and s2[0] == s2[1] and p2[0] < p2[1] and p2[0] == [0, 1, 2, 5, 7, 8]
+
+
+def check_k_worst_refuses_non_endpoint(B):
+    """test_paths.cpp:76-82 — EndpointError ("is not an endpoint")."""
+    d = make_diamond()
+    try:
+        B(d).k_worst(_pin(d, "M.out"), 1)
+    except Exception as e:  # noqa: BLE001  (backend-specific exception class)
+        assert "is not an endpoint" in str(e)
+    else:
+        raise AssertionError("no EndpointError")
+
+
+def check_topn_t2(B):
+    """test_paths.cpp:105-139 — topn(2) piles onto EP1 (-5, -4), 4 candidates; topn(10) -> all 3 paths."""
+    r = B(make_t2()).extract(n=2, policy=1)
+    assert r["n_paths"] == 2 and list(r["slack"]) == [-5.0, -4.0]
+    assert r["unique_endpoints"] == 1 and r["candidates_generated"] == 4 and r["unique_pin_pairs"] == 5
+    r = B(make_t2()).extract(n=10, policy=1)
+    assert r["n_paths"] == 3 and r["candidates_generated"] == 20 and r["unique_endpoints"] == 2
+
+
+def check_topn_trunk16(B):
+    """test_paths.cpp:141-166 — topn(16): T16 swallows the budget (1 endpoint, 256 candidates, 18 pairs);
+    every endpoint has 16 trunk variants, ascending slack."""
+    d = make_trunk16()
+    r = B(d).extract(n=16, policy=1)
+    assert r["n_paths"] == 16 and r["unique_endpoints"] == 1 and r["candidates_generated"] == 256
+    assert r["unique_pin_pairs"] == 18
+    paths, sl = B(d).k_worst(_pin(d, "T7"), 32)
+    assert len(paths) == 16 and all(sl[i - 1] <= sl[i] for i in range(1, 16))
+
+
+ALL = [check_k_worst_diamond, check_k_worst_refuses_non_endpoint, check_topn_t2, check_topn_trunk16, check_schedule, check_t1_sta, check_t2_sta, check_t1_graph, check_diamond_paths, check_t2_endpoint, check_trunk16,
        check_t1_pairs, check_t1_hpwl, check_wa_closed_form, check_pp_hand_values, check_ledger, check_adam]

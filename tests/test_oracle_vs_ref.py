@@ -89,3 +89,46 @@ def test_generated_10k_snapshot():
     tr, gr = r.objective(xy, nx=32, ny=32, td=0.6, gamma=0.01 * d.span, lam=1e-3, beta=2.5e-5,
                          ledger=r.pp_update(None, er["hits"], r.sta(xy)["wns"]))
     assert np.array_equal(to, tr) and np.array_equal(go, gr)
+
+
+@pytest.mark.parametrize("seed", range(1, 41))
+def test_random_designs_kbest_and_topn(seed):
+    """The lazy PathEnumerator restatement (k > 1 per endpoint, the topn policy, k_worst_paths_to)
+    against the reference's own report_timing_endpoint / report_timing / k_worst_paths_to."""
+    d = random_design(seed)
+    o, r = Oracle(d), RefOracle(d)
+    for policy, n, k in ((0, 0, 2), (0, 0, 5), (0, 3, 4), (1, 0, 1), (1, 2, 1), (1, 7, 1)):
+        eo, er = o.extract(n=n, k=k, policy=policy), r.extract(n=n, k=k, policy=policy)
+        assert _paths(eo) == _paths(er), (policy, n, k)
+        assert np.array_equal(eo["slack"], er["slack"])
+        for key in ("unique_endpoints", "unique_pin_pairs", "candidates_generated"):
+            assert eo[key] == er[key], (key, policy, n, k)
+        for x, y in zip(eo["hits"], er["hits"]):
+            assert np.array_equal(x, y)
+    for e in d.endpoints[:4]:
+        po, so = o.k_worst(int(e), 6)
+        pr, sr = r.k_worst(int(e), 6)
+        assert po == pr and np.array_equal(so, sr)
+
+
+def test_trunk16_kbest_and_topn_spread():
+    d = make_trunk16()
+    o, r = Oracle(d), RefOracle(d)
+    for policy, n, k in ((0, 16, 16), (1, 16, 1), (1, 40, 1)):
+        eo, er = o.extract(n=n, k=k, policy=policy), r.extract(n=n, k=k, policy=policy)
+        assert _paths(eo) == _paths(er) and np.array_equal(eo["slack"], er["slack"])
+
+
+def test_generated_2k_kbest_topn_spread():
+    """A generated 2K-cell design on a spread snapshot with most endpoints failing."""
+    from paper_2503_11674_b200.engine import generate
+    d = generate(seed=3, cells=2000, fail_frac=0.5, calibrate=False)
+    xy = spread_positions(d, 2)
+    arr = Oracle(d).sta(xy)["arr"][d.endpoints]
+    d.clock_period = float(np.quantile(arr, 0.3))
+    o, r = Oracle(d), RefOracle(d)
+    for policy, n, k in ((0, 50, 3), (0, 0, 2), (1, 40, 1)):
+        eo, er = o.extract(xy, n=n, k=k, policy=policy), r.extract(xy, n=n, k=k, policy=policy)
+        assert eo["n_paths"] > 0
+        assert _paths(eo) == _paths(er) and np.array_equal(eo["slack"], er["slack"]), (policy, n, k)
+        assert eo["unique_pin_pairs"] == er["unique_pin_pairs"]
