@@ -23,7 +23,9 @@
  *   tdpg_objective           objective_and_gradient                   src/placer.cpp:275-343
  *   tdpg_adam_step           AdamState::step                          src/placer.cpp:345-356
  *   tdpg_sta                 run_sta (arrival/required/slack/tns/wns) src/sta.cpp:33-143
- *   tdpg_extract_endpoint    report_timing_endpoint (k = 1)           src/paths.cpp:167-189
+ *   tdpg_extract_endpoint    report_timing_endpoint (n, k)            src/paths.cpp:167-189
+ *   tdpg_extract             report_timing_endpoint / report_timing   src/paths.cpp:136-189
+ *   tdpg_k_worst             k_worst_paths_to                         src/paths.cpp:57-72
  *   tdpg_paths_hits          collect_pin_pairs                        src/paths.cpp:191-203
  *   tdpg_place               run_placement                            src/placer.cpp:358-484
  *   tdpg_generate            generate_synthetic                       src/generator.cpp:60-263
@@ -177,6 +179,15 @@ int tdpg_sta(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* 
 /* report_timing_endpoint(n, k=1) on the last STA; counts[0..3] = n_paths, total_pins,
  * unique_endpoints, unique_pin_pairs; candidates_generated = n_paths. */
 int tdpg_extract_endpoint(tdpg_session* s, int32_t n, int32_t k, int64_t counts[4]);
+/* report_timing_endpoint(n, k) (policy 0, paths.cpp:167-189) or report_timing(n) ("topn", policy 1,
+ * paths.cpp:136-165) on the last STA; n <= 0 = every violated endpoint.  counts[0..4] = n_paths,
+ * total_pins, unique_endpoints, unique_pin_pairs, candidates_generated. */
+int tdpg_extract(tdpg_session* s, int32_t policy, int32_t n, int32_t k, int64_t counts[5]);
+int tdpg_paths_candidates(tdpg_session* s, int64_t* candidates);
+/* k_worst_paths_to(endpoint, k) (paths.cpp:57-72); TDPG_ERR_ENDPOINT for a non-endpoint.
+ * start [k+1], pins [cap], slack [k]. */
+int tdpg_k_worst(tdpg_session* s, int32_t endpoint, int32_t k, int32_t* n_paths, int32_t* start, int32_t* pins,
+                 int32_t cap, double* slack);
 int tdpg_paths_get(tdpg_session* s, int32_t* path_start /* [n_paths+1] */, int32_t* pins, double* slack);
 /* Counts of the last extraction (same layout as tdpg_extract_endpoint's counts). */
 int tdpg_paths_counts(tdpg_session* s, int64_t counts[4]);
@@ -188,7 +199,7 @@ int tdpg_set_pin_positions(tdpg_session* s, const double* pin_xy);
 /* Download the last STA without recomputing it. */
 int tdpg_sta_fetch(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* arr_known,
                    uint8_t* req_known, double* tns, double* wns);
-/* PathEnumerator::path_to(pin, rank) (paths.hpp:54), rank 0: *n_pins = 0 when no source reaches pin. */
+/* PathEnumerator::path_to(pin, rank) (paths.hpp:54): *n_pins = 0 when the pin has no rank-th path. */
 int tdpg_path_to(tdpg_session* s, int32_t pin, int32_t rank, int32_t* pins, int32_t cap, int32_t* n_pins,
                  double* delay);
 /* Device-timed duration (ms) of the last STA / extraction call, CUDA events. */

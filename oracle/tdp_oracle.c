@@ -1235,8 +1235,6 @@ int orc_place(void* h, const double* init_xy, const uint8_t* pos_explicit, const
     orc_session* s = h;
     const tdpg_netlist* nl = &s->nl;
     const int32_t C = nl->n_cells, P = nl->n_pins;
-    if (cfg->extraction != 0 || cfg->k != 1)
-        return fail(TDPG_ERR_INTERNAL, "oracle restates the endpoint policy with k = 1 only");
     const double* core = nl->core;
     const double cw = core[2] - core[0], ch = core[3] - core[1];
     const double span = cw > ch ? cw : ch;
@@ -1287,8 +1285,9 @@ int orc_place(void* h, const double* init_xy, const uint8_t* pos_explicit, const
         double row_tns = 0.0, row_wns = 0.0;
         if (iter >= cfg->timing_start_iter && (iter - cfg->timing_start_iter) % cfg->m == 0) {
             engaged = 1;
-            int64_t cnt[4];
-            orc_extract(s, out_xy, 0, cnt); /* runs STA; n = n_fail */
+            int64_t cnt[5];
+            if (cfg->extraction == 0 && cfg->k == 1) orc_extract(s, out_xy, 0, cnt); /* runs STA; n = n_fail */
+            else orc_extract_policy(s, out_xy, cfg->extraction, 0, cfg->k, cnt);    /* placer.cpp:424-429 */
             sta_row = 1, row_tns = s->tns, row_wns = s->wns;
             if (s->wns < 0.0) orc_pp_update(s, s->n_hits, s->h_a, s->h_b, s->h_s, s->wns, cfg->w0, cfg->w1, NULL);
             if (cfg->net_weighting) { /* apply_net_weights, placer.cpp:262-273 */

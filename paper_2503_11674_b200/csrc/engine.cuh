@@ -148,7 +148,14 @@ struct tdpg_session {
     tdpg::DBuf<int> hit_idx, hit_idx_s;
     tdpg::DBuf<double> hit_slack;
     int n_paths = 0;
-    long long n_path_pins = 0, n_hits = 0, uniq_pairs = 0;
+    long long n_path_pins = 0, n_hits = 0, uniq_pairs = 0, uniq_endpoints = 0, candidates = 0;
+    // k-best path lists (kpaths.cu): per pin K records (delay, pred pin / pred rank), record counts
+    tdpg::DBuf<double> kb_delay;
+    tdpg::DBuf<int2> kb_pred;
+    tdpg::DBuf<int> kb_cnt;
+    int kb_K = 0;
+    tdpg::DBuf<unsigned> kh_key, kh_key_s; // engine refresh with k > 1 / topn: hits keyed by sink pin
+    tdpg::DBuf<int> kh_idx_s;
     bool hits_sorted = false;
     double last_sta_ms = 0, last_extract_ms = 0;
 
@@ -202,5 +209,11 @@ void extract_endpoint_dev(tdpg_session* s, int n);
 void resolve_ties_dev(tdpg_session* s);
 void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool hits_all_violated);
 void net_weights_dev(tdpg_session* s);
+int sorted_violated(tdpg_session* s);
+
+// kpaths.cu
+void kbest_build(tdpg_session* s, int K);
+void extract_policy_dev(tdpg_session* s, int policy, int n, int k, bool sink_keys);
+void kbest_paths_of(tdpg_session* s, int pin, int K, std::vector<std::vector<int>>& paths, std::vector<double>& delay);
 
 } // namespace tdpg

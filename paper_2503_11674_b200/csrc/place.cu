@@ -98,8 +98,7 @@ void validate_config(const tdpg_config& c)
     if (!(c.adam_eps > 0.0)) bad("adam_eps must be > 0");
     if (c.init_jitter_frac < 0.0) bad("init_jitter_frac must be >= 0");
     if (c.threads < 1) bad("threads must be >= 1");
-    if (c.extraction != 0) throw Error(TDPG_ERR_INTERNAL, "the topn extraction policy is not implemented on the device yet");
-    if (c.k != 1) throw Error(TDPG_ERR_INTERNAL, "k > 1 per endpoint is not implemented on the device yet");
+    if (c.extraction != 0 && c.extraction != 1) bad("extraction must be \"endpoint\" or \"topn\"");
 }
 
 __global__ void k_l1_pair(int C, const double2* __restrict__ a, const double2* __restrict__ b,
@@ -309,11 +308,98 @@ __global__ void k_count_heads32(long long n, const unsigned* __restrict__ k, uns
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, static_cast<unsigned long long>(c));
 }
 
+__global__ void k_refresh_begin_gen(const double* sta_out, Ctrl* ctrl, double* timing_row)
+{
+    if (ctrl->stopped) return;
+    timing_row[0] = 1.0, timing_row[1] = sta_out[0], timing_row[2] = sta_out[1];
+    ctrl->engaged = 1;
+}
+
+__global__ void k_ledger_dense_gen(long long H, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                                   const unsigned* __restrict__ hk, const int* __restrict__ hidx,
+                                   const double* __restrict__ hslack, double w0, double w1, double* __restrict__ dl_w,
+                                   double* __restrict__ ppw_e, const int* __restrict__ pin_entry,
+                                   const int* __restrict__ pin_loc, uint32_t* __restrict__ pp_mask,
+                                   unsigned long long* __restrict__ q_count)
+{ // update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger, hits sorted stably by sink pin
+    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (i >= H || ctrl->stopped || !(sta_out[1] < 0.0)) return;
+    const unsigned key = hk[i];
+    if (key == 0xFFFFFFFFu || (i > 0 && hk[i - 1] == key)) return;
+    const double wns = sta_out[1];
+    const int v = static_cast<int>(key);
+    double w = dl_w[v];
+    const bool fresh = !(w > 0.0);
+    long long j = i;
+    if (fresh) w = w0, ++j;
+    for (; j < H && hk[j] == key; ++j) w += w1 * (hslack[hidx[j]] / wns);
+    dl_w[v] = w;
+    ppw_e[pin_entry[v]] = w;
+    if (fresh) {
+        const int loc = pin_loc[v];
+        if (loc >= 0) atomicOr(&pp_mask[loc >> 3], 1u << (loc & 7));
+        atomicAdd(q_count, 1ull);
+    }
+}
+
+void net_weights_engine(tdpg_session* s, const Ctrl* ctrl);
+
+// Timing round with k > 1 or the topn policy (placer.cpp:415-435): STA graph, then the k-best
+// extraction (host-sized: the path count is data dependent), then the dense-ledger update and net
+// weights, all on the session stream.
+void timing_refresh_general(tdpg_session* s)
+{
+    Engine& E = *s->eng;
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    CK(cudaEventCreate(&ev.first));
+    CK(cudaEventCreate(&ev.second));
+    CK(cudaEventRecord(ev.first, s->st));
+    run_sta_async(s, s->sta_out);
+    k_refresh_begin_gen<<<1, 1, 0, s->st>>>(s->sta_out, E.ctrl, E.timing_row);
+    CK_LAUNCH();
+    double h[3];
+    Ctrl c;
+    CK(cudaMemcpyAsync(h, s->sta_out.p, sizeof h, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&c, E.ctrl.p, sizeof c, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    s->tns = h[0], s->wns = h[1];
+    s->sta_valid = true, s->ties_resolved = false;
+    s->n_paths = 0, s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0, s->uniq_endpoints = 0, s->candidates = 0;
+    E.kernel_launches += 2LL * s->L + 4;
+    if (!c.stopped && h[1] < 0.0) {
+        extract_policy_dev(s, E.cfg.extraction, static_cast<int>(h[2]), E.cfg.k, true);
+        E.kernel_launches += s->L + 16;
+        const long long H = s->n_hits;
+        if (H > 0) {
+            k_ledger_dense_gen<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(
+                H, s->sta_out, E.ctrl, s->kh_key_s, s->kh_idx_s, s->hit_slack, E.cfg.w0, E.cfg.w1, s->dl_w, s->ppw_e,
+                s->pin_entry, s->pin_loc, s->pp_mask, s->q_count);
+            CK_LAUNCH();
+            ++E.kernel_launches;
+        }
+    }
+    if (E.cfg.net_weighting) {
+        net_weights_engine(s, E.ctrl);
+        ++E.kernel_launches;
+    }
+    CK(cudaEventRecord(ev.second, s->st));
+    E.refresh_ev.push_back(ev);
+    ++E.refreshes;
+    if (s->round_cb) {
+        CK(cudaStreamSynchronize(s->st));
+        s->round_cb(s->round_user, E.launched);
+    }
+}
+
 // Timing round (placer.cpp:415-435) as one graph launch: STA, extraction of every violated endpoint,
 // ledger update, net weights; nothing comes back to the host unless an observer is registered.
 void timing_refresh(tdpg_session* s)
 {
     Engine& E = *s->eng;
+    if (E.cfg.extraction != 0 || E.cfg.k != 1) {
+        timing_refresh_general(s);
+        return;
+    }
     std::pair<cudaEvent_t, cudaEvent_t> ev;
     CK(cudaEventCreate(&ev.first));
     CK(cudaEventCreate(&ev.second));

@@ -418,6 +418,36 @@ void resolve_ties_dev(tdpg_session* s)
     s->ties_resolved = true;
 }
 
+// violated_endpoints (paths.cpp:77-87) of the current STA: (slack, pin) order in sort_v1; returns
+// how many endpoints violate.
+int sorted_violated(tdpg_session* s)
+{
+    s->sta_out.reserve(4);
+    double* out3 = s->sta_out.p;
+    const int P = s->P;
+    const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
+    s->part.reserve(3 * nb + 8);
+    const size_t ep = static_cast<size_t>(std::max(s->EP, 1));
+    s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
+    k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0, s->sort_v0,
+                                           s->part);
+    CK_LAUNCH();
+    k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
+    CK_LAUNCH();
+    if (s->EP > 0) {
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, s->EP,
+                                        0, 64, s->st);
+        void* tmp = cub_scratch(s, bytes);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, s->EP,
+                                           0, 64, s->st));
+    }
+    double h[3];
+    CK(cudaMemcpyAsync(h, out3, sizeof h, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    return static_cast<int>(h[2]);
+}
+
 // report_timing_endpoint(n, k = 1) on the current STA (paths.cpp:167-189).
 void extract_endpoint_dev(tdpg_session* s, int n)
 {
@@ -457,6 +487,7 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     }
     const int np = s->n_paths;
     s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0;
+    s->uniq_endpoints = np, s->candidates = np; // k = 1: one path per selected endpoint
     if (np == 0) return;
     s->ex_len.reserve(np), s->ex_hops.reserve(np), s->ex_off.reserve(np), s->ex_hoff.reserve(np);
     s->ex_slack.reserve(np);
@@ -686,6 +717,14 @@ __global__ void k_net_weights_dev(int N, const int* __restrict__ net_start, cons
     w[e] = r;
 }
 
+void net_weights_engine(tdpg_session* s, const Ctrl* ctrl)
+{
+    if (!s->N) return;
+    k_net_weights_dev<<<blocks_for(s->N, kBlock), kBlock, 0, s->st>>>(s->N, s->net_start, s->net_pins, s->slack,
+                                                                      s->sta_out, ctrl, s->net_w);
+    CK_LAUNCH();
+}
+
 static int bits_for(long long n)
 {
     int b = 1;
@@ -858,32 +897,53 @@ int tdpg_sta(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* 
     API_END
 }
 
-int tdpg_extract_endpoint(tdpg_session* s, int32_t n, int32_t k, int64_t counts[4])
+static void extract_timed(tdpg_session* s, int policy, int n, int k)
 {
-    API_BEGIN
-    if (k != 1) throw Error(TDPG_ERR_INTERNAL, "k > 1 per endpoint is not implemented on the device yet");
+    if (k < 1) throw Error(TDPG_ERR_VALIDATION, "validation error: k must be >= 1");
+    if (policy != 0 && policy != 1) throw Error(TDPG_ERR_VALIDATION, "validation error: policy must be \"endpoint\" or \"topn\"");
+    if (!s->sta_valid) run_sta_dev(s);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s->st));
-    extract_endpoint_dev(s, n);
+    if (policy == 0 && k == 1) extract_endpoint_dev(s, n);
+    else extract_policy_dev(s, policy, n, k, false);
     CK(cudaEventRecord(e1, s->st));
     CK(cudaEventSynchronize(e1));
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     s->last_extract_ms = ms;
     cudaEventDestroy(e0), cudaEventDestroy(e1);
-    counts[0] = s->n_paths;
-    counts[1] = s->n_path_pins;
-    counts[2] = s->n_paths; // k = 1: every selected endpoint is covered once
-    counts[3] = s->uniq_pairs;
+}
+
+int tdpg_extract_endpoint(tdpg_session* s, int32_t n, int32_t k, int64_t counts[4])
+{
+    API_BEGIN
+    extract_timed(s, 0, n, k);
+    counts[0] = s->n_paths, counts[1] = s->n_path_pins, counts[2] = s->uniq_endpoints, counts[3] = s->uniq_pairs;
+    API_END
+}
+
+int tdpg_extract(tdpg_session* s, int32_t policy, int32_t n, int32_t k, int64_t counts[5])
+{
+    API_BEGIN
+    extract_timed(s, policy, n, k);
+    counts[0] = s->n_paths, counts[1] = s->n_path_pins, counts[2] = s->uniq_endpoints, counts[3] = s->uniq_pairs;
+    counts[4] = s->candidates;
     API_END
 }
 
 int tdpg_paths_counts(tdpg_session* s, int64_t counts[4])
 {
     API_BEGIN
-    counts[0] = s->n_paths, counts[1] = s->n_path_pins, counts[2] = s->n_paths, counts[3] = s->uniq_pairs;
+    counts[0] = s->n_paths, counts[1] = s->n_path_pins, counts[2] = s->uniq_endpoints, counts[3] = s->uniq_pairs;
+    API_END
+}
+
+int tdpg_paths_candidates(tdpg_session* s, int64_t* candidates)
+{
+    API_BEGIN
+    *candidates = s->candidates;
     API_END
 }
 
@@ -982,7 +1042,21 @@ int tdpg_path_to(tdpg_session* s, int32_t pin, int32_t rank, int32_t* pins, int3
 {
     API_BEGIN
     if (pin < 0 || pin >= s->P) throw Error(TDPG_ERR_VALIDATION, "validation error: pin id out of range");
-    if (rank != 0) throw Error(TDPG_ERR_INTERNAL, "path ranks > 0 (k > 1) are not implemented on the device yet");
+    if (rank < 0) throw Error(TDPG_ERR_VALIDATION, "validation error: rank must be >= 0");
+    if (rank > 0) { // rank-th record of the pin's k-best list (K = rank + 1)
+        std::vector<std::vector<int>> paths;
+        std::vector<double> d;
+        kbest_paths_of(s, pin, rank + 1, paths, d);
+        *n_pins = 0;
+        if (static_cast<int>(paths.size()) <= rank) return TDPG_OK; // exhausted: nullptr in the reference
+        const auto& p = paths[rank];
+        if (static_cast<int>(p.size()) > cap)
+            throw Error(TDPG_ERR_VALIDATION, "validation error: path longer than the output buffer");
+        std::copy(p.begin(), p.end(), pins);
+        *n_pins = static_cast<int32_t>(p.size());
+        if (delay) *delay = d[rank];
+        return TDPG_OK;
+    }
     if (!s->sta_valid) run_sta_dev(s);
     resolve_ties_dev(s);
     uint8_t known = 0;
@@ -1012,6 +1086,33 @@ int tdpg_path_to(tdpg_session* s, int32_t pin, int32_t rank, int32_t* pins, int3
     *n_pins = L;
     if (delay) *delay = a;
     s->n_hits = 0, s->n_paths = 0; // scratch hit buffers were reused
+    API_END
+}
+
+// k_worst_paths_to (paths.cpp:57-72): EndpointError unless `endpoint` is a graph endpoint.
+int tdpg_k_worst(tdpg_session* s, int32_t endpoint, int32_t k, int32_t* n_paths, int32_t* start, int32_t* pins,
+                 int32_t cap, double* slack)
+{
+    API_BEGIN
+    if (endpoint < 0 || endpoint >= s->P || !s->h_is_endpoint[endpoint])
+        throw Error(TDPG_ERR_ENDPOINT, "validation error: pin " + std::to_string(endpoint) + " is not an endpoint");
+    *n_paths = 0;
+    if (start) start[0] = 0;
+    if (k <= 0) return TDPG_OK;
+    std::vector<std::vector<int>> paths;
+    std::vector<double> d;
+    kbest_paths_of(s, endpoint, k, paths, d);
+    int off = 0;
+    for (size_t i = 0; i < paths.size(); ++i) {
+        if (off + static_cast<int>(paths[i].size()) > cap)
+            throw Error(TDPG_ERR_VALIDATION, "validation error: paths exceed the output buffer");
+        if (start) start[i] = off;
+        std::copy(paths[i].begin(), paths[i].end(), pins + off);
+        off += static_cast<int>(paths[i].size());
+        if (slack) slack[i] = s->clock - d[i]; // paths.cpp:69
+    }
+    if (start) start[paths.size()] = off;
+    *n_paths = static_cast<int32_t>(paths.size());
     API_END
 }
 

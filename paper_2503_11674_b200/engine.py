@@ -99,6 +99,9 @@ _SIGS = {
     "tdpg_set_constraints": (C.c_int, [_P, C.c_double, C.c_double, C.c_double]),
     "tdpg_sta_fetch": (C.c_int, [_P, _P, _P, _P, _P, _P, _F64P, _F64P]),
     "tdpg_path_to": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int32, _I32P, _F64P]),
+    "tdpg_extract": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P]),
+    "tdpg_paths_candidates": (C.c_int, [_P, _I64P]),
+    "tdpg_k_worst": (C.c_int, [_P, C.c_int32, C.c_int32, _I32P, _P, _P, C.c_int32, _P]),
     "tdpg_set_round_callback": (C.c_int, [_P, _P, _P]),
     "tdpg_engine_times": (C.c_int, [_P, _F64P, _F64P, _I64P]),
     "tdpg_profile_iteration": (C.c_int, [_P, C.c_int32, _F64P, C.c_int32, C.c_char_p, C.c_int32]),
@@ -264,13 +267,36 @@ class Session:
                                  rk.ctypes.data, C.byref(tns), C.byref(wns)))
         return dict(arr=arr, req=req, slack=slack, arr_known=ak, req_known=rk, tns=tns.value, wns=wns.value)
 
-    def extract(self, xy=None, n=0, k=1, run_sta=True):
+    def extract(self, xy=None, n=0, k=1, run_sta=True, policy=0):
+        """report_timing_endpoint(n, k) (policy 0) / report_timing(n) (policy 1, "topn"); n <= 0 = every
+        violated endpoint."""
         if run_sta or xy is not None:
             self._pos(xy)
             tns, wns = C.c_double(), C.c_double()
             _check(self.lib.tdpg_sta(self.h, None, None, None, None, None, C.byref(tns), C.byref(wns)))
-        cnt = (C.c_int64 * 4)()
-        _check(self.lib.tdpg_extract_endpoint(self.h, n, k, cnt))
+        cnt = (C.c_int64 * 5)()
+        _check(self.lib.tdpg_extract(self.h, policy, n, k, cnt))
+        return self._report(cnt)
+
+    def k_worst(self, endpoint, k, xy=None):
+        """k_worst_paths_to (paths.cpp:57-72): (paths, slacks); EndpointError for a non-endpoint."""
+        if xy is not None:
+            self._pos(xy)
+        n = C.c_int32()
+        cap = max(k, 1) * (self.d.n_pins + 1)
+        start, pins, slack = np.zeros(k + 1, np.int32), np.zeros(cap, np.int32), np.zeros(max(k, 1))
+        _check(self.lib.tdpg_k_worst(self.h, endpoint, k, C.byref(n), start.ctypes.data, pins.ctypes.data, cap,
+                                     slack.ctypes.data))
+        return [pins[start[i]:start[i + 1]].tolist() for i in range(n.value)], slack[:n.value]
+
+    def path_to(self, pin, rank=0):
+        """PathEnumerator::path_to(pin, rank): (pins, delay) or None once exhausted."""
+        buf = np.zeros(self.d.n_pins + 1, np.int32)
+        n, dl = C.c_int32(), C.c_double()
+        _check(self.lib.tdpg_path_to(self.h, pin, rank, buf.ctypes.data, buf.size, C.byref(n), C.byref(dl)))
+        return (buf[:n.value].tolist(), dl.value) if n.value else None
+
+    def _report(self, cnt):
         npath, total = cnt[0], cnt[1]
         start = np.zeros(npath + 1, np.int32)
         pins = np.zeros(max(total, 1), np.int32)
@@ -284,7 +310,7 @@ class Session:
         sta_ms, ex_ms = C.c_double(), C.c_double()
         _check(self.lib.tdpg_last_timing_ms(self.h, C.byref(sta_ms), C.byref(ex_ms)))
         return dict(start=start, pins=pins[:total], slack=slack[:npath], n_paths=npath, unique_endpoints=cnt[2],
-                    unique_pin_pairs=cnt[3], candidates_generated=npath,
+                    unique_pin_pairs=cnt[3], candidates_generated=cnt[4],
                     hits=(ha[:nh.value], hb[:nh.value], hs[:nh.value]), sta_ms=sta_ms.value, extract_ms=ex_ms.value)
 
     # placement -------------------------------------------------------------

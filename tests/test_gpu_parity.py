@@ -224,3 +224,79 @@ def test_large_sta_and_extraction_bitwise(cells):
     assert np.array_equal(es["pins"], eo["pins"]) and np.array_equal(es["slack"], eo["slack"])
     for x, y in zip(es["hits"], eo["hits"]):
         assert np.array_equal(x, y)
+
+
+# ---- k > 1 per endpoint, the topn policy, k_worst_paths_to ----------------------
+POLICIES = ((0, 0, 2), (0, 0, 5), (0, 3, 4), (1, 0, 1), (1, 2, 1), (1, 7, 1))
+
+
+def _same_report(es, eo, tag):
+    assert _paths(es) == _paths(eo), tag
+    assert np.array_equal(es["slack"], eo["slack"]), tag
+    for key in ("unique_endpoints", "unique_pin_pairs", "candidates_generated"):
+        assert es[key] == eo[key], (key, tag)
+    for x, y in zip(es["hits"], eo["hits"]):
+        assert np.array_equal(x, y), tag
+
+
+@pytest.mark.parametrize("seed", range(1, 41))
+def test_random_designs_kbest_and_topn_bitwise(seed):
+    d = random_design(seed)
+    s, o = Session(d), Oracle(d)
+    for policy, n, k in POLICIES:
+        _same_report(s.extract(n=n, k=k, policy=policy), o.extract(n=n, k=k, policy=policy), (policy, n, k))
+    for e in d.endpoints[:4]:
+        ps, ss = s.k_worst(int(e), 6)
+        po, so = o.k_worst(int(e), 6)
+        assert ps == po and np.array_equal(ss, so)
+
+
+def test_path_to_ranks_diamond():
+    """test_paths.cpp:84-103 — M.out rank 0 {0,1,2,5,7} delay 8, rank 1 delay 6, rank 2 exhausted."""
+    from fixtures import make_diamond
+    d = make_diamond()
+    s = Session(d)
+    m_out = d.pin_names.index("M.out")
+    assert s.path_to(m_out, 0) == ([0, 1, 2, 5, 7], 8.0)
+    r1 = s.path_to(m_out, 1)
+    assert r1 is not None and r1[1] == 6.0
+    assert s.path_to(m_out, 2) is None
+
+
+def test_generated_10k_kbest_and_topn(design_10k):
+    d = design_10k
+    xy = spread_positions(d, 3)
+    s, o = Session(d), Oracle(d)
+    for policy, n, k in ((0, 1000, 3), (0, 0, 2), (1, 300, 1)):
+        es, eo = s.extract(xy, n=n, k=k, policy=policy), o.extract(xy, n=n, k=k, policy=policy)
+        assert es["n_paths"] > 0
+        _same_report(es, eo, (policy, n, k))
+
+
+@pytest.mark.parametrize("extraction,k", [("endpoint", 3), ("topn", 1)])
+def test_place_kbest_and_topn_trace_tight(extraction, k):
+    """run_placement with k > 1 / topn: the device loop tracks the oracle row by row (1e-6)."""
+    d = generate(seed=5, cells=300, fail_frac=0.5, calibrate=False)
+    d.clock_period = 0.05
+    cfg = {"max_iters": 40, "timing_start_iter": 10, "m": 5, "grid_nx": 8, "grid_ny": 8, "seed": 5,
+           "extraction": extraction, "k": k}
+    ps, po = Session(d).place(cfg), Oracle(d).place(cfg)
+    assert len(ps["trace"]) == len(po["trace"]) == 40
+    for rs, ro in zip(ps["trace"], po["trace"]):
+        assert abs(rs.hpwl - ro.hpwl) <= 1e-6 * ro.hpwl
+        assert abs(rs.pp_term - ro.pp_term) <= 1e-6 * max(ro.pp_term, 1e-12)
+        if ro.has_timing:
+            assert abs(rs.tns - ro.tns) <= 1e-6 * max(1.0, abs(ro.tns))
+    assert po["trace"][-1].pp_term > 0.0
+
+
+def test_large_kbest_extraction_bitwise():
+    """200K-cell design: endpoint policy k = 4 over the top 5K endpoints, bit-exact vs the C oracle."""
+    d = generate(seed=2, cells=200000, fail_frac=0.4, calibrate=False)
+    d.clock_period = 1.0
+    xy = spread_positions(d, 1)
+    d.clock_period = float(np.quantile(Oracle(d).sta(xy)["arr"][d.endpoints], 0.6))
+    s, o = Session(d), Oracle(d)
+    es, eo = s.extract(xy, n=5000, k=4), o.extract(xy, n=5000, k=4)
+    assert es["n_paths"] > 5000
+    _same_report(es, eo, "200k k=4")

@@ -132,3 +132,18 @@ def test_generated_2k_kbest_topn_spread():
         assert eo["n_paths"] > 0
         assert _paths(eo) == _paths(er) and np.array_equal(eo["slack"], er["slack"]), (policy, n, k)
         assert eo["unique_pin_pairs"] == er["unique_pin_pairs"]
+
+
+@pytest.mark.parametrize("extraction,k", [(0, 3), (1, 1)])
+def test_place_kbest_and_topn_policies_bitwise(extraction, k):
+    """run_placement with k > 1 per endpoint and with the topn policy: the restatement reproduces the
+    reference's whole trajectory bitwise (same fp64 op order, same glibc libm)."""
+    from paper_2503_11674_b200.engine import generate
+    d = generate(seed=5, cells=300, fail_frac=0.5, calibrate=False)
+    d.clock_period = 0.05
+    cfg = {"max_iters": 40, "timing_start_iter": 10, "m": 5, "grid_nx": 8, "grid_ny": 8, "seed": 5,
+           "extraction": "topn" if extraction else "endpoint", "k": k}
+    po, pr = Oracle(d).place(cfg), RefOracle(d).place(cfg)
+    assert po["iterations"] == pr["iterations"]
+    assert (po["tns"], po["wns"], po["hpwl"]) == (pr["tns"], pr["wns"], pr["hpwl"])
+    assert np.array_equal(po["positions"], pr["positions"])
