@@ -12,6 +12,7 @@ import this module, and only as the checker / the timed CPU baseline.
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
 
 import numpy as np
@@ -522,7 +523,7 @@ class RefOracle(_Base):
         self._pos(xy)
         fin = (C.c_double * 3)()
         it, so, npairs, ms = C.c_int32(), C.c_int32(), C.c_int64(), C.c_double()
-        self._check(self.lib.ref_place(self.h, _json.dumps(cfg or {}).encode(), fin, C.byref(it), C.byref(so),
+        self._check(self.lib.ref_place(self.h, json.dumps(cfg or {}).encode(), fin, C.byref(it), C.byref(so),
                                        C.byref(npairs), C.byref(ms)))
         pos = np.zeros((self.d.n_cells, 2))
         self.lib.ref_place_positions(self.h, pos.ctypes.data)
@@ -532,3 +533,9 @@ class RefOracle(_Base):
         return dict(positions=pos, iterations=it.value, stop_reason="overflow" if so.value else "max_iters",
                     tns=fin[0], wns=fin[1], hpwl=fin[2], metrics_csv=csv, trace=parse_metrics_csv(csv),
                     ledger=ledger, elapsed_ms=ms.value)
+
+    def compare(self, configs, parallel=False):
+        """run_compare + compare_to_csv of the reference (compare.cpp:37-122); configs are dicts."""
+        arr = (C.c_char_p * len(configs))(*[json.dumps(c).encode() for c in configs])
+        self._check(self.lib.ref_compare(self.h, arr, len(configs), int(parallel)))
+        return self.lib.ref_place_csv(self.h).decode()

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "tdp/compare.hpp"
 #include "tdp/density.hpp"
 #include "tdp/design_io.hpp"
 #include "tdp/errors.hpp"
@@ -450,6 +451,17 @@ int ref_place_positions(void* h, double* xy)
 }
 
 const char* ref_place_csv(void* h) { return static_cast<RefSession*>(h)->csv.c_str(); }
+
+// run_compare + compare_to_csv (compare.cpp:37-122) with JSON configs; the CSV via ref_place_csv.
+int ref_compare(void* h, const char* const* config_jsons, int32_t n, int32_t parallel)
+{
+    return guard([&] {
+        auto* s = static_cast<RefSession*>(h);
+        std::vector<tdp::OptimizerConfig> cfgs;
+        for (int32_t i = 0; i < n; ++i) cfgs.push_back(tdp::config_from_json(config_jsons[i]));
+        s->csv = tdp::compare_to_csv(tdp::run_compare(s->design, cfgs, parallel != 0));
+    });
+}
 
 // generate_synthetic: the design is held in a fresh session; fetch with ref_design_*.
 int ref_generate(uint64_t seed, int cells, int registers, double fanout, double fail_frac, double r_unit,

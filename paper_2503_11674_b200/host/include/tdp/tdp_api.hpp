@@ -202,8 +202,8 @@ class PathEnumerator {
     const Netlist& netlist_;
     const PinPositions& pos_;
     const DesignConstraints& constraints_;
-    std::map<int, Record> found_;
-    std::map<int, bool> none_;
+    std::map<std::pair<int, std::size_t>, Record> found_;
+    std::map<std::pair<int, std::size_t>, bool> none_;
 };
 
 std::vector<CriticalPath> k_worst_paths_to(const TimingGraph& graph, const Netlist& netlist, const PinPositions& pos,
@@ -314,5 +314,21 @@ using TimingRoundObserver =
 PlacementOutcome run_placement(const Design& design, const OptimizerConfig& config,
                                const TimingRoundObserver& observer = {});
 std::string weights_to_json(const PinPairWeights& weights, const Netlist& netlist);
+
+// ---- ablation harness (include/tdp/compare.hpp) ------------------------------------------------------
+struct CompareRow {
+    std::string config_name;
+    bool ok = false;
+    std::string error;
+    double tns = 0.0, wns = 0.0, hpwl = 0.0, runtime_s = 0.0;
+    int unique_endpoints = 0, unique_pin_pairs = 0;
+    long long candidates_generated = 0;
+};
+struct CompareReport {
+    std::vector<CompareRow> rows;
+};
+CompareReport run_compare(const Design& design, const std::vector<OptimizerConfig>& configs, bool parallel = false);
+std::string compare_to_csv(const CompareReport& report);
+std::string compare_to_table(const CompareReport& report);
 
 } // namespace tdp

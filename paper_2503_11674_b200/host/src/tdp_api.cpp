@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <set>
 
 #include "tdp/tdp_api.hpp"
@@ -116,6 +117,17 @@ std::vector<std::size_t> fingerprint(const Netlist& nl)
 std::mutex g_mu;
 std::map<const Netlist*, std::shared_ptr<Sess>> g_cache;
 
+// A private device session (not cached): concurrent callers (run_compare's parallel rows) each own one.
+std::shared_ptr<Sess> fresh_session(const Netlist& nl, const DesignConstraints& c)
+{
+    auto S = std::make_shared<Sess>();
+    S->flat = std::make_unique<FlatNetlist>(nl, c);
+    S->fp = fingerprint(nl);
+    ck(tdpg_session_create(&S->flat->view, &S->s));
+    ck(tdpg_set_constraints(S->s, c.clock_period > 0 ? c.clock_period : 1.0, c.r_unit, c.c_unit));
+    return S;
+}
+
 // Device session for this netlist (rebuilt when the netlist or the core changed).
 std::shared_ptr<Sess> session(const Netlist& nl, const DesignConstraints& c)
 {
@@ -222,10 +234,11 @@ TimingAnnotation fetch_annotation(tdpg_session* s, const Netlist& nl)
     return ann;
 }
 
-ExtractionReport fetch_report(tdpg_session* s, const Netlist& nl, int n, int k, const int64_t counts[4], double ms)
+ExtractionReport fetch_report(tdpg_session* s, const Netlist& nl, int n, int k, const int64_t counts[5], double ms,
+                              const char* policy = "endpoint")
 {
     ExtractionReport r;
-    r.policy = "endpoint", r.n = n, r.k = k;
+    r.policy = policy, r.n = n, r.k = k;
     const int np = static_cast<int>(counts[0]);
     std::vector<int32_t> start(np + 1), pins(std::max<int64_t>(counts[1], 1));
     std::vector<double> slack(std::max(np, 1));
@@ -234,7 +247,7 @@ ExtractionReport fetch_report(tdpg_session* s, const Netlist& nl, int n, int k, 
         r.paths.push_back(CriticalPath{std::vector<int>(pins.begin() + start[i], pins.begin() + start[i + 1]), slack[i]});
     r.unique_endpoints = static_cast<int>(counts[2]);
     r.unique_pin_pairs = static_cast<int>(counts[3]);
-    r.candidates_generated = np;
+    r.candidates_generated = counts[4];
     r.elapsed_ms = ms;
     (void)nl;
     return r;
@@ -386,22 +399,22 @@ PathEnumerator::PathEnumerator(const TimingGraph& graph, const Netlist& nl, cons
 
 const PathEnumerator::Record* PathEnumerator::path_to(int pin, std::size_t rank)
 {
-    if (rank > 0) throw std::logic_error("path ranks > 0 (k > 1) are not implemented on the device yet");
-    if (auto it = found_.find(pin); it != found_.end()) return &it->second;
-    if (none_.count(pin)) return nullptr;
+    const auto key = std::make_pair(pin, rank);
+    if (auto it = found_.find(key); it != found_.end()) return &it->second;
+    if (none_.count(key)) return nullptr;
     auto S = sta_at(graph_, netlist_, pos_, constraints_);
     std::vector<int32_t> buf(static_cast<std::size_t>(graph_.levels.size()) + 2);
     int32_t n = 0;
     double delay = 0.0;
-    ck(tdpg_path_to(S->s, pin, 0, buf.data(), static_cast<int32_t>(buf.size()), &n, &delay));
+    ck(tdpg_path_to(S->s, pin, static_cast<int32_t>(rank), buf.data(), static_cast<int32_t>(buf.size()), &n, &delay));
     if (n == 0) {
-        none_[pin] = true;
+        none_[key] = true;
         return nullptr;
     }
     Record r;
     r.delay = delay;
     r.pins.assign(buf.begin(), buf.begin() + n);
-    return &found_.emplace(pin, std::move(r)).first->second;
+    return &found_.emplace(key, std::move(r)).first->second;
 }
 
 std::vector<CriticalPath> k_worst_paths_to(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
@@ -411,32 +424,54 @@ std::vector<CriticalPath> k_worst_paths_to(const TimingGraph& graph, const Netli
         throw EndpointError("pin " + std::to_string(endpoint) + " is not an endpoint");
     std::vector<CriticalPath> out;
     if (k <= 0) return out;
-    if (k > 1) throw std::logic_error("k > 1 per endpoint is not implemented on the device yet");
-    PathEnumerator en(graph, nl, pos, c);
-    if (const auto* r = en.path_to(endpoint, 0)) out.push_back(CriticalPath{r->pins, c.clock_period - r->delay});
+    auto S = sta_at(graph, nl, pos, c);
+    const std::size_t cap = static_cast<std::size_t>(k) * (graph.levels.size() + 2);
+    std::vector<int32_t> start(static_cast<std::size_t>(k) + 1), pins(cap);
+    std::vector<double> slack(static_cast<std::size_t>(k));
+    int32_t np = 0;
+    ck(tdpg_k_worst(S->s, endpoint, k, &np, start.data(), pins.data(), static_cast<int32_t>(cap), slack.data()));
+    for (int i = 0; i < np; ++i)
+        out.push_back(CriticalPath{std::vector<int>(pins.begin() + start[i], pins.begin() + start[i + 1]), slack[i]});
     return out;
 }
 
-ExtractionReport report_timing(const TimingGraph&, const Netlist&, const PinPositions&, const DesignConstraints&,
-                               const TimingAnnotation&, int, int)
+namespace {
+// report_timing (policy 1) / report_timing_endpoint (policy 0) through tdpg_extract.  The C-ABI's
+// n <= 0 means "every violated endpoint"; the reference's own n <= 0 clips the selection to nothing
+// (paths.cpp:147, :178), so that case never reaches the device.
+ExtractionReport extract_report(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                                const DesignConstraints& c, const TimingAnnotation& ann, int n, int k, int policy)
 {
-    throw std::logic_error("the topn extraction policy is not implemented on the device yet");
+    const auto t0 = std::chrono::steady_clock::now();
+    ExtractionReport r;
+    r.policy = policy ? "topn" : "endpoint", r.n = n, r.k = policy ? n : k;
+    if (n <= 0) {
+        if (policy) { // candidates_generated = violated.size() * n (paths.cpp:149)
+            long long nv = 0;
+            for (const auto& [pin, slack] : ann.endpoint_slacks) nv += slack < 0.0;
+            r.candidates_generated = n < 0 ? nv * n : 0;
+        }
+        return r;
+    }
+    auto S = sta_at(graph, nl, pos, c);
+    int64_t counts[5];
+    ck(tdpg_extract(S->s, policy, n, k, counts));
+    r = fetch_report(S->s, nl, n, policy ? n : k, counts, 0.0, policy ? "topn" : "endpoint");
+    r.elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return r;
+}
+} // namespace
+
+ExtractionReport report_timing(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
+                               const DesignConstraints& c, const TimingAnnotation& ann, int n, int)
+{
+    return extract_report(graph, nl, pos, c, ann, n, 1, 1);
 }
 
 ExtractionReport report_timing_endpoint(const TimingGraph& graph, const Netlist& nl, const PinPositions& pos,
-                                        const DesignConstraints& c, const TimingAnnotation&, int n, int k, int)
+                                        const DesignConstraints& c, const TimingAnnotation& ann, int n, int k, int)
 {
-    if (k != 1) throw std::logic_error("k > 1 per endpoint is not implemented on the device yet");
-    const auto t0 = std::chrono::steady_clock::now();
-    ExtractionReport r;
-    r.policy = "endpoint", r.n = n, r.k = k;
-    if (n <= 0) return r; // violated.resize(0) (paths.cpp:178)
-    auto S = sta_at(graph, nl, pos, c);
-    int64_t counts[4];
-    ck(tdpg_extract_endpoint(S->s, n, 1, counts));
-    r = fetch_report(S->s, nl, n, k, counts, 0.0);
-    r.elapsed_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    return r;
+    return extract_report(graph, nl, pos, c, ann, n, k, 0);
 }
 
 std::vector<PairHit> collect_pin_pairs(const Netlist& nl, const std::vector<CriticalPath>& paths)
@@ -651,24 +686,41 @@ struct ObserverCtx {
     tdpg_session* s;
     const Netlist* nl;
     const TimingRoundObserver* obs;
+    int policy, k;
 };
 
 void observer_trampoline(void* user, int32_t iter)
 {
     auto* c = static_cast<ObserverCtx*>(user);
     const TimingAnnotation ann = fetch_annotation(c->s, *c->nl);
-    int64_t counts[4];
+    int64_t counts[5];
     ck(tdpg_paths_counts(c->s, counts));
-    ExtractionReport r = fetch_report(c->s, *c->nl, static_cast<int>(counts[0]), 1, counts, 0.0);
+    ck(tdpg_paths_candidates(c->s, &counts[4]));
+    long long n_fail = 0; // the round extracts for n = n_fail (placer.cpp:424-429)
+    for (const auto& [pin, slack] : ann.endpoint_slacks) n_fail += slack < 0.0;
+    const int n = static_cast<int>(n_fail);
+    ExtractionReport r = fetch_report(c->s, *c->nl, n, c->policy ? n : c->k, counts, 0.0,
+                                      c->policy ? "topn" : "endpoint");
     if (ann.wns >= 0.0) r = ExtractionReport{}; // the round was skipped (placer.cpp:422-432)
     (*c->obs)(iter, ann, r);
 }
 } // namespace
 
+namespace {
+PlacementOutcome place_on(const std::shared_ptr<Sess>& S, const Design& design, const OptimizerConfig& config,
+                          const TimingRoundObserver& observer, double* final_hpwl);
+} // namespace
+
 PlacementOutcome run_placement(const Design& design, const OptimizerConfig& config, const TimingRoundObserver& observer)
 {
+    return place_on(session(design.netlist, design.constraints), design, config, observer, nullptr);
+}
+
+namespace {
+PlacementOutcome place_on(const std::shared_ptr<Sess>& S, const Design& design, const OptimizerConfig& config,
+                          const TimingRoundObserver& observer, double* final_hpwl)
+{
     const Netlist& nl = design.netlist;
-    auto S = session(nl, design.constraints);
     set_core(S->s, design.constraints.core);
     const auto xy = flat_points(design.positions);
     ck(tdpg_set_positions(S->s, xy.data()));
@@ -678,7 +730,7 @@ PlacementOutcome run_placement(const Design& design, const OptimizerConfig& conf
     std::vector<tdpg_trace_row> rows(static_cast<std::size_t>(std::max(config.max_iters, 1)));
     int32_t n_rows = 0, stop = 0;
     double fin[3];
-    ObserverCtx ctx{S->s, &nl, &observer};
+    ObserverCtx ctx{S->s, &nl, &observer, cfg.extraction, cfg.k};
     ck(tdpg_set_round_callback(S->s, observer ? observer_trampoline : nullptr, &ctx));
     const int rc = tdpg_place(S->s, &cfg, expl.data(), rows.data(), &n_rows, &stop, fin);
     tdpg_set_round_callback(S->s, nullptr, nullptr);
@@ -699,6 +751,127 @@ PlacementOutcome run_placement(const Design& design, const OptimizerConfig& conf
     out.final_timing = fetch_annotation(S->s, nl); // tdpg_place ran STA at the returned positions
     out.iterations = n_rows;
     out.stop_reason = stop ? "overflow" : "max_iters";
+    if (final_hpwl) *final_hpwl = fin[2];
+    return out;
+}
+
+std::string fmt_g(double v, const char* spec)
+{
+    char buf[64];
+    std::snprintf(buf, sizeof buf, spec, v);
+    return buf;
+}
+
+std::string csv_escape(const std::string& s)
+{
+    if (s.find_first_of(",\"\n") == std::string::npos) return s;
+    std::string out = "\"";
+    for (char c : s) {
+        if (c == '"') out += "\"\"";
+        else out += c;
+    }
+    return out + "\"";
+}
+} // namespace
+
+// run_compare (compare.cpp:37-95): coverage columns on one frozen snapshot, then every configuration in
+// full; with `parallel` the full runs execute concurrently on private device sessions (own streams).
+CompareReport run_compare(const Design& design, const std::vector<OptimizerConfig>& configs, bool parallel)
+{
+    if (configs.size() < 2) throw ValidationError("compare: need >= 2 configurations");
+    for (const OptimizerConfig& c : configs)
+        if (c.seed != configs.front().seed)
+            throw ValidationError("compare: all configurations must share one seed (config \"" + c.name +
+                                  "\" differs)");
+    CompareReport report;
+    report.rows.resize(configs.size());
+    OptimizerConfig snap_cfg = configs.front();
+    snap_cfg.beta = 0.0;
+    snap_cfg.net_weighting = false;
+    snap_cfg.max_iters = std::min(snap_cfg.max_iters, snap_cfg.timing_start_iter);
+    snap_cfg.timing_start_iter = snap_cfg.max_iters + 1;
+    snap_cfg.stop_overflow = 0.0;
+    const PlacementOutcome snapshot = run_placement(design, snap_cfg);
+    const TimingGraph graph = build_timing_graph(design.netlist);
+    const PinPositions snap_pins = pin_positions(design.netlist, snapshot.positions);
+    const TimingAnnotation snap_ann = run_sta(graph, design.netlist, snap_pins, design.constraints);
+    int n_fail = 0;
+    for (const auto& [pin, slack] : snap_ann.endpoint_slacks) n_fail += slack < 0.0;
+    for (std::size_t i = 0; i < configs.size(); ++i) { // coverage (serial: the cached session)
+        CompareRow& row = report.rows[i];
+        row.config_name = configs[i].name;
+        if (n_fail <= 0) continue;
+        try {
+            const ExtractionReport ext =
+                configs[i].extraction == ExtractionPolicy::Endpoint
+                    ? report_timing_endpoint(graph, design.netlist, snap_pins, design.constraints, snap_ann, n_fail,
+                                             configs[i].k)
+                    : report_timing(graph, design.netlist, snap_pins, design.constraints, snap_ann, n_fail);
+            row.unique_endpoints = ext.unique_endpoints;
+            row.unique_pin_pairs = ext.unique_pin_pairs;
+            row.candidates_generated = ext.candidates_generated;
+        } catch (const std::exception& e) {
+            row.error = e.what();
+        }
+    }
+    auto run = [&](std::size_t i, bool priv) {
+        CompareRow& row = report.rows[i];
+        if (!row.error.empty()) return;
+        try {
+            const auto t0 = std::chrono::steady_clock::now();
+            double h = 0.0;
+            const auto S = priv ? fresh_session(design.netlist, design.constraints)
+                                : session(design.netlist, design.constraints);
+            const PlacementOutcome outcome = place_on(S, design, configs[i], {}, &h);
+            row.runtime_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            row.tns = outcome.final_timing.tns;
+            row.wns = outcome.final_timing.wns;
+            row.hpwl = h; // hpwl_total at the final positions (tdpg_place)
+            row.ok = true;
+        } catch (const std::exception& e) {
+            row.ok = false;
+            row.error = e.what();
+        }
+    };
+    if (parallel) {
+        std::vector<std::thread> ts;
+        for (std::size_t i = 0; i < configs.size(); ++i) ts.emplace_back(run, i, true);
+        for (auto& t : ts) t.join();
+    } else {
+        for (std::size_t i = 0; i < configs.size(); ++i) run(i, false);
+    }
+    return report;
+}
+
+std::string compare_to_csv(const CompareReport& report)
+{ // compare.cpp:97-122
+    std::string out = "config,status,tns,wns,hpwl,runtime_s,unique_endpoints,unique_pin_pairs,candidates_generated\n";
+    for (const CompareRow& r : report.rows) {
+        out += csv_escape(r.config_name) + ',' + (r.ok ? std::string("ok") : csv_escape(r.error)) + ',';
+        out += fmt_g(r.tns, "%.17g") + ',' + fmt_g(r.wns, "%.17g") + ',' + fmt_g(r.hpwl, "%.17g") + ',';
+        out += fmt_g(r.runtime_s, "%.3f") + ',' + std::to_string(r.unique_endpoints) + ',';
+        out += std::to_string(r.unique_pin_pairs) + ',' + std::to_string(r.candidates_generated) + '\n';
+    }
+    return out;
+}
+
+std::string compare_to_table(const CompareReport& report)
+{ // compare.cpp:124-150
+    std::string out;
+    char line[256];
+    std::snprintf(line, sizeof line, "%-24s %-6s %14s %12s %14s %10s %8s %8s %12s\n", "config", "status", "tns",
+                  "wns", "hpwl", "runtime_s", "uniq_ep", "uniq_pp", "candidates");
+    out += line;
+    out += std::string(24 + 1 + 6 + 1 + 14 + 1 + 12 + 1 + 14 + 1 + 10 + 1 + 8 + 1 + 8 + 1 + 12, '-') + '\n';
+    for (const CompareRow& r : report.rows) {
+        if (r.ok)
+            std::snprintf(line, sizeof line, "%-24s %-6s %14.4f %12.4f %14.2f %10.2f %8d %8d %12lld\n",
+                          r.config_name.c_str(), "ok", r.tns, r.wns, r.hpwl, r.runtime_s, r.unique_endpoints,
+                          r.unique_pin_pairs, r.candidates_generated);
+        else
+            std::snprintf(line, sizeof line, "%-24s %-6s %s\n", r.config_name.c_str(), "error", r.error.c_str());
+        out += line;
+    }
     return out;
 }
 

@@ -3,9 +3,8 @@
 Same functions, arguments, JSON shapes and exception types as the reference's
 pybind11 ``_core`` + wrapper (python/src/bindings.cpp:28-160,
 python/tdplace/__init__.py:42-98), computed by the sm_100a engine through the
-C-ABI.  Not on the device yet: ``compare_csv`` (ablation harness) and
-``render_svg`` (visualisation) — SURVEY.md §8(f)/out of scope; the ``topn``
-policy and k > 1 raise NotImplementedError.
+C-ABI (``compare_csv`` orchestrates device sessions).  ``render_svg``
+(visualisation) is out of scope.
 """
 from __future__ import annotations
 
@@ -179,14 +178,20 @@ def report_paths(design, placement=None, policy="endpoint", n=0, k=1):
     """Worst-path report dict (report_to_json); n <= 0 covers every violated endpoint."""
     if policy not in ("endpoint", "topn"):
         raise ValidationError('validation error: policy must be "endpoint" or "topn"')
-    if policy == "topn" or k != 1:
-        raise NotImplementedError("the topn policy and k > 1 are not implemented on the device yet")
     d = _design(design, placement)
-    r = _engine.Session(d).extract(n=n if n > 0 else 0)
+    s = _engine.Session(d)
+    t = s.sta()
+    if n <= 0:  # bindings.cpp:82-86
+        n = int(_np.sum(t["slack"][d.endpoints] < 0.0))
+    topn = policy == "topn"
+    if n <= 0:
+        return {"policy": policy, "n": 0, "k": 0 if topn else k, "candidates_generated": 0, "elapsed_ms": 0.0,
+                "paths": [], "unique_endpoints": 0, "unique_pin_pairs": 0}
+    r = s.extract(n=n, k=k, run_sta=False, policy=1 if topn else 0)
     pn = d.pin_names
     paths = [{"slack": float(r["slack"][i]), "pins": [pn[p] for p in r["pins"][r["start"][i]:r["start"][i + 1]]]}
              for i in range(r["n_paths"])]
-    return {"policy": "endpoint", "n": int(n if n > 0 else r["n_paths"]), "k": k,
+    return {"policy": policy, "n": int(n), "k": int(n if topn else k),
             "candidates_generated": int(r["candidates_generated"]), "elapsed_ms": float(r["extract_ms"]),
             "paths": paths, "unique_endpoints": int(r["unique_endpoints"]),
             "unique_pin_pairs": int(r["unique_pin_pairs"])}
@@ -227,9 +232,75 @@ def hpwl(design, placement=None):
     return _engine.Session(d).hpwl()
 
 
+def _csv_escape(t: str) -> str:  # compare.cpp:24-34
+    if not any(ch in t for ch in ',"\n'):
+        return t
+    return '"' + t.replace('"', '""') + '"'
+
+
+@_guard
 def compare_csv(design, configs, parallel=False):
-    """Ablation comparison (run_compare) — not on the device yet."""
-    raise NotImplementedError("compare_csv: the ablation harness is not part of the device hot path yet")
+    """Ablation comparison (run_compare, compare.cpp:37-95 + compare_to_csv :97-122) on the device.
+
+    Coverage columns come from one frozen snapshot (the first config with beta = 0 and no net
+    weighting, stopped where its timing rounds would begin), STA'd once, each row's extraction policy
+    evaluated there; then every config runs in full.  With ``parallel`` the full runs execute
+    concurrently, one device session (own stream) per config."""
+    import concurrent.futures as _cf
+
+    d = _design(design)
+    raw = [dict(_load(c) or {}) for c in configs]
+    if len(raw) < 2:
+        raise ValidationError("validation error: compare: need >= 2 configurations")
+    full = [dict(_DEFAULTS, **c) for c in raw]
+    for c in full:
+        if c["seed"] != full[0]["seed"]:
+            raise ValidationError("validation error: compare: all configurations must share one seed "
+                                  f'(config "{c.get("name", "default")}" differs)')
+    names = [c.pop("name", "default") for c in full]
+    snap = dict(full[0], beta=0.0, net_weighting=False, stop_overflow=0.0)
+    snap["max_iters"] = min(snap["max_iters"], snap["timing_start_iter"])
+    snap["timing_start_iter"] = snap["max_iters"] + 1
+    snap_xy = _engine.Session(d).place(snap)["positions"]
+    probe = _engine.Session(d)
+    t = probe.sta(snap_xy)
+    n_fail = int(_np.sum(t["slack"][d.endpoints] < 0.0))
+    rows = [{"config": names[i], "ok": False, "error": "", "tns": 0.0, "wns": 0.0, "hpwl": 0.0, "runtime_s": 0.0,
+             "ue": 0, "upp": 0, "cand": 0} for i in range(len(full))]
+    for i, c in enumerate(full):  # coverage on the shared snapshot
+        if n_fail <= 0:
+            continue
+        try:
+            r = probe.extract(n=n_fail, k=int(c["k"]), run_sta=False, policy=1 if c["extraction"] == "topn" else 0)
+            rows[i].update(ue=int(r["unique_endpoints"]), upp=int(r["unique_pin_pairs"]),
+                           cand=int(r["candidates_generated"]))
+        except Exception as e:  # noqa: BLE001  (a failing row records its error, compare.cpp:88-91)
+            rows[i]["error"] = str(e)
+
+    def run(i):
+        if rows[i]["error"]:
+            return
+        try:
+            t0 = _time.perf_counter()
+            out = _engine.Session(d).place(full[i])
+            rows[i].update(runtime_s=_time.perf_counter() - t0, tns=out["tns"], wns=out["wns"], hpwl=out["hpwl"],
+                           ok=True)
+        except Exception as e:  # noqa: BLE001
+            rows[i]["error"] = str(e)
+
+    if parallel:
+        with _cf.ThreadPoolExecutor(max_workers=len(full)) as ex:
+            list(ex.map(run, range(len(full))))
+    else:
+        for i in range(len(full)):
+            run(i)
+    g = lambda v: "%.17g" % v  # noqa: E731
+    out = ["config,status,tns,wns,hpwl,runtime_s,unique_endpoints,unique_pin_pairs,candidates_generated"]
+    for r in rows:
+        out.append(",".join([_csv_escape(r["config"]), "ok" if r["ok"] else _csv_escape(r["error"]), g(r["tns"]),
+                             g(r["wns"]), g(r["hpwl"]), "%.3f" % r["runtime_s"], str(r["ue"]), str(r["upp"]),
+                             str(r["cand"])]))
+    return "\n".join(out) + "\n"
 
 
 def render_svg(design, placement=None, paths=None):

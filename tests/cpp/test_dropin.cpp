@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "tdp/compare.hpp"
 #include "tdp/density.hpp"
 #include "tdp/errors.hpp"
 #include "tdp/netlist.hpp"
@@ -148,6 +149,59 @@ int main()
             CHECK(r0 && r0->delay == 8.0 && r0->pins == (std::vector<int>{0, 1, 2, 5, 7}));
         }
         std::printf("ok   diamond paths / tie / EndpointError / PathEnumerator rank 0\n");
+    }
+    { // test_paths.cpp:42-103: k worst paths, the tie order for k = 2, path_to ranks and exhaustion
+        const Design d = diamond(7, 5);
+        const TimingGraph g = build_timing_graph(d.netlist);
+        const auto pos = pin_positions(d.netlist, d.positions);
+        const auto t = run_sta(g, d.netlist, pos, d.constraints);
+        const auto k2 = k_worst_paths_to(g, d.netlist, pos, d.constraints, t, 8, 2);
+        CHECK(k2.size() == 2 && k2[1].pins == (std::vector<int>{0, 3, 4, 6, 7, 8}) && k2[1].slack == 4.0);
+        CHECK(k_worst_paths_to(g, d.netlist, pos, d.constraints, t, 8, 3).size() == 2);
+        PathEnumerator en(g, d.netlist, pos, d.constraints);
+        const auto* r1 = en.path_to(7, 1);
+        CHECK(r1 && r1->delay == 6.0 && en.path_to(7, 2) == nullptr);
+        const Design e = diamond(7, 7);
+        const TimingGraph ge = build_timing_graph(e.netlist);
+        const auto pe = pin_positions(e.netlist, e.positions);
+        const auto te = run_sta(ge, e.netlist, pe, e.constraints);
+        const auto tie = k_worst_paths_to(ge, e.netlist, pe, e.constraints, te, 8, 2);
+        CHECK(tie.size() == 2 && tie[0].slack == tie[1].slack && tie[0].pins < tie[1].pins);
+        std::printf("ok   k worst paths / path_to ranks / tie order\n");
+    }
+    { // test_paths.cpp:105-139: topn piles onto the worst endpoint; n beyond the violated set
+        const Design d = t2();
+        const TimingGraph g = build_timing_graph(d.netlist);
+        const auto pos = pin_positions(d.netlist, d.positions);
+        const auto t = run_sta(g, d.netlist, pos, d.constraints);
+        const auto r = report_timing(g, d.netlist, pos, d.constraints, t, 2);
+        CHECK(r.policy == "topn" && r.paths.size() == 2 && r.paths[0].slack == -5.0 && r.paths[1].slack == -4.0);
+        CHECK(r.unique_endpoints == 1 && r.candidates_generated == 4 && r.unique_pin_pairs == 5);
+        const auto r10 = report_timing(g, d.netlist, pos, d.constraints, t, 10);
+        CHECK(r10.paths.size() == 3 && r10.candidates_generated == 20 && r10.unique_endpoints == 2);
+        std::printf("ok   topn policy\n");
+    }
+    { // compare.cpp:37-95: two configs on a tight T2, serial and parallel give the same rows
+        Design d = t2();
+        d.constraints.clock_period = 2.0;
+        OptimizerConfig a, b;
+        a.name = "endpoint", a.max_iters = 30, a.timing_start_iter = 10, a.m = 5, a.grid_nx = a.grid_ny = 8;
+        b = a, b.name = "topn", b.extraction = ExtractionPolicy::TopN;
+        const CompareReport s = run_compare(d, {a, b}, false), p = run_compare(d, {a, b}, true);
+        CHECK(s.rows.size() == 2 && s.rows[0].ok && s.rows[1].ok);
+        for (int i = 0; i < 2; ++i)
+            CHECK(s.rows[i].tns == p.rows[i].tns && s.rows[i].hpwl == p.rows[i].hpwl &&
+                  s.rows[i].candidates_generated == p.rows[i].candidates_generated);
+        CHECK(compare_to_csv(s).rfind("config,status,tns,wns,hpwl,runtime_s,", 0) == 0);
+        b.seed = 2;
+        bool threw = false;
+        try {
+            run_compare(d, {a, b});
+        } catch (const ValidationError& e) {
+            threw = std::string(e.what()).find("share one seed") != std::string::npos;
+        }
+        CHECK(threw);
+        std::printf("ok   run_compare / compare_to_csv\n");
     }
     { // test_paths.cpp:105-139 endpoint policy counters
         const Design d = t2();

@@ -90,3 +90,53 @@ def test_generated_names_match_reference_json():
     assert [c["name"] for c in d["cells"]] == [c["name"] for c in ref["cells"]]
     assert [p["name"] for p in d["pins"]] == [p["name"] for p in ref["pins"]]
     assert d["nets"] == ref["nets"] and d["sources"] == ref["sources"] and d["endpoints"] == ref["endpoints"]
+
+
+@pytest.mark.gpu
+def test_report_paths_topn_and_k():
+    """report_paths with the topn policy and k > 1 (bindings.cpp:75-97) against the compiled reference."""
+    from oracle.oracle import RefOracle
+    if not RefOracle.available():
+        pytest.skip("oracle/_ref not built")
+    dj = tdplace.generate(seed=6, cells=400, fail_frac=0.6)
+    from paper_2503_11674_b200.design import Design
+    d = Design.from_json(dj)
+    for policy, n, k in (("endpoint", 20, 3), ("topn", 15, 1), ("endpoint", 0, 2)):
+        rep = tdplace.report_paths(dj, policy=policy, n=n, k=k)
+        ref = RefOracle(d).extract(n=n, k=k, policy=1 if policy == "topn" else 0)
+        assert rep["policy"] == policy and len(rep["paths"]) == ref["n_paths"] > 0
+        assert [p["slack"] for p in rep["paths"]] == list(ref["slack"])
+        names = d.pin_names
+        ref_paths = [[names[q] for q in ref["pins"][ref["start"][i]:ref["start"][i + 1]]] for i in range(ref["n_paths"])]
+        assert [p["pins"] for p in rep["paths"]] == ref_paths
+        assert rep["candidates_generated"] == ref["candidates_generated"]
+        assert rep["unique_pin_pairs"] == ref["unique_pin_pairs"] and rep["unique_endpoints"] == ref["unique_endpoints"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parallel", [False, True])
+def test_compare_csv_against_reference(parallel):
+    """run_compare (compare.cpp:37-95): coverage columns bit-exact (same snapshot, same extraction),
+    final TNS / WNS / HPWL of every row within 1e-6 of the compiled reference on a short schedule."""
+    from oracle.oracle import RefOracle
+    if not RefOracle.available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2503_11674_b200.design import Design
+    dj = tdplace.generate(seed=7, cells=300, fail_frac=0.6)
+    base = {"max_iters": 40, "timing_start_iter": 15, "m": 5, "grid_nx": 8, "grid_ny": 8, "seed": 3}
+    cfgs = [dict(base, name="endpoint"), dict(base, name="endpoint_k3", k=3), dict(base, name="topn", extraction="topn"),
+            dict(base, name="netw", net_weighting=True, beta=0.0)]
+    ours = tdplace.compare_csv(dj, cfgs, parallel=parallel).splitlines()
+    ref = RefOracle(Design.from_json(dj)).compare(cfgs).splitlines()
+    assert ours[0] == ref[0] and len(ours) == len(ref) == 5
+    for a, b in zip(ours[1:], ref[1:]):
+        ra, rb = a.split(","), b.split(",")
+        assert ra[0] == rb[0] and ra[1] == rb[1] == "ok"
+        assert ra[6:] == rb[6:], (ra, rb)  # unique endpoints / pairs / candidates
+        for j in (2, 3, 4):
+            x, y = float(ra[j]), float(rb[j])
+            assert abs(x - y) <= 1e-6 * max(1.0, abs(y)), (ra[0], j, x, y)
+    with pytest.raises(tdplace.ValidationError, match="share one seed"):
+        tdplace.compare_csv(dj, [base, dict(base, seed=9)])
+    with pytest.raises(tdplace.ValidationError, match="need >= 2"):
+        tdplace.compare_csv(dj, [base])
