@@ -116,7 +116,7 @@ struct tdpg_session {
     tdpg::DBuf<double> sta_out;  // tns, wns, n_violated
     tdpg::DBuf<double> sta_part; // STA reduction partials
     cudaGraphExec_t sta_gexec = nullptr; // the per-level STA sweep, captured once
-    std::array<const void*, 6> sta_graph_key{};
+    std::array<uint64_t, 9> sta_graph_key{};
     // ledger-update scratch
     tdpg::DBuf<uint8_t> lg_flag;
     tdpg::DBuf<double> lg_w, lg_new_w;

@@ -7,6 +7,7 @@
 #include <array>
 #include <climits>
 #include <cmath>
+#include <cstring>
 
 #include "gp_kernels.cuh"
 
@@ -380,8 +381,12 @@ void run_sta_async(tdpg_session* s, double* out3)
     s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
     const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(s->P, s->EP), kBlock))));
     s->sta_part.reserve(3 * nb + 8);
-    const std::array<const void*, 6> key = {s->pin_xy_external ? s->pin_xy.p : nullptr, s->cell_xy.p, s->sort_k0.p,
-                                            s->sort_v0.p, s->sta_part.p, out3};
+    // the graph bakes buffer pointers and the constraints (kernel arguments) in: re-capture on any change
+    auto bits = [](double x) { uint64_t u; std::memcpy(&u, &x, sizeof u); return u; };
+    auto ptr = [](const void* p) { return static_cast<uint64_t>(reinterpret_cast<uintptr_t>(p)); };
+    const std::array<uint64_t, 9> key = {ptr(s->pin_xy_external ? s->pin_xy.p : nullptr), ptr(s->cell_xy.p),
+                                         ptr(s->sort_k0.p), ptr(s->sort_v0.p), ptr(s->sta_part.p), ptr(out3),
+                                         bits(s->clock), bits(s->r_unit), bits(s->c_unit)};
     if (!s->sta_gexec || key != s->sta_graph_key) {
         if (s->sta_gexec) cudaGraphExecDestroy(s->sta_gexec), s->sta_gexec = nullptr;
         cudaGraph_t g = nullptr;

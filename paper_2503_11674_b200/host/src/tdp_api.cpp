@@ -98,20 +98,30 @@ struct Sess {
     }
 };
 
+// Content hash of everything the device session holds (sizes, cell geometry/delays/fixed flags, pin
+// ownership/offsets/terminal positions/directions/caps, net membership, sources, endpoints): a cached
+// session is reused only for an identical netlist, never for a different one at the same address.
 std::vector<std::size_t> fingerprint(const Netlist& nl)
 {
-    std::vector<std::size_t> f = {nl.cells.size(), nl.pins.size(), nl.nets.size(), nl.sources.size(),
-                                  nl.endpoints.size()};
-    const std::size_t P = nl.pins.size(), N = nl.nets.size();
-    for (std::size_t k = 0; k < 16 && P; ++k) {
-        const Pin& p = nl.pins[k * P / 16];
-        f.push_back(static_cast<std::size_t>(p.cell + 7) * 31 + (p.dir == PinDir::Output));
+    std::uint64_t h = 1469598103934665603ull; // FNV-1a over the raw field bytes
+    auto mix = [&](const void* p, std::size_t n) {
+        const auto* b = static_cast<const unsigned char*>(p);
+        for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    };
+    auto d = [&](double x) { mix(&x, sizeof x); };
+    auto i32 = [&](int x) { mix(&x, sizeof x); };
+    for (const Cell& c : nl.cells) d(c.width), d(c.height), d(c.delay), i32(c.is_fixed);
+    for (const Pin& p : nl.pins)
+        i32(p.cell), d(p.terminal_pos.x), d(p.terminal_pos.y), d(p.offset.x), d(p.offset.y),
+            i32(p.dir == PinDir::Output), d(p.load_cap);
+    for (const Net& n : nl.nets) {
+        i32(n.driver), i32(static_cast<int>(n.sinks.size()));
+        if (!n.sinks.empty()) mix(n.sinks.data(), n.sinks.size() * sizeof(int));
     }
-    for (std::size_t k = 0; k < 16 && N; ++k) {
-        const Net& n = nl.nets[k * N / 16];
-        f.push_back(static_cast<std::size_t>(n.driver) * 131 + n.sinks.size());
-    }
-    return f;
+    if (!nl.sources.empty()) mix(nl.sources.data(), nl.sources.size() * sizeof(int));
+    if (!nl.endpoints.empty()) mix(nl.endpoints.data(), nl.endpoints.size() * sizeof(int));
+    return {nl.cells.size(), nl.pins.size(), nl.nets.size(), nl.sources.size(), nl.endpoints.size(),
+            static_cast<std::size_t>(h)};
 }
 
 std::mutex g_mu;
