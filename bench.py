@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--fail-frac", type=float, default=0.8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-evals", type=int, default=2)
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "partition"],
+                    help="N > 1: independent designs per GPU (weak scaling) or one design with nets partitioned "
+                         "across GPUs and the cell gradient all-reduced by NCCL inside the iteration graph "
+                         "(strong scaling, SURVEY §8e)")
     return ap.parse_args()
 
 
@@ -271,10 +275,14 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2503_11674_b200.engine import Session
 
-    d, gen_s = make_design(args, rank)
+    partition = world > 1 and args.mode == "partition"
+    d, gen_s = make_design(args, 0 if partition else rank)  # partition: every rank holds the same design
     total_iters = args.warmup + args.steps + 64
     cfg = bench_config(args, total_iters)
     s = Session(d)
+    if partition:
+        from paper_2503_11674_b200 import distributed as D
+        D.init_partitioned(s, rank, world)
     t0 = time.time()
     s.engine_init(cfg)
     init_s = time.time() - t0
@@ -300,13 +308,22 @@ def run_ours(args):
         import torch.distributed as dist
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dev_ms_max = float(ms.item())
-    value = world * args.steps / (dev_ms_max / 1000.0)
+    value = (1 if partition else world) * args.steps / (dev_ms_max / 1000.0)
     launches = st1["kernel_launches"] - st0["kernel_launches"]
     refreshes = st1["refreshes"] - st0["refreshes"]
     refresh_ms = st1["refresh_ms"] - st0["refresh_ms"]
 
-    # per-kernel profile of loop iterations (roofline of the dominant kernel)
-    prof = s.profile_iteration(5)
+    # per-kernel profile of loop iterations (roofline of the dominant kernel); a partitioned engine
+    # is profiled through its replica twin on rank 0 below
+    if partition and rank != 0:
+        prof = {}
+    elif partition:
+        s_prof = Session(d)
+        s_prof.engine_init(cfg)
+        s_prof.iterate(args.warmup)
+        prof = s_prof.profile_iteration(5)
+    else:
+        prof = s.profile_iteration(5)
 
     # e2e: the same iterations through host buffers (pinned), positions in/out every step
     C = d.n_cells
@@ -319,7 +336,7 @@ def run_ours(args):
         s.step_host(hin.data_ptr(), hout.data_ptr())
         hin, hout = hout, hin
     e2e_s = time.perf_counter() - t0
-    e2e_val = world * e2e_steps / e2e_s
+    e2e_val = (1 if partition else world) * e2e_steps / e2e_s
     sweep, xy_snap = (extraction_sweep(d) if rank == 0 else ({}, None))
 
     if rank != 0:
@@ -345,7 +362,7 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "iters/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if partition else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"configs[2]: synthetic {d.n_cells}-cell / {d.n_nets}-net netlist "
                                f"(generator spec {args.cells}, fail_frac {args.fail_frac}), full timing-driven GP "
                                f"iteration, grid {args.grid}^2, timing refresh every {args.m} iterations "
@@ -353,7 +370,8 @@ def run_ours(args):
                    "cells": d.n_cells, "pins": d.n_pins, "nets": d.n_nets, "net_pins": d.n_net_pins,
                    "endpoints": int(d.endpoints.size), "grid": args.grid, "m": args.m,
                    "l2": "working set per iteration > L2 (positions+netlist+gradients+grid ~ 2x 126 MB)",
-                   "parallelism": "replicas only" if world > 1 else "single GPU", "refreshes_timed": refreshes,
+                   "parallelism": ("nets partitioned, NCCL all-reduce of the cell gradient" if partition else
+                                   "replicas") if world > 1 else "single GPU", "refreshes_timed": refreshes,
                    "refresh_ms_timed": round(refresh_ms, 3), "ledger_pairs_end": st1["ledger_pairs"]},
         "e2e": {"value": round(e2e_val, 3), "unit": "iters/s", "h2d_bytes_per_step": 16 * C,
                 "d2h_bytes_per_step": 16 * C + 88, "path": "tdpg_step_host (C-ABI, pinned host positions)"},

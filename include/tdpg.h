@@ -229,6 +229,22 @@ int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_tr
 /* Per-kernel device time (ms) of one iteration of each kind, measured with events. */
 int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_t n_out, char* names, int32_t name_len);
 
+/* ---- single-design multi-GPU: net-partitioned gradient + NCCL all-reduce --------
+ * Nets (WA entries and the net-arc pin pairs fused into WA) are split into contiguous WA-block ranges
+ * balanced by net-pin entries; each rank folds its entries into a partial cell gradient, one NCCL sum
+ * all-reduce over [partial d_cell | WA, HPWL, PP block partials] completes gradient and objective terms
+ * on every rank; density, Adam and timing refreshes are replicated (run_placement semantics kept).
+ * tdpg_partition_plan: bounds [world+1] = per-rank WA block ranges, rank_entries [world] (host only).   */
+int tdpg_partition_plan(int32_t n_nets, const int32_t* net_start, int32_t world, int32_t* bounds,
+                        int64_t* rank_entries);
+int tdpg_set_partition(tdpg_session* s, int32_t rank, int32_t world); /* no communicator: split-phase API */
+int tdpg_comm_unique_id(uint8_t id[128]);                            /* ncclGetUniqueId (rank 0)        */
+int tdpg_comm_init(tdpg_session* s, int32_t rank, int32_t world, const uint8_t id[128]);
+/* Split-phase partitioned iteration (the caller reduces, e.g. tests on one GPU): phase A returns this
+ * rank's all-reduce buffer (n_red doubles); phase B takes the element-wise sum over ranks. */
+int tdpg_part_step_a(tdpg_session* s, double* red, int64_t* n_red);
+int tdpg_part_step_b(tdpg_session* s, const double* red);
+
 /* ---- synthetic designs (generate_synthetic semantics) ---------------- */
 typedef struct tdpg_design tdpg_design;
 /* Builds the netlist exactly as the reference generator (same mt19937_64 stream);

@@ -105,7 +105,9 @@ struct tdpg_session {
     std::vector<int> h_pin_driver;
 
     // device timing graph
-    tdpg::DBuf<int> lvl_pins, in_start, in_from, out_start, out_to, ep_sorted;
+    tdpg::DBuf<int> lvl_pins, lvl_start, in_start, in_from, out_start, out_to, ep_sorted;
+    tdpg::DBuf<unsigned> grid_bar;   // persistent STA: grid barrier (arrival count, generation)
+    int sta_grid = 0;                // co-resident blocks of the persistent STA kernel (0: per-level launches)
 
     // STA state
     tdpg::DBuf<double2> pin_xy;
@@ -173,6 +175,11 @@ struct tdpg_session {
     tdpg::DBuf<int> sort_v0, sort_v1;
     tdpg::HBuf<long long> h_small;
 
+    // partitioned multi-GPU mode (partition.cu): this rank's WA block range, NCCL communicator
+    int part_rank = 0, part_world = 1, part_b0 = 0, part_b1 = 0;
+    bool part_active = false; // WA launches honour the range only while the partitioned graph is recorded
+    void* comm = nullptr; // ncclComm_t
+
     // placement engine
     tdpg::Engine* eng = nullptr;
     tdpg_round_cb round_cb = nullptr; // called after every timing round of tdpg_place
@@ -202,6 +209,7 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
 
 // timing.cu
 void run_sta_dev(tdpg_session* s);
+void sta_setup(tdpg_session* s);
 void refresh_reserve(tdpg_session* s);
 void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting);
 void dense_ledger_to_sorted(tdpg_session* s);
@@ -210,6 +218,10 @@ void resolve_ties_dev(tdpg_session* s);
 void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool hits_all_violated);
 void net_weights_dev(tdpg_session* s);
 int sorted_violated(tdpg_session* s);
+
+// partition.cu
+void comm_allreduce(tdpg_session* s, double* buf, size_t n);
+void comm_destroy(tdpg_session* s);
 
 // kpaths.cu
 void kbest_build(tdpg_session* s, int K);

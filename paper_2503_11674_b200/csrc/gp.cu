@@ -717,6 +717,7 @@ struct CellArgs {
     const double2* wh;
     const double2* dgrad;
     double2* d_cell;    // optional gradient output
+    const double2* folded; // partitioned mode: the all-reduced fold (skips the fold)
     double2* m;         // Adam state (iteration mode)
     double2* v;
     double b1, b2, eps;
@@ -730,7 +731,9 @@ __global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __r
     const bool adam = cur->do_adam;
     if (ctrl && !adam && !a.d_cell) return; // stopped: nothing to do
     double gx = 0.0, gy = 0.0;
-    {   // fold in ascending pin order (placer.cpp:318-325); loads batched 4 at a time
+    if (a.folded) {
+        gx = a.folded[c].x, gy = a.folded[c].y;
+    } else { // fold in ascending pin order (placer.cpp:318-325); loads batched 4 at a time
         const int j0 = a.ent_start[c], j1 = a.ent_start[c + 1];
         for (int j = j0; j < j1; j += 4) {
             double2 ge[4];
@@ -766,6 +769,22 @@ __global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __r
     y = y < a.core_y0 ? a.core_y0 : (yhi < y ? yhi : y);
     a.m[c] = m, a.v[c] = v;
     a.xy[c] = make_double2(x, y);
+}
+
+// Partitioned mode: this rank's share of the fold (placer.cpp:318-325) — entries of other ranks' nets
+// hold 0 — into the all-reduce buffer.
+__global__ void __launch_bounds__(kBlock) k_fold(int C, const int* __restrict__ ent_start, const int* __restrict__ ent,
+                                                 const double2* __restrict__ grad_e, double2* __restrict__ out,
+                                                 const Ctrl* __restrict__ ctrl)
+{
+    const int c = blockIdx.x * kBlock + threadIdx.x;
+    if (c >= C || (ctrl && ctrl->stopped)) return;
+    double gx = 0.0, gy = 0.0;
+    for (int j = ent_start[c]; j < ent_start[c + 1]; ++j) {
+        const double2 g = grad_e[ent[j]];
+        gx += g.x, gy += g.y;
+    }
+    out[c] = make_double2(gx, gy);
 }
 
 // hpwl_total on caller-provided pin positions (wirelength.cpp:74-85), one thread per net.
@@ -894,12 +913,22 @@ void rebuild_pp_incidence(tdpg_session* s)
     CK_LAUNCH();
 }
 
+// The class's block range clipped to this rank's partition [part_b0, part_b1) (whole design at world 1).
+inline bool wa_range(const tdpg_session* s, int cls, int& b0, int& nb)
+{
+    const int lo = s->part_active ? s->part_b0 : 0, hi = s->part_active ? s->part_b1 : s->n_wa_blocks;
+    b0 = std::max(s->wa_cls_blk0[cls], lo);
+    nb = std::min(s->wa_cls_blk0[cls] + s->wa_cls_nblk[cls], hi) - b0;
+    return nb > 0;
+}
+
 template <int N>
 void launch_wa_class(tdpg_session* s, const double* nw, double inv_gamma, double* pw, double* ph, const PPArgs& pp,
                      double* ppart, const Ctrl* ctrl, cudaStream_t st)
 {
-    if (!s->wa_cls_nblk[N]) return;
-    k_wa_class<N><<<s->wa_cls_nblk[N], kBlock, 0, st>>>(s->wa_cls_blk0[N], s->wa_blk, s->net_by_size, s->e_cell,
+    int b0, nb;
+    if (!wa_range(s, N, b0, nb)) return;
+    k_wa_class<N><<<nb, kBlock, 0, st>>>(b0, s->wa_blk, s->net_by_size, s->e_cell,
                                                            s->e_off, s->cell_xy, s->anchor, nw, inv_gamma, s->grad_e,
                                                            pw, ph, pp, ppart, ctrl);
     CK_LAUNCH();
@@ -925,8 +954,9 @@ void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double*
     launch_wa_class<6>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(5));
     launch_wa_class<7>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(6));
     launch_wa_class<8>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(7));
-    if (s->wa_cls_nblk[0]) {
-        k_wa_generic<<<s->wa_cls_nblk[0], kBlock, 0, st(0)>>>(s->wa_cls_blk0[0], s->wa_blk, s->net_by_size,
+    int g0, gn;
+    if (wa_range(s, 0, g0, gn)) {
+        k_wa_generic<<<gn, kBlock, 0, st(0)>>>(g0, s->wa_blk, s->net_by_size,
                                                               s->wa_gen_start, s->net_start, s->e_cell, s->e_off,
                                                               s->cell_xy, s->anchor, nw, ig, s->grad_e, part_wl,
                                                               part_hp, pp, s->wa_gen_ord, ppart, ctrl);
@@ -1027,6 +1057,7 @@ CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, dou
     a.wh = s->cell_wh;
     a.dgrad = s->dgrad;
     a.d_cell = d_cell;
+    a.folded = nullptr;
     a.m = m, a.v = v;
     a.b1 = b1, a.b2 = b2, a.eps = eps;
     a.core_x0 = s->core[0], a.core_y0 = s->core[1], a.core_x1 = s->core[2], a.core_y1 = s->core[3];
@@ -1301,9 +1332,16 @@ void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cu
     CK_LAUNCH();
 }
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
-                  const IterCur* cur, Ctrl* ctrl, bool dens_grad)
+                  const IterCur* cur, Ctrl* ctrl, bool dens_grad, const double2* folded)
 {
-    const CellArgs ca = cell_args(s, d_cell, m, v, b1, b2, eps);
+    CellArgs ca = cell_args(s, d_cell, m, v, b1, b2, eps);
+    ca.folded = folded;
     launch_cell_pass(s, ca, cur, ctrl, dens_grad);
+}
+
+void launch_fold(tdpg_session* s, double2* out, const Ctrl* ctrl)
+{
+    k_fold<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(s->C, s->cell_ent_start, s->cell_ent, s->grad_e, out, ctrl);
+    CK_LAUNCH();
 }
 } // namespace tdpg

@@ -246,7 +246,8 @@ void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl);
 void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl);
 void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur);
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
-                  const IterCur* cur, Ctrl* ctrl, bool dens_grad = true);
+                  const IterCur* cur, Ctrl* ctrl, bool dens_grad = true, const double2* folded = nullptr);
+void launch_fold(tdpg_session* s, double2* out, const Ctrl* ctrl);
 void run_sta_async(tdpg_session* s, double* out3);
 void ledger_apply_sorted(tdpg_session* s, long long H, double wns, double w0, double w1);
 int api_fail(int kind, const std::string& msg);

@@ -46,6 +46,12 @@ struct Engine {
     // branch streams + fork/join events of the captured iteration graph (density chain and the WA
     // size classes run as parallel graph branches)
     static constexpr int kBranches = 8;
+    // partitioned mode: all-reduce buffer [partial d_cell (2C) | WA, HPWL, PP block partials (3 nb_wa)];
+    // with a communicator the all-reduce sits inside gexec, otherwise (tests: reduction done by the
+    // caller) the iteration is two graphs around it
+    bool partitioned = false;
+    DBuf<double> red;
+    cudaGraphExec_t gexec_a = nullptr, gexec_b = nullptr;
     cudaStream_t br[kBranches] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[kBranches] = {};
     ~Engine()
@@ -56,6 +62,8 @@ struct Engine {
             if (e) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (gexec_a) cudaGraphExecDestroy(gexec_a);
+        if (gexec_b) cudaGraphExecDestroy(gexec_b);
         if (graph) cudaGraphDestroy(graph);
         if (refresh_gexec) cudaGraphExecDestroy(refresh_gexec);
         if (sort_gexec) cudaGraphExecDestroy(sort_gexec);
@@ -179,6 +187,62 @@ void capture_iteration(tdpg_session* s, Engine& E)
             CK(cudaEventCreateWithFlags(&E.ev_join[k], cudaEventDisableTiming));
         }
     }
+    if (E.partitioned) {
+        const long long C2 = 2LL * s->C;
+        double* r_wl = E.red.p + C2;
+        double* r_hp = r_wl + E.nb_wa;
+        double* r_pp = r_hp + E.nb_wa;
+        FinArgs fp = fa;
+        fp.part_wl = r_wl, fp.part_hp = r_hp, fp.part_pp = r_pp;
+        double2* folded = reinterpret_cast<double2*>(E.red.p);
+        // A: fork the (replicated) density chain, WA over this rank's nets, join, fold this rank's entries
+        auto record_a = [&] {
+            cudaStream_t main = s->st;
+            CK(cudaEventRecord(E.ev_fork, main));
+            for (int k = 0; k < Engine::kBranches; ++k) CK(cudaStreamWaitEvent(E.br[k], E.ev_fork, 0));
+            s->st = E.br[0];
+            launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
+            launch_dens_grad(s, E.ctrl, E.br[0]);
+            s->st = main;
+            cudaStream_t wa_st[Engine::kBranches] = {main};
+            for (int k = 1; k < Engine::kBranches; ++k) wa_st[k] = E.br[k];
+            launch_wirelength_pp(s, E.gamma, E.cfg.net_weighting != 0, r_wl, r_hp, true, E.cfg.pp_loss, E.cfg.beta,
+                                 r_pp, E.ctrl, wa_st, Engine::kBranches);
+            for (int k = 1; k < Engine::kBranches; ++k) {
+                CK(cudaEventRecord(E.ev_join[k], E.br[k]));
+                CK(cudaStreamWaitEvent(main, E.ev_join[k], 0));
+            }
+            launch_fold(s, folded, E.ctrl);
+        };
+        auto join_density = [&] {
+            CK(cudaEventRecord(E.ev_join[0], E.br[0]));
+            CK(cudaStreamWaitEvent(s->st, E.ev_join[0], 0));
+        };
+        // B: terms from the reduced partials, cells from the reduced fold + replicated density gradient
+        auto record_b = [&] {
+            launch_finalize(s, fp, E.ctrl, E.cur);
+            launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
+                         false, folded);
+        };
+        const size_t n_red = static_cast<size_t>(C2) + 3 * static_cast<size_t>(E.nb_wa);
+        s->part_active = true;
+        if (s->comm) {
+            E.gexec = capture(s, [&] {
+                record_a();
+                comm_allreduce(s, E.red.p, n_red); // overlaps the density branch
+                join_density();
+                record_b();
+            });
+        } else {
+            E.gexec_a = capture(s, [&] {
+                record_a();
+                join_density();
+            });
+            E.gexec_b = capture(s, record_b);
+        }
+        s->part_active = false;
+        return;
+    }
     E.gexec = capture(s, [&] {
         // fork: density chain (scatter -> bins -> density gradient) on branch 0, the WA size classes
         // (+ fused pin pairs, dense ledger) on the main stream and branches 1..7; join -> finalize -> cells
@@ -274,6 +338,12 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->nb_wa = wa_blocks(s), E->nb_pp = wa_blocks(s), E->nb_d = bins_blocks(s); // PP partials per WA block
     E->part.alloc(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
+    E->partitioned = s->part_world > 1;
+    if (E->partitioned) { // entries of other ranks' nets must read as 0 in this rank's fold
+        E->red.alloc(2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E->nb_wa) + 8);
+        E->red.zero(s->st);
+        s->grad_e.zero(s->st);
+    }
     if (const char* se = std::getenv("TDPG_SORT_EVERY")) E->sort_every = std::max(1, std::atoi(se));
     // every buffer the graphs touch is sized before capture, so their pointers never move
     refresh_reserve(s);
@@ -444,11 +514,41 @@ int engine_run(tdpg_session* s, int n)
             CK(cudaGraphLaunch(E.sort_gexec, s->st)); // refresh the scatter's spatial cell order
             E.kernel_launches += 1;
         }
+        if (!E.gexec) throw Error(TDPG_ERR_INTERNAL, "partitioned engine without a communicator: use "
+                                                      "tdpg_comm_init or the split-phase API");
         CK(cudaGraphLaunch(E.gexec, s->st));
-        E.kernel_launches += E.kernels_per_iter;
+        E.kernel_launches += E.kernels_per_iter + (E.partitioned ? 1 : 0);
         ++E.launched;
     }
     return done;
+}
+
+// Split-phase iteration for a partitioned engine without a communicator (the caller reduces):
+// phase A runs the scheduled refresh / re-sort and the pre-reduction graph and returns this rank's
+// all-reduce buffer; phase B takes the reduced buffer and finishes the iteration.
+size_t part_phase_a(tdpg_session* s, double* red_host)
+{
+    Engine& E = *s->eng;
+    if (!E.partitioned || !E.gexec_a) throw Error(TDPG_ERR_INTERNAL, "engine is not in split-phase partitioned mode");
+    const int it = E.launched;
+    if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0) timing_refresh(s);
+    if (it % E.sort_every == 0) CK(cudaGraphLaunch(E.sort_gexec, s->st));
+    CK(cudaGraphLaunch(E.gexec_a, s->st));
+    const size_t n = 2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E.nb_wa);
+    if (red_host) E.red.download(red_host, n, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    return n;
+}
+
+void part_phase_b(tdpg_session* s, const double* red_host)
+{
+    Engine& E = *s->eng;
+    if (!E.partitioned || !E.gexec_b) throw Error(TDPG_ERR_INTERNAL, "engine is not in split-phase partitioned mode");
+    const size_t n = 2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E.nb_wa);
+    CK(cudaMemcpyAsync(E.red.p, red_host, n * sizeof(double), cudaMemcpyHostToDevice, s->st));
+    CK(cudaGraphLaunch(E.gexec_b, s->st));
+    ++E.launched;
+    CK(cudaStreamSynchronize(s->st));
 }
 
 } // namespace tdpg
@@ -456,6 +556,7 @@ int engine_run(tdpg_session* s, int n)
 tdpg_session::~tdpg_session()
 {
     delete eng; // Engine is complete here
+    tdpg::comm_destroy(this);
     if (sta_gexec) cudaGraphExecDestroy(sta_gexec);
     if (st) {
         cudaStreamSynchronize(st);
@@ -595,6 +696,23 @@ int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_tr
         row->tns = r.tns, row->wns = r.wns, row->wl_term = r.wl_term, row->density_term = r.density_term;
         row->pp_term = r.pp_term, row->lambda = r.lambda, row->beta_pp = r.beta_pp;
     }
+    API_END
+}
+
+int tdpg_part_step_a(tdpg_session* s, double* red, int64_t* n_red)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
+    const size_t n = part_phase_a(s, red);
+    if (n_red) *n_red = static_cast<int64_t>(n);
+    API_END
+}
+
+int tdpg_part_step_b(tdpg_session* s, const double* red)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
+    part_phase_b(s, red);
     API_END
 }
 

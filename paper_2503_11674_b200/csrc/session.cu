@@ -257,10 +257,12 @@ void build_graph(tdpg_session* s)
     s->out_start.upload(out_s, s->st);
     s->out_to.upload(out_to, s->st);
     s->lvl_pins.upload(s->h_lvl_pins, s->st);
+    s->lvl_start.upload(s->h_lvl_start, s->st);
     s->d_level.upload(s->h_level, s->st);
     std::vector<int> eps(s->h_endpoints);
     std::sort(eps.begin(), eps.end());
     s->ep_sorted.upload(eps, s->st);
+    sta_setup(s);
 }
 
 void check_netlist(const tdpg_netlist* d)
@@ -400,6 +402,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         pos += k;
     }
     s->n_wa_blocks = static_cast<int>(blk.size());
+    s->part_b0 = 0, s->part_b1 = s->n_wa_blocks; // whole design until tdpg_set_partition / tdpg_comm_init
     s->E_lay = pos;
     {   // fused pin-pair tables (engine mode): per class-ordered net the sink slots in ascending pin
         // id (3 bits each), per generic net the same as a list; per sink pin its (net index, slot)

@@ -7,6 +7,7 @@
 #include <array>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "gp_kernels.cuh"
@@ -45,11 +46,8 @@ struct StaArgs {
 
 // propagate_arrival for one level (sta.cpp:41-62): max over known fan-in, strict '>' in
 // ascending arc id; records the winning fan-in pin and whether another arc tied it exactly.
-__global__ void __launch_bounds__(kBlock) k_arrival(int lo, int hi, StaArgs a)
+__device__ __forceinline__ void arrival_pin(int v, const StaArgs& a)
 {
-    const int i = lo + blockIdx.x * kBlock + threadIdx.x;
-    if (i >= hi) return;
-    const int v = a.lvl_pins[i];
     if (a.is_source[v]) {
         a.arr[v] = 0.0, a.ak[v] = 1, a.pred[v] = -1, a.tie[v] = 0;
         return;
@@ -82,12 +80,15 @@ __global__ void __launch_bounds__(kBlock) k_arrival(int lo, int hi, StaArgs a)
     if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = v;
 }
 
-// propagate_required for one level (sta.cpp:77-97): min over known fan-out, strict '<'.
-__global__ void __launch_bounds__(kBlock) k_required(int lo, int hi, StaArgs a)
+__global__ void __launch_bounds__(kBlock) k_arrival(int lo, int hi, StaArgs a)
 {
     const int i = lo + blockIdx.x * kBlock + threadIdx.x;
-    if (i >= hi) return;
-    const int u = a.lvl_pins[i];
+    if (i < hi) arrival_pin(a.lvl_pins[i], a);
+}
+
+// propagate_required for one level (sta.cpp:77-97): min over known fan-out, strict '<'.
+__device__ __forceinline__ void required_pin(int u, const StaArgs& a)
+{
     double best = INFINITY;
     bool found = false;
     if (a.is_endpoint[u]) best = a.clock, found = true;
@@ -106,6 +107,59 @@ __global__ void __launch_bounds__(kBlock) k_required(int lo, int hi, StaArgs a)
     }
     a.req[u] = found ? best : a.clock;
     a.rk[u] = found ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kBlock) k_required(int lo, int hi, StaArgs a)
+{
+    const int i = lo + blockIdx.x * kBlock + threadIdx.x;
+    if (i < hi) required_pin(a.lvl_pins[i], a);
+}
+
+// Grid-wide barrier for the persistent STA (all blocks co-resident: cooperative launch).  Arrival
+// counter + generation word; the last block to arrive resets the counter and bumps the generation.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// The whole level sweep in one launch: pin positions, arrival levels ascending, required levels
+// descending (sta.cpp:33-102), a grid barrier between dependent levels instead of a kernel boundary.
+__global__ void __launch_bounds__(kBlock) k_sta_persist(StaArgs a, const int* __restrict__ lvl_start, int L, int P,
+                                                        bool pin_xy_from_cells, const double2* __restrict__ off,
+                                                        const double2* __restrict__ cell_xy,
+                                                        const double2* __restrict__ anchor, unsigned* bar)
+{
+    const unsigned nb = gridDim.x;
+    const int tid = blockIdx.x * kBlock + threadIdx.x, nt = gridDim.x * kBlock;
+    if (pin_xy_from_cells) {
+        for (int p = tid; p < P; p += nt)
+            const_cast<double2*>(a.pin_xy)[p] = pin_pos(p, a.pin_cell, off, cell_xy, anchor);
+        grid_barrier(bar, nb);
+    }
+    for (int l = 0; l < L; ++l) {
+        const int lo = lvl_start[l], hi = lvl_start[l + 1];
+        for (int i = lo + tid; i < hi; i += nt) arrival_pin(a.lvl_pins[i], a);
+        grid_barrier(bar, nb);
+    }
+    for (int l = L - 1; l >= 0; --l) {
+        const int lo = lvl_start[l], hi = lvl_start[l + 1];
+        for (int i = lo + tid; i < hi; i += nt) required_pin(a.lvl_pins[i], a);
+        if (l > 0) grid_barrier(bar, nb);
+    }
 }
 
 // compute_slacks + endpoint keys (sta.cpp:104-133, paths.cpp:77-87): orderable slack keys
@@ -350,13 +404,26 @@ StaArgs sta_args(tdpg_session* s)
 void sta_record(tdpg_session* s, double* out3)
 {
     const int P = s->P;
-    if (!s->pin_xy_external) { // pin positions from the cells (netlist.cpp:23-32) unless the caller gave them
+    const bool persist = s->sta_grid > 0;
+    if (!s->pin_xy_external && !persist) { // pin positions from the cells (netlist.cpp:23-32) unless given
         k_pin_xy<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor,
                                                               s->pin_xy);
         CK_LAUNCH();
     }
     CK(cudaMemsetAsync(s->counters.p, 0, sizeof(int) * 4, s->st));
     const StaArgs a = sta_args(s);
+    if (persist) { // one cooperative launch for the whole sweep, pin positions included
+        CK(cudaMemsetAsync(s->grid_bar.p, 0, 2 * sizeof(unsigned), s->st));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(s->sta_grid), cfg.blockDim = dim3(kBlock), cfg.stream = s->st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative, attr[0].val.cooperative = 1;
+        cfg.attrs = attr, cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, k_sta_persist, a, static_cast<const int*>(s->lvl_start.p), s->L, P,
+                              !s->pin_xy_external,
+                              static_cast<const double2*>(s->pin_off.p), static_cast<const double2*>(s->cell_xy.p),
+                              static_cast<const double2*>(s->anchor.p), s->grid_bar.p));
+    } else {
     for (int l = 0; l < s->L; ++l) {
         const int lo = s->h_lvl_start[l], hi = s->h_lvl_start[l + 1];
         if (hi > lo) k_arrival<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, a);
@@ -367,12 +434,30 @@ void sta_record(tdpg_session* s, double* out3)
         if (hi > lo) k_required<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, a);
     }
     CK_LAUNCH();
+    }
     const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
     k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0, s->sort_v0,
                                            s->sta_part);
     CK_LAUNCH();
     k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->sta_part, out3);
     CK_LAUNCH();
+}
+
+// Size the persistent STA for co-residency (every block resident at once, cooperative launch);
+// TDPG_STA_PERSIST=0 falls back to one launch per level.
+void sta_setup(tdpg_session* s)
+{
+    s->sta_grid = 0;
+    const char* e = std::getenv("TDPG_STA_PERSIST");
+    if (e && std::atoi(e) == 0) return;
+    int coop = 0, sms = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, s->device));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sta_persist, kBlock, 0));
+    if (!coop || per_sm < 1) return;
+    s->grid_bar.alloc(2);
+    const char* b = std::getenv("TDPG_STA_BLOCKS_PER_SM");
+    s->sta_grid = sms * std::max(1, std::min(per_sm, b ? std::atoi(b) : 2));
 }
 
 void run_sta_async(tdpg_session* s, double* out3)

@@ -100,6 +100,12 @@ _SIGS = {
     "tdpg_sta_fetch": (C.c_int, [_P, _P, _P, _P, _P, _P, _F64P, _F64P]),
     "tdpg_path_to": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int32, _I32P, _F64P]),
     "tdpg_extract": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P]),
+    "tdpg_partition_plan": (C.c_int, [C.c_int32, _P, C.c_int32, _P, _P]),
+    "tdpg_set_partition": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "tdpg_comm_unique_id": (C.c_int, [_P]),
+    "tdpg_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, _P]),
+    "tdpg_part_step_a": (C.c_int, [_P, _P, _I64P]),
+    "tdpg_part_step_b": (C.c_int, [_P, _P]),
     "tdpg_paths_candidates": (C.c_int, [_P, _I64P]),
     "tdpg_k_worst": (C.c_int, [_P, C.c_int32, C.c_int32, _I32P, _P, _P, C.c_int32, _P]),
     "tdpg_set_round_callback": (C.c_int, [_P, _P, _P]),
@@ -289,6 +295,23 @@ class Session:
                                      slack.ctypes.data))
         return [pins[start[i]:start[i + 1]].tolist() for i in range(n.value)], slack[:n.value]
 
+    # partitioned multi-GPU mode -------------------------------
+    def set_partition(self, rank, world):
+        _check(self.lib.tdpg_set_partition(self.h, rank, world))
+
+    def comm_init(self, rank, world, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(self.lib.tdpg_comm_init(self.h, rank, world, buf))
+
+    def part_step_a_into(self, out: np.ndarray):
+        n = C.c_int64()
+        _check(self.lib.tdpg_part_step_a(self.h, out.ctypes.data, C.byref(n)))
+        return n.value
+
+    def part_step_b(self, red: np.ndarray):
+        red = np.ascontiguousarray(red, np.float64)
+        _check(self.lib.tdpg_part_step_b(self.h, red.ctypes.data))
+
     def path_to(self, pin, rank=0):
         """PathEnumerator::path_to(pin, rank): (pins, delay) or None once exhausted."""
         buf = np.zeros(self.d.n_pins + 1, np.int32)
@@ -397,6 +420,27 @@ class Session:
         _check(lib().tdpg_adam_step(x.size, x.ctypes.data, g.ctypes.data, m.ctypes.data, v.ctypes.data, C.byref(tt),
                                     lr, b1, b2, eps))
         return tt.value
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 creates it, every rank passes it to Session.comm_init)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().tdpg_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def partition_plan(net_start, world):
+    """Per-rank WA block ranges [bounds[r], bounds[r+1]) and their net-pin entry counts (host only)."""
+    ns = np.ascontiguousarray(net_start, np.int32)
+    bounds = np.zeros(world + 1, np.int32)
+    ent = np.zeros(world, np.int64)
+    _check(lib().tdpg_partition_plan(ns.size - 1, ns.ctypes.data, world, bounds.ctypes.data, ent.ctypes.data))
+    return bounds, ent
+
+
+def red_size(session) -> int:
+    """Length of the partitioned engine's all-reduce buffer (2C + 3 WA blocks)."""
+    return 2 * session.d.n_cells + 3 * int(partition_plan(session.d.net_start, 1)[0][1])
 
 
 def generate(seed=1, cells=100, registers=-1, fanout=2.0, fail_frac=0.2, r_unit=1e-4, c_unit=1e-4,
