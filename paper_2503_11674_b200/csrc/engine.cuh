@@ -106,6 +106,10 @@ struct tdpg_session {
 
     // device timing graph
     tdpg::DBuf<int> lvl_pins, lvl_start, in_start, in_from, out_start, out_to, ep_sorted;
+    // STA sweep over driver levels only: Output pins grouped by level, all Input pins (timing.cu)
+    tdpg::DBuf<int> sta_out_pins, sta_in_pins;           // Output pins / Input pins, each grouped by level
+    std::vector<int> h_sta_out_start, h_sta_in_start;    // [L + 1]
+    tdpg::DBuf<unsigned long long> sta_akey, sta_rkey;   // push sweep: Output pins' arrival / required keys
     tdpg::DBuf<unsigned> grid_bar;   // persistent STA: grid barrier (arrival count, generation)
     int sta_grid = 0;                // co-resident blocks of the persistent STA kernel (0: per-level launches)
 

@@ -5,6 +5,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 #include "gp_kernels.cuh"
 
@@ -133,10 +134,13 @@ __device__ __forceinline__ void wa_net_slots(int base, double w, const int* __re
 }
 
 constexpr int kWaMaxN = 8;
+#ifndef WA_MINB
+#define WA_MINB 1
+#endif
 
 // One launch per pin count N: thread t of block b owns the t-th net of the block.
 template <int N>
-__global__ void __launch_bounds__(kBlock) k_wa_class(int blk0, const int4* __restrict__ blk,
+__global__ void __launch_bounds__(kBlock, WA_MINB) k_wa_class(int blk0, const int4* __restrict__ blk,
                                                      const int* __restrict__ net_by_size,
                                                      const int* __restrict__ e_cell, const double2* __restrict__ e_off,
                                                      const double2* __restrict__ cell_xy,
@@ -161,6 +165,91 @@ __global__ void __launch_bounds__(kBlock) k_wa_class(int blk0, const int4* __res
     const double bw = block_sum<kBlock>(wl, sh);
     const double bh = block_sum<kBlock>(hp, sh);
     const double bp = part_pp ? block_sum<kBlock>(ppv, sh) : 0.0;
+    if (threadIdx.x == 0) {
+        part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
+        if (part_pp) part_pp[blk0 + blockIdx.x] = bp;
+    }
+}
+
+// Axis-split variant: two threads per net (lane pairs), one per axis, so a thread keeps only its axis's
+// N coordinates and exponentials in registers (half the register footprint of wa_net_slots, twice the
+// resident warps for latency hiding).  Each thread loads only its coordinate component (the pair's
+// two 8-byte loads share a sector).  Everything that couples the axes — the net value w·(vx + vy), the
+// HPWL, the pin-pair value w·(dx² + dy²) and the linear-loss distance — is formed after exchanging the
+// partner's term with one shuffle, in the reference's operand order, so results are bitwise those of the
+// one-thread form.
+template <int N>
+__global__ void __launch_bounds__(2 * kBlock, (N <= 5 ? 2 : 1)) k_wa_axis(int blk0, const int4* __restrict__ blk,
+                                                        const int* __restrict__ net_by_size,
+                                                        const int* __restrict__ e_cell, const double* __restrict__ e_off,
+                                                        const double* __restrict__ cell_xy,
+                                                        const double* __restrict__ anchor,
+                                                        const double* __restrict__ net_w, double inv_gamma,
+                                                        double* __restrict__ grad_e, double* __restrict__ part_wl,
+                                                        double* __restrict__ part_hp, PPArgs pp,
+                                                        double* __restrict__ part_pp, const Ctrl* __restrict__ ctrl)
+{
+    __shared__ double sh[2 * kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    const int4 b = blk[blk0 + blockIdx.x]; // (N, first in net_by_size, count, entry base)
+    const int t = threadIdx.x >> 1, axis = threadIdx.x & 1;
+    const bool on = t < b.z;
+    const int base = b.w + (on ? t : 0);
+    double x[N], g[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) { // entry_pos (netlist.cpp:28-29), this axis only
+        const int e = base + i * kBlock;
+        const int ec = __ldcs(e_cell + e);
+        const double a = ec >= 0 ? cell_xy[2 * ec + axis] : anchor[2 * (-1 - ec) + axis];
+        x[i] = a + __ldcs(e_off + 2 * e + axis);
+    }
+    double v, ext;
+    wa_axis<N>(x, inv_gamma, g, v, ext);
+    const double v_other = __shfl_xor_sync(0xffffffffu, v, 1), e_other = __shfl_xor_sync(0xffffffffu, ext, 1);
+    const int i_net = b.y + (on ? t : 0);
+    const double w = net_w ? net_w[net_by_size[i_net]] : 1.0;
+    double wl = 0.0, hp = 0.0, ppv = 0.0;
+    if (on && axis == 0) wl = w * (v + v_other), hp = ext + e_other;
+    const uint32_t mask = (on && pp.mask) ? pp.mask[i_net] : 0u;
+    double p[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i] = 0.0;
+    if (pp.mask) { // pin pairs of this net (pin_pairs.cpp:17-49), see pp_net
+        const uint32_t ord = mask ? pp.ord[i_net] : 0u;
+#pragma unroll
+        for (int j = 1; j < N; ++j) {
+            const double d = x[j] - x[0];
+            const double d_other = __shfl_xor_sync(0xffffffffu, d, 1);
+            if (!(mask >> j & 1u)) continue;
+            const double wt = pp.w_e[base + j * kBlock];
+            const double dx = axis ? d_other : d, dy = axis ? d : d_other;
+            if (pp.kind == 0) {
+                if (axis == 0) ppv += wt * (dx * dx + dy * dy);
+                p[j] = 2.0 * wt * d;
+            } else {
+                const double dist = sqrt(dx * dx + dy * dy);
+                if (axis == 0) ppv += wt * dist;
+                if (dist > 0.0) p[j] = wt * d / dist;
+            }
+        }
+        double sd = 0.0; // driver: terms in ascending sink pin id
+#pragma unroll
+        for (int k = 0; k < N - 1; ++k) {
+            const int j = (ord >> (3 * k)) & 7;
+#pragma unroll
+            for (int q = 1; q < N; ++q)
+                if (q == j && (mask >> q & 1u)) sd -= p[q];
+        }
+        p[0] = sd;
+    }
+    if (on) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) // fold term pin_grad + beta * pp.d_pin (placer.cpp:323)
+            grad_e[2 * (base + i * kBlock) + axis] = mask ? w * g[i] + pp.beta * p[i] : w * g[i];
+    }
+    const double bw = block_sum<2 * kBlock>(wl, sh);
+    const double bh = block_sum<2 * kBlock>(hp, sh);
+    const double bp = part_pp ? block_sum<2 * kBlock>(ppv, sh) : 0.0;
     if (threadIdx.x == 0) {
         part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
         if (part_pp) part_pp[blk0 + blockIdx.x] = bp;
@@ -537,40 +626,61 @@ __global__ void k_spatial_keys(int C, const double2* __restrict__ cell_xy, const
     vals[c] = c;
 }
 
-// Two bins per thread (16-byte loads/stores); one pass: read the accumulator, reset it, write excess.
+// Grid-stride over bin pairs (16-byte loads/stores), four pairs per thread per step with every load issued
+// before use; one pass: read the accumulator, reset it, write excess.  Per block one (value, overflow)
+// partial in fixed order.
+constexpr int kBinsBlocks = 148 * 4;
+
 __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g, long long* __restrict__ acc,
                                                          const double* __restrict__ base,
                                                          double* __restrict__ excess, double* __restrict__ part_d,
                                                          const Ctrl* __restrict__ ctrl)
 {
-    __shared__ double sh[kBlock / 32];
+    __shared__ double sh[2][kBlock / 32];
     if (ctrl && ctrl->stopped) return;
     double v2 = 0.0, v1 = 0.0;
-    const long long b = 2 * (blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x);
-    auto one = [&](long long q, long long k, double& ex) {
+    auto one = [&](long long q, long long k) {
         const double mov = static_cast<double>(q) * g.inv_scale;
         const double occ = base ? base[k] + mov : mov;
-        ex = smax(0.0, occ - g.cap);
+        const double ex = smax(0.0, occ - g.cap);
         v2 += ex * ex;
         v1 += ex;
+        return ex;
     };
-    if (b + 1 < B) {
-        const longlong2 q = *reinterpret_cast<const longlong2*>(acc + b);
-        *reinterpret_cast<longlong2*>(acc + b) = make_longlong2(0, 0);
-        double2 ex;
-        one(q.x, b, ex.x);
-        one(q.y, b + 1, ex.y);
-        *reinterpret_cast<double2*>(excess + b) = ex;
-    } else if (b < B) {
-        const long long q = acc[b];
-        acc[b] = 0;
-        double ex;
-        one(q, b, ex);
-        excess[b] = ex;
+    const long long pairs = B / 2, stride = static_cast<long long>(gridDim.x) * kBlock;
+    constexpr int U = 4;
+    for (long long p0 = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; p0 < pairs; p0 += U * stride) {
+        longlong2 q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = p0 + u * stride;
+            q[u] = p < pairs ? reinterpret_cast<const longlong2*>(acc)[p] : make_longlong2(0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = p0 + u * stride;
+            if (p >= pairs) break;
+            reinterpret_cast<longlong2*>(acc)[p] = make_longlong2(0, 0);
+            double2 ex;
+            ex.x = one(q[u].x, 2 * p);
+            ex.y = one(q[u].y, 2 * p + 1);
+            reinterpret_cast<double2*>(excess)[p] = ex;
+        }
     }
-    const double s2 = block_sum<kBlock>(v2, sh);
-    const double s1 = block_sum<kBlock>(v1, sh);
-    if (threadIdx.x == 0) part_d[2 * blockIdx.x] = s2, part_d[2 * blockIdx.x + 1] = s1;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (B & 1)) { // odd bin count: the last bin
+        const long long q = acc[B - 1];
+        acc[B - 1] = 0;
+        excess[B - 1] = one(q, B - 1);
+    }
+    v2 = warp_sum(v2), v1 = warp_sum(v1);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sh[0][w] = v2, sh[1][w] = v1;
+    __syncthreads();
+    if (w == 0) {
+        double a = lane < kBlock / 32 ? sh[0][lane] : 0.0, b = lane < kBlock / 32 ? sh[1][lane] : 0.0;
+        a = warp_sum(a), b = warp_sum(b);
+        if (lane == 0) part_d[2 * blockIdx.x] = a, part_d[2 * blockIdx.x + 1] = b;
+    }
 }
 
 // =====================================================================================
@@ -591,15 +701,40 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(FinArgs a, Ctrl* ctrl, I
         if (threadIdx.x == 0) cur->do_adam = 0;
         return;
     }
-    double wl = 0, hp = 0, pp = 0, d2 = 0, d1 = 0;
-    for (int i = threadIdx.x; i < a.nb_wa; i += kFinBlock) wl += a.part_wl[i], hp += a.part_hp[i];
-    for (int i = threadIdx.x; i < a.nb_pp; i += kFinBlock) pp += a.part_pp[i];
-    for (int i = threadIdx.x; i < a.nb_d; i += kFinBlock) d2 += a.part_d[2 * i], d1 += a.part_d[2 * i + 1];
-    wl = block_sum<kFinBlock>(wl, sh);
-    hp = block_sum<kFinBlock>(hp, sh);
-    pp = block_sum<kFinBlock>(pp, sh);
-    d2 = block_sum<kFinBlock>(d2, sh);
-    d1 = block_sum<kFinBlock>(d1, sh);
+    double r[5] = {0, 0, 0, 0, 0}; // wl, hpwl, pp, density value, overflow numerator
+    // loads batched 8 deep (all issued before the adds) so the single block is not latency-serialised
+    auto acc = [&](const double* p, int n, int stride, int off, double& out) {
+        for (int i0 = threadIdx.x; i0 < n; i0 += 8 * kFinBlock) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * kFinBlock;
+                v[u] = i < n ? p[static_cast<long long>(i) * stride + off] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) out += v[u];
+        }
+    };
+    acc(a.part_wl, a.nb_wa, 1, 0, r[0]);
+    acc(a.part_hp, a.nb_wa, 1, 0, r[1]);
+    acc(a.part_pp, a.nb_pp, 1, 0, r[2]);
+    acc(a.part_d, a.nb_d, 2, 0, r[3]);
+    acc(a.part_d, a.nb_d, 2, 1, r[4]);
+    {   // one fixed-order tree for all five sums
+        __shared__ double sh5[5][kFinBlock / 32];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) r[k] = warp_sum(r[k]);
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 5; ++k) sh5[k][w] = r[k];
+        __syncthreads();
+        if (w != 0) return;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) r[k] = warp_sum(lane < kFinBlock / 32 ? sh5[k][lane] : 0.0);
+    }
+    (void)sh;
+    double wl = r[0], hp = r[1], pp = r[2], d2 = r[3], d1 = r[4];
     if (threadIdx.x != 0) return;
     const int it = ctrl ? ctrl->iter : 0;
     const double lambda = a.sched ? a.sched[it].lambda : a.lambda_single;
@@ -836,7 +971,7 @@ int wa_blocks(const tdpg_session* s) { return std::max(1, s->n_wa_blocks); }
 int pp_blocks(const tdpg_session*) { return 148 * 4; }
 int bins_blocks(const tdpg_session* s)
 {
-    return std::max(1, static_cast<int>(blocks_for((s->grid.bins() + 1) / 2, kBlock)));
+    return std::max(1, std::min(kBinsBlocks, static_cast<int>(blocks_for((s->grid.bins() + 1) / 2, kBlock))));
 }
 
 // Per-pin incidence CSR of the ledger (rebuilt when the ledger changes).
@@ -913,6 +1048,16 @@ void rebuild_pp_incidence(tdpg_session* s)
     CK_LAUNCH();
 }
 
+// TDPG_WA_AXIS=0 selects the one-thread-per-net class kernels (A/B switch).
+inline bool wa_axis_split()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_WA_AXIS");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 // The class's block range clipped to this rank's partition [part_b0, part_b1) (whole design at world 1).
 inline bool wa_range(const tdpg_session* s, int cls, int& b0, int& nb)
 {
@@ -928,6 +1073,15 @@ void launch_wa_class(tdpg_session* s, const double* nw, double inv_gamma, double
 {
     int b0, nb;
     if (!wa_range(s, N, b0, nb)) return;
+    if (wa_axis_split()) {
+        k_wa_axis<N><<<nb, 2 * kBlock, 0, st>>>(b0, s->wa_blk, s->net_by_size, s->e_cell,
+                                                reinterpret_cast<const double*>(s->e_off.p),
+                                                reinterpret_cast<const double*>(s->cell_xy.p),
+                                                reinterpret_cast<const double*>(s->anchor.p), nw, inv_gamma,
+                                                reinterpret_cast<double*>(s->grad_e.p), pw, ph, pp, ppart, ctrl);
+        CK_LAUNCH();
+        return;
+    }
     k_wa_class<N><<<nb, kBlock, 0, st>>>(b0, s->wa_blk, s->net_by_size, s->e_cell,
                                                            s->e_off, s->cell_xy, s->anchor, nw, inv_gamma, s->grad_e,
                                                            pw, ph, pp, ppart, ctrl);

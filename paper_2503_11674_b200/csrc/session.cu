@@ -258,6 +258,23 @@ void build_graph(tdpg_session* s)
     s->out_to.upload(out_to, s->st);
     s->lvl_pins.upload(s->h_lvl_pins, s->st);
     s->lvl_start.upload(s->h_lvl_start, s->st);
+    {   // push-sweep tables (timing.cu): Output pins and Input pins, each grouped by level (ascending id)
+        std::vector<int> outs, ins;
+        s->h_sta_out_start.assign(s->L + 1, 0), s->h_sta_in_start.assign(s->L + 1, 0);
+        for (int l = 0; l < s->L; ++l) {
+            for (int i = s->h_lvl_start[l]; i < s->h_lvl_start[l + 1]; ++i) {
+                const int p = s->h_lvl_pins[i];
+                (s->h_pin_dir[p] == 1 ? outs : ins).push_back(p);
+            }
+            s->h_sta_out_start[l + 1] = static_cast<int>(outs.size());
+            s->h_sta_in_start[l + 1] = static_cast<int>(ins.size());
+        }
+        if (outs.empty()) outs.push_back(0);
+        if (ins.empty()) ins.push_back(0);
+        s->sta_out_pins.upload(outs, s->st);
+        s->sta_in_pins.upload(ins, s->st);
+        s->sta_akey.alloc(std::max(P, 1)), s->sta_rkey.alloc(std::max(P, 1));
+    }
     s->d_level.upload(s->h_level, s->st);
     std::vector<int> eps(s->h_endpoints);
     std::sort(eps.begin(), eps.end());

@@ -115,6 +115,152 @@ __global__ void __launch_bounds__(kBlock) k_required(int lo, int hi, StaArgs a)
     if (i < hi) required_pin(a.lvl_pins[i], a);
 }
 
+// Push sweep over sink levels.  Every arc into an Input pin is a net arc from an Output pin and every arc
+// into an Output pin is a cell arc from an Input pin (sta.cpp:16-21).  So only levels holding Input pins
+// need a dependent launch: an Input pin reads its driver's arrival and pushes arr + cell delay into its
+// cell's outputs with a 64-bit atomicMax on the order-preserving key of the double (exact: max/min need
+// no rounding); backwards, it takes its outputs' required times and pushes req - net delay into its
+// driver with atomicMin.  Each thread's work is one pin and its (small) cell fan-out, instead of an
+// Output pin looping over a whole net.  A final pass per direction decodes the Output pins' keys; the
+// arrival decode re-evaluates the fan-in to recover the first maximising arc (pred) and exact ties,
+// exactly like propagate_arrival's strict '>' in ascending arc id (sta.cpp:51-58).
+__device__ __forceinline__ double key_double(unsigned long long k)
+{ // inverse of double_key
+    const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+constexpr unsigned long long kNoArr = 0ull, kNoReq = ~0ull;
+
+__global__ void __launch_bounds__(kBlock) k_sta_init(int P, StaArgs a, bool pin_xy_from_cells,
+                                                     const double2* __restrict__ off,
+                                                     const double2* __restrict__ cell_xy,
+                                                     const double2* __restrict__ anchor,
+                                                     unsigned long long* __restrict__ akey,
+                                                     unsigned long long* __restrict__ rkey)
+{
+    const int p = blockIdx.x * kBlock + threadIdx.x;
+    if (p >= P) return;
+    if (pin_xy_from_cells) const_cast<double2*>(a.pin_xy)[p] = pin_pos(p, a.pin_cell, off, cell_xy, anchor);
+    akey[p] = a.is_source[p] ? double_key(0.0) : kNoArr;
+    rkey[p] = a.is_endpoint[p] ? double_key(a.clock) : kNoReq;
+}
+
+__global__ void __launch_bounds__(kBlock) k_arr_push(int lo, int hi, const int* __restrict__ pins, StaArgs a,
+                                                     unsigned long long* __restrict__ akey)
+{
+    const int i = lo + blockIdx.x * kBlock + threadIdx.x;
+    if (i >= hi) return;
+    const int t = pins[i];
+    double best = 0.0;
+    bool found = false;
+    int bu = -1, ntie = 0;
+    if (a.is_source[t]) {
+        found = true;
+    } else {
+        const int j0 = a.in_start[t], j1 = a.in_start[t + 1];
+        if (j1 > j0) {
+            const double2 pt = a.pin_xy[t];
+            const double cap = a.pin_cap[t];
+            for (int j = j0; j < j1; ++j) { // net arcs from drivers (final: lower levels)
+                const int u = a.in_from[j];
+                const unsigned long long k = akey[u];
+                if (k == kNoArr) continue;
+                const double cand = key_double(k) + net_delay(a.pin_xy[u], pt, cap, a.r, a.c);
+                if (!found || cand > best) {
+                    best = cand, found = true, bu = u, ntie = 1;
+                } else if (cand == best) {
+                    ++ntie;
+                }
+            }
+        }
+    }
+    a.arr[t] = found ? best : 0.0;
+    a.ak[t] = found ? 1 : 0;
+    a.pred[t] = found ? bu : -1;
+    a.tie[t] = ntie > 1;
+    if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = t;
+    if (!found) return;
+    const int o0 = a.out_start[t], o1 = a.out_start[t + 1];
+    if (o1 > o0) {
+        const double cand = best + a.cell_delay[a.pin_cell[t]];
+        const unsigned long long k = double_key(cand);
+        for (int j = o0; j < o1; ++j) atomicMax(&akey[a.out_to[j]], k);
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_arr_decode(int n, const int* __restrict__ pins, StaArgs a,
+                                                       const unsigned long long* __restrict__ akey)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const int v = pins[i];
+    if (a.is_source[v]) {
+        a.arr[v] = 0.0, a.ak[v] = 1, a.pred[v] = -1, a.tie[v] = 0;
+        return;
+    }
+    const unsigned long long k = akey[v];
+    if (k == kNoArr) {
+        a.arr[v] = 0.0, a.ak[v] = 0, a.pred[v] = -1, a.tie[v] = 0;
+        return;
+    }
+    const double best = key_double(k), dcell = a.cell_delay[a.pin_cell[v]];
+    int bu = -1, ntie = 0;
+    for (int j = a.in_start[v]; j < a.in_start[v + 1]; ++j) {
+        const int u = a.in_from[j];
+        if (!a.ak[u]) continue;
+        if (a.arr[u] + dcell == best) {
+            if (bu < 0) bu = u;
+            ++ntie;
+        }
+    }
+    a.arr[v] = best, a.ak[v] = 1, a.pred[v] = bu, a.tie[v] = ntie > 1;
+    if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = v;
+}
+
+__global__ void __launch_bounds__(kBlock) k_req_push(int lo, int hi, const int* __restrict__ pins, StaArgs a,
+                                                     unsigned long long* __restrict__ rkey)
+{
+    const int i = lo + blockIdx.x * kBlock + threadIdx.x;
+    if (i >= hi) return;
+    const int t = pins[i];
+    double best = INFINITY;
+    bool found = false;
+    if (a.is_endpoint[t]) best = a.clock, found = true;
+    const int o0 = a.out_start[t], o1 = a.out_start[t + 1];
+    if (o1 > o0) {
+        const double dcell = a.cell_delay[a.pin_cell[t]];
+        for (int j = o0; j < o1; ++j) { // cell arcs to outputs (final: higher levels)
+            const unsigned long long k = rkey[a.out_to[j]];
+            if (k == kNoReq) continue;
+            const double cand = key_double(k) - dcell;
+            if (!found || cand < best) best = cand, found = true;
+        }
+    }
+    a.req[t] = found ? best : a.clock;
+    a.rk[t] = found ? 1 : 0;
+    if (!found) return;
+    const int j0 = a.in_start[t], j1 = a.in_start[t + 1];
+    if (j1 > j0) {
+        const double2 pt = a.pin_xy[t];
+        const double cap = a.pin_cap[t];
+        for (int j = j0; j < j1; ++j) {
+            const int u = a.in_from[j];
+            atomicMin(&rkey[u], double_key(best - net_delay(a.pin_xy[u], pt, cap, a.r, a.c)));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_req_decode(int n, const int* __restrict__ pins, StaArgs a,
+                                                       const unsigned long long* __restrict__ rkey)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const int u = pins[i];
+    const unsigned long long k = rkey[u];
+    a.req[u] = k == kNoReq ? a.clock : key_double(k);
+    a.rk[u] = k == kNoReq ? 0 : 1;
+}
+
 // Grid-wide barrier for the persistent STA (all blocks co-resident: cooperative launch).  Arrival
 // counter + generation word; the last block to arrive resets the counter and bumps the generation.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks)
@@ -398,6 +544,16 @@ StaArgs sta_args(tdpg_session* s)
     return a;
 }
 
+// TDPG_STA_ALL_LEVELS=1: the plain pull sweep, one launch per level over every pin (A/B switch).
+static bool all_levels_sweep()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_STA_ALL_LEVELS");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // Full STA at the current positions; leaves endpoint keys in sort_k0/sort_v0 and
 // [tns, wns, n_violated] in out3. Stream-ordered, no host sync.  The 2L per-level launches are
 // captured once into a CUDA graph (re-captured only if a buffer it uses moved).
@@ -405,7 +561,7 @@ void sta_record(tdpg_session* s, double* out3)
 {
     const int P = s->P;
     const bool persist = s->sta_grid > 0;
-    if (!s->pin_xy_external && !persist) { // pin positions from the cells (netlist.cpp:23-32) unless given
+    if (!s->pin_xy_external && !persist && all_levels_sweep()) { // pin positions from the cells (netlist.cpp:23-32) unless given
         k_pin_xy<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor,
                                                               s->pin_xy);
         CK_LAUNCH();
@@ -423,6 +579,24 @@ void sta_record(tdpg_session* s, double* out3)
                               !s->pin_xy_external,
                               static_cast<const double2*>(s->pin_off.p), static_cast<const double2*>(s->cell_xy.p),
                               static_cast<const double2*>(s->anchor.p), s->grid_bar.p));
+    } else if (!all_levels_sweep()) { // push sweep over sink levels (see k_arr_push)
+        k_sta_init<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, a, !s->pin_xy_external, s->pin_off, s->cell_xy,
+                                                                 s->anchor, s->sta_akey, s->sta_rkey);
+        for (int l = 0; l < s->L; ++l) {
+            const int lo = s->h_sta_in_start[l], hi = s->h_sta_in_start[l + 1];
+            if (hi > lo) k_arr_push<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, s->sta_in_pins, a,
+                                                                                        s->sta_akey);
+        }
+        const int n_out = s->h_sta_out_start[s->L];
+        if (n_out) k_arr_decode<<<blocks_for(n_out, kBlock), kBlock, 0, s->st>>>(n_out, s->sta_out_pins, a, s->sta_akey);
+        CK_LAUNCH();
+        for (int l = s->L - 1; l >= 0; --l) {
+            const int lo = s->h_sta_in_start[l], hi = s->h_sta_in_start[l + 1];
+            if (hi > lo) k_req_push<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, s->sta_in_pins, a,
+                                                                                        s->sta_rkey);
+        }
+        if (n_out) k_req_decode<<<blocks_for(n_out, kBlock), kBlock, 0, s->st>>>(n_out, s->sta_out_pins, a, s->sta_rkey);
+        CK_LAUNCH();
     } else {
     for (int l = 0; l < s->L; ++l) {
         const int lo = s->h_lvl_start[l], hi = s->h_lvl_start[l + 1];
@@ -443,13 +617,15 @@ void sta_record(tdpg_session* s, double* out3)
     CK_LAUNCH();
 }
 
-// Size the persistent STA for co-residency (every block resident at once, cooperative launch);
-// TDPG_STA_PERSIST=0 falls back to one launch per level.
+// Size the persistent STA for co-residency (every block resident at once, cooperative launch).
+// Opt-in (TDPG_STA_PERSIST=1): measured on B200 at 1M cells it is slower than one launch per level
+// (1.32-1.68 ms vs 1.12 ms: the level sweep is bound by dependent gathers, not by launch gaps, and
+// the co-resident grid holds fewer loads in flight than a full grid per level).
 void sta_setup(tdpg_session* s)
 {
     s->sta_grid = 0;
     const char* e = std::getenv("TDPG_STA_PERSIST");
-    if (e && std::atoi(e) == 0) return;
+    if (!(e && std::atoi(e) != 0)) return;
     int coop = 0, sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, s->device));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
