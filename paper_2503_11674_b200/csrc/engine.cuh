@@ -69,6 +69,13 @@ struct TraceRowDev {
 
 struct Engine; // placement loop state (gp.cu)
 
+// k-best extraction scratch (kpaths.cu), grow-only
+struct KbScratch {
+    DBuf<int> npath, npins, poff, pinoff, cstart, clen, cpins, order, idx0, flag;
+    DBuf<double> cslack;
+    DBuf<unsigned long long> key0, key1;
+};
+
 } // namespace tdpg
 
 struct tdpg_session {
@@ -160,6 +167,7 @@ struct tdpg_session {
     tdpg::DBuf<int2> kb_pred;
     tdpg::DBuf<int> kb_cnt;
     int kb_K = 0;
+    tdpg::KbScratch kbx;
     tdpg::DBuf<unsigned> kh_key, kh_key_s; // engine refresh with k > 1 / topn: hits keyed by sink pin
     tdpg::DBuf<int> kh_idx_s;
     bool hits_sorted = false;

@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
     if (X0 > bb[1]) return; // no movable cell in this block
     const double area = s.x * s.y;
     if (W * H <= kWinBins) {
-        for (int k = threadIdx.x; k < W * H; k += kBlock) win_lo[k] = 0u, win_hi[k] = 0u;
+        for (int k = threadIdx.x; k < static_cast<int>(W * H); k += kBlock) win_lo[k] = 0u, win_hi[k] = 0u;
         __syncthreads();
         if (valid) {
             const SmemAcc sa{win_lo, win_hi};
@@ -602,9 +602,11 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
             else scatter_cell_wide(p, s, g, sa, H, Y0, X0);
         }
         __syncthreads();
-        for (int k = threadIdx.x; k < W * H; k += kBlock) {
+        const int h = static_cast<int>(H), n = static_cast<int>(W * H);
+        for (int k = threadIdx.x; k < n; k += kBlock) {
             const unsigned long long v = (static_cast<unsigned long long>(win_hi[k]) << 32) | win_lo[k];
-            if (v) atomicAdd(&acc[static_cast<long long>(X0 + k / H) * g.ny + (Y0 + k % H)], v);
+            const int col = k / h;
+            if (v) atomicAdd(&acc[static_cast<long long>(X0 + col) * g.ny + (Y0 + k - col * h)], v);
         }
     } else if (valid) {
         const GlobalAcc ga{acc};

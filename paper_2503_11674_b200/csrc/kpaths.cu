@@ -376,13 +376,16 @@ void extract_policy_dev(tdpg_session* s, int policy, int n, int k, bool sink_key
     s->hits_sorted = false;
     if (nsel <= 0 || per <= 0) return;
     const int* ep = s->sort_v1.p;
-    DBuf<int> npath(nsel), npins(nsel), poff(nsel), pinoff(nsel);
+    // session-owned grow-only scratch: no cudaMalloc / cudaFree (device-synchronising) per extraction
+    KbScratch& X = s->kbx;
+    DBuf<int>&npath = X.npath, &npins = X.npins, &poff = X.poff, &pinoff = X.pinoff;
+    npath.reserve(nsel), npins.reserve(nsel), poff.reserve(nsel), pinoff.reserve(nsel);
     int K = policy == 1 ? std::min(per, 16) : per;
     long long np = 0, npins_tot = 0;
-    DBuf<int> cstart, clen, cpins, order;
-    DBuf<double> cslack;
-    DBuf<unsigned long long> key0, key1;
-    DBuf<int> idx0;
+    DBuf<int>&cstart = X.cstart, &clen = X.clen, &cpins = X.cpins, &order = X.order;
+    DBuf<double>& cslack = X.cslack;
+    DBuf<unsigned long long>&key0 = X.key0, &key1 = X.key1;
+    DBuf<int>& idx0 = X.idx0;
     for (;;) {
         kbest_build(s, K);
         k_kb_count<<<blocks_for(nsel, kBlock), kBlock, 0, s->st>>>(nsel, ep, per, s->kb_pred, s->kb_cnt, K, npath,
@@ -461,8 +464,9 @@ void extract_policy_dev(tdpg_session* s, int policy, int n, int k, bool sink_key
                                                                 s->pin_dir, s->ex_hoff, s->hit_key, s->hit_slack,
                                                                 s->hit_idx, sink_keys ? s->kh_key.p : nullptr);
     CK_LAUNCH();
-    DBuf<int> flag(std::max(s->P, 1));
-    flag.zero(s->st);
+    DBuf<int>& flag = X.flag;
+    flag.reserve(std::max(s->P, 1));
+    flag.zero(s->st, std::max(s->P, 1));
     CK(cudaMemsetAsync(s->counters.p + 4, 0, 2 * sizeof(int), s->st));
     k_unique_last<<<blocks_for(nfin, kBlock), kBlock, 0, s->st>>>(nfin, s->ex_off, s->ex_len, s->ex_pins, flag,
                                                                   s->counters.p + 4);
