@@ -9,8 +9,8 @@ region.  fp64 throughout, like the reference.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 `value` = GP iterations/s over the whole job (N independent replicas when N > 1,
-"replicas only").  `e2e` = the same iterations through the C-ABI with
-host buffers (positions H2D + new positions/trace row D2H every step).  Extra keys
+"replicas only").  `e2e` = run_placement through the C-ABI (tdpg_place) with pinned
+host buffers (positions in, positions + trace rows out).  Extra keys
 report the STA + top-k extraction sweep on the same 1M timing graph, the dominant
 kernel's roofline and the reference CPU baseline.
 """
@@ -133,6 +133,21 @@ def kernel_bytes(d, grid, E_tot):
         # fold CSR + entry gradients + fixed/positions/sizes/density gradient + Adam m,v r/w + positions written
         "cells": 4 * (C + 1) + 4 * E_tot + 16 * E_tot + C * (1 + 16 + 16 + 16) + C * (32 + 32) + 16 * C,
     }
+
+
+def footprint_entries(d, xy, grid):
+    """Non-zero density footprint entries (bins a cell's B-spline weights touch, five-bin form) at the
+    given positions: (a_hi - a_lo + 3) bins per axis, clipped to the grid (gp_kernels.cuh axis5)."""
+    x0, y0, x1, y1 = d.core
+    tot = 0
+    for lo, w, o, span in ((xy[:, 0], d.cell_w, x0, x1 - x0), (xy[:, 1], d.cell_h, y0, y1 - y0)):
+        pitch = span / grid
+        al = np.floor((lo - o) / pitch - 1.0)
+        ah = np.floor((lo + w - o) / pitch - 1.0)
+        b0, b1 = np.maximum(al, 0), np.minimum(ah + 2, grid - 1)
+        n = np.maximum(b1 - b0 + 1, 0)
+        tot = n if isinstance(tot, int) else tot * n
+    return int(np.sum(tot[d.cell_fixed == 0]))
 
 
 def iteration_bytes(d, grid, Q=0):
@@ -325,18 +340,25 @@ def run_ours(args):
     else:
         prof = s.profile_iteration(5)
 
-    # e2e: the same iterations through host buffers (pinned), positions in/out every step
+    # e2e: the call a user makes — run_placement through the C-ABI (tdpg_place) on the same design and
+    # schedule, `steps` iterations with a timing refresh every m, from pinned host positions to pinned
+    # host positions + the per-iteration trace rows; wall clock over the whole call (device loop, its
+    # engine set-up, the final STA), max over ranks.
     C = d.n_cells
     hin = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
     hout = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
-    hin.numpy()[:] = s.positions().reshape(-1)
-    e2e_steps = min(args.steps, 20)
+    hin.numpy()[:] = d.positions.reshape(-1)
+    e2e_cfg = bench_config(args, args.steps)
+    barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        s.step_host(hin.data_ptr(), hout.data_ptr())
-        hin, hout = hout, hin
+    e2e_rows, _ = s.place_host(e2e_cfg, hin.data_ptr(), hout.data_ptr())
     e2e_s = time.perf_counter() - t0
-    e2e_val = (1 if partition else world) * e2e_steps / e2e_s
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = (1 if partition else world) * e2e_rows / e2e_s
     sweep, xy_snap = (extraction_sweep(d) if rank == 0 else ({}, None))
 
     if rank != 0:
@@ -348,6 +370,14 @@ def run_ours(args):
     dom_ms = prof[dom]
     achieved = kb[dom] / (dom_ms / 1000.0) / 1e9
     iter_ms = sum(prof.values())
+    # the scatter's real limiter: shared-memory atomics, two 32-bit lane-atomics per footprint entry
+    # (fixed-point lo word + hi word); peak = 4 SMSPs x 148 SMs x clock / 2 cycles per spread lane-atomic
+    # (B300_MICROARCH.md "ATOMS (spread-addr) 2 cyc/lane"; same SM design on B200)
+    n_ent = footprint_entries(d, s.positions(), args.grid)
+    clk_summary = clk.summary()
+    sm_ghz = (clk_summary.get("sm_mhz") or 1965.0) / 1000.0
+    atom_peak = 148 * 4 * sm_ghz * 1e9 / 2 / 1e9  # G lane-atomics/s
+    atom_ach = 2 * n_ent / (prof.get("density_scatter", 1e9) / 1000.0) / 1e9
     ib = iteration_bytes(d, args.grid)
     cpu = None
     if not args.no_cpu_baseline:
@@ -373,20 +403,28 @@ def run_ours(args):
                    "parallelism": ("nets partitioned, NCCL all-reduce of the cell gradient" if partition else
                                    "replicas") if world > 1 else "single GPU", "refreshes_timed": refreshes,
                    "refresh_ms_timed": round(refresh_ms, 3), "ledger_pairs_end": st1["ledger_pairs"]},
-        "e2e": {"value": round(e2e_val, 3), "unit": "iters/s", "h2d_bytes_per_step": 16 * C,
-                "d2h_bytes_per_step": 16 * C + 88, "path": "tdpg_step_host (C-ABI, pinned host positions)"},
+        "e2e": {"value": round(e2e_val, 3), "unit": "iters/s",
+                "h2d_bytes_per_step": round(16 * C / max(e2e_rows, 1), 1),
+                "d2h_bytes_per_step": round((16 * C + 88 * e2e_rows) / max(e2e_rows, 1), 1),
+                "steps": e2e_rows, "wall_s": round(e2e_s, 4),
+                "path": "tdpg_place (run_placement through the C-ABI): pinned positions in, device loop with "
+                        "timing refresh every m, positions + trace rows out"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk.get("hbm_gbs"),
                      "unit": "GB/s", "frac": round(achieved / pk.get("hbm_gbs", 6650.0), 4), "traffic": traffic,
                      "algorithmic_bytes": kb[dom], "kernel_ms": round(dom_ms, 4),
-                     "peak_source": "measured" if "fallback" not in pk else "fallback"},
+                     "peak_source": "measured" if "fallback" not in pk else "fallback",
+                     "limiter": {"kernel": "density_scatter", "bound": "smem_atomics", "unit": "G lane-atomics/s",
+                                 "achieved": round(atom_ach, 1), "peak": round(atom_peak, 1),
+                                 "frac": round(atom_ach / atom_peak, 3), "footprint_entries": n_ent,
+                                 "peak_source": "B300_MICROARCH.md ATOMS spread-addr 2 cyc/lane x 4 SMSP x 148 SM"}},
         "iteration": {"gp_iteration_ms": round((dev_ms_max - refresh_ms) / args.steps, 4),
                       "refresh_ms_each": round(refresh_ms / max(refreshes, 1), 3),
                       "kernels_ms_serialised": {k: round(v, 4) for k, v in prof.items()}, "sum_ms": round(iter_ms, 4),
                       "bytes_iter_survey": ib,
                       "frac_of_hbm": round(ib / (iter_ms / 1000.0) / 1e9 / pk.get("hbm_gbs", 6650.0), 4)},
         "extraction_sweep_ms": sweep,
-        "clocks": clk.summary(),
+        "clocks": clk_summary,
         "cpu_baseline": cpu,
         "setup_s": {"generate_and_calibrate": round(gen_s, 2), "engine_init": round(init_s, 2)},
     }

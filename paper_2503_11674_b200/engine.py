@@ -349,6 +349,19 @@ class Session:
                     stop_reason="overflow" if so.value else "max_iters", tns=fin[0], wns=fin[1], hpwl=fin[2],
                     ledger=self.ledger())
 
+    def place_host(self, cfg: dict, xy_in_ptr: int, xy_out_ptr: int):
+        """run_placement through the C-ABI with caller-owned host buffers (e.g. pinned): positions in,
+        the whole device loop (tdpg_place), positions and trace out.  Returns (rows, final tns/wns/hpwl)."""
+        c = make_config(cfg)
+        rows = (TdpgTraceRow * max(c.max_iters, 1))()
+        nr, so = C.c_int32(), C.c_int32()
+        fin = (C.c_double * 3)()
+        _check(self.lib.tdpg_set_positions(self.h, C.c_void_p(xy_in_ptr)))
+        _check(self.lib.tdpg_place(self.h, C.byref(c), self.d.pos_explicit.ctypes.data, rows, C.byref(nr),
+                                   C.byref(so), fin))
+        _check(self.lib.tdpg_get_positions(self.h, C.c_void_p(xy_out_ptr)))
+        return nr.value, tuple(fin)
+
     def engine_init(self, cfg: dict | None = None, xy=None):
         c = make_config(cfg)
         self._pos(xy if xy is not None else self.d.positions)
