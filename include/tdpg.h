@@ -108,6 +108,7 @@ typedef struct tdpg_config {
     uint64_t seed;
     double init_jitter_frac;
     int32_t threads;           /* accepted for drop-in parity; ignored        */
+    int32_t density_model;     /* extension: 0 bin overflow (the reference), 1 electrostatic (DCT Poisson) */
 } tdpg_config;
 
 void tdpg_config_default(tdpg_config* cfg);
@@ -153,6 +154,11 @@ int tdpg_set_constraints(tdpg_session* s, double clock_period, double r_unit, do
 /* DensityGrid(nx, ny, target_density) then evaluate; d_cell [2*n_cells] may be NULL. */
 int tdpg_set_grid(tdpg_session* s, int32_t nx, int32_t ny, double target_density);
 int tdpg_density(tdpg_session* s, double* value, double* overflow, double* d_cell);
+/* Density model of one-off evaluations (tdpg_density / tdpg_objective); the placement loop takes
+ * tdpg_config.density_model.  Electrostatic: value = 1/2 sum rho psi with L psi = rho - mean(rho). */
+int tdpg_set_density_model(tdpg_session* s, int32_t model);
+/* Last electrostatic evaluation's charge map rho and potential psi ([nx*ny], bin bx*ny + by). */
+int tdpg_density_fields(tdpg_session* s, double* rho, double* psi);
 
 /* ---- pin-pair ledger (PinPairWeights) ------------------------------- */
 int tdpg_pp_set(tdpg_session* s, int64_t q, const int32_t* a, const int32_t* b, const double* w);

@@ -20,13 +20,28 @@
 #include <string>
 #include <vector>
 
+#include <cufft.h>
+
 #include "common.cuh"
 
 struct tdpg_session;
 
 namespace tdpg {
 
+// Electrostatic density (electro.cu): cuFFT plans and work arrays of the grid's Poisson solve.
+struct ElectroPlan {
+    int nx = 0, ny = 0;
+    cufftHandle plan[4] = {0, 0, 0, 0}; // D2Z along y, D2Z along x, Z2D along x, Z2D along y
+    DBuf<double> rho, psi, r1, r2;
+    DBuf<double2> z;
+    void ensure(int gx, int gy);
+    void release();
+    ~ElectroPlan();
+};
+
 struct Grid {
+    int model = 0; // 0: bin overflow penalty (density.cpp, the reference); 1: electrostatic (electro.cu)
+    ElectroPlan electro;
     int nx = 0, ny = 0;
     double td = 0.0;
     double x0 = 0, y0 = 0, bw = 0, bh = 0, cap = 0, total_movable = 0;
@@ -205,6 +220,7 @@ namespace tdpg {
 // session.cu
 void upload_positions(tdpg_session* s, const double* xy);
 void ensure_grid(tdpg_session* s, int nx, int ny, double td);
+void set_density_model(tdpg_session* s, int model);
 void* cub_scratch(tdpg_session* s, size_t bytes);
 void sort_cells_spatial(tdpg_session* s);
 
@@ -234,6 +250,10 @@ int sorted_violated(tdpg_session* s);
 // partition.cu
 void comm_allreduce(tdpg_session* s, double* buf, size_t n);
 void comm_destroy(tdpg_session* s);
+
+// electro.cu
+void electro_solve(tdpg_session* s, cudaStream_t st);
+void electro_energy(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl, cudaStream_t st);
 
 // kpaths.cu
 void kbest_build(tdpg_session* s, int K);

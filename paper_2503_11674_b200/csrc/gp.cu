@@ -636,7 +636,7 @@ constexpr int kBinsBlocks = 148 * 4;
 __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g, long long* __restrict__ acc,
                                                          const double* __restrict__ base,
                                                          double* __restrict__ excess, double* __restrict__ part_d,
-                                                         const Ctrl* __restrict__ ctrl)
+                                                         const Ctrl* __restrict__ ctrl, double* __restrict__ rho)
 {
     __shared__ double sh[2][kBlock / 32];
     if (ctrl && ctrl->stopped) return;
@@ -644,6 +644,7 @@ __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g,
     auto one = [&](long long q, long long k) {
         const double mov = static_cast<double>(q) * g.inv_scale;
         const double occ = base ? base[k] + mov : mov;
+        if (rho) rho[k] = occ; // electrostatic model: the charge map
         const double ex = smax(0.0, occ - g.cap);
         v2 += ex * ex;
         v1 += ex;
@@ -780,7 +781,7 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(FinArgs a, Ctrl* ctrl, I
 // column: dgx = sum_bx area*dwx(bx) * 2*sum_by f(bx,by)*wy(by), dgy = sum_bx area*wx(bx) * 2*sum_by f*dwy.
 // =====================================================================================
 __device__ __noinline__ double2 dens_grad_wide(const double2 p, const double2 s, const GridDev& g,
-                                               const double* __restrict__ excess)
+                                               const double* __restrict__ excess, double fscale)
 {   // general footprint (cells wider than ~2 bins)
     const Axis ax = make_axis(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx);
     const Axis ay = make_axis(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny);
@@ -798,8 +799,8 @@ __device__ __noinline__ double2 dens_grad_wide(const double2 p, const double2 s,
             const double f = excess[static_cast<long long>(bx) * g.ny + by];
             sx += f * wy, sy += f * dwy;
         }
-        dgx += (area * dwx) * (2.0 * sx);
-        dgy += (area * wx) * (2.0 * sy);
+        dgx += (area * dwx) * (fscale * sx);
+        dgy += (area * wx) * (fscale * sy);
     }
     return make_double2(dgx, dgy);
 }
@@ -808,8 +809,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_dens_grad(int n_mov, const int* _
                                                       const double2* __restrict__ cell_xy,
                                                       const double2* __restrict__ cell_wh, GridDev g,
                                                       const double* __restrict__ excess, double2* __restrict__ dgrad,
-                                                      const Ctrl* __restrict__ ctrl)
-{
+                                                      const Ctrl* __restrict__ ctrl, double fscale)
+{   // field = excess with fscale 2 (d sum excess^2, density.cpp:148-156) or the potential with fscale 1
     if (ctrl && ctrl->stopped) return;
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n_mov) return;
@@ -819,7 +820,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dens_grad(int n_mov, const int* _
     int bx, by;
     if (!(axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx) &&
           axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy))) {
-        dgrad[c] = dens_grad_wide(p, s, g, excess);
+        dgrad[c] = dens_grad_wide(p, s, g, excess, fscale);
         return;
     }
     const double area = s.x * s.y;
@@ -834,8 +835,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_dens_grad(int n_mov, const int* _
         double sx = 0.0, sy = 0.0;
 #pragma unroll
         for (int j = 0; j < kF5; ++j) sx += f[j] * wy[j], sy += f[j] * dwy[j];
-        dgx += (area * dwx[a]) * (2.0 * sx);
-        dgy += (area * wx[a]) * (2.0 * sy);
+        dgx += (area * dwx[a]) * (fscale * sx);
+        dgy += (area * wx[a]) * (fscale * sy);
     }
     dgrad[c] = make_double2(dgx, dgy);
 }
@@ -1176,9 +1177,7 @@ void launch_density(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl)
     const GridDev g = grid_dev(s);
     if (!ctrl) sort_cells_spatial(s); // one-off evaluations sort first; the loop sorts on its own schedule
     launch_density_scatter_ctrl(s, ctrl);
-    k_density_bins<<<nblk, kBlock, 0, s->st>>>(s->grid.bins(), g, s->grid.acc, s->grid.has_fixed ? s->grid.base.p : nullptr,
-                                               s->grid.excess, part_d, ctrl);
-    CK_LAUNCH();
+    launch_density_bins_ctrl(s, part_d, nblk, ctrl);
 }
 
 void launch_density(tdpg_session* s, double* part_d, int nblk) { launch_density(s, part_d, nblk, nullptr); }
@@ -1196,9 +1195,14 @@ void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl)
 void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl)
 {
     const GridDev g = grid_dev(s);
+    const bool el = s->grid.model == 1;
     k_density_bins<<<nblk, kBlock, 0, s->st>>>(s->grid.bins(), g, s->grid.acc, s->grid.has_fixed ? s->grid.base.p : nullptr,
-                                               s->grid.excess, part_d, ctrl);
+                                               s->grid.excess, part_d, ctrl, el ? s->grid.electro.rho.p : nullptr);
     CK_LAUNCH();
+    if (el) { // potential, then the energy partials replace the overflow-penalty value partials
+        electro_solve(s, s->st);
+        electro_energy(s, part_d, nblk, ctrl, s->st);
+    }
 }
 
 CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps)
@@ -1224,8 +1228,10 @@ void launch_dens_grad(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st)
 {
     const int n_mov = s->grid.n_movable;
     if (n_mov > 0) {
+        const bool el = s->grid.model == 1;
         k_dens_grad<<<blocks_for(n_mov, kBlock), kBlock, 0, st>>>(n_mov, s->grid.perm, s->cell_xy, s->cell_wh,
-                                                                  grid_dev(s), s->grid.excess, s->dgrad, ctrl);
+                                                                  grid_dev(s), el ? s->grid.electro.psi.p : s->grid.excess.p,
+                                                                  s->dgrad, ctrl, el ? 1.0 : 2.0);
         CK_LAUNCH();
     }
 }

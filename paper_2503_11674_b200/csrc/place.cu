@@ -107,6 +107,7 @@ void validate_config(const tdpg_config& c)
     if (c.init_jitter_frac < 0.0) bad("init_jitter_frac must be >= 0");
     if (c.threads < 1) bad("threads must be >= 1");
     if (c.extraction != 0 && c.extraction != 1) bad("extraction must be \"endpoint\" or \"topn\"");
+    if (c.density_model != 0 && c.density_model != 1) bad("density_model must be \"overflow\" or \"electrostatic\"");
 }
 
 __global__ void k_l1_pair(int C, const double2* __restrict__ a, const double2* __restrict__ b,
@@ -296,6 +297,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     }
     upload_positions(s, xy.data());
     ensure_grid(s, cfg->grid_nx, cfg->grid_ny, cfg->target_density);
+    set_density_model(s, cfg->density_model);
 
     // fresh PinPairWeights: the engine keeps it dense (weight per sink pin, fused into WA)
     s->Q = 0;

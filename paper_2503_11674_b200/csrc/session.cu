@@ -121,6 +121,17 @@ void ensure_grid(tdpg_session* s, int nx, int ny, double td)
     } else {
         g.base.release();
     }
+    if (g.model == 1) g.electro.ensure(nx, ny);
+}
+
+// Density model of the session's grid (0 = bin overflow, 1 = electrostatic); plans are made here, never
+// inside a graph capture.
+void set_density_model(tdpg_session* s, int model)
+{
+    if (model != 0 && model != 1)
+        throw Error(TDPG_ERR_VALIDATION, "validation error: density_model must be \"overflow\" or \"electrostatic\"");
+    s->grid.model = model;
+    if (model == 1 && s->grid.valid()) s->grid.electro.ensure(s->grid.nx, s->grid.ny);
 }
 
 } // namespace tdpg
@@ -566,6 +577,25 @@ int tdpg_get_positions(tdpg_session* s, double* xy)
 {
     API_BEGIN
     s->cell_xy.download(reinterpret_cast<double2*>(xy), s->C, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_set_density_model(tdpg_session* s, int32_t model)
+{
+    API_BEGIN
+    set_density_model(s, model);
+    API_END
+}
+
+int tdpg_density_fields(tdpg_session* s, double* rho, double* psi)
+{
+    API_BEGIN
+    if (s->grid.model != 1 || s->grid.electro.nx == 0)
+        throw Error(TDPG_ERR_VALIDATION, "validation error: no electrostatic density evaluated");
+    const size_t B = static_cast<size_t>(s->grid.bins());
+    if (rho) s->grid.electro.rho.download(rho, B, s->st);
+    if (psi) s->grid.electro.psi.download(psi, B, s->st);
     CK(cudaStreamSynchronize(s->st));
     API_END
 }

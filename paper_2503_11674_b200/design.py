@@ -77,6 +77,7 @@ class TdpgConfig(C.Structure):
         ("seed", C.c_uint64),
         ("init_jitter_frac", C.c_double),
         ("threads", C.c_int32),
+        ("density_model", C.c_int32),  # extension: "overflow" (the reference) | "electrostatic"
     ]
 
 
@@ -125,6 +126,7 @@ CONFIG_DEFAULTS = {
     "seed": 1,
     "init_jitter_frac": 0.02,
     "threads": 1,
+    "density_model": "overflow",  # extension (not a reference key): "overflow" | "electrostatic"
 }
 
 
@@ -142,6 +144,8 @@ def make_config(cfg: dict | None = None) -> TdpgConfig:
             v = {"quadratic": 0, "linear": 1}[v]
         elif name == "extraction":
             v = {"endpoint": 0, "topn": 1}[v]
+        elif name == "density_model":
+            v = {"overflow": 0, "electrostatic": 1}[v]
         elif name == "lambda0":
             v = 0.0 if v == "auto" else float(v)
         elif name == "net_weighting":

@@ -100,6 +100,8 @@ _SIGS = {
     "tdpg_sta_fetch": (C.c_int, [_P, _P, _P, _P, _P, _P, _F64P, _F64P]),
     "tdpg_path_to": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int32, _I32P, _F64P]),
     "tdpg_extract": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P]),
+    "tdpg_set_density_model": (C.c_int, [_P, C.c_int32]),
+    "tdpg_density_fields": (C.c_int, [_P, _P, _P]),
     "tdpg_partition_plan": (C.c_int, [C.c_int32, _P, C.c_int32, _P, _P]),
     "tdpg_set_partition": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "tdpg_comm_unique_id": (C.c_int, [_P]),
@@ -218,6 +220,17 @@ class Session:
         d = np.zeros((self.d.n_cells, 2))
         _check(self.lib.tdpg_density(self.h, C.byref(v), C.byref(o), d.ctypes.data))
         return v.value, o.value, d
+
+    def set_density_model(self, model):
+        """0 / "overflow": the reference's bin-overflow penalty; 1 / "electrostatic": DCT Poisson energy."""
+        m = {"overflow": 0, "electrostatic": 1}.get(model, model)
+        _check(self.lib.tdpg_set_density_model(self.h, int(m)))
+
+    def density_fields(self, nx, ny):
+        """Charge map and potential of the last electrostatic evaluation, shaped [nx, ny]."""
+        rho, psi = np.zeros((nx, ny)), np.zeros((nx, ny))
+        _check(self.lib.tdpg_density_fields(self.h, rho.ctypes.data, psi.ctypes.data))
+        return rho, psi
 
     def set_ledger(self, ledger):
         if ledger is None or len(ledger[0]) == 0:

@@ -158,7 +158,7 @@ def validate(design):
 
 
 def default_config():
-    return dict(_DEFAULTS)
+    return {k: v for k, v in _DEFAULTS.items() if k != "density_model"}  # the reference's keys only
 
 
 @_guard
