@@ -12,7 +12,8 @@ warm = int(sys.argv[2]) if len(sys.argv) > 2 else 17
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 d = generate(seed=1, cells=cells, fail_frac=0.8, calibrate=True)
 s = Session(d)
-s.engine_init({"grid_nx": 1024, "grid_ny": 1024, "m": 15, "timing_start_iter": 0, "max_iters": warm + 40, "seed": 1})
+grid = int(sys.argv[4]) if len(sys.argv) > 4 else 1024
+s.engine_init({"grid_nx": grid, "grid_ny": grid, "m": 15, "timing_start_iter": 0, "max_iters": warm + 40, "seed": 1})
 s.iterate(warm)
 import torch  # noqa: E402  (cudaProfilerStart/Stop on the primary context the engine uses)
 torch.cuda.synchronize()
