@@ -165,7 +165,7 @@ def make_design(args, rank):
     return d, time.time() - t0
 
 
-def extraction_sweep(d, ns=(1000, 10000, 100000)):
+def extraction_sweep(d, ns=(1000, 3000, 10000, 30000, 100000)):
     """STA + report_timing_endpoint(n, 1) on a spread snapshot of the 1M graph, clock set so
     80% of endpoints fail (configs[3]); device time per n (CUDA events)."""
     from paper_2503_11674_b200.engine import Session
