@@ -805,7 +805,7 @@ __device__ __noinline__ double2 dens_grad_wide(const double2 p, const double2 s,
     return make_double2(dgx, dgy);
 }
 
-__global__ void __launch_bounds__(kBlock, 3) k_dens_grad(int n_mov, const int* __restrict__ perm,
+__global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* __restrict__ perm,
                                                       const double2* __restrict__ cell_xy,
                                                       const double2* __restrict__ cell_wh, GridDev g,
                                                       const double* __restrict__ excess, double2* __restrict__ dgrad,
@@ -862,7 +862,7 @@ struct CellArgs {
     double core_x0, core_y0, core_x1, core_y1;
 };
 
-__global__ void __launch_bounds__(kBlock) k_cells(CellArgs a, const IterCur* __restrict__ cur, Ctrl* ctrl)
+__global__ void __launch_bounds__(kBlock, 6) k_cells(CellArgs a, const IterCur* __restrict__ cur, Ctrl* ctrl)
 {
     const int c = blockIdx.x * kBlock + threadIdx.x;
     if (c >= a.C) return;
