@@ -132,6 +132,13 @@ struct tdpg_session {
     tdpg::DBuf<int> sta_out_pins, sta_in_pins;           // Output pins / Input pins, each grouped by level
     std::vector<int> h_sta_out_start, h_sta_in_start;    // [L + 1]
     tdpg::DBuf<unsigned long long> sta_akey, sta_rkey;   // push sweep: Output pins' arrival / required keys
+    // Level-major copy of the timing graph for the push sweep (L-space index i <-> pin L_pin[i]; per
+    // level its Input pins then its Output pins): every per-pin access of a level is coalesced.
+    tdpg::DBuf<int> L_pin, L_in_start, L_in_from, L_out_start, L_out_to, L_cell, L_pred;
+    tdpg::DBuf<uint8_t> L_flags, L_ak, L_rk, L_tie; // flags: 1 source, 2 endpoint, 4 output
+    tdpg::DBuf<double> L_cap, L_arr, L_req;
+    tdpg::DBuf<double2> L_off, L_anchor, L_xy;
+    std::vector<int> h_L_in_lo, h_L_in_hi; // per level: its Input pins' L range
     tdpg::DBuf<unsigned> grid_bar;   // persistent STA: grid barrier (arrival count, generation)
     int sta_grid = 0;                // co-resident blocks of the persistent STA kernel (0: per-level launches)
 

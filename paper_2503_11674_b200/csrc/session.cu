@@ -287,6 +287,46 @@ void build_graph(tdpg_session* s)
         s->sta_in_pins.upload(ins, s->st);
         s->sta_akey.alloc(std::max(P, 1)), s->sta_rkey.alloc(std::max(P, 1));
     }
+    {   // level-major L-space copy of the graph (timing.cu push sweep)
+        std::vector<int> Lpin, Lidx(P);
+        Lpin.reserve(P);
+        s->h_L_in_lo.assign(s->L, 0), s->h_L_in_hi.assign(s->L, 0);
+        for (int l = 0; l < s->L; ++l) {
+            s->h_L_in_lo[l] = static_cast<int>(Lpin.size());
+            for (int i = s->h_lvl_start[l]; i < s->h_lvl_start[l + 1]; ++i)
+                if (s->h_pin_dir[s->h_lvl_pins[i]] != 1) Lpin.push_back(s->h_lvl_pins[i]);
+            s->h_L_in_hi[l] = static_cast<int>(Lpin.size());
+            for (int i = s->h_lvl_start[l]; i < s->h_lvl_start[l + 1]; ++i)
+                if (s->h_pin_dir[s->h_lvl_pins[i]] == 1) Lpin.push_back(s->h_lvl_pins[i]);
+        }
+        for (int i = 0; i < P; ++i) Lidx[Lpin[i]] = i;
+        std::vector<int> Lis(P + 1, 0), Lif, Los(P + 1, 0), Lot, Lcell(P);
+        Lif.reserve(A), Lot.reserve(A);
+        std::vector<uint8_t> Lfl(P);
+        std::vector<double> Lcap(P);
+        std::vector<double2> Loff(P), Lanc(P);
+        for (int i = 0; i < P; ++i) {
+            const int p = Lpin[i];
+            for (int j = in_s[p]; j < in_s[p + 1]; ++j) Lif.push_back(Lidx[in_from[j]]);
+            for (int j = out_s[p]; j < out_s[p + 1]; ++j) Lot.push_back(Lidx[out_to[j]]);
+            Lis[i + 1] = static_cast<int>(Lif.size()), Los[i + 1] = static_cast<int>(Lot.size());
+            Lfl[i] = static_cast<uint8_t>((s->h_is_source[p] ? 1 : 0) | (s->h_is_endpoint[p] ? 2 : 0) |
+                                          (s->h_pin_dir[p] == 1 ? 4 : 0));
+            Lcap[i] = s->h_pin_cap[p], Lcell[i] = s->h_pin_cell[p];
+            Loff[i] = make_double2(s->h_pin_off[2 * p], s->h_pin_off[2 * p + 1]);
+            Lanc[i] = make_double2(s->h_pin_term[2 * p], s->h_pin_term[2 * p + 1]);
+        }
+        if (Lif.empty()) Lif.push_back(0), Lot.push_back(0);
+        if (Lpin.empty()) Lpin.push_back(0), Lcell.push_back(0), Lfl.push_back(0), Lcap.push_back(0.0),
+            Loff.push_back(make_double2(0, 0)), Lanc.push_back(make_double2(0, 0));
+        s->L_pin.upload(Lpin, s->st), s->L_cell.upload(Lcell, s->st), s->L_flags.upload(Lfl, s->st);
+        s->L_in_start.upload(Lis, s->st), s->L_in_from.upload(Lif, s->st);
+        s->L_out_start.upload(Los, s->st), s->L_out_to.upload(Lot, s->st);
+        s->L_cap.upload(Lcap, s->st), s->L_off.upload(Loff, s->st), s->L_anchor.upload(Lanc, s->st);
+        const size_t n = static_cast<size_t>(std::max(P, 1));
+        s->L_pred.alloc(n), s->L_ak.alloc(n), s->L_rk.alloc(n), s->L_tie.alloc(n);
+        s->L_arr.alloc(n), s->L_req.alloc(n), s->L_xy.alloc(n);
+    }
     s->d_level.upload(s->h_level, s->st);
     std::vector<int> eps(s->h_endpoints);
     std::sort(eps.begin(), eps.end());

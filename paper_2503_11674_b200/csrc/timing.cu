@@ -261,6 +261,166 @@ __global__ void __launch_bounds__(kBlock) k_req_decode(int n, const int* __restr
     a.rk[u] = k == kNoReq ? 0 : 1;
 }
 
+// ---- the push sweep in level-major L-space (default) --------------------------------------------
+// Same arithmetic as k_arr_push / k_req_push / decodes above, on the level-major copy of the graph
+// (session.cu): a level's Input pins are one contiguous L range, so every per-pin load and store of a
+// launch is coalesced and only the driver / fan-out accesses remain gathers.  A final pass writes the
+// results back to pin order (and maps pred / tie-list entries back to pin ids).
+struct LArgs {
+    const int *in_start, *in_from, *out_start, *out_to, *cell, *pin;
+    const uint8_t* flags;
+    const double *cap, *cell_delay;
+    const double2 *off, *anchor;
+    double2* xy;
+    double r, c, clock;
+    double *arr, *req;
+    uint8_t *ak, *rk, *tie;
+    int* pred;
+    unsigned long long *akey, *rkey;
+    int *tie_list, *counters;
+};
+
+__global__ void __launch_bounds__(kBlock) k_L_init(int P, LArgs a, bool from_cells, const double2* __restrict__ cell_xy,
+                                                   const double2* __restrict__ pin_xy)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= P) return;
+    if (from_cells) { // pin_positions (netlist.cpp:23-32)
+        const int c = a.cell[i];
+        const double2 o = a.off[i], b = c >= 0 ? cell_xy[c] : a.anchor[i];
+        a.xy[i] = make_double2(b.x + o.x, b.y + o.y);
+    } else {
+        a.xy[i] = pin_xy[a.pin[i]];
+    }
+    const uint8_t f = a.flags[i];
+    a.akey[i] = (f & 1) ? double_key(0.0) : kNoArr;
+    a.rkey[i] = (f & 2) ? double_key(a.clock) : kNoReq;
+}
+
+__global__ void __launch_bounds__(kBlock) k_L_arr_push(int lo, int hi, LArgs a)
+{
+    const int t = lo + blockIdx.x * kBlock + threadIdx.x;
+    if (t >= hi) return;
+    double best = 0.0;
+    bool found = false;
+    int bu = -1, ntie = 0;
+    if (a.flags[t] & 1) {
+        found = true;
+    } else {
+        const int j0 = a.in_start[t], j1 = a.in_start[t + 1];
+        if (j1 > j0) {
+            const double2 pt = a.xy[t];
+            const double cap = a.cap[t];
+            for (int j = j0; j < j1; ++j) {
+                const int u = a.in_from[j];
+                const unsigned long long k = a.akey[u];
+                if (k == kNoArr) continue;
+                const double cand = key_double(k) + net_delay(a.xy[u], pt, cap, a.r, a.c);
+                if (!found || cand > best) {
+                    best = cand, found = true, bu = u, ntie = 1;
+                } else if (cand == best) {
+                    ++ntie;
+                }
+            }
+        }
+    }
+    a.arr[t] = found ? best : 0.0;
+    a.ak[t] = found ? 1 : 0;
+    a.pred[t] = found ? bu : -1;
+    a.tie[t] = ntie > 1;
+    if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = t;
+    if (!found) return;
+    const int o0 = a.out_start[t], o1 = a.out_start[t + 1];
+    if (o1 > o0) {
+        const unsigned long long k = double_key(best + a.cell_delay[a.cell[t]]);
+        for (int j = o0; j < o1; ++j) atomicMax(&a.akey[a.out_to[j]], k);
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_L_arr_decode(int P, LArgs a)
+{
+    const int v = blockIdx.x * kBlock + threadIdx.x;
+    if (v >= P) return;
+    const uint8_t f = a.flags[v];
+    if (!(f & 4)) return; // Input pins were stored by the push
+    if (f & 1) {
+        a.arr[v] = 0.0, a.ak[v] = 1, a.pred[v] = -1, a.tie[v] = 0;
+        return;
+    }
+    const unsigned long long k = a.akey[v];
+    if (k == kNoArr) {
+        a.arr[v] = 0.0, a.ak[v] = 0, a.pred[v] = -1, a.tie[v] = 0;
+        return;
+    }
+    const double best = key_double(k), dcell = a.cell_delay[a.cell[v]];
+    int bu = -1, ntie = 0;
+    for (int j = a.in_start[v]; j < a.in_start[v + 1]; ++j) {
+        const int u = a.in_from[j];
+        if (!a.ak[u]) continue;
+        if (a.arr[u] + dcell == best) {
+            if (bu < 0) bu = u;
+            ++ntie;
+        }
+    }
+    a.arr[v] = best, a.ak[v] = 1, a.pred[v] = bu, a.tie[v] = ntie > 1;
+    if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = v;
+}
+
+__global__ void __launch_bounds__(kBlock) k_L_req_push(int lo, int hi, LArgs a)
+{
+    const int t = lo + blockIdx.x * kBlock + threadIdx.x;
+    if (t >= hi) return;
+    double best = INFINITY;
+    bool found = false;
+    if (a.flags[t] & 2) best = a.clock, found = true;
+    const int o0 = a.out_start[t], o1 = a.out_start[t + 1];
+    if (o1 > o0) {
+        const double dcell = a.cell_delay[a.cell[t]];
+        for (int j = o0; j < o1; ++j) {
+            const unsigned long long k = a.rkey[a.out_to[j]];
+            if (k == kNoReq) continue;
+            const double cand = key_double(k) - dcell;
+            if (!found || cand < best) best = cand, found = true;
+        }
+    }
+    a.req[t] = found ? best : a.clock;
+    a.rk[t] = found ? 1 : 0;
+    if (!found) return;
+    const int j0 = a.in_start[t], j1 = a.in_start[t + 1];
+    if (j1 > j0) {
+        const double2 pt = a.xy[t];
+        const double cap = a.cap[t];
+        for (int j = j0; j < j1; ++j) {
+            const int u = a.in_from[j];
+            atomicMin(&a.rkey[u], double_key(best - net_delay(a.xy[u], pt, cap, a.r, a.c)));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_L_req_decode(int P, LArgs a)
+{
+    const int u = blockIdx.x * kBlock + threadIdx.x;
+    if (u >= P || !(a.flags[u] & 4)) return;
+    const unsigned long long k = a.rkey[u];
+    a.req[u] = k == kNoReq ? a.clock : key_double(k);
+    a.rk[u] = k == kNoReq ? 0 : 1;
+}
+
+// L-space results back to pin order; pred and tie-list entries become pin ids.
+__global__ void __launch_bounds__(kBlock) k_L_to_pins(int P, LArgs a, bool write_xy, double* __restrict__ arr,
+                                                      double* __restrict__ req, uint8_t* __restrict__ ak,
+                                                      uint8_t* __restrict__ rk, uint8_t* __restrict__ tie,
+                                                      int* __restrict__ pred, double2* __restrict__ pin_xy)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i < a.counters[0]) a.tie_list[i] = a.pin[a.tie_list[i]];
+    if (i >= P) return;
+    const int p = a.pin[i], q = a.pred[i];
+    arr[p] = a.arr[i], req[p] = a.req[i], ak[p] = a.ak[i], rk[p] = a.rk[i], tie[p] = a.tie[i];
+    pred[p] = q >= 0 ? a.pin[q] : -1;
+    if (write_xy) pin_xy[p] = a.xy[i];
+}
+
 // Grid-wide barrier for the persistent STA (all blocks co-resident: cooperative launch).  Arrival
 // counter + generation word; the last block to arrive resets the counter and bumps the generation.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks)
@@ -544,6 +704,16 @@ StaArgs sta_args(tdpg_session* s)
     return a;
 }
 
+// TDPG_STA_PIN_ORDER=1: the push sweep on pin-indexed arrays (A/B switch for the L-space copy).
+static bool pin_order_push()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_STA_PIN_ORDER");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // TDPG_STA_ALL_LEVELS=1: the plain pull sweep, one launch per level over every pin (A/B switch).
 static bool all_levels_sweep()
 {
@@ -579,7 +749,32 @@ void sta_record(tdpg_session* s, double* out3)
                               !s->pin_xy_external,
                               static_cast<const double2*>(s->pin_off.p), static_cast<const double2*>(s->cell_xy.p),
                               static_cast<const double2*>(s->anchor.p), s->grid_bar.p));
-    } else if (!all_levels_sweep()) { // push sweep over sink levels (see k_arr_push)
+    } else if (!all_levels_sweep() && !pin_order_push()) { // L-space push sweep (default)
+        LArgs la;
+        la.in_start = s->L_in_start, la.in_from = s->L_in_from, la.out_start = s->L_out_start;
+        la.out_to = s->L_out_to, la.cell = s->L_cell, la.pin = s->L_pin, la.flags = s->L_flags;
+        la.cap = s->L_cap, la.cell_delay = s->cell_delay, la.off = s->L_off, la.anchor = s->L_anchor;
+        la.xy = s->L_xy, la.r = s->r_unit, la.c = s->c_unit, la.clock = s->clock;
+        la.arr = s->L_arr, la.req = s->L_req, la.ak = s->L_ak, la.rk = s->L_rk, la.tie = s->L_tie;
+        la.pred = s->L_pred, la.akey = s->sta_akey, la.rkey = s->sta_rkey;
+        la.tie_list = s->tie_list, la.counters = s->counters;
+        const unsigned nbP = blocks_for(P, kBlock);
+        k_L_init<<<nbP, kBlock, 0, s->st>>>(P, la, !s->pin_xy_external, s->cell_xy, s->pin_xy);
+        for (int l = 0; l < s->L; ++l) {
+            const int lo = s->h_L_in_lo[l], hi = s->h_L_in_hi[l];
+            if (hi > lo) k_L_arr_push<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, la);
+        }
+        k_L_arr_decode<<<nbP, kBlock, 0, s->st>>>(P, la);
+        CK_LAUNCH();
+        for (int l = s->L - 1; l >= 0; --l) {
+            const int lo = s->h_L_in_lo[l], hi = s->h_L_in_hi[l];
+            if (hi > lo) k_L_req_push<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, la);
+        }
+        k_L_req_decode<<<nbP, kBlock, 0, s->st>>>(P, la);
+        k_L_to_pins<<<nbP, kBlock, 0, s->st>>>(P, la, !s->pin_xy_external, s->arr, s->req, s->ak, s->rk, s->tie,
+                                               s->pred, s->pin_xy);
+        CK_LAUNCH();
+    } else if (!all_levels_sweep()) { // push sweep over sink levels in pin order (see k_arr_push)
         k_sta_init<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, a, !s->pin_xy_external, s->pin_off, s->cell_xy,
                                                                  s->anchor, s->sta_akey, s->sta_rkey);
         for (int l = 0; l < s->L; ++l) {
