@@ -327,7 +327,6 @@ __global__ void __launch_bounds__(kBlock) k_L_arr_push(int lo, int hi, LArgs a)
     a.arr[t] = found ? best : 0.0;
     a.ak[t] = found ? 1 : 0;
     a.pred[t] = found ? bu : -1;
-    a.tie[t] = ntie > 1;
     if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = t;
     if (!found) return;
     const int o0 = a.out_start[t], o1 = a.out_start[t + 1];
@@ -344,12 +343,12 @@ __global__ void __launch_bounds__(kBlock) k_L_arr_decode(int P, LArgs a)
     const uint8_t f = a.flags[v];
     if (!(f & 4)) return; // Input pins were stored by the push
     if (f & 1) {
-        a.arr[v] = 0.0, a.ak[v] = 1, a.pred[v] = -1, a.tie[v] = 0;
+        a.arr[v] = 0.0, a.ak[v] = 1, a.pred[v] = -1;
         return;
     }
     const unsigned long long k = a.akey[v];
     if (k == kNoArr) {
-        a.arr[v] = 0.0, a.ak[v] = 0, a.pred[v] = -1, a.tie[v] = 0;
+        a.arr[v] = 0.0, a.ak[v] = 0, a.pred[v] = -1;
         return;
     }
     const double best = key_double(k), dcell = a.cell_delay[a.cell[v]];
@@ -362,7 +361,7 @@ __global__ void __launch_bounds__(kBlock) k_L_arr_decode(int P, LArgs a)
             ++ntie;
         }
     }
-    a.arr[v] = best, a.ak[v] = 1, a.pred[v] = bu, a.tie[v] = ntie > 1;
+    a.arr[v] = best, a.ak[v] = 1, a.pred[v] = bu;
     if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = v;
 }
 
@@ -407,18 +406,18 @@ __global__ void __launch_bounds__(kBlock) k_L_req_decode(int P, LArgs a)
 }
 
 // L-space results back to pin order; pred and tie-list entries become pin ids.
-__global__ void __launch_bounds__(kBlock) k_L_to_pins(int P, LArgs a, bool write_xy, double* __restrict__ arr,
+// (pin positions are rebuilt in pin order by the coalesced k_pin_xy instead of scattered from L_xy, and the
+// per-pin tie flags are never read back: ties travel in tie_list)
+__global__ void __launch_bounds__(kBlock) k_L_to_pins(int P, LArgs a, double* __restrict__ arr,
                                                       double* __restrict__ req, uint8_t* __restrict__ ak,
-                                                      uint8_t* __restrict__ rk, uint8_t* __restrict__ tie,
-                                                      int* __restrict__ pred, double2* __restrict__ pin_xy)
+                                                      uint8_t* __restrict__ rk, int* __restrict__ pred)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i < a.counters[0]) a.tie_list[i] = a.pin[a.tie_list[i]];
     if (i >= P) return;
     const int p = a.pin[i], q = a.pred[i];
-    arr[p] = a.arr[i], req[p] = a.req[i], ak[p] = a.ak[i], rk[p] = a.rk[i], tie[p] = a.tie[i];
+    arr[p] = a.arr[i], req[p] = a.req[i], ak[p] = a.ak[i], rk[p] = a.rk[i];
     pred[p] = q >= 0 ? a.pin[q] : -1;
-    if (write_xy) pin_xy[p] = a.xy[i];
 }
 
 // Grid-wide barrier for the persistent STA (all blocks co-resident: cooperative launch).  Arrival
@@ -771,8 +770,9 @@ void sta_record(tdpg_session* s, double* out3)
             if (hi > lo) k_L_req_push<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, la);
         }
         k_L_req_decode<<<nbP, kBlock, 0, s->st>>>(P, la);
-        k_L_to_pins<<<nbP, kBlock, 0, s->st>>>(P, la, !s->pin_xy_external, s->arr, s->req, s->ak, s->rk, s->tie,
-                                               s->pred, s->pin_xy);
+        k_L_to_pins<<<nbP, kBlock, 0, s->st>>>(P, la, s->arr, s->req, s->ak, s->rk, s->pred);
+        if (!s->pin_xy_external)
+            k_pin_xy<<<nbP, kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor, s->pin_xy);
         CK_LAUNCH();
     } else if (!all_levels_sweep()) { // push sweep over sink levels in pin order (see k_arr_push)
         k_sta_init<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, a, !s->pin_xy_external, s->pin_off, s->cell_xy,
