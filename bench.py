@@ -343,12 +343,13 @@ def run_ours(args):
     # e2e: the call a user makes — run_placement through the C-ABI (tdpg_place) on the same design and
     # schedule, `steps` iterations with a timing refresh every m, from pinned host positions to pinned
     # host positions + the per-iteration trace rows; wall clock over the whole call (device loop, its
-    # engine set-up, the final STA), max over ranks.
+    # engine set-up, the final STA), max over ranks; one untimed warm-up call first.
     C = d.n_cells
     hin = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
     hout = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
     hin.numpy()[:] = d.positions.reshape(-1)
     e2e_cfg = bench_config(args, args.steps)
+    s.place_host(e2e_cfg, hin.data_ptr(), hout.data_ptr())  # warm-up call (lazy module loads, first captures)
     barrier()
     t0 = time.perf_counter()
     e2e_rows, _ = s.place_host(e2e_cfg, hin.data_ptr(), hout.data_ptr())

@@ -270,8 +270,30 @@ void capture_iteration(tdpg_session* s, Engine& E)
 
 } // namespace
 
+// TDPG_TRACE_INIT=1: engine_init phase times on stderr (host clock, stream synchronised)
+struct InitTrace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t;
+    tdpg_session* s;
+    explicit InitTrace(tdpg_session* ss) : s(ss)
+    {
+        const char* e = std::getenv("TDPG_TRACE_INIT");
+        on = e && std::atoi(e) != 0;
+        t = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what)
+    {
+        if (!on) return;
+        cudaStreamSynchronize(s->st);
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "engine_init %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit)
 {
+    InitTrace tr(s);
     validate_config(*cfg);
     auto E = std::make_unique<Engine>();
     E->cfg = *cfg;
@@ -295,6 +317,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
         x = std::clamp(x, s->core[0], xh);
         y = std::clamp(y, s->core[1], yh);
     }
+    tr.mark("jitter (host)");
     upload_positions(s, xy.data());
     ensure_grid(s, cfg->grid_nx, cfg->grid_ny, cfg->target_density);
     set_density_model(s, cfg->density_model);
@@ -311,7 +334,9 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
         s->net_w.upload(ones, s->st);
     }
 
+    tr.mark("upload + grid + ledger");
     E->lambda = cfg->lambda0 > 0.0 ? cfg->lambda0 : lambda_auto(s, E->gamma, cfg->pp_loss);
+    tr.mark("lambda auto");
     E->lambda_cap = E->lambda * cfg->lambda_max;
 
     // per-iteration schedule (placer.cpp:470-471, :349-350, :477)
@@ -348,17 +373,23 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     }
     if (const char* se = std::getenv("TDPG_SORT_EVERY")) E->sort_every = std::max(1, std::atoi(se));
     // every buffer the graphs touch is sized before capture, so their pointers never move
+    tr.mark("schedule + buffers");
     refresh_reserve(s);
     s->pin_xy_external = false;
     sort_cells_spatial(s);
+    tr.mark("reserve + sort");
     delete s->eng;
+    tr.mark("old engine freed");
     s->eng = E.release();
     Engine& G = *s->eng;
     capture_iteration(s, G);
+    tr.mark("iteration graph");
     G.refresh_gexec = capture(s, [&] {
         refresh_record(s, G.ctrl, G.timing_row, G.cfg.w0, G.cfg.w1, G.cfg.net_weighting != 0);
     });
+    tr.mark("refresh graph");
     G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
+    tr.mark("sort graph");
     CK(cudaStreamSynchronize(s->st));
 }
 
