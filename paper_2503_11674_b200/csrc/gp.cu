@@ -178,20 +178,29 @@ __global__ void __launch_bounds__(kBlock, WA_MINB) k_wa_class(int blk0, const in
 // HPWL, the pin-pair value w·(dx² + dy²) and the linear-loss distance — is formed after exchanging the
 // partner's term with one shuffle, in the reference's operand order, so results are bitwise those of the
 // one-thread form.
+struct WaAxisArgs {
+    const int4* blk;
+    const int* net_by_size;
+    const int* e_cell;
+    const double *e_off, *cell_xy, *anchor, *net_w;
+    double inv_gamma;
+    double *grad_e, *part_wl, *part_hp;
+    PPArgs pp;
+    double* part_pp;
+};
+
 template <int N>
-__global__ void __launch_bounds__(2 * kBlock, (N <= 5 ? 2 : 1)) k_wa_axis(int blk0, const int4* __restrict__ blk,
-                                                        const int* __restrict__ net_by_size,
-                                                        const int* __restrict__ e_cell, const double* __restrict__ e_off,
-                                                        const double* __restrict__ cell_xy,
-                                                        const double* __restrict__ anchor,
-                                                        const double* __restrict__ net_w, double inv_gamma,
-                                                        double* __restrict__ grad_e, double* __restrict__ part_wl,
-                                                        double* __restrict__ part_hp, PPArgs pp,
-                                                        double* __restrict__ part_pp, const Ctrl* __restrict__ ctrl)
+__device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAxisArgs& A, double* sh)
 {
-    __shared__ double sh[2 * kBlock / 32];
-    if (ctrl && ctrl->stopped) return;
-    const int4 b = blk[blk0 + blockIdx.x]; // (N, first in net_by_size, count, entry base)
+    const int* __restrict__ net_by_size = A.net_by_size;
+    const int* __restrict__ e_cell = A.e_cell;
+    const double* __restrict__ e_off = A.e_off;
+    const double* __restrict__ cell_xy = A.cell_xy;
+    const double* __restrict__ anchor = A.anchor;
+    const double* __restrict__ net_w = A.net_w;
+    const double inv_gamma = A.inv_gamma;
+    double* __restrict__ grad_e = A.grad_e;
+    const PPArgs& pp = A.pp;
     const int t = threadIdx.x >> 1, axis = threadIdx.x & 1;
     const bool on = t < b.z;
     const int base = b.w + (on ? t : 0);
@@ -249,10 +258,41 @@ __global__ void __launch_bounds__(2 * kBlock, (N <= 5 ? 2 : 1)) k_wa_axis(int bl
     }
     const double bw = block_sum<2 * kBlock>(wl, sh);
     const double bh = block_sum<2 * kBlock>(hp, sh);
-    const double bp = part_pp ? block_sum<2 * kBlock>(ppv, sh) : 0.0;
+    const double bp = A.part_pp ? block_sum<2 * kBlock>(ppv, sh) : 0.0;
     if (threadIdx.x == 0) {
-        part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
-        if (part_pp) part_pp[blk0 + blockIdx.x] = bp;
+        A.part_wl[gblk] = bw, A.part_hp[gblk] = bh;
+        if (A.part_pp) A.part_pp[gblk] = bp;
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(2 * kBlock, (N <= 5 ? 2 : 1)) k_wa_axis(int blk0, WaAxisArgs A,
+                                                                          const Ctrl* __restrict__ ctrl)
+{
+    __shared__ double sh[2 * kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    wa_axis_block<N>(A.blk[blk0 + blockIdx.x], blk0 + blockIdx.x, A, sh);
+}
+
+// Several size classes in one launch (their blocks are contiguous in the table): each block dispatches
+// on its pin count; the register budget is the group's largest class.
+template <int LO, int HI, int MINB>
+__global__ void __launch_bounds__(2 * kBlock, MINB) k_wa_axis_group(int blk0, WaAxisArgs A,
+                                                                    const Ctrl* __restrict__ ctrl)
+{
+    __shared__ double sh[2 * kBlock / 32];
+    if (ctrl && ctrl->stopped) return;
+    const int g = blk0 + blockIdx.x;
+    const int4 b = A.blk[g];
+    switch (b.x) {
+    case 2: if (LO <= 2 && 2 <= HI) wa_axis_block<(LO <= 2 && 2 <= HI) ? 2 : LO>(b, g, A, sh); break;
+    case 3: if (LO <= 3 && 3 <= HI) wa_axis_block<(LO <= 3 && 3 <= HI) ? 3 : LO>(b, g, A, sh); break;
+    case 4: if (LO <= 4 && 4 <= HI) wa_axis_block<(LO <= 4 && 4 <= HI) ? 4 : LO>(b, g, A, sh); break;
+    case 5: if (LO <= 5 && 5 <= HI) wa_axis_block<(LO <= 5 && 5 <= HI) ? 5 : LO>(b, g, A, sh); break;
+    case 6: if (LO <= 6 && 6 <= HI) wa_axis_block<(LO <= 6 && 6 <= HI) ? 6 : LO>(b, g, A, sh); break;
+    case 7: if (LO <= 7 && 7 <= HI) wa_axis_block<(LO <= 7 && 7 <= HI) ? 7 : LO>(b, g, A, sh); break;
+    case 8: if (LO <= 8 && 8 <= HI) wa_axis_block<(LO <= 8 && 8 <= HI) ? 8 : LO>(b, g, A, sh); break;
+    default: break;
     }
 }
 
@@ -364,13 +404,42 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
                                  : entry_pos(e_cell[s0], e_off[s0], cell_xy, anchor);
             const double gx = wa_lane(p.x, on, inv_gamma, vx, hx);
             const double gy = wa_lane(p.y, on, inv_gamma, vy, hy);
-            if (on) grad_e[s0 + lane] = make_double2(w * gx, w * gy);
+            double ex = w * gx, ey = w * gy;
+            if (pp.w_e) { // pin pairs of the net (pin_pairs.cpp:17-49), one sink per lane
+                const double wt = (on && lane > 0) ? pp.w_e[s0 + lane] : 0.0;
+                const double pdx = __shfl_sync(0xffffffffu, p.x, 0), pdy = __shfl_sync(0xffffffffu, p.y, 0);
+                const double dx = p.x - pdx, dy = p.y - pdy;
+                double px = 0.0, py = 0.0, pv = 0.0;
+                if (wt != 0.0) {
+                    if (pp.kind == 0) {
+                        pv = wt * (dx * dx + dy * dy);
+                        px = 2.0 * wt * dx, py = 2.0 * wt * dy;
+                    } else {
+                        const double dist = sqrt(dx * dx + dy * dy);
+                        pv = wt * dist;
+                        if (dist > 0.0) px = wt * dx / dist, py = wt * dy / dist;
+                    }
+                    ex = ex + pp.beta * px, ey = ey + pp.beta * py;
+                }
+                // the driver's terms and the net's value in ascending sink pin id (gen_ord), as the
+                // reference accumulates them in map-key order
+                const int o = lane + 1 < n ? gen_ord[s0 + lane] : 0;
+                double sx = 0.0, sy = 0.0;
+                for (int k = 0; k + 1 < n; ++k) {
+                    const int j = __shfl_sync(0xffffffffu, o, k);
+                    const double gxj = __shfl_sync(0xffffffffu, px, j), gyj = __shfl_sync(0xffffffffu, py, j);
+                    const double vj = __shfl_sync(0xffffffffu, pv, j), wj = __shfl_sync(0xffffffffu, wt, j);
+                    if (lane == 0 && wj != 0.0) ppv += vj, sx -= gxj, sy -= gyj; // counted once, by the driver
+                }
+                if (lane == 0) ex = ex + pp.beta * sx, ey = ey + pp.beta * sy;
+            }
+            if (on) grad_e[s0 + lane] = make_double2(ex, ey);
         } else {
             wa_axis_warp(s0, n, 0, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vx, hx);
             wa_axis_warp(s0, n, 1, e_cell, e_off, cell_xy, anchor, inv_gamma, w, grad_e, vy, hy);
         }
         if (lane == 0) wl += w * (vx + vy), hp += hx + hy;
-        if (pp.w_e) { // rare large nets: lane 0 walks the sinks in ascending pin id
+        if (pp.w_e && n > 32) { // nets beyond a warp: lane 0 walks the sinks in ascending pin id
             __syncwarp();
             if (lane == 0) {
                 const double2 pd = entry_pos(e_cell[s0], e_off[s0], cell_xy, anchor);
@@ -1051,6 +1120,17 @@ void rebuild_pp_incidence(tdpg_session* s)
     CK_LAUNCH();
 }
 
+// TDPG_WA_GROUPS: 0 one launch per size class, 1 (default) classes 2-5 and 6-8 in two launches, 2 all
+// in one (measured at 1M: 0.301 / 0.296 / 0.334 ms per iteration).
+inline int wa_groups()
+{
+    static const int g = [] {
+        const char* e = std::getenv("TDPG_WA_GROUPS");
+        return e ? std::atoi(e) : 1;
+    }();
+    return g;
+}
+
 // TDPG_WA_AXIS=0 selects the one-thread-per-net class kernels (A/B switch).
 inline bool wa_axis_split()
 {
@@ -1059,6 +1139,17 @@ inline bool wa_axis_split()
         return !(e && std::atoi(e) == 0);
     }();
     return on;
+}
+
+WaAxisArgs wa_axis_args(tdpg_session* s, const double* nw, double inv_gamma, double* pw, double* ph, const PPArgs& pp,
+                        double* ppart)
+{
+    WaAxisArgs A;
+    A.blk = s->wa_blk, A.net_by_size = s->net_by_size, A.e_cell = s->e_cell;
+    A.e_off = reinterpret_cast<const double*>(s->e_off.p), A.cell_xy = reinterpret_cast<const double*>(s->cell_xy.p);
+    A.anchor = reinterpret_cast<const double*>(s->anchor.p), A.net_w = nw, A.inv_gamma = inv_gamma;
+    A.grad_e = reinterpret_cast<double*>(s->grad_e.p), A.part_wl = pw, A.part_hp = ph, A.pp = pp, A.part_pp = ppart;
+    return A;
 }
 
 // The class's block range clipped to this rank's partition [part_b0, part_b1) (whole design at world 1).
@@ -1077,11 +1168,7 @@ void launch_wa_class(tdpg_session* s, const double* nw, double inv_gamma, double
     int b0, nb;
     if (!wa_range(s, N, b0, nb)) return;
     if (wa_axis_split()) {
-        k_wa_axis<N><<<nb, 2 * kBlock, 0, st>>>(b0, s->wa_blk, s->net_by_size, s->e_cell,
-                                                reinterpret_cast<const double*>(s->e_off.p),
-                                                reinterpret_cast<const double*>(s->cell_xy.p),
-                                                reinterpret_cast<const double*>(s->anchor.p), nw, inv_gamma,
-                                                reinterpret_cast<double*>(s->grad_e.p), pw, ph, pp, ppart, ctrl);
+        k_wa_axis<N><<<nb, 2 * kBlock, 0, st>>>(b0, wa_axis_args(s, nw, inv_gamma, pw, ph, pp, ppart), ctrl);
         CK_LAUNCH();
         return;
     }
@@ -1104,6 +1191,24 @@ void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double*
     if (pp_fused) pp = PPArgs{s->pp_mask.p, s->pp_ord.p, s->ppw_e.p, beta, kind};
     double* ppart = pp_fused ? part_pp : nullptr;
     auto st = [&](int k) { return n_branch > 0 ? branch[k % n_branch] : s->st; };
+    const int groups = wa_groups();
+    if (groups > 0 && wa_axis_split()) { // size classes merged into one or two launches
+        const WaAxisArgs A = wa_axis_args(s, nw, ig, part_wl, part_hp, pp, ppart);
+        auto range = [&](int lo, int hi, int& b0, int& nb) {
+            const int plo = s->part_active ? s->part_b0 : 0, phi = s->part_active ? s->part_b1 : s->n_wa_blocks;
+            b0 = std::max(s->wa_cls_blk0[lo], plo);
+            nb = std::min(s->wa_cls_blk0[hi] + s->wa_cls_nblk[hi], phi) - b0;
+            return nb > 0;
+        };
+        int b0, nb;
+        if (groups == 1) {
+            if (range(2, 5, b0, nb)) k_wa_axis_group<2, 5, 2><<<nb, 2 * kBlock, 0, st(1)>>>(b0, A, ctrl);
+            if (range(6, 8, b0, nb)) k_wa_axis_group<6, 8, 1><<<nb, 2 * kBlock, 0, st(2)>>>(b0, A, ctrl);
+        } else {
+            if (range(2, 8, b0, nb)) k_wa_axis_group<2, 8, 1><<<nb, 2 * kBlock, 0, st(1)>>>(b0, A, ctrl);
+        }
+        CK_LAUNCH();
+    } else {
     launch_wa_class<2>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(1));
     launch_wa_class<3>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(2));
     launch_wa_class<4>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(3));
@@ -1111,6 +1216,7 @@ void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double*
     launch_wa_class<6>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(5));
     launch_wa_class<7>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(6));
     launch_wa_class<8>(s, nw, ig, part_wl, part_hp, pp, ppart, ctrl, st(7));
+    }
     int g0, gn;
     if (wa_range(s, 0, g0, gn)) {
         k_wa_generic<<<gn, kBlock, 0, st(0)>>>(g0, s->wa_blk, s->net_by_size,

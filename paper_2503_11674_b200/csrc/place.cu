@@ -37,7 +37,7 @@ struct Engine {
     cudaGraphExec_t gexec = nullptr;
     int launched = 0, refreshes = 0;
     long long kernel_launches = 0;
-    int kernels_per_iter = 13; // 7 WA classes + generic + scatter + bins + finalize + dens_grad + cells (max)
+    int kernels_per_iter = 8; // 2 WA class groups + generic + scatter + bins + dens_grad + finalize + cells
     cudaGraphExec_t refresh_gexec = nullptr; // the whole timing refresh, captured once
     cudaGraphExec_t sort_gexec = nullptr;    // spatial re-sort of the cells
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
