@@ -10,7 +10,7 @@ import math
 
 import numpy as np
 
-from fixtures import make_diamond, make_t1, make_t2, make_trunk16
+from fixtures import IN, OUT, MT64, Builder, make_diamond, make_t1, make_t2, make_trunk16, random_design
 
 
 def _pin(d, name):
@@ -209,5 +209,167 @@ def check_topn_trunk16(B):
     assert len(paths) == 16 and all(sl[i - 1] <= sl[i] for i in range(1, 16))
 
 
-ALL = [check_k_worst_diamond, check_k_worst_refuses_non_endpoint, check_topn_t2, check_topn_trunk16, check_schedule, check_t1_sta, check_t2_sta, check_t1_graph, check_diamond_paths, check_t2_endpoint, check_trunk16,
+def _two_pin(a, b, cap, r, c):
+    bd = Builder((0, 0, 10, 10), 1e9, r, c)
+    s = bd.terminal("S", a, OUT)
+    e = bd.terminal("E", b, IN, cap)
+    bd.cell("u", 1, 1, 1.0, (5, 5))
+    bd.src.append(s), bd.eps.append(e)
+    bd.net("n", s, [e])
+    return bd.finish()
+
+
+def check_net_delay(B):
+    """test_sta.cpp:23-36 — (0,0)->(3,4), r=2, c=3, cap 0.5 -> 301; L = 0 -> 0; doubled L -> 4x delay."""
+    assert B(_two_pin((0, 0), (3, 4), 0.5, 2.0, 3.0)).sta()["arr"][1] == 301.0
+    assert B(_two_pin((5, 5), (5, 5), 2.0, 2.0, 3.0)).sta()["arr"][1] == 0.0
+    d1 = B(_two_pin((0, 0), (1, 2), 0.0, 2.0, 3.0)).sta()["arr"][1]
+    d2 = B(_two_pin((0, 0), (2, 4), 0.0, 2.0, 3.0)).sta()["arr"][1]
+    assert abs(d2 - 4.0 * d1) <= 1e-12 * d2
+
+
+def check_register_cut(B):
+    """test_sta.cpp:105-129 — arrival restarts at the register: d 4, q 0, po 256; slack 1 / -251."""
+    bd = Builder((0, 0, 10, 10), 5.0, 1.0, 1.0)
+    r = bd.cell("r0", 1, 1, 1.0, (1, 1))
+    s = bd.terminal("pi", (0, 0), OUT)
+    dp, qp = bd.pin("r0.d", r, IN), bd.pin("r0.q", r, OUT)
+    po = bd.terminal("po", (9, 9), IN)
+    bd.net("n0", s, [dp]), bd.net("n1", qp, [po])
+    bd.src += [s, qp]
+    bd.eps += [dp, po]
+    t = B(bd.finish()).sta()
+    assert t["arr"][dp] == 4.0 and t["arr"][qp] == 0.0 and t["arr"][po] == 256.0
+    assert t["slack"][dp] == 1.0 and t["slack"][po] == -251.0 and t["tns"] == -251.0 and t["wns"] == -251.0
+
+
+def check_unreachable_flags(B):
+    """test_sta.cpp:131-155 — a pin no source reaches: arr 0 unknown, req = clock unknown."""
+    bd = Builder((0, 0, 10, 10), 5.0, 1.0, 1.0)
+    c0 = bd.cell("u0", 1, 1, 1.0, (1, 1))
+    bd.cell("u1", 1, 1, 1.0, (2, 2))
+    s = bd.terminal("pi", (0, 0), OUT)
+    i0, o0 = bd.pin("u0.a", c0, IN), bd.pin("u0.o", c0, OUT)
+    dang = bd.pin("u1.o", 1, OUT)
+    po = bd.terminal("po", (3, 3), IN)
+    bd.net("n0", s, [i0]), bd.net("n1", o0, [po])
+    bd.src.append(s), bd.eps.append(po)
+    t = B(bd.finish()).sta()
+    assert not t["arr_known"][dang] and t["arr"][dang] == 0.0
+    assert not t["req_known"][dang] and t["req"][dang] == 5.0
+    assert t["arr_known"][po] and t["req_known"][s]
+
+
+def check_clock_shift(B):
+    """test_sta.cpp:189-203 — +2.5 on the clock moves required and slack only; tns -3, wns -2.5."""
+    d = make_t2()
+    base = B(d).sta()
+    d.clock_period += 2.5
+    sh = B(d).sta()
+    assert np.array_equal(sh["arr"], base["arr"])
+    assert np.max(np.abs(sh["req"] - (base["req"] + 2.5))) <= 1e-12
+    assert np.max(np.abs(sh["slack"] - (base["slack"] + 2.5))) <= 1e-12
+    assert sh["tns"] == -3.0 and sh["wns"] == -2.5
+
+
+def check_shared_arc_hits(B):
+    """test_paths.cpp:213-230 — diamond k = 2: 6 hits, the merge arc (7, 8) hit once per path."""
+    d = make_diamond()
+    d.clock_period = 1.0  # both diamond paths violate, so the endpoint report carries them with k = 2
+    r = B(d).extract(n=1, k=2)
+    a, b, sl = r["hits"]
+    assert len(a) == 6 and all(x < y for x, y in zip(a, b))
+    merge = [s for x, y, s in zip(a, b, sl) if (x, y) == (7, 8)]
+    assert len(merge) == 2 and sorted(merge) == sorted(r["slack"].tolist())
+
+
+def _pins_rng(rng, n, span=20.0):
+    return np.array([[rng.uniform(0.0, span), rng.uniform(0.0, span)] for _ in range(n)])
+
+
+def check_wa_smoothing_bound(B):
+    """test_placer.cpp:67-93 — 0 <= HPWL - WA <= 2 gamma ln p per dimension (summed for both)."""
+    rng = MT64(11)
+    gamma = 0.01 * 20.0
+    for _ in range(60):
+        p = rng.randint(2, 12)
+        pins = _pins_rng(rng, p)
+        bound = 2.0 * gamma * math.log(p)
+        for dim in (0, 1):
+            flat = pins.copy()
+            flat[:, 1 - dim] = 0.0
+            wa, _ = B.wa(flat, gamma)
+            hp = flat[:, dim].max() - flat[:, dim].min()
+            assert 0.0 <= hp - wa <= bound + 1e-12
+        wa2, _ = B.wa(pins, gamma)
+        hp2 = np.ptp(pins[:, 0]) + np.ptp(pins[:, 1])
+        assert -1e-12 <= hp2 - wa2 <= 2.0 * bound + 1e-12
+
+
+def check_wa_translation_invariance(B):
+    """test_placer.cpp:95-119 — integer coordinates and shifts: the anchored WA is bit-exact."""
+    rng = MT64(12)
+    for _ in range(30):
+        p = rng.randint(2, 8)
+        pins = np.array([[float(rng.randint(0, 64)), float(rng.randint(0, 64))] for _ in range(p)])
+        base, _ = B.wa(pins, 0.37)
+        dx, dy = float(rng.randint(-1024, 1024)), float(rng.randint(-1024, 1024))
+        moved, _ = B.wa(pins + np.array([dx, dy]), 0.37)
+        assert moved == base
+
+
+def _one_cell(w=1.0, h=1.0, fixed=()):
+    bd = Builder((0, 0, 20, 20), 1e9, 1.0, 1.0)
+    s = bd.terminal("S", (0, 0), OUT)
+    e = bd.terminal("E", (20, 20), IN)
+    bd.src.append(s), bd.eps.append(e)
+    bd.net("n", s, [e])
+    for i, fx in enumerate(fixed or (False,)):
+        bd.cell(f"u{i}", w, h, 1.0, (9.0, 9.0), fixed=fx)
+    return bd.finish()
+
+
+def _approx(a, b, eps):
+    """doctest::Approx(b).epsilon(eps): |a - b| < eps * (1 + max(|a|, |b|))."""
+    return abs(a - b) < eps * (1.0 + max(abs(a), abs(b)))
+
+
+def check_density_properties(B):
+    """test_placer.cpp:160-268 — uncrowded -> 0; mirror symmetry; whole-bin shift invariance; fixed
+    cells add occupancy, never a gradient; overflow grows with crowding."""
+    d = _one_cell()
+    v, o, g = B(d).density(np.array([[9.5, 9.5]]), nx=4, ny=4, td=0.9)
+    assert v == 0.0 and o == 0.0 and g[0, 0] == 0.0 and g[0, 1] == 0.0
+    for x in (3.25, 6.5, 8.0):
+        mx = 20.0 - 1.0 - x
+        va, _, ga = B(d).density(np.array([[x, 7.0]]), nx=4, ny=4, td=1e-4)
+        vb, _, gb = B(d).density(np.array([[mx, 7.0]]), nx=4, ny=4, td=1e-4)
+        assert va > 0.0 and _approx(va, vb, 1e-12)
+        assert _approx(ga[0, 0], -gb[0, 0], 1e-12) and _approx(ga[0, 1], gb[0, 1], 1e-12)
+    va, _, ga = B(d).density(np.array([[7.0, 9.0]]), nx=8, ny=8, td=1e-4)
+    vb, _, gb = B(d).density(np.array([[9.5, 9.0]]), nx=8, ny=8, td=1e-4)
+    assert va > 0.0 and _approx(va, vb, 1e-12) and _approx(ga[0, 0], gb[0, 0], 1e-9)
+    both = _one_cell(2.0, 2.0, fixed=(False, True))
+    vf, _, gf = B(both).density(np.array([[9.0, 9.0], [9.0, 9.0]]), nx=4, ny=4, td=0.02)
+    solo = _one_cell(2.0, 2.0)
+    vs, _, _ = B(solo).density(np.array([[9.0, 9.0]]), nx=4, ny=4, td=0.02)
+    assert gf[1, 0] == 0.0 and gf[1, 1] == 0.0 and vf > vs
+    four = _one_cell(4.0, 4.0, fixed=(False,) * 4)
+    pa, oa, _ = B(four).density(np.array([[8.0, 8.0]] * 4), nx=4, ny=4, td=0.3)
+    pb, ob, _ = B(four).density(np.array([[1, 1], [14, 1], [1, 14], [14, 14]], dtype=float), nx=4, ny=4, td=0.3)
+    assert oa > ob and pa > pb and oa > 0.0
+
+
+def check_beta_zero_reduction(B):
+    """test_placer.cpp:434-451 — with beta = 0 the objective equals the pair-free one, bit for bit."""
+    d = random_design(9)
+    led = ([0], [1], [10.0]) if d.n_pins > 1 else None
+    t0, g0 = B(d).objective(nx=8, ny=8, td=0.05, gamma=0.3, lam=0.7, beta=0.0, ledger=led)
+    t1, g1 = B(d).objective(nx=8, ny=8, td=0.05, gamma=0.3, lam=0.7, beta=0.0, ledger=None)
+    assert np.array_equal(t0[[0, 1, 2, 4, 5]], t1[[0, 1, 2, 4, 5]]) and np.array_equal(g0, g1)
+
+
+ALL = [check_net_delay, check_register_cut, check_unreachable_flags, check_clock_shift, check_shared_arc_hits,
+       check_wa_smoothing_bound, check_wa_translation_invariance, check_density_properties,
+       check_beta_zero_reduction, check_k_worst_diamond, check_k_worst_refuses_non_endpoint, check_topn_t2, check_topn_trunk16, check_schedule, check_t1_sta, check_t2_sta, check_t1_graph, check_diamond_paths, check_t2_endpoint, check_trunk16,
        check_t1_pairs, check_t1_hpwl, check_wa_closed_form, check_pp_hand_values, check_ledger, check_adam]
