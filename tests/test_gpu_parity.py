@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import kat
-from fixtures import make_t1, make_trunk16, random_design, spread_positions
+from fixtures import MT64, make_t1, make_trunk16, random_design, spread_positions
 from oracle.oracle import Oracle, RefOracle
 
 pytestmark = pytest.mark.gpu
@@ -300,3 +300,40 @@ def test_large_kbest_extraction_bitwise():
     es, eo = s.extract(xy, n=5000, k=4), o.extract(xy, n=5000, k=4)
     assert es["n_paths"] > 5000
     _same_report(es, eo, "200k k=4")
+
+
+def _max_grad_error(f, pos, grad, h):
+    """oracles.hpp:155-179: relative error against central differences, floored at 1e-3 x field scale."""
+    scale = float(np.max(np.abs(grad))) if grad.size else 0.0
+    floor = max(1e-3 * scale, 1e-12)
+    worst = 0.0
+    for i in range(grad.shape[0]):
+        for ax in (0, 1):
+            p, m = pos.copy(), pos.copy()
+            p[i, ax] += h
+            m[i, ax] -= h
+            fd = (f(p) - f(m)) / (2.0 * h)
+            an = grad[i, ax]
+            worst = max(worst, abs(fd - an) / max(abs(fd), abs(an), floor))
+    return worst
+
+
+@pytest.mark.parametrize("seed", range(1, 13))
+def test_objective_gradient_finite_differences(seed):
+    """test_placer.cpp:453-479 on the device: WA + pin pairs (quadratic / linear) + density, kFdH = 2e-4,
+    kGradTol = 1e-4."""
+    d = random_design(seed)
+    rng = MT64(37 + seed)
+    a, b, w = [], [], []
+    for _ in range(6):
+        x, y = rng.randint(0, d.n_pins - 1), rng.randint(0, d.n_pins - 1)
+        if x != y and (min(x, y), max(x, y)) not in zip(a, b):
+            a.append(min(x, y)), b.append(max(x, y)), w.append(rng.uniform(1.0, 20.0))
+    order = np.lexsort((b, a))
+    led = (np.array(a)[order], np.array(b)[order], np.array(w)[order])
+    kind = 0 if seed % 2 == 0 else 1
+    s = Session(d)
+    args = dict(nx=8, ny=8, td=0.05, gamma=0.2, lam=0.7, beta=0.3, kind=kind, ledger=led)
+    _, g = s.objective(d.positions, **args)
+    f = lambda xy: s.objective(xy, **args)[0][0]  # noqa: E731
+    assert _max_grad_error(f, d.positions.copy(), g, 1e-5 * 20.0) <= 1e-4
