@@ -551,7 +551,6 @@ __global__ void __launch_bounds__(kBlock) k_pin_pairs(const int* __restrict__ n_
 // hence run-to-run deterministic).  Bins: excess = max(0, occ - cap), value / overflow
 // partial sums, accumulators reset for the next evaluation.
 // =====================================================================================
-constexpr int kFootCache = 16;
 
 // Scatter over cells in spatial order (perm, refreshed by sort_cells_spatial): the block's
 // footprints usually cover a small window of bins, which is accumulated in shared memory

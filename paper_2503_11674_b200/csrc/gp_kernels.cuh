@@ -8,7 +8,6 @@
 namespace tdpg {
 
 constexpr int kBlock = 256;
-constexpr int kWaRegPins = 8; // nets up to this size keep pins/exps in registers
 
 __device__ __forceinline__ double2 entry_pos(int ec, double2 off, const double2* __restrict__ cell_xy,
                                              const double2* __restrict__ anchor)
@@ -26,77 +25,10 @@ __device__ __forceinline__ double2 pin_pos(int p, const int* __restrict__ pin_ce
     return make_double2(a.x + o.x, a.y + o.y);
 }
 
-// ---- bspline footprint (density.cpp:13-49) ---------------------------------------
-__device__ __forceinline__ double bspline2(double u)
-{
-    const double a = fabs(u);
-    if (a >= 1.5) return 0.0;
-    if (a <= 0.5) return 0.75 - a * a;
-    const double t = 1.5 - a;
-    return 0.5 * t * t;
-}
-
-__device__ __forceinline__ double bspline2_integral(double u)
-{
-    if (u <= -1.5) return 0.0;
-    if (u >= 1.5) return 1.0;
-    if (u <= -0.5) {
-        const double t = u + 1.5;
-        return t * t * t / 6.0;
-    }
-    if (u <= 0.5) return 0.5 + 0.75 * u - u * u * u / 3.0;
-    const double t = 1.5 - u;
-    return 1.0 - t * t * t / 6.0;
-}
-
-__device__ __forceinline__ double extent_weight(double lo, double hi, double c, double h)
-{
-    return (bspline2_integral((hi - c) / h) - bspline2_integral((lo - c) / h)) * h / (hi - lo);
-}
-
-__device__ __forceinline__ double extent_weight_grad(double lo, double hi, double c, double h)
-{
-    return (bspline2((hi - c) / h) - bspline2((lo - c) / h)) / (hi - lo);
-}
-
 struct GridDev {
     int nx, ny;
     double x0, y0, bw, bh, cap, scale, inv_scale, total_movable, inv_bw, inv_bh;
 };
-
-// bspline2 / bspline2_integral (density.cpp:15-36), divisions by 6 and 3 as reciprocal multiplies,
-// evaluated branch-free: every piece is computed and the right one selected (same formula per piece,
-// so the selected value is unchanged; lanes of a warp no longer diverge on the bin position).
-__device__ __forceinline__ double bspline2_bf(double u)
-{
-    const double a = fabs(u);
-    const double t = 1.5 - a;
-    const double inner = 0.75 - a * a, outer = 0.5 * t * t;
-    return a >= 1.5 ? 0.0 : (a <= 0.5 ? inner : outer);
-}
-
-__device__ __forceinline__ double bspline2_integral_r(double u)
-{
-    constexpr double kSixth = 1.0 / 6.0, kThird = 1.0 / 3.0;
-    const double t1 = u + 1.5, t3 = 1.5 - u;
-    const double left = t1 * t1 * t1 * kSixth;
-    const double mid = 0.5 + 0.75 * u - u * u * u * kThird;
-    const double right = 1.0 - t3 * t3 * t3 * kSixth;
-    const double r = u <= -0.5 ? left : (u <= 0.5 ? mid : right);
-    return u <= -1.5 ? 0.0 : (u >= 1.5 ? 1.0 : r);
-}
-
-// extent_weight + extent_weight_grad (density.cpp:41-49) for one bin centre c, with the
-// per-cell reciprocal of the extent and the grid's reciprocal pitch.
-__device__ __forceinline__ void extent_w(double lo, double hi, double c, double h, double inv_h, double inv_len,
-                                         double& w, double& dw)
-{
-    const double uh = (hi - c) * inv_h, ul = (lo - c) * inv_h;
-    w = (bspline2_integral_r(uh) - bspline2_integral_r(ul)) * h * inv_len;
-    dw = (bspline2_bf(uh) - bspline2_bf(ul)) * inv_len;
-}
-
-constexpr int kFoot = 7; // footprint bins per dimension kept in registers (wider footprints loop)
 
 // Footprint of one cell along one axis (extent_weight / extent_weight_grad, density.cpp:41-49, and the
 // bin range, :109-112) in three-point form.  Bin centres step by one pitch, so u = (edge - c_j) / pitch
@@ -194,25 +126,6 @@ __device__ __forceinline__ bool axis5(double lo, double hi, double origin, doubl
     }
     b = al;
     return true;
-}
-
-// Footprint bin range (density.cpp:109-112) with reciprocal pitch; bins at the range ends
-// carry zero weight, so a one-bin difference from the division form changes nothing.
-__device__ __forceinline__ void foot_range(double lo, double hi, double origin, double pitch, double inv_pitch,
-                                           int nbins, int& b0, int& b1)
-{
-    b0 = max(0, static_cast<int>(floor((lo - 1.5 * pitch - origin) * inv_pitch - 0.5)));
-    b1 = min(nbins - 1, static_cast<int>(ceil((hi + 1.5 * pitch - origin) * inv_pitch - 0.5)));
-}
-
-// Footprint bin range of a movable cell (density.cpp:109-112).
-__device__ __forceinline__ void footprint_range(const GridDev& g, double xl, double xh, double yl, double yh, int& bx0,
-                                                int& bx1, int& by0, int& by1)
-{
-    bx0 = max(0, static_cast<int>(floor((xl - 1.5 * g.bw - g.x0) / g.bw - 0.5)));
-    bx1 = min(g.nx - 1, static_cast<int>(ceil((xh + 1.5 * g.bw - g.x0) / g.bw - 0.5)));
-    by0 = max(0, static_cast<int>(floor((yl - 1.5 * g.bh - g.y0) / g.bh - 0.5)));
-    by1 = min(g.ny - 1, static_cast<int>(ceil((yh + 1.5 * g.bh - g.y0) / g.bh - 0.5)));
 }
 
 struct IterCur { // schedule values of the iteration being executed
