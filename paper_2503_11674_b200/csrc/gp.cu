@@ -218,7 +218,8 @@ __device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAx
     const int i_net = b.y + (on ? t : 0);
     const double w = net_w ? net_w[net_by_size[i_net]] : 1.0;
     double wl = 0.0, hp = 0.0, ppv = 0.0;
-    if (on && axis == 0) wl = w * (v + v_other), hp = ext + e_other;
+    if (on && axis == 0) wl = w * (v + v_other);   // w (vx + vy), on the x thread
+    if (on && axis == 1) hp = e_other + ext;        // hx + hy, on the y thread (see the reduction below)
     const uint32_t mask = (on && pp.mask) ? pp.mask[i_net] : 0u;
     double p[N];
 #pragma unroll
@@ -256,12 +257,33 @@ __device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAx
         for (int i = 0; i < N; ++i) // fold term pin_grad + beta * pp.d_pin (placer.cpp:323)
             grad_e[2 * (base + i * kBlock) + axis] = mask ? w * g[i] + pp.beta * p[i] : w * g[i];
     }
-    const double bw = block_sum<2 * kBlock>(wl, sh);
-    const double bh = block_sum<2 * kBlock>(hp, sh);
-    const double bp = A.part_pp ? block_sum<2 * kBlock>(ppv, sh) : 0.0;
-    if (threadIdx.x == 0) {
-        A.part_wl[gblk] = bw, A.part_hp[gblk] = bh;
-        if (A.part_pp) A.part_pp[gblk] = bp;
+    // block partials of (WA, HPWL, pair value) in one fixed-order tree: the net terms live on the
+    // axis-0 (even) lanes, so even lanes carry WA and the pair value and odd lanes the HPWL through a
+    // parity-preserving butterfly (offsets 16..2), then 16 warps x 3 values in one shared round
+    double r1 = axis == 0 ? wl : hp, r2 = ppv;
+#pragma unroll
+    for (int o = 16; o > 1; o >>= 1) {
+        r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    }
+    double* s3 = sh; // [3][16]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) s3[wid] = r1, s3[32 + wid] = r2;
+    if (lane == 1) s3[16 + wid] = r1;
+    __syncthreads();
+    if (wid == 0) {
+        double a = lane < 16 ? s3[lane] : s3[lane]; // lanes 0..15: WA, 16..31: HPWL
+        double c = lane < 16 ? s3[32 + lane] : 0.0;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0) {
+            A.part_wl[gblk] = a;
+            if (A.part_pp) A.part_pp[gblk] = c;
+        }
+        if (lane == 16) A.part_hp[gblk] = a;
     }
 }
 
@@ -269,7 +291,7 @@ template <int N>
 __global__ void __launch_bounds__(2 * kBlock, (N <= 5 ? 2 : 1)) k_wa_axis(int blk0, WaAxisArgs A,
                                                                           const Ctrl* __restrict__ ctrl)
 {
-    __shared__ double sh[2 * kBlock / 32];
+    __shared__ double sh[48];
     if (ctrl && ctrl->stopped) return;
     wa_axis_block<N>(A.blk[blk0 + blockIdx.x], blk0 + blockIdx.x, A, sh);
 }
@@ -280,7 +302,7 @@ template <int LO, int HI, int MINB>
 __global__ void __launch_bounds__(2 * kBlock, MINB) k_wa_axis_group(int blk0, WaAxisArgs A,
                                                                     const Ctrl* __restrict__ ctrl)
 {
-    __shared__ double sh[2 * kBlock / 32];
+    __shared__ double sh[48];
     if (ctrl && ctrl->stopped) return;
     const int g = blk0 + blockIdx.x;
     const int4 b = A.blk[g];
