@@ -141,6 +141,22 @@ __device__ __forceinline__ double block_sum(double v, double* sh)
     return r;
 }
 
+// Three deterministic block sums in one shared round (results valid in thread 0); sh >= 3 * BLOCK / 32.
+template <int BLOCK>
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* sh)
+{
+    a = warp_sum(a), b = warp_sum(b), c = warp_sum(c);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int NW = BLOCK / 32;
+    if (lane == 0) sh[w] = a, sh[NW + w] = b, sh[2 * NW + w] = c;
+    __syncthreads();
+    if (w == 0) {
+        a = warp_sum(lane < NW ? sh[lane] : 0.0);
+        b = warp_sum(lane < NW ? sh[NW + lane] : 0.0);
+        c = warp_sum(lane < NW ? sh[2 * NW + lane] : 0.0);
+    }
+}
+
 // Orderable 64-bit key of a double (ascending key == ascending value, -0 < +0).
 __device__ __forceinline__ uint64_t double_key(double d)
 {

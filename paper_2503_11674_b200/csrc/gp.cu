@@ -391,6 +391,80 @@ __device__ __forceinline__ double wa_lane(double x, bool on, double inv_gamma, d
            (el * is_min) * (1.0 - ((x - lo) - min_term) * inv_gamma);
 }
 
+// wa_lane over a W-lane segment of the warp (W = 16: two nets per warp).
+template <int W>
+__device__ __forceinline__ double wa_lane_w(double x, bool on, double inv_gamma, double& value, double& extent)
+{
+    double hi = x, lo = x;
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+        hi = smax(hi, __shfl_xor_sync(0xffffffffu, hi, o, W));
+        lo = smin(lo, __shfl_xor_sync(0xffffffffu, lo, o, W));
+    }
+    const double eu = on ? exp((x - hi) * inv_gamma) : 0.0;
+    const double el = on ? exp(-(x - lo) * inv_gamma) : 0.0;
+    double s_max = eu, t_max = (x - hi) * eu, s_min = el, t_min = (x - lo) * el;
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+        s_max += __shfl_xor_sync(0xffffffffu, s_max, o, W), t_max += __shfl_xor_sync(0xffffffffu, t_max, o, W);
+        s_min += __shfl_xor_sync(0xffffffffu, s_min, o, W), t_min += __shfl_xor_sync(0xffffffffu, t_min, o, W);
+    }
+    const double is_max = 1.0 / s_max, is_min = 1.0 / s_min;
+    const double max_term = t_max * is_max, min_term = t_min * is_min;
+    value = (hi - lo) + (max_term - min_term);
+    extent = hi - lo;
+    return (eu * is_max) * (1.0 + ((x - hi) - max_term) * inv_gamma) -
+           (el * is_min) * (1.0 - ((x - lo) - min_term) * inv_gamma);
+}
+
+// One net of <= 16 pins per half-warp (lane `sub` of the segment holds pin `sub`): WA both axes and the
+// net's pin pairs, the driver's pair terms summed in ascending sink pin id (kmax: the longer net of the
+// two segments, so every lane runs the same shuffles).
+__device__ __forceinline__ void wa_half_net(int sub, int s0, int n, int kmax, double w, const int* __restrict__ e_cell,
+                                            const double2* __restrict__ e_off, const double2* __restrict__ cell_xy,
+                                            const double2* __restrict__ anchor, double inv_gamma,
+                                            double2* __restrict__ grad_e, const PPArgs& pp,
+                                            const int* __restrict__ gen_ord, double& wl, double& hp, double& ppv)
+{
+    const bool live = n >= 2; // single-pin nets: zero gradient, no terms (wirelength.cpp:53)
+    const bool on = live ? sub < n : sub == 0;
+    // lanes past the net hold its first pin, so they leave the max / min butterflies unchanged
+    const int q = sub < n ? sub : 0;
+    const double2 p = n > 0 ? entry_pos(e_cell[s0 + q], e_off[s0 + q], cell_xy, anchor) : make_double2(0.0, 0.0);
+    double vx, vy, hx, hy;
+    const double gx = wa_lane_w<16>(p.x, on, inv_gamma, vx, hx);
+    const double gy = wa_lane_w<16>(p.y, on, inv_gamma, vy, hy);
+    double ex = w * gx, ey = w * gy;
+    if (pp.w_e) {
+        const double wt = (live && on && sub > 0) ? pp.w_e[s0 + sub] : 0.0;
+        const double pdx = __shfl_sync(0xffffffffu, p.x, 0, 16), pdy = __shfl_sync(0xffffffffu, p.y, 0, 16);
+        const double dx = p.x - pdx, dy = p.y - pdy;
+        double px = 0.0, py = 0.0, pv = 0.0;
+        if (wt != 0.0) {
+            if (pp.kind == 0) {
+                pv = wt * (dx * dx + dy * dy);
+                px = 2.0 * wt * dx, py = 2.0 * wt * dy;
+            } else {
+                const double dist = sqrt(dx * dx + dy * dy);
+                pv = wt * dist;
+                if (dist > 0.0) px = wt * dx / dist, py = wt * dy / dist;
+            }
+            ex = ex + pp.beta * px, ey = ey + pp.beta * py;
+        }
+        const int o = (live && sub + 1 < n) ? gen_ord[s0 + sub] : 0;
+        double sx = 0.0, sy = 0.0;
+        for (int k = 0; k < kmax; ++k) {
+            const int j = __shfl_sync(0xffffffffu, o, k, 16);
+            const double gxj = __shfl_sync(0xffffffffu, px, j, 16), gyj = __shfl_sync(0xffffffffu, py, j, 16);
+            const double vj = __shfl_sync(0xffffffffu, pv, j, 16), wj = __shfl_sync(0xffffffffu, wt, j, 16);
+            if (sub == 0 && k + 1 < n && wj != 0.0) ppv += vj, sx -= gxj, sy -= gyj;
+        }
+        if (sub == 0) ex = ex + pp.beta * sx, ey = ey + pp.beta * sy;
+    }
+    if (sub < n) grad_e[s0 + sub] = live ? make_double2(ex, ey) : make_double2(0.0, 0.0);
+    if (sub == 0 && live) wl += w * (vx + vy), hp += hx + hy;
+}
+
 __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __restrict__ blk,
                                                        const int* __restrict__ net_by_size,
                                                        const int* __restrict__ gen_start,
@@ -405,12 +479,35 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
                                                        const int* __restrict__ gen_ord, double* __restrict__ part_pp,
                                                        const Ctrl* __restrict__ ctrl)
 {
-    __shared__ double sh[kBlock / 32];
+    __shared__ double sh[3 * kBlock / 32];
     if (ctrl && ctrl->stopped) return;
     const int4 b = blk[blk0 + blockIdx.x];
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double wl = 0.0, hp = 0.0, ppv = 0.0;
-    for (int t = threadIdx.x >> 5; t < b.z; t += kBlock / 32) { // one warp per net
+    // nets in pairs per warp: two nets of <= 16 pins share the warp (a half each); otherwise the warp
+    // takes them one after the other
+    const int t0 = 2 * warp, t1 = t0 + 1;
+    auto size_of = [&](int t) {
+        if (t >= b.z) return 0;
+        const int net = net_by_size[b.y + t];
+        return net_start[net + 1] - net_start[net];
+    };
+    const int n0 = size_of(t0), n1 = size_of(t1);
+    const bool halves = t0 < b.z && n0 <= 16 && n1 <= 16;
+    if (halves) {
+        const int seg = lane >> 4, t = seg ? t1 : t0, n = seg ? n1 : n0;
+        const bool have = t < b.z;
+        const int i = b.y + (have ? t : t0);
+        const int net = net_by_size[i];
+        const int s0 = gen_start[i];
+        const double w = net_w ? net_w[net] : 1.0;
+        const int kmax = max(n0, n1) - 1;
+        double wl_l = 0.0, hp_l = 0.0, pp_l = 0.0;
+        wa_half_net(lane & 15, s0, have ? n : 0, kmax, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, pp,
+                    gen_ord, wl_l, hp_l, pp_l);
+        wl += wl_l, hp += hp_l, ppv += pp_l;
+    }
+    for (int t = halves ? b.z : t0; t < b.z && t <= t1; ++t) { // one warp per net
         const int i = b.y + t;
         const int net = net_by_size[i];
         const int s0 = gen_start[i], n = net_start[net + 1] - net_start[net];
@@ -493,12 +590,10 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
             __syncwarp();
         }
     }
-    const double bw = block_sum<kBlock>(wl, sh);
-    const double bh = block_sum<kBlock>(hp, sh);
-    const double bp = part_pp ? block_sum<kBlock>(ppv, sh) : 0.0;
+    block_sum3<kBlock>(wl, hp, ppv, sh);
     if (threadIdx.x == 0) {
-        part_wl[blk0 + blockIdx.x] = bw, part_hp[blk0 + blockIdx.x] = bh;
-        if (part_pp) part_pp[blk0 + blockIdx.x] = bp;
+        part_wl[blk0 + blockIdx.x] = wl, part_hp[blk0 + blockIdx.x] = hp;
+        if (part_pp) part_pp[blk0 + blockIdx.x] = ppv;
     }
 }
 

@@ -20,10 +20,10 @@ namespace tdpg {
 int api_fail(int kind, const std::string& msg);
 
 // Entry weight of every WA block, in the session's block order (session.cu: classes N = 2..8 of 256
-// nets each in size-stable order, then the other nets 8 per block).
+// nets each in size-stable order, then the other nets 16 per block).
 std::vector<long long> wa_block_weights(int N, const int* net_start)
 {
-    constexpr int kMaxN = 8, kB = 256, kGen = 8;
+    constexpr int kMaxN = 8, kB = 256, kGen = 16;
     auto size = [&](int n) { return net_start[n + 1] - net_start[n]; };
     auto cls = [&](int k) { return (k >= 2 && k <= kMaxN) ? k : 0; };
     std::vector<int> cnt(kMaxN + 1, 0);

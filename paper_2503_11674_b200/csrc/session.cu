@@ -461,7 +461,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         s->wa_cls_nblk[k] = static_cast<int>(blk.size()) - s->wa_cls_blk0[k];
     }
     s->wa_cls_blk0[0] = static_cast<int>(blk.size());
-    constexpr int kGenNets = 8; // generic nets per block: one warp per net
+    constexpr int kGenNets = 16; // generic nets per block: two per warp (half-warps for nets <= 16 pins)
     for (int i = cnt[0]; i < cnt[1]; i += kGenNets) blk.push_back(make_int4(0, i, std::min(kGenNets, cnt[1] - i), 0));
     s->wa_cls_nblk[0] = static_cast<int>(blk.size()) - s->wa_cls_blk0[0];
     for (int i = cnt[0]; i < cnt[1]; ++i) {
