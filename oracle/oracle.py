@@ -122,6 +122,7 @@ class Oracle(_Base):
             lib.orc_hits_get.argtypes = [_P, _P, _P, _P]
             lib.orc_graph_info.argtypes = [_P, _I32P, _P, _P, _P, _P, _P]
             lib.orc_place.argtypes = [_P, _P, _P, _P, _P, _P, _I32P, _I32P, _F64P]
+            lib.orc_jitter.argtypes = [_P, _P, _P, _P, _P]
             cls._lib = lib
         return cls._lib
 
@@ -257,6 +258,15 @@ class Oracle(_Base):
         self._check(self.lib.orc_objective(C.byref(self._view), xy.ctypes.data, nx, ny, td, gamma, lam, beta, kind,
                                            _p(nw), q, _p(a), _p(b), _p(w), terms.ctypes.data, d.ctypes.data))
         return terms, d
+
+    def jitter(self, cfg: dict | None = None, xy=None):
+        """The run's starting positions: the seeded jitter of placer.cpp:375-382."""
+        c = make_config(cfg)
+        xy = self.d.positions if xy is None else np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
+        out = np.zeros_like(xy)
+        self._check(self.lib.orc_jitter(self.h, xy.ctypes.data, self.d.pos_explicit.ctypes.data, C.byref(c),
+                                        out.ctypes.data))
+        return out
 
     def place(self, cfg: dict | None = None, xy=None):
         c = make_config(cfg)

@@ -1229,6 +1229,26 @@ static void clamp_to_core(double* x, double* y, double w, double h, const double
     *y = *y < core[1] ? core[1] : (yh < *y ? yh : *y);
 }
 
+/* placer.cpp:375-382: seeded jitter of every cell that is neither fixed nor explicitly placed */
+int orc_jitter(void* h, const double* init_xy, const uint8_t* pos_explicit, const tdpg_config* cfg, double* out_xy)
+{
+    orc_session* s = h;
+    const tdpg_netlist* nl = &s->nl;
+    const int32_t C = nl->n_cells;
+    const double* core = nl->core;
+    const double cw = core[2] - core[0], ch = core[3] - core[1];
+    memcpy(out_xy, init_xy, (size_t)C * 2 * sizeof(double));
+    orc_mt64 rng;
+    orc_mt64_seed(&rng, cfg->seed);
+    for (int32_t c = 0; c < C; ++c) {
+        if (nl->cell_fixed[c] || (pos_explicit && pos_explicit[c])) continue;
+        out_xy[2 * c] += rng_uniform(&rng, -1.0, 1.0) * cfg->init_jitter_frac * cw;
+        out_xy[2 * c + 1] += rng_uniform(&rng, -1.0, 1.0) * cfg->init_jitter_frac * ch;
+        clamp_to_core(&out_xy[2 * c], &out_xy[2 * c + 1], nl->cell_w[c], nl->cell_h[c], core);
+    }
+    return 0;
+}
+
 int orc_place(void* h, const double* init_xy, const uint8_t* pos_explicit, const tdpg_config* cfg, double* out_xy,
               tdpg_trace_row* trace, int32_t* n_rows, int32_t* stop_overflow, double final_[3])
 {
@@ -1239,15 +1259,7 @@ int orc_place(void* h, const double* init_xy, const uint8_t* pos_explicit, const
     const double cw = core[2] - core[0], ch = core[3] - core[1];
     const double span = cw > ch ? cw : ch;
     const double gamma = cfg->gamma_frac * span;
-    memcpy(out_xy, init_xy, (size_t)C * 2 * sizeof(double));
-    orc_mt64 rng;
-    orc_mt64_seed(&rng, cfg->seed);
-    for (int32_t c = 0; c < C; ++c) {
-        if (nl->cell_fixed[c] || (pos_explicit && pos_explicit[c])) continue;
-        out_xy[2 * c] += rng_uniform(&rng, -1.0, 1.0) * cfg->init_jitter_frac * cw;
-        out_xy[2 * c + 1] += rng_uniform(&rng, -1.0, 1.0) * cfg->init_jitter_frac * ch;
-        clamp_to_core(&out_xy[2 * c], &out_xy[2 * c + 1], nl->cell_w[c], nl->cell_h[c], core);
-    }
+    orc_jitter(h, init_xy, pos_explicit, cfg, out_xy);
     s->q = 0; /* fresh PinPairWeights */
     double* net_w = NULL;
     double terms[6];

@@ -62,6 +62,7 @@ int orc_pp_update(void* h, int64_t n, const int32_t* a, const int32_t* b, const 
                   double w1, int64_t* q_out);
 int orc_pp_get(void* h, int32_t* a, int32_t* b, double* w);
 /* run_placement; extraction must be endpoint/k = 1. final = tns, wns, hpwl. */
+int orc_jitter(void* h, const double* init_xy, const uint8_t* pos_explicit, const tdpg_config* cfg, double* out_xy);
 int orc_place(void* h, const double* init_xy, const uint8_t* pos_explicit, const tdpg_config* cfg, double* out_xy,
               tdpg_trace_row* trace, int32_t* n_rows, int32_t* stop_overflow, double final_[3]);
 

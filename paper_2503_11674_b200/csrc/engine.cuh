@@ -107,7 +107,6 @@ struct tdpg_session {
     std::vector<int> h_pin_cell, h_net_start, h_net_pins, h_sources, h_endpoints, h_pin_net, h_pin_entry;
     std::vector<std::string> pin_names;
     std::vector<int> h_level, h_lvl_start, h_lvl_pins, h_arc_from, h_arc_to, h_arc_kind, h_arc_owner;
-    std::vector<double> h_cell_xy; // last uploaded positions (for fixed-cell baseline)
 
     // device netlist
     tdpg::DBuf<double2> cell_xy, cell_wh, anchor, pin_off, e_off;
@@ -208,6 +207,13 @@ struct tdpg_session {
     tdpg::DBuf<unsigned long long> sort_k0, sort_k1;
     tdpg::DBuf<int> sort_v0, sort_v1;
     tdpg::HBuf<long long> h_small;
+    // initial jitter (place.cu): per-cell jitter flag / rank, the raw mt19937_64 stream, explicit flags
+    tdpg::DBuf<int> jit_flag, jit_rank;
+    // dense ledger -> sorted ledger (timing.cu dense_ledger_to_sorted): keys and weights, grow-only
+    tdpg::DBuf<unsigned long long> dl_k0, dl_k1;
+    tdpg::DBuf<double> dl_w0, dl_w1;
+    tdpg::DBuf<unsigned long long> jit_raw;
+    tdpg::DBuf<uint8_t> jit_expl;
 
     // partitioned multi-GPU mode (partition.cu): this rank's WA block range, NCCL communicator
     int part_rank = 0, part_world = 1, part_b0 = 0, part_b1 = 0;
@@ -226,6 +232,7 @@ namespace tdpg {
 
 // session.cu
 void upload_positions(tdpg_session* s, const double* xy);
+void refresh_fixed_baseline(tdpg_session* s);
 void ensure_grid(tdpg_session* s, int nx, int ny, double td);
 void set_density_model(tdpg_session* s, int model);
 void* cub_scratch(tdpg_session* s, size_t bytes);

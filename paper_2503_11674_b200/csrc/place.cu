@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <random>
 
+#include <cub/cub.cuh>
+
 #include "gp_kernels.cuh"
 
 namespace tdpg {
@@ -68,6 +70,15 @@ struct Engine {
         if (refresh_gexec) cudaGraphExecDestroy(refresh_gexec);
         if (sort_gexec) cudaGraphExecDestroy(sort_gexec);
         for (auto& e : refresh_ev) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    }
+    // a previous engine of the session (engine_init again): its buffers, branch streams and events are
+    // taken over instead of freed and re-allocated (cudaFree synchronises the device)
+    void recycle(Engine& o)
+    {
+        sched = std::move(o.sched), ctrl = std::move(o.ctrl), trace = std::move(o.trace);
+        timing_row = std::move(o.timing_row), cur = std::move(o.cur), terms = std::move(o.terms);
+        m = std::move(o.m), v = std::move(o.v), part = std::move(o.part), red = std::move(o.red);
+        std::swap(br, o.br), std::swap(ev_fork, o.ev_fork), std::swap(ev_join, o.ev_join);
     }
     double refresh_ms()
     {
@@ -129,26 +140,27 @@ __global__ void k_l1_pair(int C, const double2* __restrict__ a, const double2* _
 double lambda_auto(tdpg_session* s, double gamma, int kind)
 {
     evaluate_objective(s, gamma, 0.0, 0.0, kind, false, nullptr);
-    DBuf<double2> wl(s->C);
-    CK(cudaMemcpyAsync(wl.p, s->d_cell.p, sizeof(double2) * s->C, cudaMemcpyDeviceToDevice, s->st));
+    // scratch in the session's jitter stream buffer (free after the jitter): [wl gradient | part | p2]
+    const int nb_d = bins_blocks(s), nb = 148 * 2;
+    s->jit_raw.reserve(2 * static_cast<size_t>(s->C) + 2 * nb_d + 64 + 2 * nb);
+    double2* wl = reinterpret_cast<double2*>(s->jit_raw.p);
+    double* part = reinterpret_cast<double*>(wl + s->C);
+    double* p2 = part + 2 * nb_d + 64;
+    CK(cudaMemcpyAsync(wl, s->d_cell.p, sizeof(double2) * s->C, cudaMemcpyDeviceToDevice, s->st));
     // density-only gradient: zero entry gradients, lambda = 1
-    const int nb_d = bins_blocks(s);
-    DBuf<double> part(2 * nb_d + 64);
-    Terms* terms = reinterpret_cast<Terms*>(part.p + 2 * nb_d);
+    Terms* terms = reinterpret_cast<Terms*>(part + 2 * nb_d);
     IterCur* cur = reinterpret_cast<IterCur*>(terms + 1);
-    launch_density(s, part.p, nb_d);
+    launch_density(s, part, nb_d);
     FinArgs fa{};
-    fa.part_d = part.p, fa.nb_d = nb_d, fa.total_movable = s->grid.total_movable, fa.lambda_single = 1.0;
+    fa.part_d = part, fa.nb_d = nb_d, fa.total_movable = s->grid.total_movable, fa.lambda_single = 1.0;
     fa.terms = terms;
     launch_finalize(s, fa, nullptr, cur);
     s->grad_e.zero(s->st, s->E_tot);
     launch_cells(s, s->d_cell, nullptr, nullptr, 0, 0, 0, cur, nullptr);
-    const int nb = 148 * 2;
-    DBuf<double> p2(2 * nb);
     k_l1_pair<<<nb, kBlock, 0, s->st>>>(s->C, wl, s->d_cell, s->cell_fixed, p2);
     CK_LAUNCH();
     std::vector<double> h(2 * nb);
-    p2.download(h.data(), h.size(), s->st);
+    CK(cudaMemcpyAsync(h.data(), p2, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
     double wl1 = 0.0, d1 = 0.0;
     for (int i = 0; i < nb; ++i) wl1 += h[2 * i], d1 += h[2 * i + 1];
@@ -291,34 +303,147 @@ struct InitTrace {
     }
 };
 
+// ---- initial jitter (placer.cpp:375-382): every cell that is neither fixed nor explicitly placed, in
+// cell order, takes two draws of a std::mt19937_64 seeded with cfg.seed (x then y), each mapped to
+// rng_uniform(-1, 1) = -1 + 2 (draw >> 11) 2^-53, scaled by init_jitter_frac * core extent, then clamped
+// into the core.  The raw engine stream is generated on the device, bitwise the libstdc++ sequence.
+// With x[0..311] the seeded state and x[312 + k] the word tempered into draw k, the engine's
+// regeneration is the lag-156 recurrence  x[j] = x[j - 156] ^ mix(x[j - 312], x[j - 311]),  so 156
+// consecutive words are independent: thread t of one block computes word 312 + 156 k + t in step k,
+// keeping x[j - 156] and x[j - 312] (its own last two words) in registers; x[j - 311] is thread t + 1's
+// word of step k - 2 (thread 0's of step k - 1 for t = 155), read from a ring of steps in shared memory.
+// Two steps per barrier: step k + 1 reads step k - 1 words only, except thread 155, which recomputes thread
+// 0's step-k word from the ring.  The untempered words are stored; k_jit_apply tempers them.
+constexpr int kMtN = 312, kMtM = 156;
+
+__device__ __forceinline__ unsigned long long mt_mix(unsigned long long a, unsigned long long b)
+{
+    const unsigned long long y = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
+    return (y >> 1) ^ ((0ull - (y & 1ull)) & 0xB5026F5AA96619E9ull);
+}
+
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long y)
+{
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    return y ^ (y >> 43);
+}
+
+__global__ void __launch_bounds__(160) k_mt19937_64(unsigned long long seed, const int* __restrict__ count,
+                                                    unsigned long long* __restrict__ out)
+{
+    __shared__ unsigned long long ring[4][kMtM];
+    const int t = threadIdx.x;
+    if (t == 0) { // the seeded state x[0..311] into ring slots 2 (x[0..155]) and 3 (x[156..311])
+        unsigned long long x = seed;
+        ring[2][0] = x;
+        for (int i = 1; i < kMtN; ++i) {
+            x = 6364136223846793005ull * (x ^ (x >> 62)) + i;
+            ring[2 + i / kMtM][i % kMtM] = x;
+        }
+    }
+    __syncthreads();
+    unsigned long long r2 = 0, r1 = 0; // this thread's words of steps k - 2 and k - 1
+    if (t < kMtM) r2 = ring[2][t], r1 = ring[3][t];
+    const long long need = 2LL * *count;
+    int s0 = 0; // ring slot of step k (steps k - 2, k - 1 in s0 + 2, s0 + 3 mod 4)
+    for (long long base = 0; base < need; base += 2 * kMtM) {
+        const int sm2 = (s0 + 2) & 3, sm1 = (s0 + 3) & 3, s1 = (s0 + 1) & 3;
+        if (t < kMtM) {
+            const unsigned long long b0 = t + 1 < kMtM ? ring[sm2][t + 1] : ring[sm1][0];
+            unsigned long long b1;
+            if (t + 1 < kMtM) b1 = ring[sm1][t + 1];
+            else b1 = ring[sm1][0] ^ mt_mix(ring[sm2][0], ring[sm2][1]); // thread 0's step-k word
+            const unsigned long long m1 = mt_mix(r1, b1);
+            const unsigned long long x0 = r1 ^ mt_mix(r2, b0);
+            const unsigned long long x1 = x0 ^ m1;
+            ring[s0][t] = x0, ring[s1][t] = x1;
+            r2 = x0, r1 = x1;
+            if (base + t < need) out[base + t] = x0;
+            if (base + kMtM + t < need) out[base + kMtM + t] = x1;
+        }
+        __syncthreads();
+        s0 = (s0 + 2) & 3;
+    }
+}
+
+__global__ void k_fill_f64(int n, double* __restrict__ p, double v)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_jit_flags(int C, const uint8_t* __restrict__ fixed, const uint8_t* __restrict__ expl,
+                            int* __restrict__ flag)
+{
+    const int c = blockIdx.x * kBlock + threadIdx.x;
+    if (c < C) flag[c] = !fixed[c] && !(expl && expl[c]);
+    else if (c == C) flag[c] = 0;
+}
+
+__global__ void k_jit_apply(int C, const int* __restrict__ flag, const int* __restrict__ rank,
+                            const unsigned long long* __restrict__ raw, const double2* __restrict__ wh,
+                            double2* __restrict__ xy, double frac, double cw, double ch, double4 core)
+{
+    const int c = blockIdx.x * kBlock + threadIdx.x;
+    if (c >= C || !flag[c]) return;
+    const long long r = 2LL * rank[c];
+    const double ux = __ull2double_rn(mt_temper(raw[r]) >> 11) * 0x1.0p-53;
+    const double uy = __ull2double_rn(mt_temper(raw[r + 1]) >> 11) * 0x1.0p-53;
+    double2 p = xy[c];
+    p.x = p.x + (-1.0 + (1.0 - -1.0) * ux) * frac * cw;
+    p.y = p.y + (-1.0 + (1.0 - -1.0) * uy) * frac * ch;
+    const double xh = core.z - wh[c].x, yh = core.w - wh[c].y;
+    p.x = p.x < core.x ? core.x : (xh < p.x ? xh : p.x); // std::clamp
+    p.y = p.y < core.y ? core.y : (yh < p.y ? yh : p.y);
+    xy[c] = p;
+}
+
+void jitter_positions(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit, double cw, double ch,
+                      InitTrace* tr = nullptr)
+{
+    const int C = s->C;
+    s->jit_flag.reserve(C + 1), s->jit_rank.reserve(C + 1), s->jit_raw.reserve(2 * static_cast<size_t>(C) + 1);
+    const uint8_t* ex = nullptr;
+    if (pos_explicit) s->jit_expl.upload(pos_explicit, C, s->st), ex = s->jit_expl.p;
+    k_jit_flags<<<blocks_for(C + 1, kBlock), kBlock, 0, s->st>>>(C, s->cell_fixed, ex, s->jit_flag);
+    CK_LAUNCH();
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st);
+    void* tmp = cub_scratch(s, bytes);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st));
+    k_mt19937_64<<<1, 160, 0, s->st>>>(static_cast<unsigned long long>(cfg->seed), s->jit_rank.p + C, s->jit_raw);
+    CK_LAUNCH();
+    if (tr) tr->mark("jitter: flags + scan + mt19937_64");
+    k_jit_apply<<<blocks_for(C, kBlock), kBlock, 0, s->st>>>(
+        C, s->jit_flag, s->jit_rank, s->jit_raw, s->cell_wh, s->cell_xy, cfg->init_jitter_frac, cw, ch,
+        make_double4(s->core[0], s->core[1], s->core[2], s->core[3]));
+    CK_LAUNCH();
+    s->sta_valid = false;
+    s->pin_xy_external = false;
+    refresh_fixed_baseline(s);
+}
+
 void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_explicit)
 {
     InitTrace tr(s);
     validate_config(*cfg);
     auto E = std::make_unique<Engine>();
+    {
+        std::unique_ptr<Engine> old(s->eng);
+        s->eng = nullptr;
+        if (old) E->recycle(*old);
+    }
+    tr.mark("old engine recycled");
     E->cfg = *cfg;
     const double cw = s->core[2] - s->core[0], ch = s->core[3] - s->core[1];
     E->span = cw > ch ? cw : ch; // Rect::span (geometry.hpp:34)
     E->gamma = cfg->gamma_frac * E->span;
 
-    // implicit starts get a seeded jitter (placer.cpp:375-382): mt19937_64 + rng_uniform
-    std::vector<double> xy(2 * static_cast<size_t>(s->C));
-    s->cell_xy.download(reinterpret_cast<double2*>(xy.data()), s->C, s->st);
-    CK(cudaStreamSynchronize(s->st));
-    std::mt19937_64 rng(cfg->seed);
-    auto unit = [&] { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
-    for (int c = 0; c < s->C; ++c) {
-        if (s->h_cell_fixed[c] || (pos_explicit && pos_explicit[c])) continue;
-        xy[2 * c] += (-1.0 + (1.0 - -1.0) * unit()) * cfg->init_jitter_frac * cw;
-        xy[2 * c + 1] += (-1.0 + (1.0 - -1.0) * unit()) * cfg->init_jitter_frac * ch;
-        const double xh = s->core[2] - s->h_cell_w[c], yh = s->core[3] - s->h_cell_h[c];
-        double& x = xy[2 * c];
-        double& y = xy[2 * c + 1];
-        x = std::clamp(x, s->core[0], xh);
-        y = std::clamp(y, s->core[1], yh);
-    }
-    tr.mark("jitter (host)");
-    upload_positions(s, xy.data());
+    // implicit starts get a seeded jitter (placer.cpp:375-382), on the device
+    jitter_positions(s, cfg, pos_explicit, cw, ch, &tr);
+    tr.mark("jitter");
     ensure_grid(s, cfg->grid_nx, cfg->grid_ny, cfg->target_density);
     set_density_model(s, cfg->density_model);
 
@@ -330,8 +455,8 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     s->q_count.zero(s->st);
     s->net_w.reserve(std::max(s->N, 1));
     if (cfg->net_weighting) {
-        std::vector<double> ones(s->N, 1.0);
-        s->net_w.upload(ones, s->st);
+        k_fill_f64<<<blocks_for(std::max(s->N, 1), kBlock), kBlock, 0, s->st>>>(s->N, s->net_w, 1.0);
+        CK_LAUNCH();
     }
 
     tr.mark("upload + grid + ledger");
@@ -353,21 +478,21 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->sched.upload(sch, s->st);
     Ctrl c0{};
     c0.nonfinite_at = INT_MAX;
-    E->ctrl.alloc(1);
+    E->ctrl.reserve(1);
     CK(cudaMemcpyAsync(E->ctrl.p, &c0, sizeof c0, cudaMemcpyHostToDevice, s->st));
-    E->trace.alloc(T);
-    E->timing_row.alloc(3);
+    E->trace.reserve(T);
+    E->timing_row.reserve(3);
     E->timing_row.zero(s->st);
-    E->cur.alloc(1);
-    E->terms.alloc(1);
-    E->m.alloc(s->C), E->v.alloc(s->C);
+    E->cur.reserve(1);
+    E->terms.reserve(1);
+    E->m.reserve(s->C), E->v.reserve(s->C);
     E->m.zero(s->st), E->v.zero(s->st);
     E->nb_wa = wa_blocks(s), E->nb_pp = wa_blocks(s), E->nb_d = bins_blocks(s); // PP partials per WA block
-    E->part.alloc(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
+    E->part.reserve(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
     E->partitioned = s->part_world > 1;
     if (E->partitioned) { // entries of other ranks' nets must read as 0 in this rank's fold
-        E->red.alloc(2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E->nb_wa) + 8);
+        E->red.reserve(2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E->nb_wa) + 8);
         E->red.zero(s->st);
         s->grad_e.zero(s->st);
     }
@@ -378,8 +503,6 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     s->pin_xy_external = false;
     sort_cells_spatial(s);
     tr.mark("reserve + sort");
-    delete s->eng;
-    tr.mark("old engine freed");
     s->eng = E.release();
     Engine& G = *s->eng;
     capture_iteration(s, G);
@@ -787,7 +910,9 @@ int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_expli
 {
     API_BEGIN
     engine_init(s, cfg, pos_explicit);
+    InitTrace tr(s);
     engine_run(s, cfg->max_iters);
+    tr.mark("place: device loop");
     const Ctrl c = read_ctrl(s);
     if (c.nonfinite_at != INT_MAX)
         throw Error(TDPG_ERR_NONFINITE, "non-finite value: non-finite objective or gradient at iteration " +
@@ -806,9 +931,12 @@ int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_expli
     }
     if (n_rows) *n_rows = rows;
     if (stop_overflow) *stop_overflow = c.stopped;
+    tr.mark("place: trace rows");
     dense_ledger_to_sorted(s); // PlacementOutcome::pair_weights as the sorted ledger (tdpg_pp_get)
+    tr.mark("place: sorted ledger");
     // final STA + exact HPWL at the returned positions (placer.cpp:482, bindings.cpp:381-382)
     run_sta_dev(s);
+    tr.mark("place: final STA");
     double hp = 0.0;
     {
         const int nb = wa_blocks(s);

@@ -76,7 +76,6 @@ void refresh_fixed_baseline(tdpg_session* s)
 
 void upload_positions(tdpg_session* s, const double* xy)
 {
-    s->h_cell_xy.assign(xy, xy + 2 * static_cast<size_t>(s->C));
     s->cell_xy.upload(reinterpret_cast<const double2*>(xy), s->C, s->st);
     s->sta_valid = false;
     s->pin_xy_external = false;

@@ -1286,8 +1286,13 @@ void dense_ledger_to_sorted(tdpg_session* s)
 {
     const int P = s->P;
     if (P == 0) return;
-    DBuf<unsigned long long> k0(P), k1(P);
-    DBuf<double> w0(P), w1(P);
+    // persistent scratch: a per-call cudaMalloc / cudaFree of these (4 x 8P bytes) cost up to ~0.8 s when the
+    // device heap is busy
+    s->dl_k0.reserve(P), s->dl_k1.reserve(P), s->dl_w0.reserve(P), s->dl_w1.reserve(P);
+    DBuf<unsigned long long>& k0 = s->dl_k0;
+    DBuf<unsigned long long>& k1 = s->dl_k1;
+    DBuf<double>& w0 = s->dl_w0;
+    DBuf<double>& w1 = s->dl_w1;
     k_dense_to_pairs<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->dl_w, s->pin_driver, k0, w0);
     CK_LAUNCH();
     size_t bytes = 0;

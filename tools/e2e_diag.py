@@ -12,3 +12,8 @@ for r in range(3):
     t0 = time.perf_counter(); n, _ = s.place_host(cfg, hin.data_ptr(), hout.data_ptr()); t1 = time.perf_counter()
     print(f"run {r}: {n} iters in {t1-t0:.4f} s -> {n/(t1-t0):.1f} it/s", flush=True)
 t0 = time.perf_counter(); s.engine_init(cfg); torch.cuda.synchronize(); print("engine_init", time.perf_counter()-t0)
+import ctypes as C
+t0 = time.perf_counter(); s.engine_init(cfg); torch.cuda.synchronize(); t1 = time.perf_counter()
+s.iterate(200); torch.cuda.synchronize(); t2 = time.perf_counter()
+print(f"engine_init {t1-t0:.4f} s, iterate(200) {t2-t1:.4f} s", flush=True)
+t0 = time.perf_counter(); s.sta(); torch.cuda.synchronize(); print(f"final sta {time.perf_counter()-t0:.4f} s")
