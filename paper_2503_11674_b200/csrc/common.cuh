@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -11,6 +12,14 @@
 #include "tdpg.h"
 
 namespace tdpg {
+
+// Bumped by every device (re)allocation: captured CUDA graphs hold raw pointers, so an engine re-captures
+// its graphs when this moved since the capture (a grow-only scratch that another API call enlarged).
+inline std::atomic<unsigned long long>& dbuf_epoch()
+{
+    static std::atomic<unsigned long long> e{0};
+    return e;
+}
 
 // Exception carrying a C-ABI status; converted at the extern "C" boundary.
 struct Error : std::runtime_error {
@@ -54,14 +63,20 @@ struct DBuf {
     ~DBuf() { release(); }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaFree(p);
+            ++dbuf_epoch();
+        }
         p = nullptr, n = 0;
     }
     void alloc(size_t count)
     {
         release();
         n = count;
-        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+        if (count) {
+            CK(cudaMalloc(&p, count * sizeof(T)));
+            ++dbuf_epoch();
+        }
     }
     // grow-only
     void reserve(size_t count)

@@ -82,7 +82,8 @@ struct TraceRowDev {
     double hpwl, overflow, tns, wns, wl_term, density_term, pp_term, lambda, beta_pp;
 };
 
-struct Engine; // placement loop state (gp.cu)
+struct Engine; // placement loop state (place.cu)
+void engine_release(tdpg_session* s); // deletes s->eng (place.cu, where Engine is complete)
 
 // k-best extraction scratch (kpaths.cu), grow-only
 struct KbScratch {

@@ -124,8 +124,7 @@ void set_partition(tdpg_session* s, int rank, int world)
         throw Error(TDPG_ERR_INTERNAL, "partition plan does not match the WA block layout");
     s->part_rank = rank, s->part_world = world;
     s->part_b0 = b[rank], s->part_b1 = world == 1 ? s->n_wa_blocks : b[rank + 1];
-    delete s->eng; // the iteration graph depends on the partition: tdpg_engine_init again
-    s->eng = nullptr;
+    engine_release(s); // the iteration graph depends on the partition: tdpg_engine_init again
 }
 
 } // namespace tdpg

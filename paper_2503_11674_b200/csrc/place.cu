@@ -34,14 +34,16 @@ struct Engine {
     DBuf<Terms> terms;
     DBuf<double2> m, v;
     DBuf<double> part;
+    DBuf<unsigned long long> obs_count; // observer rounds: unique pin pairs of the refresh
     int nb_wa = 0, nb_pp = 0, nb_d = 0;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
-    int launched = 0, refreshes = 0;
+    int launched = 0, refreshes = 0, recaptures = 0;
     long long kernel_launches = 0;
     int kernels_per_iter = 8; // 2 WA class groups + generic + scatter + bins + dens_grad + finalize + cells
     cudaGraphExec_t refresh_gexec = nullptr; // the whole timing refresh, captured once
     cudaGraphExec_t sort_gexec = nullptr;    // spatial re-sort of the cells
+    unsigned long long epoch = 0;            // dbuf_epoch() when the graphs were captured
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
     int sort_every = 4; // iterations between spatial re-sorts of the cells (2: 0.310, 4: 0.301, 8: 0.334 ms/iteration at 1M)
     double last_refresh_ms = 0, total_refresh_ms = 0;
@@ -78,6 +80,7 @@ struct Engine {
         sched = std::move(o.sched), ctrl = std::move(o.ctrl), trace = std::move(o.trace);
         timing_row = std::move(o.timing_row), cur = std::move(o.cur), terms = std::move(o.terms);
         m = std::move(o.m), v = std::move(o.v), part = std::move(o.part), red = std::move(o.red);
+        obs_count = std::move(o.obs_count);
         std::swap(br, o.br), std::swap(ev_fork, o.ev_fork), std::swap(ev_join, o.ev_join);
     }
     double refresh_ms()
@@ -485,6 +488,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->timing_row.zero(s->st);
     E->cur.reserve(1);
     E->terms.reserve(1);
+    E->obs_count.reserve(1);
     E->m.reserve(s->C), E->v.reserve(s->C);
     E->m.zero(s->st), E->v.zero(s->st);
     E->nb_wa = wa_blocks(s), E->nb_pp = wa_blocks(s), E->nb_d = bins_blocks(s); // PP partials per WA block
@@ -512,6 +516,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     });
     tr.mark("refresh graph");
     G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
+    G.epoch = dbuf_epoch();
     tr.mark("sort graph");
     CK(cudaStreamSynchronize(s->st));
 }
@@ -642,12 +647,12 @@ void timing_refresh(tdpg_session* s)
         long long c[3];
         CK(cudaMemcpyAsync(h, s->sta_out.p, sizeof h, cudaMemcpyDeviceToHost, s->st));
         CK(cudaMemcpyAsync(c, s->ex_counts.p, sizeof c, cudaMemcpyDeviceToHost, s->st));
-        DBuf<unsigned long long> u(1);
-        u.zero(s->st);
+        unsigned long long* u = E.obs_count;
+        CK(cudaMemsetAsync(u, 0, sizeof *u, s->st));
         k_count_heads32<<<148 * 4, kBlock, 0, s->st>>>(s->hcap, s->eh_key_s, u);
         CK_LAUNCH();
         unsigned long long uq = 0;
-        u.download(&uq, 1, s->st);
+        CK(cudaMemcpyAsync(&uq, u, sizeof uq, cudaMemcpyDeviceToHost, s->st));
         CK(cudaStreamSynchronize(s->st));
         s->tns = h[0], s->wns = h[1];
         s->sta_valid = true, s->ties_resolved = true;
@@ -659,11 +664,35 @@ void timing_refresh(tdpg_session* s)
 
 // Run up to n iterations of the loop (refreshes per schedule), all enqueued without host syncs;
 // after a stop (stop_overflow) the kernels see the device flag and do nothing.
+void engine_release(tdpg_session* s)
+{
+    delete s->eng;
+    s->eng = nullptr;
+}
+
+// Re-capture the engine's graphs when a device buffer they point into was (re)allocated since.
+void ensure_graphs(tdpg_session* s, Engine& E)
+{
+    if (E.epoch == dbuf_epoch()) return;
+    if (E.gexec_a) cudaGraphExecDestroy(E.gexec_a), E.gexec_a = nullptr;
+    if (E.gexec_b) cudaGraphExecDestroy(E.gexec_b), E.gexec_b = nullptr;
+    capture_iteration(s, E);
+    if (E.refresh_gexec) cudaGraphExecDestroy(E.refresh_gexec);
+    E.refresh_gexec = capture(s, [&] {
+        refresh_record(s, E.ctrl, E.timing_row, E.cfg.w0, E.cfg.w1, E.cfg.net_weighting != 0);
+    });
+    if (E.sort_gexec) cudaGraphExecDestroy(E.sort_gexec);
+    E.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
+    E.epoch = dbuf_epoch();
+    ++E.recaptures;
+}
+
 int engine_run(tdpg_session* s, int n)
 {
     Engine& E = *s->eng;
     int done = 0;
     for (; done < n && E.launched < E.cfg.max_iters; ++done) {
+        ensure_graphs(s, E);
         const int it = E.launched;
         if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0) timing_refresh(s);
         if (it % E.sort_every == 0) {
@@ -686,6 +715,7 @@ size_t part_phase_a(tdpg_session* s, double* red_host)
 {
     Engine& E = *s->eng;
     if (!E.partitioned || !E.gexec_a) throw Error(TDPG_ERR_INTERNAL, "engine is not in split-phase partitioned mode");
+    ensure_graphs(s, E);
     const int it = E.launched;
     if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0) timing_refresh(s);
     if (it % E.sort_every == 0) CK(cudaGraphLaunch(E.sort_gexec, s->st));

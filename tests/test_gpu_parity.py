@@ -337,3 +337,22 @@ def test_objective_gradient_finite_differences(seed):
     _, g = s.objective(d.positions, **args)
     f = lambda xy: s.objective(xy, **args)[0][0]  # noqa: E731
     assert _max_grad_error(f, d.positions.copy(), g, 1e-5 * 20.0) <= 1e-4
+
+
+def test_engine_recaptures_after_interleaved_api_calls():
+    """The engine's CUDA graphs hold raw pointers into grow-only session scratch; an API call between
+    iterations that enlarges one (here a k = 6 report sorting more candidates than the refresh ever
+    did) must not leave the graphs pointing at freed memory: the run ends bitwise where an
+    uninterrupted run ends."""
+    d = generate(seed=5, cells=20000, fail_frac=1.0, calibrate=True)
+    cfg = {"grid_nx": 32, "grid_ny": 32, "m": 5, "timing_start_iter": 0, "max_iters": 40, "seed": 3}
+    a = Session(d)
+    a.engine_init(cfg)
+    a.iterate(40)
+    b = Session(d)
+    b.engine_init(cfg)
+    b.iterate(3)
+    r = b.extract(n=0, k=6, run_sta=False)
+    assert r["n_paths"] > 0, r["n_paths"]
+    b.iterate(37)
+    assert np.array_equal(a.positions(), b.positions())
