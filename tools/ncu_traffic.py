@@ -1,0 +1,29 @@
+"""profiles/traffic_<tag>.json: DRAM bytes (read + write) per launch of each GP kernel from one
+`ncu --set full` capture (bench.py reads it into roofline.traffic).  Usage: ncu_traffic.py REPORT OUT"""
+import csv
+import json
+import subprocess
+import sys
+
+MAP = {"k_density_scatter_win": "density_scatter", "k_dens_grad": "dens_grad", "k_cells": "cells",
+       "k_density_bins": "density_bins", "k_finalize": "finalize", "k_wa_": "wirelength_pp"}
+raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(raw.splitlines()))
+h = r[0]
+per = {}
+for row in r[2:]:
+    d = dict(zip(h, row))
+    name = d["Kernel Name"]
+    key = next((v for k, v in MAP.items() if k in name), None)
+    if key is None:
+        continue
+    b = float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])
+    unit = h and r[1][h.index("dram__bytes_read.sum")]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    per.setdefault(key, {}).setdefault(name, []).append(b * scale)
+out = {}
+for key, kernels in per.items():  # sum over the kernels of one stage, mean over repeated launches
+    out[key] = round(sum(sum(v) / len(v) for v in kernels.values()))
+out["_source"] = sys.argv[1].split("/")[-1] + " (ncu --set full --clock-control none, 1M-cell iteration)"
+json.dump(out, open(sys.argv[2], "w"), indent=1)
+print(out)
