@@ -7,11 +7,31 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "tdpg.h"
 
 namespace tdpg {
+
+// Programmatic dependent launch (sm_90+): a kernel launched with programmatic stream serialization may
+// start once every block of the kernel before it has called pdl_trigger(); pdl_wait() then blocks until
+// that kernel has completed and its writes are visible.  Code before pdl_wait() may only read data that
+// no kernel still in flight writes.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... P, typename... A>
+inline cudaError_t launch_pdl(void (*k)(P...), unsigned grid, unsigned block, cudaStream_t st, bool pdl, A&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid), cfg.blockDim = dim3(block), cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at, cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
 
 // Bumped by every device (re)allocation: captured CUDA graphs hold raw pointers, so an engine re-captures
 // its graphs when this moved since the capture (a grow-only scratch that another API call enlarged).

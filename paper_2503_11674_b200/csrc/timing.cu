@@ -29,6 +29,8 @@ __global__ void k_pin_xy(int P, const int* __restrict__ pin_cell, const double2*
                          const double2* __restrict__ cell_xy, const double2* __restrict__ anchor,
                          double2* __restrict__ pin_xy)
 {
+    pdl_trigger();
+    pdl_wait();
     const int p = blockIdx.x * kBlock + threadIdx.x;
     if (p < P) pin_xy[p] = pin_pos(p, pin_cell, off, cell_xy, anchor);
 }
@@ -297,25 +299,33 @@ __global__ void __launch_bounds__(kBlock) k_L_init(int P, LArgs a, bool from_cel
     a.rkey[i] = (f & 2) ? double_key(a.clock) : kNoReq;
 }
 
+// Levels after the first are launched as programmatic dependents of the previous level: the static part
+// (graph tables, this refresh's pin positions from k_L_init, which completed before the first level)
+// is loaded before pdl_wait().
 __global__ void __launch_bounds__(kBlock) k_L_arr_push(int lo, int hi, LArgs a)
 {
+    pdl_trigger();
     const int t = lo + blockIdx.x * kBlock + threadIdx.x;
     if (t >= hi) return;
+    const uint8_t fl = a.flags[t];
+    const int j0 = a.in_start[t], j1 = a.in_start[t + 1], o0 = a.out_start[t], o1 = a.out_start[t + 1];
+    const double2 pt = a.xy[t];
+    const double cap = a.cap[t], dcell = o1 > o0 ? a.cell_delay[a.cell[t]] : 0.0;
+    const int u0 = j1 > j0 ? a.in_from[j0] : 0;
+    const double2 xu0 = a.xy[u0];
+    pdl_wait();
     double best = 0.0;
     bool found = false;
     int bu = -1, ntie = 0;
-    if (a.flags[t] & 1) {
+    if (fl & 1) {
         found = true;
     } else {
-        const int j0 = a.in_start[t], j1 = a.in_start[t + 1];
         if (j1 > j0) {
-            const double2 pt = a.xy[t];
-            const double cap = a.cap[t];
             for (int j = j0; j < j1; ++j) {
-                const int u = a.in_from[j];
+                const int u = j == j0 ? u0 : a.in_from[j];
                 const unsigned long long k = a.akey[u];
                 if (k == kNoArr) continue;
-                const double cand = key_double(k) + net_delay(a.xy[u], pt, cap, a.r, a.c);
+                const double cand = key_double(k) + net_delay(j == j0 ? xu0 : a.xy[u], pt, cap, a.r, a.c);
                 if (!found || cand > best) {
                     best = cand, found = true, bu = u, ntie = 1;
                 } else if (cand == best) {
@@ -329,15 +339,16 @@ __global__ void __launch_bounds__(kBlock) k_L_arr_push(int lo, int hi, LArgs a)
     a.pred[t] = found ? bu : -1;
     if (ntie > 1) a.tie_list[atomicAdd(&a.counters[0], 1)] = t;
     if (!found) return;
-    const int o0 = a.out_start[t], o1 = a.out_start[t + 1];
     if (o1 > o0) {
-        const unsigned long long k = double_key(best + a.cell_delay[a.cell[t]]);
+        const unsigned long long k = double_key(best + dcell);
         for (int j = o0; j < o1; ++j) atomicMax(&a.akey[a.out_to[j]], k);
     }
 }
 
 __global__ void __launch_bounds__(kBlock) k_L_arr_decode(int P, LArgs a)
 {
+    pdl_trigger();
+    pdl_wait();
     const int v = blockIdx.x * kBlock + threadIdx.x;
     if (v >= P) return;
     const uint8_t f = a.flags[v];
@@ -367,16 +378,22 @@ __global__ void __launch_bounds__(kBlock) k_L_arr_decode(int P, LArgs a)
 
 __global__ void __launch_bounds__(kBlock) k_L_req_push(int lo, int hi, LArgs a)
 {
+    pdl_trigger();
     const int t = lo + blockIdx.x * kBlock + threadIdx.x;
     if (t >= hi) return;
+    const uint8_t fl = a.flags[t];
+    const int o0 = a.out_start[t], o1 = a.out_start[t + 1], j0 = a.in_start[t], j1 = a.in_start[t + 1];
+    const double dcell = o1 > o0 ? a.cell_delay[a.cell[t]] : 0.0;
+    const double2 pt = a.xy[t];
+    const double cap = a.cap[t];
+    const int v0 = o1 > o0 ? a.out_to[o0] : 0;
+    pdl_wait();
     double best = INFINITY;
     bool found = false;
-    if (a.flags[t] & 2) best = a.clock, found = true;
-    const int o0 = a.out_start[t], o1 = a.out_start[t + 1];
+    if (fl & 2) best = a.clock, found = true;
     if (o1 > o0) {
-        const double dcell = a.cell_delay[a.cell[t]];
         for (int j = o0; j < o1; ++j) {
-            const unsigned long long k = a.rkey[a.out_to[j]];
+            const unsigned long long k = a.rkey[j == o0 ? v0 : a.out_to[j]];
             if (k == kNoReq) continue;
             const double cand = key_double(k) - dcell;
             if (!found || cand < best) best = cand, found = true;
@@ -385,10 +402,7 @@ __global__ void __launch_bounds__(kBlock) k_L_req_push(int lo, int hi, LArgs a)
     a.req[t] = found ? best : a.clock;
     a.rk[t] = found ? 1 : 0;
     if (!found) return;
-    const int j0 = a.in_start[t], j1 = a.in_start[t + 1];
     if (j1 > j0) {
-        const double2 pt = a.xy[t];
-        const double cap = a.cap[t];
         for (int j = j0; j < j1; ++j) {
             const int u = a.in_from[j];
             atomicMin(&a.rkey[u], double_key(best - net_delay(a.xy[u], pt, cap, a.r, a.c)));
@@ -398,6 +412,8 @@ __global__ void __launch_bounds__(kBlock) k_L_req_push(int lo, int hi, LArgs a)
 
 __global__ void __launch_bounds__(kBlock) k_L_req_decode(int P, LArgs a)
 {
+    pdl_trigger();
+    pdl_wait();
     const int u = blockIdx.x * kBlock + threadIdx.x;
     if (u >= P || !(a.flags[u] & 4)) return;
     const unsigned long long k = a.rkey[u];
@@ -412,6 +428,8 @@ __global__ void __launch_bounds__(kBlock) k_L_to_pins(int P, LArgs a, double* __
                                                       double* __restrict__ req, uint8_t* __restrict__ ak,
                                                       uint8_t* __restrict__ rk, int* __restrict__ pred)
 {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i < a.counters[0]) a.tie_list[i] = a.pin[a.tie_list[i]];
     if (i >= P) return;
@@ -475,6 +493,8 @@ __global__ void __launch_bounds__(kBlock) k_slack_keys(int P, int EP, const doub
                                                        unsigned long long* __restrict__ keys, int* __restrict__ vals,
                                                        double* __restrict__ part)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double sh[kBlock / 32];
     __shared__ double shm[kBlock / 32];
     __shared__ int shc[kBlock / 32];
@@ -513,6 +533,8 @@ __global__ void __launch_bounds__(kBlock) k_slack_keys(int P, int EP, const doub
 
 __global__ void k_sta_final(int nb, const double* part, double* out3)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double sh[kBlock / 32];
     double t = 0.0, m = 0.0, c = 0.0;
     for (int i = threadIdx.x; i < nb; i += kBlock) t += part[3 * i], m = fmin(m, part[3 * i + 1]), c += part[3 * i + 2];
@@ -726,6 +748,16 @@ static bool all_levels_sweep()
 // Full STA at the current positions; leaves endpoint keys in sort_k0/sort_v0 and
 // [tns, wns, n_violated] in out3. Stream-ordered, no host sync.  The 2L per-level launches are
 // captured once into a CUDA graph (re-captured only if a buffer it uses moved).
+// TDPG_STA_PDL=0: launch the level sweep without programmatic dependent launch
+static bool sta_pdl()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_STA_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 void sta_record(tdpg_session* s, double* out3)
 {
     const int P = s->P;
@@ -759,21 +791,25 @@ void sta_record(tdpg_session* s, double* out3)
         la.tie_list = s->tie_list, la.counters = s->counters;
         const unsigned nbP = blocks_for(P, kBlock);
         k_L_init<<<nbP, kBlock, 0, s->st>>>(P, la, !s->pin_xy_external, s->cell_xy, s->pin_xy);
+        const bool pdl = sta_pdl();
+        bool first = true;
         for (int l = 0; l < s->L; ++l) {
             const int lo = s->h_L_in_lo[l], hi = s->h_L_in_hi[l];
-            if (hi > lo) k_L_arr_push<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, la);
+            if (hi > lo) CK(launch_pdl(k_L_arr_push, blocks_for(hi - lo, kBlock), kBlock, s->st, pdl && !first, lo, hi, la));
+            first = first && !(hi > lo);
         }
-        k_L_arr_decode<<<nbP, kBlock, 0, s->st>>>(P, la);
-        CK_LAUNCH();
+        CK(launch_pdl(k_L_arr_decode, nbP, kBlock, s->st, pdl, P, la));
+        first = true;
         for (int l = s->L - 1; l >= 0; --l) {
             const int lo = s->h_L_in_lo[l], hi = s->h_L_in_hi[l];
-            if (hi > lo) k_L_req_push<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, la);
+            if (hi > lo) CK(launch_pdl(k_L_req_push, blocks_for(hi - lo, kBlock), kBlock, s->st, pdl && !first, lo, hi, la));
+            first = first && !(hi > lo);
         }
-        k_L_req_decode<<<nbP, kBlock, 0, s->st>>>(P, la);
-        k_L_to_pins<<<nbP, kBlock, 0, s->st>>>(P, la, s->arr, s->req, s->ak, s->rk, s->pred);
+        CK(launch_pdl(k_L_req_decode, nbP, kBlock, s->st, pdl, P, la));
+        CK(launch_pdl(k_L_to_pins, nbP, kBlock, s->st, pdl, P, la, s->arr.p, s->req.p, s->ak.p, s->rk.p, s->pred.p));
         if (!s->pin_xy_external)
-            k_pin_xy<<<nbP, kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor, s->pin_xy);
-        CK_LAUNCH();
+            CK(launch_pdl(k_pin_xy, nbP, kBlock, s->st, pdl, P, s->pin_cell.p, s->pin_off.p, s->cell_xy.p, s->anchor.p,
+                          s->pin_xy.p));
     } else if (!all_levels_sweep()) { // push sweep over sink levels in pin order (see k_arr_push)
         k_sta_init<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, a, !s->pin_xy_external, s->pin_off, s->cell_xy,
                                                                  s->anchor, s->sta_akey, s->sta_rkey);
@@ -805,11 +841,10 @@ void sta_record(tdpg_session* s, double* out3)
     CK_LAUNCH();
     }
     const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
-    k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0, s->sort_v0,
-                                           s->sta_part);
-    CK_LAUNCH();
-    k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->sta_part, out3);
-    CK_LAUNCH();
+    const bool pdl = sta_pdl();
+    CK(launch_pdl(k_slack_keys, nb, kBlock, s->st, pdl, P, s->EP, s->arr.p, s->req.p, s->slack.p, s->ep_sorted.p,
+                  s->sort_k0.p, s->sort_v0.p, s->sta_part.p));
+    CK(launch_pdl(k_sta_final, 1, kBlock, s->st, pdl, nb, s->sta_part.p, out3));
 }
 
 // Size the persistent STA for co-residency (every block resident at once, cooperative launch).
