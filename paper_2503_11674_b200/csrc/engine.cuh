@@ -223,6 +223,7 @@ struct tdpg_session {
 
     // placement engine
     tdpg::Engine* eng = nullptr;
+    bool pdl_graph = false; // recording the iteration graph: GP kernels chained by programmatic dependent launch
     tdpg_round_cb round_cb = nullptr; // called after every timing round of tdpg_place
     void* round_user = nullptr; // owned; deleted in ~tdpg_session (place.cu)
 

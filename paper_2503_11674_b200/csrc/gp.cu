@@ -823,6 +823,8 @@ __global__ void __launch_bounds__(kBlock) k_density_bins(long long B, GridDev g,
                                                          double* __restrict__ excess, double* __restrict__ part_d,
                                                          const Ctrl* __restrict__ ctrl, double* __restrict__ rho)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double sh[2][kBlock / 32];
     if (ctrl && ctrl->stopped) return;
     double v2 = 0.0, v1 = 0.0;
@@ -995,7 +997,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* _
                                                       const double2* __restrict__ cell_wh, GridDev g,
                                                       const double* __restrict__ excess, double2* __restrict__ dgrad,
                                                       const Ctrl* __restrict__ ctrl, double fscale)
-{   // field = excess with fscale 2 (d sum excess^2, density.cpp:148-156) or the potential with fscale 1
+{
+    pdl_trigger();
+    pdl_wait();   // field = excess with fscale 2 (d sum excess^2, density.cpp:148-156) or the potential with fscale 1
     if (ctrl && ctrl->stopped) return;
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n_mov) return;
@@ -1049,6 +1053,8 @@ struct CellArgs {
 
 __global__ void __launch_bounds__(kBlock, 6) k_cells(CellArgs a, const IterCur* __restrict__ cur, Ctrl* ctrl)
 {
+    pdl_trigger();
+    pdl_wait();
     const int c = blockIdx.x * kBlock + threadIdx.x;
     if (c >= a.C) return;
     const bool adam = cur->do_adam;
@@ -1418,9 +1424,9 @@ void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const C
 {
     const GridDev g = grid_dev(s);
     const bool el = s->grid.model == 1;
-    k_density_bins<<<nblk, kBlock, 0, s->st>>>(s->grid.bins(), g, s->grid.acc, s->grid.has_fixed ? s->grid.base.p : nullptr,
-                                               s->grid.excess, part_d, ctrl, el ? s->grid.electro.rho.p : nullptr);
-    CK_LAUNCH();
+    CK(launch_pdl(k_density_bins, nblk, kBlock, s->st, s->pdl_graph && s->grid.n_movable > 0, s->grid.bins(), g,
+                  s->grid.acc.p, static_cast<const double*>(s->grid.has_fixed ? s->grid.base.p : nullptr),
+                  s->grid.excess.p, part_d, ctrl, el ? s->grid.electro.rho.p : nullptr));
     if (el) { // potential, then the energy partials replace the overflow-penalty value partials
         electro_solve(s, s->st);
         electro_energy(s, part_d, nblk, ctrl, s->st);
@@ -1451,10 +1457,11 @@ void launch_dens_grad(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st)
     const int n_mov = s->grid.n_movable;
     if (n_mov > 0) {
         const bool el = s->grid.model == 1;
-        k_dens_grad<<<blocks_for(n_mov, kBlock), kBlock, 0, st>>>(n_mov, s->grid.perm, s->cell_xy, s->cell_wh,
-                                                                  grid_dev(s), el ? s->grid.electro.psi.p : s->grid.excess.p,
-                                                                  s->dgrad, ctrl, el ? 1.0 : 2.0);
-        CK_LAUNCH();
+        CK(launch_pdl(k_dens_grad, blocks_for(n_mov, kBlock), kBlock, st, s->pdl_graph,
+                      n_mov, static_cast<const int*>(s->grid.perm.p), static_cast<const double2*>(s->cell_xy.p),
+                      static_cast<const double2*>(s->cell_wh.p), grid_dev(s),
+                      static_cast<const double*>(el ? s->grid.electro.psi.p : s->grid.excess.p), s->dgrad.p, ctrl,
+                      el ? 1.0 : 2.0));
     }
 }
 
@@ -1462,8 +1469,7 @@ void launch_dens_grad(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st)
 void launch_cell_pass(tdpg_session* s, const CellArgs& ca, const IterCur* cur, Ctrl* ctrl, bool dens_grad = true)
 {
     if (dens_grad) launch_dens_grad(s, ctrl, s->st);
-    k_cells<<<blocks_for(s->C, kBlock), kBlock, 0, s->st>>>(ca, cur, ctrl);
-    CK_LAUNCH();
+    CK(launch_pdl(k_cells, blocks_for(s->C, kBlock), kBlock, s->st, s->pdl_graph, ca, cur, ctrl));
 }
 
 // One full objective_and_gradient evaluation at the session's positions.

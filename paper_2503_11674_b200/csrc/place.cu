@@ -183,6 +183,16 @@ cudaGraphExec_t capture(tdpg_session* s, F&& record)
     return x;
 }
 
+// TDPG_GP_PDL=0: record the iteration graph without programmatic dependent launch edges
+bool pdl_gp()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_GP_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 void capture_iteration(tdpg_session* s, Engine& E)
 {
     if (E.gexec) cudaGraphExecDestroy(E.gexec), E.gexec = nullptr;
@@ -259,6 +269,7 @@ void capture_iteration(tdpg_session* s, Engine& E)
         s->part_active = false;
         return;
     }
+    s->pdl_graph = pdl_gp();
     E.gexec = capture(s, [&] {
         // fork: density chain (scatter -> bins -> density gradient) on branch 0, the WA size classes
         // (+ fused pin pairs, dense ledger) on the main stream and branches 1..7; join -> finalize -> cells
@@ -281,6 +292,7 @@ void capture_iteration(tdpg_session* s, Engine& E)
         launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
                      false);
     });
+    s->pdl_graph = false;
 }
 
 } // namespace
