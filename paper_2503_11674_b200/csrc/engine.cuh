@@ -53,6 +53,11 @@ struct Grid {
     DBuf<int> perm, perm_tmp;  // movable cells in spatial (tile) order, for the windowed scatter
     DBuf<unsigned> perm_keys;
     int n_movable = 0;
+    // movable cells that may span more than five bins on an axis (width > 1.99 pitch): their density
+    // gradient runs in a separate pass, so the five-bin kernel carries no general-footprint code
+    DBuf<int> wide;
+    int n_wide = 0;
+    double wide_w = 0, wide_h = 0;
     bool valid() const { return nx > 0; }
     long long bins() const { return static_cast<long long>(nx) * ny; }
 };

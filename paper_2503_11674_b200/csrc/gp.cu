@@ -992,27 +992,12 @@ __device__ __noinline__ double2 dens_grad_wide(const double2 p, const double2 s,
     return make_double2(dgx, dgy);
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* __restrict__ perm,
-                                                      const double2* __restrict__ cell_xy,
-                                                      const double2* __restrict__ cell_wh, GridDev g,
-                                                      const double* __restrict__ excess, double2* __restrict__ dgrad,
-                                                      const Ctrl* __restrict__ ctrl, double fscale)
+// Five-bin footprint gradient (axis5 on both axes): per bin column, dgx += area*dwx * fscale*sum f*wy,
+// dgy += area*wx * fscale*sum f*dwy.
+__device__ __forceinline__ double2 dens_grad5(int bx, int by, const double (&wx)[kF5], const double (&dwx)[kF5],
+                                              const double (&wy)[kF5], const double (&dwy)[kF5], double area,
+                                              const GridDev& g, const double* __restrict__ excess, double fscale)
 {
-    pdl_trigger();
-    pdl_wait();   // field = excess with fscale 2 (d sum excess^2, density.cpp:148-156) or the potential with fscale 1
-    if (ctrl && ctrl->stopped) return;
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n_mov) return;
-    const int c = perm[i];
-    const double2 p = cell_xy[c], s = cell_wh[c];
-    double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
-    int bx, by;
-    if (!(axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx) &&
-          axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy))) {
-        dgrad[c] = dens_grad_wide(p, s, g, excess, fscale);
-        return;
-    }
-    const double area = s.x * s.y;
     double dgx = 0.0, dgy = 0.0;
 #pragma unroll
     for (int a = 0; a < kF5; ++a) {
@@ -1027,7 +1012,51 @@ __global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* _
         dgx += (area * dwx[a]) * (fscale * sx);
         dgy += (area * wx[a]) * (fscale * sy);
     }
-    dgrad[c] = make_double2(dgx, dgy);
+    return make_double2(dgx, dgy);
+}
+
+// field = excess with fscale 2 (d sum excess^2, density.cpp:148-156) or the potential with fscale 1.
+// Cells of Grid::wide are skipped here (k_dens_grad_wide).
+__global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* __restrict__ perm,
+                                                      const double2* __restrict__ cell_xy,
+                                                      const double2* __restrict__ cell_wh, GridDev g,
+                                                      const double* __restrict__ excess, double2* __restrict__ dgrad,
+                                                      const Ctrl* __restrict__ ctrl, double fscale)
+{
+    pdl_trigger();
+    pdl_wait();
+    if (ctrl && ctrl->stopped) return;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n_mov) return;
+    const int c = perm[i];
+    const double2 p = cell_xy[c], s = cell_wh[c];
+    if (s.x > g.wide_w || s.y > g.wide_h) return;
+    double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
+    int bx, by;
+    axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx);
+    axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy);
+    dgrad[c] = dens_grad5(bx, by, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
+}
+
+__global__ void __launch_bounds__(kBlock) k_dens_grad_wide(int n, const int* __restrict__ wide,
+                                                           const double2* __restrict__ cell_xy,
+                                                           const double2* __restrict__ cell_wh, GridDev g,
+                                                           const double* __restrict__ excess,
+                                                           double2* __restrict__ dgrad, const Ctrl* __restrict__ ctrl,
+                                                           double fscale)
+{
+    if (ctrl && ctrl->stopped) return;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const int c = wide[i];
+    const double2 p = cell_xy[c], s = cell_wh[c];
+    double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
+    int bx, by;
+    if (axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx) &&
+        axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy))
+        dgrad[c] = dens_grad5(bx, by, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
+    else
+        dgrad[c] = dens_grad_wide(p, s, g, excess, fscale);
 }
 
 // =====================================================================================
@@ -1158,7 +1187,7 @@ GridDev grid_dev(const tdpg_session* s)
 {
     const Grid& g = s->grid;
     return GridDev{g.nx, g.ny, g.x0, g.y0, g.bw, g.bh, g.cap, g.scale, g.inv_scale, g.total_movable, 1.0 / g.bw,
-                   1.0 / g.bh};
+                   1.0 / g.bh, g.wide_w, g.wide_h};
 }
 
 int wa_blocks(const tdpg_session* s) { return std::max(1, s->n_wa_blocks); }
@@ -1462,6 +1491,12 @@ void launch_dens_grad(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st)
                       static_cast<const double2*>(s->cell_wh.p), grid_dev(s),
                       static_cast<const double*>(el ? s->grid.electro.psi.p : s->grid.excess.p), s->dgrad.p, ctrl,
                       el ? 1.0 : 2.0));
+        if (s->grid.n_wide > 0) {
+            k_dens_grad_wide<<<blocks_for(s->grid.n_wide, kBlock), kBlock, 0, st>>>(
+                s->grid.n_wide, s->grid.wide, s->cell_xy, s->cell_wh, grid_dev(s),
+                el ? s->grid.electro.psi.p : s->grid.excess.p, s->dgrad, ctrl, el ? 1.0 : 2.0);
+            CK_LAUNCH();
+        }
     }
 }
 

@@ -28,6 +28,7 @@ __device__ __forceinline__ double2 pin_pos(int p, const int* __restrict__ pin_ce
 struct GridDev {
     int nx, ny;
     double x0, y0, bw, bh, cap, scale, inv_scale, total_movable, inv_bw, inv_bh;
+    double wide_w, wide_h; // cells wider / taller than this may span more than five bins (Grid::wide)
 };
 
 // Footprint of one cell along one axis (extent_weight / extent_weight_grad, density.cpp:41-49, and the

@@ -105,6 +105,14 @@ void ensure_grid(tdpg_session* s, int nx, int ny, double td)
     g.has_fixed = fixed;
     g.n_movable = 0;
     for (int c = 0; c < s->C; ++c) g.n_movable += s->h_cell_fixed[c] ? 0 : 1;
+    g.wide_w = 1.99 * g.bw, g.wide_h = 1.99 * g.bh;
+    {
+        std::vector<int> wide;
+        for (int c = 0; c < s->C; ++c)
+            if (!s->h_cell_fixed[c] && (s->h_cell_w[c] > g.wide_w || s->h_cell_h[c] > g.wide_h)) wide.push_back(c);
+        g.n_wide = static_cast<int>(wide.size());
+        g.wide.upload(wide, s->st);
+    }
     // Fixed point: every bin's movable occupancy is <= total area, keep 2 bits of headroom.
     int ex = 0;
     std::frexp(std::max(all, 1e-300), &ex);
