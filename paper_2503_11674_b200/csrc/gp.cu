@@ -752,15 +752,13 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
     if (valid) {
         const int c = perm[i];
         p = cell_xy[c], s = cell_wh[c];
-        fast = axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dw) &&
+        // cells of Grid::wide are scattered by k_density_scatter_wide; every other cell spans at most
+        // 1.99 pitches, so its footprint has at most five bins per axis (axis5 succeeds)
+        fast = !(s.x > g.wide_w || s.y > g.wide_h) &&
+               axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dw) &&
                axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dw);
-        if (fast) {
+        if (fast)
             bx0 = max(bx, 0), bx1 = min(bx + kF5 - 1, g.nx - 1), by0 = max(by, 0), by1 = min(by + kF5 - 1, g.ny - 1);
-        } else {
-            const Axis ax = make_axis(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx);
-            const Axis ay = make_axis(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny);
-            bx0 = ax.b0, bx1 = ax.b1, by0 = ay.b0, by1 = ay.b1;
-        }
     }
     if (threadIdx.x == 0) bb[0] = INT_MAX, bb[1] = INT_MIN, bb[2] = INT_MAX, bb[3] = INT_MIN;
     int a0 = bx0, a1 = bx1, c0 = by0, c1 = by1;
@@ -781,11 +779,7 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
     if (W * H <= kWinBins) {
         for (int k = threadIdx.x; k < static_cast<int>(W * H); k += kBlock) win_lo[k] = 0u, win_hi[k] = 0u;
         __syncthreads();
-        if (valid) {
-            const SmemAcc sa{win_lo, win_hi};
-            if (fast) scatter_cell5(area, bx, by, wx, wy, g, sa, H, Y0, X0);
-            else scatter_cell_wide(p, s, g, sa, H, Y0, X0);
-        }
+        if (fast) scatter_cell5(area, bx, by, wx, wy, g, SmemAcc{win_lo, win_hi}, H, Y0, X0);
         __syncthreads();
         const int h = static_cast<int>(H), n = static_cast<int>(W * H);
         for (int k = threadIdx.x; k < n; k += kBlock) {
@@ -793,11 +787,30 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
             const int col = k / h;
             if (v) atomicAdd(&acc[static_cast<long long>(X0 + col) * g.ny + (Y0 + k - col * h)], v);
         }
-    } else if (valid) {
-        const GlobalAcc ga{acc};
-        if (fast) scatter_cell5(area, bx, by, wx, wy, g, ga, g.ny, 0, 0);
-        else scatter_cell_wide(p, s, g, ga, g.ny, 0, 0);
+    } else if (fast) {
+        scatter_cell5(area, bx, by, wx, wy, g, GlobalAcc{acc}, g.ny, 0, 0);
     }
+}
+
+// Cells of Grid::wide: global int64 atomics (they are few), five-bin form when it applies.
+__global__ void __launch_bounds__(kBlock) k_density_scatter_wide(int n, const int* __restrict__ wide,
+                                                                 const double2* __restrict__ cell_xy,
+                                                                 const double2* __restrict__ cell_wh, GridDev g,
+                                                                 unsigned long long* __restrict__ acc,
+                                                                 const Ctrl* __restrict__ ctrl)
+{
+    if (ctrl && ctrl->stopped) return;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const int c = wide[i];
+    const double2 p = cell_xy[c], s = cell_wh[c];
+    double wx[kF5], wy[kF5], dw[kF5];
+    int bx, by;
+    if (axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dw) &&
+        axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dw))
+        scatter_cell5(s.x * s.y, bx, by, wx, wy, g, GlobalAcc{acc}, g.ny, 0, 0);
+    else
+        scatter_cell_wide(p, s, g, GlobalAcc{acc}, g.ny, 0, 0);
 }
 
 // Spatial order of the movable cells: key = 8x8-bin tile of the cell's lower-left corner.
@@ -1447,6 +1460,12 @@ void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl)
     k_density_scatter_win<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(
         n_mov, s->grid.perm, s->cell_xy, s->cell_wh, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
     CK_LAUNCH();
+    if (s->grid.n_wide > 0) {
+        k_density_scatter_wide<<<blocks_for(s->grid.n_wide, kBlock), kBlock, 0, s->st>>>(
+            s->grid.n_wide, s->grid.wide, s->cell_xy, s->cell_wh, g,
+            reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
+        CK_LAUNCH();
+    }
 }
 
 void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl)

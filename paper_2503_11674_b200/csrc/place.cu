@@ -506,7 +506,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->nb_wa = wa_blocks(s), E->nb_pp = wa_blocks(s), E->nb_d = bins_blocks(s); // PP partials per WA block
     E->part.reserve(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
-    E->kernels_per_iter = 8 + (s->grid.n_wide > 0 ? 1 : 0); // (+ the wide-cell density gradient)
+    E->kernels_per_iter = 8 + (s->grid.n_wide > 0 ? 2 : 0); // (+ wide-cell scatter and density gradient)
     E->partitioned = s->part_world > 1;
     if (E->partitioned) { // entries of other ranks' nets must read as 0 in this rank's fold
         E->red.reserve(2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E->nb_wa) + 8);

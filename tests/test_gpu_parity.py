@@ -356,3 +356,20 @@ def test_engine_recaptures_after_interleaved_api_calls():
     assert r["n_paths"] > 0, r["n_paths"]
     b.iterate(37)
     assert np.array_equal(a.positions(), b.positions())
+
+
+@pytest.mark.parametrize("seed", range(1, 21))
+def test_fine_grid_density_mixed_wide_cells(seed):
+    """Grid pitch below the cell sizes: some cells span more than 1.99 pitches (the separate wide-cell
+    scatter and gradient passes), the rest take the five-bin kernels; both against the oracle."""
+    d = random_design(seed)
+    s, o = Session(d), Oracle(d)
+    for nx, ny in ((24, 24), (16, 40)):
+        vs, os_, ds = s.density(nx=nx, ny=ny, td=0.3)
+        vo, oo, do = o.density(nx=nx, ny=ny, td=0.3)
+        assert abs(vs - vo) <= 1e-9 * max(vo, 1e-300) and abs(os_ - oo) <= 1e-9 * max(oo, 1e-300)
+        assert field_err(ds, do) <= 1e-9
+        ts, gs = s.objective(nx=nx, ny=ny, td=0.3, gamma=0.3, lam=0.7, beta=0.0, kind=0)
+        to, go = o.objective(nx=nx, ny=ny, td=0.3, gamma=0.3, lam=0.7, beta=0.0, kind=0)
+        assert np.allclose(ts, to, rtol=1e-9, atol=1e-12), (ts, to)
+        assert field_err(gs, go) <= 1e-9
