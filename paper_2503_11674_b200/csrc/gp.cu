@@ -1093,7 +1093,7 @@ struct CellArgs {
     double core_x0, core_y0, core_x1, core_y1;
 };
 
-__global__ void __launch_bounds__(kBlock, 6) k_cells(CellArgs a, const IterCur* __restrict__ cur, Ctrl* ctrl)
+__global__ void __launch_bounds__(kBlock, 5) k_cells(CellArgs a, const IterCur* __restrict__ cur, Ctrl* ctrl)
 {
     pdl_trigger();
     pdl_wait();
