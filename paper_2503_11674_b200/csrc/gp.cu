@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(kBlock, WA_MINB) k_wa_class(int blk0, const in
 // partner's term with one shuffle, in the reference's operand order, so results are bitwise those of the
 // one-thread form.
 struct WaAxisArgs {
+    // size-class layout (session.cu): blocks of class k are [cls_blk0[k], cls_blk0[k+1]), their nets
+    // [cls_net0[k], cls_net1[k]) of net_by_size, their entries from cls_pos0[k] (k * 256 per block)
+    int cls_blk0[10], cls_net0[9], cls_net1[9], cls_pos0[9];
     const int4* blk;
     const int* net_by_size;
     const int* e_cell;
@@ -189,9 +192,24 @@ struct WaAxisArgs {
     double* part_pp;
 };
 
-template <int N>
-__device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAxisArgs& A, double* sh)
+// Block descriptor (N, first net, nets, entry base) of size-class block g from the kernel parameters:
+// no table load ahead of the entry loads.
+__device__ __forceinline__ int4 wa_blk_of(int g, const WaAxisArgs& A)
 {
+    int k = 2;
+#pragma unroll
+    for (int c = 3; c <= 8; ++c)
+        if (g >= A.cls_blk0[c]) k = c;
+    const int j = g - A.cls_blk0[k];
+    const int net0 = A.cls_net0[k] + j * kBlock;
+    return make_int4(k, net0, min(kBlock, A.cls_net1[k] - net0), A.cls_pos0[k] + j * kBlock * k);
+}
+
+template <int N>
+__device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAxisArgs& A, double* sh,
+                                              const Ctrl* __restrict__ ctrl)
+{
+    const bool stop = ctrl && ctrl->stopped; // (checked after the entry loads are issued)
     const int* __restrict__ net_by_size = A.net_by_size;
     const int* __restrict__ e_cell = A.e_cell;
     const double* __restrict__ e_off = A.e_off;
@@ -212,6 +230,7 @@ __device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAx
         const double a = ec >= 0 ? cell_xy[2 * ec + axis] : anchor[2 * (-1 - ec) + axis];
         x[i] = a + __ldcs(e_off + 2 * e + axis);
     }
+    if (stop) return; // (uniform over the block)
     double v, ext;
     wa_axis<N>(x, inv_gamma, g, v, ext);
     const double v_other = __shfl_xor_sync(0xffffffffu, v, 1), e_other = __shfl_xor_sync(0xffffffffu, ext, 1);
@@ -292,8 +311,7 @@ __global__ void __launch_bounds__(2 * kBlock, (N <= 5 ? 2 : 1)) k_wa_axis(int bl
                                                                           const Ctrl* __restrict__ ctrl)
 {
     __shared__ double sh[48];
-    if (ctrl && ctrl->stopped) return;
-    wa_axis_block<N>(A.blk[blk0 + blockIdx.x], blk0 + blockIdx.x, A, sh);
+    wa_axis_block<N>(wa_blk_of(blk0 + blockIdx.x, A), blk0 + blockIdx.x, A, sh, ctrl);
 }
 
 // Several size classes in one launch (their blocks are contiguous in the table): each block dispatches
@@ -303,17 +321,16 @@ __global__ void __launch_bounds__(2 * kBlock, MINB) k_wa_axis_group(int blk0, Wa
                                                                     const Ctrl* __restrict__ ctrl)
 {
     __shared__ double sh[48];
-    if (ctrl && ctrl->stopped) return;
     const int g = blk0 + blockIdx.x;
-    const int4 b = A.blk[g];
+    const int4 b = wa_blk_of(g, A);
     switch (b.x) {
-    case 2: if (LO <= 2 && 2 <= HI) wa_axis_block<(LO <= 2 && 2 <= HI) ? 2 : LO>(b, g, A, sh); break;
-    case 3: if (LO <= 3 && 3 <= HI) wa_axis_block<(LO <= 3 && 3 <= HI) ? 3 : LO>(b, g, A, sh); break;
-    case 4: if (LO <= 4 && 4 <= HI) wa_axis_block<(LO <= 4 && 4 <= HI) ? 4 : LO>(b, g, A, sh); break;
-    case 5: if (LO <= 5 && 5 <= HI) wa_axis_block<(LO <= 5 && 5 <= HI) ? 5 : LO>(b, g, A, sh); break;
-    case 6: if (LO <= 6 && 6 <= HI) wa_axis_block<(LO <= 6 && 6 <= HI) ? 6 : LO>(b, g, A, sh); break;
-    case 7: if (LO <= 7 && 7 <= HI) wa_axis_block<(LO <= 7 && 7 <= HI) ? 7 : LO>(b, g, A, sh); break;
-    case 8: if (LO <= 8 && 8 <= HI) wa_axis_block<(LO <= 8 && 8 <= HI) ? 8 : LO>(b, g, A, sh); break;
+    case 2: if (LO <= 2 && 2 <= HI) wa_axis_block<(LO <= 2 && 2 <= HI) ? 2 : LO>(b, g, A, sh, ctrl); break;
+    case 3: if (LO <= 3 && 3 <= HI) wa_axis_block<(LO <= 3 && 3 <= HI) ? 3 : LO>(b, g, A, sh, ctrl); break;
+    case 4: if (LO <= 4 && 4 <= HI) wa_axis_block<(LO <= 4 && 4 <= HI) ? 4 : LO>(b, g, A, sh, ctrl); break;
+    case 5: if (LO <= 5 && 5 <= HI) wa_axis_block<(LO <= 5 && 5 <= HI) ? 5 : LO>(b, g, A, sh, ctrl); break;
+    case 6: if (LO <= 6 && 6 <= HI) wa_axis_block<(LO <= 6 && 6 <= HI) ? 6 : LO>(b, g, A, sh, ctrl); break;
+    case 7: if (LO <= 7 && 7 <= HI) wa_axis_block<(LO <= 7 && 7 <= HI) ? 7 : LO>(b, g, A, sh, ctrl); break;
+    case 8: if (LO <= 8 && 8 <= HI) wa_axis_block<(LO <= 8 && 8 <= HI) ? 8 : LO>(b, g, A, sh, ctrl); break;
     default: break;
     }
 }
@@ -1313,6 +1330,12 @@ WaAxisArgs wa_axis_args(tdpg_session* s, const double* nw, double inv_gamma, dou
     A.e_off = reinterpret_cast<const double*>(s->e_off.p), A.cell_xy = reinterpret_cast<const double*>(s->cell_xy.p);
     A.anchor = reinterpret_cast<const double*>(s->anchor.p), A.net_w = nw, A.inv_gamma = inv_gamma;
     A.grad_e = reinterpret_cast<double*>(s->grad_e.p), A.part_wl = pw, A.part_hp = ph, A.pp = pp, A.part_pp = ppart;
+    for (int k = 0; k <= 8; ++k) {
+        A.cls_blk0[k] = s->wa_cls_blk0[k], A.cls_net0[k] = s->wa_cls_net0[k], A.cls_net1[k] = s->wa_cls_net1[k];
+        A.cls_pos0[k] = s->wa_cls_pos0[k];
+    }
+    A.cls_blk0[9] = s->wa_cls_blk0[0]; // (the generic blocks follow class 8; an empty class starts where
+                                       // the next one does, so in wa_blk_of the last match wins)
     return A;
 }
 

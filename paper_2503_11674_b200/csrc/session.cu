@@ -458,6 +458,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     int pos = 0;
     for (int k = 2; k <= kMaxN; ++k) {
         s->wa_cls_blk0[k] = static_cast<int>(blk.size());
+        s->wa_cls_net0[k] = cnt[k], s->wa_cls_net1[k] = cnt[k + 1], s->wa_cls_pos0[k] = pos;
         for (int i = cnt[k]; i < cnt[k + 1]; i += kB) {
             const int count = std::min(kB, cnt[k + 1] - i);
             blk.push_back(make_int4(k, i, count, pos));
