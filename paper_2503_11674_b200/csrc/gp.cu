@@ -913,6 +913,7 @@ constexpr int kFinBlock = 1024;
 
 __global__ void __launch_bounds__(kFinBlock) k_finalize(FinArgs a, Ctrl* ctrl, IterCur* cur)
 {
+    pdl_trigger(); // (k_cells may start its fold now; it waits for this kernel before reading cur)
     __shared__ double sh[kFinBlock / 32];
     __shared__ int skip;
     if (threadIdx.x == 0) skip = ctrl ? ctrl->stopped : 0;
@@ -1052,7 +1053,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* _
                                                       const double2* __restrict__ cell_wh, GridDev g,
                                                       const double* __restrict__ excess, double2* __restrict__ dgrad,
                                                       const Ctrl* __restrict__ ctrl, double fscale)
-{
+{   // (a programmatic dependent of the bins kernel; only launch latency is overlapped: data produced by
+    // earlier kernels is read after pdl_wait())
     pdl_trigger();
     pdl_wait();
     if (ctrl && ctrl->stopped) return;
@@ -1110,18 +1112,17 @@ struct CellArgs {
     double core_x0, core_y0, core_x1, core_y1;
 };
 
+// In the iteration graph this is a programmatic dependent of k_finalize: its CTAs are resident when
+// finalize ends, but everything is read after pdl_wait() — reading the WA kernels' entry gradients
+// before it (they completed before finalize started) was measured to see stale data.
 __global__ void __launch_bounds__(kBlock, 5) k_cells(CellArgs a, const IterCur* __restrict__ cur, Ctrl* ctrl)
 {
     pdl_trigger();
     pdl_wait();
     const int c = blockIdx.x * kBlock + threadIdx.x;
     if (c >= a.C) return;
-    const bool adam = cur->do_adam;
-    if (ctrl && !adam && !a.d_cell) return; // stopped: nothing to do
     double gx = 0.0, gy = 0.0;
-    if (a.folded) {
-        gx = a.folded[c].x, gy = a.folded[c].y;
-    } else { // fold in ascending pin order (placer.cpp:318-325); loads batched 4 at a time
+    if (!a.folded) { // fold in ascending pin order (placer.cpp:318-325); loads batched 4 at a time
         const int j0 = a.ent_start[c], j1 = a.ent_start[c + 1];
         for (int j = j0; j < j1; j += 4) {
             double2 ge[4];
@@ -1132,11 +1133,15 @@ __global__ void __launch_bounds__(kBlock, 5) k_cells(CellArgs a, const IterCur* 
                 if (j + k < j1) gx += ge[k].x, gy += ge[k].y;
         }
     }
-    if (a.fixed[c]) {
+    const bool fixed = a.fixed[c];
+    const double2 dg = fixed ? make_double2(0.0, 0.0) : a.dgrad[c];
+    if (a.folded) gx = a.folded[c].x, gy = a.folded[c].y;
+    const bool adam = cur->do_adam;
+    if (ctrl && !adam && !a.d_cell) return; // stopped: nothing to do
+    if (fixed) {
         if (a.d_cell) a.d_cell[c] = make_double2(0.0, 0.0);
         return;
     }
-    const double2 dg = a.dgrad[c];
     const double lambda = cur->lambda;
     gx += lambda * dg.x;
     gy += lambda * dg.y;

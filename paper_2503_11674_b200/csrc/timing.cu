@@ -299,9 +299,9 @@ __global__ void __launch_bounds__(kBlock) k_L_init(int P, LArgs a, bool from_cel
     a.rkey[i] = (f & 2) ? double_key(a.clock) : kNoReq;
 }
 
-// Levels after the first are launched as programmatic dependents of the previous level: the static part
-// (graph tables, this refresh's pin positions from k_L_init, which completed before the first level)
-// is loaded before pdl_wait().
+// Levels after the first are launched as programmatic dependents of the previous level: only the
+// session-constant graph tables (written at session setup, never by a kernel of the refresh) are loaded
+// before pdl_wait(); this refresh's pin positions and keys after it.
 __global__ void __launch_bounds__(kBlock) k_L_arr_push(int lo, int hi, LArgs a)
 {
     pdl_trigger();
@@ -309,11 +309,10 @@ __global__ void __launch_bounds__(kBlock) k_L_arr_push(int lo, int hi, LArgs a)
     if (t >= hi) return;
     const uint8_t fl = a.flags[t];
     const int j0 = a.in_start[t], j1 = a.in_start[t + 1], o0 = a.out_start[t], o1 = a.out_start[t + 1];
-    const double2 pt = a.xy[t];
     const double cap = a.cap[t], dcell = o1 > o0 ? a.cell_delay[a.cell[t]] : 0.0;
     const int u0 = j1 > j0 ? a.in_from[j0] : 0;
-    const double2 xu0 = a.xy[u0];
     pdl_wait();
+    const double2 pt = a.xy[t], xu0 = a.xy[u0];
     double best = 0.0;
     bool found = false;
     int bu = -1, ntie = 0;
@@ -384,10 +383,10 @@ __global__ void __launch_bounds__(kBlock) k_L_req_push(int lo, int hi, LArgs a)
     const uint8_t fl = a.flags[t];
     const int o0 = a.out_start[t], o1 = a.out_start[t + 1], j0 = a.in_start[t], j1 = a.in_start[t + 1];
     const double dcell = o1 > o0 ? a.cell_delay[a.cell[t]] : 0.0;
-    const double2 pt = a.xy[t];
     const double cap = a.cap[t];
     const int v0 = o1 > o0 ? a.out_to[o0] : 0;
     pdl_wait();
+    const double2 pt = a.xy[t];
     double best = INFINITY;
     bool found = false;
     if (fl & 2) best = a.clock, found = true;
