@@ -141,6 +141,8 @@ struct tdpg_session {
     // Level-major copy of the timing graph for the push sweep (L-space index i <-> pin L_pin[i]; per
     // level its Input pins then its Output pins): every per-pin access of a level is coalesced.
     tdpg::DBuf<int> L_pin, L_in_start, L_in_from, L_out_start, L_out_to, L_cell, L_pred;
+    tdpg::DBuf<int> L_of; // pin -> L-space index
+    bool pins_stale = false; // the last STA left its results in L-space only (sta_materialize_pins)
     tdpg::DBuf<uint8_t> L_flags, L_ak, L_rk, L_tie; // flags: 1 source, 2 endpoint, 4 output
     tdpg::DBuf<double> L_cap, L_arr, L_req;
     tdpg::DBuf<double2> L_off, L_anchor, L_xy;
@@ -241,6 +243,7 @@ namespace tdpg {
 // session.cu
 void upload_positions(tdpg_session* s, const double* xy);
 void refresh_fixed_baseline(tdpg_session* s);
+void sta_materialize_pins(tdpg_session* s); // per-pin STA arrays of an L-space-only sweep (timing.cu)
 void ensure_grid(tdpg_session* s, int nx, int ny, double td);
 void set_density_model(tdpg_session* s, int model);
 void* cub_scratch(tdpg_session* s, size_t bytes);

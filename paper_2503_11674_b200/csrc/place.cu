@@ -44,6 +44,7 @@ struct Engine {
     cudaGraphExec_t refresh_gexec = nullptr; // the whole timing refresh, captured once
     cudaGraphExec_t sort_gexec = nullptr;    // spatial re-sort of the cells
     unsigned long long epoch = 0;            // dbuf_epoch() when the graphs were captured
+    bool refresh_lonly = false;              // the refresh graph leaves the STA results in L-space only
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
     int sort_every = 4; // iterations between spatial re-sorts of the cells (2: 0.310, 4: 0.301, 8: 0.334 ms/iteration at 1M)
     double last_refresh_ms = 0, total_refresh_ms = 0;
@@ -527,6 +528,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     G.refresh_gexec = capture(s, [&] {
         refresh_record(s, G.ctrl, G.timing_row, G.cfg.w0, G.cfg.w1, G.cfg.net_weighting != 0);
     });
+    G.refresh_lonly = s->pins_stale, s->pins_stale = false; // (recorded, not run)
     tr.mark("refresh graph");
     G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
     G.epoch = dbuf_epoch();
@@ -649,6 +651,7 @@ void timing_refresh(tdpg_session* s)
     CK(cudaEventCreate(&ev.second));
     CK(cudaEventRecord(ev.first, s->st));
     CK(cudaGraphLaunch(E.refresh_gexec, s->st));
+    s->pins_stale = E.refresh_lonly; // the sweep's per-pin arrays are left in L-space
     CK(cudaEventRecord(ev.second, s->st));
     E.refresh_ev.push_back(ev);
     // our kernels: pin_xy, 2 per level, slack keys, sta final, begin, ties, bt count, fill, bt write,
@@ -656,6 +659,7 @@ void timing_refresh(tdpg_session* s)
     E.kernel_launches += 2LL * s->L + 10 + (E.cfg.net_weighting ? 1 : 0);
     ++E.refreshes;
     if (s->round_cb) { // TimingRoundObserver (placer.cpp:434): this round's annotation and report
+        sta_materialize_pins(s); // the observer may read per-pin timing
         double h[3];
         long long c[3];
         CK(cudaMemcpyAsync(h, s->sta_out.p, sizeof h, cudaMemcpyDeviceToHost, s->st));
@@ -694,6 +698,7 @@ void ensure_graphs(tdpg_session* s, Engine& E)
     E.refresh_gexec = capture(s, [&] {
         refresh_record(s, E.ctrl, E.timing_row, E.cfg.w0, E.cfg.w1, E.cfg.net_weighting != 0);
     });
+    E.refresh_lonly = s->pins_stale, s->pins_stale = false;
     if (E.sort_gexec) cudaGraphExecDestroy(E.sort_gexec);
     E.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
     E.epoch = dbuf_epoch();

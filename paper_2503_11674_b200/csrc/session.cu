@@ -307,6 +307,7 @@ void build_graph(tdpg_session* s)
                 if (s->h_pin_dir[s->h_lvl_pins[i]] == 1) Lpin.push_back(s->h_lvl_pins[i]);
         }
         for (int i = 0; i < P; ++i) Lidx[Lpin[i]] = i;
+        s->L_of.upload(Lidx.empty() ? std::vector<int>(1, 0) : Lidx, s->st);
         std::vector<int> Lis(P + 1, 0), Lif, Los(P + 1, 0), Lot, Lcell(P);
         Lif.reserve(A), Lot.reserve(A);
         std::vector<uint8_t> Lfl(P);

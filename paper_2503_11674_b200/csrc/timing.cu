@@ -530,6 +530,55 @@ __global__ void __launch_bounds__(kBlock) k_slack_keys(int P, int EP, const doub
     }
 }
 
+// k_slack_keys on the L-space results (engine refresh): endpoint keys only, the per-pin slack array is
+// not written (sta_materialize_pins does it when a caller needs it).
+__global__ void __launch_bounds__(kBlock) k_slack_keys_L(int EP, const int* __restrict__ ep_sorted,
+                                                         const int* __restrict__ L_of,
+                                                         const double* __restrict__ L_arr,
+                                                         const double* __restrict__ L_req,
+                                                         unsigned long long* __restrict__ keys, int* __restrict__ vals,
+                                                         double* __restrict__ part)
+{
+    pdl_trigger();
+    pdl_wait();
+    __shared__ double sh[kBlock / 32];
+    __shared__ double shm[kBlock / 32];
+    __shared__ int shc[kBlock / 32];
+    double tns = 0.0, wns = 0.0;
+    int nv = 0;
+    for (int i = blockIdx.x * kBlock + threadIdx.x; i < EP; i += gridDim.x * kBlock) {
+        const int e = ep_sorted[i], u = L_of[e];
+        const double s = L_req[u] - L_arr[u];
+        const bool viol = s < 0.0;
+        keys[i] = viol ? double_key(s) : kNoKey;
+        vals[i] = e;
+        if (viol) tns += s, wns = fmin(wns, s), ++nv;
+    }
+    const double bt = block_sum<kBlock>(tns, sh);
+    double m = wns;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int c = nv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) shm[w] = m, shc[w] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = 0.0;
+        int cc = 0;
+        for (int k = 0; k < kBlock / 32; ++k) mm = fmin(mm, shm[k]), cc += shc[k];
+        part[3 * blockIdx.x] = bt, part[3 * blockIdx.x + 1] = mm, part[3 * blockIdx.x + 2] = cc;
+    }
+}
+
+__global__ void k_slack_all(int P, const double* __restrict__ arr, const double* __restrict__ req,
+                            double* __restrict__ slack)
+{
+    const int p = blockIdx.x * kBlock + threadIdx.x;
+    if (p < P) slack[p] = req[p] - arr[p];
+}
+
 __global__ void k_sta_final(int nb, const double* part, double* out3)
 {
     pdl_trigger();
@@ -588,6 +637,57 @@ __global__ void k_resolve_ties(StaArgs a, const int* __restrict__ level, int L, 
                     continue;
                 }
                 // lexicographic compare of b1[0..n1] vs b2[0..nb)
+                const int m = min(n1 + 1, nb);
+                int k = 0;
+                while (k < m && b1[k] == b2[k]) ++k;
+                const bool less = (k < m) ? (b1[k] < b2[k]) : (n1 + 1 < nb);
+                if (less) {
+                    for (int q = 0; q <= n1; ++q) b2[q] = b1[q];
+                    nb = n1 + 1, bu = u;
+                }
+            }
+            if (bu >= 0) a.pred[v] = bu;
+        }
+        __syncthreads();
+    }
+}
+
+// k_resolve_ties on the L-space results: tie_list holds L indices, paths are compared by pin id.
+__device__ int materialize_L(const int* L_pred, const int* L_pin, int v, int* buf)
+{
+    int n = 0;
+    for (int u = v; u >= 0; u = L_pred[u]) ++n;
+    int k = n;
+    for (int u = v; u >= 0; u = L_pred[u]) buf[--k] = L_pin[u];
+    return n;
+}
+
+__global__ void k_resolve_ties_L(LArgs a, const int* __restrict__ level, int L, int* scratch, int stride)
+{
+    const int ntie = a.counters[0];
+    if (ntie == 0) return;
+    int* b1 = scratch + static_cast<long long>(threadIdx.x) * 2 * stride;
+    int* b2 = b1 + stride;
+    for (int l = 1; l < L; ++l) {
+        for (int t = threadIdx.x; t < ntie; t += blockDim.x) {
+            const int v = a.tie_list[t];
+            const int pv_id = a.pin[v];
+            if (level[pv_id] != l) continue;
+            const bool sink = !(a.flags[v] & 4);
+            const double2 pv = a.xy[v];
+            int bu = -1, nb = 0;
+            for (int j = a.in_start[v]; j < a.in_start[v + 1]; ++j) {
+                const int u = a.in_from[j];
+                if (!a.ak[u]) continue;
+                const double d = sink ? net_delay(a.xy[u], pv, a.cap[v], a.r, a.c) : a.cell_delay[a.cell[v]];
+                if (a.arr[u] + d != a.arr[v]) continue;
+                const int n1 = materialize_L(a.pred, a.pin, u, b1);
+                b1[n1] = pv_id;
+                if (bu < 0) {
+                    for (int k = 0; k <= n1; ++k) b2[k] = b1[k];
+                    nb = n1 + 1, bu = u;
+                    continue;
+                }
                 const int m = min(n1 + 1, nb);
                 int k = 0;
                 while (k < m && b1[k] == b2[k]) ++k;
@@ -757,8 +857,42 @@ static bool sta_pdl()
     return on;
 }
 
-void sta_record(tdpg_session* s, double* out3)
+static LArgs make_largs(tdpg_session* s)
 {
+    LArgs la;
+    la.in_start = s->L_in_start, la.in_from = s->L_in_from, la.out_start = s->L_out_start;
+    la.out_to = s->L_out_to, la.cell = s->L_cell, la.pin = s->L_pin, la.flags = s->L_flags;
+    la.cap = s->L_cap, la.cell_delay = s->cell_delay, la.off = s->L_off, la.anchor = s->L_anchor;
+    la.xy = s->L_xy, la.r = s->r_unit, la.c = s->c_unit, la.clock = s->clock;
+    la.arr = s->L_arr, la.req = s->L_req, la.ak = s->L_ak, la.rk = s->L_rk, la.tie = s->L_tie;
+    la.pred = s->L_pred, la.akey = s->sta_akey, la.rkey = s->sta_rkey;
+    la.tie_list = s->tie_list, la.counters = s->counters;
+    return la;
+}
+
+// The L-space sweep is the default; pin_space = false (the engine's k = 1 refresh) leaves the results
+// there: endpoint keys and TNS / WNS straight from L-space, no per-pin arrays (s->pins_stale).
+static bool l_space_sweep() { return !all_levels_sweep() && !pin_order_push(); }
+
+// Per-pin arrays of an L-space-only sweep (arr, req, known flags, pred, tie list as pins, pin
+// positions, slack), for callers that read them.
+void sta_materialize_pins(tdpg_session* s)
+{
+    if (!s->pins_stale) return;
+    const int P = s->P;
+    const unsigned nbP = blocks_for(std::max(P, 1), kBlock);
+    k_L_to_pins<<<nbP, kBlock, 0, s->st>>>(P, make_largs(s), s->arr, s->req, s->ak, s->rk, s->pred);
+    if (!s->pin_xy_external)
+        k_pin_xy<<<nbP, kBlock, 0, s->st>>>(P, s->pin_cell, s->pin_off, s->cell_xy, s->anchor, s->pin_xy);
+    k_slack_all<<<nbP, kBlock, 0, s->st>>>(P, s->arr, s->req, s->slack);
+    CK_LAUNCH();
+    s->pins_stale = false;
+}
+
+void sta_record(tdpg_session* s, double* out3, bool pin_space)
+{
+    const bool lonly = !pin_space && l_space_sweep() && s->sta_grid <= 0;
+    s->pins_stale = lonly;
     const int P = s->P;
     const bool persist = s->sta_grid > 0;
     if (!s->pin_xy_external && !persist && all_levels_sweep()) { // pin positions from the cells (netlist.cpp:23-32) unless given
@@ -780,14 +914,7 @@ void sta_record(tdpg_session* s, double* out3)
                               static_cast<const double2*>(s->pin_off.p), static_cast<const double2*>(s->cell_xy.p),
                               static_cast<const double2*>(s->anchor.p), s->grid_bar.p));
     } else if (!all_levels_sweep() && !pin_order_push()) { // L-space push sweep (default)
-        LArgs la;
-        la.in_start = s->L_in_start, la.in_from = s->L_in_from, la.out_start = s->L_out_start;
-        la.out_to = s->L_out_to, la.cell = s->L_cell, la.pin = s->L_pin, la.flags = s->L_flags;
-        la.cap = s->L_cap, la.cell_delay = s->cell_delay, la.off = s->L_off, la.anchor = s->L_anchor;
-        la.xy = s->L_xy, la.r = s->r_unit, la.c = s->c_unit, la.clock = s->clock;
-        la.arr = s->L_arr, la.req = s->L_req, la.ak = s->L_ak, la.rk = s->L_rk, la.tie = s->L_tie;
-        la.pred = s->L_pred, la.akey = s->sta_akey, la.rkey = s->sta_rkey;
-        la.tie_list = s->tie_list, la.counters = s->counters;
+        const LArgs la = make_largs(s);
         const unsigned nbP = blocks_for(P, kBlock);
         k_L_init<<<nbP, kBlock, 0, s->st>>>(P, la, !s->pin_xy_external, s->cell_xy, s->pin_xy);
         const bool pdl = sta_pdl();
@@ -805,10 +932,13 @@ void sta_record(tdpg_session* s, double* out3)
             first = first && !(hi > lo);
         }
         CK(launch_pdl(k_L_req_decode, nbP, kBlock, s->st, pdl, P, la));
-        CK(launch_pdl(k_L_to_pins, nbP, kBlock, s->st, pdl, P, la, s->arr.p, s->req.p, s->ak.p, s->rk.p, s->pred.p));
-        if (!s->pin_xy_external)
-            CK(launch_pdl(k_pin_xy, nbP, kBlock, s->st, pdl, P, s->pin_cell.p, s->pin_off.p, s->cell_xy.p, s->anchor.p,
-                          s->pin_xy.p));
+        if (!lonly) {
+            CK(launch_pdl(k_L_to_pins, nbP, kBlock, s->st, pdl, P, la, s->arr.p, s->req.p, s->ak.p, s->rk.p,
+                          s->pred.p));
+            if (!s->pin_xy_external)
+                CK(launch_pdl(k_pin_xy, nbP, kBlock, s->st, pdl, P, s->pin_cell.p, s->pin_off.p, s->cell_xy.p,
+                              s->anchor.p, s->pin_xy.p));
+        }
     } else if (!all_levels_sweep()) { // push sweep over sink levels in pin order (see k_arr_push)
         k_sta_init<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, a, !s->pin_xy_external, s->pin_off, s->cell_xy,
                                                                  s->anchor, s->sta_akey, s->sta_rkey);
@@ -841,8 +971,12 @@ void sta_record(tdpg_session* s, double* out3)
     }
     const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
     const bool pdl = sta_pdl();
-    CK(launch_pdl(k_slack_keys, nb, kBlock, s->st, pdl, P, s->EP, s->arr.p, s->req.p, s->slack.p, s->ep_sorted.p,
-                  s->sort_k0.p, s->sort_v0.p, s->sta_part.p));
+    if (lonly)
+        CK(launch_pdl(k_slack_keys_L, nb, kBlock, s->st, pdl, s->EP, s->ep_sorted.p, s->L_of.p, s->L_arr.p,
+                      s->L_req.p, s->sort_k0.p, s->sort_v0.p, s->sta_part.p));
+    else
+        CK(launch_pdl(k_slack_keys, nb, kBlock, s->st, pdl, P, s->EP, s->arr.p, s->req.p, s->slack.p,
+                      s->ep_sorted.p, s->sort_k0.p, s->sort_v0.p, s->sta_part.p));
     CK(launch_pdl(k_sta_final, 1, kBlock, s->st, pdl, nb, s->sta_part.p, out3));
 }
 
@@ -881,7 +1015,7 @@ void run_sta_async(tdpg_session* s, double* out3)
         if (s->sta_gexec) cudaGraphExecDestroy(s->sta_gexec), s->sta_gexec = nullptr;
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
-        sta_record(s, out3);
+        sta_record(s, out3, true);
         CK(cudaStreamEndCapture(s->st, &g));
         CK(cudaGraphInstantiate(&s->sta_gexec, g, 0));
         cudaGraphDestroy(g);
@@ -1149,6 +1283,53 @@ __global__ void k_bt_write_dev(int EP, const double* __restrict__ sta_out, const
     }
 }
 
+// k_bt_count_dev / k_bt_write_dev walking the L-space predecessors (pins translated on output).
+__global__ void k_bt_count_L(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                             const int* __restrict__ ep, const int* __restrict__ L_of, const int* __restrict__ L_pred,
+                             const uint8_t* __restrict__ L_flags, int* __restrict__ len, int* __restrict__ hops)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= EP) return;
+    const int n_paths = refresh_active(sta_out, ctrl) ? static_cast<int>(sta_out[2]) : 0;
+    if (i >= n_paths) {
+        len[i] = 0, hops[i] = 0;
+        return;
+    }
+    int v = L_of[ep[i]], l = 1, h = 0;
+    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) ++l, h += (L_flags[u] & 4) != 0;
+    len[i] = l, hops[i] = h;
+}
+
+__global__ void k_bt_write_L(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                             const int* __restrict__ ep, const int* __restrict__ L_of, const int* __restrict__ L_pin,
+                             const int* __restrict__ L_pred, const uint8_t* __restrict__ L_flags,
+                             const int* __restrict__ len, const int* __restrict__ off, const int* __restrict__ hops,
+                             const int* __restrict__ hoff, const double* __restrict__ L_arr, double clock,
+                             int* __restrict__ pins, double* __restrict__ pslack, unsigned* __restrict__ hkey,
+                             double* __restrict__ hslack, int* __restrict__ hidx)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= EP || len[i] == 0) return;
+    const int e = ep[i];
+    int v = L_of[e];
+    const double sl = clock - L_arr[v]; // paths.cpp:123
+    pslack[i] = sl;
+    int k = off[i] + len[i] - 1, h = hoff[i] + hops[i] - 1;
+    pins[k] = e;
+    int vp = e; // pin id of v
+    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) {
+        const int up = L_pin[u];
+        pins[--k] = up;
+        if (L_flags[u] & 4) {
+            hkey[h] = sl < 0.0 ? static_cast<unsigned>(vp) : 0xFFFFFFFFu; // pin_pairs.cpp:11
+            hslack[h] = sl;
+            hidx[h] = h;
+            --h;
+        }
+        vp = up;
+    }
+}
+
 __global__ void k_fill_u32(long long n, unsigned* p, unsigned v)
 {
     for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < n;
@@ -1256,7 +1437,9 @@ void refresh_reserve(tdpg_session* s)
 // The whole refresh, stream-ordered and host-sync-free (captured by the engine).
 void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting)
 {
-    sta_record(s, s->sta_out);
+    // net weighting reads every pin's slack: keep the per-pin arrays then
+    sta_record(s, s->sta_out, net_weighting);
+    const bool lonly = s->pins_stale;
     k_refresh_begin<<<1, 1, 0, s->st>>>(s->sta_out, ctrl, timing_row);
     CK_LAUNCH();
     const int EP = s->EP;
@@ -1264,10 +1447,15 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     size_t bytes = s->cub_tmp.n;
     CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP,
                                        0, 64, s->st));
-    k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), s->d_level, s->L, s->tie_scratch, s->L + 2);
-    CK_LAUNCH();
-    k_bt_count_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred,
-                                                                 s->pin_dir, s->ex_len, s->ex_hops);
+    if (lonly) {
+        k_resolve_ties_L<<<1, kBlock, 0, s->st>>>(make_largs(s), s->d_level, s->L, s->tie_scratch, s->L + 2);
+        k_bt_count_L<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->L_of,
+                                                                   s->L_pred, s->L_flags, s->ex_len, s->ex_hops);
+    } else {
+        k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), s->d_level, s->L, s->tie_scratch, s->L + 2);
+        k_bt_count_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred,
+                                                                     s->pin_dir, s->ex_len, s->ex_hops);
+    }
     CK_LAUNCH();
     bytes = s->cub_tmp.n;
     CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_len.p, s->ex_off.p, EP, s->st));
@@ -1276,10 +1464,17 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     const long long H = s->hcap;
     k_fill_u32<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 8), kBlock, 0, s->st>>>(H, s->eh_key, 0xFFFFFFFFu);
     CK_LAUNCH();
-    k_bt_write_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred, s->pin_dir,
-                                                                 s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff, s->arr,
-                                                                 s->clock, s->ex_pins, s->ex_slack, s->eh_key,
-                                                                 s->eh_slack, s->eh_idx);
+    if (lonly)
+        k_bt_write_L<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->L_of, s->L_pin,
+                                                                   s->L_pred, s->L_flags, s->ex_len, s->ex_off,
+                                                                   s->ex_hops, s->ex_hoff, s->L_arr, s->clock,
+                                                                   s->ex_pins, s->ex_slack, s->eh_key, s->eh_slack,
+                                                                   s->eh_idx);
+    else
+        k_bt_write_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred,
+                                                                     s->pin_dir, s->ex_len, s->ex_off, s->ex_hops,
+                                                                     s->ex_hoff, s->arr, s->clock, s->ex_pins,
+                                                                     s->ex_slack, s->eh_key, s->eh_slack, s->eh_idx);
     CK_LAUNCH();
     k_extract_counts<<<1, 1, 0, s->st>>>(EP, s->sta_out, ctrl, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff,
                                          s->ex_counts);
