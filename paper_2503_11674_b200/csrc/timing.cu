@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(kBlock) k_L_init(int P, LArgs a, bool from_cel
         a.xy[i] = pin_xy[a.pin[i]];
     }
     const uint8_t f = a.flags[i];
+    if (!(f & 4)) return; // keys are read and pushed for Output pins only (Input pins store arr / req)
     a.akey[i] = (f & 1) ? double_key(0.0) : kNoArr;
     a.rkey[i] = (f & 2) ? double_key(a.clock) : kNoReq;
 }
