@@ -160,6 +160,8 @@ struct tdpg_session {
     tdpg::DBuf<double> sta_part; // STA reduction partials
     cudaGraphExec_t sta_gexec = nullptr; // the per-level STA sweep, captured once
     std::array<uint64_t, 9> sta_graph_key{};
+    cudaGraphExec_t sta_gexec_L = nullptr; // the same sweep leaving its results in L-space
+    std::array<uint64_t, 9> sta_graph_key_L{};
     // ledger-update scratch
     tdpg::DBuf<uint8_t> lg_flag;
     tdpg::DBuf<double> lg_w, lg_new_w;
@@ -261,7 +263,7 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
                          double* d_cell_host);
 
 // timing.cu
-void run_sta_dev(tdpg_session* s);
+void run_sta_dev(tdpg_session* s, bool pin_space = true); // pin_space = false: results left in L-space
 void sta_setup(tdpg_session* s);
 void refresh_reserve(tdpg_session* s);
 void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting);

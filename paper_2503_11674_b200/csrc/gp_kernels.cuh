@@ -162,7 +162,7 @@ void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cu
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
                   const IterCur* cur, Ctrl* ctrl, bool dens_grad = true, const double2* folded = nullptr);
 void launch_fold(tdpg_session* s, double2* out, const Ctrl* ctrl);
-void run_sta_async(tdpg_session* s, double* out3);
+void run_sta_async(tdpg_session* s, double* out3, bool pin_space = true);
 void ledger_apply_sorted(tdpg_session* s, long long H, double wns, double w0, double w1);
 int api_fail(int kind, const std::string& msg);
 

@@ -25,7 +25,6 @@
 namespace tdpg {
 
 int api_fail(int kind, const std::string& msg);
-void run_sta_dev(tdpg_session* s);
 void* cub_scratch(tdpg_session* s, size_t bytes);
 
 namespace {
@@ -332,6 +331,7 @@ void exclusive_scan(tdpg_session* s, const int* in, int* out, int n)
 // The K-best lists of every pin at the current STA's pin positions.
 void kbest_build(tdpg_session* s, int K)
 {
+    sta_materialize_pins(s);
     const size_t P = static_cast<size_t>(std::max(s->P, 1));
     const double bytes = static_cast<double>(P) * K * (sizeof(double) + sizeof(int2));
     if (K < 1 || bytes > 48e9)

@@ -762,6 +762,7 @@ tdpg_session::~tdpg_session()
     delete eng; // Engine is complete here
     tdpg::comm_destroy(this);
     if (sta_gexec) cudaGraphExecDestroy(sta_gexec);
+    if (sta_gexec_L) cudaGraphExecDestroy(sta_gexec_L);
     if (st) {
         cudaStreamSynchronize(st);
         cudaCtxResetPersistingL2Cache(); // release the L2 lines this session pinned

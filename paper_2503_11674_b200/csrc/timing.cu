@@ -746,6 +746,48 @@ __global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restr
     }
 }
 
+// k_bt_count / k_bt_write on L-space predecessors (an L-space-only STA), pins translated on output.
+__global__ void k_bt_count_Ln(int n, const int* __restrict__ ep, const int* __restrict__ L_of,
+                              const int* __restrict__ L_pred, const uint8_t* __restrict__ L_flags,
+                              int* __restrict__ len, int* __restrict__ hops)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    int v = L_of[ep[i]], l = 1, h = 0;
+    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) ++l, h += (L_flags[u] & 4) != 0;
+    len[i] = l, hops[i] = h;
+}
+
+__global__ void k_bt_write_Ln(int n, const int* __restrict__ ep, const int* __restrict__ L_of,
+                              const int* __restrict__ L_pin, const int* __restrict__ L_pred,
+                              const uint8_t* __restrict__ L_flags, const int* __restrict__ len,
+                              const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
+                              const double* __restrict__ L_arr, double clock, int* __restrict__ pins,
+                              double* __restrict__ pslack, unsigned long long* __restrict__ hkey,
+                              double* __restrict__ hslack, int* __restrict__ hidx)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const int e = ep[i];
+    int v = L_of[e], vp = e;
+    const double sl = clock - L_arr[v]; // paths.cpp:123
+    pslack[i] = sl;
+    int k = off[i] + len[i] - 1, h = hoff[i] + hops[i] - 1;
+    pins[k] = e;
+    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) {
+        const int up = L_pin[u];
+        pins[--k] = up;
+        if (L_flags[u] & 4) {
+            const unsigned lo = static_cast<unsigned>(min(up, vp)), hi = static_cast<unsigned>(max(up, vp));
+            hkey[h] = (static_cast<unsigned long long>(lo) << 32) | hi;
+            hslack[h] = sl;
+            hidx[h] = h;
+            --h;
+        }
+        vp = up;
+    }
+}
+
 __global__ void k_count_heads(long long n, const unsigned long long* __restrict__ k, int* __restrict__ out)
 {
     int c = 0;
@@ -1000,7 +1042,7 @@ void sta_setup(tdpg_session* s)
     s->sta_grid = sms * std::max(1, std::min(per_sm, b ? std::atoi(b) : 2));
 }
 
-void run_sta_async(tdpg_session* s, double* out3)
+void run_sta_async(tdpg_session* s, double* out3, bool pin_space)
 {
     const size_t ep = static_cast<size_t>(std::max(s->EP, 1));
     s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
@@ -1012,23 +1054,27 @@ void run_sta_async(tdpg_session* s, double* out3)
     const std::array<uint64_t, 9> key = {ptr(s->pin_xy_external ? s->pin_xy.p : nullptr), ptr(s->cell_xy.p),
                                          ptr(s->sort_k0.p), ptr(s->sort_v0.p), ptr(s->sta_part.p), ptr(out3),
                                          bits(s->clock), bits(s->r_unit), bits(s->c_unit)};
-    if (!s->sta_gexec || key != s->sta_graph_key) {
-        if (s->sta_gexec) cudaGraphExecDestroy(s->sta_gexec), s->sta_gexec = nullptr;
+    const bool lonly = !pin_space && l_space_sweep() && s->sta_grid <= 0;
+    cudaGraphExec_t& gx = lonly ? s->sta_gexec_L : s->sta_gexec;
+    std::array<uint64_t, 9>& gk = lonly ? s->sta_graph_key_L : s->sta_graph_key;
+    if (!gx || key != gk) {
+        if (gx) cudaGraphExecDestroy(gx), gx = nullptr;
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
-        sta_record(s, out3, true);
+        sta_record(s, out3, !lonly);
         CK(cudaStreamEndCapture(s->st, &g));
-        CK(cudaGraphInstantiate(&s->sta_gexec, g, 0));
+        CK(cudaGraphInstantiate(&gx, g, 0));
         cudaGraphDestroy(g);
-        s->sta_graph_key = key;
+        gk = key;
     }
-    CK(cudaGraphLaunch(s->sta_gexec, s->st));
+    CK(cudaGraphLaunch(gx, s->st));
+    s->pins_stale = lonly;
 }
 
-void run_sta_dev(tdpg_session* s)
+void run_sta_dev(tdpg_session* s, bool pin_space)
 {
     s->sta_out.reserve(4);
-    run_sta_async(s, s->sta_out);
+    run_sta_async(s, s->sta_out, pin_space);
     double h[3];
     s->sta_out.download(h, 3, s->st);
     CK(cudaStreamSynchronize(s->st));
@@ -1040,6 +1086,7 @@ void run_sta_dev(tdpg_session* s)
 // Exact-delay ties of the last STA resolved to the lexicographically smallest path (idempotent).
 void resolve_ties_dev(tdpg_session* s)
 {
+    sta_materialize_pins(s);
     if (s->ties_resolved) return;
     const int stride = s->L + 2;
     s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * stride);
@@ -1052,6 +1099,7 @@ void resolve_ties_dev(tdpg_session* s)
 // how many endpoints violate.
 int sorted_violated(tdpg_session* s)
 {
+    sta_materialize_pins(s);
     s->sta_out.reserve(4);
     double* out3 = s->sta_out.p;
     const int P = s->P;
@@ -1081,7 +1129,8 @@ int sorted_violated(tdpg_session* s)
 // report_timing_endpoint(n, k = 1) on the current STA (paths.cpp:167-189).
 void extract_endpoint_dev(tdpg_session* s, int n)
 {
-    if (!s->sta_valid) run_sta_dev(s);
+    if (!s->sta_valid) run_sta_dev(s, false);
+    const bool Lsp = s->pins_stale; // the sweep's results are in L-space (no per-pin arrays)
     // endpoint keys from the current STA (cheap; keeps extraction self-contained)
     s->sta_out.reserve(4);
     double* out3 = s->sta_out.p;
@@ -1091,8 +1140,12 @@ void extract_endpoint_dev(tdpg_session* s, int n)
         s->part.reserve(3 * nb + 8);
         const size_t ep = static_cast<size_t>(std::max(s->EP, 1));
         s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
-        k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0,
-                                               s->sort_v0, s->part);
+        if (Lsp)
+            k_slack_keys_L<<<nb, kBlock, 0, s->st>>>(s->EP, s->ep_sorted, s->L_of, s->L_arr, s->L_req, s->sort_k0,
+                                                     s->sort_v0, s->part);
+        else
+            k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0,
+                                                   s->sort_v0, s->part);
         CK_LAUNCH();
         k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
         CK_LAUNCH();
@@ -1108,7 +1161,15 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     }
     // ties: resolve before any backtrace
     {
-        resolve_ties_dev(s);
+        if (!Lsp) {
+            resolve_ties_dev(s);
+        } else if (!s->ties_resolved) {
+            const int stride = s->L + 2;
+            s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * stride);
+            k_resolve_ties_L<<<1, kBlock, 0, s->st>>>(make_largs(s), s->d_level, s->L, s->tie_scratch, stride);
+            CK_LAUNCH();
+            s->ties_resolved = true;
+        }
         double h[3];
         CK(cudaMemcpyAsync(h, out3, sizeof h, cudaMemcpyDeviceToHost, s->st));
         CK(cudaStreamSynchronize(s->st));
@@ -1121,8 +1182,12 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     if (np == 0) return;
     s->ex_len.reserve(np), s->ex_hops.reserve(np), s->ex_off.reserve(np), s->ex_hoff.reserve(np);
     s->ex_slack.reserve(np);
-    k_bt_count<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
-                                                             s->ex_hops);
+    if (Lsp)
+        k_bt_count_Ln<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->L_of, s->L_pred, s->L_flags,
+                                                                    s->ex_len, s->ex_hops);
+    else
+        k_bt_count<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
+                                                                 s->ex_hops);
     CK_LAUNCH();
     size_t bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->ex_len.p, s->ex_off.p, np, s->st);
@@ -1141,10 +1206,16 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     s->ex_pins.reserve(s->n_path_pins + 1);
     s->hit_key.reserve(H + 1), s->hit_slack.reserve(H + 1), s->hit_idx.reserve(H + 1);
     s->hit_key_s.reserve(H + 1), s->hit_idx_s.reserve(H + 1);
-    k_bt_write<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
-                                                             s->ex_off, s->ex_hops, s->ex_hoff, s->arr, s->clock,
-                                                             s->ex_pins, s->ex_slack, s->hit_key, s->hit_slack,
-                                                             s->hit_idx);
+    if (Lsp)
+        k_bt_write_Ln<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->L_of, s->L_pin, s->L_pred,
+                                                                    s->L_flags, s->ex_len, s->ex_off, s->ex_hops,
+                                                                    s->ex_hoff, s->L_arr, s->clock, s->ex_pins,
+                                                                    s->ex_slack, s->hit_key, s->hit_slack, s->hit_idx);
+    else
+        k_bt_write<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
+                                                                 s->ex_off, s->ex_hops, s->ex_hoff, s->arr, s->clock,
+                                                                 s->ex_pins, s->ex_slack, s->hit_key, s->hit_slack,
+                                                                 s->hit_idx);
     CK_LAUNCH();
     if (H > 0) {
         bytes = 0;
@@ -1397,6 +1468,7 @@ __global__ void k_net_weights_dev(int N, const int* __restrict__ net_start, cons
 void net_weights_engine(tdpg_session* s, const Ctrl* ctrl)
 {
     if (!s->N) return;
+    sta_materialize_pins(s);
     k_net_weights_dev<<<blocks_for(s->N, kBlock), kBlock, 0, s->st>>>(s->N, s->net_start, s->net_pins, s->slack,
                                                                       s->sta_out, ctrl, s->net_w);
     CK_LAUNCH();
@@ -1574,7 +1646,7 @@ int tdpg_sta(tdpg_session* s, double* arr, double* req, double* slack, uint8_t* 
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s->st));
-    run_sta_dev(s);
+    run_sta_dev(s, arr || req || slack || ak || rk); // no per-pin outputs asked for: leave them in L-space
     CK(cudaEventRecord(e1, s->st));
     CK(cudaEventSynchronize(e1));
     float ms = 0;
@@ -1597,7 +1669,8 @@ static void extract_timed(tdpg_session* s, int policy, int n, int k)
 {
     if (k < 1) throw Error(TDPG_ERR_VALIDATION, "validation error: k must be >= 1");
     if (policy != 0 && policy != 1) throw Error(TDPG_ERR_VALIDATION, "validation error: policy must be \"endpoint\" or \"topn\"");
-    if (!s->sta_valid) run_sta_dev(s);
+    // report_timing_endpoint(n, 1) reads the sweep in L-space; the other policies need the per-pin arrays
+    if (!s->sta_valid) run_sta_dev(s, !(policy == 0 && k == 1));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -1720,6 +1793,7 @@ int tdpg_sta_fetch(tdpg_session* s, double* arr, double* req, double* slack, uin
 {
     API_BEGIN
     if (!s->sta_valid) throw Error(TDPG_ERR_GRAPH, "graph error: no timing annotation (run tdpg_sta first)");
+    sta_materialize_pins(s);
     const size_t P = static_cast<size_t>(s->P);
     if (arr) s->arr.download(arr, P, s->st);
     if (req) s->req.download(req, P, s->st);
@@ -1754,7 +1828,7 @@ int tdpg_path_to(tdpg_session* s, int32_t pin, int32_t rank, int32_t* pins, int3
         return TDPG_OK;
     }
     if (!s->sta_valid) run_sta_dev(s);
-    resolve_ties_dev(s);
+    resolve_ties_dev(s); // (materialises the per-pin arrays of an L-space-only STA)
     uint8_t known = 0;
     CK(cudaMemcpyAsync(&known, s->ak.p + pin, 1, cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));

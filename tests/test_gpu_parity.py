@@ -373,3 +373,27 @@ def test_fine_grid_density_mixed_wide_cells(seed):
         to, go = o.objective(nx=nx, ny=ny, td=0.3, gamma=0.3, lam=0.7, beta=0.0, kind=0)
         assert np.allclose(ts, to, rtol=1e-9, atol=1e-12), (ts, to)
         assert field_err(gs, go) <= 1e-9
+
+
+@pytest.mark.parametrize("seed", [3, 8, 17, 29, 44])
+def test_l_space_sta_then_per_pin_consumers(seed):
+    """An STA asked for no per-pin outputs leaves its results in the level-major copy; every consumer
+    of the per-pin arrays that follows (rank-0 path_to, k_worst, the topn policy, a full STA fetch)
+    sees the same results as after a per-pin STA, bitwise against the oracle."""
+    d = random_design(seed)
+    s, o = Session(d), Oracle(d)
+    es, eo = s.extract(n=0), o.extract(n=0)  # (tdpg_sta without outputs, then the L-space backtrace)
+    assert _paths(es) == _paths(eo) and np.array_equal(es["slack"], eo["slack"])
+    for ep in d.endpoints[:4]:
+        po, so = o.k_worst(int(ep), 3)
+        got = s.path_to(int(ep), 0)  # rank 0 = the worst path, the first of k_worst
+        assert (got[0] if got else []) == (po[0] if po else [])
+        pg, sg = s.k_worst(int(ep), 3)
+        assert pg == po and np.array_equal(sg, so)
+    es = s.extract(n=0, policy=1, run_sta=False)
+    eo = o.extract(n=0, policy=1)
+    assert _paths(es) == _paths(eo) and np.array_equal(es["slack"], eo["slack"])
+    s.extract(n=0)  # L-space again, then the per-pin arrays through a fetch-style STA read
+    ts, to = s.sta(), o.sta()
+    for k in ("arr", "req", "slack", "arr_known", "req_known"):
+        assert np.array_equal(ts[k], to[k]), k
