@@ -126,6 +126,7 @@ struct tdpg_session {
     int n_wa_blocks = 0, E_lay = 0;
     int wa_cls_blk0[9] = {0}, wa_cls_nblk[9] = {0};
     int wa_cls_net0[9] = {0}, wa_cls_net1[9] = {0}, wa_cls_pos0[9] = {0}; // (WaAxisArgs)
+    int wa_gen_nets = 0; // generic (class 0) nets: order positions [0, wa_gen_nets)
     // engine-mode pin pairs (dense ledger indexed by sink pin; fused into WA)
     tdpg::DBuf<uint32_t> pp_mask, pp_ord;   // per class-ordered net
     tdpg::DBuf<int> wa_gen_ord, pin_loc, pin_driver;

@@ -482,10 +482,11 @@ __device__ __forceinline__ void wa_half_net(int sub, int s0, int n, int kmax, do
     if (sub == 0 && live) wl += w * (vx + vy), hp += hx + hy;
 }
 
-__global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __restrict__ blk,
+// Block g holds generic nets [16 (g - gen_blk0), +16) of the order; a net's pin count is the difference of
+// consecutive layout starts (gen_start has a sentinel), so no net table is read ahead of the entries.
+__global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, int gen_blk0, int gen_nets,
                                                        const int* __restrict__ net_by_size,
                                                        const int* __restrict__ gen_start,
-                                                       const int* __restrict__ net_start,
                                                        const int* __restrict__ e_cell,
                                                        const double2* __restrict__ e_off,
                                                        const double2* __restrict__ cell_xy,
@@ -497,27 +498,24 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
                                                        const Ctrl* __restrict__ ctrl)
 {
     __shared__ double sh[3 * kBlock / 32];
-    if (ctrl && ctrl->stopped) return;
-    const int4 b = blk[blk0 + blockIdx.x];
+    const bool stop = ctrl && ctrl->stopped; // (checked once the net sizes are loaded)
+    const int first = (blk0 + blockIdx.x - gen_blk0) * 16;
+    const int4 b = make_int4(0, first, min(16, gen_nets - first), 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double wl = 0.0, hp = 0.0, ppv = 0.0;
     // nets in pairs per warp: two nets of <= 16 pins share the warp (a half each); otherwise the warp
     // takes them one after the other
     const int t0 = 2 * warp, t1 = t0 + 1;
-    auto size_of = [&](int t) {
-        if (t >= b.z) return 0;
-        const int net = net_by_size[b.y + t];
-        return net_start[net + 1] - net_start[net];
-    };
+    auto size_of = [&](int t) { return t < b.z ? gen_start[b.y + t + 1] - gen_start[b.y + t] : 0; };
     const int n0 = size_of(t0), n1 = size_of(t1);
+    if (stop) return; // (uniform over the block)
     const bool halves = t0 < b.z && n0 <= 16 && n1 <= 16;
     if (halves) {
         const int seg = lane >> 4, t = seg ? t1 : t0, n = seg ? n1 : n0;
         const bool have = t < b.z;
         const int i = b.y + (have ? t : t0);
-        const int net = net_by_size[i];
         const int s0 = gen_start[i];
-        const double w = net_w ? net_w[net] : 1.0;
+        const double w = net_w ? net_w[net_by_size[i]] : 1.0;
         const int kmax = max(n0, n1) - 1;
         double wl_l = 0.0, hp_l = 0.0, pp_l = 0.0;
         wa_half_net(lane & 15, s0, have ? n : 0, kmax, w, e_cell, e_off, cell_xy, anchor, inv_gamma, grad_e, pp,
@@ -526,9 +524,8 @@ __global__ void __launch_bounds__(kBlock) k_wa_generic(int blk0, const int4* __r
     }
     for (int t = halves ? b.z : t0; t < b.z && t <= t1; ++t) { // one warp per net
         const int i = b.y + t;
-        const int net = net_by_size[i];
-        const int s0 = gen_start[i], n = net_start[net + 1] - net_start[net];
-        const double w = net_w ? net_w[net] : 1.0;
+        const int s0 = gen_start[i], n = gen_start[i + 1] - s0;
+        const double w = net_w ? net_w[net_by_size[i]] : 1.0;
         if (n < 2) {
             for (int k = lane; k < n; k += 32) grad_e[s0 + k] = make_double2(0.0, 0.0);
             continue;
@@ -1411,8 +1408,8 @@ void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double*
     }
     int g0, gn;
     if (wa_range(s, 0, g0, gn)) {
-        k_wa_generic<<<gn, kBlock, 0, st(0)>>>(g0, s->wa_blk, s->net_by_size,
-                                                              s->wa_gen_start, s->net_start, s->e_cell, s->e_off,
+        k_wa_generic<<<gn, kBlock, 0, st(0)>>>(g0, s->wa_cls_blk0[0], s->wa_gen_nets, s->net_by_size,
+                                                              s->wa_gen_start, s->e_cell, s->e_off,
                                                               s->cell_xy, s->anchor, nw, ig, s->grad_e, part_wl,
                                                               part_hp, pp, s->wa_gen_ord, ppart, ctrl);
         CK_LAUNCH();

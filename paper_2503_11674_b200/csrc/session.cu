@@ -454,7 +454,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     for (int k = 0; k <= kMaxN; ++k) cnt[k + 1] += cnt[k];
     std::vector<int> order(std::max(N, 1)), fill(cnt.begin(), cnt.end() - 1);
     for (int n = 0; n < N; ++n) order[fill[cls(s->h_net_start[n + 1] - s->h_net_start[n])]++] = n;
-    std::vector<int> new_id(std::max(E, 1), -1), gen_start(std::max(N, 1), 0);
+    std::vector<int> new_id(std::max(E, 1), -1), gen_start(std::max(N, 1) + 1, 0);
     std::vector<int4> blk;
     int pos = 0;
     for (int k = 2; k <= kMaxN; ++k) {
@@ -479,6 +479,8 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         for (int j = 0; j < k; ++j) new_id[b0 + j] = pos + j;
         pos += k;
     }
+    gen_start[cnt[1]] = pos; // sentinel: generic net i has gen_start[i + 1] - gen_start[i] pins
+    s->wa_gen_nets = cnt[1];
     s->n_wa_blocks = static_cast<int>(blk.size());
     s->part_b0 = 0, s->part_b1 = s->n_wa_blocks; // whole design until tdpg_set_partition / tdpg_comm_init
     s->E_lay = pos;
