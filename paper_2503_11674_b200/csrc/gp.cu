@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
 {
     __shared__ unsigned win_lo[kWinBins], win_hi[kWinBins];
     __shared__ int bb[4];
-    if (ctrl && ctrl->stopped) return;
+    const bool stop = ctrl && ctrl->stopped; // (checked once the cell loads are in flight)
     const int i = blockIdx.x * kBlock + threadIdx.x;
     const bool valid = i < n_mov;
     double2 p = make_double2(0, 0), s = make_double2(1, 1);
@@ -774,6 +774,7 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
         if (fast)
             bx0 = max(bx, 0), bx1 = min(bx + kF5 - 1, g.nx - 1), by0 = max(by, 0), by1 = min(by + kF5 - 1, g.ny - 1);
     }
+    if (stop) return; // (uniform over the block)
     if (threadIdx.x == 0) bb[0] = INT_MAX, bb[1] = INT_MIN, bb[2] = INT_MAX, bb[3] = INT_MIN;
     int a0 = bx0, a1 = bx1, c0 = by0, c1 = by1;
 #pragma unroll
@@ -1054,12 +1055,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* _
     // earlier kernels is read after pdl_wait())
     pdl_trigger();
     pdl_wait();
-    if (ctrl && ctrl->stopped) return;
+    const bool stop = ctrl && ctrl->stopped;
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n_mov) return;
     const int c = perm[i];
     const double2 p = cell_xy[c], s = cell_wh[c];
-    if (s.x > g.wide_w || s.y > g.wide_h) return;
+    if (stop || s.x > g.wide_w || s.y > g.wide_h) return;
     double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
     int bx, by;
     axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx);
