@@ -446,20 +446,21 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     InitTrace tr(s);
     validate_config(*cfg);
     auto E = std::make_unique<Engine>();
+    E->cfg = *cfg;
+    const double cw = s->core[2] - s->core[0], ch = s->core[3] - s->core[1];
+    E->span = cw > ch ? cw : ch; // Rect::span (geometry.hpp:34)
+    E->gamma = cfg->gamma_frac * E->span;
+
+    // implicit starts get a seeded jitter (placer.cpp:375-382), on the device; the host work below
+    // (old engine, graph captures) overlaps it
+    jitter_positions(s, cfg, pos_explicit, cw, ch, &tr);
+    tr.mark("jitter");
     {
         std::unique_ptr<Engine> old(s->eng);
         s->eng = nullptr;
         if (old) E->recycle(*old);
     }
     tr.mark("old engine recycled");
-    E->cfg = *cfg;
-    const double cw = s->core[2] - s->core[0], ch = s->core[3] - s->core[1];
-    E->span = cw > ch ? cw : ch; // Rect::span (geometry.hpp:34)
-    E->gamma = cfg->gamma_frac * E->span;
-
-    // implicit starts get a seeded jitter (placer.cpp:375-382), on the device
-    jitter_positions(s, cfg, pos_explicit, cw, ch, &tr);
-    tr.mark("jitter");
     ensure_grid(s, cfg->grid_nx, cfg->grid_ny, cfg->target_density);
     set_density_model(s, cfg->density_model);
 
@@ -476,22 +477,8 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     }
 
     tr.mark("upload + grid + ledger");
-    E->lambda = cfg->lambda0 > 0.0 ? cfg->lambda0 : lambda_auto(s, E->gamma, cfg->pp_loss);
-    tr.mark("lambda auto");
-    E->lambda_cap = E->lambda * cfg->lambda_max;
-
-    // per-iteration schedule (placer.cpp:470-471, :349-350, :477)
     const int T = std::max(cfg->max_iters, 1);
-    std::vector<Sched> sch(T);
-    double lam = E->lambda;
-    for (int it = 0; it < T; ++it) {
-        sch[it].lr = cfg->step0_frac * E->span * std::pow(cfg->step_decay, it);
-        sch[it].c1 = 1.0 - std::pow(cfg->adam_beta1, it + 1);
-        sch[it].c2 = 1.0 - std::pow(cfg->adam_beta2, it + 1);
-        sch[it].lambda = lam;
-        lam = std::min(lam * cfg->mu, E->lambda_cap);
-    }
-    E->sched.upload(sch, s->st);
+    E->sched.reserve(T); // (filled after lambda_auto, below)
     Ctrl c0{};
     c0.nonfinite_at = INT_MAX;
     E->ctrl.reserve(1);
@@ -531,8 +518,23 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     G.refresh_lonly = s->pins_stale, s->pins_stale = false; // (recorded, not run)
     tr.mark("refresh graph");
     G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
-    G.epoch = dbuf_epoch();
+    G.epoch = dbuf_epoch(); // (an allocation by lambda_auto below re-captures at the first run)
     tr.mark("sort graph");
+
+    G.lambda = cfg->lambda0 > 0.0 ? cfg->lambda0 : lambda_auto(s, G.gamma, cfg->pp_loss);
+    tr.mark("lambda auto");
+    G.lambda_cap = G.lambda * cfg->lambda_max;
+    // per-iteration schedule (placer.cpp:470-471, :349-350, :477)
+    std::vector<Sched> sch(T);
+    double lam = G.lambda;
+    for (int it = 0; it < T; ++it) {
+        sch[it].lr = cfg->step0_frac * G.span * std::pow(cfg->step_decay, it);
+        sch[it].c1 = 1.0 - std::pow(cfg->adam_beta1, it + 1);
+        sch[it].c2 = 1.0 - std::pow(cfg->adam_beta2, it + 1);
+        sch[it].lambda = lam;
+        lam = std::min(lam * cfg->mu, G.lambda_cap);
+    }
+    G.sched.upload(sch, s->st);
     CK(cudaStreamSynchronize(s->st));
 }
 
