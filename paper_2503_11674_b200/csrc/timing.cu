@@ -706,11 +706,25 @@ __global__ void k_resolve_ties_L(LArgs a, const int* __restrict__ level, int L, 
 
 // Backtrace of the rank-0 path of each selected endpoint: pass 1 counts pins and
 // net hops (hops leaving an Output pin, paths.cpp:195-200), pass 2 writes them.
+// selected(): with nvp (the STA's [tns, wns, violated] on the device) only the first
+// min(n_req or all, violated) of the n slots are paths; the rest get length 0.
+__device__ __forceinline__ int selected(int n, const double* nvp, int n_req)
+{
+    if (!nvp) return n;
+    const int nv = static_cast<int>(nvp[2]);
+    return min(n, n_req <= 0 ? nv : min(n_req, nv));
+}
+
 __global__ void k_bt_count(int n, const int* __restrict__ ep, const int* __restrict__ pred,
-                           const uint8_t* __restrict__ pin_dir, int* __restrict__ len, int* __restrict__ hops)
+                           const uint8_t* __restrict__ pin_dir, int* __restrict__ len, int* __restrict__ hops,
+                           const double* __restrict__ nvp = nullptr, int n_req = 0)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
+    if (i >= selected(n, nvp, n_req)) {
+        len[i] = 0, hops[i] = 0;
+        return;
+    }
     int v = ep[i], l = 1, h = 0;
     for (int u = pred[v]; u >= 0; v = u, u = pred[v]) {
         ++l;
@@ -727,7 +741,7 @@ __global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restr
                            double* __restrict__ hslack, int* __restrict__ hidx)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || len[i] == 0) return;
     int v = ep[i];
     const double sl = clock - arr[v]; // path slack = clock - rank-0 delay (paths.cpp:123)
     pslack[i] = sl;
@@ -749,10 +763,15 @@ __global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restr
 // k_bt_count / k_bt_write on L-space predecessors (an L-space-only STA), pins translated on output.
 __global__ void k_bt_count_Ln(int n, const int* __restrict__ ep, const int* __restrict__ L_of,
                               const int* __restrict__ L_pred, const uint8_t* __restrict__ L_flags,
-                              int* __restrict__ len, int* __restrict__ hops)
+                              int* __restrict__ len, int* __restrict__ hops, const double* __restrict__ nvp,
+                              int n_req)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
+    if (i >= selected(n, nvp, n_req)) {
+        len[i] = 0, hops[i] = 0;
+        return;
+    }
     int v = L_of[ep[i]], l = 1, h = 0;
     for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) ++l, h += (L_flags[u] & 4) != 0;
     len[i] = l, hops[i] = h;
@@ -767,7 +786,7 @@ __global__ void k_bt_write_Ln(int n, const int* __restrict__ ep, const int* __re
                               double* __restrict__ hslack, int* __restrict__ hidx)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || len[i] == 0) return;
     const int e = ep[i];
     int v = L_of[e], vp = e;
     const double sl = clock - L_arr[v]; // paths.cpp:123
@@ -1126,6 +1145,8 @@ int sorted_violated(tdpg_session* s)
     return static_cast<int>(h[2]);
 }
 
+static int bits_for(long long n);
+
 // report_timing_endpoint(n, k = 1) on the current STA (paths.cpp:167-189).
 void extract_endpoint_dev(tdpg_session* s, int n)
 {
@@ -1170,36 +1191,39 @@ void extract_endpoint_dev(tdpg_session* s, int n)
             CK_LAUNCH();
             s->ties_resolved = true;
         }
-        double h[3];
-        CK(cudaMemcpyAsync(h, out3, sizeof h, cudaMemcpyDeviceToHost, s->st));
-        CK(cudaStreamSynchronize(s->st));
-        const int nv = static_cast<int>(h[2]);
-        s->n_paths = (n <= 0) ? nv : std::min(n, nv);
     }
-    const int np = s->n_paths;
-    s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0;
-    s->uniq_endpoints = np, s->candidates = np; // k = 1: one path per selected endpoint
-    if (np == 0) return;
-    s->ex_len.reserve(np), s->ex_hops.reserve(np), s->ex_off.reserve(np), s->ex_hoff.reserve(np);
-    s->ex_slack.reserve(np);
+    // the selection size min(n, violated) stays on the device: the backtrace runs over an upper bound of
+    // slots (zero-length past the selection), one host read brings back every count
+    const int ub = (n <= 0) ? EP : std::min(n, EP);
+    s->n_paths = 0, s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0, s->uniq_endpoints = 0, s->candidates = 0;
+    if (ub <= 0) return;
+    s->ex_len.reserve(ub), s->ex_hops.reserve(ub), s->ex_off.reserve(ub), s->ex_hoff.reserve(ub);
+    s->ex_slack.reserve(ub);
     if (Lsp)
-        k_bt_count_Ln<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->L_of, s->L_pred, s->L_flags,
-                                                                    s->ex_len, s->ex_hops);
+        k_bt_count_Ln<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->L_of, s->L_pred, s->L_flags,
+                                                                    s->ex_len, s->ex_hops, out3, n);
     else
-        k_bt_count<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
-                                                                 s->ex_hops);
+        k_bt_count<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
+                                                                 s->ex_hops, out3, n);
     CK_LAUNCH();
     size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->ex_len.p, s->ex_off.p, np, s->st);
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->ex_len.p, s->ex_off.p, ub, s->st);
     void* tmp = cub_scratch(s, bytes);
-    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_len.p, s->ex_off.p, np, s->st));
-    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_hops.p, s->ex_hoff.p, np, s->st));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_len.p, s->ex_off.p, ub, s->st));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_hops.p, s->ex_hoff.p, ub, s->st));
     int tail[4];
-    CK(cudaMemcpyAsync(&tail[0], s->ex_off.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(&tail[1], s->ex_len.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(&tail[2], s->ex_hoff.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(&tail[3], s->ex_hops.p + np - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    double h3[3];
+    CK(cudaMemcpyAsync(h3, out3, sizeof h3, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[0], s->ex_off.p + ub - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[1], s->ex_len.p + ub - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[2], s->ex_hoff.p + ub - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[3], s->ex_hops.p + ub - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
+    const int nv = static_cast<int>(h3[2]);
+    const int np = (n <= 0) ? nv : std::min(n, nv);
+    s->n_paths = np;
+    s->uniq_endpoints = np, s->candidates = np; // k = 1: one path per selected endpoint
+    if (np == 0) return;
     s->n_path_pins = static_cast<long long>(tail[0]) + tail[1];
     s->n_hits = static_cast<long long>(tail[2]) + tail[3];
     const long long H = s->n_hits;
@@ -1219,11 +1243,12 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     CK_LAUNCH();
     if (H > 0) {
         bytes = 0;
+        const int kb = std::min(64, 32 + bits_for(s->P)); // pair keys (lo << 32) | hi with lo, hi < P
         cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
-                                        static_cast<int>(H), 0, 64, s->st);
+                                        static_cast<int>(H), 0, kb, s->st);
         tmp = cub_scratch(s, bytes);
         CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
-                                           static_cast<int>(H), 0, 64, s->st));
+                                           static_cast<int>(H), 0, kb, s->st));
         CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
         k_count_heads<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 4), kBlock, 0, s->st>>>(H, s->hit_key_s,
                                                                                                  s->counters.p + 1);
