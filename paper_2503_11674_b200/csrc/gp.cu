@@ -830,14 +830,15 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_wide(int n, const in
 
 // Spatial order of the movable cells: key = 8x8-bin tile of the cell's lower-left corner.
 __global__ void k_spatial_keys(int C, const double2* __restrict__ cell_xy, const uint8_t* __restrict__ fixed,
-                               GridDev g, int tiles_y, unsigned* __restrict__ keys, int* __restrict__ vals)
+                               GridDev g, int tiles_y, unsigned fixed_key, unsigned* __restrict__ keys,
+                               int* __restrict__ vals)
 {
     const int c = blockIdx.x * kBlock + threadIdx.x;
     if (c >= C) return;
     const double2 p = cell_xy[c];
     const int bx = min(g.nx - 1, max(0, static_cast<int>((p.x - g.x0) * g.inv_bw)));
     const int by = min(g.ny - 1, max(0, static_cast<int>((p.y - g.y0) * g.inv_bh)));
-    keys[c] = fixed[c] ? 0xFFFFFFFFu : static_cast<unsigned>((bx >> 3) * tiles_y + (by >> 3));
+    keys[c] = fixed[c] ? fixed_key : static_cast<unsigned>((bx >> 3) * tiles_y + (by >> 3)); // fixed: last
     vals[c] = c;
 }
 
@@ -1453,17 +1454,16 @@ void sort_cells_spatial(tdpg_session* s)
     const int tiles_y = (g.ny + 7) / 8, tiles_x = (g.nx + 7) / 8;
     unsigned* k0 = gr.perm_keys.p;
     unsigned* k1 = gr.perm_keys.p + C;
-    k_spatial_keys<<<blocks_for(C, kBlock), kBlock, 0, s->st>>>(C, s->cell_xy, s->cell_fixed, g, tiles_y, k0,
-                                                                gr.perm_tmp);
+    const long long ntiles = static_cast<long long>(tiles_x) * tiles_y;
+    k_spatial_keys<<<blocks_for(C, kBlock), kBlock, 0, s->st>>>(C, s->cell_xy, s->cell_fixed, g, tiles_y,
+                                                                static_cast<unsigned>(ntiles), k0, gr.perm_tmp);
     CK_LAUNCH();
-    int bits = 1;
-    while ((1ll << bits) < static_cast<long long>(tiles_x) * tiles_y + 1) ++bits;
+    int bits = 1; // keys 0..ntiles (fixed cells sort last)
+    while ((1ll << bits) < ntiles + 1) ++bits;
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0, k1, gr.perm_tmp.p, gr.perm.p, C, 0, 32, s->st);
     void* tmp = cub_scratch(s, bytes);
-    // fixed cells carry key 0xFFFFFFFF: sort all 32 bits only when any exist
-    CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, gr.perm_tmp.p, gr.perm.p, C, 0,
-                                       gr.has_fixed ? 32 : bits, s->st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, gr.perm_tmp.p, gr.perm.p, C, 0, bits, s->st));
 }
 
 void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl);

@@ -46,7 +46,8 @@ struct Engine {
     unsigned long long epoch = 0;            // dbuf_epoch() when the graphs were captured
     bool refresh_lonly = false;              // the refresh graph leaves the STA results in L-space only
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
-    int sort_every = 4; // iterations between spatial re-sorts of the cells (2: 0.310, 4: 0.301, 8: 0.334 ms/iteration at 1M)
+    int sort_every = 2; // iterations between spatial re-sorts of the cells (1M, iterations 20-220 with refresh:
+                        // 1: 0.317, 2: 0.299, 3: 0.301, 4: 0.305 ms; the order goes stale as the cells spread)
     double last_refresh_ms = 0, total_refresh_ms = 0;
     // branch streams + fork/join events of the captured iteration graph (density chain and the WA
     // size classes run as parallel graph branches)
