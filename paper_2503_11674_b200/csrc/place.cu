@@ -43,6 +43,7 @@ struct Engine {
     int kernels_per_iter = 8; // 2 WA class groups + generic + scatter + bins + dens_grad + finalize + cells
     cudaGraphExec_t refresh_gexec = nullptr; // the whole timing refresh, captured once
     cudaGraphExec_t sort_gexec = nullptr;    // spatial re-sort of the cells
+    cudaGraphExec_t gexec_sorted = nullptr;  // re-sort + iteration (non-partitioned engine)
     unsigned long long epoch = 0;            // dbuf_epoch() when the graphs were captured
     bool refresh_lonly = false;              // the refresh graph leaves the STA results in L-space only
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
@@ -73,6 +74,7 @@ struct Engine {
         if (graph) cudaGraphDestroy(graph);
         if (refresh_gexec) cudaGraphExecDestroy(refresh_gexec);
         if (sort_gexec) cudaGraphExecDestroy(sort_gexec);
+        if (gexec_sorted) cudaGraphExecDestroy(gexec_sorted);
         for (auto& e : refresh_ev) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     }
     // a previous engine of the session (engine_init again): its buffers, branch streams and events are
@@ -272,7 +274,7 @@ void capture_iteration(tdpg_session* s, Engine& E)
         return;
     }
     s->pdl_graph = pdl_gp();
-    E.gexec = capture(s, [&] {
+    auto record = [&] {
         // fork: density chain (scatter -> bins -> density gradient) on branch 0, the WA size classes
         // (+ fused pin pairs, dense ledger) on the main stream and branches 1..7; join -> finalize -> cells
         cudaStream_t main = s->st;
@@ -293,6 +295,13 @@ void capture_iteration(tdpg_session* s, Engine& E)
         launch_finalize(s, fa, E.ctrl, E.cur);
         launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
                      false);
+    };
+    E.gexec = capture(s, record);
+    // the iterations that re-sort the cells first: one graph launch for both
+    if (E.gexec_sorted) cudaGraphExecDestroy(E.gexec_sorted);
+    E.gexec_sorted = capture(s, [&] {
+        sort_cells_spatial(s);
+        record();
     });
     s->pdl_graph = false;
 }
@@ -716,13 +725,19 @@ int engine_run(tdpg_session* s, int n)
         ensure_graphs(s, E);
         const int it = E.launched;
         if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0) timing_refresh(s);
-        if (it % E.sort_every == 0) {
-            CK(cudaGraphLaunch(E.sort_gexec, s->st)); // refresh the scatter's spatial cell order
-            E.kernel_launches += 1;
-        }
         if (!E.gexec) throw Error(TDPG_ERR_INTERNAL, "partitioned engine without a communicator: use "
                                                       "tdpg_comm_init or the split-phase API");
-        CK(cudaGraphLaunch(E.gexec, s->st));
+        if (it % E.sort_every == 0) { // refresh the scatter's spatial cell order first
+            if (E.gexec_sorted) {
+                CK(cudaGraphLaunch(E.gexec_sorted, s->st));
+            } else {
+                CK(cudaGraphLaunch(E.sort_gexec, s->st));
+                CK(cudaGraphLaunch(E.gexec, s->st));
+            }
+            E.kernel_launches += 1;
+        } else {
+            CK(cudaGraphLaunch(E.gexec, s->st));
+        }
         E.kernel_launches += E.kernels_per_iter + (E.partitioned ? 1 : 0);
         ++E.launched;
     }
