@@ -371,14 +371,17 @@ def run_ours(args):
     dom_ms = prof[dom]
     achieved = kb[dom] / (dom_ms / 1000.0) / 1e9
     iter_ms = sum(prof.values())
-    # the scatter's real limiter: shared-memory atomics, two 32-bit lane-atomics per footprint entry
-    # (fixed-point lo word + hi word); peak = 4 SMSPs x 148 SMs x clock / 2 cycles per spread lane-atomic
+    # the scatter's real limiter: shared-memory atomics, one 32-bit lane-atomic per non-zero footprint entry
+    # (fixed-point low word) plus one when the entry needs the high word, counted on the device at the
+    # profiled positions; peak = 4 SMSPs x 148 SMs x clock / 2 cycles per spread lane-atomic
     # (B300_MICROARCH.md "ATOMS (spread-addr) 2 cyc/lane"; same SM design on B200)
     n_ent = footprint_entries(d, s.positions(), args.grid)
+    from paper_2503_11674_b200.design import CONFIG_DEFAULTS
+    at_lo, at_hi = s.density_atomics(args.grid, args.grid, CONFIG_DEFAULTS["target_density"], xy=s.positions())
     clk_summary = clk.summary()
     sm_ghz = (clk_summary.get("sm_mhz") or 1965.0) / 1000.0
     atom_peak = 148 * 4 * sm_ghz * 1e9 / 2 / 1e9  # G lane-atomics/s
-    atom_ach = 2 * n_ent / (prof.get("density_scatter", 1e9) / 1000.0) / 1e9
+    atom_ach = (at_lo + at_hi) / (prof.get("density_scatter", 1e9) / 1000.0) / 1e9
     ib = iteration_bytes(d, args.grid)
     cpu = None
     if not args.no_cpu_baseline:
@@ -417,7 +420,7 @@ def run_ours(args):
                      "peak_source": "measured" if "fallback" not in pk else "fallback",
                      "limiter": {"kernel": "density_scatter", "bound": "smem_atomics", "unit": "G lane-atomics/s",
                                  "achieved": round(atom_ach, 1), "peak": round(atom_peak, 1),
-                                 "frac": round(atom_ach / atom_peak, 3), "footprint_entries": n_ent,
+                                 "frac": round(atom_ach / atom_peak, 3), "footprint_entries": n_ent, "lane_atomics": at_lo + at_hi,
                                  "peak_source": "B300_MICROARCH.md ATOMS spread-addr 2 cyc/lane x 4 SMSP x 148 SM"}},
         "iteration": {"gp_iteration_ms": round((dev_ms_max - refresh_ms) / args.steps, 4),
                       "refresh_ms_each": round(refresh_ms / max(refreshes, 1), 3),

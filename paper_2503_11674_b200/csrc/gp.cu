@@ -1647,6 +1647,56 @@ int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* 
     API_END
 }
 
+// Shared-memory atomics the windowed scatter issues at the session's positions (measurement aid for the
+// roofline limiter): one 32-bit atomic per non-zero footprint entry of a five-bin cell, a second when the
+// entry's fixed-point value needs the high word (carries from the low word are not counted).
+__global__ void k_count_scatter_atomics(int n_mov, const int* __restrict__ perm, const double2* __restrict__ cell_xy,
+                                        const double2* __restrict__ cell_wh, GridDev g,
+                                        unsigned long long* __restrict__ out)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    unsigned long long lo = 0, hi = 0;
+    if (i < n_mov) {
+        const int c = perm[i];
+        const double2 p = cell_xy[c], s = cell_wh[c];
+        double wx[kF5], wy[kF5], dw[kF5];
+        int bx, by;
+        if (!(s.x > g.wide_w || s.y > g.wide_h) && axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dw) &&
+            axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dw)) {
+            const double area = s.x * s.y;
+            for (int a = 0; a < kF5; ++a) {
+                if (wx[a] == 0.0) continue;
+                const double aw = area * wx[a];
+                for (int j = 0; j < kF5; ++j) {
+                    const long long q = __double2ll_rn(aw * wy[j] * g.scale);
+                    lo += q != 0, hi += (static_cast<unsigned long long>(q) >> 32) != 0;
+                }
+            }
+        }
+    }
+    lo = warp_sum(lo), hi = warp_sum(hi);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, lo), atomicAdd(out + 1, hi);
+}
+
+int tdpg_density_atomics(tdpg_session* s, int64_t* lo_hi)
+{
+    API_BEGIN
+    if (!s->grid.valid()) throw Error(TDPG_ERR_VALIDATION, "validation error: density grid not set");
+    sort_cells_spatial(s);
+    DBuf<unsigned long long> out(2);
+    out.zero(s->st);
+    const int n_mov = s->grid.n_movable;
+    if (n_mov > 0)
+        k_count_scatter_atomics<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(n_mov, s->grid.perm, s->cell_xy,
+                                                                                s->cell_wh, grid_dev(s), out);
+    CK_LAUNCH();
+    unsigned long long h[2];
+    out.download(h, 2, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    lo_hi[0] = static_cast<int64_t>(h[0]), lo_hi[1] = static_cast<int64_t>(h[1]);
+    API_END
+}
+
 int tdpg_density(tdpg_session* s, double* value, double* overflow, double* d_cell)
 {
     API_BEGIN

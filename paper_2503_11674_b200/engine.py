@@ -102,6 +102,7 @@ _SIGS = {
     "tdpg_extract": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P]),
     "tdpg_set_density_model": (C.c_int, [_P, C.c_int32]),
     "tdpg_density_fields": (C.c_int, [_P, _P, _P]),
+    "tdpg_density_atomics": (C.c_int, [_P, _P]),
     "tdpg_partition_plan": (C.c_int, [C.c_int32, _P, C.c_int32, _P, _P]),
     "tdpg_set_partition": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "tdpg_comm_unique_id": (C.c_int, [_P]),
@@ -225,6 +226,14 @@ class Session:
         """0 / "overflow": the reference's bin-overflow penalty; 1 / "electrostatic": DCT Poisson energy."""
         m = {"overflow": 0, "electrostatic": 1}.get(model, model)
         _check(self.lib.tdpg_set_density_model(self.h, int(m)))
+
+    def density_atomics(self, nx, ny, td=0.6, xy=None):
+        """(low-word, high-word) shared-memory atomics of the density scatter at these positions."""
+        self._pos(xy)
+        _check(self.lib.tdpg_set_grid(self.h, nx, ny, td))
+        out = np.zeros(2, np.int64)
+        _check(self.lib.tdpg_density_atomics(self.h, out.ctypes.data))
+        return int(out[0]), int(out[1])
 
     def density_fields(self, nx, ny):
         """Charge map and potential of the last electrostatic evaluation, shaped [nx, ny]."""
