@@ -47,8 +47,9 @@ struct Engine {
     unsigned long long epoch = 0;            // dbuf_epoch() when the graphs were captured
     bool refresh_lonly = false;              // the refresh graph leaves the STA results in L-space only
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
-    int sort_every = 2; // iterations between spatial re-sorts of the cells (1M, iterations 20-220 with refresh:
-                        // 1: 0.317, 2: 0.299, 3: 0.301, 4: 0.305 ms; the order goes stale as the cells spread)
+    int sort_every = 2; // iterations between spatial re-sorts of the cells (engine_init: 2 from 500K movable cells,
+                        // else 4; bench iters/s at 200K: 2: 9,397, 3: 9,852, 4: 10,095; 1M ms/step over iterations
+                        // 20-220: 1: 0.317, 2: 0.299, 3: 0.301, 4: 0.305; 4M: 2 vs 4 = 904 vs ~790 iters/s)
     double last_refresh_ms = 0, total_refresh_ms = 0;
     // branch streams + fork/join events of the captured iteration graph (density chain and the WA
     // size classes run as parallel graph branches)
@@ -511,6 +512,8 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
         E->red.zero(s->st);
         s->grad_e.zero(s->st);
     }
+    // the order goes stale as the cells spread; the re-sort's fixed cost weighs more on small designs
+    E->sort_every = s->grid.n_movable >= 500000 ? 2 : 4;
     if (const char* se = std::getenv("TDPG_SORT_EVERY")) E->sort_every = std::max(1, std::atoi(se));
     // every buffer the graphs touch is sized before capture, so their pointers never move
     tr.mark("schedule + buffers");
