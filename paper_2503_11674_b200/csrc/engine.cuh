@@ -225,6 +225,11 @@ struct tdpg_session {
     tdpg::DBuf<unsigned long long> dl_k0, dl_k1;
     tdpg::DBuf<double> dl_w0, dl_w1;
     tdpg::DBuf<unsigned long long> jit_raw;
+    unsigned long long jit_seed = 0;   // jit_raw holds the first jit_count draws of mt19937_64(jit_seed)
+    long long jit_count = -1;
+    const unsigned long long* jit_ptr = nullptr;
+    int n_free = -1;                   // cells that are not fixed (host count, lazily)
+    tdpg::DBuf<double> lam_scratch;    // lambda_auto scratch
     tdpg::DBuf<uint8_t> jit_expl;
 
     // partitioned multi-GPU mode (partition.cu): this rank's WA block range, NCCL communicator

@@ -150,8 +150,8 @@ double lambda_auto(tdpg_session* s, double gamma, int kind)
     evaluate_objective(s, gamma, 0.0, 0.0, kind, false, nullptr);
     // scratch in the session's jitter stream buffer (free after the jitter): [wl gradient | part | p2]
     const int nb_d = bins_blocks(s), nb = 148 * 2;
-    s->jit_raw.reserve(2 * static_cast<size_t>(s->C) + 2 * nb_d + 64 + 2 * nb);
-    double2* wl = reinterpret_cast<double2*>(s->jit_raw.p);
+    s->lam_scratch.reserve(2 * static_cast<size_t>(s->C) + 2 * nb_d + 64 + 2 * nb);
+    double2* wl = reinterpret_cast<double2*>(s->lam_scratch.p);
     double* part = reinterpret_cast<double*>(wl + s->C);
     double* p2 = part + 2 * nb_d + 64;
     CK(cudaMemcpyAsync(wl, s->d_cell.p, sizeof(double2) * s->C, cudaMemcpyDeviceToDevice, s->st));
@@ -358,7 +358,7 @@ __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y)
 }
 
 __global__ void __launch_bounds__(160) k_mt19937_64(unsigned long long seed, const int* __restrict__ count,
-                                                    unsigned long long* __restrict__ out)
+                                                    int count_host, unsigned long long* __restrict__ out)
 {
     __shared__ unsigned long long ring[4][kMtM];
     const int t = threadIdx.x;
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(160) k_mt19937_64(unsigned long long seed, con
     __syncthreads();
     unsigned long long r2 = 0, r1 = 0; // this thread's words of steps k - 2 and k - 1
     if (t < kMtM) r2 = ring[2][t], r1 = ring[3][t];
-    const long long need = 2LL * *count;
+    const long long need = 2LL * (count ? *count : count_host);
     int s0 = 0; // ring slot of step k (steps k - 2, k - 1 in s0 + 2, s0 + 3 mod 4)
     for (long long base = 0; base < need; base += 2 * kMtM) {
         const int sm2 = (s0 + 2) & 3, sm1 = (s0 + 3) & 3, s1 = (s0 + 1) & 3;
@@ -440,8 +440,21 @@ void jitter_positions(tdpg_session* s, const tdpg_config* cfg, const uint8_t* po
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st);
     void* tmp = cub_scratch(s, bytes);
     CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st));
-    k_mt19937_64<<<1, 160, 0, s->st>>>(static_cast<unsigned long long>(cfg->seed), s->jit_rank.p + C, s->jit_raw);
-    CK_LAUNCH();
+    // the raw stream depends on the seed only: every free cell's two draws are generated once per seed
+    // (explicitly placed cells only shorten the prefix used) and kept for the next run with that seed
+    if (s->n_free < 0) {
+        int nf = 0;
+        for (int c = 0; c < C; ++c) nf += s->h_cell_fixed[c] ? 0 : 1;
+        s->n_free = nf;
+    }
+    const unsigned long long seed = static_cast<unsigned long long>(cfg->seed);
+    const long long need = 2LL * s->n_free;
+    if (!(s->jit_count >= need && s->jit_seed == seed && s->jit_ptr == s->jit_raw.p)) {
+        s->jit_rank.reserve(C + 2);
+        k_mt19937_64<<<1, 160, 0, s->st>>>(seed, nullptr, static_cast<int>(s->n_free), s->jit_raw);
+        CK_LAUNCH();
+        s->jit_seed = seed, s->jit_count = need, s->jit_ptr = s->jit_raw.p;
+    }
     if (tr) tr->mark("jitter: flags + scan + mt19937_64");
     k_jit_apply<<<blocks_for(C, kBlock), kBlock, 0, s->st>>>(
         C, s->jit_flag, s->jit_rank, s->jit_raw, s->cell_wh, s->cell_xy, cfg->init_jitter_frac, cw, ch,

@@ -46,3 +46,16 @@ def test_jitter_zero_frac_and_all_explicit():
     d.pos_explicit[:] = 1
     cfg["init_jitter_frac"] = 0.1
     assert np.array_equal(_start(d, cfg), d.positions)
+
+
+def test_jitter_stream_reused_across_runs_of_a_session():
+    """The session keeps the raw mt19937_64 stream per seed: later runs with the same seed (other
+    explicit cells), then another seed, still start bitwise where the oracle does."""
+    d = generate(seed=6, cells=8000, fail_frac=0.5)
+    s = Session(d)
+    cfg = {"seed": 77, "init_jitter_frac": 0.05, "grid_nx": 16, "grid_ny": 16, "max_iters": 2}
+    for frac_explicit, seed in ((0.0, 77), (0.3, 77), (0.1, 77), (0.0, 78), (0.2, 77)):
+        d.pos_explicit[:] = (np.random.default_rng(seed).random(d.n_cells) < frac_explicit).astype(np.uint8)
+        cfg["seed"] = seed
+        s.engine_init(cfg, xy=d.positions)
+        assert np.array_equal(s.positions(), Oracle(d).jitter(cfg)), (frac_explicit, seed)
