@@ -252,6 +252,7 @@ namespace tdpg {
 void upload_positions(tdpg_session* s, const double* xy);
 void refresh_fixed_baseline(tdpg_session* s);
 void sta_materialize_pins(tdpg_session* s); // per-pin STA arrays of an L-space-only sweep (timing.cu)
+void place_tail_reserve(tdpg_session* s); // (timing.cu)
 void ensure_grid(tdpg_session* s, int nx, int ny, double td);
 void set_density_model(tdpg_session* s, int model);
 void* cub_scratch(tdpg_session* s, size_t bytes);

@@ -44,6 +44,11 @@ struct Engine {
     cudaGraphExec_t refresh_gexec = nullptr; // the whole timing refresh, captured once
     cudaGraphExec_t sort_gexec = nullptr;    // spatial re-sort of the cells
     cudaGraphExec_t gexec_sorted = nullptr;  // re-sort + iteration (non-partitioned engine)
+    cudaGraphExec_t old_gexec = nullptr, old_gexec_sorted = nullptr, old_refresh = nullptr, old_sort = nullptr;
+    bool old_lonly = false;
+    unsigned long long old_epoch = 0;
+    tdpg_config old_cfg{};
+    int old_sort_every = 0;
     unsigned long long epoch = 0;            // dbuf_epoch() when the graphs were captured
     bool refresh_lonly = false;              // the refresh graph leaves the STA results in L-space only
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
@@ -76,6 +81,8 @@ struct Engine {
         if (refresh_gexec) cudaGraphExecDestroy(refresh_gexec);
         if (sort_gexec) cudaGraphExecDestroy(sort_gexec);
         if (gexec_sorted) cudaGraphExecDestroy(gexec_sorted);
+        for (cudaGraphExec_t g : {old_gexec, old_gexec_sorted, old_refresh, old_sort})
+            if (g) cudaGraphExecDestroy(g);
         for (auto& e : refresh_ev) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
     }
     // a previous engine of the session (engine_init again): its buffers, branch streams and events are
@@ -87,6 +94,23 @@ struct Engine {
         m = std::move(o.m), v = std::move(o.v), part = std::move(o.part), red = std::move(o.red);
         obs_count = std::move(o.obs_count);
         std::swap(br, o.br), std::swap(ev_fork, o.ev_fork), std::swap(ev_join, o.ev_join);
+        if (!o.partitioned && o.gexec && !o.gexec_a) { // its graphs, for adopt_graphs
+            std::swap(old_gexec, o.gexec), std::swap(old_gexec_sorted, o.gexec_sorted);
+            std::swap(old_refresh, o.refresh_gexec), std::swap(old_sort, o.sort_gexec);
+            old_lonly = o.refresh_lonly, old_epoch = o.epoch, old_cfg = o.cfg, old_sort_every = o.sort_every;
+        }
+    }
+    // The previous engine's graphs point into exactly this engine's (recycled) buffers when no device
+    // buffer moved since they were captured and the configuration (baked into kernel arguments) matches.
+    bool adopt_graphs()
+    {
+        if (!old_gexec || old_epoch != dbuf_epoch() || partitioned || old_sort_every != sort_every ||
+            std::memcmp(&old_cfg, &cfg, sizeof cfg) != 0)
+            return false;
+        std::swap(gexec, old_gexec), std::swap(gexec_sorted, old_gexec_sorted);
+        std::swap(refresh_gexec, old_refresh), std::swap(sort_gexec, old_sort);
+        refresh_lonly = old_lonly, epoch = old_epoch;
+        return true;
     }
     double refresh_ms()
     {
@@ -531,21 +555,26 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     // every buffer the graphs touch is sized before capture, so their pointers never move
     tr.mark("schedule + buffers");
     refresh_reserve(s);
+    place_tail_reserve(s); // (so a later run of the session finds every buffer where its graphs point)
     s->pin_xy_external = false;
     sort_cells_spatial(s);
     tr.mark("reserve + sort");
     s->eng = E.release();
     Engine& G = *s->eng;
-    capture_iteration(s, G);
-    tr.mark("iteration graph");
-    G.refresh_gexec = capture(s, [&] {
-        refresh_record(s, G.ctrl, G.timing_row, G.cfg.w0, G.cfg.w1, G.cfg.net_weighting != 0);
-    });
-    G.refresh_lonly = s->pins_stale, s->pins_stale = false; // (recorded, not run)
-    tr.mark("refresh graph");
-    G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
-    G.epoch = dbuf_epoch(); // (an allocation by lambda_auto below re-captures at the first run)
-    tr.mark("sort graph");
+    if (!G.adopt_graphs()) {
+        capture_iteration(s, G);
+        tr.mark("iteration graph");
+        G.refresh_gexec = capture(s, [&] {
+            refresh_record(s, G.ctrl, G.timing_row, G.cfg.w0, G.cfg.w1, G.cfg.net_weighting != 0);
+        });
+        G.refresh_lonly = s->pins_stale, s->pins_stale = false; // (recorded, not run)
+        tr.mark("refresh graph");
+        G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
+        G.epoch = dbuf_epoch(); // (an allocation by lambda_auto below re-captures at the first run)
+        tr.mark("sort graph");
+    } else {
+        tr.mark("graphs adopted");
+    }
 
     G.lambda = cfg->lambda0 > 0.0 ? cfg->lambda0 : lambda_auto(s, G.gamma, cfg->pp_loss);
     tr.mark("lambda auto");

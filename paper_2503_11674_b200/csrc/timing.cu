@@ -1591,6 +1591,19 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     }
 }
 
+// Buffers tdpg_place touches after its loop (the sorted ledger, the final HPWL partials), reserved
+// with the engine's own so that allocation-free runs can reuse the previous run's graphs.
+void place_tail_reserve(tdpg_session* s)
+{
+    const int P = std::max(s->P, 1);
+    s->dl_k0.reserve(P), s->dl_k1.reserve(P), s->dl_w0.reserve(P), s->dl_w1.reserve(P);
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->dl_k0.p, s->dl_k1.p, s->dl_w0.p, s->dl_w1.p, P, 0, 64, s->st);
+    cub_scratch(s, bytes);
+    s->part.reserve(2 * static_cast<size_t>(wa_blocks(s)) + 8);
+    s->sta_out.reserve(4);
+}
+
 // Dense ledger -> the sorted (a, b, w) ledger of the session (tdpg_pp_get), after a run.
 __global__ void k_dense_to_pairs(int P, const double* __restrict__ dl_w, const int* __restrict__ pin_driver,
                                  unsigned long long* __restrict__ key, double* __restrict__ w)
