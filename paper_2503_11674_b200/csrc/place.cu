@@ -1046,8 +1046,9 @@ int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_expli
     tr.mark("place: trace rows");
     dense_ledger_to_sorted(s); // PlacementOutcome::pair_weights as the sorted ledger (tdpg_pp_get)
     tr.mark("place: sorted ledger");
-    // final STA + exact HPWL at the returned positions (placer.cpp:482, bindings.cpp:381-382)
-    run_sta_dev(s);
+    // final STA + exact HPWL at the returned positions (placer.cpp:482, bindings.cpp:381-382); TNS / WNS
+    // only, the per-pin arrays stay in L-space until a caller reads them
+    run_sta_dev(s, false);
     tr.mark("place: final STA");
     double hp = 0.0;
     {
