@@ -206,9 +206,10 @@ def test_nonfinite_raises_with_iteration():
     assert "at iteration" in str(es.value) and str(es.value) == str(eo.value)
 
 
-@pytest.mark.parametrize("cells", [200000])
+@pytest.mark.parametrize("cells", [200000, 1000000])
 def test_large_sta_and_extraction_bitwise(cells):
-    """200K-cell design: STA + top-10K extraction bit-exact against the C oracle."""
+    """200K- and 1M-cell (the headline config's size) designs: STA + top-10K extraction bit-exact
+    against the C oracle."""
     d = generate(seed=1, cells=cells, fail_frac=0.4, calibrate=False)
     d.clock_period = 1.0
     xy = spread_positions(d, 1)
