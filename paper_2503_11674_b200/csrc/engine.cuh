@@ -105,6 +105,8 @@ struct tdpg_session {
     int C = 0, P = 0, N = 0, E = 0, E_tot = 0, S = 0, EP = 0, A = 0, A_net = 0, A_cell = 0, L = 0;
     double clock = 0, r_unit = 0, c_unit = 0, core[4] = {0, 0, 0, 0};
     cudaStream_t st = nullptr;
+    cudaStream_t st_req = nullptr;                    // the STA's required-time sweep (beside arrival)
+    cudaEvent_t ev_sta_fork = nullptr, ev_sta_join = nullptr;
     int device = 0;
 
     // host copies

@@ -826,6 +826,9 @@ tdpg_session::~tdpg_session()
     tdpg::comm_destroy(this);
     if (sta_gexec) cudaGraphExecDestroy(sta_gexec);
     if (sta_gexec_L) cudaGraphExecDestroy(sta_gexec_L);
+    if (st_req) cudaStreamSynchronize(st_req), cudaStreamDestroy(st_req);
+    if (ev_sta_fork) cudaEventDestroy(ev_sta_fork);
+    if (ev_sta_join) cudaEventDestroy(ev_sta_join);
     if (st) {
         cudaStreamSynchronize(st);
         cudaCtxResetPersistingL2Cache(); // release the L2 lines this session pinned

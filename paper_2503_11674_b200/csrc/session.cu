@@ -405,6 +405,9 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     auto s = std::make_unique<tdpg_session>();
     CK(cudaGetDevice(&s->device));
     CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->st_req, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->ev_sta_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->ev_sta_join, cudaEventDisableTiming));
     s->C = d->n_cells, s->P = d->n_pins, s->N = d->n_nets, s->S = d->n_sources, s->EP = d->n_endpoints;
     s->E = d->net_start[d->n_nets];
     s->clock = d->clock_period, s->r_unit = d->r_unit, s->c_unit = d->c_unit;

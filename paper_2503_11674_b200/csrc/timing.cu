@@ -980,6 +980,10 @@ void sta_record(tdpg_session* s, double* out3, bool pin_space)
         const unsigned nbP = blocks_for(P, kBlock);
         k_L_init<<<nbP, kBlock, 0, s->st>>>(P, la, !s->pin_xy_external, s->cell_xy, s->pin_xy);
         const bool pdl = sta_pdl();
+        // required times do not depend on arrival times (sta.cpp:69-102): the backward sweep runs on a
+        // second stream beside the forward one (both are latency-bound level chains)
+        CK(cudaEventRecord(s->ev_sta_fork, s->st));
+        CK(cudaStreamWaitEvent(s->st_req, s->ev_sta_fork, 0));
         bool first = true;
         for (int l = 0; l < s->L; ++l) {
             const int lo = s->h_L_in_lo[l], hi = s->h_L_in_hi[l];
@@ -990,10 +994,13 @@ void sta_record(tdpg_session* s, double* out3, bool pin_space)
         first = true;
         for (int l = s->L - 1; l >= 0; --l) {
             const int lo = s->h_L_in_lo[l], hi = s->h_L_in_hi[l];
-            if (hi > lo) CK(launch_pdl(k_L_req_push, blocks_for(hi - lo, kBlock), kBlock, s->st, pdl && !first, lo, hi, la));
+            if (hi > lo)
+                CK(launch_pdl(k_L_req_push, blocks_for(hi - lo, kBlock), kBlock, s->st_req, pdl && !first, lo, hi, la));
             first = first && !(hi > lo);
         }
-        CK(launch_pdl(k_L_req_decode, nbP, kBlock, s->st, pdl, P, la));
+        CK(launch_pdl(k_L_req_decode, nbP, kBlock, s->st_req, pdl && !first, P, la));
+        CK(cudaEventRecord(s->ev_sta_join, s->st_req));
+        CK(cudaStreamWaitEvent(s->st, s->ev_sta_join, 0));
         if (!lonly) {
             CK(launch_pdl(k_L_to_pins, nbP, kBlock, s->st, pdl, P, la, s->arr.p, s->req.p, s->ak.p, s->rk.p,
                           s->pred.p));
