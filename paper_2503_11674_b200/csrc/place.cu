@@ -299,13 +299,14 @@ void capture_iteration(tdpg_session* s, Engine& E)
         return;
     }
     s->pdl_graph = pdl_gp();
-    auto record = [&] {
+    auto record = [&](bool sort) {
         // fork: density chain (scatter -> bins -> density gradient) on branch 0, the WA size classes
         // (+ fused pin pairs, dense ledger) on the main stream and branches 1..7; join -> finalize -> cells
         cudaStream_t main = s->st;
         CK(cudaEventRecord(E.ev_fork, main));
         for (int k = 0; k < Engine::kBranches; ++k) CK(cudaStreamWaitEvent(E.br[k], E.ev_fork, 0));
         s->st = E.br[0];
+        if (sort) sort_cells_spatial(s); // (only the density kernels read the spatial order)
         launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
         launch_dens_grad(s, E.ctrl, E.br[0]);
         s->st = main;
@@ -321,13 +322,10 @@ void capture_iteration(tdpg_session* s, Engine& E)
         launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
                      false);
     };
-    E.gexec = capture(s, record);
-    // the iterations that re-sort the cells first: one graph launch for both
+    E.gexec = capture(s, [&] { record(false); });
+    // the iterations that re-sort the cells: the sort heads the density branch, beside the WA kernels
     if (E.gexec_sorted) cudaGraphExecDestroy(E.gexec_sorted);
-    E.gexec_sorted = capture(s, [&] {
-        sort_cells_spatial(s);
-        record();
-    });
+    E.gexec_sorted = capture(s, [&] { record(true); });
     s->pdl_graph = false;
 }
 
