@@ -66,7 +66,7 @@ struct Engine {
     DBuf<double> red;
     cudaGraphExec_t gexec_a = nullptr, gexec_b = nullptr;
     cudaStream_t br[kBranches] = {};
-    cudaEvent_t ev_fork = nullptr, ev_join[kBranches] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[kBranches] = {}, ev_bins = nullptr;
     ~Engine()
     {
         for (auto& b : br)
@@ -74,6 +74,7 @@ struct Engine {
         for (auto& e : ev_join)
             if (e) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_bins) cudaEventDestroy(ev_bins);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (gexec_a) cudaGraphExecDestroy(gexec_a);
         if (gexec_b) cudaGraphExecDestroy(gexec_b);
@@ -94,6 +95,7 @@ struct Engine {
         m = std::move(o.m), v = std::move(o.v), part = std::move(o.part), red = std::move(o.red);
         obs_count = std::move(o.obs_count);
         std::swap(br, o.br), std::swap(ev_fork, o.ev_fork), std::swap(ev_join, o.ev_join);
+        std::swap(ev_bins, o.ev_bins);
         if (!o.partitioned && o.gexec && !o.gexec_a) { // its graphs, for adopt_graphs
             std::swap(old_gexec, o.gexec), std::swap(old_gexec_sorted, o.gexec_sorted);
             std::swap(old_refresh, o.refresh_gexec), std::swap(old_sort, o.sort_gexec);
@@ -235,6 +237,7 @@ void capture_iteration(tdpg_session* s, Engine& E)
     fa.total_movable = s->grid.total_movable, fa.beta = E.cfg.beta;
     fa.sched = E.sched, fa.stop_overflow = E.cfg.stop_overflow, fa.terms = E.terms, fa.trace = E.trace;
     fa.timing_row = E.timing_row, fa.timing_row_clear = E.timing_row;
+    if (!E.ev_bins) CK(cudaEventCreateWithFlags(&E.ev_bins, cudaEventDisableTiming));
     if (!E.ev_fork) {
         CK(cudaEventCreateWithFlags(&E.ev_fork, cudaEventDisableTiming));
         for (int k = 0; k < Engine::kBranches; ++k) {
@@ -308,17 +311,23 @@ void capture_iteration(tdpg_session* s, Engine& E)
         s->st = E.br[0];
         if (sort) sort_cells_spatial(s); // (only the density kernels read the spatial order)
         launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
+        CK(cudaEventRecord(E.ev_bins, E.br[0])); // the density value partials are ready
         launch_dens_grad(s, E.ctrl, E.br[0]);
         s->st = main;
         cudaStream_t wa_st[Engine::kBranches] = {main};
         for (int k = 1; k < Engine::kBranches; ++k) wa_st[k] = E.br[k];
         launch_wirelength_pp(s, E.gamma, E.cfg.net_weighting != 0, part_wl, part_hp, true, E.cfg.pp_loss,
                              E.cfg.beta, part_pp, E.ctrl, wa_st, Engine::kBranches);
-        for (int k = 0; k < Engine::kBranches; ++k) {
+        // finalize needs the WA partials and the density value, not the density gradient: it runs
+        // beside the gradient kernel, and the cell kernel joins both
+        for (int k = 1; k < Engine::kBranches; ++k) {
             CK(cudaEventRecord(E.ev_join[k], E.br[k]));
             CK(cudaStreamWaitEvent(main, E.ev_join[k], 0));
         }
+        CK(cudaStreamWaitEvent(main, E.ev_bins, 0));
         launch_finalize(s, fa, E.ctrl, E.cur);
+        CK(cudaEventRecord(E.ev_join[0], E.br[0]));
+        CK(cudaStreamWaitEvent(main, E.ev_join[0], 0));
         launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
                      false);
     };
