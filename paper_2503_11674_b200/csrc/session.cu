@@ -45,10 +45,13 @@ void* cub_scratch(tdpg_session* s, size_t bytes)
 }
 
 // Kernel: pin positions (netlist.cpp:23-32): anchor + offset, two IEEE adds.
+// Fixed-cell baseline (density.cpp:75-93): exact overlap areas, accumulated in the grid's fixed point
+// (integer atomics commute, so the baseline is the same bits whatever the order), then converted.
 __global__ void k_fixed_baseline(int C, const double2* xy, const double2* wh, const uint8_t* fixed, double x0,
-                                 double y0, double bw, double bh, int nx, int ny, double* base)
+                                 double y0, double bw, double bh, int nx, int ny, double scale,
+                                 unsigned long long* base_q)
 {
-    // Fixed cells are few; one thread per fixed cell, fp64 atomics into the baseline.
+    // Fixed cells are few; one thread per fixed cell.
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C || !fixed[c]) return;
     const double xl = xy[c].x, xh = xl + wh[c].x, yl = xy[c].y, yh = yl + wh[c].y;
@@ -60,17 +63,27 @@ __global__ void k_fixed_baseline(int C, const double2* xy, const double2* wh, co
         for (int by = by0; by <= by1; ++by) {
             const double ox = smin(xh, x0 + (bx + 1) * bw) - smax(xl, x0 + bx * bw);
             const double oy = smin(yh, y0 + (by + 1) * bh) - smax(yl, y0 + by * bh);
-            if (ox > 0.0 && oy > 0.0) atomicAdd(&base[static_cast<long long>(bx) * ny + by], ox * oy);
+            if (ox > 0.0 && oy > 0.0)
+                atomicAdd(&base_q[static_cast<long long>(bx) * ny + by],
+                          static_cast<unsigned long long>(__double2ll_rn(ox * oy * scale)));
         }
+}
+
+__global__ void k_fixed_to_double(long long B, double* base, double inv_scale)
+{
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < B) base[i] = static_cast<double>(reinterpret_cast<const long long*>(base)[i]) * inv_scale;
 }
 
 void refresh_fixed_baseline(tdpg_session* s)
 {
     Grid& g = s->grid;
     if (!g.valid() || !g.has_fixed) return;
-    g.base.zero(s->st);
+    g.base.zero(s->st); // (as int64 zeros)
     k_fixed_baseline<<<blocks_for(s->C, 256), 256, 0, s->st>>>(s->C, s->cell_xy, s->cell_wh, s->cell_fixed, g.x0,
-                                                                g.y0, g.bw, g.bh, g.nx, g.ny, g.base);
+                                                                g.y0, g.bw, g.bh, g.nx, g.ny, g.scale,
+                                                                reinterpret_cast<unsigned long long*>(g.base.p));
+    k_fixed_to_double<<<blocks_for(g.bins(), 256), 256, 0, s->st>>>(g.bins(), g.base, g.inv_scale);
     CK_LAUNCH();
 }
 
