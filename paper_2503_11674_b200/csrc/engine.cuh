@@ -163,6 +163,8 @@ struct tdpg_session {
     tdpg::DBuf<double> sta_part; // STA reduction partials
     cudaGraphExec_t sta_gexec = nullptr; // the per-level STA sweep, captured once
     std::array<uint64_t, 9> sta_graph_key{};
+    cudaGraphExec_t ex_gexec = nullptr;    // endpoint extraction up to the host count read (timing.cu)
+    std::array<long long, 4> ex_key{};
     cudaGraphExec_t sta_gexec_L = nullptr; // the same sweep leaving its results in L-space
     std::array<uint64_t, 9> sta_graph_key_L{};
     // ledger-update scratch

@@ -833,6 +833,7 @@ tdpg_session::~tdpg_session()
     tdpg::comm_destroy(this);
     if (sta_gexec) cudaGraphExecDestroy(sta_gexec);
     if (sta_gexec_L) cudaGraphExecDestroy(sta_gexec_L);
+    if (ex_gexec) cudaGraphExecDestroy(ex_gexec);
     if (st_req) cudaStreamSynchronize(st_req), cudaStreamDestroy(st_req);
     if (ev_sta_fork) cudaEventDestroy(ev_sta_fork);
     if (ev_sta_join) cudaEventDestroy(ev_sta_join);

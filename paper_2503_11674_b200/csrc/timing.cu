@@ -1159,65 +1159,71 @@ void extract_endpoint_dev(tdpg_session* s, int n)
 {
     if (!s->sta_valid) run_sta_dev(s, false);
     const bool Lsp = s->pins_stale; // the sweep's results are in L-space (no per-pin arrays)
-    // endpoint keys from the current STA (cheap; keeps extraction self-contained)
-    s->sta_out.reserve(4);
-    double* out3 = s->sta_out.p;
-    {
-        const int P = s->P;
-        const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, s->EP), kBlock))));
-        s->part.reserve(3 * nb + 8);
-        const size_t ep = static_cast<size_t>(std::max(s->EP, 1));
-        s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
-        if (Lsp)
-            k_slack_keys_L<<<nb, kBlock, 0, s->st>>>(s->EP, s->ep_sorted, s->L_of, s->L_arr, s->L_req, s->sort_k0,
-                                                     s->sort_v0, s->part);
-        else
-            k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, s->EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0,
-                                                   s->sort_v0, s->part);
+    // exact ties first (the backtrace reads the resolved predecessors; host-side state, outside the graph)
+    if (!Lsp) {
+        resolve_ties_dev(s);
+    } else if (!s->ties_resolved) {
+        const int stride = s->L + 2;
+        s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * stride);
+        k_resolve_ties_L<<<1, kBlock, 0, s->st>>>(make_largs(s), s->d_level, s->L, s->tie_scratch, stride);
         CK_LAUNCH();
-        k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
-        CK_LAUNCH();
+        s->ties_resolved = true;
     }
-    const int EP = s->EP;
-    if (EP > 0) {
-        size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP, 0,
-                                        64, s->st);
-        void* tmp = cub_scratch(s, bytes);
-        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP, 0, 64,
-                                           s->st));
-    }
-    // ties: resolve before any backtrace
-    {
-        if (!Lsp) {
-            resolve_ties_dev(s);
-        } else if (!s->ties_resolved) {
-            const int stride = s->L + 2;
-            s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * stride);
-            k_resolve_ties_L<<<1, kBlock, 0, s->st>>>(make_largs(s), s->d_level, s->L, s->tie_scratch, stride);
-            CK_LAUNCH();
-            s->ties_resolved = true;
-        }
-    }
+    const int EP = s->EP, P = s->P;
     // the selection size min(n, violated) stays on the device: the backtrace runs over an upper bound of
     // slots (zero-length past the selection), one host read brings back every count
     const int ub = (n <= 0) ? EP : std::min(n, EP);
     s->n_paths = 0, s->n_path_pins = 0, s->n_hits = 0, s->uniq_pairs = 0, s->uniq_endpoints = 0, s->candidates = 0;
     if (ub <= 0) return;
+    // endpoint keys, the (slack, pin) sort, the backtrace lengths and their scans: a fixed-size sequence
+    // of ~17 launches, replayed as one graph (re-captured when n, the STA form or any buffer changes)
+    s->sta_out.reserve(4);
+    double* out3 = s->sta_out.p;
+    const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(P, EP), kBlock))));
+    s->part.reserve(3 * nb + 8);
+    const size_t ep = static_cast<size_t>(std::max(EP, 1));
+    s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
     s->ex_len.reserve(ub), s->ex_hops.reserve(ub), s->ex_off.reserve(ub), s->ex_hoff.reserve(ub);
     s->ex_slack.reserve(ub);
-    if (Lsp)
-        k_bt_count_Ln<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->L_of, s->L_pred, s->L_flags,
-                                                                    s->ex_len, s->ex_hops, out3, n);
-    else
-        k_bt_count<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
-                                                                 s->ex_hops, out3, n);
-    CK_LAUNCH();
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->ex_len.p, s->ex_off.p, ub, s->st);
-    void* tmp = cub_scratch(s, bytes);
-    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_len.p, s->ex_off.p, ub, s->st));
-    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->ex_hops.p, s->ex_hoff.p, ub, s->st));
+    size_t b_sort = 0, b_scan = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b_sort, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP, 0,
+                                    64, s->st);
+    cub::DeviceScan::ExclusiveSum(nullptr, b_scan, s->ex_len.p, s->ex_off.p, ub, s->st);
+    cub_scratch(s, std::max(b_sort, b_scan));
+    const std::array<long long, 4> key = {n, ub, Lsp ? 1 : 0, static_cast<long long>(dbuf_epoch())};
+    auto record = [&] {
+        if (Lsp)
+            k_slack_keys_L<<<nb, kBlock, 0, s->st>>>(EP, s->ep_sorted, s->L_of, s->L_arr, s->L_req, s->sort_k0,
+                                                     s->sort_v0, s->part);
+        else
+            k_slack_keys<<<nb, kBlock, 0, s->st>>>(P, EP, s->arr, s->req, s->slack, s->ep_sorted, s->sort_k0,
+                                                   s->sort_v0, s->part);
+        k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
+        size_t bytes = s->cub_tmp.n;
+        CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p,
+                                           s->sort_v1.p, EP, 0, 64, s->st));
+        if (Lsp)
+            k_bt_count_Ln<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->L_of, s->L_pred,
+                                                                        s->L_flags, s->ex_len, s->ex_hops, out3, n);
+        else
+            k_bt_count<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
+                                                                     s->ex_hops, out3, n);
+        bytes = s->cub_tmp.n;
+        CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_len.p, s->ex_off.p, ub, s->st));
+        bytes = s->cub_tmp.n;
+        CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_hops.p, s->ex_hoff.p, ub, s->st));
+    };
+    if (!s->ex_gexec || key != s->ex_key) {
+        if (s->ex_gexec) cudaGraphExecDestroy(s->ex_gexec), s->ex_gexec = nullptr;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal));
+        record();
+        CK(cudaStreamEndCapture(s->st, &g));
+        CK(cudaGraphInstantiate(&s->ex_gexec, g, 0));
+        cudaGraphDestroy(g);
+        s->ex_key = key;
+    }
+    CK(cudaGraphLaunch(s->ex_gexec, s->st));
     int tail[4];
     double h3[3];
     CK(cudaMemcpyAsync(h3, out3, sizeof h3, cudaMemcpyDeviceToHost, s->st));
@@ -1249,11 +1255,11 @@ void extract_endpoint_dev(tdpg_session* s, int n)
                                                                  s->hit_idx);
     CK_LAUNCH();
     if (H > 0) {
-        bytes = 0;
+        size_t bytes = 0;
         const int kb = std::min(64, 32 + bits_for(s->P)); // pair keys (lo << 32) | hi with lo, hi < P
         cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
                                         static_cast<int>(H), 0, kb, s->st);
-        tmp = cub_scratch(s, bytes);
+        void* tmp = cub_scratch(s, bytes);
         CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
                                            static_cast<int>(H), 0, kb, s->st));
         CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
