@@ -195,6 +195,7 @@ struct tdpg_session {
     tdpg::DBuf<int> ex_ep, ex_len, ex_hops, ex_off, ex_hoff, ex_pins;
     tdpg::DBuf<double> ex_slack;
     tdpg::DBuf<unsigned long long> hit_key, hit_key_s;
+    tdpg::DBuf<unsigned> pair_bits; // unique-pair bits over sink pins (endpoint extraction)
     tdpg::DBuf<int> hit_idx, hit_idx_s;
     tdpg::DBuf<double> hit_slack;
     int n_paths = 0;

@@ -733,12 +733,22 @@ __global__ void k_bt_count(int n, const int* __restrict__ ep, const int* __restr
     len[i] = l, hops[i] = h;
 }
 
+// mark_pair(): the pair of a hop is its net arc, identified by the sink pin; the first hit of a pair
+// sets its bit and counts it (collect_pin_pairs' unique set, paths.cpp:89-102)
+__device__ __forceinline__ void mark_pair(unsigned* bits, int* uniq, int sink)
+{
+    if (!bits) return;
+    const unsigned m = 1u << (sink & 31);
+    if (!(atomicOr(&bits[sink >> 5], m) & m)) atomicAdd(uniq, 1);
+}
+
 __global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restrict__ pred,
                            const uint8_t* __restrict__ pin_dir, const int* __restrict__ len,
                            const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
                            const double* __restrict__ arr, double clock, int* __restrict__ pins,
                            double* __restrict__ pslack, unsigned long long* __restrict__ hkey,
-                           double* __restrict__ hslack, int* __restrict__ hidx)
+                           double* __restrict__ hslack, int* __restrict__ hidx, unsigned* __restrict__ bits = nullptr,
+                           int* __restrict__ uniq = nullptr)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n || len[i] == 0) return;
@@ -756,6 +766,7 @@ __global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restr
             hslack[h] = sl;
             hidx[h] = h;
             --h;
+            mark_pair(bits, uniq, v);
         }
     }
 }
@@ -783,7 +794,8 @@ __global__ void k_bt_write_Ln(int n, const int* __restrict__ ep, const int* __re
                               const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
                               const double* __restrict__ L_arr, double clock, int* __restrict__ pins,
                               double* __restrict__ pslack, unsigned long long* __restrict__ hkey,
-                              double* __restrict__ hslack, int* __restrict__ hidx)
+                              double* __restrict__ hslack, int* __restrict__ hidx, unsigned* __restrict__ bits,
+                              int* __restrict__ uniq)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n || len[i] == 0) return;
@@ -802,6 +814,7 @@ __global__ void k_bt_write_Ln(int n, const int* __restrict__ ep, const int* __re
             hslack[h] = sl;
             hidx[h] = h;
             --h;
+            mark_pair(bits, uniq, vp);
         }
         vp = up;
     }
@@ -1243,35 +1256,28 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     s->ex_pins.reserve(s->n_path_pins + 1);
     s->hit_key.reserve(H + 1), s->hit_slack.reserve(H + 1), s->hit_idx.reserve(H + 1);
     s->hit_key_s.reserve(H + 1), s->hit_idx_s.reserve(H + 1);
+    // unique pairs (net arcs) as bits over the sink pins, set by the backtrace itself
+    const size_t nbits = static_cast<size_t>(P) / 32 + 1;
+    s->pair_bits.reserve(nbits);
+    CK(cudaMemsetAsync(s->pair_bits.p, 0, nbits * sizeof(unsigned), s->st));
+    CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
     if (Lsp)
         k_bt_write_Ln<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->L_of, s->L_pin, s->L_pred,
                                                                     s->L_flags, s->ex_len, s->ex_off, s->ex_hops,
                                                                     s->ex_hoff, s->L_arr, s->clock, s->ex_pins,
-                                                                    s->ex_slack, s->hit_key, s->hit_slack, s->hit_idx);
+                                                                    s->ex_slack, s->hit_key, s->hit_slack, s->hit_idx,
+                                                                    s->pair_bits.p, s->counters.p + 1);
     else
         k_bt_write<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
                                                                  s->ex_off, s->ex_hops, s->ex_hoff, s->arr, s->clock,
                                                                  s->ex_pins, s->ex_slack, s->hit_key, s->hit_slack,
-                                                                 s->hit_idx);
+                                                                 s->hit_idx, s->pair_bits.p, s->counters.p + 1);
     CK_LAUNCH();
-    if (H > 0) {
-        size_t bytes = 0;
-        const int kb = std::min(64, 32 + bits_for(s->P)); // pair keys (lo << 32) | hi with lo, hi < P
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
-                                        static_cast<int>(H), 0, kb, s->st);
-        void* tmp = cub_scratch(s, bytes);
-        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
-                                           static_cast<int>(H), 0, kb, s->st));
-        CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
-        k_count_heads<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 4), kBlock, 0, s->st>>>(H, s->hit_key_s,
-                                                                                                 s->counters.p + 1);
-        CK_LAUNCH();
-        int u = 0;
-        CK(cudaMemcpyAsync(&u, s->counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
-        CK(cudaStreamSynchronize(s->st));
-        s->uniq_pairs = u;
-    }
-    s->hits_sorted = true;
+    int u = 0;
+    CK(cudaMemcpyAsync(&u, s->counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    s->uniq_pairs = H > 0 ? u : 0;
+    s->hits_sorted = false; // (sorted by ledger_update_dev when the ledger takes them)
 }
 
 // Apply the last sorted hits (hit_key_s / hit_idx_s / hit_slack) to the ledger.
@@ -1320,7 +1326,17 @@ void ledger_apply_sorted(tdpg_session* s, long long H, double wns, double w0, do
 
 void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool)
 {
-    ledger_apply_sorted(s, s->n_hits, wns, w0, w1);
+    const long long H = s->n_hits;
+    if (!s->hits_sorted && H > 0) { // stable sort of the hits by pair (update_pair_weights order per pair)
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
+                                        static_cast<int>(H), 0, 64, s->st);
+        void* tmp = cub_scratch(s, bytes);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->hit_key.p, s->hit_key_s.p, s->hit_idx.p, s->hit_idx_s.p,
+                                           static_cast<int>(H), 0, 64, s->st));
+        s->hits_sorted = true;
+    }
+    ledger_apply_sorted(s, H, wns, w0, w1);
 }
 
 void net_weights_dev(tdpg_session* s)
