@@ -196,6 +196,8 @@ struct tdpg_session {
     tdpg::DBuf<double> ex_slack;
     tdpg::DBuf<unsigned long long> hit_key, hit_key_s;
     tdpg::DBuf<unsigned> pair_bits; // unique-pair bits over sink pins (endpoint extraction)
+    tdpg::DBuf<int> ex_tmp_pins;                // fixed-stride path slots (endpoint extraction)
+    tdpg::DBuf<unsigned long long> ex_tmp_keys;
     tdpg::DBuf<int> hit_idx, hit_idx_s;
     tdpg::DBuf<double> hit_slack;
     int n_paths = 0;

@@ -771,52 +771,62 @@ __global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restr
     }
 }
 
-// k_bt_count / k_bt_write on L-space predecessors (an L-space-only STA), pins translated on output.
-__global__ void k_bt_count_Ln(int n, const int* __restrict__ ep, const int* __restrict__ L_of,
-                              const int* __restrict__ L_pred, const uint8_t* __restrict__ L_flags,
-                              int* __restrict__ len, int* __restrict__ hops, const double* __restrict__ nvp,
-                              int n_req)
+// One-pass backtrace of the selected endpoints into fixed-stride slots (path i's pins end at
+// pins[i S + S - 1], its hits at keys[i SH + SH - 1], both written from the endpoint backwards), with the
+// path slack, lengths and unique-pair bits; k_bt_compact then packs the slots by the scanned lengths.
+// Level-major predecessors when L_of is given (an L-space-only STA), per-pin ones otherwise.
+__global__ void k_bt_walk(int ub, const int* __restrict__ ep, const double* __restrict__ nvp, int n_req,
+                          const int* __restrict__ L_of, const int* __restrict__ L_pin, const int* __restrict__ pred,
+                          const uint8_t* __restrict__ L_flags, const uint8_t* __restrict__ pin_dir,
+                          const double* __restrict__ arr, double clock, int S, int SH, int* __restrict__ pins,
+                          unsigned long long* __restrict__ keys, int* __restrict__ len, int* __restrict__ hops,
+                          double* __restrict__ pslack, unsigned* __restrict__ bits, int* __restrict__ uniq)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
-    if (i >= selected(n, nvp, n_req)) {
+    if (i >= ub) return;
+    if (i >= selected(ub, nvp, n_req)) {
         len[i] = 0, hops[i] = 0;
         return;
     }
-    int v = L_of[ep[i]], l = 1, h = 0;
-    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) ++l, h += (L_flags[u] & 4) != 0;
-    len[i] = l, hops[i] = h;
-}
-
-__global__ void k_bt_write_Ln(int n, const int* __restrict__ ep, const int* __restrict__ L_of,
-                              const int* __restrict__ L_pin, const int* __restrict__ L_pred,
-                              const uint8_t* __restrict__ L_flags, const int* __restrict__ len,
-                              const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
-                              const double* __restrict__ L_arr, double clock, int* __restrict__ pins,
-                              double* __restrict__ pslack, unsigned long long* __restrict__ hkey,
-                              double* __restrict__ hslack, int* __restrict__ hidx, unsigned* __restrict__ bits,
-                              int* __restrict__ uniq)
-{
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n || len[i] == 0) return;
     const int e = ep[i];
-    int v = L_of[e], vp = e;
-    const double sl = clock - L_arr[v]; // paths.cpp:123
+    int v = L_of ? L_of[e] : e, vp = e;
+    const double sl = clock - arr[v]; // paths.cpp:123
     pslack[i] = sl;
-    int k = off[i] + len[i] - 1, h = hoff[i] + hops[i] - 1;
-    pins[k] = e;
-    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) {
-        const int up = L_pin[u];
-        pins[--k] = up;
-        if (L_flags[u] & 4) {
+    int* pp = pins + static_cast<long long>(i) * S;
+    unsigned long long* kk = keys + static_cast<long long>(i) * SH;
+    int k = S - 1, kh = SH - 1;
+    pp[k] = e;
+    for (int u = pred[v]; u >= 0; v = u, u = pred[v]) {
+        const int up = L_of ? L_pin[u] : u;
+        pp[--k] = up;
+        if (L_of ? (L_flags[u] & 4) != 0 : pin_dir[u] == 1) { // a hop leaving an Output pin (paths.cpp:195-200)
             const unsigned lo = static_cast<unsigned>(min(up, vp)), hi = static_cast<unsigned>(max(up, vp));
-            hkey[h] = (static_cast<unsigned long long>(lo) << 32) | hi;
-            hslack[h] = sl;
-            hidx[h] = h;
-            --h;
+            kk[kh--] = (static_cast<unsigned long long>(lo) << 32) | hi;
             mark_pair(bits, uniq, vp);
         }
         vp = up;
+    }
+    len[i] = S - k, hops[i] = SH - 1 - kh;
+}
+
+__global__ void k_bt_compact(int ub, int S, int SH, const int* __restrict__ pins,
+                             const unsigned long long* __restrict__ keys, const int* __restrict__ len,
+                             const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
+                             const double* __restrict__ pslack, int* __restrict__ out_pins,
+                             unsigned long long* __restrict__ hkey, double* __restrict__ hslack,
+                             int* __restrict__ hidx)
+{
+    const long long t = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
+    if (t >= static_cast<long long>(ub) * S) return;
+    const int i = static_cast<int>(t / S), j = static_cast<int>(t - static_cast<long long>(i) * S);
+    const int l = len[i];
+    if (j < l) out_pins[off[i] + j] = pins[static_cast<long long>(i) * S + S - l + j];
+    const int nh = hops[i];
+    if (j < nh) {
+        const int h = hoff[i] + j;
+        hkey[h] = keys[static_cast<long long>(i) * SH + SH - nh + j];
+        hslack[h] = pslack[i];
+        hidx[h] = h;
     }
 }
 
@@ -1198,6 +1208,10 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     s->sort_k0.reserve(ep), s->sort_k1.reserve(ep), s->sort_v0.reserve(ep), s->sort_v1.reserve(ep);
     s->ex_len.reserve(ub), s->ex_hops.reserve(ub), s->ex_off.reserve(ub), s->ex_hoff.reserve(ub);
     s->ex_slack.reserve(ub);
+    const int S = s->L + 1, SH = s->L / 2 + 2; // pins per path <= levels, hits <= Output pins on it
+    s->ex_tmp_pins.reserve(static_cast<size_t>(ub) * S), s->ex_tmp_keys.reserve(static_cast<size_t>(ub) * SH);
+    const size_t nbits = static_cast<size_t>(P) / 32 + 1;
+    s->pair_bits.reserve(nbits);
     size_t b_sort = 0, b_scan = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b_sort, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP, 0,
                                     64, s->st);
@@ -1215,12 +1229,12 @@ void extract_endpoint_dev(tdpg_session* s, int n)
         size_t bytes = s->cub_tmp.n;
         CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p,
                                            s->sort_v1.p, EP, 0, 64, s->st));
-        if (Lsp)
-            k_bt_count_Ln<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->L_of, s->L_pred,
-                                                                        s->L_flags, s->ex_len, s->ex_hops, out3, n);
-        else
-            k_bt_count<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(ub, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
-                                                                     s->ex_hops, out3, n);
+        CK(cudaMemsetAsync(s->pair_bits.p, 0, nbits * sizeof(unsigned), s->st));
+        CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
+        k_bt_walk<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(
+            ub, s->sort_v1, out3, n, Lsp ? s->L_of.p : nullptr, s->L_pin, Lsp ? s->L_pred.p : s->pred.p, s->L_flags,
+            s->pin_dir, Lsp ? s->L_arr.p : s->arr.p, s->clock, S, SH, s->ex_tmp_pins, s->ex_tmp_keys, s->ex_len,
+            s->ex_hops, s->ex_slack, s->pair_bits, s->counters.p + 1);
         bytes = s->cub_tmp.n;
         CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_len.p, s->ex_off.p, ub, s->st));
         bytes = s->cub_tmp.n;
@@ -1237,9 +1251,10 @@ void extract_endpoint_dev(tdpg_session* s, int n)
         s->ex_key = key;
     }
     CK(cudaGraphLaunch(s->ex_gexec, s->st));
-    int tail[4];
+    int tail[5];
     double h3[3];
     CK(cudaMemcpyAsync(h3, out3, sizeof h3, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&tail[4], s->counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(&tail[0], s->ex_off.p + ub - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(&tail[1], s->ex_len.p + ub - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(&tail[2], s->ex_hoff.p + ub - 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
@@ -1256,27 +1271,12 @@ void extract_endpoint_dev(tdpg_session* s, int n)
     s->ex_pins.reserve(s->n_path_pins + 1);
     s->hit_key.reserve(H + 1), s->hit_slack.reserve(H + 1), s->hit_idx.reserve(H + 1);
     s->hit_key_s.reserve(H + 1), s->hit_idx_s.reserve(H + 1);
-    // unique pairs (net arcs) as bits over the sink pins, set by the backtrace itself
-    const size_t nbits = static_cast<size_t>(P) / 32 + 1;
-    s->pair_bits.reserve(nbits);
-    CK(cudaMemsetAsync(s->pair_bits.p, 0, nbits * sizeof(unsigned), s->st));
-    CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
-    if (Lsp)
-        k_bt_write_Ln<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->L_of, s->L_pin, s->L_pred,
-                                                                    s->L_flags, s->ex_len, s->ex_off, s->ex_hops,
-                                                                    s->ex_hoff, s->L_arr, s->clock, s->ex_pins,
-                                                                    s->ex_slack, s->hit_key, s->hit_slack, s->hit_idx,
-                                                                    s->pair_bits.p, s->counters.p + 1);
-    else
-        k_bt_write<<<blocks_for(np, kBlock), kBlock, 0, s->st>>>(np, s->sort_v1, s->pred, s->pin_dir, s->ex_len,
-                                                                 s->ex_off, s->ex_hops, s->ex_hoff, s->arr, s->clock,
-                                                                 s->ex_pins, s->ex_slack, s->hit_key, s->hit_slack,
-                                                                 s->hit_idx, s->pair_bits.p, s->counters.p + 1);
+    // pack the fixed-stride slots (coalesced; the unique pairs were counted by the walk)
+    k_bt_compact<<<blocks_for(static_cast<long long>(np) * S, kBlock), kBlock, 0, s->st>>>(
+        np, S, SH, s->ex_tmp_pins, s->ex_tmp_keys, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff, s->ex_slack,
+        s->ex_pins, s->hit_key, s->hit_slack, s->hit_idx);
     CK_LAUNCH();
-    int u = 0;
-    CK(cudaMemcpyAsync(&u, s->counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s->st));
-    CK(cudaStreamSynchronize(s->st));
-    s->uniq_pairs = H > 0 ? u : 0;
+    s->uniq_pairs = H > 0 ? tail[4] : 0;
     s->hits_sorted = false; // (sorted by ledger_update_dev when the ledger takes them)
 }
 
