@@ -398,3 +398,18 @@ def test_l_space_sta_then_per_pin_consumers(seed):
     ts, to = s.sta(), o.sta()
     for k in ("arr", "req", "slack", "arr_known", "req_known"):
         assert np.array_equal(ts[k], to[k]), k
+
+
+def test_repeated_runs_adopt_graphs_and_stay_exact():
+    """A session's later runs reuse the previous run's CUDA graphs when nothing moved and the
+    configuration matches (and re-capture when it does not): every run ends bitwise where a fresh
+    session with the same configuration ends."""
+    d = generate(seed=7, cells=6000, fail_frac=0.8, calibrate=True)
+    base = {"grid_nx": 32, "grid_ny": 32, "m": 5, "timing_start_iter": 0, "max_iters": 30, "seed": 4}
+    other = dict(base, gamma_frac=base.get("gamma_frac", 0.01) * 1.5)
+    s = Session(d)
+    runs = [s.place(base), s.place(base), s.place(other), s.place(base)]
+    fresh_base, fresh_other = Session(d).place(base), Session(d).place(other)
+    for r, f in zip(runs, (fresh_base, fresh_base, fresh_other, fresh_base)):
+        assert np.array_equal(r["positions"], f["positions"])
+        assert [t.hpwl for t in r["trace"]] == [t.hpwl for t in f["trace"]]
