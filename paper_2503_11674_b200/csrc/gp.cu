@@ -231,6 +231,19 @@ __device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAx
         x[i] = a + __ldcs(e_off + 2 * e + axis);
     }
     if (stop) return; // (uniform over the block)
+    // pin-pair operands: for the larger nets issued ahead of the WA math so their latency overlaps it
+    // (measured: 6-8 pins 35 -> 28 us once the ledger is populated; the 2-5 group, at its 64-register
+    // budget, only spills more)
+    constexpr bool kEarlyPP = N >= 6;
+    uint32_t mask = 0u, ord = 0u;
+    double wts[N];
+    if constexpr (kEarlyPP) {
+        const int i_net0 = b.y + (on ? t : 0);
+        mask = (on && pp.mask) ? pp.mask[i_net0] : 0u;
+        ord = mask ? pp.ord[i_net0] : 0u;
+#pragma unroll
+        for (int j = 0; j < N; ++j) wts[j] = (j > 0 && (mask >> j & 1u)) ? pp.w_e[base + j * kBlock] : 0.0;
+    }
     double v, ext;
     wa_axis<N>(x, inv_gamma, g, v, ext);
     const double v_other = __shfl_xor_sync(0xffffffffu, v, 1), e_other = __shfl_xor_sync(0xffffffffu, ext, 1);
@@ -239,18 +252,20 @@ __device__ __forceinline__ void wa_axis_block(const int4 b, int gblk, const WaAx
     double wl = 0.0, hp = 0.0, ppv = 0.0;
     if (on && axis == 0) wl = w * (v + v_other);   // w (vx + vy), on the x thread
     if (on && axis == 1) hp = e_other + ext;        // hx + hy, on the y thread (see the reduction below)
-    const uint32_t mask = (on && pp.mask) ? pp.mask[i_net] : 0u;
+    if constexpr (!kEarlyPP) {
+        mask = (on && pp.mask) ? pp.mask[i_net] : 0u;
+        ord = mask ? pp.ord[i_net] : 0u;
+    }
     double p[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) p[i] = 0.0;
     if (pp.mask) { // pin pairs of this net (pin_pairs.cpp:17-49), see pp_net
-        const uint32_t ord = mask ? pp.ord[i_net] : 0u;
 #pragma unroll
         for (int j = 1; j < N; ++j) {
             const double d = x[j] - x[0];
             const double d_other = __shfl_xor_sync(0xffffffffu, d, 1);
             if (!(mask >> j & 1u)) continue;
-            const double wt = pp.w_e[base + j * kBlock];
+            const double wt = kEarlyPP ? wts[j] : pp.w_e[base + j * kBlock];
             const double dx = axis ? d_other : d, dy = axis ? d : d_other;
             if (pp.kind == 0) {
                 if (axis == 0) ppv += wt * (dx * dx + dy * dy);
