@@ -1633,24 +1633,22 @@ void place_tail_reserve(tdpg_session* s)
     s->sta_out.reserve(4);
 }
 
-// Dense ledger -> the sorted (a, b, w) ledger of the session (tdpg_pp_get), after a run.
-__global__ void k_dense_to_pairs(int P, const double* __restrict__ dl_w, const int* __restrict__ pin_driver,
-                                 unsigned long long* __restrict__ key, double* __restrict__ w)
+// The dense ledger's pairs (weight > 0), compacted in any order (the sort below fixes it).
+__global__ void k_dense_compact(int P, const double* __restrict__ dl_w, const int* __restrict__ pin_driver,
+                                unsigned long long* __restrict__ key, double* __restrict__ w, int* __restrict__ n)
 {
     const int v = blockIdx.x * kBlock + threadIdx.x;
     if (v >= P) return;
     const double x = dl_w[v];
     const int d = pin_driver[v];
-    if (x > 0.0 && d >= 0) {
-        const unsigned lo = static_cast<unsigned>(min(v, d)), hi = static_cast<unsigned>(max(v, d));
-        key[v] = (static_cast<unsigned long long>(lo) << 32) | hi;
-        w[v] = x;
-    } else {
-        key[v] = kNoKey;
-        w[v] = 0.0;
-    }
+    if (!(x > 0.0 && d >= 0)) return;
+    const unsigned lo = static_cast<unsigned>(min(v, d)), hi = static_cast<unsigned>(max(v, d));
+    const int k = atomicAdd(n, 1);
+    key[k] = (static_cast<unsigned long long>(lo) << 32) | hi;
+    w[k] = x;
 }
 
+// Dense ledger -> the sorted (a, b, w) ledger of the session (tdpg_pp_get), after a run.
 void dense_ledger_to_sorted(tdpg_session* s)
 {
     const int P = s->P;
@@ -1662,15 +1660,21 @@ void dense_ledger_to_sorted(tdpg_session* s)
     DBuf<unsigned long long>& k1 = s->dl_k1;
     DBuf<double>& w0 = s->dl_w0;
     DBuf<double>& w1 = s->dl_w1;
-    k_dense_to_pairs<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->dl_w, s->pin_driver, k0, w0);
-    CK_LAUNCH();
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0.p, k1.p, w0.p, w1.p, P, 0, 64, s->st);
-    void* tmp = cub_scratch(s, bytes);
-    CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0.p, k1.p, w0.p, w1.p, P, 0, 64, s->st));
+    // only the Q pairs are sorted (by their key bits), not the P-slot dense array
     unsigned long long q = 0;
     CK(cudaMemcpyAsync(&q, s->q_count.p, sizeof q, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemsetAsync(s->counters.p + 4, 0, sizeof(int), s->st));
+    k_dense_compact<<<blocks_for(P, kBlock), kBlock, 0, s->st>>>(P, s->dl_w, s->pin_driver, k0, w0,
+                                                                 s->counters.p + 4);
+    CK_LAUNCH();
     CK(cudaStreamSynchronize(s->st));
+    if (q) {
+        size_t bytes = 0;
+        const int kb = std::min(64, 32 + bits_for(P));
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0.p, k1.p, w0.p, w1.p, static_cast<int>(q), 0, kb, s->st);
+        void* tmp = cub_scratch(s, bytes);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, k0.p, k1.p, w0.p, w1.p, static_cast<int>(q), 0, kb, s->st));
+    }
     s->led_key.reserve(q + 1), s->led_w.reserve(q + 1);
     if (q) {
         CK(cudaMemcpyAsync(s->led_key.p, k1.p, q * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s->st));
