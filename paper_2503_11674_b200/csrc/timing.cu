@@ -830,15 +830,6 @@ __global__ void k_bt_compact(int ub, int S, int SH, const int* __restrict__ pins
     }
 }
 
-__global__ void k_count_heads(long long n, const unsigned long long* __restrict__ k, int* __restrict__ out)
-{
-    int c = 0;
-    for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * kBlock)
-        c += (k[i] != kNoKey) && (i == 0 || k[i - 1] != k[i]);
-    c = warp_sum(c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
-}
 
 // update_pair_weights (pin_pairs.cpp:7-15) over hits sorted stably by pair: one thread per
 // group of equal pairs applies the group's additions in hit order; new pairs enter at w0.
