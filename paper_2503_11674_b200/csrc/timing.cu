@@ -775,16 +775,24 @@ __global__ void k_bt_write(int n, const int* __restrict__ ep, const int* __restr
 // pins[i S + S - 1], its hits at keys[i SH + SH - 1], both written from the endpoint backwards), with the
 // path slack, lengths and unique-pair bits; k_bt_compact then packs the slots by the scanned lengths.
 // Level-major predecessors when L_of is given (an L-space-only STA), per-pin ones otherwise.
+__device__ __forceinline__ bool refresh_active(const double* sta_out, const Ctrl* ctrl)
+{
+    return !(ctrl && ctrl->stopped) && sta_out[1] < 0.0;
+}
+
+// With ctrl (the engine's refresh: every violated endpoint while the refresh is active) the hit key is
+// the sink pin of a violated path (the dense ledger's key, pin_pairs.cpp:11), else the pair key.
 __global__ void k_bt_walk(int ub, const int* __restrict__ ep, const double* __restrict__ nvp, int n_req,
                           const int* __restrict__ L_of, const int* __restrict__ L_pin, const int* __restrict__ pred,
                           const uint8_t* __restrict__ L_flags, const uint8_t* __restrict__ pin_dir,
                           const double* __restrict__ arr, double clock, int S, int SH, int* __restrict__ pins,
                           unsigned long long* __restrict__ keys, int* __restrict__ len, int* __restrict__ hops,
-                          double* __restrict__ pslack, unsigned* __restrict__ bits, int* __restrict__ uniq)
+                          double* __restrict__ pslack, unsigned* __restrict__ bits, int* __restrict__ uniq,
+                          const Ctrl* __restrict__ ctrl = nullptr)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= ub) return;
-    if (i >= selected(ub, nvp, n_req)) {
+    if (i >= (ctrl ? (refresh_active(nvp, ctrl) ? static_cast<int>(nvp[2]) : 0) : selected(ub, nvp, n_req))) {
         len[i] = 0, hops[i] = 0;
         return;
     }
@@ -801,7 +809,8 @@ __global__ void k_bt_walk(int ub, const int* __restrict__ ep, const double* __re
         pp[--k] = up;
         if (L_of ? (L_flags[u] & 4) != 0 : pin_dir[u] == 1) { // a hop leaving an Output pin (paths.cpp:195-200)
             const unsigned lo = static_cast<unsigned>(min(up, vp)), hi = static_cast<unsigned>(max(up, vp));
-            kk[kh--] = (static_cast<unsigned long long>(lo) << 32) | hi;
+            kk[kh--] = ctrl ? (sl < 0.0 ? static_cast<unsigned>(vp) : 0xFFFFFFFFu)
+                            : (static_cast<unsigned long long>(lo) << 32) | hi;
             mark_pair(bits, uniq, vp);
         }
         vp = up;
@@ -814,7 +823,7 @@ __global__ void k_bt_compact(int ub, int S, int SH, const int* __restrict__ pins
                              const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
                              const double* __restrict__ pslack, int* __restrict__ out_pins,
                              unsigned long long* __restrict__ hkey, double* __restrict__ hslack,
-                             int* __restrict__ hidx)
+                             int* __restrict__ hidx, unsigned* __restrict__ hkey32 = nullptr)
 {
     const long long t = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
     if (t >= static_cast<long long>(ub) * S) return;
@@ -824,7 +833,9 @@ __global__ void k_bt_compact(int ub, int S, int SH, const int* __restrict__ pins
     const int nh = hops[i];
     if (j < nh) {
         const int h = hoff[i] + j;
-        hkey[h] = keys[static_cast<long long>(i) * SH + SH - nh + j];
+        const unsigned long long key = keys[static_cast<long long>(i) * SH + SH - nh + j];
+        if (hkey32) hkey32[h] = static_cast<unsigned>(key);
+        else hkey[h] = key;
         hslack[h] = pslack[i];
         hidx[h] = h;
     }
@@ -1344,10 +1355,6 @@ void net_weights_dev(tdpg_session* s)
 // whole refresh is captured once as a CUDA graph.  The reference skips extraction and the ledger
 // when wns >= 0; here the kernels read wns (sta_out[1]) and exit.
 // =====================================================================================
-__device__ __forceinline__ bool refresh_active(const double* sta_out, const Ctrl* ctrl)
-{
-    return !(ctrl && ctrl->stopped) && sta_out[1] < 0.0;
-}
 
 __global__ void k_refresh_begin(const double* sta_out, Ctrl* ctrl, double* timing_row)
 {
@@ -1397,53 +1404,6 @@ __global__ void k_bt_write_dev(int EP, const double* __restrict__ sta_out, const
             hidx[h] = h;
             --h;
         }
-    }
-}
-
-// k_bt_count_dev / k_bt_write_dev walking the L-space predecessors (pins translated on output).
-__global__ void k_bt_count_L(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
-                             const int* __restrict__ ep, const int* __restrict__ L_of, const int* __restrict__ L_pred,
-                             const uint8_t* __restrict__ L_flags, int* __restrict__ len, int* __restrict__ hops)
-{
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= EP) return;
-    const int n_paths = refresh_active(sta_out, ctrl) ? static_cast<int>(sta_out[2]) : 0;
-    if (i >= n_paths) {
-        len[i] = 0, hops[i] = 0;
-        return;
-    }
-    int v = L_of[ep[i]], l = 1, h = 0;
-    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) ++l, h += (L_flags[u] & 4) != 0;
-    len[i] = l, hops[i] = h;
-}
-
-__global__ void k_bt_write_L(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
-                             const int* __restrict__ ep, const int* __restrict__ L_of, const int* __restrict__ L_pin,
-                             const int* __restrict__ L_pred, const uint8_t* __restrict__ L_flags,
-                             const int* __restrict__ len, const int* __restrict__ off, const int* __restrict__ hops,
-                             const int* __restrict__ hoff, const double* __restrict__ L_arr, double clock,
-                             int* __restrict__ pins, double* __restrict__ pslack, unsigned* __restrict__ hkey,
-                             double* __restrict__ hslack, int* __restrict__ hidx)
-{
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= EP || len[i] == 0) return;
-    const int e = ep[i];
-    int v = L_of[e];
-    const double sl = clock - L_arr[v]; // paths.cpp:123
-    pslack[i] = sl;
-    int k = off[i] + len[i] - 1, h = hoff[i] + hops[i] - 1;
-    pins[k] = e;
-    int vp = e; // pin id of v
-    for (int u = L_pred[v]; u >= 0; v = u, u = L_pred[v]) {
-        const int up = L_pin[u];
-        pins[--k] = up;
-        if (L_flags[u] & 4) {
-            hkey[h] = sl < 0.0 ? static_cast<unsigned>(vp) : 0xFFFFFFFFu; // pin_pairs.cpp:11
-            hslack[h] = sl;
-            hidx[h] = h;
-            --h;
-        }
-        vp = up;
     }
 }
 
@@ -1536,6 +1496,7 @@ void refresh_reserve(tdpg_session* s)
     s->sort_k0.reserve(EP), s->sort_k1.reserve(EP), s->sort_v0.reserve(EP), s->sort_v1.reserve(EP);
     s->ex_len.reserve(EP), s->ex_hops.reserve(EP), s->ex_off.reserve(EP), s->ex_hoff.reserve(EP);
     s->ex_slack.reserve(EP), s->ex_pins.reserve(EP * L + 1);
+    s->ex_tmp_pins.reserve(EP * (L + 1)), s->ex_tmp_keys.reserve(EP * (L / 2 + 2)); // (k_bt_walk slots)
     s->eh_key.reserve(H), s->eh_key_s.reserve(H), s->eh_idx.reserve(H), s->eh_idx_s.reserve(H);
     s->eh_slack.reserve(H);
     s->ex_counts.reserve(4), s->q_count.reserve(2), s->sta_out.reserve(4);
@@ -1565,10 +1526,12 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     size_t bytes = s->cub_tmp.n;
     CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP,
                                        0, 64, s->st));
-    if (lonly) {
+    const int S = s->L + 1, SH = s->L / 2 + 2; // (k_bt_walk's slot strides)
+    if (lonly) { // one backtrace pass into fixed-stride slots, packed after the scans (k_bt_compact)
         k_resolve_ties_L<<<1, kBlock, 0, s->st>>>(make_largs(s), s->d_level, s->L, s->tie_scratch, s->L + 2);
-        k_bt_count_L<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->L_of,
-                                                                   s->L_pred, s->L_flags, s->ex_len, s->ex_hops);
+        k_bt_walk<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(
+            EP, s->sort_v1, s->sta_out, 0, s->L_of, s->L_pin, s->L_pred, s->L_flags, s->pin_dir, s->L_arr, s->clock,
+            S, SH, s->ex_tmp_pins, s->ex_tmp_keys, s->ex_len, s->ex_hops, s->ex_slack, nullptr, nullptr, ctrl);
     } else {
         k_resolve_ties<<<1, kBlock, 0, s->st>>>(sta_args(s), s->d_level, s->L, s->tie_scratch, s->L + 2);
         k_bt_count_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred,
@@ -1583,11 +1546,9 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     k_fill_u32<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 8), kBlock, 0, s->st>>>(H, s->eh_key, 0xFFFFFFFFu);
     CK_LAUNCH();
     if (lonly)
-        k_bt_write_L<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->L_of, s->L_pin,
-                                                                   s->L_pred, s->L_flags, s->ex_len, s->ex_off,
-                                                                   s->ex_hops, s->ex_hoff, s->L_arr, s->clock,
-                                                                   s->ex_pins, s->ex_slack, s->eh_key, s->eh_slack,
-                                                                   s->eh_idx);
+        k_bt_compact<<<blocks_for(static_cast<long long>(EP) * S, kBlock), kBlock, 0, s->st>>>(
+            EP, S, SH, s->ex_tmp_pins, s->ex_tmp_keys, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff, s->ex_slack,
+            s->ex_pins, nullptr, s->eh_slack, s->eh_idx, s->eh_key);
     else
         k_bt_write_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred,
                                                                      s->pin_dir, s->ex_len, s->ex_off, s->ex_hops,
