@@ -106,6 +106,7 @@ struct tdpg_session {
     double clock = 0, r_unit = 0, c_unit = 0, core[4] = {0, 0, 0, 0};
     cudaStream_t st = nullptr;
     cudaStream_t st_req = nullptr;                    // the STA's required-time sweep (beside arrival)
+    cudaStream_t st_cond = nullptr;                   // captures conditional-node bodies (size-class sorts)
     cudaEvent_t ev_sta_fork = nullptr, ev_sta_join = nullptr;
     int device = 0;
 

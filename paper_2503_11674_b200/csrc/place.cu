@@ -608,8 +608,10 @@ Ctrl read_ctrl(tdpg_session* s)
     return c;
 }
 
-__global__ void k_count_heads32(long long n, const unsigned* __restrict__ k, unsigned long long* __restrict__ out)
+__global__ void k_count_heads32(long long cap, const long long* __restrict__ n_hits, const unsigned* __restrict__ k,
+                                unsigned long long* __restrict__ out)
 {
+    const long long n = min(cap, *n_hits); // (the refresh sorts only the first size class >= the hit count)
     int c = 0;
     for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * kBlock)
@@ -719,8 +721,8 @@ void timing_refresh(tdpg_session* s)
     CK(cudaEventRecord(ev.second, s->st));
     E.refresh_ev.push_back(ev);
     // our kernels: pin_xy, 2 per level, slack keys, sta final, begin, ties, bt count, fill, bt write,
-    // counts, ledger (+ net weights)
-    E.kernel_launches += 2LL * s->L + 10 + (E.cfg.net_weighting ? 1 : 0);
+    // counts, size-class pick, ledger (+ net weights)
+    E.kernel_launches += 2LL * s->L + 11 + (E.cfg.net_weighting ? 1 : 0);
     ++E.refreshes;
     if (s->round_cb) { // TimingRoundObserver (placer.cpp:434): this round's annotation and report
         sta_materialize_pins(s); // the observer may read per-pin timing
@@ -730,7 +732,7 @@ void timing_refresh(tdpg_session* s)
         CK(cudaMemcpyAsync(c, s->ex_counts.p, sizeof c, cudaMemcpyDeviceToHost, s->st));
         unsigned long long* u = E.obs_count;
         CK(cudaMemsetAsync(u, 0, sizeof *u, s->st));
-        k_count_heads32<<<148 * 4, kBlock, 0, s->st>>>(s->hcap, s->eh_key_s, u);
+        k_count_heads32<<<148 * 4, kBlock, 0, s->st>>>(s->hcap, s->ex_counts.p + 2, s->eh_key_s, u);
         CK_LAUNCH();
         unsigned long long uq = 0;
         CK(cudaMemcpyAsync(&uq, u, sizeof uq, cudaMemcpyDeviceToHost, s->st));
@@ -835,6 +837,7 @@ tdpg_session::~tdpg_session()
     if (sta_gexec_L) cudaGraphExecDestroy(sta_gexec_L);
     if (ex_gexec) cudaGraphExecDestroy(ex_gexec);
     if (st_req) cudaStreamSynchronize(st_req), cudaStreamDestroy(st_req);
+    if (st_cond) cudaStreamDestroy(st_cond);
     if (ev_sta_fork) cudaEventDestroy(ev_sta_fork);
     if (ev_sta_join) cudaEventDestroy(ev_sta_join);
     if (st) {

@@ -419,6 +419,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     CK(cudaGetDevice(&s->device));
     CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&s->st_req, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->st_cond, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&s->ev_sta_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&s->ev_sta_join, cudaEventDisableTiming));
     s->C = d->n_cells, s->P = d->n_pins, s->N = d->n_nets, s->S = d->n_sources, s->EP = d->n_endpoints;

@@ -1416,15 +1416,17 @@ __global__ void k_fill_u32(long long n, unsigned* p, unsigned v)
 
 // update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin;
 // the head of each group applies the group's additions in hit order.
-__global__ void k_ledger_dense(long long H, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
-                               const unsigned* __restrict__ hk, const int* __restrict__ hidx,
-                               const double* __restrict__ hslack, double w0, double w1, double* __restrict__ dl_w,
-                               double* __restrict__ ppw_e, const int* __restrict__ pin_entry,
+__global__ void k_ledger_dense(long long cap, const long long* __restrict__ n_hits, const double* __restrict__ sta_out,
+                               const Ctrl* __restrict__ ctrl, const unsigned* __restrict__ hk,
+                               const int* __restrict__ hidx, const double* __restrict__ hslack, double w0, double w1,
+                               double* __restrict__ dl_w, double* __restrict__ ppw_e, const int* __restrict__ pin_entry,
                                const int* __restrict__ pin_loc, uint32_t* __restrict__ pp_mask,
                                unsigned long long* __restrict__ q_count)
 {
     const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= H || !refresh_active(sta_out, ctrl)) return;
+    if (i >= cap || !refresh_active(sta_out, ctrl)) return;
+    const long long H = *n_hits; // (only the hits are sorted; the tail past them is stale)
+    if (i >= H) return;
     const unsigned key = hk[i];
     if (key == 0xFFFFFFFFu || (i > 0 && hk[i - 1] == key)) return;
     const double wns = sta_out[1];
@@ -1513,6 +1515,62 @@ void refresh_reserve(tdpg_session* s)
     if (s->N) s->net_w.reserve(s->N);
 }
 
+// Size classes for a stream-ordered count known only on the device (cap/64, cap/16, cap/4, cap).
+struct SizeClasses {
+    long long c[4];
+    int k;
+};
+
+__global__ void k_pick_class(const long long* __restrict__ n, SizeClasses sc, cudaGraphConditionalHandle h)
+{
+    const long long v = *n;
+    unsigned k = static_cast<unsigned>(sc.k); // (no body when there is nothing to process)
+    if (v > 0)
+        for (k = 0; k + 1 < static_cast<unsigned>(sc.k) && v > sc.c[k]; ++k) {}
+    cudaGraphSetConditional(h, k);
+}
+
+// Record body(stream, n) for the smallest size class n >= *d_n: under stream capture one SWITCH
+// conditional node whose bodies are the size classes, selected on the device by k_pick_class (the
+// graph stays host-sync-free); eagerly, body runs over the full capacity.
+template <typename F>
+void switch_by_count(tdpg_session* s, const long long* d_n, long long cap, F&& body)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s->st, &cs));
+    if (cs != cudaStreamCaptureStatusActive || cap < 64) {
+        body(s->st, cap);
+        return;
+    }
+    SizeClasses sc{};
+    for (const long long c : {cap >> 6, cap >> 4, cap >> 2, cap})
+        if (c > 0 && (sc.k == 0 || c > sc.c[sc.k - 1])) sc.c[sc.k++] = c;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s->st, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphConditionalHandle h{};
+    CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+    k_pick_class<<<1, 1, 0, s->st>>>(d_n, sc, h);
+    CK_LAUNCH();
+    CK(cudaStreamGetCaptureInfo(s->st, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeSwitch;
+    p.conditional.size = static_cast<unsigned>(sc.k);
+    cudaGraphNode_t node = nullptr;
+    CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+    for (int k = 0; k < sc.k; ++k) {
+        CK(cudaStreamBeginCaptureToGraph(s->st_cond, p.conditional.phGraph_out[k], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+        body(s->st_cond, sc.c[k]);
+        cudaGraph_t out = nullptr;
+        CK(cudaStreamEndCapture(s->st_cond, &out));
+    }
+    CK(cudaStreamUpdateCaptureDependencies(s->st, &node, 1, cudaStreamSetCaptureDependencies));
+}
+
 // The whole refresh, stream-ordered and host-sync-free (captured by the engine).
 void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting)
 {
@@ -1558,10 +1616,14 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     k_extract_counts<<<1, 1, 0, s->st>>>(EP, s->sta_out, ctrl, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff,
                                          s->ex_counts);
     CK_LAUNCH();
-    bytes = s->cub_tmp.n;
-    CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->eh_key.p, s->eh_key_s.p, s->eh_idx.p, s->eh_idx_s.p,
-                                       static_cast<int>(H), 0, bits_for(s->P), s->st));
-    k_ledger_dense<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(H, s->sta_out, ctrl, s->eh_key_s, s->eh_idx_s,
+    // the hits are packed at the front (k_extract_counts' total); sort the smallest size class that holds them
+    const int kbits = bits_for(s->P);
+    switch_by_count(s, s->ex_counts.p + 2, H, [&](cudaStream_t st, long long n) {
+        size_t b = s->cub_tmp.n;
+        CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, b, s->eh_key.p, s->eh_key_s.p, s->eh_idx.p, s->eh_idx_s.p,
+                                           static_cast<int>(n), 0, kbits, st));
+    });
+    k_ledger_dense<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(H, s->ex_counts.p + 2, s->sta_out, ctrl, s->eh_key_s, s->eh_idx_s,
                                                                 s->eh_slack, w0, w1, s->dl_w, s->ppw_e, s->pin_entry,
                                                                 s->pin_loc, s->pp_mask, s->q_count);
     CK_LAUNCH();
