@@ -823,21 +823,27 @@ __global__ void k_bt_compact(int ub, int S, int SH, const int* __restrict__ pins
                              const int* __restrict__ off, const int* __restrict__ hops, const int* __restrict__ hoff,
                              const double* __restrict__ pslack, int* __restrict__ out_pins,
                              unsigned long long* __restrict__ hkey, double* __restrict__ hslack,
-                             int* __restrict__ hidx, unsigned* __restrict__ hkey32 = nullptr)
+                             int* __restrict__ hidx, unsigned* __restrict__ hkey32 = nullptr,
+                             const long long* __restrict__ n_dev = nullptr)
 {
-    const long long t = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (t >= static_cast<long long>(ub) * S) return;
-    const int i = static_cast<int>(t / S), j = static_cast<int>(t - static_cast<long long>(i) * S);
-    const int l = len[i];
-    if (j < l) out_pins[off[i] + j] = pins[static_cast<long long>(i) * S + S - l + j];
-    const int nh = hops[i];
-    if (j < nh) {
-        const int h = hoff[i] + j;
-        const unsigned long long key = keys[static_cast<long long>(i) * SH + SH - nh + j];
-        if (hkey32) hkey32[h] = static_cast<unsigned>(key);
-        else hkey[h] = key;
-        hslack[h] = pslack[i];
-        hidx[h] = h;
+    // n_dev (the refresh): the selected paths are the first *n_dev sorted endpoints; a fixed grid
+    // strides over their slots only
+    const long long n = n_dev ? min(static_cast<long long>(ub), *n_dev) : ub;
+    const long long end = n * S;
+    for (long long t = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; t < end;
+         t += static_cast<long long>(gridDim.x) * kBlock) {
+        const int i = static_cast<int>(t / S), j = static_cast<int>(t - static_cast<long long>(i) * S);
+        const int l = len[i];
+        if (j < l) out_pins[off[i] + j] = pins[static_cast<long long>(i) * S + S - l + j];
+        const int nh = hops[i];
+        if (j < nh) {
+            const int h = hoff[i] + j;
+            const unsigned long long key = keys[static_cast<long long>(i) * SH + SH - nh + j];
+            if (hkey32) hkey32[h] = static_cast<unsigned>(key);
+            else hkey[h] = key;
+            hslack[h] = pslack[i];
+            hidx[h] = h;
+        }
     }
 }
 
@@ -1414,6 +1420,16 @@ __global__ void k_fill_u32(long long n, unsigned* p, unsigned v)
         p[i] = v;
 }
 
+// The pad past the packed hits up to the largest size class switch_by_count can pick for them:
+// the smallest class >= nh is at most max(cap/64, 4 nh).
+__global__ void k_fill_hit_pad(long long cap, const long long* __restrict__ n_hits, unsigned* p)
+{
+    const long long nh = min(cap, *n_hits), end = min(cap, max(cap >> 6, 4 * nh));
+    for (long long i = nh + blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < end;
+         i += static_cast<long long>(gridDim.x) * kBlock)
+        p[i] = 0xFFFFFFFFu;
+}
+
 // update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin;
 // the head of each group applies the group's additions in hit order.
 __global__ void k_ledger_dense(long long cap, const long long* __restrict__ n_hits, const double* __restrict__ sta_out,
@@ -1533,15 +1549,21 @@ __global__ void k_pick_class(const long long* __restrict__ n, SizeClasses sc, cu
 // Record body(stream, n) for the smallest size class n >= *d_n: under stream capture one SWITCH
 // conditional node whose bodies are the size classes, selected on the device by k_pick_class (the
 // graph stays host-sync-free); eagerly, body runs over the full capacity.
-template <typename F>
-void switch_by_count(tdpg_session* s, const long long* d_n, long long cap, F&& body)
+static bool size_classes_apply(tdpg_session* s, long long cap)
 {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(s->st, &cs));
-    if (cs != cudaStreamCaptureStatusActive || cap < 64) {
+    return cs == cudaStreamCaptureStatusActive && cap >= 64;
+}
+
+template <typename F>
+void switch_by_count(tdpg_session* s, const long long* d_n, long long cap, F&& body)
+{
+    if (!size_classes_apply(s, cap)) {
         body(s->st, cap);
         return;
     }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     SizeClasses sc{};
     for (const long long c : {cap >> 6, cap >> 4, cap >> 2, cap})
         if (c > 0 && (sc.k == 0 || c > sc.c[sc.k - 1])) sc.c[sc.k++] = c;
@@ -1600,21 +1622,27 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_len.p, s->ex_off.p, EP, s->st));
     bytes = s->cub_tmp.n;
     CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, bytes, s->ex_hops.p, s->ex_hoff.p, EP, s->st));
+    k_extract_counts<<<1, 1, 0, s->st>>>(EP, s->sta_out, ctrl, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff,
+                                         s->ex_counts);
+    CK_LAUNCH();
     const long long H = s->hcap;
-    k_fill_u32<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 8), kBlock, 0, s->st>>>(H, s->eh_key, 0xFFFFFFFFu);
+    if (!size_classes_apply(s, H)) // (switch_by_count sorts the full capacity then)
+        k_fill_u32<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 8), kBlock, 0, s->st>>>(H, s->eh_key,
+                                                                                             0xFFFFFFFFu);
+    else
+        k_fill_hit_pad<<<std::min<unsigned>(blocks_for(H, kBlock), 148 * 8), kBlock, 0, s->st>>>(
+            H, s->ex_counts.p + 2, s->eh_key);
     CK_LAUNCH();
     if (lonly)
-        k_bt_compact<<<blocks_for(static_cast<long long>(EP) * S, kBlock), kBlock, 0, s->st>>>(
-            EP, S, SH, s->ex_tmp_pins, s->ex_tmp_keys, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff, s->ex_slack,
-            s->ex_pins, nullptr, s->eh_slack, s->eh_idx, s->eh_key);
+        k_bt_compact<<<std::min<unsigned>(blocks_for(static_cast<long long>(EP) * S, kBlock), 148 * 8), kBlock, 0,
+                       s->st>>>(EP, S, SH, s->ex_tmp_pins, s->ex_tmp_keys, s->ex_len, s->ex_off, s->ex_hops,
+                                s->ex_hoff, s->ex_slack, s->ex_pins, nullptr, s->eh_slack, s->eh_idx, s->eh_key,
+                                s->ex_counts.p);
     else
         k_bt_write_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, s->pred,
                                                                      s->pin_dir, s->ex_len, s->ex_off, s->ex_hops,
                                                                      s->ex_hoff, s->arr, s->clock, s->ex_pins,
                                                                      s->ex_slack, s->eh_key, s->eh_slack, s->eh_idx);
-    CK_LAUNCH();
-    k_extract_counts<<<1, 1, 0, s->st>>>(EP, s->sta_out, ctrl, s->ex_len, s->ex_off, s->ex_hops, s->ex_hoff,
-                                         s->ex_counts);
     CK_LAUNCH();
     // the hits are packed at the front (k_extract_counts' total); sort the smallest size class that holds them
     const int kbits = bits_for(s->P);
