@@ -225,6 +225,10 @@ struct tdpg_session {
     // sort / scan scratch
     tdpg::DBuf<unsigned char> cub_tmp;
     tdpg::DBuf<unsigned long long> sort_k0, sort_k1;
+    tdpg::DBuf<unsigned long long> ep_kc;             // the refresh's violated endpoints, compacted
+    tdpg::DBuf<int> ep_vc;
+    tdpg::DBuf<uint8_t> ep_flag;
+    tdpg::DBuf<long long> ep_nv;                     // [0] violated count, [1..2] compaction counts
     tdpg::DBuf<int> sort_v0, sort_v1;
     tdpg::HBuf<long long> h_small;
     // initial jitter (place.cu): per-cell jitter flag / rank, the raw mt19937_64 stream, explicit flags

@@ -1526,9 +1526,34 @@ void refresh_reserve(tdpg_session* s)
     cub::DeviceScan::ExclusiveSum(nullptr, b2, s->ex_len.p, s->ex_off.p, static_cast<int>(EP), s->st);
     cub::DeviceRadixSort::SortPairs(nullptr, b3, s->eh_key.p, s->eh_key_s.p, s->eh_idx.p, s->eh_idx_s.p,
                                     static_cast<int>(H), 0, 32, s->st);
-    cub_scratch(s, std::max({b1, b2, b3}));
+    s->ep_kc.reserve(EP), s->ep_vc.reserve(EP), s->ep_flag.reserve(EP), s->ep_nv.reserve(4);
+    size_t b4 = 0, b5 = 0;
+    cub::DeviceSelect::Flagged(nullptr, b4, s->sort_k0.p, s->ep_flag.p, s->ep_kc.p, s->ep_nv.p + 1,
+                               static_cast<int>(EP), s->st);
+    cub::DeviceSelect::Flagged(nullptr, b5, s->sort_v0.p, s->ep_flag.p, s->ep_vc.p, s->ep_nv.p + 2,
+                               static_cast<int>(EP), s->st);
+    cub_scratch(s, std::max({b1, b2, b3, b4, b5}));
     s->tie_scratch.reserve(static_cast<size_t>(kBlock) * 2 * (s->L + 2));
     if (s->N) s->net_w.reserve(s->N);
+}
+
+__global__ void k_ep_violated(const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                              long long* __restrict__ nv)
+{
+    nv[0] = refresh_active(sta_out, ctrl) ? static_cast<long long>(sta_out[2]) : 0;
+}
+
+__global__ void k_flag_keys(int n, const unsigned long long* __restrict__ keys, uint8_t* __restrict__ flag)
+{
+    for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) flag[i] = keys[i] != kNoKey;
+}
+
+// kNoKey past the compacted violated keys, up to the size class being sorted
+__global__ void k_pad_keys(long long n, const long long* __restrict__ nv, unsigned long long* __restrict__ keys)
+{
+    for (long long i = nv[1] + blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * kBlock)
+        keys[i] = kNoKey;
 }
 
 // Size classes for a stream-ordered count known only on the device (cap/64, cap/16, cap/4, cap).
@@ -1603,9 +1628,30 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
     CK_LAUNCH();
     const int EP = s->EP;
     if (EP == 0) return;
-    size_t bytes = s->cub_tmp.n;
-    CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, EP,
-                                       0, 64, s->st));
+    // the walk reads only the first (violated-count) sorted endpoints: when few fail, compact them
+    // stably and sort the smallest size class holding them; else sort every endpoint
+    k_ep_violated<<<1, 1, 0, s->st>>>(s->sta_out, ctrl, s->ep_nv);
+    CK_LAUNCH();
+    switch_by_count(s, s->ep_nv.p, EP, [&](cudaStream_t st, long long n) {
+        size_t b = s->cub_tmp.n;
+        if (n >= EP) {
+            CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, b, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p,
+                                               s->sort_v1.p, EP, 0, 64, st));
+            return;
+        }
+        k_flag_keys<<<std::min<unsigned>(blocks_for(EP, kBlock), 148 * 4), kBlock, 0, st>>>(EP, s->sort_k0, s->ep_flag);
+        CK_LAUNCH();
+        CK(cub::DeviceSelect::Flagged(s->cub_tmp.p, b, s->sort_k0.p, s->ep_flag.p, s->ep_kc.p, s->ep_nv.p + 1, EP, st));
+        b = s->cub_tmp.n;
+        CK(cub::DeviceSelect::Flagged(s->cub_tmp.p, b, s->sort_v0.p, s->ep_flag.p, s->ep_vc.p, s->ep_nv.p + 2, EP, st));
+        k_pad_keys<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(n, kBlock), 148 * 4)), kBlock, 0, st>>>(
+            n, s->ep_nv, s->ep_kc);
+        CK_LAUNCH();
+        b = s->cub_tmp.n;
+        CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, b, s->ep_kc.p, s->sort_k1.p, s->ep_vc.p, s->sort_v1.p,
+                                           static_cast<int>(n), 0, 64, st));
+    });
+    size_t bytes = 0;
     const int S = s->L + 1, SH = s->L / 2 + 2; // (k_bt_walk's slot strides)
     if (lonly) { // one backtrace pass into fixed-stride slots, packed after the scans (k_bt_compact)
         k_resolve_ties_L<<<1, kBlock, 0, s->st>>>(make_largs(s), s->d_level, s->L, s->tie_scratch, s->L + 2);
