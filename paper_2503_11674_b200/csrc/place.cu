@@ -721,8 +721,8 @@ void timing_refresh(tdpg_session* s)
     CK(cudaEventRecord(ev.second, s->st));
     E.refresh_ev.push_back(ev);
     // our kernels: pin_xy, 2 per level, slack keys, sta final, begin, ties, bt count, fill, bt write,
-    // counts, size-class pick, ledger (+ net weights)
-    E.kernel_launches += 2LL * s->L + 11 + (E.cfg.net_weighting ? 1 : 0);
+    // counts, violated count + two size-class picks, ledger (+ net weights)
+    E.kernel_launches += 2LL * s->L + 13 + (E.cfg.net_weighting ? 1 : 0);
     ++E.refreshes;
     if (s->round_cb) { // TimingRoundObserver (placer.cpp:434): this round's annotation and report
         sta_materialize_pins(s); // the observer may read per-pin timing
