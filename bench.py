@@ -45,10 +45,10 @@ def parse():
     ap.add_argument("--fail-frac", type=float, default=0.8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-evals", type=int, default=2)
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "partition"],
+    ap.add_argument("--mode", default=None, choices=["replicas", "partition"],
                     help="N > 1: independent designs per GPU (weak scaling) or one design with nets partitioned "
                          "across GPUs and the cell gradient all-reduced by NCCL inside the iteration graph "
-                         "(strong scaling, SURVEY §8e)")
+                         "(strong scaling, SURVEY §8e); default: partition when N > 1")
     return ap.parse_args()
 
 
@@ -106,8 +106,43 @@ class Clocks:
 
 
 def bench_config(args, iters):
-    return {"grid_nx": args.grid, "grid_ny": args.grid, "m": args.m, "timing_start_iter": 0, "max_iters": iters,
-            "seed": 1}
+    """The run_placement config of the timed workload (both arms).  Timing engages at the first timed
+    iteration (timing_start_iter = W), so whatever --steps / --warmup are, the timed window opens with a
+    timing refresh and holds one every m iterations."""
+    return {"grid_nx": args.grid, "grid_ny": args.grid, "m": args.m, "timing_start_iter": args.warmup,
+            "max_iters": iters, "seed": 1}
+
+
+def lround(x):
+    return int(np.floor(x + 0.5)) if x >= 0 else -int(np.floor(-x + 0.5))
+
+
+def calibrate_clock(arr_ep, fail_frac):
+    """generate_synthetic's clock rule (generator.cpp:249-260) applied at the run's start snapshot:
+    the period at the (1 - fail_frac) quantile of the sorted endpoint arrivals."""
+    a = np.sort(np.asarray(arr_ep, np.float64))
+    n = a.size
+    n_pass = min(max(lround((1.0 - fail_frac) * n), 0), n)
+    if n_pass == 0:
+        return max(a[0] * 0.95, 1e-9)
+    if n_pass == n:
+        return a[-1] * 1.05
+    return 0.5 * (a[n_pass - 1] + a[n_pass])
+
+
+def workload_config(args, d, world):
+    """The `config` object both arms print (identical by construction)."""
+    return {"workload": f"configs[2]: synthetic {d.n_cells}-cell / {d.n_nets}-net netlist (generator spec "
+                        f"{args.cells}, seed 1), run_placement from its seeded jittered start (placer.cpp:375-382), "
+                        f"clock calibrated there so {args.fail_frac:g} of the endpoints fail (generator.cpp:249-260); "
+                        f"full timing-driven GP iteration (WA + pin-pair attraction + bin density + Adam), grid "
+                        f"{args.grid}^2; timing engages at the first timed iteration and refreshes every {args.m} "
+                        f"(STA + endpoint extraction of every violated endpoint + ledger update) inside the timed region",
+            "cells": d.n_cells, "pins": d.n_pins, "nets": d.n_nets, "net_pins": d.n_net_pins,
+            "endpoints": int(d.endpoints.size), "grid": args.grid, "m": args.m, "timing_start_iter": args.warmup,
+            "fail_frac": args.fail_frac, "clock_period": float(d.clock_period),
+            "l2": "working set per iteration > L2 (positions+netlist+gradients+grid ~ 2x 126 MB)",
+            "parallelism": "single GPU" if world == 1 else f"{world} GPUs"}
 
 
 def peaks():
@@ -122,8 +157,9 @@ def kernel_bytes(d, grid, E_tot):
     C, P, N, E = d.n_cells, d.n_pins, d.n_nets, d.n_net_pins
     B = grid * grid
     return {
-        # net CSR + entry record (cell id, offset) + cell positions once + per-entry gradient write
-        "wirelength": 4 * (N + 1) + E * (4 + 16) + 16 * C + 16 * E,
+        # WA + the fused pin pairs (3 size-class kernels): net CSR + entry record (cell id, offset) + cell
+        # positions once + per-entry gradient write
+        "wirelength_pp": 4 * (N + 1) + E * (4 + 16) + 16 * C + 16 * E,
         # positions + sizes + fixed flags once, grid accumulators written once
         "density_scatter": C * (16 + 16 + 1) + 8 * B,
         # accumulators read + reset, excess written
@@ -158,11 +194,36 @@ def iteration_bytes(d, grid, Q=0):
     return 2 * C * p + 2 * C * p + E * (4 + 2 * p) + 4 * (N + 1) + 4 * E + Q * (8 + p) + 2 * C * p + 2 * B * p + 2 * C * p * 7
 
 
-def make_design(args, rank):
-    from paper_2503_11674_b200.engine import generate
+def make_design(args, seed=1):
+    """The timed workload's design, built by the product: the generator's netlist, the run's jittered start
+    (on the device, bitwise the reference's mt19937_64 draws) made explicit, the clock calibrated at that
+    start with a device STA (bit-exact).  Returns (design, seconds)."""
+    from paper_2503_11674_b200.engine import Session, generate
     t0 = time.time()
-    d = generate(seed=1 + rank, cells=args.cells, fail_frac=args.fail_frac, calibrate=True)
+    d = generate(seed=seed, cells=args.cells, fail_frac=args.fail_frac, calibrate=False)
+    s = Session(d)
+    s.engine_init(bench_config(args, 1))
+    xy0 = s.positions()
+    arr = s.sta(xy0)["arr"]
+    s.close()
+    d.positions = xy0
+    d.pos_explicit = np.ones(d.n_cells, np.uint8)
+    d.clock_period = calibrate_clock(arr[d.endpoints], args.fail_frac)
     return d, time.time() - t0
+
+
+def make_design_reference(args, seed=1):
+    """The same design built without the product library: the oracle's generator restatement
+    (tdp_oracle_gen.c, netlist-identical to the reference's and to the product's), its jitter
+    restatement (placer.cpp:375-382) and the reference's own run_sta for the clock."""
+    from oracle.oracle import Oracle, RefOracle
+    d = Oracle.generate(seed=seed, cells=args.cells, fail_frac=args.fail_frac)
+    xy0 = Oracle(d).jitter(bench_config(args, 1))
+    arr = RefOracle(d).sta(xy0, threads=os.cpu_count() or 1)["arr"]
+    d.positions = xy0
+    d.pos_explicit = np.ones(d.n_cells, np.uint8)
+    d.clock_period = calibrate_clock(arr[d.endpoints], args.fail_frac)
+    return d
 
 
 def extraction_sweep(d, ns=(1000, 3000, 10000, 30000, 100000)):
@@ -226,59 +287,77 @@ def cpu_baseline(d, args, xy_snapshot):
         r = o.extract(xy_snapshot, n=10000, threads=1)
         ex = {"sta_ms": round(r["sta_ms"], 1), "extract_top10k_ms": round(r["extract_ms"], 1)}
     return {"value": round(1.0 / res[best_th], 4), "unit": "iters/s", "cores": best_th, "kind": kind,
+            "cpu_model": lscpu_model(), "nproc": nproc,
             "sample": f"objective_and_gradient on the {d.n_cells}-cell design, grid {args.grid}^2, "
                       f"{args.cpu_sample_evals} evals per thread count, best of threads {sorted(res)} "
                       f"(s/eval: {', '.join(f'{k}T {v:.2f}' for k, v in res.items())}); Adam + refresh excluded",
             "threads_tried": {str(k): round(v, 3) for k, v in res.items()}, "setup_s": round(setup_s, 1), **ex}
 
 
+def lscpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation (its sources compiled by oracle/Makefile
+    into oracle/_ref/libtdpref.so) on the same workload and schedule.  The design comes from the oracle's
+    restatements, so this process never maps a product library.  Objective and STA use every host
+    thread, extraction one (the enumerator memoises prefixes only single-threaded)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle.oracle import Oracle, RefOracle
-    from paper_2503_11674_b200.engine import generate
-    kind = "reference" if RefOracle.available() else "port"
-    try:
-        d = generate(seed=1, cells=args.cells, fail_frac=args.fail_frac, calibrate=False)
-    except Exception:
-        # no GPU for the generator's calibration is fine: the netlist is host-built
-        raise
-    d.clock_period = 1.0
-    o = (RefOracle if kind == "reference" else Oracle)(d)
+    from oracle.oracle import RefOracle
+    if not RefOracle.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtdpref.so was not built"}), flush=True)
+        return
     nproc = os.cpu_count() or 1
-    gamma = 0.01 * d.span
-    xy = d.positions.copy()
-    x = xy.reshape(-1).copy()
-    m = np.zeros_like(x)
-    v = np.zeros_like(x)
-    t = 0
-    times = []
-    total_steps = args.warmup + args.steps
-    for it in range(total_steps):
-        t1 = time.perf_counter()
-        if kind == "reference":
-            _, g = o.objective(x.reshape(-1, 2), args.grid, args.grid, 0.6, gamma, 1e-4, 2.5e-5, threads=nproc)
-        else:
-            _, g = o.objective(x.reshape(-1, 2), args.grid, args.grid, 0.6, gamma, 1e-4, 2.5e-5)
-        t = (RefOracle if kind == "reference" else Oracle).adam_step(x, g.reshape(-1), m, v, t,
-                                                                     0.01 * d.span * 0.999 ** it)
-        dt = time.perf_counter() - t1
-        if it >= args.warmup:
-            times.append(dt)
-    tot = sum(times)
-    val = len(times) / tot
+    t0 = time.time()
+    d = make_design_reference(args)
+    setup_s = time.time() - t0
+    r = RefOracle(d)
+    W, K = args.warmup, args.steps
+    res = r.place_bench(bench_config(args, W + K), threads_obj=nproc, threads_sta=nproc, threads_ex=1)
+    it_ms = res["iter_ms"][W:W + K]
+    if it_ms.size < K:
+        raise SystemExit(f"reference run stopped after {res['rows']} rows (stop_overflow)")
+    tot_s = float(np.sum(it_ms)) / 1000.0
+    val = K / tot_s
+    paths_timed = int(np.sum(res["paths"][W:W + K]))
+    rf = res["refresh_ms"][W:W + K]
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "iters/s",
-                      "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                      "ms_per_step": round(1000 * tot / len(times), 1), "higher_is_better": True,
-                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                      "config": {"workload": f"synthetic {args.cells}-spec-cell netlist ({d.n_cells} cells, "
-                                             f"{d.n_nets} nets), GP iteration (objective_and_gradient + Adam), "
-                                             f"grid {args.grid}^2", "cells": d.n_cells, "nets": d.n_nets},
-                      "cpu_baseline": {"value": round(val, 4), "unit": "iters/s", "cores": nproc, "kind": kind,
-                                       "sample": "every step one full-size GP iteration (timing refresh excluded)"},
+                      "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(1000 * tot_s / K, 2),
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic", "config": workload_config(args, d, world),
+                      "timed_window": {"refreshes": int(np.count_nonzero(rf)), "refresh_ms_each": round(
+                          float(np.sum(rf)) / max(1, np.count_nonzero(rf)), 1), "paths_extracted": paths_timed,
+                          "ledger_pairs_end": res["ledger_pairs"], "gp_iteration_ms": round(
+                              float(np.sum(it_ms) - np.sum(rf)) / K, 2)},
+                      "cpu_baseline": {"value": round(val, 4), "unit": "iters/s", "cores": nproc, "kind": "reference",
+                                       "cpu_model": lscpu_model(),
+                                       "sample": f"the whole workload: {W} warm-up + {K} timed iterations of the "
+                                                 f"reference's run_placement loop (ref_harness.cpp ref_place_bench: "
+                                                 f"objective_and_gradient + Adam every step, run_sta + "
+                                                 f"report_timing_endpoint + collect_pin_pairs + update_pair_weights "
+                                                 f"every {args.m}); objective/STA at {nproc} threads, extraction at 1"},
                       "e2e": {"value": round(val, 4), "unit": "iters/s", "h2d_bytes_per_step": 0,
-                              "d2h_bytes_per_step": 0}}), flush=True)
+                              "d2h_bytes_per_step": 0},
+                      "setup_s": round(setup_s, 1), "final": {"tns": res["tns"], "wns": res["wns"], "hpwl": res["hpwl"]}}),
+          flush=True)
+
+
+def traffic_for(d, grid, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of THIS configuration (cells and
+    grid), or None when no capture of it exists."""
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(tfile):
+        return None
+    return json.load(open(tfile)).get(f"{d.n_cells}x{grid}", {}).get(kernel)
 
 
 def run_ours(args):
@@ -287,14 +366,19 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # (NCCL's init lines name the ranks and the transport)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2503_11674_b200.engine import Session
 
-    partition = world > 1 and args.mode == "partition"
-    d, gen_s = make_design(args, 0 if partition else rank)  # partition: every rank holds the same design
-    total_iters = args.warmup + args.steps + 64
+    mode = args.mode or ("partition" if world > 1 else "replicas")
+    partition = world > 1 and mode == "partition"
+    d, gen_s = make_design(args, 1 if partition else 1 + rank)  # partition: every rank holds the same design
+    W, K = args.warmup, args.steps
+    total_iters = W + K + 64
     cfg = bench_config(args, total_iters)
+    t0 = time.time()
     s = Session(d)
+    create_s = time.time() - t0
     if partition:
         from paper_2503_11674_b200 import distributed as D
         D.init_partitioned(s, rank, world)
@@ -311,10 +395,10 @@ def run_ours(args):
     # the sampler runs from before the warm-up until after the timed region
     with Clocks(local) as clk:
         time.sleep(0.5)
-        s.iterate(args.warmup)
+        s.iterate(W)
         barrier()
         st0 = s.engine_stats()
-        dev_ms = s.iterate(args.steps)
+        dev_ms = s.iterate(K)
         st1 = s.engine_stats()
         barrier()
         time.sleep(0.3)
@@ -323,10 +407,14 @@ def run_ours(args):
         import torch.distributed as dist
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dev_ms_max = float(ms.item())
-    value = (1 if partition else world) * args.steps / (dev_ms_max / 1000.0)
+    value = (1 if partition else world) * K / (dev_ms_max / 1000.0)
     launches = st1["kernel_launches"] - st0["kernel_launches"]
     refreshes = st1["refreshes"] - st0["refreshes"]
     refresh_ms = st1["refresh_ms"] - st0["refresh_ms"]
+    paths_timed = st1["paths"] - st0["paths"]
+    if paths_timed <= 0:
+        raise SystemExit(f"bench: the timed window extracted no path ({refreshes} refreshes): the workload "
+                         "would not exercise the timing-driven path")
 
     # per-kernel profile of loop iterations (roofline of the dominant kernel); a partitioned engine
     # is profiled through its replica twin on rank 0 below
@@ -335,30 +423,44 @@ def run_ours(args):
     elif partition:
         s_prof = Session(d)
         s_prof.engine_init(cfg)
-        s_prof.iterate(args.warmup)
+        s_prof.iterate(W + K)
         prof = s_prof.profile_iteration(5)
     else:
         prof = s.profile_iteration(5)
 
     # e2e: the call a user makes — run_placement through the C-ABI (tdpg_place) on the same design and
-    # schedule, `steps` iterations with a timing refresh every m, from pinned host positions to pinned
-    # host positions + the per-iteration trace rows; wall clock over the whole call (device loop, its
-    # engine set-up, the final STA), max over ranks; one untimed warm-up call first.
+    # schedule (timing from the first iteration, a refresh every m), K iterations from pinned host
+    # positions to pinned host positions + the per-iteration trace rows; wall clock over the whole call
+    # (its engine set-up, device loop, final STA), max over ranks.  Warm: on the session above after one
+    # untimed call; cold: a fresh session (netlist upload + timing-graph levelization) + the call.
     C = d.n_cells
     hin = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
     hout = torch.empty(2 * C, dtype=torch.float64, pin_memory=True)
     hin.numpy()[:] = d.positions.reshape(-1)
-    e2e_cfg = bench_config(args, args.steps)
+    e2e_cfg = dict(bench_config(args, K), timing_start_iter=0)
+
+    def maxr(x):
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([x], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    cold_s, cold_rows = None, 0
+    if not partition:
+        barrier()
+        t0 = time.perf_counter()
+        s_cold = Session(d)
+        cold_rows, _ = s_cold.place_host(e2e_cfg, hin.data_ptr(), hout.data_ptr())
+        cold_s = time.perf_counter() - t0
+        s_cold.close()
+        cold_s = maxr(cold_s)
     s.place_host(e2e_cfg, hin.data_ptr(), hout.data_ptr())  # warm-up call (lazy module loads, first captures)
     barrier()
     t0 = time.perf_counter()
     e2e_rows, _ = s.place_host(e2e_cfg, hin.data_ptr(), hout.data_ptr())
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = maxr(time.perf_counter() - t0)
     e2e_val = (1 if partition else world) * e2e_rows / e2e_s
     sweep, xy_snap = (extraction_sweep(d) if rank == 0 else ({}, None))
 
@@ -371,17 +473,17 @@ def run_ours(args):
     dom_ms = prof[dom]
     achieved = kb[dom] / (dom_ms / 1000.0) / 1e9
     iter_ms = sum(prof.values())
-    # the scatter's real limiter: shared-memory atomics, one 32-bit lane-atomic per non-zero footprint entry
-    # (fixed-point low word) plus one when the entry needs the high word, counted on the device at the
+    # the scatter's limiter besides HBM: shared-memory atomics, one 32-bit lane-atomic per non-zero footprint
+    # entry (fixed-point low word) plus one when the entry needs the high word, counted on the device at the
     # profiled positions; peak = 4 SMSPs x 148 SMs x clock / 2 cycles per spread lane-atomic
-    # (B300_MICROARCH.md "ATOMS (spread-addr) 2 cyc/lane"; same SM design on B200)
+    # (B300_MICROARCH.md "ATOMS (spread-addr) 2 cyc/lane"; modelled, not measured on B200)
     n_ent = footprint_entries(d, s.positions(), args.grid)
     from paper_2503_11674_b200.design import CONFIG_DEFAULTS
     at_lo, at_hi = s.density_atomics(args.grid, args.grid, CONFIG_DEFAULTS["target_density"], xy=s.positions())
     clk_summary = clk.summary()
     sm_ghz = (clk_summary.get("sm_mhz") or 1965.0) / 1000.0
     atom_peak = 148 * 4 * sm_ghz * 1e9 / 2 / 1e9  # G lane-atomics/s
-    atom_ach = (at_lo + at_hi) / (prof.get("density_scatter", 1e9) / 1000.0) / 1e9
+    atom_ach = (at_lo + at_hi) / (prof.get("density_scatter", 1e9) / 1000.0) / 1e9 if "density_scatter" in prof else None
     ib = iteration_bytes(d, args.grid)
     cpu = None
     if not args.no_cpu_baseline:
@@ -389,48 +491,47 @@ def run_ours(args):
             cpu = cpu_baseline(d, args, xy_snap)
         except Exception as e:  # reported, never fatal
             cpu = {"error": str(e)[:200]}
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(dom)
+    gp_ms = (dev_ms_max - refresh_ms) / K
     out = {
-        "metric": METRIC, "value": round(value, 3), "unit": "iters/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4), "higher_is_better": True,
+        "metric": METRIC, "value": round(value, 3), "unit": "iters/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": round(dev_ms_max / K, 4), "higher_is_better": True,
         "scaling": "strong" if partition else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"configs[2]: synthetic {d.n_cells}-cell / {d.n_nets}-net netlist "
-                               f"(generator spec {args.cells}, fail_frac {args.fail_frac}), full timing-driven GP "
-                               f"iteration, grid {args.grid}^2, timing refresh every {args.m} iterations "
-                               f"(STA + endpoint extraction of all violated endpoints + ledger) inside the timed region",
-                   "cells": d.n_cells, "pins": d.n_pins, "nets": d.n_nets, "net_pins": d.n_net_pins,
-                   "endpoints": int(d.endpoints.size), "grid": args.grid, "m": args.m,
-                   "l2": "working set per iteration > L2 (positions+netlist+gradients+grid ~ 2x 126 MB)",
-                   "parallelism": ("nets partitioned, NCCL all-reduce of the cell gradient" if partition else
-                                   "replicas") if world > 1 else "single GPU", "refreshes_timed": refreshes,
-                   "refresh_ms_timed": round(refresh_ms, 3), "ledger_pairs_end": st1["ledger_pairs"]},
+        "config": workload_config(args, d, world),
+        "mode": ("nets partitioned, NCCL all-reduce of the cell gradient inside the iteration graph" if partition
+                 else "replicas") if world > 1 else "single GPU",
+        "timed_window": {"refreshes": refreshes, "refresh_ms_each": round(refresh_ms / max(refreshes, 1), 3),
+                         "paths_extracted": paths_timed, "path_pins_extracted": st1["path_pins"] - st0["path_pins"],
+                         "ledger_pairs_end": st1["ledger_pairs"], "gp_iteration_ms": round(gp_ms, 4)},
         "e2e": {"value": round(e2e_val, 3), "unit": "iters/s",
                 "h2d_bytes_per_step": round(16 * C / max(e2e_rows, 1), 1),
                 "d2h_bytes_per_step": round((16 * C + 88 * e2e_rows) / max(e2e_rows, 1), 1),
                 "steps": e2e_rows, "wall_s": round(e2e_s, 4),
+                "cold": None if cold_s is None else {
+                    "value": round(cold_rows / cold_s, 3), "wall_s": round(cold_s, 4),
+                    "what": "fresh session (netlist upload + timing-graph levelization) + the same tdpg_place call"},
                 "path": "tdpg_place (run_placement through the C-ABI): pinned positions in, device loop with "
-                        "timing refresh every m, positions + trace rows out"},
+                        "timing refresh every m from the first iteration, positions + trace rows out"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": pk.get("hbm_gbs"),
-                     "unit": "GB/s", "frac": round(achieved / pk.get("hbm_gbs", 6650.0), 4), "traffic": traffic,
-                     "algorithmic_bytes": kb[dom], "kernel_ms": round(dom_ms, 4),
+                     "unit": "GB/s", "frac": round(achieved / pk.get("hbm_gbs", 6650.0), 4),
+                     "traffic": traffic_for(d, args.grid, dom), "algorithmic_bytes": kb[dom],
+                     "kernel_ms": round(dom_ms, 4),
                      "peak_source": "measured" if "fallback" not in pk else "fallback",
-                     "limiter": {"kernel": "density_scatter", "bound": "smem_atomics", "unit": "G lane-atomics/s",
-                                 "achieved": round(atom_ach, 1), "peak": round(atom_peak, 1),
-                                 "frac": round(atom_ach / atom_peak, 3), "footprint_entries": n_ent, "lane_atomics": at_lo + at_hi,
-                                 "peak_source": "B300_MICROARCH.md ATOMS spread-addr 2 cyc/lane x 4 SMSP x 148 SM"}},
-        "iteration": {"gp_iteration_ms": round((dev_ms_max - refresh_ms) / args.steps, 4),
-                      "refresh_ms_each": round(refresh_ms / max(refreshes, 1), 3),
+                     "limiter": None if atom_ach is None else {
+                         "kernel": "density_scatter", "bound": "smem_atomics", "unit": "G lane-atomics/s",
+                         "achieved": round(atom_ach, 1), "peak": round(atom_peak, 1),
+                         "frac": round(atom_ach / atom_peak, 3), "footprint_entries": n_ent,
+                         "lane_atomics": at_lo + at_hi,
+                         "peak_source": "modelled: B300_MICROARCH.md ATOMS spread-addr 2 cyc/lane x 4 SMSP x 148 SM"}},
+        "iteration": {"gp_iteration_ms": round(gp_ms, 4),
                       "kernels_ms_serialised": {k: round(v, 4) for k, v in prof.items()}, "sum_ms": round(iter_ms, 4),
                       "bytes_iter_survey": ib,
-                      "frac_of_hbm": round(ib / (iter_ms / 1000.0) / 1e9 / pk.get("hbm_gbs", 6650.0), 4)},
+                      "frac_of_hbm_serialised": round(ib / (iter_ms / 1000.0) / 1e9 / pk.get("hbm_gbs", 6650.0), 4),
+                      "frac_of_hbm_graph": round(ib / (gp_ms / 1000.0) / 1e9 / pk.get("hbm_gbs", 6650.0), 4)},
         "extraction_sweep_ms": sweep,
         "clocks": clk_summary,
         "cpu_baseline": cpu,
-        "setup_s": {"generate_and_calibrate": round(gen_s, 2), "engine_init": round(init_s, 2)},
+        "setup_s": {"design": round(gen_s, 2), "session_create": round(create_s, 3), "engine_init": round(init_s, 3)},
     }
     print(json.dumps(out), flush=True)
 

@@ -233,6 +233,8 @@ int tdpg_iterate_dev(tdpg_session* s, int32_t n_iters, double* device_ms);
 int tdpg_engine_stats(tdpg_session* s, int32_t* iter, int32_t* refreshes, int64_t* launches);
 /* Device time spent in timing refreshes so far (CUDA events), the last one, and the ledger size. */
 int tdpg_engine_times(tdpg_session* s, double* refresh_ms_total, double* last_refresh_ms, int64_t* ledger_pairs);
+/* Paths (and their pins) extracted by the engine's timing refreshes since tdpg_engine_init. */
+int tdpg_engine_paths(tdpg_session* s, int64_t* paths, int64_t* path_pins);
 /* One iteration through host buffers (positions in, positions + trace row out) — the e2e path. */
 int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_trace_row* row);
 /* Per-kernel device time (ms) of one iteration of each kind, measured with events. */

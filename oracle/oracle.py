@@ -268,6 +268,45 @@ class Oracle(_Base):
                                         out.ctypes.data))
         return out
 
+    @classmethod
+    def generate(cls, seed=1, cells=100, registers=-1, fanout=2.0, fail_frac=0.2, r_unit=1e-4, c_unit=1e-4):
+        """generate_synthetic's netlist (generator.cpp:60-244, tdp_oracle_gen.c) without the clock
+        calibration: clock_period stays 1.0, positions are the centred starts (all implicit)."""
+        lib = cls.lib_()
+        lib.orc_generate.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, C.POINTER(_P)]
+        lib.orc_design_view.argtypes = [_P, _P, C.POINTER(_P)]
+        lib.orc_design_destroy.argtypes = [_P]
+        h = _P()
+        rc = lib.orc_generate(seed, cells, registers, fanout, fail_frac, r_unit, c_unit, C.byref(h))
+        if rc:
+            raise OracleError(rc, "validation error: generator: invalid spec")
+        try:
+            from paper_2503_11674_b200.design import TdpgNetlist
+            v = TdpgNetlist()
+            pos = _P()
+            lib.orc_design_view(h, C.byref(v), C.byref(pos))
+
+            def arr(ptr, n, ct, shape=None):
+                if n == 0:
+                    return np.zeros(shape or (0,), dtype=np.dtype(ct))
+                a = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
+                return a.reshape(shape) if shape else a
+
+            Cn, P, N = v.n_cells, v.n_pins, v.n_nets
+            E = int(arr(v.net_start, N + 1, C.c_int32)[-1])
+            return Design(cell_w=arr(v.cell_w, Cn, C.c_double), cell_h=arr(v.cell_h, Cn, C.c_double),
+                          cell_delay=arr(v.cell_delay, Cn, C.c_double), cell_fixed=arr(v.cell_fixed, Cn, C.c_uint8),
+                          pin_cell=arr(v.pin_cell, P, C.c_int32), pin_term=arr(v.pin_term, 2 * P, C.c_double, (P, 2)),
+                          pin_off=arr(v.pin_off, 2 * P, C.c_double, (P, 2)), pin_dir=arr(v.pin_dir, P, C.c_uint8),
+                          pin_cap=arr(v.pin_cap, P, C.c_double), net_start=arr(v.net_start, N + 1, C.c_int32),
+                          net_pins=arr(v.net_pins, E, C.c_int32), sources=arr(v.sources, v.n_sources, C.c_int32),
+                          endpoints=arr(v.endpoints, v.n_endpoints, C.c_int32), clock_period=v.clock_period,
+                          r_unit=v.r_unit, c_unit=v.c_unit, core=tuple(v.core),
+                          positions=arr(pos.value, 2 * Cn, C.c_double, (Cn, 2)), pos_explicit=np.zeros(Cn, np.uint8))
+        finally:
+            lib.orc_design_destroy(h)
+
     def place(self, cfg: dict | None = None, xy=None):
         c = make_config(cfg)
         xy = self.d.positions if xy is None else np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
@@ -543,6 +582,25 @@ class RefOracle(_Base):
         return dict(positions=pos, iterations=it.value, stop_reason="overflow" if so.value else "max_iters",
                     tns=fin[0], wns=fin[1], hpwl=fin[2], metrics_csv=csv, trace=parse_metrics_csv(csv),
                     ledger=ledger, elapsed_ms=ms.value)
+
+    def place_bench(self, cfg: dict, threads_obj=1, threads_sta=1, threads_ex=1, xy=None):
+        """run_placement's loop through the reference's own functions with a thread count per phase
+        (ref_harness.cpp ref_place_bench); per-iteration wall ms, refresh ms and extracted paths."""
+        self._pos(xy)
+        T = max(int(cfg.get("max_iters", 1500)), 1)
+        it_ms, rf_ms, paths = np.zeros(T), np.zeros(T), np.zeros(T, np.int64)
+        pairs, nr = C.c_int64(), C.c_int32()
+        fin = (C.c_double * 3)()
+        self.lib.ref_place_bench.argtypes = [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, _P, _P, _P, _I64P, _F64P,
+                                             _I32P]
+        self._check(self.lib.ref_place_bench(self.h, json.dumps(cfg).encode(), threads_obj, threads_sta, threads_ex,
+                                             it_ms.ctypes.data, rf_ms.ctypes.data, paths.ctypes.data,
+                                             C.byref(pairs), fin, C.byref(nr)))
+        n = nr.value
+        pos = np.zeros((self.d.n_cells, 2))
+        self.lib.ref_place_positions(self.h, pos.ctypes.data)
+        return dict(iter_ms=it_ms[:n], refresh_ms=rf_ms[:n], paths=paths[:n], rows=n, ledger_pairs=pairs.value,
+                    tns=fin[0], wns=fin[1], hpwl=fin[2], positions=pos)
 
     def compare(self, configs, parallel=False):
         """run_compare + compare_to_csv of the reference (compare.cpp:37-122); configs are dicts."""

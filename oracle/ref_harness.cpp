@@ -7,8 +7,11 @@
 // reference functions directly, so the tests and bench.py's CPU baseline
 // can run the reference itself on exactly the inputs the GPU engine sees.
 // Nothing in the product links or loads this file.
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
+#include <random>
 #include <map>
 #include <memory>
 #include <string>
@@ -23,6 +26,7 @@
 #include "tdp/paths.hpp"
 #include "tdp/pin_pairs.hpp"
 #include "tdp/placer.hpp"
+#include "tdp/rng.hpp"
 #include "tdp/sta.hpp"
 #include "tdp/timing_graph.hpp"
 #include "tdp/wirelength.hpp"
@@ -442,6 +446,114 @@ int ref_place(void* h, const char* config_json, double final_[3], int32_t* itera
         s->ledger = s->outcome.pair_weights;
         *n_pairs = static_cast<int64_t>(s->ledger.size());
         s->csv = tdp::metrics_to_csv(s->outcome.trace);
+    });
+}
+
+// bench.py's reference arm: run_placement's loop (placer.cpp:358-484) driven through the reference's
+// own public functions — objective_and_gradient, AdamState::step, run_sta, report_timing_endpoint /
+// report_timing, collect_pin_pairs, update_pair_weights, apply_net_weights — with a thread count per
+// phase (the reference's STA / objective are fastest at nproc threads, its extraction at one
+// thread, where the enumerator memoises prefixes).  Every loop step is the reference's, in its order;
+// only the per-phase `threads` argument differs from run_placement(cfg.threads).  Per iteration: wall ms
+// (refresh included), refresh ms and extracted paths (0 on non-timing iterations).
+int ref_place_bench(void* h, const char* config_json, int threads_obj, int threads_sta, int threads_ex,
+                    double* iter_ms, double* refresh_ms, int64_t* paths, int64_t* pairs_end, double final_[3],
+                    int32_t* n_rows)
+{
+    return guard([&] {
+        auto* s = static_cast<RefSession*>(h);
+        const tdp::OptimizerConfig config =
+            (config_json && *config_json) ? tdp::config_from_json(config_json) : tdp::OptimizerConfig{};
+        const tdp::Design& design = s->design;
+        const tdp::Netlist& nl = design.netlist;
+        const tdp::DesignConstraints& dc = design.constraints;
+        const tdp::TimingGraph& graph = s->g();
+        std::vector<tdp::Point> pos = design.positions;
+        auto clamp = [&](tdp::Point& p, const tdp::Cell& cell) { // clamp_to_core (placer.cpp:99-103)
+            p.x = std::clamp(p.x, dc.core.x_lo, dc.core.x_hi - cell.width);
+            p.y = std::clamp(p.y, dc.core.y_lo, dc.core.y_hi - cell.height);
+        };
+        const double span = dc.core.span();
+        const double gamma = config.gamma_frac * span;
+        std::mt19937_64 rng(config.seed); // placer.cpp:375-382
+        for (std::size_t c = 0; c < nl.cells.size(); ++c) {
+            const tdp::Cell& cell = nl.cells[c];
+            if (cell.is_fixed || design.pos_explicit[c]) continue;
+            pos[c].x += tdp::rng_uniform(rng, -1.0, 1.0) * config.init_jitter_frac * dc.core.width();
+            pos[c].y += tdp::rng_uniform(rng, -1.0, 1.0) * config.init_jitter_frac * dc.core.height();
+            clamp(pos[c], cell);
+        }
+        const tdp::DensityGrid grid(nl, dc.core, config.grid_nx, config.grid_ny, config.target_density);
+        tdp::PinPairWeights pairs;
+        std::vector<double> net_weights;
+        double lambda = config.lambda0;
+        if (lambda <= 0.0) { // placer.cpp:388-402
+            const tdp::ObjectiveResult wl_only = tdp::objective_and_gradient(nl, pos, grid, {}, {}, gamma, 0.0, 0.0,
+                                                                             config.pp_loss, threads_obj);
+            const tdp::DensityResult d0 = grid.evaluate(nl, pos, threads_obj);
+            double wl_l1 = 0.0, d_l1 = 0.0;
+            for (std::size_t c = 0; c < nl.cells.size(); ++c) {
+                if (nl.cells[c].is_fixed) continue;
+                wl_l1 += std::abs(wl_only.d_cell[c].x) + std::abs(wl_only.d_cell[c].y);
+                d_l1 += std::abs(d0.d_cell[c].x) + std::abs(d0.d_cell[c].y);
+            }
+            lambda = (wl_l1 > 0.0 && d_l1 > 0.0) ? wl_l1 / d_l1 : 1.0;
+        }
+        const double lambda_cap = lambda * config.lambda_max;
+        tdp::AdamState adam(2 * nl.cells.size());
+        std::vector<double> flat(2 * nl.cells.size()), grad_flat(2 * nl.cells.size());
+        bool timing_engaged = false;
+        int rows = 0;
+        for (int iter = 0; iter < config.max_iters; ++iter) {
+            const auto t0 = std::chrono::steady_clock::now();
+            refresh_ms[iter] = 0.0, paths[iter] = 0;
+            if (iter >= config.timing_start_iter && (iter - config.timing_start_iter) % config.m == 0) {
+                timing_engaged = true;
+                const tdp::PinPositions ppos = tdp::pin_positions(nl, pos);
+                const tdp::TimingAnnotation ann = tdp::run_sta(graph, nl, ppos, dc, threads_sta);
+                tdp::ExtractionReport report;
+                if (ann.wns < 0.0) {
+                    int n_fail = 0;
+                    for (const auto& [pin, slack] : ann.endpoint_slacks)
+                        if (slack < 0.0) ++n_fail;
+                    report = config.extraction == tdp::ExtractionPolicy::Endpoint
+                                 ? tdp::report_timing_endpoint(graph, nl, ppos, dc, ann, n_fail, config.k, threads_ex)
+                                 : tdp::report_timing(graph, nl, ppos, dc, ann, n_fail, threads_ex);
+                    const std::vector<tdp::PairHit> hits = tdp::collect_pin_pairs(nl, report.paths);
+                    tdp::update_pair_weights(pairs, hits, ann.wns, config.w0, config.w1);
+                }
+                if (config.net_weighting) net_weights = tdp::apply_net_weights(ann, nl);
+                refresh_ms[iter] = ms_since(t0);
+                paths[iter] = static_cast<int64_t>(report.paths.size());
+            }
+            const tdp::ObjectiveResult obj = tdp::objective_and_gradient(nl, pos, grid, pairs, net_weights, gamma, lambda,
+                                                                         config.beta, config.pp_loss, threads_obj);
+            ++rows;
+            if (timing_engaged && obj.overflow <= config.stop_overflow) {
+                iter_ms[iter] = ms_since(t0);
+                break;
+            }
+            for (std::size_t c = 0; c < nl.cells.size(); ++c) {
+                flat[2 * c] = pos[c].x, flat[2 * c + 1] = pos[c].y;
+                grad_flat[2 * c] = obj.d_cell[c].x, grad_flat[2 * c + 1] = obj.d_cell[c].y;
+            }
+            const double lr = config.step0_frac * span * std::pow(config.step_decay, iter);
+            adam.step(flat, grad_flat, lr, config.adam_beta1, config.adam_beta2, config.adam_eps);
+            for (std::size_t c = 0; c < nl.cells.size(); ++c) {
+                if (nl.cells[c].is_fixed) continue;
+                pos[c] = tdp::Point{flat[2 * c], flat[2 * c + 1]};
+                clamp(pos[c], nl.cells[c]);
+            }
+            lambda = std::min(lambda * config.mu, lambda_cap);
+            iter_ms[iter] = ms_since(t0);
+        }
+        *n_rows = rows;
+        *pairs_end = static_cast<int64_t>(pairs.size());
+        const tdp::TimingAnnotation fin = tdp::run_sta(graph, nl, tdp::pin_positions(nl, pos), dc, threads_sta);
+        final_[0] = fin.tns, final_[1] = fin.wns;
+        final_[2] = tdp::hpwl_total(nl, tdp::pin_positions(nl, pos));
+        s->outcome.positions = std::move(pos);
+        s->ledger = std::move(pairs);
     });
 }
 

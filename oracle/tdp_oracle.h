@@ -68,6 +68,13 @@ int orc_place(void* h, const double* init_xy, const uint8_t* pos_explicit, const
 
 void orc_config_default(tdpg_config* cfg);
 
+/* generate_synthetic's netlist (generator.cpp:60-244) without the clock calibration (clock 1.0);
+ * tdp_oracle_gen.c.  orc_design_view points into the handle's arrays. */
+int orc_generate(uint64_t seed, int32_t n_cells, int32_t n_registers, double avg_fanout, double fail_frac,
+                 double r_unit, double c_unit, void** out);
+int orc_design_view(void* d, tdpg_netlist* view, const double** positions);
+void orc_design_destroy(void* d);
+
 /* mt19937_64 (the C++ standard's engine), exposed for tests. */
 typedef struct { uint64_t mt[312]; int idx; } orc_mt64;
 void orc_mt64_seed(orc_mt64* r, uint64_t seed);

@@ -40,6 +40,7 @@ struct Engine {
     cudaGraphExec_t gexec = nullptr;
     int launched = 0, refreshes = 0, recaptures = 0;
     long long kernel_launches = 0;
+    long long paths_host = 0, path_pins_host = 0; // paths extracted by host-sized refreshes (k > 1 / topn)
     int kernels_per_iter = 8; // 2 WA class groups + generic + scatter + bins + dens_grad + finalize + cells
     cudaGraphExec_t refresh_gexec = nullptr; // the whole timing refresh, captured once
     cudaGraphExec_t sort_gexec = nullptr;    // spatial re-sort of the cells
@@ -49,6 +50,7 @@ struct Engine {
     unsigned long long old_epoch = 0;
     tdpg_config old_cfg{};
     int old_sort_every = 0;
+    double consts[3] = {0, 0, 0}, old_consts[3] = {0, 0, 0}; // clock, r_unit, c_unit baked into the graphs
     unsigned long long epoch = 0;            // dbuf_epoch() when the graphs were captured
     bool refresh_lonly = false;              // the refresh graph leaves the STA results in L-space only
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> refresh_ev;
@@ -100,18 +102,44 @@ struct Engine {
             std::swap(old_gexec, o.gexec), std::swap(old_gexec_sorted, o.gexec_sorted);
             std::swap(old_refresh, o.refresh_gexec), std::swap(old_sort, o.sort_gexec);
             old_lonly = o.refresh_lonly, old_epoch = o.epoch, old_cfg = o.cfg, old_sort_every = o.sort_every;
+            std::memcpy(old_consts, o.consts, sizeof consts);
         }
+    }
+    // the configuration fields the captured graphs depend on (kernel arguments, schedule layout); the
+    // ignored `threads` and the iteration count are not among them, nor are padding bytes
+    static bool graph_cfg_equal(const tdpg_config& a, const tdpg_config& b)
+    {
+        auto same = [](double x, double y) { return std::memcmp(&x, &y, sizeof x) == 0; };
+        return same(a.gamma_frac, b.gamma_frac) && a.grid_nx == b.grid_nx && a.grid_ny == b.grid_ny &&
+               same(a.target_density, b.target_density) && same(a.beta, b.beta) && a.pp_loss == b.pp_loss &&
+               a.net_weighting == b.net_weighting && a.m == b.m && same(a.w0, b.w0) && same(a.w1, b.w1) &&
+               a.timing_start_iter == b.timing_start_iter && a.extraction == b.extraction && a.k == b.k &&
+               same(a.stop_overflow, b.stop_overflow) && same(a.mu, b.mu) && same(a.lambda0, b.lambda0) &&
+               same(a.lambda_max, b.lambda_max) && same(a.step0_frac, b.step0_frac) &&
+               same(a.step_decay, b.step_decay) && same(a.adam_beta1, b.adam_beta1) &&
+               same(a.adam_beta2, b.adam_beta2) && same(a.adam_eps, b.adam_eps) && a.seed == b.seed &&
+               same(a.init_jitter_frac, b.init_jitter_frac) && a.density_model == b.density_model;
+    }
+    static void session_consts(const tdpg_session* s, double (&c)[3]) { c[0] = s->clock, c[1] = s->r_unit, c[2] = s->c_unit; }
+    bool consts_match(const tdpg_session* s) const
+    {
+        double c[3];
+        session_consts(s, c);
+        return std::memcmp(c, consts, sizeof c) == 0;
     }
     // The previous engine's graphs point into exactly this engine's (recycled) buffers when no device
     // buffer moved since they were captured and the configuration (baked into kernel arguments) matches.
-    bool adopt_graphs()
+    bool adopt_graphs(const tdpg_session* s)
     {
+        double c[3];
+        session_consts(s, c);
         if (!old_gexec || old_epoch != dbuf_epoch() || partitioned || old_sort_every != sort_every ||
-            std::memcmp(&old_cfg, &cfg, sizeof cfg) != 0)
+            !graph_cfg_equal(old_cfg, cfg) || std::memcmp(c, old_consts, sizeof c) != 0)
             return false;
         std::swap(gexec, old_gexec), std::swap(gexec_sorted, old_gexec_sorted);
         std::swap(refresh_gexec, old_refresh), std::swap(sort_gexec, old_sort);
         refresh_lonly = old_lonly, epoch = old_epoch;
+        std::memcpy(consts, old_consts, sizeof consts);
         return true;
     }
     double refresh_ms()
@@ -562,13 +590,15 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     // every buffer the graphs touch is sized before capture, so their pointers never move
     tr.mark("schedule + buffers");
     refresh_reserve(s);
+    s->ex_counts.zero(s->st); // (the refresh graph accumulates the run's path totals in [3], [4])
     place_tail_reserve(s); // (so a later run of the session finds every buffer where its graphs point)
     s->pin_xy_external = false;
     sort_cells_spatial(s);
     tr.mark("reserve + sort");
     s->eng = E.release();
     Engine& G = *s->eng;
-    if (!G.adopt_graphs()) {
+    if (!G.adopt_graphs(s)) {
+        Engine::session_consts(s, G.consts);
         capture_iteration(s, G);
         tr.mark("iteration graph");
         G.refresh_gexec = capture(s, [&] {
@@ -681,6 +711,7 @@ void timing_refresh_general(tdpg_session* s)
     if (!c.stopped && h[1] < 0.0) {
         extract_policy_dev(s, E.cfg.extraction, static_cast<int>(h[2]), E.cfg.k, true);
         E.kernel_launches += s->L + 16;
+        E.paths_host += s->n_paths, E.path_pins_host += s->n_path_pins;
         const long long H = s->n_hits;
         if (H > 0) {
             k_ledger_dense_gen<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(
@@ -753,10 +784,12 @@ void engine_release(tdpg_session* s)
     s->eng = nullptr;
 }
 
-// Re-capture the engine's graphs when a device buffer they point into was (re)allocated since.
+// Re-capture the engine's graphs when a device buffer they point into was (re)allocated since, or when
+// the clock / RC units baked into their kernel arguments changed (tdpg_set_constraints).
 void ensure_graphs(tdpg_session* s, Engine& E)
 {
-    if (E.epoch == dbuf_epoch()) return;
+    if (E.epoch == dbuf_epoch() && E.consts_match(s)) return; // (tdpg_set_constraints may have moved them)
+    Engine::session_consts(s, E.consts);
     if (E.gexec_a) cudaGraphExecDestroy(E.gexec_a), E.gexec_a = nullptr;
     if (E.gexec_b) cudaGraphExecDestroy(E.gexec_b), E.gexec_b = nullptr;
     capture_iteration(s, E);
@@ -1005,6 +1038,18 @@ int tdpg_engine_stats(tdpg_session* s, int32_t* iter, int32_t* refreshes, int64_
     if (iter) *iter = s->eng->launched;
     if (refreshes) *refreshes = s->eng->refreshes;
     if (launches) *launches = s->eng->kernel_launches;
+    API_END
+}
+
+int tdpg_engine_paths(tdpg_session* s, int64_t* paths, int64_t* path_pins)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised");
+    long long c[5] = {0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(c, s->ex_counts.p, sizeof c, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (paths) *paths = c[3] + s->eng->paths_host;
+    if (path_pins) *path_pins = c[4] + s->eng->path_pins_host;
     API_END
 }
 

@@ -1470,6 +1470,8 @@ __global__ void k_extract_counts(int EP, const double* __restrict__ sta_out, con
     counts[0] = on ? static_cast<long long>(sta_out[2]) : 0;
     counts[1] = on ? static_cast<long long>(off[EP - 1]) + len[EP - 1] : 0;
     counts[2] = on ? static_cast<long long>(hoff[EP - 1]) + hops[EP - 1] : 0;
+    counts[3] += counts[0]; // engine totals over every refresh since engine_init (tdpg_engine_paths)
+    counts[4] += counts[1];
 }
 
 __global__ void k_net_weights_dev(int N, const int* __restrict__ net_start, const int* __restrict__ net_pins,
@@ -1509,6 +1511,12 @@ void refresh_reserve(tdpg_session* s)
 {
     const size_t EP = static_cast<size_t>(std::max(s->EP, 1));
     const size_t L = static_cast<size_t>(std::max(s->L, 1));
+    // the refresh's path slots, hits and scans are int-indexed (cub counts, slot offsets): refuse designs
+    // whose worst case would overflow them instead of corrupting memory
+    if (EP * (L + 1) > static_cast<size_t>(INT_MAX) || EP * ((L + 1) / 2 + 1) > static_cast<size_t>(INT_MAX))
+        throw Error(TDPG_ERR_VALIDATION, "validation error: design too large for the timing refresh: " +
+                                             std::to_string(EP) + " endpoints x " + std::to_string(L + 1) +
+                                             " levels exceed 2^31 path-pin slots");
     s->hcap = static_cast<long long>(EP) * static_cast<long long>((L + 1) / 2 + 1);
     const size_t H = static_cast<size_t>(s->hcap);
     s->sort_k0.reserve(EP), s->sort_k1.reserve(EP), s->sort_v0.reserve(EP), s->sort_v1.reserve(EP);
@@ -1517,7 +1525,7 @@ void refresh_reserve(tdpg_session* s)
     s->ex_tmp_pins.reserve(EP * (L + 1)), s->ex_tmp_keys.reserve(EP * (L / 2 + 2)); // (k_bt_walk slots)
     s->eh_key.reserve(H), s->eh_key_s.reserve(H), s->eh_idx.reserve(H), s->eh_idx_s.reserve(H);
     s->eh_slack.reserve(H);
-    s->ex_counts.reserve(4), s->q_count.reserve(2), s->sta_out.reserve(4);
+    s->ex_counts.reserve(8), s->q_count.reserve(2), s->sta_out.reserve(4);
     const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(s->P, s->EP), kBlock))));
     s->sta_part.reserve(3 * nb + 8);
     size_t b1 = 0, b2 = 0, b3 = 0;

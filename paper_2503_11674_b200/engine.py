@@ -113,6 +113,7 @@ _SIGS = {
     "tdpg_k_worst": (C.c_int, [_P, C.c_int32, C.c_int32, _I32P, _P, _P, C.c_int32, _P]),
     "tdpg_set_round_callback": (C.c_int, [_P, _P, _P]),
     "tdpg_engine_times": (C.c_int, [_P, _F64P, _F64P, _I64P]),
+    "tdpg_engine_paths": (C.c_int, [_P, _I64P, _I64P]),
     "tdpg_profile_iteration": (C.c_int, [_P, C.c_int32, _F64P, C.c_int32, C.c_char_p, C.c_int32]),
     "tdpg_generate": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
                                 C.c_double, C.c_int32, C.POINTER(_P)]),
@@ -170,6 +171,14 @@ class Session:
             self.close()
         except Exception:
             pass
+
+    def set_constraints(self, clock_period, r_unit=None, c_unit=None):
+        """DesignConstraints of the session (clock, RC units); the design copy follows."""
+        r = self.d.r_unit if r_unit is None else r_unit
+        c = self.d.c_unit if c_unit is None else c_unit
+        _check(self.lib.tdpg_set_constraints(self.h, float(clock_period), float(r), float(c)))
+        self.d = self.d.copy()  # (the caller's design object is left as it was)
+        self.d.clock_period, self.d.r_unit, self.d.c_unit = float(clock_period), float(r), float(c)
 
     # positions -----------------------------------------------------------
     def set_positions(self, xy):
@@ -406,8 +415,10 @@ class Session:
         _check(self.lib.tdpg_engine_stats(self.h, C.byref(it), C.byref(rf), C.byref(ln)))
         tot, last, q = C.c_double(), C.c_double(), C.c_int64()
         _check(self.lib.tdpg_engine_times(self.h, C.byref(tot), C.byref(last), C.byref(q)))
+        pa, pp = C.c_int64(), C.c_int64()
+        _check(self.lib.tdpg_engine_paths(self.h, C.byref(pa), C.byref(pp)))
         return dict(iterations=it.value, refreshes=rf.value, kernel_launches=ln.value, refresh_ms=tot.value,
-                    last_refresh_ms=last.value, ledger_pairs=q.value)
+                    last_refresh_ms=last.value, ledger_pairs=q.value, paths=pa.value, path_pins=pp.value)
 
     def profile_iteration(self, reps=5):
         n = 16

@@ -413,3 +413,35 @@ def test_repeated_runs_adopt_graphs_and_stay_exact():
     for r, f in zip(runs, (fresh_base, fresh_base, fresh_other, fresh_base)):
         assert np.array_equal(r["positions"], f["positions"])
         assert [t.hpwl for t in r["trace"]] == [t.hpwl for t in f["trace"]]
+
+
+def test_repeated_runs_follow_changed_constraints():
+    """The clock and RC units are kernel arguments of the captured refresh graph: a run after
+    tdpg_set_constraints must not adopt the previous run's graphs (place.cu adopt_graphs),
+    and an engine whose constraints change between iterations re-captures."""
+    d = generate(seed=7, cells=6000, fail_frac=0.8, calibrate=True)
+    cfg = {"grid_nx": 32, "grid_ny": 32, "m": 5, "timing_start_iter": 0, "max_iters": 30, "seed": 4}
+    s = Session(d)
+    s.place(cfg)
+    for clock, r, c in ((d.clock_period * 0.7, d.r_unit, d.c_unit), (d.clock_period, d.r_unit * 2, d.c_unit),
+                        (d.clock_period, d.r_unit, d.c_unit * 0.5)):
+        s.set_constraints(clock, r, c)
+        got = s.place(cfg)
+        d2 = d.copy()
+        d2.clock_period, d2.r_unit, d2.c_unit = clock, r, c
+        want = Session(d2).place(cfg)
+        assert np.array_equal(got["positions"], want["positions"])
+        assert [(t.tns, t.wns) for t in got["trace"]] == [(t.tns, t.wns) for t in want["trace"]]  # (same engine code)
+        assert any(t.has_timing and t.wns < 0 for t in want["trace"])
+    # mid-run change: the next refresh of a running engine sees the new clock
+    s2 = Session(d)
+    s2.engine_init(dict(cfg, max_iters=20))
+    s2.iterate(10)  # iterations 0..9; the refresh of iteration 10 runs first in the next step
+    new_clock = d.clock_period * 0.6
+    s2.set_constraints(new_clock)
+    d3 = d.copy()
+    d3.clock_period = new_clock
+    want = Session(d3).sta(s2.positions())
+    row = s2.step_host(None, None)
+    assert row.iter == 10 and row.has_timing
+    assert row.wns == want["wns"] and abs(row.tns - want["tns"]) <= 1e-12 * abs(want["tns"])
