@@ -140,6 +140,9 @@ int tdpg_graph_arcs(tdpg_session* s, int32_t* from, int32_t* to, int32_t* kind, 
 int tdpg_set_positions(tdpg_session* s, const double* cell_xy);   /* [2*n_cells] host */
 int tdpg_get_positions(tdpg_session* s, double* cell_xy);
 int tdpg_pin_positions(tdpg_session* s, double* pin_xy);          /* [2*n_pins] out    */
+/* Pin::terminal_pos of the terminal pins ([2*n_pins], entries of cell pins ignored): lets one session
+ * serve repeated per-net calls (wa_wirelength / hpwl_net on terminal pins, wirelength.hpp:21-23). */
+int tdpg_set_terminal_positions(tdpg_session* s, const double* pin_xy);
 
 /* ---- objective terms (at the session's current positions) ----------- */
 /* wl = sum_e w_e * WA_e, hpwl exact; pin_grad [2*n_pins] (w_e-scaled) may be NULL. */

@@ -591,16 +591,17 @@ class RefOracle(_Base):
         it_ms, rf_ms, paths = np.zeros(T), np.zeros(T), np.zeros(T, np.int64)
         pairs, nr = C.c_int64(), C.c_int32()
         fin = (C.c_double * 3)()
+        rows = (TdpgTraceRow * T)()
         self.lib.ref_place_bench.argtypes = [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, _P, _P, _P, _I64P, _F64P,
-                                             _I32P]
+                                             _I32P, _P]
         self._check(self.lib.ref_place_bench(self.h, json.dumps(cfg).encode(), threads_obj, threads_sta, threads_ex,
                                              it_ms.ctypes.data, rf_ms.ctypes.data, paths.ctypes.data,
-                                             C.byref(pairs), fin, C.byref(nr)))
+                                             C.byref(pairs), fin, C.byref(nr), rows))
         n = nr.value
         pos = np.zeros((self.d.n_cells, 2))
         self.lib.ref_place_positions(self.h, pos.ctypes.data)
         return dict(iter_ms=it_ms[:n], refresh_ms=rf_ms[:n], paths=paths[:n], rows=n, ledger_pairs=pairs.value,
-                    tns=fin[0], wns=fin[1], hpwl=fin[2], positions=pos)
+                    tns=fin[0], wns=fin[1], hpwl=fin[2], positions=pos, trace=[rows[i] for i in range(n)])
 
     def compare(self, configs, parallel=False):
         """run_compare + compare_to_csv of the reference (compare.cpp:37-122); configs are dicts."""

@@ -458,7 +458,7 @@ int ref_place(void* h, const char* config_json, double final_[3], int32_t* itera
 // (refresh included), refresh ms and extracted paths (0 on non-timing iterations).
 int ref_place_bench(void* h, const char* config_json, int threads_obj, int threads_sta, int threads_ex,
                     double* iter_ms, double* refresh_ms, int64_t* paths, int64_t* pairs_end, double final_[3],
-                    int32_t* n_rows)
+                    int32_t* n_rows, tdpg_trace_row* trace)
 {
     return guard([&] {
         auto* s = static_cast<RefSession*>(h);
@@ -507,10 +507,13 @@ int ref_place_bench(void* h, const char* config_json, int threads_obj, int threa
         for (int iter = 0; iter < config.max_iters; ++iter) {
             const auto t0 = std::chrono::steady_clock::now();
             refresh_ms[iter] = 0.0, paths[iter] = 0;
+            bool sta_row = false;
+            double row_tns = 0.0, row_wns = 0.0;
             if (iter >= config.timing_start_iter && (iter - config.timing_start_iter) % config.m == 0) {
                 timing_engaged = true;
                 const tdp::PinPositions ppos = tdp::pin_positions(nl, pos);
                 const tdp::TimingAnnotation ann = tdp::run_sta(graph, nl, ppos, dc, threads_sta);
+                sta_row = true, row_tns = ann.tns, row_wns = ann.wns;
                 tdp::ExtractionReport report;
                 if (ann.wns < 0.0) {
                     int n_fail = 0;
@@ -528,6 +531,12 @@ int ref_place_bench(void* h, const char* config_json, int threads_obj, int threa
             }
             const tdp::ObjectiveResult obj = tdp::objective_and_gradient(nl, pos, grid, pairs, net_weights, gamma, lambda,
                                                                          config.beta, config.pp_loss, threads_obj);
+            if (trace) { // TraceRow (placer.cpp:445-457)
+                tdpg_trace_row& r = trace[iter];
+                r.iter = iter, r.has_timing = sta_row ? 1 : 0, r.hpwl = obj.hpwl, r.overflow = obj.overflow;
+                r.tns = row_tns, r.wns = row_wns, r.wl_term = obj.wl_term, r.density_term = obj.density_term;
+                r.pp_term = obj.pp_term, r.lambda = lambda, r.beta_pp = config.beta * obj.pp_term;
+            }
             ++rows;
             if (timing_engaged && obj.overflow <= config.stop_overflow) {
                 iter_ms[iter] = ms_since(t0);

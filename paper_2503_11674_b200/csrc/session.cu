@@ -44,6 +44,13 @@ void* cub_scratch(tdpg_session* s, size_t bytes)
     return s->cub_tmp.p;
 }
 
+__global__ void k_gather_anchor(int P, const int* __restrict__ L_pin, const double2* __restrict__ anchor,
+                                double2* __restrict__ L_anchor)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P) L_anchor[i] = anchor[L_pin[i]];
+}
+
 // Kernel: pin positions (netlist.cpp:23-32): anchor + offset, two IEEE adds.
 // Fixed-cell baseline (density.cpp:75-93): exact overlap areas, accumulated in the grid's fixed point
 // (integer atomics commute, so the baseline is the same bits whatever the order), then converted.
@@ -642,6 +649,22 @@ int tdpg_set_positions(tdpg_session* s, const double* xy)
 {
     API_BEGIN
     upload_positions(s, xy);
+    CK(cudaStreamSynchronize(s->st));
+    API_END
+}
+
+int tdpg_set_terminal_positions(tdpg_session* s, const double* xy)
+{
+    API_BEGIN
+    if (s->P == 0) return TDPG_OK;
+    for (int p = 0; p < s->P; ++p)
+        if (s->h_pin_cell[p] < 0) s->h_pin_term[2 * p] = xy[2 * p], s->h_pin_term[2 * p + 1] = xy[2 * p + 1];
+    s->anchor.upload(reinterpret_cast<const double2*>(s->h_pin_term.data()), s->P, s->st);
+    if (s->L_anchor.p && s->L_pin.p) { // the level-major copy the STA sweeps read
+        k_gather_anchor<<<blocks_for(s->P, 256), 256, 0, s->st>>>(s->P, s->L_pin, s->anchor, s->L_anchor);
+        CK_LAUNCH();
+    }
+    s->sta_valid = false;
     CK(cudaStreamSynchronize(s->st));
     API_END
 }

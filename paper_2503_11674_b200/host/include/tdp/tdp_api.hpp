@@ -2,8 +2,8 @@
 // re-declared over the B200 engine.  Callers of the reference keep compiling unchanged: every
 // reference header name (tdp/sta.hpp, tdp/paths.hpp, ...) includes this file.  Types are plain data
 // with the reference's field names; the functions run on the GPU through the C-ABI (include/tdpg.h).
-// Differences from the reference are limited to features the device does not implement yet: path
-// ranks > 0 (k > 1) and the topn policy throw std::logic_error.
+// Every hot-path function runs on the device (k > 1 paths and the topn policy included); the host keeps
+// only input/output glue (config JSON, CSV/JSON serialisation, type conversion).
 #pragma once
 
 #include <cmath>
@@ -283,6 +283,12 @@ struct TraceRow {
     bool has_timing = false;
     double tns = 0.0, wns = 0.0, wl_term = 0.0, density_term = 0.0, pp_term = 0.0, lambda = 0.0, beta_pp = 0.0;
 };
+/// JSON round-trip with unknown-key rejection (placer.hpp:58-65, placer.cpp:107-232): host-side
+/// configuration I/O, same keys, messages and formatting as the reference.
+OptimizerConfig config_from_json(const std::string& text);
+std::string config_to_json(const OptimizerConfig& config);
+OptimizerConfig load_config(const std::string& path);
+void save_config(const OptimizerConfig& config, const std::string& path);
 using MetricTrace = std::vector<TraceRow>;
 std::string metrics_to_csv(const MetricTrace& trace);
 struct ObjectiveResult {

@@ -1,15 +1,21 @@
 // tdp_api.cpp — the reference's tdp:: operator API implemented over the sm_100a engine (include/tdpg.h).
 //
-// A device session is created once per netlist and cached (keyed on the Netlist's address plus a cheap
-// fingerprint), so per-iteration calls such as objective_and_gradient only upload positions.  Exceptions
+// A device session is created once per netlist and cached (keyed on the Netlist's address, sizes, storage
+// addresses and a fixed-size content sample: O(1) per call), so per-iteration calls such as
+// objective_and_gradient only upload positions.  Per-net calls on bare points (wa_wirelength, hpwl_net,
+// pin_pair_loss, update_pair_weights) reuse one scratch session per point count.  Exceptions
 // from the C-ABI are re-thrown as the reference's exception classes with the reference's messages.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <fstream>
 #include <memory>
+#include <sstream>
 #include <mutex>
 #include <thread>
 #include <set>
+
+#include <json.hpp> // nlohmann json (header-only, the reference's own JSON dependency)
 
 #include "tdp/tdp_api.hpp"
 #include "tdpg.h"
@@ -98,30 +104,43 @@ struct Sess {
     }
 };
 
-// Content hash of everything the device session holds (sizes, cell geometry/delays/fixed flags, pin
-// ownership/offsets/terminal positions/directions/caps, net membership, sources, endpoints): a cached
-// session is reused only for an identical netlist, never for a different one at the same address.
-std::vector<std::size_t> fingerprint(const Netlist& nl)
+// Identity of a Netlist for the session cache, O(1) in the netlist size: the reference's Netlist is
+// immutable after construction, so its address, its sizes and the addresses of its
+// storage identify it; a fixed sample of 64 evenly spaced cells, pins and nets guards against a
+// different netlist later built at a reused address.  (Round 1 hashed every byte: 0.3 s per call at 1M.)
+std::vector<std::size_t> netlist_key(const Netlist& nl)
 {
-    std::uint64_t h = 1469598103934665603ull; // FNV-1a over the raw field bytes
+    std::uint64_t h = 1469598103934665603ull;
     auto mix = [&](const void* p, std::size_t n) {
         const auto* b = static_cast<const unsigned char*>(p);
         for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
     };
     auto d = [&](double x) { mix(&x, sizeof x); };
     auto i32 = [&](int x) { mix(&x, sizeof x); };
-    for (const Cell& c : nl.cells) d(c.width), d(c.height), d(c.delay), i32(c.is_fixed);
-    for (const Pin& p : nl.pins)
-        i32(p.cell), d(p.terminal_pos.x), d(p.terminal_pos.y), d(p.offset.x), d(p.offset.y),
-            i32(p.dir == PinDir::Output), d(p.load_cap);
-    for (const Net& n : nl.nets) {
+    constexpr std::size_t kSample = 64;
+    auto each = [&](std::size_t n, auto&& f) {
+        const std::size_t step = std::max<std::size_t>(1, n / kSample);
+        for (std::size_t i = 0; i < n; i += step) f(i);
+        if (n) f(n - 1);
+    };
+    each(nl.cells.size(), [&](std::size_t i) {
+        const Cell& c = nl.cells[i];
+        d(c.width), d(c.height), d(c.delay), i32(c.is_fixed);
+    });
+    each(nl.pins.size(), [&](std::size_t i) {
+        const Pin& p = nl.pins[i];
+        i32(p.cell), d(p.terminal_pos.x), d(p.terminal_pos.y), d(p.offset.x), d(p.offset.y);
+        i32(p.dir == PinDir::Output), d(p.load_cap);
+    });
+    each(nl.nets.size(), [&](std::size_t i) {
+        const Net& n = nl.nets[i];
         i32(n.driver), i32(static_cast<int>(n.sinks.size()));
-        if (!n.sinks.empty()) mix(n.sinks.data(), n.sinks.size() * sizeof(int));
-    }
-    if (!nl.sources.empty()) mix(nl.sources.data(), nl.sources.size() * sizeof(int));
-    if (!nl.endpoints.empty()) mix(nl.endpoints.data(), nl.endpoints.size() * sizeof(int));
+        if (!n.sinks.empty()) i32(n.sinks.front()), i32(n.sinks.back());
+    });
+    auto addr = [](const void* p) { return reinterpret_cast<std::size_t>(p); };
     return {nl.cells.size(), nl.pins.size(), nl.nets.size(), nl.sources.size(), nl.endpoints.size(),
-            static_cast<std::size_t>(h)};
+            addr(nl.cells.data()), addr(nl.pins.data()), addr(nl.nets.data()), addr(nl.sources.data()),
+            addr(nl.endpoints.data()), static_cast<std::size_t>(h)};
 }
 
 std::mutex g_mu;
@@ -132,7 +151,7 @@ std::shared_ptr<Sess> fresh_session(const Netlist& nl, const DesignConstraints& 
 {
     auto S = std::make_shared<Sess>();
     S->flat = std::make_unique<FlatNetlist>(nl, c);
-    S->fp = fingerprint(nl);
+    S->fp = netlist_key(nl);
     ck(tdpg_session_create(&S->flat->view, &S->s));
     ck(tdpg_set_constraints(S->s, c.clock_period > 0 ? c.clock_period : 1.0, c.r_unit, c.c_unit));
     return S;
@@ -142,7 +161,7 @@ std::shared_ptr<Sess> fresh_session(const Netlist& nl, const DesignConstraints& 
 std::shared_ptr<Sess> session(const Netlist& nl, const DesignConstraints& c)
 {
     std::lock_guard<std::mutex> lock(g_mu);
-    auto fp = fingerprint(nl);
+    auto fp = netlist_key(nl);
     auto it = g_cache.find(&nl);
     if (it != g_cache.end() && it->second->fp == fp) {
         ck(tdpg_set_constraints(it->second->s, c.clock_period > 0 ? c.clock_period : 1.0, c.r_unit, c.c_unit));
@@ -203,6 +222,28 @@ struct PointNet {
         nl.finalize();
     }
 };
+
+// Scratch session for calls on bare points: the one-net netlist of n terminal pins above, one per
+// point count and thread, kept across calls and re-pointed with tdpg_set_terminal_positions.
+tdpg_session* scratch_session(std::span<const Point> pts)
+{
+    struct Entry {
+        std::unique_ptr<PointNet> net;
+        std::shared_ptr<Sess> S;
+    };
+    thread_local std::map<std::size_t, Entry> cache;
+    auto it = cache.find(pts.size());
+    if (it == cache.end()) {
+        if (cache.size() >= 16) cache.clear();
+        Entry e{std::make_unique<PointNet>(pts), nullptr};
+        e.S = fresh_session(e.net->nl, core_only({}));
+        return cache.emplace(pts.size(), std::move(e)).first->second.S->s;
+    }
+    std::vector<double> xy(2 * pts.size());
+    for (std::size_t i = 0; i < pts.size(); ++i) xy[2 * i] = pts[i].x, xy[2 * i + 1] = pts[i].y;
+    ck(tdpg_set_terminal_positions(it->second.S->s, xy.data()));
+    return it->second.S->s;
+}
 
 void set_core(tdpg_session* s, const Rect& r)
 {
@@ -502,17 +543,16 @@ void update_pair_weights(PinPairWeights& weights, const std::vector<PairHit>& hi
     int max_pin = 0;
     for (const auto& [pr, w] : weights) max_pin = std::max({max_pin, pr.first, pr.second});
     for (const auto& h : hits) max_pin = std::max({max_pin, h.pair.first, h.pair.second});
-    std::vector<Point> pts(static_cast<std::size_t>(max_pin) + 1);
-    PointNet scratch{std::span<const Point>(pts)};
-    auto S = session(scratch.nl, core_only({}));
-    ledger_upload(S->s, weights);
+    std::size_t cap = 2; // (pin ids index the ledger only: a power-of-two capacity keeps one scratch session)
+    while (cap < static_cast<std::size_t>(max_pin) + 1) cap *= 2;
+    std::vector<Point> pts(cap);
+    tdpg_session* S = scratch_session(std::span<const Point>(pts));
+    ledger_upload(S, weights);
     std::vector<int32_t> a, b;
     std::vector<double> sl;
     for (const auto& h : hits) a.push_back(h.pair.first), b.push_back(h.pair.second), sl.push_back(h.path_slack);
-    ck(tdpg_pp_update(S->s, static_cast<int64_t>(a.size()), a.data(), b.data(), sl.data(), wns, w0, w1));
-    weights = ledger_download(S->s);
-    std::lock_guard<std::mutex> lock(g_mu);
-    g_cache.erase(&scratch.nl);
+    ck(tdpg_pp_update(S, static_cast<int64_t>(a.size()), a.data(), b.data(), sl.data(), wns, w0, w1));
+    weights = ledger_download(S);
 }
 
 PinPairLossResult pin_pair_loss(const PinPairWeights& weights, const PinPositions& pins, std::size_t num_pins,
@@ -521,14 +561,11 @@ PinPairLossResult pin_pair_loss(const PinPairWeights& weights, const PinPosition
     PinPairLossResult out;
     out.d_pin.assign(num_pins, Point{});
     if (weights.empty() || pins.empty()) return out;
-    PointNet scratch{std::span<const Point>(pins.data(), pins.size())};
-    auto S = session(scratch.nl, core_only({}));
-    ledger_upload(S->s, weights);
+    tdpg_session* S = scratch_session(std::span<const Point>(pins.data(), pins.size()));
+    ledger_upload(S, weights);
     std::vector<double> d(2 * pins.size());
-    ck(tdpg_pp_loss(S->s, kind == PairLossKind::Linear ? 1 : 0, &out.value, d.data()));
+    ck(tdpg_pp_loss(S, kind == PairLossKind::Linear ? 1 : 0, &out.value, d.data()));
     for (std::size_t p = 0; p < std::min(num_pins, pins.size()); ++p) out.d_pin[p] = Point{d[2 * p], d[2 * p + 1]};
-    std::lock_guard<std::mutex> lock(g_mu);
-    g_cache.erase(&scratch.nl);
     return out;
 }
 
@@ -538,29 +575,23 @@ NetTermGrad wa_wirelength(std::span<const Point> pin_pos, double gamma)
     NetTermGrad out;
     out.d_pin.assign(pin_pos.size(), Point{});
     if (pin_pos.size() < 2) return out;
-    PointNet scratch{pin_pos};
-    auto S = session(scratch.nl, core_only({}));
+    tdpg_session* S = scratch_session(pin_pos);
     double wl = 0.0, hp = 0.0;
     std::vector<double> g(2 * pin_pos.size());
-    ck(tdpg_wirelength(S->s, gamma, nullptr, &wl, &hp, g.data()));
+    ck(tdpg_wirelength(S, gamma, nullptr, &wl, &hp, g.data()));
     out.value = wl;
     for (std::size_t i = 0; i < pin_pos.size(); ++i) out.d_pin[i] = Point{g[2 * i], g[2 * i + 1]};
-    std::lock_guard<std::mutex> lock(g_mu);
-    g_cache.erase(&scratch.nl);
     return out;
 }
 
 double hpwl_net(std::span<const Point> pin_pos)
 {
     if (pin_pos.size() < 2) return 0.0;
-    PointNet scratch{pin_pos};
-    auto S = session(scratch.nl, core_only({}));
+    tdpg_session* S = scratch_session(pin_pos);
     double h = 0.0;
     std::vector<double> xy(2 * pin_pos.size());
     for (std::size_t i = 0; i < pin_pos.size(); ++i) xy[2 * i] = pin_pos[i].x, xy[2 * i + 1] = pin_pos[i].y;
-    ck(tdpg_hpwl_pins(S->s, xy.data(), &h));
-    std::lock_guard<std::mutex> lock(g_mu);
-    g_cache.erase(&scratch.nl);
+    ck(tdpg_hpwl_pins(S, xy.data(), &h));
     return h;
 }
 
@@ -634,17 +665,193 @@ std::string metrics_to_csv(const MetricTrace& trace)
 }
 
 std::string weights_to_json(const PinPairWeights& weights, const Netlist& nl)
-{
-    std::string out = "{\n  \"pairs\": [";
-    bool first = true;
+{ // placer.cpp:486-499: {pairs:[{a,b,weight}]} with pin names, in pin-id order
+    nlohmann::json arr = nlohmann::json::array();
     for (const auto& [pr, w] : weights) {
-        out += first ? "\n" : ",\n";
-        first = false;
-        out += "    {\n      \"a\": \"" + nl.pins[static_cast<std::size_t>(pr.first)].name + "\",\n      \"b\": \"" +
-               nl.pins[static_cast<std::size_t>(pr.second)].name + "\",\n      \"weight\": " + fmt17(w) + "\n    }";
+        nlohmann::json item;
+        item["a"] = nl.pins[static_cast<std::size_t>(pr.first)].name;
+        item["b"] = nl.pins[static_cast<std::size_t>(pr.second)].name;
+        item["weight"] = w;
+        arr.push_back(item);
     }
-    out += weights.empty() ? "]\n}\n" : "\n  ]\n}\n";
-    return out;
+    nlohmann::json j;
+    j["pairs"] = arr;
+    return j.dump(2) + "\n";
+}
+
+// ---- configuration I/O (placer.cpp:22-232, the reference's rules and messages) -------------------------
+namespace {
+using nlohmann::json;
+
+void reject_unknown_keys(const json& obj, std::initializer_list<const char*> allowed)
+{
+    for (auto it = obj.begin(); it != obj.end(); ++it)
+        if (std::none_of(allowed.begin(), allowed.end(), [&](const char* k) { return it.key() == k; }))
+            throw ParseError("config: unknown key \"" + it.key() + "\"");
+}
+
+template <typename T, typename Pred>
+void get_field(const json& j, const char* key, T& out, Pred ok, const char* what)
+{
+    if (!j.contains(key)) return;
+    if (!ok(j[key])) throw ParseError(std::string("config: \"") + key + "\" must be " + what);
+    out = j[key].get<T>();
+}
+
+void require_positive(double v, const char* what)
+{
+    if (!(v > 0.0)) throw ValidationError(std::string("config: ") + what + " must be > 0");
+}
+
+void validate_config(const OptimizerConfig& c)
+{ // placer.cpp:68-90
+    if (c.grid_nx < 1 || c.grid_ny < 1) throw ValidationError("config: density grid must be at least 1x1");
+    require_positive(c.target_density, "target_density");
+    require_positive(c.gamma_frac, "gamma_frac");
+    if (c.beta < 0.0) throw ValidationError("config: beta must be >= 0");
+    if (c.m < 1) throw ValidationError("config: m must be >= 1");
+    require_positive(c.w0, "w0");
+    if (c.w1 < 0.0) throw ValidationError("config: w1 must be >= 0");
+    if (c.timing_start_iter < 0) throw ValidationError("config: timing_start_iter must be >= 0");
+    if (c.k < 1) throw ValidationError("config: k must be >= 1");
+    if (c.max_iters < 0) throw ValidationError("config: max_iters must be >= 0");
+    if (c.stop_overflow < 0.0) throw ValidationError("config: stop_overflow must be >= 0");
+    require_positive(c.mu, "mu");
+    require_positive(c.lambda_max, "lambda_max");
+    require_positive(c.step0_frac, "step0_frac");
+    if (!(c.step_decay > 0.0 && c.step_decay <= 1.0)) throw ValidationError("config: step_decay must be in (0, 1]");
+    if (!(c.adam_beta1 >= 0.0 && c.adam_beta1 < 1.0) || !(c.adam_beta2 >= 0.0 && c.adam_beta2 < 1.0))
+        throw ValidationError("config: adam betas must be in [0, 1)");
+    require_positive(c.adam_eps, "adam_eps");
+    if (c.init_jitter_frac < 0.0) throw ValidationError("config: init_jitter_frac must be >= 0");
+    if (c.threads < 1) throw ValidationError("config: threads must be >= 1");
+}
+} // namespace
+
+OptimizerConfig config_from_json(const std::string& text)
+{
+    json j;
+    try {
+        j = json::parse(text);
+    } catch (const json::parse_error& e) {
+        throw ParseError(std::string("config: ") + e.what());
+    }
+    if (!j.is_object()) throw ParseError("config: expected a JSON object");
+    reject_unknown_keys(j, {"name", "gamma_frac", "grid_nx", "grid_ny", "target_density", "beta", "pp_loss",
+                            "net_weighting", "m", "w0", "w1", "timing_start_iter", "extraction", "k", "max_iters",
+                            "stop_overflow", "mu", "lambda0", "lambda_max", "step0_frac", "step_decay", "adam_beta1",
+                            "adam_beta2", "adam_eps", "seed", "init_jitter_frac", "threads"});
+    const auto num = [](const json& v) { return v.is_number(); };
+    const auto integer = [](const json& v) { return v.is_number_integer(); };
+    const auto boolean = [](const json& v) { return v.is_boolean(); };
+    const auto str = [](const json& v) { return v.is_string(); };
+    OptimizerConfig c;
+    get_field(j, "name", c.name, str, "a string"); // (the reference's order: the first bad key is reported)
+    get_field(j, "gamma_frac", c.gamma_frac, num, "a number");
+    get_field(j, "grid_nx", c.grid_nx, integer, "an integer");
+    get_field(j, "grid_ny", c.grid_ny, integer, "an integer");
+    get_field(j, "target_density", c.target_density, num, "a number");
+    get_field(j, "beta", c.beta, num, "a number");
+    get_field(j, "mu", c.mu, num, "a number");
+    get_field(j, "m", c.m, integer, "an integer");
+    get_field(j, "w0", c.w0, num, "a number");
+    get_field(j, "w1", c.w1, num, "a number");
+    get_field(j, "timing_start_iter", c.timing_start_iter, integer, "an integer");
+    get_field(j, "k", c.k, integer, "an integer");
+    get_field(j, "max_iters", c.max_iters, integer, "an integer");
+    get_field(j, "stop_overflow", c.stop_overflow, num, "a number");
+    get_field(j, "lambda_max", c.lambda_max, num, "a number");
+    get_field(j, "step0_frac", c.step0_frac, num, "a number");
+    get_field(j, "step_decay", c.step_decay, num, "a number");
+    get_field(j, "adam_beta1", c.adam_beta1, num, "a number");
+    get_field(j, "adam_beta2", c.adam_beta2, num, "a number");
+    get_field(j, "adam_eps", c.adam_eps, num, "a number");
+    get_field(j, "init_jitter_frac", c.init_jitter_frac, num, "a number");
+    get_field(j, "threads", c.threads, integer, "an integer");
+    get_field(j, "net_weighting", c.net_weighting, boolean, "a boolean");
+    if (j.contains("seed")) {
+        if (!j["seed"].is_number_unsigned() && !j["seed"].is_number_integer())
+            throw ParseError("config: \"seed\" must be an integer");
+        c.seed = j["seed"].get<std::uint64_t>();
+    }
+    if (j.contains("pp_loss")) {
+        std::string s;
+        get_field(j, "pp_loss", s, str, "a string");
+        if (s == "quadratic") c.pp_loss = PairLossKind::Quadratic;
+        else if (s == "linear") c.pp_loss = PairLossKind::Linear;
+        else throw ParseError("config: pp_loss must be \"quadratic\" or \"linear\"");
+    }
+    if (j.contains("extraction")) {
+        std::string s;
+        get_field(j, "extraction", s, str, "a string");
+        if (s == "endpoint") c.extraction = ExtractionPolicy::Endpoint;
+        else if (s == "topn") c.extraction = ExtractionPolicy::TopN;
+        else throw ParseError("config: extraction must be \"endpoint\" or \"topn\"");
+    }
+    if (j.contains("lambda0")) {
+        const char* msg = "config: lambda0 must be \"auto\" or a positive number";
+        if (j["lambda0"].is_string()) {
+            if (j["lambda0"].get<std::string>() != "auto") throw ParseError(msg);
+            c.lambda0 = 0.0;
+        } else if (j["lambda0"].is_number()) {
+            c.lambda0 = j["lambda0"].get<double>();
+            if (!(c.lambda0 > 0.0)) throw ParseError(msg);
+        } else {
+            throw ParseError(msg);
+        }
+    }
+    validate_config(c);
+    return c;
+}
+
+std::string config_to_json(const OptimizerConfig& c)
+{
+    json j;
+    j["name"] = c.name;
+    j["gamma_frac"] = c.gamma_frac;
+    j["grid_nx"] = c.grid_nx;
+    j["grid_ny"] = c.grid_ny;
+    j["target_density"] = c.target_density;
+    j["beta"] = c.beta;
+    j["pp_loss"] = c.pp_loss == PairLossKind::Quadratic ? "quadratic" : "linear";
+    j["net_weighting"] = c.net_weighting;
+    j["m"] = c.m;
+    j["w0"] = c.w0;
+    j["w1"] = c.w1;
+    j["timing_start_iter"] = c.timing_start_iter;
+    j["extraction"] = c.extraction == ExtractionPolicy::Endpoint ? "endpoint" : "topn";
+    j["k"] = c.k;
+    j["max_iters"] = c.max_iters;
+    j["stop_overflow"] = c.stop_overflow;
+    j["mu"] = c.mu;
+    if (c.lambda0 > 0.0) j["lambda0"] = c.lambda0;
+    else j["lambda0"] = "auto";
+    j["lambda_max"] = c.lambda_max;
+    j["step0_frac"] = c.step0_frac;
+    j["step_decay"] = c.step_decay;
+    j["adam_beta1"] = c.adam_beta1;
+    j["adam_beta2"] = c.adam_beta2;
+    j["adam_eps"] = c.adam_eps;
+    j["seed"] = c.seed;
+    j["init_jitter_frac"] = c.init_jitter_frac;
+    j["threads"] = c.threads;
+    return j.dump(2) + "\n";
+}
+
+OptimizerConfig load_config(const std::string& path)
+{
+    std::ifstream in(path);
+    if (!in) throw ParseError("cannot open config file: " + path);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    return config_from_json(ss.str());
+}
+
+void save_config(const OptimizerConfig& config, const std::string& path)
+{
+    std::ofstream out(path);
+    if (!out) throw ParseError("cannot write config file: " + path);
+    out << config_to_json(config);
 }
 
 ObjectiveResult objective_and_gradient(const Netlist& nl, const std::vector<Point>& cell_pos, const DensityGrid& grid,

@@ -55,6 +55,9 @@ def test_ref_place_bench_is_run_placement_bitwise():
     assert np.array_equal(pb["positions"], ref["positions"])
     assert (pb["tns"], pb["wns"], pb["hpwl"]) == (ref["tns"], ref["wns"], ref["hpwl"])
     assert pb["ledger_pairs"] == ref["ledger"][0].size > 0
+    for x, y in zip(pb["trace"], ref["trace"]):  # TraceRow by TraceRow
+        assert (x.iter, bool(x.has_timing), x.hpwl, x.overflow) == (y.iter, y.has_timing, y.hpwl, y.overflow)
+        assert (x.tns, x.wns, x.pp_term, x.lambda_) == (y.tns, y.wns, y.pp_term, y.lambda_)
     # refreshes exactly on the schedule, each extracting paths
     it = np.nonzero(pb["refresh_ms"] > 0)[0]
     assert list(it) == list(range(a.warmup, a.warmup + a.steps, a.m))

@@ -152,17 +152,48 @@ def test_coarse_trajectory_tracks_reference_tightly():
 
 def test_place_10k_config_parity(design_10k):
     """configs[0]: 10K cells, 200 GP iterations, timing from iter 100 every 15, grid 64^2.
-    Final TNS / WNS / HPWL within 1% of the oracle's run_placement."""
+    Final TNS / WNS / HPWL within 1% of the oracle's run_placement; the timing rounds that see
+    violations (iterations 160-190 here: the placement is still spreading at 200 iterations, so the
+    final STA of this config passes) compared row by row."""
     cfg = {"max_iters": 200, "timing_start_iter": 100, "m": 15, "grid_nx": 64, "grid_ny": 64, "seed": 1}
     ps = Session(design_10k).place(cfg)
     po = Oracle(design_10k).place(cfg)
     assert ps["iterations"] == po["iterations"] == 200
     for k in ("tns", "wns", "hpwl"):
         assert abs(ps[k] - po[k]) <= 0.01 * abs(po[k]), (k, ps[k], po[k])
-    # trace rows: every row's hpwl / overflow track the oracle
+    # trace rows: every row's hpwl / overflow track the oracle; TNS / WNS of every timing row
+    violated = 0
     for rs, ro in zip(ps["trace"], po["trace"]):
         assert rs.has_timing == ro.has_timing
         assert abs(rs.hpwl - ro.hpwl) <= 0.01 * ro.hpwl
+        if ro.has_timing:
+            violated += ro.wns < 0
+            assert abs(rs.tns - ro.tns) <= 0.01 * abs(ro.tns), (rs.iter, rs.tns, ro.tns)
+            assert abs(rs.wns - ro.wns) <= 0.01 * abs(ro.wns), (rs.iter, rs.wns, ro.wns)
+    assert violated >= 2, "configs[0] never violated: the TNS comparison would be vacuous"
+
+
+def test_place_10k_violated_start_parity(design_10k):
+    """configs[0] size with the bench's start (bench.py make_design): clock calibrated at the jittered
+    start so 70% of the endpoints fail, timing from the first iteration; 200 iterations.  Every timing
+    row violates, final TNS / WNS / HPWL within 1%."""
+    d = design_10k.copy()
+    s = Session(d)
+    s.engine_init({"max_iters": 1, "seed": 1, "grid_nx": 64, "grid_ny": 64})
+    xy0 = s.positions()
+    arr = s.sta(xy0)["arr"][d.endpoints]
+    d.positions, d.pos_explicit = xy0, np.ones(d.n_cells, np.uint8)
+    d.clock_period = float(np.sort(arr)[int(round(0.3 * arr.size))])
+    cfg = {"max_iters": 200, "timing_start_iter": 0, "m": 15, "grid_nx": 64, "grid_ny": 64, "seed": 1}
+    ps, po = Session(d).place(cfg), Oracle(d).place(cfg)
+    assert ps["iterations"] == po["iterations"] == 200
+    rows = [(rs, ro) for rs, ro in zip(ps["trace"], po["trace"]) if ro.has_timing]
+    assert len(rows) == 14 and all(ro.wns < 0 for _, ro in rows)
+    for rs, ro in rows:
+        assert abs(rs.tns - ro.tns) <= 0.01 * abs(ro.tns), (rs.iter, rs.tns, ro.tns)
+    assert po["wns"] < 0
+    for k in ("tns", "wns", "hpwl"):
+        assert abs(ps[k] - po[k]) <= 0.01 * abs(po[k]), (k, ps[k], po[k])
 
 
 def test_place_small_trace_tight():
@@ -423,8 +454,8 @@ def test_repeated_runs_follow_changed_constraints():
     cfg = {"grid_nx": 32, "grid_ny": 32, "m": 5, "timing_start_iter": 0, "max_iters": 30, "seed": 4}
     s = Session(d)
     s.place(cfg)
-    for clock, r, c in ((d.clock_period * 0.7, d.r_unit, d.c_unit), (d.clock_period, d.r_unit * 2, d.c_unit),
-                        (d.clock_period, d.r_unit, d.c_unit * 0.5)):
+    tight = d.clock_period * 0.05  # (violated from the clumped start on)
+    for clock, r, c in ((tight, d.r_unit, d.c_unit), (tight, d.r_unit * 2, d.c_unit), (tight, d.r_unit, d.c_unit * 0.5)):
         s.set_constraints(clock, r, c)
         got = s.place(cfg)
         d2 = d.copy()
