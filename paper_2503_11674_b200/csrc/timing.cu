@@ -1584,6 +1584,11 @@ __global__ void k_pick_class(const long long* __restrict__ n, SizeClasses sc, cu
 // graph stays host-sync-free); eagerly, body runs over the full capacity.
 static bool size_classes_apply(tdpg_session* s, long long cap)
 {
+    static const bool off = [] { // TDPG_NO_COND=1: full-capacity bodies (profilers that skip conditional graphs)
+        const char* e = std::getenv("TDPG_NO_COND");
+        return e && std::atoi(e) != 0;
+    }();
+    if (off) return false;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(s->st, &cs));
     return cs == cudaStreamCaptureStatusActive && cap >= 64;
