@@ -95,7 +95,7 @@ typedef struct tdpg_config {
     int32_t m;
     double w0, w1;
     int32_t timing_start_iter;
-    int32_t extraction;        /* 0 endpoint (the only policy on device yet)  */
+    int32_t extraction;        /* 0 endpoint, 1 topn (both on the device)     */
     int32_t k;
     int32_t max_iters;
     double stop_overflow;

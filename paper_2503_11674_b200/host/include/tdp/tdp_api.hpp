@@ -194,7 +194,7 @@ class PathEnumerator {
         double delay = 0.0;
         std::vector<int> pins;
     };
-    // rank 0 only on the device (rank > 0: std::logic_error)
+    // any rank: rank 0 from the k = 1 backtrace, rank > 0 from the device k-best lists (csrc/kpaths.cu)
     const Record* path_to(int pin, std::size_t rank);
 
   private:

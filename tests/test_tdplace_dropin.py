@@ -1,6 +1,6 @@
 """The reference's Python API (tdplace) as a drop-in: the reference's own smoke tests
 (proj/tests/python/test_smoke.py:42-113) restated against paper_2503_11674_b200.tdplace.
-compare_csv / render_svg are not on the device."""
+compare_csv runs on device sessions; render_svg is out of scope."""
 import pytest
 
 from paper_2503_11674_b200 import tdplace
