@@ -220,6 +220,8 @@ struct tdpg_session {
     tdpg::DBuf<double> eh_slack;
     tdpg::DBuf<long long> ex_counts;                 // n_paths, path pins, hits of the last refresh
     tdpg::DBuf<unsigned long long> q_count;          // pairs in the dense ledger
+    tdpg::DBuf<long long> ld_long;                   // ledger update: starts of long hit runs
+    tdpg::DBuf<unsigned long long> ld_nlong;         // ... and their count
     long long hcap = 0;
 
     // sort / scan scratch
@@ -290,6 +292,28 @@ void dense_ledger_to_sorted(tdpg_session* s);
 void extract_endpoint_dev(tdpg_session* s, int n);
 void resolve_ties_dev(tdpg_session* s);
 void ledger_update_dev(tdpg_session* s, double wns, double w0, double w1, bool hits_all_violated);
+// dense-ledger update (update_pair_weights) over hits sorted stably by sink pin (timing.cu)
+struct LedgerArgs {
+    const long long* n_hits; // device hit count (engine refresh) or nullptr: H
+    long long H;
+    const double* sta_out;
+    const Ctrl* ctrl;
+    bool gen;                // k > 1 / topn refresh (active while not stopped and wns < 0)
+    const unsigned* hk;
+    const int* hidx;
+    const double* hslack;
+    double w0, w1;
+    double* dl_w;
+    double* ppw_e;
+    const int* pin_entry;
+    const int* pin_loc;
+    uint32_t* pp_mask;
+    unsigned long long* q_count;
+    long long* long_runs;
+    unsigned long long* n_long;
+};
+void launch_ledger_update(tdpg_session* s, long long cap, const LedgerArgs& a);
+void ledger_reserve(tdpg_session* s, long long cap);
 void net_weights_dev(tdpg_session* s);
 int sorted_violated(tdpg_session* s);
 

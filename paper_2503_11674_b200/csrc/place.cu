@@ -657,33 +657,6 @@ __global__ void k_refresh_begin_gen(const double* sta_out, Ctrl* ctrl, double* t
     ctrl->engaged = 1;
 }
 
-__global__ void k_ledger_dense_gen(long long H, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
-                                   const unsigned* __restrict__ hk, const int* __restrict__ hidx,
-                                   const double* __restrict__ hslack, double w0, double w1, double* __restrict__ dl_w,
-                                   double* __restrict__ ppw_e, const int* __restrict__ pin_entry,
-                                   const int* __restrict__ pin_loc, uint32_t* __restrict__ pp_mask,
-                                   unsigned long long* __restrict__ q_count)
-{ // update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger, hits sorted stably by sink pin
-    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= H || ctrl->stopped || !(sta_out[1] < 0.0)) return;
-    const unsigned key = hk[i];
-    if (key == 0xFFFFFFFFu || (i > 0 && hk[i - 1] == key)) return;
-    const double wns = sta_out[1];
-    const int v = static_cast<int>(key);
-    double w = dl_w[v];
-    const bool fresh = !(w > 0.0);
-    long long j = i;
-    if (fresh) w = w0, ++j;
-    for (; j < H && hk[j] == key; ++j) w += w1 * (hslack[hidx[j]] / wns);
-    dl_w[v] = w;
-    ppw_e[pin_entry[v]] = w;
-    if (fresh) {
-        const int loc = pin_loc[v];
-        if (loc >= 0) atomicOr(&pp_mask[loc >> 3], 1u << (loc & 7));
-        atomicAdd(q_count, 1ull);
-    }
-}
-
 void net_weights_engine(tdpg_session* s, const Ctrl* ctrl);
 
 // Timing round with k > 1 or the topn policy (placer.cpp:415-435): STA graph, then the k-best
@@ -714,11 +687,14 @@ void timing_refresh_general(tdpg_session* s)
         E.paths_host += s->n_paths, E.path_pins_host += s->n_path_pins;
         const long long H = s->n_hits;
         if (H > 0) {
-            k_ledger_dense_gen<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(
-                H, s->sta_out, E.ctrl, s->kh_key_s, s->kh_idx_s, s->hit_slack, E.cfg.w0, E.cfg.w1, s->dl_w, s->ppw_e,
-                s->pin_entry, s->pin_loc, s->pp_mask, s->q_count);
-            CK_LAUNCH();
-            ++E.kernel_launches;
+            ledger_reserve(s, H);
+            LedgerArgs la{};
+            la.n_hits = nullptr, la.H = H, la.sta_out = s->sta_out, la.ctrl = E.ctrl, la.gen = true;
+            la.hk = s->kh_key_s, la.hidx = s->kh_idx_s, la.hslack = s->hit_slack, la.w0 = E.cfg.w0;
+            la.w1 = E.cfg.w1, la.dl_w = s->dl_w, la.ppw_e = s->ppw_e, la.pin_entry = s->pin_entry;
+            la.pin_loc = s->pin_loc, la.pp_mask = s->pp_mask, la.q_count = s->q_count;
+            launch_ledger_update(s, H, la);
+            E.kernel_launches += 2;
         }
     }
     if (E.cfg.net_weighting) {
@@ -752,8 +728,8 @@ void timing_refresh(tdpg_session* s)
     CK(cudaEventRecord(ev.second, s->st));
     E.refresh_ev.push_back(ev);
     // our kernels: pin_xy, 2 per level, slack keys, sta final, begin, ties, bt count, fill, bt write,
-    // counts, violated count + two size-class picks, ledger (+ net weights)
-    E.kernel_launches += 2LL * s->L + 13 + (E.cfg.net_weighting ? 1 : 0);
+    // counts, violated count + two size-class picks, ledger short + long runs (+ net weights)
+    E.kernel_launches += 2LL * s->L + 14 + (E.cfg.net_weighting ? 1 : 0);
     ++E.refreshes;
     if (s->round_cb) { // TimingRoundObserver (placer.cpp:434): this round's annotation and report
         sta_materialize_pins(s); // the observer may read per-pin timing

@@ -1432,33 +1432,116 @@ __global__ void k_fill_hit_pad(long long cap, const long long* __restrict__ n_hi
 
 // update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin;
 // the head of each group applies the group's additions in hit order.
-__global__ void k_ledger_dense(long long cap, const long long* __restrict__ n_hits, const double* __restrict__ sta_out,
-                               const Ctrl* __restrict__ ctrl, const unsigned* __restrict__ hk,
-                               const int* __restrict__ hidx, const double* __restrict__ hslack, double w0, double w1,
-                               double* __restrict__ dl_w, double* __restrict__ ppw_e, const int* __restrict__ pin_entry,
-                               const int* __restrict__ pin_loc, uint32_t* __restrict__ pp_mask,
-                               unsigned long long* __restrict__ q_count)
+// update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin, so a
+// pair's hits are one contiguous run in hit order and its weight is the serial sum over that run (kept
+// serial: bitwise the reference's left-to-right additions).  A run start with at most kLedRun hits is
+// summed by its own thread; longer runs (a pin shared by thousands of critical paths — a single thread
+// walking one took 1.7 ms of a 1M refresh) are queued for k_ledger_long, where a block gathers and
+// scales 256 terms at a time in parallel (double-buffered) and one thread adds them in order.
+constexpr int kLedRun = 32;
+constexpr int kLedBlock = 256;
+constexpr int kLedLongBlocks = 148 * 2;
+
+__device__ __forceinline__ void ledger_store(const LedgerArgs& a, int v, double w, bool fresh)
+{
+    a.dl_w[v] = w;
+    a.ppw_e[a.pin_entry[v]] = w;
+    if (fresh) {
+        const int loc = a.pin_loc[v];
+        if (loc >= 0) atomicOr(&a.pp_mask[loc >> 3], 1u << (loc & 7));
+        atomicAdd(a.q_count, 1ull);
+    }
+}
+
+__device__ __forceinline__ long long ledger_hits(const LedgerArgs& a)
+{
+    return a.n_hits ? *a.n_hits : a.H;
+}
+
+__device__ __forceinline__ bool ledger_active(const LedgerArgs& a)
+{
+    return a.gen ? !(a.ctrl->stopped) && a.sta_out[1] < 0.0 : refresh_active(a.sta_out, a.ctrl);
+}
+
+__global__ void k_ledger_dense(long long cap, LedgerArgs a)
 {
     const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= cap || !refresh_active(sta_out, ctrl)) return;
-    const long long H = *n_hits; // (only the hits are sorted; the tail past them is stale)
+    if (i >= cap || !ledger_active(a)) return;
+    const long long H = ledger_hits(a); // (only the hits are sorted; the tail past them is stale)
     if (i >= H) return;
-    const unsigned key = hk[i];
-    if (key == 0xFFFFFFFFu || (i > 0 && hk[i - 1] == key)) return;
-    const double wns = sta_out[1];
+    const unsigned key = a.hk[i];
+    if (key == 0xFFFFFFFFu || (i > 0 && a.hk[i - 1] == key)) return;
+    if (i + kLedRun < H && a.hk[i + kLedRun] == key) { // long run: k_ledger_long
+        a.long_runs[atomicAdd(a.n_long, 1ull)] = i;
+        return;
+    }
+    const double wns = a.sta_out[1];
     const int v = static_cast<int>(key);
-    double w = dl_w[v];
+    double w = a.dl_w[v];
     const bool fresh = !(w > 0.0); // weights start at w0 > 0 and never decrease
     long long j = i;
-    if (fresh) w = w0, ++j;
-    for (; j < H && hk[j] == key; ++j) w += w1 * (hslack[hidx[j]] / wns);
-    dl_w[v] = w;
-    ppw_e[pin_entry[v]] = w;
-    if (fresh) {
-        const int loc = pin_loc[v];
-        if (loc >= 0) atomicOr(&pp_mask[loc >> 3], 1u << (loc & 7));
-        atomicAdd(q_count, 1ull);
+    if (fresh) w = a.w0, ++j;
+    for (; j < H && a.hk[j] == key; ++j) w += a.w1 * (a.hslack[a.hidx[j]] / wns);
+    ledger_store(a, v, w, fresh);
+}
+
+__global__ void __launch_bounds__(kLedBlock) k_ledger_long(LedgerArgs a)
+{
+    __shared__ double term[2][kLedBlock];
+    if (!ledger_active(a)) return;
+    const long long H = ledger_hits(a);
+    const double wns = a.sta_out[1];
+    const long long n_runs = static_cast<long long>(*a.n_long);
+    const int t = threadIdx.x;
+    for (long long r = blockIdx.x; r < n_runs; r += gridDim.x) {
+        const long long i = a.long_runs[r];
+        const unsigned key = a.hk[i];
+        const int v = static_cast<int>(key);
+        double w = a.dl_w[v]; // (read by every thread; only thread 0 uses it)
+        const bool fresh = !(w > 0.0);
+        if (fresh) w = a.w0;
+        long long base = fresh ? i + 1 : i;
+        auto gather = [&](long long b, bool& in) {
+            const long long j = b + t;
+            in = j < H && a.hk[j] == key; // (the run is contiguous: the lanes in it are a prefix)
+            return in ? a.w1 * (a.hslack[a.hidx[j]] / wns) : 0.0;
+        };
+        bool in;
+        term[0][t] = gather(base, in);
+        int n = __syncthreads_count(in), cur = 0;
+        for (;;) {
+            const bool more = n == kLedBlock;
+            double nxt = 0.0;
+            bool in2 = false;
+            if (more) nxt = gather(base + kLedBlock, in2); // next chunk in flight while thread 0 adds
+            if (t == 0)
+                for (int k = 0; k < n; ++k) w += term[cur][k];
+            if (!more) break; // (block-uniform)
+            term[cur ^ 1][t] = nxt;
+            n = __syncthreads_count(in2);
+            base += kLedBlock, cur ^= 1;
+        }
+        if (t == 0) ledger_store(a, v, w, fresh);
+        __syncthreads();
     }
+}
+
+// Both ledger kernels on s->st; the long-run queue is reset in the same stream order (capturable).
+void launch_ledger_update(tdpg_session* s, long long cap, const LedgerArgs& a0)
+{
+    LedgerArgs a = a0;
+    a.long_runs = s->ld_long.p, a.n_long = s->ld_nlong.p;
+    CK(cudaMemsetAsync(s->ld_nlong.p, 0, sizeof(unsigned long long), s->st));
+    k_ledger_dense<<<blocks_for(cap, kBlock), kBlock, 0, s->st>>>(cap, a);
+    CK_LAUNCH();
+    k_ledger_long<<<kLedLongBlocks, kLedBlock, 0, s->st>>>(a);
+    CK_LAUNCH();
+}
+
+void ledger_reserve(tdpg_session* s, long long cap)
+{
+    s->ld_long.reserve(static_cast<size_t>(cap / (kLedRun + 1) + 2));
+    s->ld_nlong.reserve(1);
 }
 
 __global__ void k_extract_counts(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
@@ -1525,6 +1608,7 @@ void refresh_reserve(tdpg_session* s)
     s->ex_tmp_pins.reserve(EP * (L + 1)), s->ex_tmp_keys.reserve(EP * (L / 2 + 2)); // (k_bt_walk slots)
     s->eh_key.reserve(H), s->eh_key_s.reserve(H), s->eh_idx.reserve(H), s->eh_idx_s.reserve(H);
     s->eh_slack.reserve(H);
+    ledger_reserve(s, s->hcap);
     s->ex_counts.reserve(8), s->q_count.reserve(2), s->sta_out.reserve(4);
     const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(s->P, s->EP), kBlock))));
     s->sta_part.reserve(3 * nb + 8);
@@ -1710,10 +1794,14 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
         CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, b, s->eh_key.p, s->eh_key_s.p, s->eh_idx.p, s->eh_idx_s.p,
                                            static_cast<int>(n), 0, kbits, st));
     });
-    k_ledger_dense<<<blocks_for(H, kBlock), kBlock, 0, s->st>>>(H, s->ex_counts.p + 2, s->sta_out, ctrl, s->eh_key_s, s->eh_idx_s,
-                                                                s->eh_slack, w0, w1, s->dl_w, s->ppw_e, s->pin_entry,
-                                                                s->pin_loc, s->pp_mask, s->q_count);
-    CK_LAUNCH();
+    {
+        LedgerArgs la{};
+        la.n_hits = s->ex_counts.p + 2, la.H = H, la.sta_out = s->sta_out, la.ctrl = ctrl, la.gen = false;
+        la.hk = s->eh_key_s, la.hidx = s->eh_idx_s, la.hslack = s->eh_slack, la.w0 = w0, la.w1 = w1;
+        la.dl_w = s->dl_w, la.ppw_e = s->ppw_e, la.pin_entry = s->pin_entry, la.pin_loc = s->pin_loc;
+        la.pp_mask = s->pp_mask, la.q_count = s->q_count;
+        launch_ledger_update(s, H, la);
+    }
     if (net_weighting && s->N) {
         k_net_weights_dev<<<blocks_for(s->N, kBlock), kBlock, 0, s->st>>>(s->N, s->net_start, s->net_pins, s->slack,
                                                                           s->sta_out, ctrl, s->net_w);

@@ -69,6 +69,7 @@ _SIGS = {
     "tdpg_graph_info": (C.c_int, [_P, _I32P, _P]),
     "tdpg_graph_arcs": (C.c_int, [_P, _P, _P, _P, _P]),
     "tdpg_set_positions": (C.c_int, [_P, _P]),
+    "tdpg_set_terminal_positions": (C.c_int, [_P, _P]),
     "tdpg_get_positions": (C.c_int, [_P, _P]),
     "tdpg_pin_positions": (C.c_int, [_P, _P]),
     "tdpg_wirelength": (C.c_int, [_P, C.c_double, _P, _F64P, _F64P, _P]),

@@ -117,3 +117,21 @@ def test_headline_extraction_sweep_bitwise(design, ref):
         assert np.array_equal(x, y)
     assert es["unique_pin_pairs"] == eo["unique_pin_pairs"]
     assert es["unique_endpoints"] == eo["unique_endpoints"]
+
+
+def test_headline_engine_ledger_bitwise(design, ref):
+    """The engine's timing refresh at the bench start (every violated endpoint of the 1M design) builds the
+    dense ledger bitwise equal to update_pair_weights (pin_pairs.cpp:7-15) over the reference's own hits.
+    Pins shared by thousands of critical paths make hit runs far longer than kLedRun, so both the
+    per-thread and the block-cooperative (k_ledger_long) summations are exercised."""
+    cfg = dict(bench.bench_config(ARGS, 1), timing_start_iter=0)
+    ps = Session(design).place(cfg)
+    t = ref.sta(design.positions, threads=NPROC)
+    eo = ref.extract(design.positions, n=0, threads=1)
+    sinks = np.asarray(eo["hits"][1])
+    assert np.max(np.unique(sinks, return_counts=True)[1]) > 1000  # long runs present
+    lo = ref.pp_update(None, eo["hits"], t["wns"])
+    ls = ps["ledger"]
+    assert ls[0].size == lo[0].size > 0
+    for x, y in zip(ls, lo):
+        assert np.array_equal(x, y)
