@@ -220,8 +220,6 @@ struct tdpg_session {
     tdpg::DBuf<double> eh_slack;
     tdpg::DBuf<long long> ex_counts;                 // n_paths, path pins, hits of the last refresh
     tdpg::DBuf<unsigned long long> q_count;          // pairs in the dense ledger
-    tdpg::DBuf<long long> ld_long;                   // ledger update: starts of long hit runs
-    tdpg::DBuf<unsigned long long> ld_nlong;         // ... and their count
     long long hcap = 0;
 
     // sort / scan scratch
@@ -309,11 +307,8 @@ struct LedgerArgs {
     const int* pin_loc;
     uint32_t* pp_mask;
     unsigned long long* q_count;
-    long long* long_runs;
-    unsigned long long* n_long;
 };
 void launch_ledger_update(tdpg_session* s, long long cap, const LedgerArgs& a);
-void ledger_reserve(tdpg_session* s, long long cap);
 void net_weights_dev(tdpg_session* s);
 int sorted_violated(tdpg_session* s);
 

@@ -687,7 +687,6 @@ void timing_refresh_general(tdpg_session* s)
         E.paths_host += s->n_paths, E.path_pins_host += s->n_path_pins;
         const long long H = s->n_hits;
         if (H > 0) {
-            ledger_reserve(s, H);
             LedgerArgs la{};
             la.n_hits = nullptr, la.H = H, la.sta_out = s->sta_out, la.ctrl = E.ctrl, la.gen = true;
             la.hk = s->kh_key_s, la.hidx = s->kh_idx_s, la.hslack = s->hit_slack, la.w0 = E.cfg.w0;

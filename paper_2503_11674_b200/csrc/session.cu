@@ -5,6 +5,8 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 
 #include "engine.cuh"
@@ -166,7 +168,21 @@ void set_density_model(tdpg_session* s, int model)
 
 namespace {
 
-void build_graph(tdpg_session* s)
+// TDPG_TRACE_CREATE=1: wall time of each session-creation phase on stderr
+struct PhaseTimer {
+    bool on = std::getenv("TDPG_TRACE_CREATE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what)
+    {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[tdpg create] %-28s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
+void build_graph(tdpg_session* s, PhaseTimer& pt)
 {
     const int P = s->P, C = s->C;
     s->h_is_source.assign(P, 0);
@@ -218,6 +234,7 @@ void build_graph(tdpg_session* s)
         std::vector<int> fi(in_s.begin(), in_s.end() - 1), fo(out_s.begin(), out_s.end() - 1);
         for (int a = 0; a < A; ++a) in_a[fi[at[a]]++] = a, out_a[fo[af[a]]++] = a;
     }
+    pt.mark("graph: arcs + CSR");
     // Kahn levelization, level = longest path from an in-degree-0 pin (timing_graph.cpp:87-104)
     std::vector<int> indeg(P), order;
     order.reserve(P);
@@ -271,6 +288,7 @@ void build_graph(tdpg_session* s)
         std::vector<int> f(s->h_lvl_start.begin(), s->h_lvl_start.end() - 1);
         for (int p = 0; p < P; ++p) s->h_lvl_pins[f[s->h_level[p]]++] = p;
     }
+    pt.mark("graph: levels");
     // endpoint reachability (timing_graph.cpp:112-135)
     std::vector<uint8_t> reach(P, 0);
     std::vector<int> stack;
@@ -288,6 +306,7 @@ void build_graph(tdpg_session* s)
         if (!reach[e])
             throw Error(TDPG_ERR_VALIDATION, "validation error: endpoint \"" + name(e) + "\" unreachable from every source");
 
+    pt.mark("graph: reachability");
     // device CSR: from-pins of in-arcs / to-pins of out-arcs, ascending arc id
     std::vector<int> in_from(A), out_to(A);
     for (int i = 0; i < A; ++i) in_from[i] = af[in_a[i]], out_to[i] = at[out_a[i]];
@@ -355,6 +374,7 @@ void build_graph(tdpg_session* s)
         s->L_pred.alloc(n), s->L_ak.alloc(n), s->L_rk.alloc(n), s->L_tie.alloc(n);
         s->L_arr.alloc(n), s->L_req.alloc(n), s->L_xy.alloc(n);
     }
+    pt.mark("graph: L-space + uploads");
     s->d_level.upload(s->h_level, s->st);
     std::vector<int> eps(s->h_endpoints);
     std::sort(eps.begin(), eps.end());
@@ -421,7 +441,9 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         cudaGetLastError();
         throw Error(TDPG_ERR_CUDA, "cuda error: no CUDA device available (the tdpg engine has no CPU fallback)");
     }
+    PhaseTimer pt;
     check_netlist(d);
+    pt.mark("check_netlist");
     auto s = std::make_unique<tdpg_session>();
     CK(cudaGetDevice(&s->device));
     CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
@@ -451,7 +473,8 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         s->pin_names.resize(P);
         for (int p = 0; p < P; ++p) s->pin_names[p] = d->pin_names[p] ? d->pin_names[p] : "";
     }
-    build_graph(s.get());
+    pt.mark("streams + host copies");
+    build_graph(s.get(), pt);
 
     // device netlist
     std::vector<double2> wh(C);
@@ -468,6 +491,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     s->is_endpoint.upload(s->h_is_endpoint, s->st);
     s->net_start.upload(s->h_net_start, s->st);
     s->net_pins.upload(s->h_net_pins, s->st);
+    pt.mark("netlist upload");
     // Net-pin entries in the WA layout: nets sorted (stably) by pin count; nets of N = 2..8 pins in
     // blocks of 256, slot-major inside a block (pin j of the block's t-th net at base + j*256 + t, so a
     // warp's loads and stores of one pin slot are contiguous); other nets (class 0) contiguous after.
@@ -555,6 +579,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
             pin_entry[p] = id;
             s->h_pin_net[p] = n;
         }
+    pt.mark("WA layout + pin pairs");
     s->e_cell.upload(e_cell, s->st);
     s->e_off.upload(e_off, s->st);
     // Cell pins on no net still take pin-pair gradient (pin_pairs.cpp:31-34 writes any pin):
@@ -579,6 +604,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     s->cell_ent_start.upload(ces, s->st);
     s->cell_ent.upload(ce, s->st);
 
+    pt.mark("entries + fold CSR");
     // state buffers
     s->cell_xy.alloc(C);
     {   // Opt-in (TDPG_L2_PERSIST=1): an L2 persisting window over the cell positions.  Measured on B200
@@ -615,6 +641,7 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     s->counters.alloc(16);
     s->h_small.reserve(64);
     CK(cudaStreamSynchronize(s->st));
+    pt.mark("state buffers + sync");
     *out = s.release();
     API_END
 }

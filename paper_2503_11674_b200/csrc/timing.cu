@@ -1434,10 +1434,14 @@ __global__ void k_fill_hit_pad(long long cap, const long long* __restrict__ n_hi
 // the head of each group applies the group's additions in hit order.
 // update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin, so a
 // pair's hits are one contiguous run in hit order and its weight is the serial sum over that run (kept
-// serial: bitwise the reference's left-to-right additions).  A run start with at most kLedRun hits is
-// summed by its own thread; longer runs (a pin shared by thousands of critical paths — a single thread
-// walking one took 1.7 ms of a 1M refresh) are queued for k_ledger_long, where a block gathers and
-// scales 256 terms at a time in parallel (double-buffered) and one thread adds them in order.
+// serial: bitwise the reference's left-to-right additions).  Two kernels on two graph branches:
+//  * k_ledger_dense: a run of at most kLedRun hits is summed by the thread at its start — run length
+//    first (keys of one L1 line), then every term's gathers issued together, then the adds;
+//  * k_ledger_long: longer runs (a pin shared by thousands of critical paths; one thread walking one
+//    took 1.7 ms of a 1M refresh).  Each block scans a slice of the hits for long-run starts and sums
+//    each such run cooperatively: 256 terms gathered and scaled in parallel (double-buffered), one
+//    thread adding them in order.  Its critical path is the longest run's add chain, overlapped with
+//    the short runs on the other branch.
 constexpr int kLedRun = 32;
 constexpr int kLedBlock = 256;
 constexpr int kLedLongBlocks = 148 * 2;
@@ -1446,10 +1450,12 @@ __device__ __forceinline__ void ledger_store(const LedgerArgs& a, int v, double 
 {
     a.dl_w[v] = w;
     a.ppw_e[a.pin_entry[v]] = w;
+    // new pairs counted with one atomic per warp (every thread of a first refresh adds one)
+    const unsigned act = __activemask(), fm = __ballot_sync(act, fresh);
     if (fresh) {
         const int loc = a.pin_loc[v];
         if (loc >= 0) atomicOr(&a.pp_mask[loc >> 3], 1u << (loc & 7));
-        atomicAdd(a.q_count, 1ull);
+        if ((threadIdx.x & 31) == __ffs(fm) - 1) atomicAdd(a.q_count, static_cast<unsigned long long>(__popc(fm)));
     }
 }
 
@@ -1463,6 +1469,12 @@ __device__ __forceinline__ bool ledger_active(const LedgerArgs& a)
     return a.gen ? !(a.ctrl->stopped) && a.sta_out[1] < 0.0 : refresh_active(a.sta_out, a.ctrl);
 }
 
+__device__ __forceinline__ bool ledger_long_start(const unsigned* hk, long long i, long long H, unsigned& key)
+{
+    key = hk[i];
+    return key != 0xFFFFFFFFu && (i == 0 || hk[i - 1] != key) && i + kLedRun < H && hk[i + kLedRun] == key;
+}
+
 __global__ void k_ledger_dense(long long cap, LedgerArgs a)
 {
     const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
@@ -1471,77 +1483,98 @@ __global__ void k_ledger_dense(long long cap, LedgerArgs a)
     if (i >= H) return;
     const unsigned key = a.hk[i];
     if (key == 0xFFFFFFFFu || (i > 0 && a.hk[i - 1] == key)) return;
-    if (i + kLedRun < H && a.hk[i + kLedRun] == key) { // long run: k_ledger_long
-        a.long_runs[atomicAdd(a.n_long, 1ull)] = i;
-        return;
-    }
+    int n = 1; // run length, at most kLedRun here (longer runs: k_ledger_long)
+    while (n <= kLedRun && i + n < H && a.hk[i + n] == key) ++n;
+    if (n > kLedRun) return;
     const double wns = a.sta_out[1];
     const int v = static_cast<int>(key);
     double w = a.dl_w[v];
     const bool fresh = !(w > 0.0); // weights start at w0 > 0 and never decrease
-    long long j = i;
-    if (fresh) w = a.w0, ++j;
-    for (; j < H && a.hk[j] == key; ++j) w += a.w1 * (a.hslack[a.hidx[j]] / wns);
+    int k = 0;
+    if (fresh) w = a.w0, k = 1;
+    for (; k < n; k += 8) { // eight terms' gathers in flight, then their adds in hit order
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = k + u < n ? a.hslack[a.hidx[i + k + u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k + u < n) w += a.w1 * (t[u] / wns);
+    }
     ledger_store(a, v, w, fresh);
 }
 
 __global__ void __launch_bounds__(kLedBlock) k_ledger_long(LedgerArgs a)
 {
     __shared__ double term[2][kLedBlock];
+    __shared__ long long found[kLedBlock];
+    __shared__ int n_found;
     if (!ledger_active(a)) return;
     const long long H = ledger_hits(a);
     const double wns = a.sta_out[1];
-    const long long n_runs = static_cast<long long>(*a.n_long);
     const int t = threadIdx.x;
-    for (long long r = blockIdx.x; r < n_runs; r += gridDim.x) {
-        const long long i = a.long_runs[r];
-        const unsigned key = a.hk[i];
-        const int v = static_cast<int>(key);
-        double w = a.dl_w[v]; // (read by every thread; only thread 0 uses it)
-        const bool fresh = !(w > 0.0);
-        if (fresh) w = a.w0;
-        long long base = fresh ? i + 1 : i;
-        auto gather = [&](long long b, bool& in) {
-            const long long j = b + t;
-            in = j < H && a.hk[j] == key; // (the run is contiguous: the lanes in it are a prefix)
-            return in ? a.w1 * (a.hslack[a.hidx[j]] / wns) : 0.0;
-        };
-        bool in;
-        term[0][t] = gather(base, in);
-        int n = __syncthreads_count(in), cur = 0;
-        for (;;) {
-            const bool more = n == kLedBlock;
-            double nxt = 0.0;
-            bool in2 = false;
-            if (more) nxt = gather(base + kLedBlock, in2); // next chunk in flight while thread 0 adds
-            if (t == 0)
-                for (int k = 0; k < n; ++k) w += term[cur][k];
-            if (!more) break; // (block-uniform)
-            term[cur ^ 1][t] = nxt;
-            n = __syncthreads_count(in2);
-            base += kLedBlock, cur ^= 1;
-        }
-        if (t == 0) ledger_store(a, v, w, fresh);
+    const long long slice = (H + gridDim.x - 1) / gridDim.x;
+    const long long lo = blockIdx.x * slice, hi = H < lo + slice ? H : lo + slice;
+    for (long long b0 = lo; b0 < hi; b0 += kLedBlock) {
+        if (t == 0) n_found = 0;
         __syncthreads();
+        unsigned key;
+        if (b0 + t < hi && ledger_long_start(a.hk, b0 + t, H, key)) found[atomicAdd(&n_found, 1)] = b0 + t;
+        __syncthreads();
+        const int nf = n_found;
+        for (int f = 0; f < nf; ++f) { // (the order among runs does not matter: disjoint keys)
+            const long long i = found[f];
+            key = a.hk[i];
+            const int v = static_cast<int>(key);
+            double w = a.dl_w[v]; // (read by every thread; only thread 0 uses it)
+            const bool fresh = !(w > 0.0);
+            if (fresh) w = a.w0;
+            long long base = fresh ? i + 1 : i;
+            auto gather = [&](long long bb, bool& in) {
+                const long long j = bb + t;
+                in = j < H && a.hk[j] == key; // (the run is contiguous: the lanes in it are a prefix)
+                return in ? a.w1 * (a.hslack[a.hidx[j]] / wns) : 0.0;
+            };
+            bool in;
+            term[0][t] = gather(base, in);
+            int n = __syncthreads_count(in), cur = 0;
+            for (;;) {
+                const bool more = n == kLedBlock;
+                double nxt = 0.0;
+                bool in2 = false;
+                if (more) nxt = gather(base + kLedBlock, in2); // next chunk in flight while thread 0 adds
+                if (t == 0) {
+                    int k = 0;
+                    for (; k + 8 <= n; k += 8) {
+                        double r[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) r[u] = term[cur][k + u];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w += r[u];
+                    }
+                    for (; k < n; ++k) w += term[cur][k];
+                }
+                if (!more) break; // (block-uniform)
+                term[cur ^ 1][t] = nxt;
+                n = __syncthreads_count(in2);
+                base += kLedBlock, cur ^= 1;
+            }
+            if (t == 0) ledger_store(a, v, w, fresh);
+            __syncthreads();
+        }
     }
 }
 
-// Both ledger kernels on s->st; the long-run queue is reset in the same stream order (capturable).
-void launch_ledger_update(tdpg_session* s, long long cap, const LedgerArgs& a0)
+// The two ledger kernels as two branches (s->st_req carries the long runs), joined on s->st; capturable.
+void launch_ledger_update(tdpg_session* s, long long cap, const LedgerArgs& a)
 {
-    LedgerArgs a = a0;
-    a.long_runs = s->ld_long.p, a.n_long = s->ld_nlong.p;
-    CK(cudaMemsetAsync(s->ld_nlong.p, 0, sizeof(unsigned long long), s->st));
+    CK(cudaEventRecord(s->ev_sta_fork, s->st));
+    CK(cudaStreamWaitEvent(s->st_req, s->ev_sta_fork, 0));
+    k_ledger_long<<<kLedLongBlocks, kLedBlock, 0, s->st_req>>>(a);
+    CK_LAUNCH();
     k_ledger_dense<<<blocks_for(cap, kBlock), kBlock, 0, s->st>>>(cap, a);
     CK_LAUNCH();
-    k_ledger_long<<<kLedLongBlocks, kLedBlock, 0, s->st>>>(a);
-    CK_LAUNCH();
-}
-
-void ledger_reserve(tdpg_session* s, long long cap)
-{
-    s->ld_long.reserve(static_cast<size_t>(cap / (kLedRun + 1) + 2));
-    s->ld_nlong.reserve(1);
+    CK(cudaEventRecord(s->ev_sta_join, s->st_req));
+    CK(cudaStreamWaitEvent(s->st, s->ev_sta_join, 0));
 }
 
 __global__ void k_extract_counts(int EP, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
@@ -1608,7 +1641,6 @@ void refresh_reserve(tdpg_session* s)
     s->ex_tmp_pins.reserve(EP * (L + 1)), s->ex_tmp_keys.reserve(EP * (L / 2 + 2)); // (k_bt_walk slots)
     s->eh_key.reserve(H), s->eh_key_s.reserve(H), s->eh_idx.reserve(H), s->eh_idx_s.reserve(H);
     s->eh_slack.reserve(H);
-    ledger_reserve(s, s->hcap);
     s->ex_counts.reserve(8), s->q_count.reserve(2), s->sta_out.reserve(4);
     const int nb = std::max(1, std::min(148 * 4, static_cast<int>(blocks_for(std::max(s->P, s->EP), kBlock))));
     s->sta_part.reserve(3 * nb + 8);
