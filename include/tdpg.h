@@ -144,6 +144,18 @@ int tdpg_pin_positions(tdpg_session* s, double* pin_xy);          /* [2*n_pins] 
  * serve repeated per-net calls (wa_wirelength / hpwl_net on terminal pins, wirelength.hpp:21-23). */
 int tdpg_set_terminal_positions(tdpg_session* s, const double* pin_xy);
 
+/* ---- binary design file ------------------------------------------------ */
+/* A scalable SoA file holding what the reference's design JSON holds (design_io.cpp:63-193 reads and
+ * writes that JSON): netlist, constraints, positions and pos_explicit (layout: design.py save_bin).
+ * info: counts = cells, pins, nets, net pins, sources, endpoints; has_pin_names may be NULL.
+ * read: the caller allocates d's arrays from the counts (n_* fields set); the scalars are filled in;
+ * pin names (optional) come back as one NUL-separated blob of at most blob_cap bytes. */
+int tdpg_design_bin_info(const char* path, int64_t counts[6], int32_t* has_pin_names);
+int tdpg_design_bin_read(const char* path, tdpg_netlist* d, double* positions, uint8_t* pos_explicit,
+                         char* pin_name_blob, int64_t blob_cap);
+int tdpg_design_bin_write(const char* path, const tdpg_netlist* d, const double* positions,
+                          const uint8_t* pos_explicit, double default_cell_delay);
+
 /* ---- objective terms (at the session's current positions) ----------- */
 /* wl = sum_e w_e * WA_e, hpwl exact; pin_grad [2*n_pins] (w_e-scaled) may be NULL. */
 int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* wl, double* hpwl,

@@ -115,7 +115,10 @@ struct tdpg_session {
     std::vector<uint8_t> h_cell_fixed, h_pin_dir, h_is_source, h_is_endpoint;
     std::vector<int> h_pin_cell, h_net_start, h_net_pins, h_sources, h_endpoints, h_pin_net, h_pin_entry;
     std::vector<std::string> pin_names;
-    std::vector<int> h_level, h_lvl_start, h_lvl_pins, h_arc_from, h_arc_to, h_arc_kind, h_arc_owner;
+    std::vector<int> h_level, h_lvl_start, h_arc_from, h_arc_to, h_arc_kind, h_arc_owner; // (level / arcs: lazy)
+    bool h_level_valid = false, h_arcs_valid = false;
+    tdpg::DBuf<int> arc_from, arc_to, arc_kind, arc_owner; // arcs by id (timing_graph.cpp:60-77)
+    tdpg::HBuf<int> h_graph_small;
 
     // device netlist
     tdpg::DBuf<double2> cell_xy, cell_wh, anchor, pin_off, e_off;
@@ -263,6 +266,10 @@ namespace tdpg {
 // session.cu
 void upload_positions(tdpg_session* s, const double* xy);
 void refresh_fixed_baseline(tdpg_session* s);
+void build_graph_device(tdpg_session* s); // graph.cu
+void graph_host_level(tdpg_session* s);
+void graph_host_arcs(tdpg_session* s);
+void sta_setup(tdpg_session* s);
 void sta_materialize_pins(tdpg_session* s); // per-pin STA arrays of an L-space-only sweep (timing.cu)
 void place_tail_reserve(tdpg_session* s); // (timing.cu)
 void ensure_grid(tdpg_session* s, int nx, int ny, double td);

@@ -182,206 +182,6 @@ struct PhaseTimer {
     }
 };
 
-void build_graph(tdpg_session* s, PhaseTimer& pt)
-{
-    const int P = s->P, C = s->C;
-    s->h_is_source.assign(P, 0);
-    s->h_is_endpoint.assign(P, 0);
-    for (int v : s->h_sources) s->h_is_source[v] = 1;
-    for (int v : s->h_endpoints) s->h_is_endpoint[v] = 1;
-    // cell_pins, ascending (netlist.cpp:12-14)
-    std::vector<int> cps(C + 1, 0), cp;
-    for (int p = 0; p < P; ++p)
-        if (s->h_pin_cell[p] >= 0) cps[s->h_pin_cell[p] + 1]++;
-    for (int c = 0; c < C; ++c) cps[c + 1] += cps[c];
-    cp.resize(cps[C]);
-    {
-        std::vector<int> f(cps.begin(), cps.end() - 1);
-        for (int p = 0; p < P; ++p)
-            if (s->h_pin_cell[p] >= 0) cp[f[s->h_pin_cell[p]]++] = p;
-    }
-    // arcs: net arcs in (net, sink) order, then cell arcs (cell, input, output) (timing_graph.cpp:60-77)
-    auto& af = s->h_arc_from;
-    auto& at = s->h_arc_to;
-    auto& ak = s->h_arc_kind;
-    auto& ao = s->h_arc_owner;
-    af.clear(), at.clear(), ak.clear(), ao.clear();
-    const size_t reserve = static_cast<size_t>(s->E) * 2 + 16;
-    af.reserve(reserve), at.reserve(reserve), ak.reserve(reserve), ao.reserve(reserve);
-    for (int n = 0; n < s->N; ++n)
-        for (int e = s->h_net_start[n] + 1; e < s->h_net_start[n + 1]; ++e) {
-            af.push_back(s->h_net_pins[s->h_net_start[n]]), at.push_back(s->h_net_pins[e]), ak.push_back(0),
-                ao.push_back(n);
-        }
-    s->A_net = static_cast<int>(af.size());
-    for (int c = 0; c < C; ++c)
-        for (int i = cps[c]; i < cps[c + 1]; ++i) {
-            const int in = cp[i];
-            if (s->h_pin_dir[in] != 0 || s->h_is_endpoint[in]) continue;
-            for (int j = cps[c]; j < cps[c + 1]; ++j) {
-                const int out = cp[j];
-                if (s->h_pin_dir[out] != 1 || s->h_is_source[out]) continue;
-                af.push_back(in), at.push_back(out), ak.push_back(1), ao.push_back(c);
-            }
-        }
-    s->A = static_cast<int>(af.size());
-    s->A_cell = s->A - s->A_net;
-    const int A = s->A;
-    std::vector<int> in_s(P + 1, 0), out_s(P + 1, 0), in_a(A), out_a(A);
-    for (int a = 0; a < A; ++a) in_s[at[a] + 1]++, out_s[af[a] + 1]++;
-    for (int p = 0; p < P; ++p) in_s[p + 1] += in_s[p], out_s[p + 1] += out_s[p];
-    {
-        std::vector<int> fi(in_s.begin(), in_s.end() - 1), fo(out_s.begin(), out_s.end() - 1);
-        for (int a = 0; a < A; ++a) in_a[fi[at[a]]++] = a, out_a[fo[af[a]]++] = a;
-    }
-    pt.mark("graph: arcs + CSR");
-    // Kahn levelization, level = longest path from an in-degree-0 pin (timing_graph.cpp:87-104)
-    std::vector<int> indeg(P), order;
-    order.reserve(P);
-    s->h_level.assign(P, 0);
-    for (int p = 0; p < P; ++p) {
-        indeg[p] = in_s[p + 1] - in_s[p];
-        if (indeg[p] == 0) order.push_back(p);
-    }
-    for (size_t h = 0; h < order.size(); ++h) {
-        const int u = order[h];
-        for (int i = out_s[u]; i < out_s[u + 1]; ++i) {
-            const int v = at[out_a[i]];
-            s->h_level[v] = std::max(s->h_level[v], s->h_level[u] + 1);
-            if (--indeg[v] == 0) order.push_back(v);
-        }
-    }
-    auto name = [&](int p) { return s->pin_names.empty() ? "p" + std::to_string(p) : s->pin_names[p]; };
-    if (static_cast<int>(order.size()) != P) { // report_cycle (timing_graph.cpp:12-45)
-        std::vector<uint8_t> rem(P, 0);
-        int start = -1;
-        for (int p = 0; p < P; ++p)
-            if (indeg[p] > 0) rem[p] = 1, start = p;
-        std::vector<int> seen(P, -1), walk;
-        int cur = start;
-        while (seen[cur] < 0) {
-            seen[cur] = static_cast<int>(walk.size());
-            walk.push_back(cur);
-            for (int i = in_s[cur]; i < in_s[cur + 1]; ++i) {
-                const int u = af[in_a[i]];
-                if (rem[u]) {
-                    cur = u;
-                    break;
-                }
-            }
-        }
-        std::string msg;
-        for (size_t i = static_cast<size_t>(seen[cur]); i < walk.size(); ++i) {
-            if (!msg.empty()) msg += " <- ";
-            msg += name(walk[i]);
-        }
-        throw Error(TDPG_ERR_CYCLE, "validation error: combinational cycle: " + msg);
-    }
-    int max_level = 0;
-    for (int p = 0; p < P; ++p) max_level = std::max(max_level, s->h_level[p]);
-    s->L = max_level + 1;
-    s->h_lvl_start.assign(s->L + 1, 0);
-    for (int p = 0; p < P; ++p) s->h_lvl_start[s->h_level[p] + 1]++;
-    for (int l = 0; l < s->L; ++l) s->h_lvl_start[l + 1] += s->h_lvl_start[l];
-    s->h_lvl_pins.resize(P);
-    {
-        std::vector<int> f(s->h_lvl_start.begin(), s->h_lvl_start.end() - 1);
-        for (int p = 0; p < P; ++p) s->h_lvl_pins[f[s->h_level[p]]++] = p;
-    }
-    pt.mark("graph: levels");
-    // endpoint reachability (timing_graph.cpp:112-135)
-    std::vector<uint8_t> reach(P, 0);
-    std::vector<int> stack;
-    for (int v : s->h_sources)
-        if (!reach[v]) reach[v] = 1, stack.push_back(v);
-    while (!stack.empty()) {
-        const int u = stack.back();
-        stack.pop_back();
-        for (int i = out_s[u]; i < out_s[u + 1]; ++i) {
-            const int v = at[out_a[i]];
-            if (!reach[v]) reach[v] = 1, stack.push_back(v);
-        }
-    }
-    for (int e : s->h_endpoints)
-        if (!reach[e])
-            throw Error(TDPG_ERR_VALIDATION, "validation error: endpoint \"" + name(e) + "\" unreachable from every source");
-
-    pt.mark("graph: reachability");
-    // device CSR: from-pins of in-arcs / to-pins of out-arcs, ascending arc id
-    std::vector<int> in_from(A), out_to(A);
-    for (int i = 0; i < A; ++i) in_from[i] = af[in_a[i]], out_to[i] = at[out_a[i]];
-    s->in_start.upload(in_s, s->st);
-    s->in_from.upload(in_from, s->st);
-    s->out_start.upload(out_s, s->st);
-    s->out_to.upload(out_to, s->st);
-    s->lvl_pins.upload(s->h_lvl_pins, s->st);
-    s->lvl_start.upload(s->h_lvl_start, s->st);
-    {   // push-sweep tables (timing.cu): Output pins and Input pins, each grouped by level (ascending id)
-        std::vector<int> outs, ins;
-        s->h_sta_out_start.assign(s->L + 1, 0), s->h_sta_in_start.assign(s->L + 1, 0);
-        for (int l = 0; l < s->L; ++l) {
-            for (int i = s->h_lvl_start[l]; i < s->h_lvl_start[l + 1]; ++i) {
-                const int p = s->h_lvl_pins[i];
-                (s->h_pin_dir[p] == 1 ? outs : ins).push_back(p);
-            }
-            s->h_sta_out_start[l + 1] = static_cast<int>(outs.size());
-            s->h_sta_in_start[l + 1] = static_cast<int>(ins.size());
-        }
-        if (outs.empty()) outs.push_back(0);
-        if (ins.empty()) ins.push_back(0);
-        s->sta_out_pins.upload(outs, s->st);
-        s->sta_in_pins.upload(ins, s->st);
-        s->sta_akey.alloc(std::max(P, 1)), s->sta_rkey.alloc(std::max(P, 1));
-    }
-    {   // level-major L-space copy of the graph (timing.cu push sweep)
-        std::vector<int> Lpin, Lidx(P);
-        Lpin.reserve(P);
-        s->h_L_in_lo.assign(s->L, 0), s->h_L_in_hi.assign(s->L, 0);
-        for (int l = 0; l < s->L; ++l) {
-            s->h_L_in_lo[l] = static_cast<int>(Lpin.size());
-            for (int i = s->h_lvl_start[l]; i < s->h_lvl_start[l + 1]; ++i)
-                if (s->h_pin_dir[s->h_lvl_pins[i]] != 1) Lpin.push_back(s->h_lvl_pins[i]);
-            s->h_L_in_hi[l] = static_cast<int>(Lpin.size());
-            for (int i = s->h_lvl_start[l]; i < s->h_lvl_start[l + 1]; ++i)
-                if (s->h_pin_dir[s->h_lvl_pins[i]] == 1) Lpin.push_back(s->h_lvl_pins[i]);
-        }
-        for (int i = 0; i < P; ++i) Lidx[Lpin[i]] = i;
-        s->L_of.upload(Lidx.empty() ? std::vector<int>(1, 0) : Lidx, s->st);
-        std::vector<int> Lis(P + 1, 0), Lif, Los(P + 1, 0), Lot, Lcell(P);
-        Lif.reserve(A), Lot.reserve(A);
-        std::vector<uint8_t> Lfl(P);
-        std::vector<double> Lcap(P);
-        std::vector<double2> Loff(P), Lanc(P);
-        for (int i = 0; i < P; ++i) {
-            const int p = Lpin[i];
-            for (int j = in_s[p]; j < in_s[p + 1]; ++j) Lif.push_back(Lidx[in_from[j]]);
-            for (int j = out_s[p]; j < out_s[p + 1]; ++j) Lot.push_back(Lidx[out_to[j]]);
-            Lis[i + 1] = static_cast<int>(Lif.size()), Los[i + 1] = static_cast<int>(Lot.size());
-            Lfl[i] = static_cast<uint8_t>((s->h_is_source[p] ? 1 : 0) | (s->h_is_endpoint[p] ? 2 : 0) |
-                                          (s->h_pin_dir[p] == 1 ? 4 : 0));
-            Lcap[i] = s->h_pin_cap[p], Lcell[i] = s->h_pin_cell[p];
-            Loff[i] = make_double2(s->h_pin_off[2 * p], s->h_pin_off[2 * p + 1]);
-            Lanc[i] = make_double2(s->h_pin_term[2 * p], s->h_pin_term[2 * p + 1]);
-        }
-        if (Lif.empty()) Lif.push_back(0), Lot.push_back(0);
-        if (Lpin.empty()) Lpin.push_back(0), Lcell.push_back(0), Lfl.push_back(0), Lcap.push_back(0.0),
-            Loff.push_back(make_double2(0, 0)), Lanc.push_back(make_double2(0, 0));
-        s->L_pin.upload(Lpin, s->st), s->L_cell.upload(Lcell, s->st), s->L_flags.upload(Lfl, s->st);
-        s->L_in_start.upload(Lis, s->st), s->L_in_from.upload(Lif, s->st);
-        s->L_out_start.upload(Los, s->st), s->L_out_to.upload(Lot, s->st);
-        s->L_cap.upload(Lcap, s->st), s->L_off.upload(Loff, s->st), s->L_anchor.upload(Lanc, s->st);
-        const size_t n = static_cast<size_t>(std::max(P, 1));
-        s->L_pred.alloc(n), s->L_ak.alloc(n), s->L_rk.alloc(n), s->L_tie.alloc(n);
-        s->L_arr.alloc(n), s->L_req.alloc(n), s->L_xy.alloc(n);
-    }
-    pt.mark("graph: L-space + uploads");
-    s->d_level.upload(s->h_level, s->st);
-    std::vector<int> eps(s->h_endpoints);
-    std::sort(eps.begin(), eps.end());
-    s->ep_sorted.upload(eps, s->st);
-    sta_setup(s);
-}
-
 void check_netlist(const tdpg_netlist* d)
 {
     auto bad = [](const std::string& m) { throw Error(TDPG_ERR_VALIDATION, "validation error: " + m); };
@@ -474,8 +274,10 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         for (int p = 0; p < P; ++p) s->pin_names[p] = d->pin_names[p] ? d->pin_names[p] : "";
     }
     pt.mark("streams + host copies");
-    build_graph(s.get(), pt);
-
+    s->h_is_source.assign(P, 0);
+    s->h_is_endpoint.assign(P, 0);
+    for (int v : s->h_sources) s->h_is_source[v] = 1;
+    for (int v : s->h_endpoints) s->h_is_endpoint[v] = 1;
     // device netlist
     std::vector<double2> wh(C);
     for (int c = 0; c < C; ++c) wh[c] = make_double2(s->h_cell_w[c], s->h_cell_h[c]);
@@ -492,6 +294,9 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     s->net_start.upload(s->h_net_start, s->st);
     s->net_pins.upload(s->h_net_pins, s->st);
     pt.mark("netlist upload");
+    build_graph_device(s.get()); // build_timing_graph (timing_graph.cpp:49-138) on the device (graph.cu)
+    sta_setup(s.get());
+    pt.mark("timing graph (device)");
     // Net-pin entries in the WA layout: nets sorted (stably) by pin count; nets of N = 2..8 pins in
     // blocks of 256, slot-major inside a block (pin j of the block's t-th net at base + j*256 + t, so a
     // warp's loads and stores of one pin slot are contiguous); other nets (class 0) contiguous after.
@@ -657,6 +462,7 @@ int tdpg_graph_info(tdpg_session* s, int32_t counts[4], int32_t* level)
 {
     API_BEGIN
     counts[0] = s->A_net, counts[1] = s->A_cell, counts[2] = s->L, counts[3] = s->L - 1;
+    if (level) graph_host_level(s);
     if (level) std::memcpy(level, s->h_level.data(), s->h_level.size() * sizeof(int32_t));
     API_END
 }
@@ -665,6 +471,7 @@ int tdpg_graph_arcs(tdpg_session* s, int32_t* from, int32_t* to, int32_t* kind, 
 {
     API_BEGIN
     const size_t A = static_cast<size_t>(s->A);
+    graph_host_arcs(s);
     if (from) std::memcpy(from, s->h_arc_from.data(), A * sizeof(int32_t));
     if (to) std::memcpy(to, s->h_arc_to.data(), A * sizeof(int32_t));
     if (kind) std::memcpy(kind, s->h_arc_kind.data(), A * sizeof(int32_t));

@@ -475,3 +475,77 @@ class Design:
         clk = z["clock"]
         return cls(**{k: z[k] for k in cls._ARRAYS}, clock_period=float(clk[0]), r_unit=float(clk[1]),
                    c_unit=float(clk[2]), core=tuple(z["core"]))
+
+
+# ---- binary design file (SoA, scalable; the reference's JSON schema does not scale to 1M cells) ----------
+# Layout (little-endian; every section starts 8-byte aligned; mirrored by csrc/design_io.cu):
+#   0   char[8] "TDPGDSN1" | u32 version (1) | u32 flags (bit 0: pin names present)
+#   16  i64 n_cells, n_pins, n_nets, n_net_pins, n_sources, n_endpoints
+#   64  f64 clock_period, r_unit, c_unit, core[4], default_cell_delay
+#   128 cell_w f64[C] | cell_h f64[C] | cell_delay f64[C] | positions f64[2C] | pin_term f64[2P] |
+#       pin_off f64[2P] | pin_cap f64[P] | pin_cell i32[P] | net_start i32[N+1] | net_pins i32[E] |
+#       sources i32[S] | endpoints i32[EP] | cell_fixed u8[C] | pos_explicit u8[C] | pin_dir u8[P] |
+#       [flags & 1] u64 byte count + the pin names, each NUL-terminated
+BIN_MAGIC = b"TDPGDSN1"
+BIN_HEADER = 128
+
+
+def _bin_sections(c):
+    C, P, N, E, S, EP = c
+    return [("cell_w", np.float64, (C,)), ("cell_h", np.float64, (C,)), ("cell_delay", np.float64, (C,)),
+            ("positions", np.float64, (C, 2)), ("pin_term", np.float64, (P, 2)), ("pin_off", np.float64, (P, 2)),
+            ("pin_cap", np.float64, (P,)), ("pin_cell", np.int32, (P,)), ("net_start", np.int32, (N + 1,)),
+            ("net_pins", np.int32, (E,)), ("sources", np.int32, (S,)), ("endpoints", np.int32, (EP,)),
+            ("cell_fixed", np.uint8, (C,)), ("pos_explicit", np.uint8, (C,)), ("pin_dir", np.uint8, (P,))]
+
+
+def save_bin(d: "Design", path: str) -> None:
+    """Write ``d`` as a binary design file (layout above)."""
+    counts = (d.n_cells, d.n_pins, d.n_nets, d.n_net_pins, int(d.sources.size), int(d.endpoints.size))
+    flags = 1 if d.pin_names is not None else 0
+    hdr = bytearray(BIN_HEADER)
+    hdr[0:8] = BIN_MAGIC
+    hdr[8:16] = np.array([1, flags], "<u4").tobytes()
+    hdr[16:64] = np.array(counts, "<i8").tobytes()
+    hdr[64:128] = np.array([d.clock_period, d.r_unit, d.c_unit, *d.core, d.default_cell_delay], "<f8").tobytes()
+    with open(path, "wb") as f:
+        f.write(hdr)
+        for name, dt, shape in _bin_sections(counts):
+            a = np.ascontiguousarray(getattr(d, name), dtype=np.dtype(dt).newbyteorder("<")).reshape(shape)
+            b = a.tobytes()
+            f.write(b)
+            f.write(b"\0" * (-len(b) % 8))
+        if flags & 1:
+            blob = b"".join(n.encode() + b"\0" for n in d.pin_names)
+            f.write(np.array([len(blob)], "<u8").tobytes())
+            f.write(blob)
+
+
+def load_bin(path: str) -> "Design":
+    """Read a binary design file (layout above)."""
+    buf = np.fromfile(path, dtype=np.uint8)
+    if buf.size < BIN_HEADER or bytes(buf[:8]) != BIN_MAGIC:
+        raise ValueError(f"parse error: {path}: not a binary design file")
+    version, flags = np.frombuffer(buf[8:16].tobytes(), "<u4")
+    if version != 1:
+        raise ValueError(f"parse error: {path}: unsupported binary design version {version}")
+    counts = tuple(int(x) for x in np.frombuffer(buf[16:64].tobytes(), "<i8"))
+    if min(counts) < 0 or counts[2] < 0:
+        raise ValueError(f"parse error: {path}: negative sizes")
+    sc = np.frombuffer(buf[64:128].tobytes(), "<f8")
+    off, kw = BIN_HEADER, {}
+    for name, dt, shape in _bin_sections(counts):
+        n = int(np.prod(shape)) * np.dtype(dt).itemsize
+        if off + n > buf.size:
+            raise ValueError(f"parse error: {path}: truncated ({name})")
+        kw[name] = np.frombuffer(buf[off:off + n].tobytes(), np.dtype(dt).newbyteorder("<")).astype(dt).reshape(shape)
+        off += n + (-n % 8)
+    pin_names = None
+    if flags & 1:
+        nb = int(np.frombuffer(buf[off:off + 8].tobytes(), "<u8")[0])
+        blob = bytes(buf[off + 8:off + 8 + nb])
+        pin_names = [s.decode() for s in blob.split(b"\0")[:-1]]
+        if len(pin_names) != counts[1]:
+            raise ValueError(f"parse error: {path}: pin name count")
+    return Design(clock_period=float(sc[0]), r_unit=float(sc[1]), c_unit=float(sc[2]), core=tuple(sc[3:7]),
+                  default_cell_delay=float(sc[7]), pin_names=pin_names, **kw)

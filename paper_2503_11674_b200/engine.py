@@ -70,6 +70,9 @@ _SIGS = {
     "tdpg_graph_arcs": (C.c_int, [_P, _P, _P, _P, _P]),
     "tdpg_set_positions": (C.c_int, [_P, _P]),
     "tdpg_set_terminal_positions": (C.c_int, [_P, _P]),
+    "tdpg_design_bin_info": (C.c_int, [C.c_char_p, _P, _P]),
+    "tdpg_design_bin_read": (C.c_int, [C.c_char_p, _P, _P, _P, _P, C.c_int64]),
+    "tdpg_design_bin_write": (C.c_int, [C.c_char_p, _P, _P, _P, C.c_double]),
     "tdpg_get_positions": (C.c_int, [_P, _P]),
     "tdpg_pin_positions": (C.c_int, [_P, _P]),
     "tdpg_wirelength": (C.c_int, [_P, C.c_double, _P, _F64P, _F64P, _P]),
@@ -522,3 +525,44 @@ def generate(seed=1, cells=100, registers=-1, fanout=2.0, fail_frac=0.2, r_unit=
         return d
     finally:
         L.tdpg_design_destroy(h)
+
+
+def design_bin_write(d: Design, path: str) -> None:
+    """tdpg_design_bin_write: the binary design file through the C-ABI (same bytes as design.save_bin)."""
+    v = d.view()
+    _check(lib().tdpg_design_bin_write(path.encode(), C.byref(v), d.positions.ctypes.data, d.pos_explicit.ctypes.data,
+                                       float(d.default_cell_delay)))
+
+
+def design_bin_read(path: str) -> Design:
+    """tdpg_design_bin_info + tdpg_design_bin_read into numpy arrays (the C-ABI reader)."""
+    L = lib()
+    cnt = np.zeros(6, np.int64)
+    names = C.c_int32()
+    _check(L.tdpg_design_bin_info(path.encode(), cnt.ctypes.data, C.byref(names)))
+    Cn, P, N, E, S, EP = (int(x) for x in cnt)
+    a = dict(cell_w=np.zeros(Cn), cell_h=np.zeros(Cn), cell_delay=np.zeros(Cn), cell_fixed=np.zeros(Cn, np.uint8),
+             pin_cell=np.zeros(P, np.int32), pin_term=np.zeros((P, 2)), pin_off=np.zeros((P, 2)),
+             pin_dir=np.zeros(P, np.uint8), pin_cap=np.zeros(P), net_start=np.zeros(N + 1, np.int32),
+             net_pins=np.zeros(E, np.int32), sources=np.zeros(S, np.int32), endpoints=np.zeros(EP, np.int32))
+    v = TdpgNetlist()
+    v.n_cells, v.n_pins, v.n_nets, v.n_sources, v.n_endpoints = Cn, P, N, S, EP
+    for k, x in a.items():
+        setattr(v, k, x.ctypes.data)
+    pos, expl = np.zeros((Cn, 2)), np.zeros(Cn, np.uint8)
+    cap = 0
+    blob = None
+    if names.value:
+        import os
+        cap = os.path.getsize(path)
+        blob = C.create_string_buffer(cap)
+    _check(L.tdpg_design_bin_read(path.encode(), C.byref(v), pos.ctypes.data, expl.ctypes.data,
+                                  C.cast(blob, C.c_void_p) if blob is not None else None, cap))
+    pin_names = None
+    if blob is not None:
+        pin_names = [s.decode() for s in blob.raw.split(b"\0")[:P]]
+    with open(path, "rb") as f:  # (default cell delay: header slot 7)
+        f.seek(64 + 7 * 8)
+        dcd = float(np.frombuffer(f.read(8), "<f8")[0])
+    return Design(clock_period=v.clock_period, r_unit=v.r_unit, c_unit=v.c_unit, core=tuple(v.core),
+                  positions=pos, pos_explicit=expl, pin_names=pin_names, default_cell_delay=dcd, **a)
