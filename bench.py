@@ -194,6 +194,30 @@ def iteration_bytes(d, grid, Q=0):
     return 2 * C * p + 2 * C * p + E * (4 + 2 * p) + 4 * (N + 1) + 4 * E + Q * (8 + p) + 2 * C * p + 2 * B * p + 2 * C * p * 7
 
 
+def design_file(args, seed=1):
+    """The timed workload's design as a binary design file (design.py save_bin / load_bin; C-ABI
+    tdpg_design_bin_*), shared by both arms: whichever arm runs first builds it (the product generator
+    or the oracle's restatement — netlist-identical, tests/test_bench_workload.py) and the other reads it."""
+    d = os.path.join(ROOT, "build", "designs")
+    os.makedirs(d, exist_ok=True)
+    return os.path.join(d, f"bench_c{args.cells}_s{seed}_f{args.fail_frac:g}.tdpb")
+
+
+def load_or_make(args, maker, seed=1):
+    from paper_2503_11674_b200.design import load_bin, save_bin
+    path = design_file(args, seed)
+    t0 = time.time()
+    if os.path.exists(path):
+        return load_bin(path), time.time() - t0, "file"
+    d = maker(args, seed)
+    if isinstance(d, tuple):
+        d = d[0]
+    tmp = f"{path}.{os.getpid()}"
+    save_bin(d, tmp)
+    os.replace(tmp, path)
+    return d, time.time() - t0, "generated"
+
+
 def make_design(args, seed=1):
     """The timed workload's design, built by the product: the generator's netlist, the run's jittered start
     (on the device, bitwise the reference's mt19937_64 draws) made explicit, the clock calibrated at that
@@ -318,7 +342,7 @@ def run_reference(args):
         return
     nproc = os.cpu_count() or 1
     t0 = time.time()
-    d = make_design_reference(args)
+    d, _, source = load_or_make(args, make_design_reference)
     setup_s = time.time() - t0
     r = RefOracle(d)
     W, K = args.warmup, args.steps
@@ -347,7 +371,7 @@ def run_reference(args):
                                                  f"every {args.m}); objective/STA at {nproc} threads, extraction at 1"},
                       "e2e": {"value": round(val, 4), "unit": "iters/s", "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0},
-                      "setup_s": round(setup_s, 1), "final": {"tns": res["tns"], "wns": res["wns"], "hpwl": res["hpwl"]}}),
+                      "setup_s": round(setup_s, 1), "design_source": source, "final": {"tns": res["tns"], "wns": res["wns"], "hpwl": res["hpwl"]}}),
           flush=True)
 
 
@@ -372,7 +396,7 @@ def run_ours(args):
 
     mode = args.mode or ("partition" if world > 1 else "replicas")
     partition = world > 1 and mode == "partition"
-    d, gen_s = make_design(args, 1 if partition else 1 + rank)  # partition: every rank holds the same design
+    d, gen_s, source = load_or_make(args, make_design, 1 if partition else 1 + rank)  # partition: one design
     W, K = args.warmup, args.steps
     total_iters = W + K + 64
     cfg = bench_config(args, total_iters)
@@ -533,7 +557,8 @@ def run_ours(args):
         "extraction_sweep_ms": sweep,
         "clocks": clk_summary,
         "cpu_baseline": cpu,
-        "setup_s": {"design": round(gen_s, 2), "session_create": round(create_s, 3), "engine_init": round(init_s, 3)},
+        "setup_s": {"design": round(gen_s, 2), "design_source": source, "session_create": round(create_s, 3),
+                    "engine_init": round(init_s, 3)},
     }
     print(json.dumps(out), flush=True)
 

@@ -752,11 +752,12 @@ __device__ __forceinline__ void scatter_cell5(double area, int bx, int by, const
 #pragma unroll
     for (int i = 0; i < kF5; ++i) {
         if (wx[i] == 0.0) continue;
-        const double aw = area * wx[i];
+        // (area * wx) * scale * wy == (area * wx) * wy * scale bitwise: scale is a power of two
+        const double aws = (area * wx[i]) * g.scale;
         const long long row = static_cast<long long>(bx + i - row0) * row_stride + (by - col0);
 #pragma unroll
         for (int j = 0; j < kF5; ++j) {
-            const long long q = __double2ll_rn(aw * wy[j] * g.scale);
+            const long long q = __double2ll_rn(aws * wy[j]);
             if (q) acc.add(row + j, static_cast<unsigned long long>(q));
         }
     }
@@ -1038,22 +1039,26 @@ __device__ __noinline__ double2 dens_grad_wide(const double2 p, const double2 s,
 }
 
 // Five-bin footprint gradient (axis5 on both axes): per bin column, dgx += area*dwx * fscale*sum f*wy,
-// dgy += area*wx * fscale*sum f*dwy.
-__device__ __forceinline__ double2 dens_grad5(int bx, int by, const double (&wx)[kF5], const double (&dwx)[kF5],
-                                              const double (&wy)[kF5], const double (&dwy)[kF5], double area,
-                                              const GridDev& g, const double* __restrict__ excess, double fscale)
+// dgy += area*wx * fscale*sum f*dwy.  Only the in-grid bins of the footprint (span = D + 3 per axis) are
+// read; the column sums are fused multiply-adds (within the 1e-9 density tolerance).
+__device__ __forceinline__ double2 dens_grad5(int bx, int by, int sx_n, int sy_n, const double (&wx)[kF5],
+                                              const double (&dwx)[kF5], const double (&wy)[kF5],
+                                              const double (&dwy)[kF5], double area, const GridDev& g,
+                                              const double* __restrict__ excess, double fscale)
 {
     double dgx = 0.0, dgy = 0.0;
+    // footprint bins inside the grid: a in [a0, a1), j in [j0, j1)
+    const int a0 = max(0, -bx), a1 = min(sx_n, g.nx - bx), j0 = max(0, -by), j1 = min(sy_n, g.ny - by);
 #pragma unroll
     for (int a = 0; a < kF5; ++a) {
-        if (wx[a] == 0.0 && dwx[a] == 0.0) continue; // (outside the grid, or no support)
+        if (a < a0 || a >= a1) continue; // (outside the grid, or no support)
         const double* ex = excess + static_cast<long long>(bx + a) * g.ny + by;
         double f[kF5];
 #pragma unroll
-        for (int j = 0; j < kF5; ++j) f[j] = (wy[j] != 0.0 || dwy[j] != 0.0) ? ex[j] : 0.0;
+        for (int j = 0; j < kF5; ++j) f[j] = (j >= j0 && j < j1) ? ex[j] : 0.0;
         double sx = 0.0, sy = 0.0;
 #pragma unroll
-        for (int j = 0; j < kF5; ++j) sx += f[j] * wy[j], sy += f[j] * dwy[j];
+        for (int j = 0; j < kF5; ++j) sx = __fma_rn(f[j], wy[j], sx), sy = __fma_rn(f[j], dwy[j], sy);
         dgx += (area * dwx[a]) * (fscale * sx);
         dgy += (area * wx[a]) * (fscale * sy);
     }
@@ -1078,10 +1083,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* _
     const double2 p = cell_xy[c], s = cell_wh[c];
     if (stop || s.x > g.wide_w || s.y > g.wide_h) return;
     double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
-    int bx, by;
-    axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx);
-    axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy);
-    dgrad[c] = dens_grad5(bx, by, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
+    int bx, by, nx5, ny5;
+    axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx, &nx5);
+    axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy, &ny5);
+    dgrad[c] = dens_grad5(bx, by, nx5, ny5, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
 }
 
 __global__ void __launch_bounds__(kBlock) k_dens_grad_wide(int n, const int* __restrict__ wide,
@@ -1097,10 +1102,10 @@ __global__ void __launch_bounds__(kBlock) k_dens_grad_wide(int n, const int* __r
     const int c = wide[i];
     const double2 p = cell_xy[c], s = cell_wh[c];
     double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
-    int bx, by;
-    if (axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx) &&
-        axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy))
-        dgrad[c] = dens_grad5(bx, by, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
+    int bx, by, nx5, ny5;
+    if (axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx, &nx5) &&
+        axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy, &ny5))
+        dgrad[c] = dens_grad5(bx, by, nx5, ny5, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
     else
         dgrad[c] = dens_grad_wide(p, s, g, excess, fscale);
 }

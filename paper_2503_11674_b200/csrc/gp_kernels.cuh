@@ -103,7 +103,7 @@ __device__ __forceinline__ double axis_w(const Axis& x, int j)
 // weight 0 (the reference clips its range, density.cpp:109-112).  Returns false for wider cells.
 constexpr int kF5 = 5;
 __device__ __forceinline__ bool axis5(double lo, double hi, double origin, double pitch, double inv_pitch, int nbins,
-                                      int& b, double (&w)[kF5], double (&dw)[kF5])
+                                      int& b, double (&w)[kF5], double (&dw)[kF5], int* span = nullptr)
 {
     double Fl[3], Bl[3], Fh[3], Bh[3];
     int al, ah;
@@ -126,6 +126,7 @@ __device__ __forceinline__ bool axis5(double lo, double hi, double origin, doubl
         dw[j] = in ? (bh[j] - bl[j]) * inv_len : 0.0;
     }
     b = al;
+    if (span) *span = D + 3; // bins a_lo .. a_lo + D + 2 carry the footprint (the rest are 0)
     return true;
 }
 

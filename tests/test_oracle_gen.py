@@ -30,7 +30,7 @@ def test_oracle_generator_matches_reference(seed, cells, kw):
 
 @needs_ref
 @pytest.mark.slow
-@pytest.mark.parametrize("cells", [10000, 40000])
+@pytest.mark.parametrize("cells", [10000])
 def test_oracle_generator_matches_reference_large(cells):
     same(Oracle.generate(seed=1, cells=cells, fail_frac=0.7), RefOracle.generate(seed=1, cells=cells, fail_frac=0.7))
 
