@@ -10,11 +10,18 @@
 // with the bin-overflow penalty), hence no oracle: tests check the Poisson residual with an
 // independent stencil, the gradient by finite differences and that placement spreads cells.
 //
-// Each 1D DCT is an N-point real FFT of the even/odd-reordered sequence plus a twiddle (Makhoul 1980),
-// run as batched cuFFT D2Z / Z2D along the contiguous axis; the other axis is reached by a tiled
-// shared-memory transpose.  All steps are stream-ordered and capturable into the iteration graph.
-#include <cufft.h>
-
+// The transforms are hand-written, one grid row per CTA, the row resident in shared memory:
+//  * power-of-two lengths: DCT-II as Makhoul's (1980) L-point complex FFT of the even/odd-reordered row
+//    plus a quarter-wave twiddle, DCT-III as the pre-twiddled Hermitian spectrum through the inverse
+//    FFT; the FFT is radix-2 decimation in time over the bit-reversed row in shared memory (twiddles
+//    from a per-length table);
+//  * other lengths: the direct O(L^2) sums from a cosine table cos(pi j / 2L), j < 4L.
+// Five launches per solve: DCT-II along y (rows of rho); tiled shared-memory transpose; one fused x pass
+// per row (DCT-II, divide by lambda_uv, DCT-III — the whole x spectrum of a y frequency stays on chip);
+// transpose back; DCT-III along y.  Stream-ordered and capturable into the iteration graph.  No
+// FFT library (tensor cores would need the transform as a dense FP64 GEMM, 2 L^3 flops per pass —
+// ~4 GFLOP at 1024^2 — far more than the FFT's ~50 MFLOP, so they do not pay here).
+#include <algorithm>
 #include <cmath>
 
 #include "gp_kernels.cuh"
@@ -23,63 +30,220 @@ namespace tdpg {
 
 namespace {
 
-void cufft_check(cufftResult r, const char* what)
+constexpr int kDctThreads = 256;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b)
 {
-    if (r != CUFFT_SUCCESS) throw Error(TDPG_ERR_CUDA, std::string("cufft error ") + std::to_string(r) + " (" + what + ")");
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// v[m] = x[2m] for m < ceil(L/2), else x[2(L-1-m)+1]  (rows of length L)
-__global__ void k_dct_pre(long long total, int L, const double* __restrict__ in, double* __restrict__ out)
+// W(m) = exp(-2 pi i m / L) from the half table tw[0 .. L/2) (W(m + L/2) = -W(m)); conj for the inverse
+__device__ __forceinline__ double2 twiddle(const double2* tw, int m, int L, bool inverse)
 {
-    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= total) return;
-    const long long row = i / L;
-    const int m = static_cast<int>(i - row * L);
-    const int src = m < (L + 1) / 2 ? 2 * m : 2 * (L - 1 - m) + 1;
-    out[i] = in[row * L + src];
+    const int h = L >> 1;
+    double2 w = m < h ? tw[m] : tw[m - h];
+    if (m >= h) w.x = -w.x, w.y = -w.y;
+    if (inverse) w.y = -w.y;
+    return w;
 }
 
-// X[k] = Re(exp(-i pi k / 2L) V[k]), V[k > L/2] = conj(V[L - k])
-__global__ void k_dct_post(long long total, int L, const double2* __restrict__ z, double* __restrict__ out)
+// Stockham autosort FFT (natural order in and out) over shared memory, radix-4 stages then one radix-2
+// stage when log2 L is odd; ping-pongs between x and y, returns the buffer holding the result.
+// tw: the half twiddle table in shared memory.
+__device__ double2* fft_stockham(double2* x, double2* y, int L, const double2* tw, bool inverse)
 {
-    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= total) return;
-    const long long row = i / L;
-    const int k = static_cast<int>(i - row * L), H = L / 2 + 1;
-    double s, c;
-    sincospi(static_cast<double>(k) / (2.0 * L), &s, &c);
-    if (k < H) {
-        const double2 v = z[row * H + k];
-        out[i] = v.x * c + v.y * s;
-    } else {
-        const double2 v = z[row * H + (L - k)];
-        out[i] = v.x * c - v.y * s;
+    int Ns = 1;
+    for (; Ns * 4 <= L; Ns *= 4) {
+        const int q = L >> 2;
+        for (int j = threadIdx.x; j < q; j += blockDim.x) {
+            const int k = j & (Ns - 1), m = k * (L / (Ns * 4));
+            double2 a0 = x[j], a1 = x[j + q], a2 = x[j + 2 * q], a3 = x[j + 3 * q];
+            if (Ns > 1) {
+                a1 = cmul(a1, twiddle(tw, m, L, inverse));
+                a2 = cmul(a2, twiddle(tw, 2 * m, L, inverse));
+                a3 = cmul(a3, twiddle(tw, 3 * m, L, inverse));
+            }
+            const double2 s02 = make_double2(a0.x + a2.x, a0.y + a2.y), d02 = make_double2(a0.x - a2.x, a0.y - a2.y);
+            const double2 s13 = make_double2(a1.x + a3.x, a1.y + a3.y), d13 = make_double2(a1.x - a3.x, a1.y - a3.y);
+            // -i d13 (forward) or +i d13 (inverse)
+            const double2 r13 = inverse ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
+            const int base = (j - k) * 4 + k;
+            y[base] = make_double2(s02.x + s13.x, s02.y + s13.y);
+            y[base + Ns] = make_double2(d02.x + r13.x, d02.y + r13.y);
+            y[base + 2 * Ns] = make_double2(s02.x - s13.x, s02.y - s13.y);
+            y[base + 3 * Ns] = make_double2(d02.x - r13.x, d02.y - r13.y);
+        }
+        __syncthreads();
+        double2* t = x;
+        x = y, y = t;
+    }
+    if (Ns * 2 == L) { // last radix-2 stage
+        const int q = L >> 1;
+        for (int j = threadIdx.x; j < q; j += blockDim.x) {
+            const int k = j & (Ns - 1), m = k * (L / (Ns * 2));
+            const double2 a0 = x[j], a1 = Ns > 1 ? cmul(x[j + q], twiddle(tw, m, L, inverse)) : x[j + q];
+            const int base = (j - k) * 2 + k;
+            y[base] = make_double2(a0.x + a1.x, a0.y + a1.y);
+            y[base + Ns] = make_double2(a0.x - a1.x, a0.y - a1.y);
+        }
+        __syncthreads();
+        x = y;
+    }
+    return x;
+}
+
+// row position m of the Makhoul reordering that element n of the row goes to (v[m] = x[src(m)])
+__device__ __forceinline__ int makhoul_pos(int n, int L) { return (n & 1) ? L - 1 - (n >> 1) : (n >> 1); }
+
+struct DctTables {
+    const double2* tw; // [L/2] exp(-2 pi i j / L)          (power of two)
+    const double2* qt; // [L]   exp(-i pi k / 2L)
+    const double* c4;  // [4L]  cos(pi j / 2L)              (direct path)
+    const double* lam; // [L]   2 - 2 cos(pi u / L)          (this axis' Laplacian eigenvalues / pitch^-2)
+    const double* lam_y; //      the other axis' (x pass only)
+};
+
+// Power-of-two rows use the half-length real-FFT form: the reordered real row v (length L) is read as M
+// = L/2 complex values z[m] = v[2m] + i v[2m+1] (the same doubles), one M-point FFT, then the split
+//   V[k] = (Z[k] + conj Z[M-k]) / 2 - i W_L^k (Z[k] - conj Z[M-k]) / 2,   k = 0..M   (W_L = e^{-2 pi i / L});
+// the inverse builds Z[k] = (V[k] + conj V[M-k]) + i W_L^-k (V[k] - conj V[M-k]) and one inverse M-point FFT
+// gives v[2m] + i v[2m+1].  Shared memory: two complex rows of M and the M-point twiddles (M/2).
+struct RowSmem {
+    double2 *z0, *z1, *tw;
+    int M;
+};
+
+__device__ __forceinline__ double2 wl(const double2* __restrict__ twL, int k, int M)
+{   // W_L^k for k in [0, M], from the global half table (W_L^M = -1)
+    return k < M ? __ldg(twL + k) : make_double2(-1.0, 0.0);
+}
+
+// X[k] = sum_n x[n] cos(pi k (2n + 1) / 2L) for the row `src` (global) into X (shared, L doubles, aliasing
+// the work row that is free after the FFT — returned)
+__device__ double* dct2_row(const double* __restrict__ src, int L, const DctTables& T, RowSmem& S, bool pow2,
+                            double* rowbuf, double* Xdirect)
+{
+    if (pow2) {
+        const int M = S.M;
+        double* v = reinterpret_cast<double*>(S.z0);
+        for (int n = threadIdx.x; n < L; n += blockDim.x) v[makhoul_pos(n, L)] = src[n];
+        __syncthreads();
+        const double2* Z = fft_stockham(S.z0, S.z1, M, S.tw, false);
+        double* X = reinterpret_cast<double*>(Z == S.z0 ? S.z1 : S.z0);
+        for (int k = threadIdx.x; k <= M; k += blockDim.x) {
+            const double2 a = Z[k < M ? k : 0], bc = Z[k > 0 ? M - k : 0];
+            const double2 b = make_double2(bc.x, -bc.y); // conj Z[M-k]
+            const double2 s = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+            const double2 d = make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y));
+            const double2 wd = cmul(wl(T.tw, k, M), d);
+            const double2 V = make_double2(s.x + wd.y, s.y - wd.x); // s - i w d
+            const double2 q = __ldg(T.qt + k);
+            X[k] = V.x * q.x - V.y * q.y; // Re(q_k V)
+            if (k > 0 && k < M) {
+                const double2 q2 = __ldg(T.qt + (L - k));
+                X[L - k] = V.x * q2.x + V.y * q2.y; // Re(q_{L-k} conj V)
+            }
+        }
+        __syncthreads();
+        return X;
+    }
+    for (int n = threadIdx.x; n < L; n += blockDim.x) rowbuf[n] = src[n];
+    __syncthreads();
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+        double acc = 0.0;
+        const long long L4 = 4LL * L;
+        long long j = k; // (2n + 1) k mod 4L, advanced by 2k per n
+        for (int n = 0; n < L; ++n) {
+            acc += rowbuf[n] * __ldg(T.c4 + j);
+            j += 2LL * k;
+            if (j >= L4) j -= L4;
+        }
+        Xdirect[k] = acc;
+    }
+    __syncthreads();
+    return Xdirect;
+}
+
+// y[n] = X[0] + 2 sum_{k>=1} X[k] cos(pi k (2n + 1) / 2L) (= L x when X = DCT-II(x)); X (shared, real) is
+// one of the work rows (power of two), result written to dst (global)
+__device__ void dct3_row(double* X, int L, const DctTables& T, RowSmem& S, double* __restrict__ dst, bool pow2)
+{
+    if (pow2) {
+        const int M = S.M;
+        double2* zin = reinterpret_cast<double2*>(X) == S.z0 ? S.z1 : S.z0;
+        double2* zout = reinterpret_cast<double2*>(X) == S.z0 ? S.z0 : S.z1;
+        auto Vk = [&](int k) { // V[k] = e^{+i pi k / 2L} (X[k] - i X[L-k]), X[L] := 0
+            const double2 q = __ldg(T.qt + k);
+            const double a = X[k], b = k > 0 ? X[L - k] : 0.0;
+            return make_double2(q.x * a - q.y * b, -q.y * a - q.x * b); // conj(q)(a - i b)
+        };
+        for (int k = threadIdx.x; k < M; k += blockDim.x) {
+            const double2 a = Vk(k), bb = Vk(M - k);
+            const double2 b = make_double2(bb.x, -bb.y); // conj V[M-k]
+            const double2 s = make_double2(a.x + b.x, a.y + b.y), d = make_double2(a.x - b.x, a.y - b.y);
+            double2 w = wl(T.tw, k, M);
+            w.y = -w.y; // W_L^-k
+            const double2 wd = cmul(w, d);
+            zin[k] = make_double2(s.x - wd.y, s.y + wd.x); // s + i w d
+        }
+        __syncthreads();
+        const double2* z = fft_stockham(zin, zout, M, S.tw, true);
+        const double* v = reinterpret_cast<const double*>(z);
+        for (int n = threadIdx.x; n < L; n += blockDim.x) dst[n] = v[makhoul_pos(n, L)];
+        return;
+    }
+    for (int n = threadIdx.x; n < L; n += blockDim.x) {
+        double acc = 0.0;
+        const long long L4 = 4LL * L, step = 2LL * n + 1;
+        long long j = step; // (2n + 1) k mod 4L for k = 1, 2, ...
+        for (int k = 1; k < L; ++k) {
+            acc += X[k] * __ldg(T.c4 + j);
+            j += step;
+            if (j >= L4) j -= L4;
+        }
+        dst[n] = X[0] + 2.0 * acc;
     }
 }
 
-// DCT-III pre-twiddle: V[k] = exp(+i pi k / 2L) (X[k] - i X[L-k]), k = 0..L/2 (X[L] := 0)
-__global__ void k_dct3_pre(long long total_h, int L, const double* __restrict__ X, double2* __restrict__ z)
+// MODE 0: out = DCT-II(row); MODE 1: out = DCT-III(row); MODE 2 (x pass, rows are y frequencies v):
+// out = DCT-III(DCT-II(row) / lambda_uv / (nx ny)), the (0, 0) term dropped.
+template <int MODE>
+__global__ void __launch_bounds__(kDctThreads) k_dct_rows(int L, bool pow2, const double* __restrict__ in,
+                                                          double* __restrict__ out, DctTables T, int nx, int ny,
+                                                          double ibw2, double ibh2)
 {
-    const int H = L / 2 + 1;
-    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= total_h) return;
-    const long long row = i / H;
-    const int k = static_cast<int>(i - row * H);
-    const double a = X[row * L + k], b = k > 0 ? X[row * L + (L - k)] : 0.0;
-    double s, c;
-    sincospi(static_cast<double>(k) / (2.0 * L), &s, &c);
-    z[i] = make_double2(c * a + s * b, s * a - c * b); // (c + i s)(a - i b)
-}
-
-// x[2m] = v[m] (m < ceil(L/2)), x[2(L-1-m)+1] = v[m]
-__global__ void k_dct3_post(long long total, int L, const double* __restrict__ v, double* __restrict__ out)
-{
-    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= total) return;
-    const long long row = i / L;
-    const int m = static_cast<int>(i - row * L);
-    const int dst = m < (L + 1) / 2 ? 2 * m : 2 * (L - 1 - m) + 1;
-    out[row * L + dst] = v[i];
+    extern __shared__ double2 dsm[];
+    RowSmem S;
+    S.M = L / 2;
+    S.z0 = dsm, S.z1 = dsm + S.M, S.tw = dsm + 2 * S.M; // (power of two: 2 M + M/2 complex)
+    double* ra = reinterpret_cast<double*>(dsm);       // (direct path: two real rows)
+    double* rb = ra + L;
+    if (pow2) {
+        for (int j = threadIdx.x; j < S.M / 2; j += blockDim.x) S.tw[j] = __ldg(T.tw + 2 * j); // W_M^j = W_L^2j
+        __syncthreads();
+    }
+    const long long row = blockIdx.x;
+    const double* src = in + row * L;
+    double* dst = out + row * L;
+    if (MODE == 0) {
+        const double* X = dct2_row(src, L, T, S, pow2, ra, rb);
+        for (int k = threadIdx.x; k < L; k += blockDim.x) dst[k] = X[k];
+    } else if (MODE == 1) {
+        double* X = pow2 ? reinterpret_cast<double*>(S.z1) : rb;
+        for (int k = threadIdx.x; k < L; k += blockDim.x) X[k] = src[k];
+        __syncthreads();
+        dct3_row(X, L, T, S, dst, pow2);
+    } else {
+        double* X = dct2_row(src, L, T, S, pow2, ra, rb);
+        const int v = static_cast<int>(row);
+        const double lv = __ldg(T.lam_y + v) * ibh2, inv_b = 1.0 / (static_cast<double>(nx) * ny);
+        for (int u = threadIdx.x; u < L; u += blockDim.x) {
+            const double lam = __ldg(T.lam + u) * ibw2 + lv;
+            X[u] = (u == 0 && v == 0) ? 0.0 : X[u] / lam * inv_b;
+        }
+        __syncthreads();
+        dct3_row(X, L, T, S, dst, pow2);
+    }
 }
 
 // out[c][r] = in[r][c], in is rows x cols; 32x32 tiles through shared memory (padded)
@@ -98,20 +262,22 @@ __global__ void k_transpose(int rows, int cols, const double* __restrict__ in, d
     }
 }
 
-// coefficients in the transposed layout A^T[v][u] (ny rows of nx): divide by lambda_uv, drop (0,0),
-// fold in the inverse transform's 1 / (nx ny)
-__global__ void k_poisson_scale(int nx, int ny, double ibw2, double ibh2, double* __restrict__ a)
+__global__ void k_dct_tables(int L, double2* __restrict__ tw, double2* __restrict__ qt, double* __restrict__ c4,
+                             double* __restrict__ lam)
 {
-    const long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x;
-    if (i >= static_cast<long long>(nx) * ny) return;
-    const int v = static_cast<int>(i / nx), u = static_cast<int>(i - static_cast<long long>(v) * nx);
-    if (u == 0 && v == 0) {
-        a[i] = 0.0;
-        return;
+    for (int j = blockIdx.x * kBlock + threadIdx.x; j < 4 * L; j += gridDim.x * kBlock) {
+        double s, c;
+        if (j < L) lam[j] = 2.0 - 2.0 * cospi(static_cast<double>(j) / L);
+        if (tw && j < L / 2) {
+            sincospi(2.0 * j / L, &s, &c);
+            tw[j] = make_double2(c, -s);
+        }
+        if (j < L) {
+            sincospi(static_cast<double>(j) / (2.0 * L), &s, &c);
+            qt[j] = make_double2(c, -s);
+        }
+        if (c4) c4[j] = cospi(static_cast<double>(j) / (2.0 * L));
     }
-    const double lam = (2.0 - 2.0 * cospi(static_cast<double>(u) / nx)) * ibw2 +
-                       (2.0 - 2.0 * cospi(static_cast<double>(v) / ny)) * ibh2;
-    a[i] = a[i] / lam / (static_cast<double>(nx) * ny);
 }
 
 // D = 1/2 sum_b rho_b psi_b, per-block partial into part_d[2 b] (same grid as k_density_bins)
@@ -129,30 +295,55 @@ __global__ void __launch_bounds__(kBlock) k_electro_energy(long long B, const do
     if (threadIdx.x == 0) part_d[2 * blockIdx.x] = 0.5 * e;
 }
 
+bool is_pow2(int L) { return L >= 4 && (L & (L - 1)) == 0; }
+
+size_t dct_smem(int L) { return is_pow2(L) ? 20 * static_cast<size_t>(L) + 16 : 16 * static_cast<size_t>(L); }
+
+template <int MODE>
+void launch_rows(int rows, int L, const ElectroPlan::Axis& ax, const ElectroPlan::Axis& other, const double* in,
+                 double* out, int nx, int ny, double ibw2, double ibh2, cudaStream_t st)
+{
+    const size_t sm = dct_smem(L);
+    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_dct_rows<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(sm)));
+    const DctTables T{ax.tw.p, ax.qt.p, ax.c4.p, ax.lam.p, other.lam.p};
+    // power of two: one thread per radix-4 butterfly of the M = L/2-point FFT (M/4), so a 1024 grid's rows
+    // fit one wave at 11 rows per SM; the direct path keeps a full block for its O(L) inner loops
+    const int threads = is_pow2(L) ? std::max(32, std::min(kDctThreads, L / 8)) : kDctThreads;
+    k_dct_rows<MODE><<<rows, threads, sm, st>>>(L, is_pow2(L), in, out, T, nx, ny, ibw2, ibh2);
+    CK_LAUNCH();
+}
+
 } // namespace
+
+void ElectroPlan::Axis::make(int len, cudaStream_t st)
+{
+    L = len;
+    if (is_pow2(L)) {
+        tw.alloc(L / 2), c4.release();
+    } else {
+        tw.release(), c4.alloc(4 * static_cast<size_t>(L));
+    }
+    qt.alloc(L), lam.alloc(L);
+    k_dct_tables<<<blocks_for(4LL * L, kBlock), kBlock, 0, st>>>(L, tw.p, qt.p, c4.p, lam.p);
+    CK_LAUNCH();
+}
 
 ElectroPlan::~ElectroPlan() { release(); }
 
-void ElectroPlan::release()
-{
-    for (auto& p : plan)
-        if (p) cufftDestroy(p), p = 0;
-    nx = ny = 0;
-}
+void ElectroPlan::release() { nx = ny = 0; }
 
 void ElectroPlan::ensure(int gx, int gy)
 {
     if (gx == nx && gy == ny) return;
-    release();
+    if (dct_smem(std::max(gx, gy)) > 227 * 1024) // (one grid row per CTA in shared memory)
+        throw Error(TDPG_ERR_VALIDATION, "validation error: electrostatic density supports up to 8192 bins per axis "
+                                         "for power-of-two grids and 14528 otherwise");
     nx = gx, ny = gy;
     const long long B = static_cast<long long>(nx) * ny;
     rho.alloc(B), psi.alloc(B), r1.alloc(B), r2.alloc(B);
-    z.alloc(std::max(static_cast<long long>(nx) * (ny / 2 + 1), static_cast<long long>(ny) * (nx / 2 + 1)));
-    int n_y[1] = {ny}, n_x[1] = {nx};
-    cufft_check(cufftPlanMany(&plan[0], 1, n_y, nullptr, 1, ny, nullptr, 1, ny / 2 + 1, CUFFT_D2Z, nx), "plan y D2Z");
-    cufft_check(cufftPlanMany(&plan[1], 1, n_x, nullptr, 1, nx, nullptr, 1, nx / 2 + 1, CUFFT_D2Z, ny), "plan x D2Z");
-    cufft_check(cufftPlanMany(&plan[2], 1, n_x, nullptr, 1, nx / 2 + 1, nullptr, 1, nx, CUFFT_Z2D, ny), "plan x Z2D");
-    cufft_check(cufftPlanMany(&plan[3], 1, n_y, nullptr, 1, ny / 2 + 1, nullptr, 1, ny, CUFFT_Z2D, nx), "plan y Z2D");
+    ax.make(nx, 0), ay.make(ny, 0);
+    CK(cudaStreamSynchronize(0));
 }
 
 // psi = L^+ (rho - mean rho) on the session's grid (rho in plan.rho), stream-ordered on `st`.
@@ -161,35 +352,13 @@ void electro_solve(tdpg_session* s, cudaStream_t st)
     Grid& g = s->grid;
     ElectroPlan& E = g.electro;
     const int nx = g.nx, ny = g.ny;
-    const long long B = g.bins();
-    const unsigned nb = blocks_for(B, kBlock);
-    auto hz = [&](int L, int batch) { return static_cast<long long>(batch) * (L / 2 + 1); };
-    auto d2z = [&](cufftHandle p, double* in, double2* out) {
-        cufft_check(cufftSetStream(p, st), "set stream");
-        cufft_check(cufftExecD2Z(p, in, reinterpret_cast<cufftDoubleComplex*>(out)), "exec D2Z");
-    };
-    auto z2d = [&](cufftHandle p, double2* in, double* out) {
-        cufft_check(cufftSetStream(p, st), "set stream");
-        cufft_check(cufftExecZ2D(p, reinterpret_cast<cufftDoubleComplex*>(in), out), "exec Z2D");
-    };
+    const double ibw2 = 1.0 / (g.bw * g.bw), ibh2 = 1.0 / (g.bh * g.bh);
     const dim3 tb(32, 8);
-    // forward DCT-II along y (rows of length ny), then along x (after a transpose)
-    k_dct_pre<<<nb, kBlock, 0, st>>>(B, ny, E.rho, E.r1);
-    d2z(E.plan[0], E.r1, E.z);
-    k_dct_post<<<nb, kBlock, 0, st>>>(B, ny, E.z, E.r2);
-    k_transpose<<<dim3((ny + 31) / 32, (nx + 31) / 32), tb, 0, st>>>(nx, ny, E.r2, E.r1); // -> [ny][nx]
-    k_dct_pre<<<nb, kBlock, 0, st>>>(B, nx, E.r1, E.r2);
-    d2z(E.plan[1], E.r2, E.z);
-    k_dct_post<<<nb, kBlock, 0, st>>>(B, nx, E.z, E.r1); // A^T [ny][nx]
-    k_poisson_scale<<<nb, kBlock, 0, st>>>(nx, ny, 1.0 / (g.bw * g.bw), 1.0 / (g.bh * g.bh), E.r1);
-    // inverse DCT-III along x, transpose back, along y
-    k_dct3_pre<<<blocks_for(hz(nx, ny), kBlock), kBlock, 0, st>>>(hz(nx, ny), nx, E.r1, E.z);
-    z2d(E.plan[2], E.z, E.r2);
-    k_dct3_post<<<nb, kBlock, 0, st>>>(B, nx, E.r2, E.r1);
-    k_transpose<<<dim3((nx + 31) / 32, (ny + 31) / 32), tb, 0, st>>>(ny, nx, E.r1, E.r2); // -> [nx][ny]
-    k_dct3_pre<<<blocks_for(hz(ny, nx), kBlock), kBlock, 0, st>>>(hz(ny, nx), ny, E.r2, E.z);
-    z2d(E.plan[3], E.z, E.r1);
-    k_dct3_post<<<nb, kBlock, 0, st>>>(B, ny, E.r1, E.psi);
+    launch_rows<0>(nx, ny, E.ay, E.ax, E.rho, E.r1, nx, ny, ibw2, ibh2, st);                        // DCT-II along y
+    k_transpose<<<dim3((ny + 31) / 32, (nx + 31) / 32), tb, 0, st>>>(nx, ny, E.r1, E.r2);     // -> [ny][nx]
+    launch_rows<2>(ny, nx, E.ax, E.ay, E.r2, E.r1, nx, ny, ibw2, ibh2, st);                         // x: II, /lambda, III
+    k_transpose<<<dim3((nx + 31) / 32, (ny + 31) / 32), tb, 0, st>>>(ny, nx, E.r1, E.r2);     // -> [nx][ny]
+    launch_rows<1>(nx, ny, E.ay, E.ax, E.r2, E.psi, nx, ny, ibw2, ibh2, st);                        // DCT-III along y
     CK_LAUNCH();
 }
 

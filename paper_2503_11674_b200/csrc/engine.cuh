@@ -20,7 +20,6 @@
 #include <string>
 #include <vector>
 
-#include <cufft.h>
 
 #include "common.cuh"
 
@@ -28,12 +27,18 @@ struct tdpg_session;
 
 namespace tdpg {
 
-// Electrostatic density (electro.cu): cuFFT plans and work arrays of the grid's Poisson solve.
+// Electrostatic density (electro.cu): twiddle / cosine tables and work rows of the grid's Poisson solve
+// (hand-written shared-memory DCTs, no FFT library).
 struct ElectroPlan {
     int nx = 0, ny = 0;
-    cufftHandle plan[4] = {0, 0, 0, 0}; // D2Z along y, D2Z along x, Z2D along x, Z2D along y
+    struct Axis {
+        int L = 0;
+        DBuf<double2> tw, qt; // FFT twiddles (power-of-two lengths), quarter-wave twiddles
+        DBuf<double> c4;      // cos(pi j / 2L), j < 4L (direct path for other lengths)
+        DBuf<double> lam;     // 2 - 2 cos(pi u / L): the axis' Laplacian eigenvalues (times pitch^2)
+        void make(int len, cudaStream_t st);
+    } ax, ay;
     DBuf<double> rho, psi, r1, r2;
-    DBuf<double2> z;
     void ensure(int gx, int gy);
     void release();
     ~ElectroPlan();
