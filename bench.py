@@ -384,6 +384,18 @@ def traffic_for(d, grid, kernel):
     return json.load(open(tfile)).get(f"{d.n_cells}x{grid}", {}).get(kernel)
 
 
+def maxr_dev(x, torch):
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def red_len(s):
+    from paper_2503_11674_b200.engine import red_size
+    return red_size(s)
+
+
 def run_ours(args):
     rank, world, local = dist_env()
     import torch
@@ -442,6 +454,17 @@ def run_ours(args):
         raise SystemExit(f"bench: the timed window extracted no path ({refreshes} refreshes): the workload "
                          "would not exercise the timing-driven path")
 
+    # partitioned: the two collectives of an iteration timed alone (device, max over ranks), beside the
+    # iteration they sit in
+    comm = None
+    if partition:
+        ms_grid, ms_red = s.comm_bench(20)
+        comm = {"allreduce_grid_ms": round(maxr_dev(ms_grid, torch), 4), "allreduce_grad_ms": round(maxr_dev(ms_red, torch), 4),
+                "grid_bytes": 8 * args.grid * args.grid, "grad_bytes": 8 * red_len(s),
+                "iteration_ms": round(dev_ms_max / K, 4),
+                "what": "NCCL sum all-reduces of the int64 density grid and of [partial cell gradient | WA/HPWL/PP "
+                        "partials], each timed alone (CUDA events, 20 reps); the iteration overlaps the second "
+                        "with nothing (it ends the pre-reduction phase) and the first with the WA branch"}
     # per-kernel profile of loop iterations (roofline of the dominant kernel); a partitioned engine
     # is profiled through its replica twin on rank 0 below
     if partition and rank != 0:
@@ -523,8 +546,9 @@ def run_ours(args):
         "warmup": W, "ms_per_step": round(dev_ms_max / K, 4), "higher_is_better": True,
         "scaling": "strong" if partition else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, d, world),
-        "mode": ("nets partitioned, NCCL all-reduce of the cell gradient inside the iteration graph" if partition
-                 else "replicas") if world > 1 else "single GPU",
+        "mode": ("nets and cells partitioned: NCCL all-reduces of the density grid and of the cell gradient inside "
+                 "the iteration graph" if partition else "replicas") if world > 1 else "single GPU",
+        "partition": comm,
         "timed_window": {"refreshes": refreshes, "refresh_ms_each": round(refresh_ms / max(refreshes, 1), 3),
                          "paths_extracted": paths_timed, "path_pins_extracted": st1["path_pins"] - st0["path_pins"],
                          "ledger_pairs_end": st1["ledger_pairs"], "gp_iteration_ms": round(gp_ms, 4)},

@@ -255,21 +255,30 @@ int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_tr
 /* Per-kernel device time (ms) of one iteration of each kind, measured with events. */
 int tdpg_profile_iteration(tdpg_session* s, int32_t reps, double* out_ms, int32_t n_out, char* names, int32_t name_len);
 
-/* ---- single-design multi-GPU: net-partitioned gradient + NCCL all-reduce --------
+/* ---- single-design multi-GPU: partitioned gradient + NCCL all-reduces ------------
  * Nets (WA entries and the net-arc pin pairs fused into WA) are split into contiguous WA-block ranges
- * balanced by net-pin entries; each rank folds its entries into a partial cell gradient, one NCCL sum
- * all-reduce over [partial d_cell | WA, HPWL, PP block partials] completes gradient and objective terms
- * on every rank; density, Adam and timing refreshes are replicated (run_placement semantics kept).
+ * balanced by net-pin entries, and the movable cells into contiguous slices of the spatial order.  Each
+ * rank rasterises its cells into the int64 fixed-point grid, which is sum-all-reduced (exact: every rank
+ * holds bitwise the single-GPU grid); bins are replicated; each rank folds its entries plus lambda x the
+ * density gradient of its cells into a partial cell gradient, and one NCCL sum all-reduce over
+ * [partial d_cell | WA, HPWL, PP block partials] completes gradient and objective terms on every rank;
+ * Adam and timing refreshes are replicated (run_placement semantics kept).
  * tdpg_partition_plan: bounds [world+1] = per-rank WA block ranges, rank_entries [world] (host only).   */
 int tdpg_partition_plan(int32_t n_nets, const int32_t* net_start, int32_t world, int32_t* bounds,
                         int64_t* rank_entries);
 int tdpg_set_partition(tdpg_session* s, int32_t rank, int32_t world); /* no communicator: split-phase API */
 int tdpg_comm_unique_id(uint8_t id[128]);                            /* ncclGetUniqueId (rank 0)        */
 int tdpg_comm_init(tdpg_session* s, int32_t rank, int32_t world, const uint8_t id[128]);
-/* Split-phase partitioned iteration (the caller reduces, e.g. tests on one GPU): phase A returns this
- * rank's all-reduce buffer (n_red doubles); phase B takes the element-wise sum over ranks. */
-int tdpg_part_step_a(tdpg_session* s, double* red, int64_t* n_red);
+/* Split-phase partitioned iteration (the caller reduces, e.g. tests on one GPU): tdpg_part_density runs
+ * the scheduled refresh / re-sort and this rank's scatter and returns its grid (n_bins int64); phase A takes
+ * the grid summed over ranks and returns this rank's all-reduce buffer (n_red doubles); phase B takes the
+ * element-wise sum of those over ranks. */
+int tdpg_part_density(tdpg_session* s, int64_t* acc, int64_t* n_bins);
+int tdpg_part_step_a(tdpg_session* s, const int64_t* acc, double* red, int64_t* n_red);
 int tdpg_part_step_b(tdpg_session* s, const double* red);
+/* Device time (ms, averaged over iters) of the two collectives of a partitioned iteration run alone:
+ * ms[0] the int64 density grid, ms[1] the gradient buffer of n_red doubles.  Collective: every rank calls. */
+int tdpg_comm_bench(tdpg_session* s, int32_t iters, int64_t n_red, double ms[2]);
 
 /* ---- synthetic designs (generate_synthetic semantics) ---------------- */
 typedef struct tdpg_design tdpg_design;

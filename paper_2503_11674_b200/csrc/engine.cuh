@@ -326,6 +326,10 @@ int sorted_violated(tdpg_session* s);
 
 // partition.cu
 void comm_allreduce(tdpg_session* s, double* buf, size_t n);
+void comm_allreduce_i64(tdpg_session* s, long long* buf, size_t n, cudaStream_t st);
+void launch_density_scatter_part(tdpg_session* s, const Ctrl* ctrl, int lo, int hi, bool wide);
+void launch_dens_grad_part(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st, int lo, int hi);
+void launch_add_dgrad(tdpg_session* s, const Sched* sched, const Ctrl* ctrl, double2* fold, int lo, int hi);
 void comm_destroy(tdpg_session* s);
 
 // electro.cu

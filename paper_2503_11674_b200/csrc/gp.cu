@@ -1125,6 +1125,7 @@ struct CellArgs {
     const double2* dgrad;
     double2* d_cell;    // optional gradient output
     const double2* folded; // partitioned mode: the all-reduced fold (skips the fold)
+    bool dgrad_folded;     // ... which already holds lambda * density gradient (sharded density)
     double2* m;         // Adam state (iteration mode)
     double2* v;
     double b1, b2, eps;
@@ -1162,8 +1163,10 @@ __global__ void __launch_bounds__(kBlock, 5) k_cells(CellArgs a, const IterCur* 
         return;
     }
     const double lambda = cur->lambda;
-    gx += lambda * dg.x;
-    gy += lambda * dg.y;
+    if (!a.dgrad_folded) {
+        gx += lambda * dg.x;
+        gy += lambda * dg.y;
+    }
     if (ctrl && !(isfinite(gx) && isfinite(gy))) atomicMin(&ctrl->nonfinite_at, cur->iter);
     if (a.d_cell) a.d_cell[c] = make_double2(gx, gy);
     if (!adam) return;
@@ -1540,6 +1543,7 @@ CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, dou
     a.dgrad = s->dgrad;
     a.d_cell = d_cell;
     a.folded = nullptr;
+    a.dgrad_folded = false;
     a.m = m, a.v = v;
     a.b1 = b1, a.b2 = b2, a.eps = eps;
     a.core_x0 = s->core[0], a.core_y0 = s->core[1], a.core_x1 = s->core[2], a.core_y1 = s->core[3];
@@ -1872,11 +1876,70 @@ void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cu
     CK_LAUNCH();
 }
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
-                  const IterCur* cur, Ctrl* ctrl, bool dens_grad, const double2* folded)
+                  const IterCur* cur, Ctrl* ctrl, bool dens_grad, const double2* folded, bool dgrad_folded)
 {
     CellArgs ca = cell_args(s, d_cell, m, v, b1, b2, eps);
     ca.folded = folded;
+    ca.dgrad_folded = dgrad_folded;
     launch_cell_pass(s, ca, cur, ctrl, dens_grad);
+}
+
+// Partitioned engine with the density sharded: this rank scatters the movable cells of its
+// slice [lo, hi) of the spatial order (rank 0 also the wide cells); the int64 grid is summed across ranks
+// (exact, order independent); bins are replicated; the density gradient is computed for the slice (the
+// few wide cells on every rank) and lambda * gradient goes into this rank's share of the all-reduced fold.
+void launch_density_scatter_part(tdpg_session* s, const Ctrl* ctrl, int lo, int hi, bool wide)
+{
+    const GridDev g = grid_dev(s);
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(s->grid.acc.p);
+    if (hi > lo) {
+        k_density_scatter_win<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(hi - lo, s->grid.perm.p + lo,
+                                                                                s->cell_xy, s->cell_wh, g, acc, ctrl);
+        CK_LAUNCH();
+    }
+    if (wide && s->grid.n_wide > 0) {
+        k_density_scatter_wide<<<blocks_for(s->grid.n_wide, kBlock), kBlock, 0, s->st>>>(
+            s->grid.n_wide, s->grid.wide, s->cell_xy, s->cell_wh, g, acc, ctrl);
+        CK_LAUNCH();
+    }
+}
+
+void launch_dens_grad_part(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st, int lo, int hi)
+{
+    const bool el = s->grid.model == 1;
+    const double* field = el ? s->grid.electro.psi.p : s->grid.excess.p;
+    if (hi > lo) {
+        k_dens_grad<<<blocks_for(hi - lo, kBlock), kBlock, 0, st>>>(hi - lo, s->grid.perm.p + lo, s->cell_xy,
+                                                                    s->cell_wh, grid_dev(s), field, s->dgrad, ctrl,
+                                                                    el ? 1.0 : 2.0);
+        CK_LAUNCH();
+    }
+    if (s->grid.n_wide > 0) {
+        k_dens_grad_wide<<<blocks_for(s->grid.n_wide, kBlock), kBlock, 0, st>>>(
+            s->grid.n_wide, s->grid.wide, s->cell_xy, s->cell_wh, grid_dev(s), field, s->dgrad, ctrl, el ? 1.0 : 2.0);
+        CK_LAUNCH();
+    }
+}
+
+__global__ void k_add_dgrad(int n, const int* __restrict__ perm, const uint8_t* __restrict__ fixed,
+                            const double2* __restrict__ dgrad, const Sched* __restrict__ sched,
+                            const Ctrl* __restrict__ ctrl, double2* __restrict__ fold)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n || ctrl->stopped) return;
+    const int c = perm[i];
+    if (fixed[c]) return;
+    const double lambda = sched[ctrl->iter].lambda; // (what k_finalize publishes for this iteration)
+    const double2 g = dgrad[c], f = fold[c];
+    fold[c] = make_double2(f.x + lambda * g.x, f.y + lambda * g.y);
+}
+
+void launch_add_dgrad(tdpg_session* s, const Sched* sched, const Ctrl* ctrl, double2* fold, int lo, int hi)
+{
+    if (hi <= lo) return;
+    k_add_dgrad<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(hi - lo, s->grid.perm.p + lo, s->cell_fixed,
+                                                                   s->dgrad, sched, ctrl, fold);
+    CK_LAUNCH();
 }
 
 void launch_fold(tdpg_session* s, double2* out, const Ctrl* ctrl)

@@ -161,7 +161,8 @@ void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl);
 void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl);
 void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur);
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
-                  const IterCur* cur, Ctrl* ctrl, bool dens_grad = true, const double2* folded = nullptr);
+                  const IterCur* cur, Ctrl* ctrl, bool dens_grad = true, const double2* folded = nullptr,
+                  bool dgrad_folded = false);
 void launch_fold(tdpg_session* s, double2* out, const Ctrl* ctrl);
 void run_sta_async(tdpg_session* s, double* out3, bool pin_space = true);
 void ledger_apply_sorted(tdpg_session* s, long long H, double wns, double w0, double w1);

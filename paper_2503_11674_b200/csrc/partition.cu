@@ -109,6 +109,14 @@ void comm_allreduce(tdpg_session* s, double* buf, size_t n)
                "ncclAllReduce");
 }
 
+// Sum-all-reduce of the fixed-point density grid (int64: exact and order independent, so every rank holds
+// bitwise the single-GPU grid) on stream `st` (capturable).
+void comm_allreduce_i64(tdpg_session* s, long long* buf, size_t n, cudaStream_t st)
+{
+    nccl_check(nccl().all_reduce(buf, buf, n, ncclInt64, ncclSum, static_cast<ncclComm_t>(s->comm), st),
+               "ncclAllReduce (density grid)");
+}
+
 void comm_destroy(tdpg_session* s)
 {
     if (s->comm && nccl().comm_destroy) nccl().comm_destroy(static_cast<ncclComm_t>(s->comm));
@@ -187,6 +195,35 @@ int tdpg_comm_init(tdpg_session* s, int32_t rank, int32_t world, const uint8_t i
         nccl_check(nccl().comm_init_rank(&c, world, u, rank), "ncclCommInitRank");
         s->comm = c;
     }
+    API_END
+}
+
+// Device time of the partitioned iteration's two collectives alone (the int64 density grid, then the
+// gradient buffer of n_red doubles), averaged over `iters` back-to-back pairs on the session stream; every
+// rank must call it (collective).  The engine's buffers are reused: the grid is zero between iterations
+// and the gradient buffer is rebuilt by the next iteration.
+int tdpg_comm_bench(tdpg_session* s, int32_t iters, int64_t n_red, double ms[2])
+{
+    API_BEGIN
+    if (!s->comm) throw Error(TDPG_ERR_VALIDATION, "validation error: tdpg_comm_bench needs a communicator");
+    if (!s->grid.valid()) throw Error(TDPG_ERR_VALIDATION, "validation error: no density grid (engine_init first)");
+    DBuf<double> buf;
+    buf.alloc(static_cast<size_t>(std::max<int64_t>(n_red, 1)));
+    buf.zero(s->st);
+    cudaEvent_t e[3];
+    for (auto& x : e) CK(cudaEventCreate(&x));
+    float t0 = 0, t1 = 0;
+    const size_t B = static_cast<size_t>(s->grid.bins());
+    CK(cudaEventRecord(e[0], s->st));
+    for (int i = 0; i < iters; ++i) comm_allreduce_i64(s, s->grid.acc.p, B, s->st);
+    CK(cudaEventRecord(e[1], s->st));
+    for (int i = 0; i < iters; ++i) comm_allreduce(s, buf.p, static_cast<size_t>(n_red));
+    CK(cudaEventRecord(e[2], s->st));
+    CK(cudaEventSynchronize(e[2]));
+    CK(cudaEventElapsedTime(&t0, e[0], e[1]));
+    CK(cudaEventElapsedTime(&t1, e[1], e[2]));
+    for (auto& x : e) cudaEventDestroy(x);
+    ms[0] = t0 / std::max(iters, 1), ms[1] = t1 / std::max(iters, 1);
     API_END
 }
 

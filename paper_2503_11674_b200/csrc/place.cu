@@ -66,7 +66,8 @@ struct Engine {
     // caller) the iteration is two graphs around it
     bool partitioned = false;
     DBuf<double> red;
-    cudaGraphExec_t gexec_a = nullptr, gexec_b = nullptr;
+    cudaGraphExec_t gexec_a0 = nullptr, gexec_a = nullptr, gexec_b = nullptr; // split phase: scatter | rest | cells
+    int mov_lo = 0, mov_hi = 0; // this rank's slice of the spatial cell order (sharded density)
     cudaStream_t br[kBranches] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[kBranches] = {}, ev_bins = nullptr;
     ~Engine()
@@ -78,6 +79,7 @@ struct Engine {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_bins) cudaEventDestroy(ev_bins);
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (gexec_a0) cudaGraphExecDestroy(gexec_a0);
         if (gexec_a) cudaGraphExecDestroy(gexec_a);
         if (gexec_b) cudaGraphExecDestroy(gexec_b);
         if (graph) cudaGraphDestroy(graph);
@@ -281,14 +283,23 @@ void capture_iteration(tdpg_session* s, Engine& E)
         FinArgs fp = fa;
         fp.part_wl = r_wl, fp.part_hp = r_hp, fp.part_pp = r_pp;
         double2* folded = reinterpret_cast<double2*>(E.red.p);
-        // A: fork the (replicated) density chain, WA over this rank's nets, join, fold this rank's entries
-        auto record_a = [&] {
+        // Sharded iteration: fork; density branch: scatter of this rank's cell slice -> [int64 grid sum over
+        // ranks] -> bins (replicated) -> density gradient of the slice; WA branches over this rank's nets;
+        // join, fold this rank's entries + lambda * its cells' density gradient -> [sum over ranks] ->
+        // finalize -> cells (replicated Adam).
+        const int lo = E.mov_lo, hi = E.mov_hi;
+        auto scatter = [&] { launch_density_scatter_part(s, E.ctrl, lo, hi, s->part_rank == 0); };
+        auto record_a = [&](bool comm) {
             cudaStream_t main = s->st;
             CK(cudaEventRecord(E.ev_fork, main));
             for (int k = 0; k < Engine::kBranches; ++k) CK(cudaStreamWaitEvent(E.br[k], E.ev_fork, 0));
             s->st = E.br[0];
-            launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
-            launch_dens_grad(s, E.ctrl, E.br[0]);
+            if (comm) {
+                scatter();
+                comm_allreduce_i64(s, s->grid.acc.p, static_cast<size_t>(s->grid.bins()), E.br[0]);
+            }
+            launch_density_bins_ctrl(s, part_d, E.nb_d, E.ctrl);
+            launch_dens_grad_part(s, E.ctrl, E.br[0], lo, hi);
             s->st = main;
             cudaStream_t wa_st[Engine::kBranches] = {main};
             for (int k = 1; k < Engine::kBranches; ++k) wa_st[k] = E.br[k];
@@ -299,31 +310,27 @@ void capture_iteration(tdpg_session* s, Engine& E)
                 CK(cudaStreamWaitEvent(main, E.ev_join[k], 0));
             }
             launch_fold(s, folded, E.ctrl);
-        };
-        auto join_density = [&] {
             CK(cudaEventRecord(E.ev_join[0], E.br[0]));
-            CK(cudaStreamWaitEvent(s->st, E.ev_join[0], 0));
+            CK(cudaStreamWaitEvent(main, E.ev_join[0], 0));
+            launch_add_dgrad(s, E.sched, E.ctrl, folded, lo, hi);
         };
-        // B: terms from the reduced partials, cells from the reduced fold + replicated density gradient
+        // B: terms from the reduced partials, cells from the reduced fold (density gradient included)
         auto record_b = [&] {
             launch_finalize(s, fp, E.ctrl, E.cur);
             launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
-                         false, folded);
+                         false, folded, true);
         };
         const size_t n_red = static_cast<size_t>(C2) + 3 * static_cast<size_t>(E.nb_wa);
         s->part_active = true;
         if (s->comm) {
             E.gexec = capture(s, [&] {
-                record_a();
-                comm_allreduce(s, E.red.p, n_red); // overlaps the density branch
-                join_density();
+                record_a(true);
+                comm_allreduce(s, E.red.p, n_red);
                 record_b();
             });
         } else {
-            E.gexec_a = capture(s, [&] {
-                record_a();
-                join_density();
-            });
+            E.gexec_a0 = capture(s, scatter);
+            E.gexec_a = capture(s, [&] { record_a(false); });
             E.gexec_b = capture(s, record_b);
         }
         s->part_active = false;
@@ -579,6 +586,12 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->part.zero(s->st);
     E->kernels_per_iter = 8 + (s->grid.n_wide > 0 ? 2 : 0); // (+ wide-cell scatter and density gradient)
     E->partitioned = s->part_world > 1;
+    if (E->partitioned) { // this rank's slice of the spatial order (the density scatter / gradient share)
+        const long long nm = s->grid.n_movable;
+        E->mov_lo = static_cast<int>(nm * s->part_rank / s->part_world);
+        E->mov_hi = static_cast<int>(nm * (s->part_rank + 1) / s->part_world);
+        E->kernels_per_iter += 1; // (the lambda * density gradient fold)
+    }
     if (E->partitioned) { // entries of other ranks' nets must read as 0 in this rank's fold
         E->red.reserve(2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E->nb_wa) + 8);
         E->red.zero(s->st);
@@ -806,17 +819,31 @@ int engine_run(tdpg_session* s, int n)
     return done;
 }
 
-// Split-phase iteration for a partitioned engine without a communicator (the caller reduces):
-// phase A runs the scheduled refresh / re-sort and the pre-reduction graph and returns this rank's
+// Split-phase iteration for a partitioned engine without a communicator (the caller reduces twice):
+// phase 0 runs the scheduled refresh / re-sort and this rank's density scatter and returns its int64 grid;
+// phase A takes the summed grid, runs the rest of the pre-reduction graph and returns this rank's
 // all-reduce buffer; phase B takes the reduced buffer and finishes the iteration.
-size_t part_phase_a(tdpg_session* s, double* red_host)
+size_t part_phase_density(tdpg_session* s, long long* acc_host)
 {
     Engine& E = *s->eng;
-    if (!E.partitioned || !E.gexec_a) throw Error(TDPG_ERR_INTERNAL, "engine is not in split-phase partitioned mode");
+    if (!E.partitioned || !E.gexec_a0) throw Error(TDPG_ERR_INTERNAL, "engine is not in split-phase partitioned mode");
     ensure_graphs(s, E);
     const int it = E.launched;
     if (it >= E.cfg.timing_start_iter && (it - E.cfg.timing_start_iter) % E.cfg.m == 0) timing_refresh(s);
     if (it % E.sort_every == 0) CK(cudaGraphLaunch(E.sort_gexec, s->st));
+    CK(cudaGraphLaunch(E.gexec_a0, s->st));
+    const size_t B = static_cast<size_t>(s->grid.bins());
+    if (acc_host) s->grid.acc.download(acc_host, B, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    return B;
+}
+
+size_t part_phase_a(tdpg_session* s, const long long* acc_host, double* red_host)
+{
+    Engine& E = *s->eng;
+    if (!E.partitioned || !E.gexec_a) throw Error(TDPG_ERR_INTERNAL, "engine is not in split-phase partitioned mode");
+    const size_t B = static_cast<size_t>(s->grid.bins());
+    CK(cudaMemcpyAsync(s->grid.acc.p, acc_host, B * sizeof(long long), cudaMemcpyHostToDevice, s->st));
     CK(cudaGraphLaunch(E.gexec_a, s->st));
     const size_t n = 2 * static_cast<size_t>(s->C) + 3 * static_cast<size_t>(E.nb_wa);
     if (red_host) E.red.download(red_host, n, s->st);
@@ -989,11 +1016,21 @@ int tdpg_step_host(tdpg_session* s, const double* xy_in, double* xy_out, tdpg_tr
     API_END
 }
 
-int tdpg_part_step_a(tdpg_session* s, double* red, int64_t* n_red)
+int tdpg_part_density(tdpg_session* s, int64_t* acc, int64_t* n_bins)
 {
     API_BEGIN
     if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
-    const size_t n = part_phase_a(s, red);
+    const size_t n = part_phase_density(s, reinterpret_cast<long long*>(acc));
+    if (n_bins) *n_bins = static_cast<int64_t>(n);
+    API_END
+}
+
+int tdpg_part_step_a(tdpg_session* s, const int64_t* acc, double* red, int64_t* n_red)
+{
+    API_BEGIN
+    if (!s->eng) throw Error(TDPG_ERR_INTERNAL, "engine not initialised (tdpg_engine_init)");
+    if (!acc) throw Error(TDPG_ERR_VALIDATION, "validation error: tdpg_part_step_a needs the summed density grid");
+    const size_t n = part_phase_a(s, reinterpret_cast<const long long*>(acc), red);
     if (n_red) *n_red = static_cast<int64_t>(n);
     API_END
 }

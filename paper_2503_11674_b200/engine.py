@@ -111,7 +111,9 @@ _SIGS = {
     "tdpg_set_partition": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "tdpg_comm_unique_id": (C.c_int, [_P]),
     "tdpg_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, _P]),
-    "tdpg_part_step_a": (C.c_int, [_P, _P, _I64P]),
+    "tdpg_part_density": (C.c_int, [_P, _P, _I64P]),
+    "tdpg_comm_bench": (C.c_int, [_P, C.c_int32, C.c_int64, _P]),
+    "tdpg_part_step_a": (C.c_int, [_P, _P, _P, _I64P]),
     "tdpg_part_step_b": (C.c_int, [_P, _P]),
     "tdpg_paths_candidates": (C.c_int, [_P, _I64P]),
     "tdpg_k_worst": (C.c_int, [_P, C.c_int32, C.c_int32, _I32P, _P, _P, C.c_int32, _P]),
@@ -338,9 +340,24 @@ class Session:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         _check(self.lib.tdpg_comm_init(self.h, rank, world, buf))
 
-    def part_step_a_into(self, out: np.ndarray):
+    def comm_bench(self, iters=20):
+        """Device ms of the partitioned iteration's two all-reduces alone: (density grid, gradient buffer)."""
+        ms = (C.c_double * 2)()
+        _check(self.lib.tdpg_comm_bench(self.h, iters, red_size(self), ms))
+        return ms[0], ms[1]
+
+    def part_density_into(self, out: np.ndarray):
+        """Split phase 0: this rank's density scatter; its int64 grid into `out` (returns the bin count)."""
         n = C.c_int64()
-        _check(self.lib.tdpg_part_step_a(self.h, out.ctypes.data, C.byref(n)))
+        _check(self.lib.tdpg_part_density(self.h, out.ctypes.data if out is not None else None, C.byref(n)))
+        return n.value
+
+    def part_step_a_into(self, acc_total: np.ndarray, out: np.ndarray):
+        """Split phase A: the grid summed over ranks in, this rank's all-reduce buffer out (returns its size)."""
+        acc_total = np.ascontiguousarray(acc_total, np.int64)
+        n = C.c_int64()
+        _check(self.lib.tdpg_part_step_a(self.h, acc_total.ctypes.data, out.ctypes.data if out is not None else None,
+                                         C.byref(n)))
         return n.value
 
     def part_step_b(self, red: np.ndarray):

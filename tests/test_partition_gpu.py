@@ -1,8 +1,9 @@
 """The partitioned single-design mode on one GPU: G sessions, one per rank, each
-owning a net range; the test performs the all-reduce (element-wise sum of the ranks' buffers, the
-operation NCCL performs in the multi-GPU graph) between the split phases.  Checks: ranks stay bitwise
-identical (replicated density / Adam / timing refresh), and the trajectory equals the single-session
-engine's to rounding (only the fold's summation order differs: sum of per-rank partial folds)."""
+owning a net range and a slice of the cells' spatial order; the test performs both all-reduces (the
+int64 density grid, then the gradient buffer: element-wise sums, the operations NCCL performs in the
+multi-GPU graph) between the split phases.  Checks: the summed grid is bitwise the single-session grid,
+ranks stay bitwise identical (replicated bins / Adam / timing refresh), and the trajectory equals the
+single-session engine's to rounding (only the fold's summation order differs)."""
 import numpy as np
 import pytest
 
@@ -26,16 +27,22 @@ def _run_split(d, cfg, world, iters):
         s.engine_init(cfg)
         ss.append(s)
     n = red_size(ss[0])
+    B = cfg["grid_nx"] * cfg["grid_ny"]
     bufs = [np.zeros(n) for _ in ss]
+    accs = [np.zeros(B, np.int64) for _ in ss]
     for _ in range(iters):
+        for s, a in zip(ss, accs):
+            assert s.part_density_into(a) == B
+        acc = np.sum(accs, axis=0)  # (int64: exact)
         for s, b in zip(ss, bufs):
-            assert s.part_step_a_into(b) == n
+            assert s.part_step_a_into(acc, b) == n
         total = bufs[0].copy()
         for b in bufs[1:]:
             total += b
         for s in ss:
             s.part_step_b(total)
     return ss
+
 
 
 @pytest.mark.parametrize("world", [2, 3])
