@@ -15,6 +15,8 @@
 //   ledger    : sorted 64-bit pair keys (a<<32|b) + weights; per-pin incidence CSR
 #pragma once
 
+#include <functional>
+
 #include <array>
 #include <memory>
 #include <string>
@@ -216,6 +218,9 @@ struct tdpg_session {
     tdpg::DBuf<int2> kb_pred;
     tdpg::DBuf<int> kb_cnt;
     int kb_K = 0;
+    tdpg::DBuf<int> kb_dn;        // k-best engine refresh: device path / path-pin counts
+    tdpg::DBuf<long long> kb_H;   // ... and hit count
+    long long kb_hcap = 0;
     tdpg::KbScratch kbx;
     tdpg::DBuf<unsigned> kh_key, kh_key_s; // engine refresh with k > 1 / topn: hits keyed by sink pin
     tdpg::DBuf<int> kh_idx_s;
@@ -275,6 +280,20 @@ void build_graph_device(tdpg_session* s); // graph.cu
 void graph_host_level(tdpg_session* s);
 void graph_host_arcs(tdpg_session* s);
 void sta_setup(tdpg_session* s);
+bool capturing(tdpg_session* s);
+void pad_hit_keys(tdpg_session* s, long long cap, const long long* n_dev, unsigned* keys);
+int bits_for_pins(int P);
+void switch_hits_by_count(tdpg_session* s, const long long* d_n, long long cap,
+                          const std::function<void(cudaStream_t, long long)>& body);
+void refresh_begin(tdpg_session* s, Ctrl* ctrl, double* timing_row);
+void net_weights_record(tdpg_session* s, const Ctrl* ctrl);
+void sort_violated_endpoints(tdpg_session* s, const Ctrl* ctrl);
+void sta_record(tdpg_session* s, double* out3, bool pin_space);
+void kbest_refresh_reserve(tdpg_session* s, int K);
+void refresh_record_kbest(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting,
+                          int K);
+void kbest_refresh_publish(tdpg_session* s);
+void kbest_check(tdpg_session* s);
 void sta_materialize_pins(tdpg_session* s); // per-pin STA arrays of an L-space-only sweep (timing.cu)
 void place_tail_reserve(tdpg_session* s); // (timing.cu)
 void ensure_grid(tdpg_session* s, int nx, int ny, double td);
@@ -296,6 +315,20 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
 // timing.cu
 void run_sta_dev(tdpg_session* s, bool pin_space = true); // pin_space = false: results left in L-space
 void sta_setup(tdpg_session* s);
+bool capturing(tdpg_session* s);
+void pad_hit_keys(tdpg_session* s, long long cap, const long long* n_dev, unsigned* keys);
+int bits_for_pins(int P);
+void switch_hits_by_count(tdpg_session* s, const long long* d_n, long long cap,
+                          const std::function<void(cudaStream_t, long long)>& body);
+void refresh_begin(tdpg_session* s, Ctrl* ctrl, double* timing_row);
+void net_weights_record(tdpg_session* s, const Ctrl* ctrl);
+void sort_violated_endpoints(tdpg_session* s, const Ctrl* ctrl);
+void sta_record(tdpg_session* s, double* out3, bool pin_space);
+void kbest_refresh_reserve(tdpg_session* s, int K);
+void refresh_record_kbest(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting,
+                          int K);
+void kbest_refresh_publish(tdpg_session* s);
+void kbest_check(tdpg_session* s);
 void refresh_reserve(tdpg_session* s);
 void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting);
 void dense_ledger_to_sorted(tdpg_session* s);

@@ -328,6 +328,106 @@ void exclusive_scan(tdpg_session* s, const int* in, int* out, int n)
 
 } // namespace
 
+// ---- the engine's timing refresh with k > 1 paths per endpoint (report_timing_endpoint(n, k),
+// placer.cpp:424-429) as one captured graph: every count lives on the device, buffers are sized for the
+// worst case (every endpoint violated, k paths each, L + 1 pins per path), sorts run over the smallest
+// size class holding the data (conditional graph node) — no host synchronisation inside the loop.
+__device__ __forceinline__ int active_nv(const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl)
+{
+    return (!ctrl->stopped && sta_out[1] < 0.0) ? static_cast<int>(sta_out[2]) : 0;
+}
+
+__global__ void k_kb_count_dev(int cap, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                               const int* __restrict__ ep, int per, const int2* __restrict__ kp,
+                               const int* __restrict__ kc, int K, int* __restrict__ npath, int* __restrict__ npins)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= cap) return;
+    if (i >= active_nv(sta_out, ctrl)) {
+        npath[i] = 0, npins[i] = 0;
+        return;
+    }
+    const int e = ep[i], c = min(per, kc[e]);
+    int pins = 0;
+    for (int r = 0; r < c; ++r) pins += kb_len(kp, K, e, r);
+    npath[i] = c, npins[i] = pins;
+}
+
+__global__ void k_kb_write_dev(int cap, const double* __restrict__ sta_out, const Ctrl* __restrict__ ctrl,
+                               const int* __restrict__ ep, const int* __restrict__ npath, const int* __restrict__ poff,
+                               const int* __restrict__ pinoff, const int2* __restrict__ kp,
+                               const double* __restrict__ kd, int K, double clock, int* __restrict__ start,
+                               int* __restrict__ len, int* __restrict__ pins, double* __restrict__ slack)
+{
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= cap || i >= active_nv(sta_out, ctrl)) return;
+    const int e = ep[i];
+    int o = pinoff[i];
+    for (int r = 0; r < npath[i]; ++r) {
+        const int p = poff[i] + r, n = kb_len(kp, K, e, r);
+        start[p] = o, len[p] = n;
+        slack[p] = clock - kd[static_cast<size_t>(e) * K + r];
+        int v = e, rr = r;
+        for (int k = o + n - 1; k >= o; --k) {
+            pins[k] = v;
+            const int2 q = kp[static_cast<size_t>(v) * K + rr];
+            v = q.x, rr = q.y;
+        }
+        o += n;
+    }
+}
+
+// totals of a capacity-sized count / exclusive-offset pair: out = off[n-1] + cnt[n-1]
+__global__ void k_kb_totals(int n, const int* __restrict__ poff, const int* __restrict__ npath,
+                            const int* __restrict__ pinoff, const int* __restrict__ npins, int* __restrict__ dn,
+                            long long* __restrict__ ex_counts)
+{
+    const int np = poff[n - 1] + npath[n - 1], pins = pinoff[n - 1] + npins[n - 1];
+    dn[0] = np, dn[1] = pins;
+    ex_counts[0] = np, ex_counts[1] = pins;
+    ex_counts[3] += np, ex_counts[4] += pins; // (engine totals, tdpg_engine_paths)
+}
+
+__global__ void k_path_hops_dev(int cap, const int* __restrict__ dn, const int* __restrict__ start,
+                                const int* __restrict__ len, const int* __restrict__ pins,
+                                const uint8_t* __restrict__ pin_dir, int* __restrict__ hops)
+{
+    const int p = blockIdx.x * kBlock + threadIdx.x;
+    if (p >= cap) return;
+    int h = 0;
+    if (p < dn[0])
+        for (int k = start[p]; k + 1 < start[p] + len[p]; ++k) h += pin_dir[pins[k]] == 1;
+    hops[p] = h;
+}
+
+__global__ void k_hits_total(int n, const int* __restrict__ hoff, const int* __restrict__ hops,
+                             long long* __restrict__ H, long long* __restrict__ ex_counts)
+{
+    H[0] = static_cast<long long>(hoff[n - 1]) + hops[n - 1];
+    ex_counts[2] = H[0];
+}
+
+// collect_pin_pairs (paths.cpp:191-203) keyed by sink pin for the dense ledger (pin_pairs.cpp:11)
+__global__ void k_path_hits_dev(int cap, const int* __restrict__ dn, const int* __restrict__ start,
+                                const int* __restrict__ len, const int* __restrict__ pins,
+                                const double* __restrict__ slack, const uint8_t* __restrict__ pin_dir,
+                                const int* __restrict__ hoff, double* __restrict__ hslack, int* __restrict__ hidx,
+                                unsigned* __restrict__ sink_key)
+{
+    const int p = blockIdx.x * kBlock + threadIdx.x;
+    if (p >= cap || p >= dn[0]) return;
+    int h = hoff[p];
+    const double sl = slack[p];
+    for (int k = start[p]; k + 1 < start[p] + len[p]; ++k) {
+        const int u = pins[k], v = pins[k + 1];
+        if (pin_dir[u] != 1) continue;
+        hslack[h] = sl;
+        hidx[h] = h;
+        sink_key[h] = sl < 0.0 ? static_cast<unsigned>(v) : 0xFFFFFFFFu;
+        ++h;
+    }
+}
+
 // The K-best lists of every pin at the current STA's pin positions.
 void kbest_build(tdpg_session* s, int K)
 {
@@ -354,8 +454,123 @@ void kbest_build(tdpg_session* s, int K)
         if (hi > lo) k_kbest_level<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(lo, hi, a);
     }
     CK_LAUNCH();
+    if (capturing(s)) return; // (the engine checks the flag after its run: kbest_check)
     if (read1(s, s->counters.p + 2))
         throw Error(TDPG_ERR_INTERNAL, "path enumeration: a pin has more than 32 in-arcs");
+}
+
+void kbest_check(tdpg_session* s)
+{
+    if (s->kb_K > 0 && read1(s, s->counters.p + 2))
+        throw Error(TDPG_ERR_INTERNAL, "path enumeration: a pin has more than 32 in-arcs");
+}
+
+// Worst-case capacities of the k-best engine refresh (every endpoint violated, K paths of <= L + 1 pins
+// and <= (L + 1) / 2 + 1 hops each); every buffer sized before capture.
+void kbest_refresh_reserve(tdpg_session* s, int K)
+{
+    const size_t P = static_cast<size_t>(std::max(s->P, 1));
+    if (s->kb_K != K) {
+        s->kb_delay.alloc(P * K), s->kb_pred.alloc(P * K);
+        s->kb_K = K;
+    }
+    s->kb_cnt.reserve(P);
+    s->counters.reserve(8);
+    const long long EP = std::max(s->EP, 1), L = std::max(s->L, 1);
+    const long long npc = EP * K, pinc = npc * (L + 1), hc = npc * ((L + 1) / 2 + 1);
+    if (pinc > INT_MAX || hc > INT_MAX)
+        throw Error(TDPG_ERR_VALIDATION, "validation error: k = " + std::to_string(K) +
+                                             " paths per endpoint exceed the 2^31 path-pin capacity for this design");
+    KbScratch& X = s->kbx;
+    X.npath.reserve(EP), X.npins.reserve(EP), X.poff.reserve(EP), X.pinoff.reserve(EP);
+    X.cstart.reserve(npc + 1), X.clen.reserve(npc + 1), X.cslack.reserve(npc + 1), X.cpins.reserve(pinc + 1);
+    X.flag.reserve(npc + 1), X.order.reserve(npc + 1); // (hops / hop offsets)
+    s->kh_key.reserve(hc + 1), s->kh_key_s.reserve(hc + 1), s->kh_idx_s.reserve(hc + 1);
+    s->hit_slack.reserve(hc + 1), s->hit_idx.reserve(hc + 1);
+    s->kb_dn.reserve(4), s->kb_H.reserve(2);
+    s->kb_hcap = hc;
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b1, X.npath.p, X.poff.p, static_cast<int>(npc), s->st);
+    cub::DeviceRadixSort::SortPairs(nullptr, b2, s->kh_key.p, s->kh_key_s.p, s->hit_idx.p, s->kh_idx_s.p,
+                                    static_cast<int>(hc), 0, 32, s->st);
+    cub_scratch(s, std::max(b1, b2));
+}
+
+void launch_ledger_update(tdpg_session* s, long long cap, const LedgerArgs& a);
+
+// The k > 1 endpoint-policy refresh (placer.cpp:415-435): STA with per-pin results, violated endpoints
+// in (slack, pin) order, the k-best lists, the first k paths of every violated endpoint, their hits keyed
+// by sink pin, the dense-ledger update, net weights.  Recorded into the engine's refresh graph.
+void refresh_record_kbest(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1,
+                          bool net_weighting, int K)
+{
+    sta_record(s, s->sta_out, true); // (the k-best merge reads per-pin arrival and positions)
+    refresh_begin(s, ctrl, timing_row);
+    const int EP = s->EP;
+    if (EP == 0) return;
+    sort_violated_endpoints(s, ctrl);
+    kbest_build(s, K);
+    KbScratch& X = s->kbx;
+    const int npc = EP * K;
+    k_kb_count_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, K, s->kb_pred,
+                                                                 s->kb_cnt, K, X.npath, X.npins);
+    CK_LAUNCH();
+    size_t b = s->cub_tmp.n;
+    CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, b, X.npath.p, X.poff.p, EP, s->st));
+    b = s->cub_tmp.n;
+    CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, b, X.npins.p, X.pinoff.p, EP, s->st));
+    k_kb_write_dev<<<blocks_for(EP, kBlock), kBlock, 0, s->st>>>(EP, s->sta_out, ctrl, s->sort_v1, X.npath, X.poff,
+                                                                 X.pinoff, s->kb_pred, s->kb_delay, K, s->clock,
+                                                                 X.cstart, X.clen, X.cpins, X.cslack);
+    CK_LAUNCH();
+    k_kb_totals<<<1, 1, 0, s->st>>>(EP, X.poff, X.npath, X.pinoff, X.npins, s->kb_dn, s->ex_counts);
+    CK_LAUNCH();
+    int* hops = X.flag.p;
+    int* hoff = X.order.p;
+    k_path_hops_dev<<<blocks_for(npc, kBlock), kBlock, 0, s->st>>>(npc, s->kb_dn, X.cstart, X.clen, X.cpins,
+                                                                   s->pin_dir, hops);
+    CK_LAUNCH();
+    b = s->cub_tmp.n;
+    CK(cub::DeviceScan::ExclusiveSum(s->cub_tmp.p, b, hops, hoff, npc, s->st));
+    k_hits_total<<<1, 1, 0, s->st>>>(npc, hoff, hops, s->kb_H, s->ex_counts);
+    CK_LAUNCH();
+    k_path_hits_dev<<<blocks_for(npc, kBlock), kBlock, 0, s->st>>>(npc, s->kb_dn, X.cstart, X.clen, X.cpins,
+                                                                   X.cslack, s->pin_dir, hoff, s->hit_slack,
+                                                                   s->hit_idx, s->kh_key);
+    CK_LAUNCH();
+    pad_hit_keys(s, s->kb_hcap, s->kb_H.p, s->kh_key.p);
+    const int kbits = bits_for_pins(s->P);
+    switch_hits_by_count(s, s->kb_H.p, s->kb_hcap, [&](cudaStream_t st, long long n) {
+        size_t bb = s->cub_tmp.n;
+        CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bb, s->kh_key.p, s->kh_key_s.p, s->hit_idx.p, s->kh_idx_s.p,
+                                           static_cast<int>(n), 0, kbits, st));
+    });
+    LedgerArgs la{};
+    la.n_hits = s->kb_H.p, la.H = s->kb_hcap, la.sta_out = s->sta_out, la.ctrl = ctrl, la.gen = true;
+    la.hk = s->kh_key_s, la.hidx = s->kh_idx_s, la.hslack = s->hit_slack, la.w0 = w0, la.w1 = w1;
+    la.dl_w = s->dl_w, la.ppw_e = s->ppw_e, la.pin_entry = s->pin_entry, la.pin_loc = s->pin_loc;
+    la.pp_mask = s->pp_mask, la.q_count = s->q_count;
+    launch_ledger_update(s, s->kb_hcap, la);
+    if (net_weighting && s->N) net_weights_record(s, ctrl);
+}
+
+// Observer rounds of the k-best refresh: this round's paths into the session's report buffers.
+void kbest_refresh_publish(tdpg_session* s)
+{
+    int dn[2];
+    CK(cudaMemcpyAsync(dn, s->kb_dn.p, sizeof dn, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    const int np = dn[0];
+    const long long pins = dn[1];
+    KbScratch& X = s->kbx;
+    s->ex_off.reserve(np + 1), s->ex_len.reserve(np + 1), s->ex_slack.reserve(np + 1), s->ex_pins.reserve(pins + 1);
+    if (np > 0) {
+        CK(cudaMemcpyAsync(s->ex_off.p, X.cstart.p, sizeof(int) * np, cudaMemcpyDeviceToDevice, s->st));
+        CK(cudaMemcpyAsync(s->ex_len.p, X.clen.p, sizeof(int) * np, cudaMemcpyDeviceToDevice, s->st));
+        CK(cudaMemcpyAsync(s->ex_slack.p, X.cslack.p, sizeof(double) * np, cudaMemcpyDeviceToDevice, s->st));
+        CK(cudaMemcpyAsync(s->ex_pins.p, X.cpins.p, sizeof(int) * pins, cudaMemcpyDeviceToDevice, s->st));
+    }
+    s->n_paths = np, s->n_path_pins = pins, s->n_hits = 0, s->candidates = np;
 }
 
 // Endpoint-sorted violated endpoints of the current STA (paths.cpp:77-87) into sort_v1; returns their count.

@@ -375,6 +375,8 @@ void capture_iteration(tdpg_session* s, Engine& E)
 
 } // namespace
 
+void record_refresh(tdpg_session* s, Engine& E);
+
 // TDPG_TRACE_INIT=1: engine_init phase times on stderr (host clock, stream synchronised)
 struct InitTrace {
     bool on = false;
@@ -603,6 +605,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     // every buffer the graphs touch is sized before capture, so their pointers never move
     tr.mark("schedule + buffers");
     refresh_reserve(s);
+    if (E->cfg.extraction == 0 && E->cfg.k > 1) kbest_refresh_reserve(s, E->cfg.k); // (the k-best refresh graph)
     s->ex_counts.zero(s->st); // (the refresh graph accumulates the run's path totals in [3], [4])
     place_tail_reserve(s); // (so a later run of the session finds every buffer where its graphs point)
     s->pin_xy_external = false;
@@ -614,9 +617,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
         Engine::session_consts(s, G.consts);
         capture_iteration(s, G);
         tr.mark("iteration graph");
-        G.refresh_gexec = capture(s, [&] {
-            refresh_record(s, G.ctrl, G.timing_row, G.cfg.w0, G.cfg.w1, G.cfg.net_weighting != 0);
-        });
+        G.refresh_gexec = capture(s, [&] { record_refresh(s, G); });
         G.refresh_lonly = s->pins_stale, s->pins_stale = false; // (recorded, not run)
         tr.mark("refresh graph");
         G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
@@ -671,6 +672,17 @@ __global__ void k_refresh_begin_gen(const double* sta_out, Ctrl* ctrl, double* t
 }
 
 void net_weights_engine(tdpg_session* s, const Ctrl* ctrl);
+
+// The engine's timing refresh as recorded into its graph: k = 1 (one backtrace per violated endpoint,
+// timing.cu refresh_record) or k > 1 (the k-best lists, kpaths.cu refresh_record_kbest).  The topn policy
+// grows its list length until the report is complete, a host-driven loop: timing_refresh_general.
+void record_refresh(tdpg_session* s, Engine& E)
+{
+    if (E.cfg.extraction == 0 && E.cfg.k > 1)
+        refresh_record_kbest(s, E.ctrl, E.timing_row, E.cfg.w0, E.cfg.w1, E.cfg.net_weighting != 0, E.cfg.k);
+    else
+        refresh_record(s, E.ctrl, E.timing_row, E.cfg.w0, E.cfg.w1, E.cfg.net_weighting != 0);
+}
 
 // Timing round with k > 1 or the topn policy (placer.cpp:415-435): STA graph, then the k-best
 // extraction (host-sized: the path count is data dependent), then the dense-ledger update and net
@@ -727,10 +739,11 @@ void timing_refresh_general(tdpg_session* s)
 void timing_refresh(tdpg_session* s)
 {
     Engine& E = *s->eng;
-    if (E.cfg.extraction != 0 || E.cfg.k != 1) {
+    if (E.cfg.extraction != 0) {
         timing_refresh_general(s);
         return;
     }
+    const bool kbest = E.cfg.k > 1;
     std::pair<cudaEvent_t, cudaEvent_t> ev;
     CK(cudaEventCreate(&ev.first));
     CK(cudaEventCreate(&ev.second));
@@ -740,8 +753,10 @@ void timing_refresh(tdpg_session* s)
     CK(cudaEventRecord(ev.second, s->st));
     E.refresh_ev.push_back(ev);
     // our kernels: pin_xy, 2 per level, slack keys, sta final, begin, ties, bt count, fill, bt write,
-    // counts, violated count + two size-class picks, ledger short + long runs (+ net weights)
-    E.kernel_launches += 2LL * s->L + 14 + (E.cfg.net_weighting ? 1 : 0);
+    // counts, violated count + two size-class picks, ledger short + long runs (+ net weights); k > 1:
+    // the STA, begin, violated count + pick, one k-best merge per level, count, write, totals, hops, hit
+    // total, hits, key pad, pick, ledger short + long runs (+ net weights)
+    E.kernel_launches += (kbest ? 3LL * s->L + 17 : 2LL * s->L + 14) + (E.cfg.net_weighting ? 1 : 0);
     ++E.refreshes;
     if (s->round_cb) { // TimingRoundObserver (placer.cpp:434): this round's annotation and report
         sta_materialize_pins(s); // the observer may read per-pin timing
@@ -751,7 +766,9 @@ void timing_refresh(tdpg_session* s)
         CK(cudaMemcpyAsync(c, s->ex_counts.p, sizeof c, cudaMemcpyDeviceToHost, s->st));
         unsigned long long* u = E.obs_count;
         CK(cudaMemsetAsync(u, 0, sizeof *u, s->st));
-        k_count_heads32<<<148 * 4, kBlock, 0, s->st>>>(s->hcap, s->ex_counts.p + 2, s->eh_key_s, u);
+        if (kbest) kbest_refresh_publish(s);
+        k_count_heads32<<<148 * 4, kBlock, 0, s->st>>>(kbest ? s->kb_hcap : s->hcap, s->ex_counts.p + 2,
+                                                        kbest ? s->kh_key_s.p : s->eh_key_s.p, u);
         CK_LAUNCH();
         unsigned long long uq = 0;
         CK(cudaMemcpyAsync(&uq, u, sizeof uq, cudaMemcpyDeviceToHost, s->st));
@@ -759,6 +776,7 @@ void timing_refresh(tdpg_session* s)
         s->tns = h[0], s->wns = h[1];
         s->sta_valid = true, s->ties_resolved = true;
         s->n_paths = static_cast<int>(c[0]), s->n_path_pins = c[1], s->n_hits = 0;
+        if (kbest) s->ties_resolved = false, s->candidates = c[0]; // (k-best paths need no tie resolution)
         s->uniq_pairs = s->n_paths ? static_cast<long long>(uq) : 0;
         s->round_cb(s->round_user, E.launched);
     }
@@ -782,9 +800,7 @@ void ensure_graphs(tdpg_session* s, Engine& E)
     if (E.gexec_b) cudaGraphExecDestroy(E.gexec_b), E.gexec_b = nullptr;
     capture_iteration(s, E);
     if (E.refresh_gexec) cudaGraphExecDestroy(E.refresh_gexec);
-    E.refresh_gexec = capture(s, [&] {
-        refresh_record(s, E.ctrl, E.timing_row, E.cfg.w0, E.cfg.w1, E.cfg.net_weighting != 0);
-    });
+    E.refresh_gexec = capture(s, [&] { record_refresh(s, E); });
     E.refresh_lonly = s->pins_stale, s->pins_stale = false;
     if (E.sort_gexec) cudaGraphExecDestroy(E.sort_gexec);
     E.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
@@ -1095,6 +1111,7 @@ int tdpg_place(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_expli
     engine_init(s, cfg, pos_explicit);
     InitTrace tr(s);
     engine_run(s, cfg->max_iters);
+    if (cfg->extraction == 0 && cfg->k > 1) kbest_check(s); // (the captured k-best merge's in-arc flag)
     tr.mark("place: device loop");
     const Ctrl c = read_ctrl(s);
     if (c.nonfinite_at != INT_MAX)

@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <functional>
 #include <array>
 #include <climits>
 #include <cmath>
@@ -1430,8 +1431,6 @@ __global__ void k_fill_hit_pad(long long cap, const long long* __restrict__ n_hi
         p[i] = 0xFFFFFFFFu;
 }
 
-// update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin;
-// the head of each group applies the group's additions in hit order.
 // update_pair_weights (pin_pairs.cpp:7-15) on the dense ledger: hits sorted stably by sink pin, so a
 // pair's hits are one contiguous run in hit order and its weight is the serial sum over that run (kept
 // serial: bitwise the reference's left-to-right additions).  Two kernels on two graph branches:
@@ -1748,17 +1747,51 @@ void switch_by_count(tdpg_session* s, const long long* d_n, long long cap, F&& b
 }
 
 // The whole refresh, stream-ordered and host-sync-free (captured by the engine).
-void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting)
+// 0xFFFFFFFF keys past the device hit count, up to the size class the following sort may pick (or the
+// whole capacity when size classes are off), so the sorted prefix holds exactly the hits.
+void pad_hit_keys(tdpg_session* s, long long cap, const long long* n_dev, unsigned* keys)
 {
-    // net weighting reads every pin's slack: keep the per-pin arrays then
-    sta_record(s, s->sta_out, net_weighting);
-    const bool lonly = s->pins_stale;
+    if (!size_classes_apply(s, cap))
+        k_fill_u32<<<std::min<unsigned>(blocks_for(cap, kBlock), 148 * 8), kBlock, 0, s->st>>>(cap, keys, 0xFFFFFFFFu);
+    else
+        k_fill_hit_pad<<<std::min<unsigned>(blocks_for(cap, kBlock), 148 * 8), kBlock, 0, s->st>>>(cap, n_dev, keys);
+    CK_LAUNCH();
+}
+
+bool capturing(tdpg_session* s)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s->st, &cs));
+    return cs == cudaStreamCaptureStatusActive;
+}
+
+int bits_for_pins(int P) { return bits_for(P); }
+
+void switch_hits_by_count(tdpg_session* s, const long long* d_n, long long cap,
+                          const std::function<void(cudaStream_t, long long)>& body)
+{
+    switch_by_count(s, d_n, cap, body);
+}
+
+void refresh_begin(tdpg_session* s, Ctrl* ctrl, double* timing_row)
+{
     k_refresh_begin<<<1, 1, 0, s->st>>>(s->sta_out, ctrl, timing_row);
     CK_LAUNCH();
+}
+
+void net_weights_record(tdpg_session* s, const Ctrl* ctrl)
+{
+    k_net_weights_dev<<<blocks_for(s->N, kBlock), kBlock, 0, s->st>>>(s->N, s->net_start, s->net_pins, s->slack,
+                                                                      s->sta_out, ctrl, s->net_w);
+    CK_LAUNCH();
+}
+
+// The endpoints in (slack, pin) order into sort_v1 (paths.cpp:77-87), from the keys sta_record left in
+// sort_k0 / sort_v0.  Readers take only the first (violated-count) entries: when few fail, compact them
+// stably and sort the smallest size class holding them; else sort every endpoint.  Capturable.
+void sort_violated_endpoints(tdpg_session* s, const Ctrl* ctrl)
+{
     const int EP = s->EP;
-    if (EP == 0) return;
-    // the walk reads only the first (violated-count) sorted endpoints: when few fail, compact them
-    // stably and sort the smallest size class holding them; else sort every endpoint
     k_ep_violated<<<1, 1, 0, s->st>>>(s->sta_out, ctrl, s->ep_nv);
     CK_LAUNCH();
     switch_by_count(s, s->ep_nv.p, EP, [&](cudaStream_t st, long long n) {
@@ -1780,6 +1813,18 @@ void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, 
         CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, b, s->ep_kc.p, s->sort_k1.p, s->ep_vc.p, s->sort_v1.p,
                                            static_cast<int>(n), 0, 64, st));
     });
+}
+
+void refresh_record(tdpg_session* s, Ctrl* ctrl, double* timing_row, double w0, double w1, bool net_weighting)
+{
+    // net weighting reads every pin's slack: keep the per-pin arrays then
+    sta_record(s, s->sta_out, net_weighting);
+    const bool lonly = s->pins_stale;
+    k_refresh_begin<<<1, 1, 0, s->st>>>(s->sta_out, ctrl, timing_row);
+    CK_LAUNCH();
+    const int EP = s->EP;
+    if (EP == 0) return;
+    sort_violated_endpoints(s, ctrl);
     size_t bytes = 0;
     const int S = s->L + 1, SH = s->L / 2 + 2; // (k_bt_walk's slot strides)
     if (lonly) { // one backtrace pass into fixed-stride slots, packed after the scans (k_bt_compact)

@@ -476,3 +476,27 @@ def test_repeated_runs_follow_changed_constraints():
     row = s2.step_host(None, None)
     assert row.iter == 10 and row.has_timing
     assert row.wns == want["wns"] and abs(row.tns - want["tns"]) <= 1e-12 * abs(want["tns"])
+
+
+@pytest.mark.parametrize("cells,k", [(3000, 3), (200000, 10)])
+def test_engine_kbest_refresh_ledger_bitwise(cells, k):
+    """The engine's k > 1 endpoint-policy refresh (one captured graph, no host synchronisation): after one
+    timing round at the run's start the dense ledger equals update_pair_weights over the oracle's own
+    report_timing_endpoint(all violated, k) hits, bitwise; path totals match."""
+    d = generate(seed=6, cells=cells, fail_frac=0.5, calibrate=False)
+    xy = spread_positions(d, 2)
+    d.clock_period = float(np.quantile(Oracle(d).sta(xy)["arr"][d.endpoints], 0.5))
+    d.positions = xy
+    d.pos_explicit = np.ones(d.n_cells, np.uint8)
+    cfg = {"max_iters": 1, "timing_start_iter": 0, "m": 5, "grid_nx": 32, "grid_ny": 32, "seed": 6, "k": k}
+    s = Session(d)
+    ps = s.place(cfg)
+    o = Oracle(d)
+    t = o.sta(xy)
+    eo = o.extract(xy, n=0, k=k)
+    lo = o.pp_update(None, eo["hits"], t["wns"])
+    ls = ps["ledger"]
+    assert ls[0].size == lo[0].size > 0
+    for x, y in zip(ls, lo):
+        assert np.array_equal(x, y)
+    assert s.engine_stats()["paths"] == eo["n_paths"]
