@@ -58,6 +58,9 @@ struct Grid {
     DBuf<double> excess;
     DBuf<double> base; // fixed-cell exact overlap (density.cpp:75-93), when any fixed cell
     DBuf<int> perm, perm_tmp;  // movable cells in spatial (tile) order, for the windowed scatter
+    // positions and sizes of the cells in that order, written by the scatter (coalesced) so the density
+    // gradient streams them instead of repeating the perm -> cell gather chain
+    DBuf<double2> xy_sp, wh_sp;
     DBuf<unsigned> perm_keys;
     int n_movable = 0;
     // movable cells that may span more than five bins on an axis (width > 1.99 pitch): their density

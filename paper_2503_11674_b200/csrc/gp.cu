@@ -767,7 +767,8 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
                                                                 const double2* __restrict__ cell_xy,
                                                                 const double2* __restrict__ cell_wh, GridDev g,
                                                                 unsigned long long* __restrict__ acc,
-                                                                const Ctrl* __restrict__ ctrl)
+                                                                const Ctrl* __restrict__ ctrl,
+                                                                double2* __restrict__ xy_sp, double2* __restrict__ wh_sp)
 {
     __shared__ unsigned win_lo[kWinBins], win_hi[kWinBins];
     __shared__ int bb[4];
@@ -782,6 +783,7 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
     if (valid) {
         const int c = perm[i];
         p = cell_xy[c], s = cell_wh[c];
+        xy_sp[i] = p, wh_sp[i] = s; // (for k_dens_grad)
         // cells of Grid::wide are scattered by k_density_scatter_wide; every other cell spans at most
         // 1.99 pitches, so its footprint has at most five bins per axis (axis5 succeeds)
         fast = !(s.x > g.wide_w || s.y > g.wide_h) &&
@@ -1008,6 +1010,95 @@ __global__ void __launch_bounds__(kFinBlock) k_finalize(FinArgs a, Ctrl* ctrl, I
     ctrl->iter = it + 1;
 }
 
+// The two halves of k_finalize (engine iteration graph).  Each series is reduced with exactly
+// k_finalize's thread layout and tree, so the terms are bitwise the single kernel's.
+template <int K>
+__device__ __forceinline__ bool fin_reduce(const double* const (&p)[K], const int (&n)[K], const int (&stride)[K],
+                                           const int (&off)[K], double (&r)[K])
+{
+    for (int k = 0; k < K; ++k) r[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        for (int i0 = threadIdx.x; i0 < n[k]; i0 += 8 * kFinBlock) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * kFinBlock;
+                v[u] = i < n[k] ? p[k][static_cast<long long>(i) * stride[k] + off[k]] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) r[k] += v[u];
+        }
+    __shared__ double sh[K][kFinBlock / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) r[k] = warp_sum(r[k]);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[k][w] = r[k];
+    __syncthreads();
+    if (w != 0) return false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) r[k] = warp_sum(lane < kFinBlock / 32 ? sh[k][lane] : 0.0);
+    return threadIdx.x == 0;
+}
+
+__global__ void __launch_bounds__(kFinBlock) k_fin_density(FinArgs a, Ctrl* ctrl, IterCur* cur)
+{
+    __shared__ int skip;
+    if (threadIdx.x == 0) skip = ctrl->stopped;
+    __syncthreads();
+    if (skip) {
+        if (threadIdx.x == 0) cur->do_adam = 0, cur->live = 0;
+        return;
+    }
+    double r[2];
+    if (!fin_reduce<2>({a.part_d, a.part_d}, {a.nb_d, a.nb_d}, {2, 2}, {0, 1}, r)) return;
+    const int it = ctrl->iter;
+    const double lambda = a.sched ? a.sched[it].lambda : a.lambda_single;
+    const double overflow = a.total_movable > 0.0 ? r[1] / a.total_movable : 0.0;
+    cur->lambda = lambda, cur->iter = it, cur->do_adam = 0, cur->live = 1;
+    cur->density = r[0], cur->overflow = overflow;
+    if (ctrl->engaged && overflow <= a.stop_overflow) { // placer.cpp:459-462
+        ctrl->stopped = 1;
+        return;
+    }
+    if (a.sched) {
+        cur->lr = a.sched[it].lr, cur->c1 = a.sched[it].c1, cur->c2 = a.sched[it].c2;
+        cur->do_adam = 1;
+    }
+    ctrl->iter = it + 1;
+}
+
+__global__ void __launch_bounds__(kFinBlock) k_fin_terms(FinArgs a, Ctrl* ctrl, const IterCur* cur)
+{
+    if (!cur->live) return; // (uniform)
+    double r[3];
+    if (!fin_reduce<3>({a.part_wl, a.part_hp, a.part_pp}, {a.nb_wa, a.nb_wa, a.nb_pp}, {1, 1, 1}, {0, 0, 0}, r))
+        return;
+    const int it = cur->iter;
+    const double lambda = cur->lambda;
+    Terms t;
+    t.wl = r[0], t.hpwl = r[1], t.pp = a.nb_pp ? r[2] : 0.0, t.density = cur->density;
+    t.overflow = cur->overflow;
+    t.value = t.wl + lambda * t.density + a.beta * t.pp;
+    *a.terms = t;
+    const bool finite = isfinite(t.value) && isfinite(t.wl) && isfinite(t.density) && isfinite(t.pp);
+    if (!finite) atomicMin(&ctrl->nonfinite_at, it);
+    if (a.trace) {
+        TraceRowDev row;
+        row.iter = it;
+        row.has_timing = a.timing_row && a.timing_row[0] != 0.0;
+        row.tns = row.has_timing ? a.timing_row[1] : 0.0;
+        row.wns = row.has_timing ? a.timing_row[2] : 0.0;
+        row.hpwl = t.hpwl, row.overflow = t.overflow, row.wl_term = t.wl, row.density_term = t.density;
+        row.pp_term = t.pp, row.lambda = lambda, row.beta_pp = a.beta * t.pp;
+        a.trace[it] = row;
+    }
+    if (a.timing_row_clear) a.timing_row_clear[0] = 0.0;
+    ctrl->rows = it + 1;
+}
+
 // =====================================================================================
 // Density gradient (density.cpp:148-156), one thread per movable cell in the scatter's spatial
 // order, so neighbouring threads read neighbouring excess bins (L1 hits).  Regrouped per bin
@@ -1067,26 +1158,30 @@ __device__ __forceinline__ double2 dens_grad5(int bx, int by, int sx_n, int sy_n
 
 // field = excess with fscale 2 (d sum excess^2, density.cpp:148-156) or the potential with fscale 1.
 // Cells of Grid::wide are skipped here (k_dens_grad_wide).
+template <bool EARLY>
 __global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* __restrict__ perm,
-                                                      const double2* __restrict__ cell_xy,
-                                                      const double2* __restrict__ cell_wh, GridDev g,
+                                                      const double2* __restrict__ xy_sp,
+                                                      const double2* __restrict__ wh_sp, GridDev g,
                                                       const double* __restrict__ excess, double2* __restrict__ dgrad,
                                                       const Ctrl* __restrict__ ctrl, double fscale)
-{   // (a programmatic dependent of the bins kernel; only launch latency is overlapped: data produced by
-    // earlier kernels is read after pdl_wait())
+{   // A programmatic dependent of the bins kernel.  The cell positions and sizes in spatial order were
+    // written by the scatter, which completed before the bins kernel started (it does not trigger early),
+    // so with EARLY they are loaded before pdl_wait(), overlapping the bins kernel; the excess field and
+    // the stop flag are read after it.
     pdl_trigger();
-    pdl_wait();
-    const bool stop = ctrl && ctrl->stopped;
     const int i = blockIdx.x * kBlock + threadIdx.x;
+    double2 p = make_double2(0.0, 0.0), s = make_double2(0.0, 0.0);
+    if (EARLY && i < n_mov) p = xy_sp[i], s = wh_sp[i];
+    pdl_wait();
     if (i >= n_mov) return;
-    const int c = perm[i];
-    const double2 p = cell_xy[c], s = cell_wh[c];
+    if (!EARLY) p = xy_sp[i], s = wh_sp[i];
+    const bool stop = ctrl && ctrl->stopped;
     if (stop || s.x > g.wide_w || s.y > g.wide_h) return;
     double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
     int bx, by, nx5, ny5;
     axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dwx, &nx5);
     axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dwy, &ny5);
-    dgrad[c] = dens_grad5(bx, by, nx5, ny5, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
+    dgrad[perm[i]] = dens_grad5(bx, by, nx5, ny5, wx, dwx, wy, dwy, s.x * s.y, g, excess, fscale);
 }
 
 __global__ void __launch_bounds__(kBlock) k_dens_grad_wide(int n, const int* __restrict__ wide,
@@ -1473,6 +1568,7 @@ void sort_cells_spatial(tdpg_session* s)
     const int C = s->C;
     if (C == 0) return;
     gr.perm.reserve(C), gr.perm_keys.reserve(2 * static_cast<size_t>(C)), gr.perm_tmp.reserve(C);
+    gr.xy_sp.reserve(C), gr.wh_sp.reserve(C);
     const GridDev g = grid_dev(s);
     const int tiles_y = (g.ny + 7) / 8, tiles_x = (g.nx + 7) / 8;
     unsigned* k0 = gr.perm_keys.p;
@@ -1507,7 +1603,8 @@ void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl)
     const int n_mov = s->grid.n_movable;
     if (n_mov == 0) return;
     k_density_scatter_win<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(
-        n_mov, s->grid.perm, s->cell_xy, s->cell_wh, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl);
+        n_mov, s->grid.perm, s->cell_xy, s->cell_wh, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl,
+        s->grid.xy_sp, s->grid.wh_sp);
     CK_LAUNCH();
     if (s->grid.n_wide > 0) {
         k_density_scatter_wide<<<blocks_for(s->grid.n_wide, kBlock), kBlock, 0, s->st>>>(
@@ -1550,14 +1647,25 @@ CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, dou
     return a;
 }
 
+// TDPG_DGRAD_EARLY=0: the density gradient loads its cells after pdl_wait() (A/B switch).
+bool dens_grad_early()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_DGRAD_EARLY");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 void launch_dens_grad(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st)
 {
     const int n_mov = s->grid.n_movable;
     if (n_mov > 0) {
         const bool el = s->grid.model == 1;
-        CK(launch_pdl(k_dens_grad, blocks_for(n_mov, kBlock), kBlock, st, s->pdl_graph,
-                      n_mov, static_cast<const int*>(s->grid.perm.p), static_cast<const double2*>(s->cell_xy.p),
-                      static_cast<const double2*>(s->cell_wh.p), grid_dev(s),
+        CK(launch_pdl(dens_grad_early() ? k_dens_grad<true> : k_dens_grad<false>, blocks_for(n_mov, kBlock), kBlock, st,
+                      s->pdl_graph,
+                      n_mov, static_cast<const int*>(s->grid.perm.p), static_cast<const double2*>(s->grid.xy_sp.p),
+                      static_cast<const double2*>(s->grid.wh_sp.p), grid_dev(s),
                       static_cast<const double*>(el ? s->grid.electro.psi.p : s->grid.excess.p), s->dgrad.p, ctrl,
                       el ? 1.0 : 2.0));
         if (s->grid.n_wide > 0) {
@@ -1875,6 +1983,18 @@ void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cu
     k_finalize<<<1, kFinBlock, 0, s->st>>>(fa, ctrl, cur);
     CK_LAUNCH();
 }
+void launch_fin_density(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur, cudaStream_t st)
+{
+    (void)s;
+    k_fin_density<<<1, kFinBlock, 0, st>>>(fa, ctrl, cur);
+    CK_LAUNCH();
+}
+void launch_fin_terms(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, const IterCur* cur, cudaStream_t st)
+{
+    (void)s;
+    k_fin_terms<<<1, kFinBlock, 0, st>>>(fa, ctrl, cur);
+    CK_LAUNCH();
+}
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
                   const IterCur* cur, Ctrl* ctrl, bool dens_grad, const double2* folded, bool dgrad_folded)
 {
@@ -1893,8 +2013,9 @@ void launch_density_scatter_part(tdpg_session* s, const Ctrl* ctrl, int lo, int 
     const GridDev g = grid_dev(s);
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(s->grid.acc.p);
     if (hi > lo) {
-        k_density_scatter_win<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(hi - lo, s->grid.perm.p + lo,
-                                                                                s->cell_xy, s->cell_wh, g, acc, ctrl);
+        k_density_scatter_win<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(
+            hi - lo, s->grid.perm.p + lo, s->cell_xy, s->cell_wh, g, acc, ctrl, s->grid.xy_sp.p + lo,
+            s->grid.wh_sp.p + lo);
         CK_LAUNCH();
     }
     if (wide && s->grid.n_wide > 0) {
@@ -1909,9 +2030,9 @@ void launch_dens_grad_part(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st, i
     const bool el = s->grid.model == 1;
     const double* field = el ? s->grid.electro.psi.p : s->grid.excess.p;
     if (hi > lo) {
-        k_dens_grad<<<blocks_for(hi - lo, kBlock), kBlock, 0, st>>>(hi - lo, s->grid.perm.p + lo, s->cell_xy,
-                                                                    s->cell_wh, grid_dev(s), field, s->dgrad, ctrl,
-                                                                    el ? 1.0 : 2.0);
+        k_dens_grad<false><<<blocks_for(hi - lo, kBlock), kBlock, 0, st>>>(hi - lo, s->grid.perm.p + lo,
+                                                                    s->grid.xy_sp.p + lo, s->grid.wh_sp.p + lo,
+                                                                    grid_dev(s), field, s->dgrad, ctrl, el ? 1.0 : 2.0);
         CK_LAUNCH();
     }
     if (s->grid.n_wide > 0) {

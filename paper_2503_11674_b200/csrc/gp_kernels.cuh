@@ -132,7 +132,8 @@ __device__ __forceinline__ bool axis5(double lo, double hi, double origin, doubl
 
 struct IterCur { // schedule values of the iteration being executed
     double lr, c1, c2, lambda;
-    int iter, do_adam, pad0, pad1;
+    int iter, do_adam, live, pad1; // live: the iteration ran (the engine was not already stopped)
+    double density, overflow;      // the density terms (k_fin_density -> k_fin_terms)
 };
 
 struct FinArgs {
@@ -160,6 +161,11 @@ void launch_density_ctrl(tdpg_session* s, double* pd, int nb, const Ctrl* ctrl);
 void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl);
 void launch_density_bins_ctrl(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl);
 void launch_finalize(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur);
+// the finalize split in two (engine iteration graph): the density terms + stop decision + schedule values
+// the cell kernel needs, on the density branch; the wirelength / pair terms, trace row and finiteness check
+// beside the cell kernel
+void launch_fin_density(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, IterCur* cur, cudaStream_t st);
+void launch_fin_terms(tdpg_session* s, const FinArgs& fa, Ctrl* ctrl, const IterCur* cur, cudaStream_t st);
 void launch_cells(tdpg_session* s, double2* d_cell, double2* m, double2* v, double b1, double b2, double eps,
                   const IterCur* cur, Ctrl* ctrl, bool dens_grad = true, const double2* folded = nullptr,
                   bool dgrad_folded = false);

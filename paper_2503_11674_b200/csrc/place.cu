@@ -254,6 +254,16 @@ bool pdl_gp()
     return on;
 }
 
+// TDPG_FIN_SPLIT=0: one finalize kernel at the join (A/B switch).
+bool fin_split()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_FIN_SPLIT");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 void capture_iteration(tdpg_session* s, Engine& E)
 {
     if (E.gexec) cudaGraphExecDestroy(E.gexec), E.gexec = nullptr;
@@ -337,6 +347,7 @@ void capture_iteration(tdpg_session* s, Engine& E)
         return;
     }
     s->pdl_graph = pdl_gp();
+    const bool split = fin_split();
     auto record = [&](bool sort) {
         // fork: density chain (scatter -> bins -> density gradient) on branch 0, the WA size classes
         // (+ fused pin pairs, dense ledger) on the main stream and branches 1..7; join -> finalize -> cells
@@ -347,6 +358,14 @@ void capture_iteration(tdpg_session* s, Engine& E)
         if (sort) sort_cells_spatial(s); // (only the density kernels read the spatial order)
         launch_density_ctrl(s, part_d, E.nb_d, E.ctrl);
         CK(cudaEventRecord(E.ev_bins, E.br[0])); // the density value partials are ready
+        // split finalize: the density half (stop decision, schedule values for the cell kernel) on its own
+        // branch beside the density gradient, so the cell kernel waits for the WA kernels, the density
+        // gradient and it; the terms half (wirelength / pair terms, trace row) runs beside the cell kernel
+        if (split) {
+            CK(cudaStreamWaitEvent(E.br[3], E.ev_bins, 0));
+            launch_fin_density(s, fa, E.ctrl, E.cur, E.br[3]);
+            CK(cudaEventRecord(E.ev_join[3], E.br[3]));
+        }
         launch_dens_grad(s, E.ctrl, E.br[0]);
         s->st = main;
         cudaStream_t wa_st[Engine::kBranches] = {main};
@@ -359,12 +378,22 @@ void capture_iteration(tdpg_session* s, Engine& E)
             CK(cudaEventRecord(E.ev_join[k], E.br[k]));
             CK(cudaStreamWaitEvent(main, E.ev_join[k], 0));
         }
-        CK(cudaStreamWaitEvent(main, E.ev_bins, 0));
-        launch_finalize(s, fa, E.ctrl, E.cur);
+        if (split) {
+            CK(cudaEventRecord(E.ev_fork, main)); // (reused: every WA kernel is done)
+            CK(cudaStreamWaitEvent(E.br[4], E.ev_fork, 0));
+            CK(cudaStreamWaitEvent(E.br[4], E.ev_join[3], 0));
+            launch_fin_terms(s, fa, E.ctrl, E.cur, E.br[4]);
+            CK(cudaEventRecord(E.ev_join[4], E.br[4]));
+            CK(cudaStreamWaitEvent(main, E.ev_join[3], 0));
+        } else {
+            CK(cudaStreamWaitEvent(main, E.ev_bins, 0));
+            launch_finalize(s, fa, E.ctrl, E.cur);
+        }
         CK(cudaEventRecord(E.ev_join[0], E.br[0]));
         CK(cudaStreamWaitEvent(main, E.ev_join[0], 0));
         launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
                      false);
+        if (split) CK(cudaStreamWaitEvent(main, E.ev_join[4], 0));
     };
     E.gexec = capture(s, [&] { record(false); });
     // the iterations that re-sort the cells: the sort heads the density branch, beside the WA kernels
@@ -587,6 +616,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->part.reserve(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
     E->kernels_per_iter = 8 + (s->grid.n_wide > 0 ? 2 : 0); // (+ wide-cell scatter and density gradient)
+    if (s->part_world <= 1 && fin_split()) E->kernels_per_iter += 1; // (finalize in two halves)
     E->partitioned = s->part_world > 1;
     if (E->partitioned) { // this rank's slice of the spatial order (the density scatter / gradient share)
         const long long nm = s->grid.n_movable;
