@@ -122,6 +122,71 @@ struct DBuf {
     operator T*() const { return p; }
 };
 
+// The device's default memory pool keeps freed memory cached (no release back to the driver at sync
+// points), so the stream-ordered scratch below is recycled across session creations.
+inline void pool_keep()
+{
+    static const bool once = [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+        return true;
+    }();
+    (void)once;
+}
+
+// Stream-ordered scratch buffer (session creation): cudaMallocAsync / cudaFreeAsync on one stream, so
+// temporaries cost neither a device-wide synchronisation on free nor a driver allocation on reuse.
+template <typename T>
+struct TBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t st = nullptr;
+    explicit TBuf(cudaStream_t s) : st(s) {}
+    TBuf(size_t count, cudaStream_t s) : st(s) { alloc(count); }
+    TBuf(const TBuf&) = delete;
+    TBuf& operator=(const TBuf&) = delete;
+    ~TBuf() { release(); }
+    void release()
+    {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr, n = 0;
+    }
+    void alloc(size_t count)
+    {
+        release();
+        n = count;
+        if (count) {
+            pool_keep();
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+        }
+    }
+    void reserve(size_t count)
+    {
+        if (count > n) alloc(count + count / 4 + 16);
+    }
+    void upload(const T* h, size_t count, cudaStream_t s)
+    {
+        if (count > n) alloc(count);
+        if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+    void download(T* h, size_t count, cudaStream_t s) const
+    {
+        if (count) CK(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    void zero(cudaStream_t s, size_t count = SIZE_MAX)
+    {
+        if (count == SIZE_MAX) count = n;
+        if (count) CK(cudaMemsetAsync(p, 0, count * sizeof(T), s));
+    }
+    operator T*() const { return p; }
+};
+
 // Pinned host buffer.
 template <typename T>
 struct HBuf {

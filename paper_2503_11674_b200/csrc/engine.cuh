@@ -121,9 +121,11 @@ struct tdpg_session {
     int device = 0;
 
     // host copies
-    std::vector<double> h_cell_w, h_cell_h, h_cell_delay, h_pin_cap, h_pin_off, h_pin_term;
-    std::vector<uint8_t> h_cell_fixed, h_pin_dir, h_is_source, h_is_endpoint;
-    std::vector<int> h_pin_cell, h_net_start, h_net_pins, h_sources, h_endpoints, h_pin_net, h_pin_entry;
+    // (only what host-side work needs after creation: pin offsets, terminals, caps, directions, delays and
+    // the net pin lists live on the device alone)
+    std::vector<double> h_cell_w, h_cell_h;
+    std::vector<uint8_t> h_cell_fixed, h_is_source, h_is_endpoint;
+    std::vector<int> h_pin_cell, h_net_start, h_sources, h_endpoints, h_pin_net, h_pin_entry;
     std::vector<std::string> pin_names;
     std::vector<int> h_level, h_lvl_start, h_arc_from, h_arc_to, h_arc_kind, h_arc_owner; // (level / arcs: lazy)
     bool h_level_valid = false, h_arcs_valid = false;
@@ -135,6 +137,8 @@ struct tdpg_session {
     tdpg::DBuf<double> cell_delay, pin_cap;
     tdpg::DBuf<uint8_t> cell_fixed, pin_dir, is_source, is_endpoint;
     tdpg::DBuf<int> pin_cell, net_start, net_pins, e_cell, pin_entry, cell_ent_start, cell_ent;
+    tdpg::DBuf<int> pin_net;        // pin -> net (-1: on no net)
+    bool h_pin_maps_valid = false;  // h_pin_entry / h_pin_net downloaded (host_pin_maps)
     // WA layout: nets sorted by pin count; per block (pin count N or 0, first, count, entry base);
     // entries of N-pin nets slot-major per block, class-0 nets contiguous (wa_gen_start)
     tdpg::DBuf<int> net_by_size, wa_gen_start;
@@ -147,7 +151,6 @@ struct tdpg_session {
     tdpg::DBuf<uint32_t> pp_mask, pp_ord;   // per class-ordered net
     tdpg::DBuf<int> wa_gen_ord, pin_loc, pin_driver;
     tdpg::DBuf<double> ppw_e, dl_w;        // pair weight per WA slot / per sink pin (0 = none)
-    std::vector<int> h_pin_driver;
 
     // device timing graph
     tdpg::DBuf<int> lvl_pins, lvl_start, in_start, in_from, out_start, out_to, ep_sorted;
@@ -278,6 +281,7 @@ namespace tdpg {
 
 // session.cu
 void upload_positions(tdpg_session* s, const double* xy);
+void host_pin_maps(tdpg_session* s);
 void refresh_fixed_baseline(tdpg_session* s);
 void build_graph_device(tdpg_session* s); // graph.cu
 void graph_host_level(tdpg_session* s);

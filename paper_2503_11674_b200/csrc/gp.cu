@@ -1770,6 +1770,7 @@ int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* 
     if (wl) *wl = a;
     if (hpwl) *hpwl = b;
     if (pin_grad) {
+        host_pin_maps(s);
         std::fill(pin_grad, pin_grad + 2 * static_cast<size_t>(s->P), 0.0);
         for (int p = 0; p < s->P; ++p) {
             const int e = s->h_pin_entry[p];
@@ -1880,6 +1881,7 @@ int tdpg_pp_loss(tdpg_session* s, int32_t kind, double* value, double* d_pin)
         }
         CK(cudaStreamSynchronize(s->st));
         for (double x : part) v += x;
+        if (d_pin) host_pin_maps(s);
         if (d_pin)
             for (int p = 0; p < s->P; ++p) {
                 const int e = s->h_pin_entry[p];

@@ -36,7 +36,8 @@ int bits_for_n(long long n)
 }
 
 struct Tmp { // scratch for one CUB call at a time
-    DBuf<unsigned char> buf;
+    explicit Tmp(cudaStream_t st) : buf(st) {}
+    TBuf<unsigned char> buf;
     void* get(size_t bytes)
     {
         buf.reserve(std::max<size_t>(bytes, 1));
@@ -240,9 +241,9 @@ void build_graph_device(tdpg_session* s)
 {
     cudaStream_t st = s->st;
     const int P = s->P, C = s->C, N = s->N;
-    Tmp tmp;
+    Tmp tmp(st);
     // ---- cell pins, ascending pin id per cell (netlist.cpp:12-14)
-    DBuf<int> key, key_s, iota, cp, cp_cnt, cp_start, n_in, n_out;
+    TBuf<int> key(st), key_s(st), iota(st), cp(st), cp_cnt(st), cp_start(st), n_in(st), n_out(st);
     key.alloc(std::max(P, 1)), key_s.alloc(std::max(P, 1)), iota.alloc(std::max(P, 1)), cp.alloc(std::max(P, 1));
     cp_cnt.alloc(C + 1), cp_start.alloc(C + 1), n_in.alloc(std::max(C, 1)), n_out.alloc(std::max(C, 1));
     cp_cnt.zero(st), n_in.zero(st), n_out.zero(st);
@@ -256,7 +257,7 @@ void build_graph_device(tdpg_session* s)
     excl_sum(tmp, cp_cnt, cp_start, C + 1, st);
     // ---- arcs
     const int A_net = s->E - N;
-    DBuf<int> ccnt, coff;
+    TBuf<int> ccnt(st), coff(st);
     ccnt.alloc(C + 1), coff.alloc(C + 1);
     ccnt.zero(st);
     if (C) k_cell_arc_count<<<grid_for(C), kGB, 0, st>>>(C, n_in, n_out, ccnt);
@@ -275,7 +276,7 @@ void build_graph_device(tdpg_session* s)
                                                      s->arc_owner);
     CK_LAUNCH();
     // ---- in / out CSR: arc ids stably sorted by to / from
-    DBuf<int> aiota, akey_s, in_a, out_a, cnt;
+    TBuf<int> aiota(st), akey_s(st), in_a(st), out_a(st), cnt(st);
     aiota.alloc(std::max(A, 1)), akey_s.alloc(std::max(A, 1)), in_a.alloc(std::max(A, 1)), out_a.alloc(std::max(A, 1));
     cnt.alloc(2 * static_cast<size_t>(P) + 4); // (histograms over pins, levels and 2 * levels + 1)
     s->in_start.alloc(P + 1), s->out_start.alloc(P + 1), s->in_from.alloc(std::max(A, 1)), s->out_to.alloc(std::max(A, 1));
@@ -297,7 +298,7 @@ void build_graph_device(tdpg_session* s)
     }
     CK_LAUNCH();
     // ---- Kahn levels by synchronous frontier rounds
-    DBuf<int> indeg, fa, fb, nf;
+    TBuf<int> indeg(st), fa(st), fb(st), nf(st);
     indeg.alloc(std::max(P, 1)), fa.alloc(std::max(P, 1)), fb.alloc(std::max(P, 1)), nf.alloc(2);
     s->d_level.alloc(std::max(P, 1));
     HBuf<int>& hn = s->h_graph_small;
@@ -369,7 +370,7 @@ void build_graph_device(tdpg_session* s)
     if (!P) s->h_lvl_start.assign(L + 1, 0);
     // ---- endpoint reachability (timing_graph.cpp:112-135)
     {
-        DBuf<uint8_t> reach;
+        TBuf<uint8_t> reach(st);
         reach.alloc(std::max(P, 1));
         reach.zero(st);
         for (int l = 0; l < L; ++l) {
@@ -379,7 +380,7 @@ void build_graph_device(tdpg_session* s)
                                                                   s->is_source, reach);
         }
         CK_LAUNCH();
-        DBuf<int> eps, first;
+        TBuf<int> eps(st), first(st);
         eps.upload(s->h_endpoints, st);
         first.alloc(1);
         const int big = INT_MAX;
@@ -396,7 +397,7 @@ void build_graph_device(tdpg_session* s)
         }
     }
     // ---- level-major L-space: per level its Input pins then its Output pins, ascending id
-    DBuf<int> Lpin, lkey_s, seg;
+    TBuf<int> Lpin(st), lkey_s(st), seg(st);
     Lpin.alloc(std::max(P, 1)), lkey_s.alloc(std::max(P, 1)), seg.alloc(2 * L + 1);
     if (P) {
         k_lkeys<<<grid_for(P), kGB, 0, st>>>(P, s->d_level, s->pin_dir, key);
@@ -420,7 +421,7 @@ void build_graph_device(tdpg_session* s)
         const int n_in = s->h_sta_in_start[L], n_out = s->h_sta_out_start[L];
         s->sta_in_pins.alloc(std::max(n_in, 1)), s->sta_out_pins.alloc(std::max(n_out, 1));
         s->sta_in_pins.zero(st), s->sta_out_pins.zero(st);
-        DBuf<int> ib, ob;
+        TBuf<int> ib(st), ob(st);
         ib.upload(s->h_sta_in_start, st), ob.upload(s->h_sta_out_start, st);
         if (P) k_split_io<<<grid_for(P), kGB, 0, st>>>(P, Lpin, lkey_s, seg, ib, ob, s->sta_in_pins, s->sta_out_pins);
         CK_LAUNCH();
@@ -433,7 +434,7 @@ void build_graph_device(tdpg_session* s)
         s->L_off.alloc(n), s->L_anchor.alloc(n);
         s->L_in_start.alloc(P + 1), s->L_out_start.alloc(P + 1);
         s->L_in_from.alloc(std::max(A, 1)), s->L_out_to.alloc(std::max(A, 1));
-        DBuf<int> icnt, ocnt;
+        TBuf<int> icnt(st), ocnt(st);
         icnt.alloc(P + 1), ocnt.alloc(P + 1);
         icnt.zero(st), ocnt.zero(st);
         if (P) {
@@ -457,7 +458,7 @@ void build_graph_device(tdpg_session* s)
         s->L_arr.alloc(n), s->L_req.alloc(n), s->L_xy.alloc(n);
     }
     {   // endpoints ascending
-        DBuf<int> e;
+        TBuf<int> e(st);
         e.upload(s->h_endpoints, st);
         s->ep_sorted.alloc(std::max(s->EP, 1));
         if (s->EP) {

@@ -8,6 +8,10 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <thread>
 
 #include "engine.cuh"
 
@@ -96,6 +100,117 @@ void refresh_fixed_baseline(tdpg_session* s)
     CK_LAUNCH();
 }
 
+// Entry layout on the device (session creation): net `order[i]`'s pins go to their WA slots — for a class
+// net of k pins at pos0[k] + block * 256 k + t + j * 256 (slot-major blocks), for a generic net contiguous
+// from gen_start[i] — with the owner cell (or -1 - pin for terminals) and the pin offset.
+struct EntryLayout {
+    int net0[9], pos0[9];
+    int gen0, gen1;
+};
+
+__global__ void k_entry_layout(int N, EntryLayout L, const int* __restrict__ order, const int* __restrict__ gen_start,
+                               const int* __restrict__ net_start, const int* __restrict__ net_pins,
+                               const int* __restrict__ pin_cell, const double2* __restrict__ pin_off,
+                               int* __restrict__ e_cell, double2* __restrict__ e_off, int* __restrict__ pin_entry,
+                               int* __restrict__ pin_net)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int n = order[i], b0 = net_start[n], k = net_start[n + 1] - b0;
+    int base, stride;
+    if (i >= L.gen0 && i < L.gen1) {
+        base = gen_start[i], stride = 1;
+    } else {
+        const int q = i - L.net0[k];
+        base = L.pos0[k] + (q / 256) * 256 * k + q % 256, stride = 256;
+    }
+    for (int j = 0; j < k; ++j) {
+        const int p = net_pins[b0 + j], id = base + j * stride;
+        const int c = pin_cell[p];
+        e_cell[id] = c >= 0 ? c : -1 - p;
+        e_off[id] = pin_off[p];
+        pin_entry[p] = id;
+        pin_net[p] = n;
+    }
+}
+
+// Sink order of each net (pin_pairs.cpp:22-34 accumulates a driver's pair terms in ascending sink pin id):
+// rank of every sink by pin id (O(k^2) per net; nets are a handful of pins), the class nets' 3-bit slot words,
+// the generic nets' slot lists, and per sink its (net index, slot) and driver.
+__global__ void k_pair_tables(int N, int gen0, int gen1, const int* __restrict__ order,
+                              const int* __restrict__ gen_start, const int* __restrict__ net_start,
+                              const int* __restrict__ net_pins, uint32_t* __restrict__ ord, int* __restrict__ gen_ord,
+                              int* __restrict__ pin_loc, int* __restrict__ pin_driver)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int n = order[i], b0 = net_start[n], k = net_start[n + 1] - b0;
+    const int drv = net_pins[b0];
+    const bool generic = i >= gen0 && i < gen1;
+    uint32_t w = 0;
+    for (int j = 1; j < k; ++j) {
+        const int pj = net_pins[b0 + j];
+        int r = 0;
+        for (int q = 1; q < k; ++q) r += net_pins[b0 + q] < pj ? 1 : 0; // (pins on a net are distinct)
+        pin_driver[pj] = drv;
+        if (generic) {
+            gen_ord[gen_start[i] + r] = j;
+        } else {
+            w |= static_cast<uint32_t>(j) << (3 * r);
+            pin_loc[pj] = (i << 3) | j;
+        }
+    }
+    if (!generic) ord[i] = w;
+}
+
+__global__ void k_offnet_flags(int P, const int* __restrict__ pin_cell, const int* __restrict__ pin_entry,
+                               int* __restrict__ flag)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p <= P) flag[p] = (p < P && pin_entry[p] < 0 && pin_cell[p] >= 0) ? 1 : 0;
+}
+
+// off-net cell pins take slot pos + rank; every cell pin is keyed by its cell for the fold CSR (terminals
+// sort last) and counted into its cell's start (exclusive-scanned after)
+__global__ void k_offnet_slots(int P, int pos, int C, const int* __restrict__ pin_cell, const int* __restrict__ flag,
+                               const int* __restrict__ rank, int* __restrict__ pin_entry, int* __restrict__ key,
+                               int* __restrict__ val, int* __restrict__ ces)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    if (flag[p]) pin_entry[p] = pos + rank[p];
+    const int c = pin_cell[p];
+    key[p] = c >= 0 ? c : C;
+    val[p] = p;
+    if (c >= 0) atomicAdd(&ces[c], 1);
+}
+
+__global__ void k_fold_entries(int n, const int* __restrict__ pin_sorted, const int* __restrict__ pin_entry,
+                               int* __restrict__ ce)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) ce[j] = pin_entry[pin_sorted[j]];
+}
+
+// Host copies of the pin -> entry and pin -> net maps (built on the device at creation), for the one-off
+// API calls that map entry gradients back to pins on the host.
+void host_pin_maps(tdpg_session* s)
+{
+    if (s->h_pin_maps_valid) return;
+    s->h_pin_entry.resize(s->P), s->h_pin_net.resize(s->P);
+    s->pin_entry.download(s->h_pin_entry.data(), s->P, s->st);
+    s->pin_net.download(s->h_pin_net.data(), s->P, s->st);
+    CK(cudaStreamSynchronize(s->st));
+    s->h_pin_maps_valid = true;
+}
+
+__global__ void k_set_terminals(int P, const int* __restrict__ pin_cell, const double2* __restrict__ xy,
+                                double2* __restrict__ anchor)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < P && pin_cell[p] < 0) anchor[p] = xy[p];
+}
+
 void upload_positions(tdpg_session* s, const double* xy)
 {
     s->cell_xy.upload(reinterpret_cast<const double2*>(xy), s->C, s->st);
@@ -182,22 +297,126 @@ struct PhaseTimer {
     }
 };
 
+// Host loop over [0, n) split into contiguous chunks on up to 16 threads (session creation at 1M+ cells).
+template <typename F>
+void par_for(long long n, F&& f, long long min_chunk = 1 << 15)
+{
+    const long long hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int nt = static_cast<int>(std::max(1LL, std::min(hw, (n + min_chunk - 1) / min_chunk)));
+    if (nt <= 1) {
+        if (n > 0) f(0LL, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(nt - 1);
+    for (int t = 1; t < nt; ++t) th.emplace_back([&f, n, nt, t] { f(n * t / nt, n * (t + 1) / nt); });
+    f(0LL, n / nt);
+    for (auto& x : th) x.join();
+}
+
+// Host -> device copies of the netlist-sized arrays through a process-wide pinned staging pair: each
+// 32 MB chunk is copied in by several threads while the previous chunk's DMA runs (pageable copies run
+// at ~5 GB/s, single threaded).  Small copies take the plain path.
+struct Stager {
+    static constexpr size_t kChunk = size_t(32) << 20;
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    std::mutex mu;
+    double ms_wait = 0, ms_copy = 0, ms_issue = 0; // (TDPG_TRACE_CREATE)
+    size_t bytes = 0;
+};
+
+Stager& stager()
+{
+    static Stager* s = new Stager; // (never freed: lives for the process, like the CUDA context)
+    return *s;
+}
+
+void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st)
+{
+    if (bytes == 0) return;
+    if (bytes < (size_t(4) << 20)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    Stager& S = stager();
+    std::lock_guard<std::mutex> lock(S.mu);
+    if (!S.buf[0]) {
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&S.buf[k]), Stager::kChunk, cudaHostAllocDefault));
+            CK(cudaEventCreateWithFlags(&S.ev[k], cudaEventDisableTiming));
+        }
+    }
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += Stager::kChunk, k ^= 1) {
+        const size_t n = std::min(Stager::kChunk, bytes - off);
+        const auto t0 = std::chrono::steady_clock::now();
+        CK(cudaEventSynchronize(S.ev[k])); // the DMA that last read this half is done
+        const auto t1 = std::chrono::steady_clock::now();
+        const char* from = static_cast<const char*>(src) + off;
+        char* to = S.buf[k];
+        par_for(static_cast<long long>(n), [&](long long lo, long long hi) { std::memcpy(to + lo, from + lo, hi - lo); },
+                size_t(4) << 20);
+        const auto t2 = std::chrono::steady_clock::now();
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, to, n, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(S.ev[k], st));
+        const auto t3 = std::chrono::steady_clock::now();
+        S.ms_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
+        S.ms_copy += std::chrono::duration<double, std::milli>(t2 - t1).count();
+        S.ms_issue += std::chrono::duration<double, std::milli>(t3 - t2).count();
+        S.bytes += n;
+    }
+}
+
+template <typename T>
+void upload_fast(DBuf<T>& b, const T* h, size_t count, cudaStream_t st)
+{
+    if (count > b.n) b.alloc(count);
+    upload_bytes(b.p, h, count * sizeof(T), st);
+}
+template <typename T>
+void upload_fast(DBuf<T>& b, const std::vector<T>& v, cudaStream_t st)
+{
+    upload_fast(b, v.data(), v.size(), st);
+}
+
 void check_netlist(const tdpg_netlist* d)
 {
     auto bad = [](const std::string& m) { throw Error(TDPG_ERR_VALIDATION, "validation error: " + m); };
     if (d->n_cells < 0 || d->n_pins < 0 || d->n_nets < 0) bad("negative sizes");
-    for (int p = 0; p < d->n_pins; ++p)
-        if (d->pin_cell[p] < -1 || d->pin_cell[p] >= d->n_cells) bad("pin cell id out of range");
+    std::atomic<int> err{0}; // first failure kind of the parallel checks (1 pin cell, 2 sinks, 3 pin id, 4 reuse)
+    auto fail = [&](int k) {
+        int z = 0;
+        err.compare_exchange_strong(z, k);
+    };
+    par_for(d->n_pins, [&](long long lo, long long hi) {
+        for (long long p = lo; p < hi; ++p)
+            if (d->pin_cell[p] < -1 || d->pin_cell[p] >= d->n_cells) return fail(1);
+    });
+    if (err.load() == 1) bad("pin cell id out of range");
     if (d->net_start[0] != 0) bad("net_start[0] must be 0");
-    std::vector<int> owner(d->n_pins, -1);
-    for (int n = 0; n < d->n_nets; ++n) {
-        if (d->net_start[n + 1] - d->net_start[n] < 2) bad("net needs at least one sink");
-        for (int e = d->net_start[n]; e < d->net_start[n + 1]; ++e) {
-            const int p = d->net_pins[e];
-            if (p < 0 || p >= d->n_pins) bad("net pin id out of range");
-            if (owner[p] >= 0) bad("pin used by two nets");
-            owner[p] = n;
+    std::unique_ptr<std::atomic<int>[]> owner(new std::atomic<int>[std::max(d->n_pins, 1)]);
+    par_for(d->n_pins, [&](long long lo, long long hi) {
+        for (long long p = lo; p < hi; ++p) owner[p].store(-1, std::memory_order_relaxed);
+    });
+    // (nets in ascending order per thread: the reported failure is one the sequential scan could report
+    // first only up to the order of independent errors)
+    par_for(d->n_nets, [&](long long lo, long long hi) {
+        for (long long n = lo; n < hi; ++n) {
+            if (d->net_start[n + 1] - d->net_start[n] < 2) return fail(2);
+            for (int e = d->net_start[n]; e < d->net_start[n + 1]; ++e) {
+                const int p = d->net_pins[e];
+                if (p < 0 || p >= d->n_pins) return fail(3);
+                int none = -1;
+                if (!owner[p].compare_exchange_strong(none, static_cast<int>(n), std::memory_order_relaxed)) return fail(4);
+            }
         }
+    });
+    switch (err.load()) {
+    case 2: bad("net needs at least one sink");
+    case 3: bad("net pin id out of range");
+    case 4: bad("pin used by two nets");
+    default: break;
     }
     for (int i = 0; i < d->n_sources; ++i)
         if (d->sources[i] < 0 || d->sources[i] >= d->n_pins) bad("source pin id out of range");
@@ -256,43 +475,51 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     s->clock = d->clock_period, s->r_unit = d->r_unit, s->c_unit = d->c_unit;
     std::memcpy(s->core, d->core, sizeof s->core);
     const int C = s->C, P = s->P, N = s->N, E = s->E;
+    // host copies kept for later host-side work (grid setup, jitter flags, partition bounds, endpoint
+    // checks, one-off gradient mapping); arrays used only here are read from the caller's buffers
     s->h_cell_w.assign(d->cell_w, d->cell_w + C);
     s->h_cell_h.assign(d->cell_h, d->cell_h + C);
-    s->h_cell_delay.assign(d->cell_delay, d->cell_delay + C);
     s->h_cell_fixed.assign(d->cell_fixed, d->cell_fixed + C);
     s->h_pin_cell.assign(d->pin_cell, d->pin_cell + P);
-    s->h_pin_term.assign(d->pin_term, d->pin_term + 2 * static_cast<size_t>(P));
-    s->h_pin_off.assign(d->pin_off, d->pin_off + 2 * static_cast<size_t>(P));
-    s->h_pin_dir.assign(d->pin_dir, d->pin_dir + P);
-    s->h_pin_cap.assign(d->pin_cap, d->pin_cap + P);
     s->h_net_start.assign(d->net_start, d->net_start + N + 1);
-    s->h_net_pins.assign(d->net_pins, d->net_pins + E);
     s->h_sources.assign(d->sources, d->sources + s->S);
     s->h_endpoints.assign(d->endpoints, d->endpoints + s->EP);
     if (d->pin_names) {
         s->pin_names.resize(P);
         for (int p = 0; p < P; ++p) s->pin_names[p] = d->pin_names[p] ? d->pin_names[p] : "";
     }
+    const int* net_pins = d->net_pins;
+    const double* pin_off = d->pin_off;
     pt.mark("streams + host copies");
     s->h_is_source.assign(P, 0);
     s->h_is_endpoint.assign(P, 0);
     for (int v : s->h_sources) s->h_is_source[v] = 1;
     for (int v : s->h_endpoints) s->h_is_endpoint[v] = 1;
     // device netlist
-    std::vector<double2> wh(C);
-    for (int c = 0; c < C; ++c) wh[c] = make_double2(s->h_cell_w[c], s->h_cell_h[c]);
-    s->cell_wh.upload(wh, s->st);
-    s->cell_delay.upload(s->h_cell_delay, s->st);
-    s->cell_fixed.upload(s->h_cell_fixed, s->st);
-    s->pin_cell.upload(s->h_pin_cell, s->st);
-    s->pin_off.upload(reinterpret_cast<const double2*>(s->h_pin_off.data()), P, s->st);
-    s->anchor.upload(reinterpret_cast<const double2*>(s->h_pin_term.data()), P, s->st);
-    s->pin_dir.upload(s->h_pin_dir, s->st);
-    s->pin_cap.upload(s->h_pin_cap, s->st);
-    s->is_source.upload(s->h_is_source, s->st);
-    s->is_endpoint.upload(s->h_is_endpoint, s->st);
-    s->net_start.upload(s->h_net_start, s->st);
-    s->net_pins.upload(s->h_net_pins, s->st);
+    {
+        std::vector<double2> wh(C);
+        par_for(C, [&](long long lo, long long hi) {
+            for (long long c = lo; c < hi; ++c) wh[c] = make_double2(d->cell_w[c], d->cell_h[c]);
+        });
+        upload_fast(s->cell_wh, wh, s->st); // (returns once the source is staged: temporaries may go)
+    }
+    upload_fast(s->cell_delay, d->cell_delay, C, s->st);
+    upload_fast(s->cell_fixed, d->cell_fixed, C, s->st);
+    upload_fast(s->pin_cell, d->pin_cell, P, s->st);
+    upload_fast(s->pin_off, reinterpret_cast<const double2*>(d->pin_off), P, s->st);
+    upload_fast(s->anchor, reinterpret_cast<const double2*>(d->pin_term), P, s->st);
+    upload_fast(s->pin_dir, d->pin_dir, P, s->st);
+    upload_fast(s->pin_cap, d->pin_cap, P, s->st);
+    upload_fast(s->is_source, s->h_is_source, s->st);
+    upload_fast(s->is_endpoint, s->h_is_endpoint, s->st);
+    upload_fast(s->net_start, s->h_net_start, s->st);
+    upload_fast(s->net_pins, net_pins, E, s->st);
+    if (pt.on) {
+        Stager& S = stager();
+        std::fprintf(stderr, "[tdpg create]   staged %.1f MB: wait %.2f ms, copy %.2f ms, issue %.2f ms\n", S.bytes / 1e6,
+                     S.ms_wait, S.ms_copy, S.ms_issue);
+        S.ms_wait = S.ms_copy = S.ms_issue = 0, S.bytes = 0;
+    }
     pt.mark("netlist upload");
     build_graph_device(s.get()); // build_timing_graph (timing_graph.cpp:49-138) on the device (graph.cu)
     sta_setup(s.get());
@@ -302,24 +529,21 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     // warp's loads and stores of one pin slot are contiguous); other nets (class 0) contiguous after.
     constexpr int kMaxN = 8, kB = 256;
     auto cls = [&](int n) { return (n >= 2 && n <= kMaxN) ? n : 0; };
+    const int* ns = d->net_start;
     std::vector<int> cnt(kMaxN + 2, 0);
-    for (int n = 0; n < N; ++n) cnt[cls(s->h_net_start[n + 1] - s->h_net_start[n]) + 1]++;
+    for (int n = 0; n < N; ++n) cnt[cls(ns[n + 1] - ns[n]) + 1]++;
     for (int k = 0; k <= kMaxN; ++k) cnt[k + 1] += cnt[k];
     std::vector<int> order(std::max(N, 1)), fill(cnt.begin(), cnt.end() - 1);
-    for (int n = 0; n < N; ++n) order[fill[cls(s->h_net_start[n + 1] - s->h_net_start[n])]++] = n;
-    std::vector<int> new_id(std::max(E, 1), -1), gen_start(std::max(N, 1) + 1, 0);
+    for (int n = 0; n < N; ++n) order[fill[cls(ns[n + 1] - ns[n])]++] = n;
+    std::vector<int> gen_start(std::max(N, 1) + 1, 0);
     std::vector<int4> blk;
     int pos = 0;
     for (int k = 2; k <= kMaxN; ++k) {
         s->wa_cls_blk0[k] = static_cast<int>(blk.size());
         s->wa_cls_net0[k] = cnt[k], s->wa_cls_net1[k] = cnt[k + 1], s->wa_cls_pos0[k] = pos;
-        for (int i = cnt[k]; i < cnt[k + 1]; i += kB) {
-            const int count = std::min(kB, cnt[k + 1] - i);
-            blk.push_back(make_int4(k, i, count, pos));
-            for (int t = 0; t < count; ++t)
-                for (int j = 0; j < k; ++j) new_id[s->h_net_start[order[i + t]] + j] = pos + j * kB + t;
-            pos += kB * k;
-        }
+        // (the t-th net of a block at base + t, its pin j at + j * 256: k_entry_layout)
+        for (int i = cnt[k]; i < cnt[k + 1]; i += kB) blk.push_back(make_int4(k, i, std::min(kB, cnt[k + 1] - i), pos + (i - cnt[k]) * k));
+        pos += ((cnt[k + 1] - cnt[k] + kB - 1) / kB) * kB * k;
         s->wa_cls_nblk[k] = static_cast<int>(blk.size()) - s->wa_cls_blk0[k];
     }
     s->wa_cls_blk0[0] = static_cast<int>(blk.size());
@@ -327,41 +551,33 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     for (int i = cnt[0]; i < cnt[1]; i += kGenNets) blk.push_back(make_int4(0, i, std::min(kGenNets, cnt[1] - i), 0));
     s->wa_cls_nblk[0] = static_cast<int>(blk.size()) - s->wa_cls_blk0[0];
     for (int i = cnt[0]; i < cnt[1]; ++i) {
-        const int n = order[i], b0 = s->h_net_start[n], k = s->h_net_start[n + 1] - b0;
+        const int n = order[i];
         gen_start[i] = pos;
-        for (int j = 0; j < k; ++j) new_id[b0 + j] = pos + j;
-        pos += k;
+        pos += ns[n + 1] - ns[n];
     }
     gen_start[cnt[1]] = pos; // sentinel: generic net i has gen_start[i + 1] - gen_start[i] pins
     s->wa_gen_nets = cnt[1];
     s->n_wa_blocks = static_cast<int>(blk.size());
     s->part_b0 = 0, s->part_b1 = s->n_wa_blocks; // whole design until tdpg_set_partition / tdpg_comm_init
     s->E_lay = pos;
-    {   // fused pin-pair tables (engine mode): per class-ordered net the sink slots in ascending pin
-        // id (3 bits each), per generic net the same as a list; per sink pin its (net index, slot)
-        std::vector<uint32_t> ord(std::max(N, 1), 0u);
-        std::vector<int> gen_ord(std::max(pos, 1), 0), pin_loc(P, -1), pin_drv(P, -1);
-        std::vector<std::pair<int, int>> sk;
-        for (int i = 0; i < N; ++i) {
-            const int n = order[i], b0 = s->h_net_start[n], k = s->h_net_start[n + 1] - b0;
-            sk.clear();
-            for (int j = 1; j < k; ++j) sk.emplace_back(s->h_net_pins[b0 + j], j);
-            std::sort(sk.begin(), sk.end());
-            for (int j = 1; j < k; ++j) pin_drv[s->h_net_pins[b0 + j]] = s->h_net_pins[b0];
-            if (i < cnt[0] || i >= cnt[1]) { // class net
-                uint32_t w = 0;
-                for (size_t q = 0; q < sk.size(); ++q) w |= static_cast<uint32_t>(sk[q].second) << (3 * q);
-                ord[i] = w;
-                for (int j = 1; j < k; ++j) pin_loc[s->h_net_pins[b0 + j]] = (i << 3) | j;
-            } else {
-                for (size_t q = 0; q < sk.size(); ++q) gen_ord[gen_start[i] + static_cast<int>(q)] = sk[q].second;
-            }
-        }
-        s->pp_ord.upload(ord, s->st);
-        s->wa_gen_ord.upload(gen_ord, s->st);
-        s->pin_loc.upload(pin_loc, s->st);
-        s->pin_driver.upload(pin_drv, s->st);
-        s->h_pin_driver = pin_drv;
+    pt.mark("  WA layout: order + slots");
+    if (blk.empty()) blk.push_back(make_int4(0, 0, 0, 0));
+    upload_fast(s->net_by_size, order, s->st);
+    upload_fast(s->wa_blk, blk, s->st);
+    upload_fast(s->wa_gen_start, gen_start, s->st);
+    {   // fused pin-pair tables (engine mode, k_pair_tables): per class-ordered net the sink slots in
+        // ascending pin id (3 bits each), per generic net the same as a list; per sink pin its (net index,
+        // slot) and its driver
+        s->pp_ord.alloc(std::max(N, 1)), s->wa_gen_ord.alloc(std::max(pos, 1));
+        s->pin_loc.alloc(std::max(P, 1)), s->pin_driver.alloc(std::max(P, 1));
+        s->wa_gen_ord.zero(s->st), s->pp_ord.zero(s->st);
+        CK(cudaMemsetAsync(s->pin_loc.p, 0xff, sizeof(int) * std::max(P, 1), s->st));
+        CK(cudaMemsetAsync(s->pin_driver.p, 0xff, sizeof(int) * std::max(P, 1), s->st));
+        if (N > 0)
+            k_pair_tables<<<blocks_for(N, 256), 256, 0, s->st>>>(N, cnt[0], cnt[1], s->net_by_size, s->wa_gen_start,
+                                                                s->net_start, s->net_pins, s->pp_ord, s->wa_gen_ord,
+                                                                s->pin_loc, s->pin_driver);
+        CK_LAUNCH();
         s->pp_mask.alloc(std::max(N, 1));
         s->pp_mask.zero(s->st);
         s->ppw_e.alloc(std::max(pos, 1));
@@ -369,45 +585,68 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
         s->dl_w.alloc(std::max(P, 1));
         s->dl_w.zero(s->st);
     }
-    if (blk.empty()) blk.push_back(make_int4(0, 0, 0, 0));
-    s->net_by_size.upload(order, s->st);
-    s->wa_blk.upload(blk, s->st);
-    s->wa_gen_start.upload(gen_start, s->st);
-    std::vector<int> e_cell(std::max(pos, 1), 0), pin_entry(P, -1);
-    std::vector<double2> e_off(std::max(pos, 1), make_double2(0.0, 0.0));
-    s->h_pin_net.assign(P, -1);
-    for (int n = 0; n < N; ++n)
-        for (int e = s->h_net_start[n]; e < s->h_net_start[n + 1]; ++e) {
-            const int p = s->h_net_pins[e], id = new_id[e];
-            e_cell[id] = s->h_pin_cell[p] >= 0 ? s->h_pin_cell[p] : -1 - p;
-            e_off[id] = make_double2(s->h_pin_off[2 * p], s->h_pin_off[2 * p + 1]);
-            pin_entry[p] = id;
-            s->h_pin_net[p] = n;
-        }
-    pt.mark("WA layout + pin pairs");
-    s->e_cell.upload(e_cell, s->st);
-    s->e_off.upload(e_off, s->st);
-    // Cell pins on no net still take pin-pair gradient (pin_pairs.cpp:31-34 writes any pin):
-    // they get extra slots after the E net entries, written only by the pin-pair kernel.
-    int extra = 0;
-    for (int p = 0; p < P; ++p)
-        if (pin_entry[p] < 0 && s->h_pin_cell[p] >= 0) pin_entry[p] = pos + extra++;
-    s->E_tot = pos + extra;
-    s->h_pin_entry = pin_entry;
-    s->pin_entry.upload(pin_entry, s->st);
-    // fold CSR: per cell, the entries of its pins in ascending pin id
-    std::vector<int> ces(C + 1, 0), ce;
-    for (int p = 0; p < P; ++p)
-        if (s->h_pin_cell[p] >= 0 && pin_entry[p] >= 0) ces[s->h_pin_cell[p] + 1]++;
-    for (int c = 0; c < C; ++c) ces[c + 1] += ces[c];
-    ce.resize(ces[C]);
+    pt.mark("  WA layout: pair tables");
+    // entries, pin -> entry / net maps, off-net pin slots and the fold CSR, built on the device from the
+    // uploaded netlist and the class order (host copies of the pin maps are made only if an API asks)
     {
-        std::vector<int> f(ces.begin(), ces.end() - 1);
-        for (int p = 0; p < P; ++p)
-            if (s->h_pin_cell[p] >= 0 && pin_entry[p] >= 0) ce[f[s->h_pin_cell[p]]++] = pin_entry[p];
+        s->e_cell.alloc(std::max(pos, 1)), s->e_off.alloc(std::max(pos, 1));
+        s->e_cell.zero(s->st), s->e_off.zero(s->st); // (padding slots of partial blocks read as cell 0 / 0)
+        s->pin_entry.alloc(std::max(P, 1)), s->pin_net.alloc(std::max(P, 1));
+        CK(cudaMemsetAsync(s->pin_entry.p, 0xff, sizeof(int) * std::max(P, 1), s->st)); // -1: no entry
+        CK(cudaMemsetAsync(s->pin_net.p, 0xff, sizeof(int) * std::max(P, 1), s->st));
+        EntryLayout L{};
+        for (int k = 0; k <= kMaxN; ++k) L.net0[k] = s->wa_cls_net0[k], L.pos0[k] = s->wa_cls_pos0[k];
+        L.gen0 = cnt[0], L.gen1 = cnt[1];
+        if (N > 0)
+            k_entry_layout<<<blocks_for(N, 256), 256, 0, s->st>>>(N, L, s->net_by_size, s->wa_gen_start, s->net_start,
+                                                                 s->net_pins, s->pin_cell, s->pin_off, s->e_cell,
+                                                                 s->e_off, s->pin_entry, s->pin_net);
+        CK_LAUNCH();
+        // cell pins on no net still take pin-pair gradient (pin_pairs.cpp:31-34 writes any pin): extra
+        // slots after the laid-out entries, in ascending pin id
+        cudaStream_t st = s->st;
+        TBuf<int> flag(P + 1, st), rank(P + 1, st), key(std::max(P, 1), st), key_s(std::max(P, 1), st),
+            val(std::max(P, 1), st), val_s(std::max(P, 1), st);
+        if (P > 0) {
+            k_offnet_flags<<<blocks_for(P + 1, 256), 256, 0, s->st>>>(P, s->pin_cell, s->pin_entry, flag);
+            CK_LAUNCH();
+            size_t b = 0;
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, b, flag.p, rank.p, P + 1, s->st));
+            CK(cub::DeviceScan::ExclusiveSum(cub_scratch(s.get(), b), b, flag.p, rank.p, P + 1, s->st));
+            int extra = 0;
+            CK(cudaMemcpyAsync(&extra, rank.p + P, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+            // fold CSR: per cell, the entries of its pins in ascending pin id (stable sort of pins by cell)
+            s->cell_ent_start.alloc(C + 1);
+            TBuf<int> ccnt(C + 1, st);
+            ccnt.zero(s->st);
+            k_offnet_slots<<<blocks_for(P, 256), 256, 0, s->st>>>(P, pos, C, s->pin_cell, flag, rank, s->pin_entry, key,
+                                                                  val, ccnt);
+            CK_LAUNCH();
+            int bits = 1;
+            while ((1LL << bits) < static_cast<long long>(C) + 1) ++bits;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, b, key.p, key_s.p, val.p, val_s.p, P, 0, bits, s->st));
+            CK(cub::DeviceRadixSort::SortPairs(cub_scratch(s.get(), b), b, key.p, key_s.p, val.p, val_s.p, P, 0, bits, s->st));
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, b, ccnt.p, s->cell_ent_start.p, C + 1, s->st));
+            CK(cub::DeviceScan::ExclusiveSum(cub_scratch(s.get(), b), b, ccnt.p, s->cell_ent_start.p, C + 1, s->st));
+            CK(cudaStreamSynchronize(s->st));
+            s->E_tot = pos + extra;
+            int n_ce = 0;
+            CK(cudaMemcpy(&n_ce, s->cell_ent_start.p + C, sizeof(int), cudaMemcpyDeviceToHost));
+            s->cell_ent.alloc(std::max(n_ce, 1));
+            if (n_ce > 0) {
+                k_fold_entries<<<blocks_for(n_ce, 256), 256, 0, s->st>>>(n_ce, val_s, s->pin_entry, s->cell_ent);
+                CK_LAUNCH();
+            }
+        } else {
+            s->E_tot = pos;
+            s->cell_ent_start.alloc(C + 1);
+            CK(cudaMemsetAsync(s->cell_ent_start.p, 0, sizeof(int) * (C + 1), s->st));
+            s->cell_ent.alloc(1);
+        }
+        CK(cudaStreamSynchronize(s->st)); // (the scratch buffers are freed on scope exit)
+        s->h_pin_maps_valid = false;
     }
-    s->cell_ent_start.upload(ces, s->st);
-    s->cell_ent.upload(ce, s->st);
+    pt.mark("  entries + fold CSR (device)");
 
     pt.mark("entries + fold CSR");
     // state buffers
@@ -491,9 +730,13 @@ int tdpg_set_terminal_positions(tdpg_session* s, const double* xy)
 {
     API_BEGIN
     if (s->P == 0) return TDPG_OK;
-    for (int p = 0; p < s->P; ++p)
-        if (s->h_pin_cell[p] < 0) s->h_pin_term[2 * p] = xy[2 * p], s->h_pin_term[2 * p + 1] = xy[2 * p + 1];
-    s->anchor.upload(reinterpret_cast<const double2*>(s->h_pin_term.data()), s->P, s->st);
+    {   // terminal pins take the new positions (the other pins' anchors are unused)
+        DBuf<double2> xy_d;
+        xy_d.upload(reinterpret_cast<const double2*>(xy), s->P, s->st);
+        k_set_terminals<<<blocks_for(s->P, 256), 256, 0, s->st>>>(s->P, s->pin_cell, xy_d, s->anchor);
+        CK_LAUNCH();
+        CK(cudaStreamSynchronize(s->st)); // (xy_d is freed on return)
+    }
     if (s->L_anchor.p && s->L_pin.p) { // the level-major copy the STA sweeps read
         k_gather_anchor<<<blocks_for(s->P, 256), 256, 0, s->st>>>(s->P, s->L_pin, s->anchor, s->L_anchor);
         CK_LAUNCH();
