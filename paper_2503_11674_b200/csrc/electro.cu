@@ -11,10 +11,11 @@
 // independent stencil, the gradient by finite differences and that placement spreads cells.
 //
 // The transforms are hand-written, one grid row per CTA, the row resident in shared memory:
-//  * power-of-two lengths: DCT-II as Makhoul's (1980) L-point complex FFT of the even/odd-reordered row
-//    plus a quarter-wave twiddle, DCT-III as the pre-twiddled Hermitian spectrum through the inverse
-//    FFT; the FFT is radix-2 decimation in time over the bit-reversed row in shared memory (twiddles
-//    from a per-length table);
+//  * power-of-two lengths: DCT-II as Makhoul's (1980) FFT of the even/odd-reordered row plus a
+//    quarter-wave twiddle, the real length-L FFT done as a half-length complex FFT and an untangling step;
+//    DCT-III as the pre-twiddled Hermitian spectrum through the inverse; the FFT is a Stockham autosort
+//    (natural order in and out) in shared memory, radix-4 stages then one radix-2 stage when needed,
+//    twiddles from a per-length table;
 //  * other lengths: the direct O(L^2) sums from a cosine table cos(pi j / 2L), j < 4L.
 // Five launches per solve: DCT-II along y (rows of rho); tiled shared-memory transpose; one fused x pass
 // per row (DCT-II, divide by lambda_uv, DCT-III — the whole x spectrum of a y frequency stays on chip);
