@@ -705,6 +705,36 @@ __global__ void __launch_bounds__(kBlock) k_pin_pairs(const int* __restrict__ n_
 // whatever the order or the path.
 constexpr int kWinBins = 4096; // 32 KB of int64 accumulators
 
+// Fixed-point entries into shared 32-bit limbs with no-return adds (RED; a 64-bit shared atomicAdd compiles
+// to a CAS spin loop on sm_100a): a block adds at most 256 entries per bin, so each limb is sized to hold
+// 256 of its parts.  LIMBS = 2 (|q| < 2^45, Grid::limbs): an unsigned 23-bit low part and a signed high
+// part; LIMBS = 3: 21-bit low and middle parts and a signed top.  The flush recombines the exact int64 sum.
+template <int LIMBS>
+struct SmemLimbs {
+    unsigned* w;    // LIMBS arrays of `stride` limbs
+    int stride;
+    __device__ __forceinline__ void add(long long k, unsigned long long u) const
+    {
+        const long long q = static_cast<long long>(u);
+        if constexpr (LIMBS == 2) {
+            atomicAdd(w + k, static_cast<unsigned>(q & 0x7FFFFF));
+            atomicAdd(reinterpret_cast<int*>(w + stride) + k, static_cast<int>(q >> 23));
+        } else {
+            atomicAdd(w + k, static_cast<unsigned>(q & 0x1FFFFF));
+            atomicAdd(w + stride + k, static_cast<unsigned>((q >> 21) & 0x1FFFFF));
+            atomicAdd(reinterpret_cast<int*>(w + 2 * stride) + k, static_cast<int>(q >> 42));
+        }
+    }
+    __device__ __forceinline__ long long sum(int k) const
+    {
+        if constexpr (LIMBS == 2)
+            return static_cast<long long>(w[k]) + static_cast<long long>(static_cast<int>(w[stride + k])) * (1LL << 23);
+        else
+            return static_cast<long long>(w[k]) + static_cast<long long>(w[stride + k]) * (1LL << 21) +
+                   static_cast<long long>(static_cast<int>(w[2 * stride + k])) * (1LL << 42);
+    }
+};
+
 // 64-bit fixed-point add into shared memory as two native 32-bit atomics with an explicit carry
 // (a 64-bit shared atomicAdd compiles to a CAS spin loop, ATOMS.CAST.SPIN.64, on sm_100a).
 struct SmemAcc {
@@ -819,6 +849,74 @@ __global__ void __launch_bounds__(kBlock) k_density_scatter_win(int n_mov, const
             const unsigned long long v = (static_cast<unsigned long long>(win_hi[k]) << 32) | win_lo[k];
             const int col = k / h;
             if (v) atomicAdd(&acc[static_cast<long long>(X0 + col) * g.ny + (Y0 + k - col * h)], v);
+        }
+    } else if (fast) {
+        scatter_cell5(area, bx, by, wx, wy, g, GlobalAcc{acc}, g.ny, 0, 0);
+    }
+}
+
+template <int LIMBS>
+__global__ void __launch_bounds__(kBlock) k_density_scatter_limbs(int n_mov, const int* __restrict__ perm,
+                                                                const double2* __restrict__ cell_xy,
+                                                                const double2* __restrict__ cell_wh, GridDev g,
+                                                                unsigned long long* __restrict__ acc,
+                                                                const Ctrl* __restrict__ ctrl,
+                                                                double2* __restrict__ xy_sp, double2* __restrict__ wh_sp)
+{
+    constexpr int kW = LIMBS == 2 ? kWinBins : 4000; // (3 limbs: 48 KB of static shared memory)
+    __shared__ unsigned win[LIMBS * kW];
+    const SmemLimbs<LIMBS> SA{win, kW};
+    __shared__ int bb[4];
+    const bool stop = ctrl && ctrl->stopped; // (checked once the cell loads are in flight)
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    const bool valid = i < n_mov;
+    double2 p = make_double2(0, 0), s = make_double2(1, 1);
+    int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+    double wx[kF5], wy[kF5], dw[kF5];
+    int bx = 0, by = 0;
+    bool fast = false;
+    if (valid) {
+        const int c = perm[i];
+        p = cell_xy[c], s = cell_wh[c];
+        xy_sp[i] = p, wh_sp[i] = s; // (for k_dens_grad)
+        // cells of Grid::wide are scattered by k_density_scatter_wide; every other cell spans at most
+        // 1.99 pitches, so its footprint has at most five bins per axis (axis5 succeeds)
+        fast = !(s.x > g.wide_w || s.y > g.wide_h) &&
+               axis5(p.x, p.x + s.x, g.x0, g.bw, g.inv_bw, g.nx, bx, wx, dw) &&
+               axis5(p.y, p.y + s.y, g.y0, g.bh, g.inv_bh, g.ny, by, wy, dw);
+        if (fast)
+            bx0 = max(bx, 0), bx1 = min(bx + kF5 - 1, g.nx - 1), by0 = max(by, 0), by1 = min(by + kF5 - 1, g.ny - 1);
+    }
+    if (stop) return; // (uniform over the block)
+    if (threadIdx.x == 0) bb[0] = INT_MAX, bb[1] = INT_MIN, bb[2] = INT_MAX, bb[3] = INT_MIN;
+    int a0 = bx0, a1 = bx1, c0 = by0, c1 = by1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 = min(a0, __shfl_xor_sync(0xffffffffu, a0, o)), a1 = max(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+        c0 = min(c0, __shfl_xor_sync(0xffffffffu, c0, o)), c1 = max(c1, __shfl_xor_sync(0xffffffffu, c1, o));
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && a0 <= a1) {
+        atomicMin(&bb[0], a0), atomicMax(&bb[1], a1), atomicMin(&bb[2], c0), atomicMax(&bb[3], c1);
+    }
+    __syncthreads();
+    const int X0 = bb[0], Y0 = bb[2];
+    const long long W = static_cast<long long>(bb[1]) - X0 + 1, H = static_cast<long long>(bb[3]) - Y0 + 1;
+    if (X0 > bb[1]) return; // no movable cell in this block
+    const double area = s.x * s.y;
+    if (W * H <= kW) {
+        for (int k = threadIdx.x; k < static_cast<int>(W * H); k += kBlock)
+#pragma unroll
+            for (int l = 0; l < LIMBS; ++l) win[l * kW + k] = 0u;
+        __syncthreads();
+        if (fast) scatter_cell5(area, bx, by, wx, wy, g, SA, H, Y0, X0);
+        __syncthreads();
+        const int h = static_cast<int>(H), n = static_cast<int>(W * H);
+        for (int k = threadIdx.x; k < n; k += kBlock) {
+            const long long v = SA.sum(k);
+            const int col = k / h;
+            if (v) atomicAdd(&acc[static_cast<long long>(X0 + col) * g.ny + (Y0 + k - col * h)],
+                             static_cast<unsigned long long>(v));
         }
     } else if (fast) {
         scatter_cell5(area, bx, by, wx, wy, g, GlobalAcc{acc}, g.ny, 0, 0);
@@ -1597,12 +1695,26 @@ void launch_density(tdpg_session* s, double* part_d, int nblk, const Ctrl* ctrl)
 
 void launch_density(tdpg_session* s, double* part_d, int nblk) { launch_density(s, part_d, nblk, nullptr); }
 
+// The windowed scatter kernel for this grid: no-return limb adds (2 or 3 limbs, Grid::limbs), or with
+// TDPG_SCATTER_LIMBS=0 the carry-propagating two-word form (A/B switch; the grids are bitwise equal).
+using ScatterKernel = void (*)(int, const int*, const double2*, const double2*, GridDev, unsigned long long*,
+                               const Ctrl*, double2*, double2*);
+ScatterKernel scatter_kernel(const tdpg_session* s)
+{
+    static const bool limbs = [] {
+        const char* e = std::getenv("TDPG_SCATTER_LIMBS");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (!limbs) return k_density_scatter_win;
+    return s->grid.limbs == 2 ? k_density_scatter_limbs<2> : k_density_scatter_limbs<3>;
+}
+
 void launch_density_scatter_ctrl(tdpg_session* s, const Ctrl* ctrl)
 {
     const GridDev g = grid_dev(s);
     const int n_mov = s->grid.n_movable;
     if (n_mov == 0) return;
-    k_density_scatter_win<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(
+    scatter_kernel(s)<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(
         n_mov, s->grid.perm, s->cell_xy, s->cell_wh, g, reinterpret_cast<unsigned long long*>(s->grid.acc.p), ctrl,
         s->grid.xy_sp, s->grid.wh_sp);
     CK_LAUNCH();
@@ -2015,7 +2127,7 @@ void launch_density_scatter_part(tdpg_session* s, const Ctrl* ctrl, int lo, int 
     const GridDev g = grid_dev(s);
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(s->grid.acc.p);
     if (hi > lo) {
-        k_density_scatter_win<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(
+        scatter_kernel(s)<<<blocks_for(hi - lo, kBlock), kBlock, 0, s->st>>>(
             hi - lo, s->grid.perm.p + lo, s->cell_xy, s->cell_wh, g, acc, ctrl, s->grid.xy_sp.p + lo,
             s->grid.wh_sp.p + lo);
         CK_LAUNCH();

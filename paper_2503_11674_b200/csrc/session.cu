@@ -230,12 +230,12 @@ void ensure_grid(tdpg_session* s, int nx, int ny, double td)
     g.bw = (s->core[2] - s->core[0]) / nx;
     g.bh = (s->core[3] - s->core[1]) / ny;
     g.cap = td * g.bw * g.bh;
-    double mov = 0.0, all = 0.0;
+    double mov = 0.0, all = 0.0, amax = 0.0;
     bool fixed = false;
     for (int c = 0; c < s->C; ++c) {
         const double a = s->h_cell_w[c] * s->h_cell_h[c];
         all += a;
-        if (!s->h_cell_fixed[c]) mov += a;
+        if (!s->h_cell_fixed[c]) mov += a, amax = std::max(amax, a);
         else fixed = true;
     }
     g.total_movable = mov;
@@ -256,6 +256,8 @@ void ensure_grid(tdpg_session* s, int nx, int ny, double td)
     const int k = std::min(60 - ex, 1000);
     g.scale = std::ldexp(1.0, k);
     g.inv_scale = std::ldexp(1.0, -k);
+    // an entry is area * wx * wy * scale with weights <= 1 (x2 margin): below 2^48 -> two 24-bit limbs
+    g.limbs = (2.0 * amax * g.scale < std::ldexp(1.0, 48)) ? 2 : 3;
     const long long B = g.bins();
     g.acc.alloc(B);
     g.acc.zero(s->st);
