@@ -298,6 +298,293 @@ __global__ void __launch_bounds__(kBlock) k_electro_energy(long long B, const do
 
 bool is_pow2(int L) { return L >= 4 && (L & (L - 1)) == 0; }
 
+// ---------------------------------------------------------------------------------------------------
+// Batched line transforms (power-of-two lengths 32 .. 4096): 128 threads carry 1024 / M lines of M = L/2
+// complex points (8 per thread), the FFT in registers by radix-8 Stockham stages (one shared-memory round
+// trip per stage, then one radix-2 or radix-4 stage when log2 M is not a multiple of 3), the M-point
+// twiddles in shared memory.  Lines are rows (contiguous, the y passes) or columns (stride ny, the x pass
+// reads 4..64 adjacent columns per CTA), so the 2-D solve needs no transposes.
+// ---------------------------------------------------------------------------------------------------
+constexpr int kLineThreads = 128;
+constexpr double kRsqrt2 = 0.70710678118654752440;
+
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3)
+{
+    const double2 s02 = make_double2(x0.x + x2.x, x0.y + x2.y), d02 = make_double2(x0.x - x2.x, x0.y - x2.y);
+    const double2 s13 = make_double2(x1.x + x3.x, x1.y + x3.y), d13 = make_double2(x1.x - x3.x, x1.y - x3.y);
+    const double2 r13 = INV ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x); // -/+ i d13
+    x0 = make_double2(s02.x + s13.x, s02.y + s13.y);
+    x2 = make_double2(s02.x - s13.x, s02.y - s13.y);
+    x1 = make_double2(d02.x + r13.x, d02.y + r13.y);
+    x3 = make_double2(d02.x - r13.x, d02.y - r13.y);
+}
+
+// a[r] -> sum_n a[n] W8^{n r} (W8 = e^{-/+ 2 pi i / 8}): b = a_r + a_{r+4} (even outputs), c = (a_r - a_{r+4}) W8^r
+// (odd outputs), two 4-point DFTs
+template <bool INV>
+__device__ __forceinline__ void dft8(double2 (&a)[8])
+{
+    double2 b[4], c[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        b[r] = make_double2(a[r].x + a[r + 4].x, a[r].y + a[r + 4].y);
+        c[r] = make_double2(a[r].x - a[r + 4].x, a[r].y - a[r + 4].y);
+    }
+    const double sg = INV ? 1.0 : -1.0; // W8^1 = (1 + sg i) / sqrt2, W8^2 = sg i, W8^3 = (-1 + sg i) / sqrt2
+    c[1] = make_double2((c[1].x - sg * c[1].y) * kRsqrt2, (c[1].y + sg * c[1].x) * kRsqrt2);
+    c[2] = make_double2(-sg * c[2].y, sg * c[2].x);
+    c[3] = make_double2((-c[3].x - sg * c[3].y) * kRsqrt2, (-c[3].y + sg * c[3].x) * kRsqrt2);
+    dft4<INV>(b[0], b[1], b[2], b[3]);
+    dft4<INV>(c[0], c[1], c[2], c[3]);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[2 * m] = b[m], a[2 * m + 1] = c[m];
+}
+
+__device__ __forceinline__ double2 tw_at(const double2* twM, int m, bool inv)
+{
+    const double2 w = twM[m];
+    return inv ? make_double2(w.x, -w.y) : w;
+}
+
+// In-place Stockham FFT of the M-point line z (natural order in and out), thread t of T = M/8 per line.
+// Every thread of the block takes part in every barrier.
+template <bool INV>
+__device__ void fft_line8(double2* z, int M, int t, const double2* twM)
+{
+    const int q8 = M >> 3;
+    int Ns = 1;
+    for (; Ns * 8 <= M; Ns *= 8) {
+        const int j = t, k = j & (Ns - 1);
+        double2 a[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = z[j + r * q8];
+        if (Ns > 1) {
+            const int step = k * (M / (8 * Ns));
+#pragma unroll
+            for (int r = 1; r < 8; ++r) a[r] = cmul(a[r], tw_at(twM, r * step, INV));
+        }
+        dft8<INV>(a);
+        __syncthreads(); // (in place: every read of the stage before any write)
+        const int base = (j - k) * 8 + k;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) z[base + r * Ns] = a[r];
+        __syncthreads();
+    }
+    if (Ns == M) return;
+    if (Ns * 4 == M) { // radix 4: two butterflies per thread
+        const int q = M >> 2;
+        double2 a[2][4];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int j = t + b * q8, k = j & (Ns - 1), step = k * (M / (4 * Ns));
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[b][r] = z[j + r * q];
+#pragma unroll
+            for (int r = 1; r < 4; ++r) a[b][r] = cmul(a[b][r], tw_at(twM, r * step, INV));
+            dft4<INV>(a[b][0], a[b][1], a[b][2], a[b][3]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int j = t + b * q8, k = j & (Ns - 1), base = (j - k) * 4 + k;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) z[base + r * Ns] = a[b][r];
+        }
+        __syncthreads();
+    } else { // radix 2: four butterflies per thread
+        const int q = M >> 1;
+        double2 a[4][2];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = t + b * q8, k = j & (Ns - 1), step = k * (M / (2 * Ns));
+            const double2 x0 = z[j], x1 = cmul(z[j + q], tw_at(twM, step, INV));
+            a[b][0] = make_double2(x0.x + x1.x, x0.y + x1.y);
+            a[b][1] = make_double2(x0.x - x1.x, x0.y - x1.y);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = t + b * q8, k = j & (Ns - 1), base = (j - k) * 2 + k;
+            z[base] = a[b][0], z[base + Ns] = a[b][1];
+        }
+        __syncthreads();
+    }
+}
+
+// DCT-II of the line held (Makhoul-reordered, as M complex) in z, FFT'd in place: the untangling split
+// (dct2_row) pair-wise (k, M - k), so every thread reads its pairs before any X is written over z.
+// X (L reals) overwrites z.  ti: this thread's index within its line, T threads per line.
+__device__ void dct2_post(double2* z, int L, int M, int ti, int T, const double2* __restrict__ wL,
+                          const double2* __restrict__ qt)
+{
+    double* X = reinterpret_cast<double*>(z);
+    constexpr int kP = 5; // pairs per thread: ceil((M/2 + 1) / (M/8)) <= 5
+    double out[kP][4];
+    const int npair = M / 2 + 1; // k = 0 .. M/2 (k and M - k together)
+#pragma unroll
+    for (int nb = 0; nb < kP; ++nb) {
+        const int k = ti + nb * T;
+        if (k >= npair) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kh = h ? M - k : k;
+            const double2 a = z[kh < M ? kh : 0], bc = z[kh > 0 ? M - kh : 0];
+            const double2 b = make_double2(bc.x, -bc.y);
+            const double2 sm = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+            const double2 d = make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y));
+            const double2 wd = cmul(wl(wL, kh, M), d);
+            const double2 V = make_double2(sm.x + wd.y, sm.y - wd.x);
+            const double2 q = __ldg(qt + kh);
+            out[nb][2 * h] = V.x * q.x - V.y * q.y;
+            if (kh > 0 && kh < M) {
+                const double2 q2 = __ldg(qt + (L - kh));
+                out[nb][2 * h + 1] = V.x * q2.x + V.y * q2.y;
+            } else {
+                out[nb][2 * h + 1] = 0.0;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < kP; ++b) {
+        const int k = ti + b * T;
+        if (k >= npair) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kh = h ? M - k : k;
+            if (h && kh == k) continue; // (k = M/2 pairs with itself)
+            X[kh] = out[b][2 * h];
+            if (kh > 0 && kh < M) X[L - kh] = out[b][2 * h + 1];
+        }
+    }
+    __syncthreads();
+}
+
+// DCT-III pre-twiddle (dct3_row) of X (L reals aliasing z) into the M-point spectrum in place, pair-wise.
+__device__ void dct3_pre(double2* z, int L, int M, int ti, int T, const double2* __restrict__ wL,
+                         const double2* __restrict__ qt)
+{
+    const double* X = reinterpret_cast<const double*>(z);
+    auto Vk = [&](int k) {
+        const double2 q = __ldg(qt + k);
+        const double a = X[k], b = k > 0 ? X[L - k] : 0.0;
+        return make_double2(q.x * a - q.y * b, -q.y * a - q.x * b);
+    };
+    constexpr int kP = 5;
+    double2 out[kP][2];
+    const int npair = M / 2 + 1;
+#pragma unroll
+    for (int nb = 0; nb < kP; ++nb) {
+        const int k = ti + nb * T;
+        if (k >= npair) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kh = h ? M - k : k;
+            if (kh >= M) { out[nb][h] = make_double2(0.0, 0.0); continue; }
+            const double2 a = Vk(kh), bb = Vk(M - kh);
+            const double2 b = make_double2(bb.x, -bb.y);
+            const double2 sm = make_double2(a.x + b.x, a.y + b.y), d = make_double2(a.x - b.x, a.y - b.y);
+            double2 w = wl(wL, kh, M);
+            w.y = -w.y;
+            const double2 wd = cmul(w, d);
+            out[nb][h] = make_double2(sm.x - wd.y, sm.y + wd.x);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < kP; ++b) {
+        const int k = ti + b * T;
+        if (k >= npair) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kh = h ? M - k : k;
+            if (kh >= M || (h && kh == k)) continue;
+            z[kh] = out[b][h];
+        }
+    }
+    __syncthreads();
+}
+
+// MODE 0: DCT-II, 1: DCT-III, 2: the x pass DCT-III(DCT-II(line) / lambda_uv / (nx ny)), (0, 0) dropped.
+// Line l of the launch: element n at in[l * line_step + n * elem_stride]; a CTA takes LPC = 1024 / M
+// consecutive lines (2 at L = 1024: 512 CTAs for a 1024-line pass, ~3.5 per SM).
+template <int MODE>
+__global__ void __launch_bounds__(kLineThreads) k_dct_lines(int L, int nlines, long long line_step,
+                                                            long long elem_stride, const double* __restrict__ in,
+                                                            double* __restrict__ out, DctTables T, int nx, int ny,
+                                                            double ibw2, double ibh2)
+{
+    extern __shared__ double2 lsm[];
+    const int M = L >> 1, TPL = M >> 3, LPC = kLineThreads / TPL;
+    const int lgL = __ffs(L) - 1, lgP = __ffs(LPC) - 1; // (powers of two: index math by shifts)
+    double2* twM = lsm;                 // [M] W_M^m
+    double2* lines = lsm + M;           // [LPC][M]
+    for (int m = threadIdx.x; m < M; m += kLineThreads) {
+        const int j = 2 * m; // W_M^m = W_L^{2m}, from the half table W_L^j (j < M), W_L^{j + M} = -W_L^j
+        const double2 w = __ldg(T.tw + (j < M ? j : j - M));
+        twM[m] = j < M ? w : make_double2(-w.x, -w.y);
+    }
+    const int l0 = blockIdx.x * LPC;
+    const int nl = min(LPC, nlines - l0);
+    // load, Makhoul-reordered (MODE 1 loads X as is)
+    const bool cols = elem_stride != 1;
+    for (int idx = threadIdx.x; idx < LPC * L; idx += kLineThreads) {
+        int l, n;
+        if (cols) l = idx & (LPC - 1), n = idx >> lgP; // (adjacent lines are adjacent in memory)
+        else l = idx >> lgL, n = idx & (L - 1);
+        double* v = reinterpret_cast<double*>(lines + l * M);
+        const double x = l < nl ? in[(l0 + l) * line_step + n * elem_stride] : 0.0;
+        v[MODE == 1 ? n : makhoul_pos(n, L)] = x;
+    }
+    __syncthreads();
+    const int li = threadIdx.x / TPL, ti = threadIdx.x & (TPL - 1);
+    double2* z = lines + li * M;
+    if (MODE != 1) {
+        fft_line8<false>(z, M, ti, twM);
+        dct2_post(z, L, M, ti, TPL, T.tw, T.qt);
+    }
+    if (MODE == 2) {
+        double* X = reinterpret_cast<double*>(z);
+        const int v = l0 + li;
+        const double lv = v < nlines ? __ldg(T.lam_y + v) * ibh2 : 1.0, inv_b = 1.0 / (static_cast<double>(nx) * ny);
+        for (int u = ti; u < L; u += TPL) {
+            const double lam = __ldg(T.lam + u) * ibw2 + lv;
+            X[u] = (u == 0 && v == 0) ? 0.0 : X[u] / lam * inv_b;
+        }
+        __syncthreads();
+    }
+    if (MODE != 0) {
+        dct3_pre(z, L, M, ti, TPL, T.tw, T.qt);
+        fft_line8<true>(z, M, ti, twM);
+    }
+    for (int idx = threadIdx.x; idx < LPC * L; idx += kLineThreads) {
+        int l, n;
+        if (cols) l = idx & (LPC - 1), n = idx >> lgP;
+        else l = idx >> lgL, n = idx & (L - 1);
+        if (l >= nl) continue;
+        const double* v = reinterpret_cast<const double*>(lines + l * M);
+        out[(l0 + l) * line_step + n * elem_stride] = v[MODE == 0 ? n : makhoul_pos(n, L)];
+    }
+}
+
+bool lines_path(int L) { return L >= 32 && L <= 2048 && (L & (L - 1)) == 0; } // (M / 8 <= 128 threads)
+
+template <int MODE>
+void launch_lines(int nlines, int L, long long line_step, long long elem_stride, const ElectroPlan::Axis& ax,
+                  const ElectroPlan::Axis& other, const double* in, double* out, int nx, int ny, double ibw2,
+                  double ibh2, cudaStream_t st)
+{
+    const int M = L / 2, LPC = kLineThreads / (M / 8);
+    const size_t sm = sizeof(double2) * static_cast<size_t>(M) * (LPC + 1);
+    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_dct_lines<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(sm)));
+    const DctTables T{ax.tw.p, ax.qt.p, ax.c4.p, ax.lam.p, other.lam.p};
+    k_dct_lines<MODE><<<(nlines + LPC - 1) / LPC, kLineThreads, sm, st>>>(L, nlines, line_step, elem_stride, in, out, T,
+                                                                          nx, ny, ibw2, ibh2);
+    CK_LAUNCH();
+}
+
 size_t dct_smem(int L) { return is_pow2(L) ? 20 * static_cast<size_t>(L) + 16 : 16 * static_cast<size_t>(L); }
 
 template <int MODE>
@@ -347,6 +634,16 @@ void ElectroPlan::ensure(int gx, int gy)
     CK(cudaStreamSynchronize(0));
 }
 
+// TDPG_DCT_LINES=0: the one-row-per-CTA kernels with transposes (A/B switch).
+bool lines_fast()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_DCT_LINES");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 // psi = L^+ (rho - mean rho) on the session's grid (rho in plan.rho), stream-ordered on `st`.
 void electro_solve(tdpg_session* s, cudaStream_t st)
 {
@@ -354,6 +651,12 @@ void electro_solve(tdpg_session* s, cudaStream_t st)
     ElectroPlan& E = g.electro;
     const int nx = g.nx, ny = g.ny;
     const double ibw2 = 1.0 / (g.bw * g.bw), ibh2 = 1.0 / (g.bh * g.bh);
+    if (lines_path(nx) && lines_path(ny) && lines_fast()) { // batched lines, no transposes (layout: bin (x, y) at x ny + y)
+        launch_lines<0>(nx, ny, ny, 1, E.ay, E.ax, E.rho, E.r1, nx, ny, ibw2, ibh2, st);   // DCT-II along y (rows)
+        launch_lines<2>(ny, nx, 1, ny, E.ax, E.ay, E.r1, E.r2, nx, ny, ibw2, ibh2, st);    // x: II, /lambda, III (columns)
+        launch_lines<1>(nx, ny, ny, 1, E.ay, E.ax, E.r2, E.psi, nx, ny, ibw2, ibh2, st);   // DCT-III along y
+        return;
+    }
     const dim3 tb(32, 8);
     launch_rows<0>(nx, ny, E.ay, E.ax, E.rho, E.r1, nx, ny, ibw2, ibh2, st);                        // DCT-II along y
     k_transpose<<<dim3((ny + 31) / 32, (nx + 31) / 32), tb, 0, st>>>(nx, ny, E.r1, E.r2);     // -> [ny][nx]

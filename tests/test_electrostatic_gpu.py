@@ -21,7 +21,7 @@ def _stencil(psi, bw, bh):
     return (2 * psi - q[:-2, 1:-1] - q[2:, 1:-1]) / bw ** 2 + (2 * psi - q[1:-1, :-2] - q[1:-1, 2:]) / bh ** 2
 
 
-@pytest.mark.parametrize("nx,ny", [(32, 32), (64, 48), (20, 12), (7, 5), (1024, 1024), (256, 96)])
+@pytest.mark.parametrize("nx,ny", [(32, 32), (64, 48), (20, 12), (7, 5), (1024, 1024), (256, 96), (128, 2048), (2048, 64), (64, 512), (4096, 32)])
 def test_poisson_residual(design, nx, ny):
     s = Session(design)
     s.set_density_model("electrostatic")
