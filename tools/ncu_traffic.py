@@ -1,11 +1,12 @@
-"""profiles/traffic_<tag>.json: DRAM bytes (read + write) per launch of each GP kernel from one
-`ncu --set full` capture (bench.py reads it into roofline.traffic).  Usage: ncu_traffic.py REPORT OUT"""
+"""DRAM bytes (read + write) per launch of each GP kernel from one `ncu --set full` capture, merged into
+profiles/traffic.json under the configuration key "<cells>x<grid>" that bench.py reads into
+roofline.traffic.  Usage: ncu_traffic.py REPORT OUT_JSON [KEY]"""
 import csv
 import json
 import subprocess
 import sys
 
-MAP = {"k_density_scatter_win": "density_scatter", "k_dens_grad": "dens_grad", "k_cells": "cells",
+MAP = {"k_density_scatter_win": "density_scatter", "k_density_scatter_limbs": "density_scatter", "k_dens_grad": "dens_grad", "k_cells": "cells",
        "k_density_bins": "density_bins", "k_finalize": "finalize", "k_wa_": "wirelength_pp"}
 raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
@@ -24,6 +25,12 @@ for row in r[2:]:
 out = {}
 for key, kernels in per.items():  # sum over the kernels of one stage, mean over repeated launches
     out[key] = round(sum(sum(v) / len(v) for v in kernels.values()))
-out["_source"] = sys.argv[1].split("/")[-1] + " (ncu --set full --clock-control none, 1M-cell iteration)"
-json.dump(out, open(sys.argv[2], "w"), indent=1)
-print(out)
+out["_source"] = sys.argv[1].split("/")[-1] + " (ncu --set full --clock-control none, one GP iteration)"
+key = sys.argv[3] if len(sys.argv) > 3 else "1100000x1024"
+try:
+    allk = json.load(open(sys.argv[2]))
+except (OSError, ValueError):
+    allk = {}
+allk[key] = out
+json.dump(allk, open(sys.argv[2], "w"), indent=1)
+print(key, out)
