@@ -331,13 +331,20 @@ __global__ void __launch_bounds__(2 * kBlock, (N <= 5 ? 2 : 1)) k_wa_axis(int bl
 
 // Several size classes in one launch (their blocks are contiguous in the table): each block dispatches
 // on its pin count; the register budget is the group's largest class.
+// L2 prefetch of a byte range (TMA engine; 16-byte aligned, size a multiple of 16).
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <int LO, int HI, int MINB>
 __global__ void __launch_bounds__(2 * kBlock, MINB) k_wa_axis_group(int blk0, WaAxisArgs A,
-                                                                    const Ctrl* __restrict__ ctrl)
+                                                                    const Ctrl* __restrict__ ctrl, int ahead)
 {
     __shared__ double sh[48];
     const int g = blk0 + blockIdx.x;
     const int4 b = wa_blk_of(g, A);
+    const int gridw = gridDim.x;
     switch (b.x) {
     case 2: if (LO <= 2 && 2 <= HI) wa_axis_block<(LO <= 2 && 2 <= HI) ? 2 : LO>(b, g, A, sh, ctrl); break;
     case 3: if (LO <= 3 && 3 <= HI) wa_axis_block<(LO <= 3 && 3 <= HI) ? 3 : LO>(b, g, A, sh, ctrl); break;
@@ -347,6 +354,15 @@ __global__ void __launch_bounds__(2 * kBlock, MINB) k_wa_axis_group(int blk0, Wa
     case 7: if (LO <= 7 && 7 <= HI) wa_axis_block<(LO <= 7 && 7 <= HI) ? 7 : LO>(b, g, A, sh, ctrl); break;
     case 8: if (LO <= 8 && 8 <= HI) wa_axis_block<(LO <= 8 && 8 <= HI) ? 8 : LO>(b, g, A, sh, ctrl); break;
     default: break;
+    }
+    // a block about one resident wave ahead (blocks are dispatched in order): its entry records into L2
+    // now, so its first loads wait for L2 instead of DRAM
+    if (ahead > 0 && threadIdx.x == 0 && blockIdx.x + ahead < gridw) {
+        const int4 f = wa_blk_of(g + ahead, A);
+        const unsigned n = static_cast<unsigned>(f.x) * kBlock;
+        prefetch_l2(A.e_cell + f.w, n * 4u);
+        prefetch_l2(A.e_off + 2 * static_cast<long long>(f.w), n * 16u);
+        if (A.pp.w_e) prefetch_l2(A.pp.w_e + f.w, n * 8u);
     }
 }
 
@@ -1532,6 +1548,18 @@ inline int wa_groups()
     return g;
 }
 
+// TDPG_WA_AHEAD: prefetch distance unit of the WA kernels' L2 prefetch (the 2-5 group prefetches 4x, the
+// 6-8 group 2x this many blocks ahead; 0 disables it).  Measured at 1M (WA serialised, bench): 0: 111-113 us,
+// 37: 112, 74 (default): 107, 148: 110.
+inline int wa_ahead()
+{
+    static const int a = [] {
+        const char* e = std::getenv("TDPG_WA_AHEAD");
+        return e ? std::atoi(e) : 74;
+    }();
+    return a;
+}
+
 // TDPG_WA_AXIS=0 selects the one-thread-per-net class kernels (A/B switch).
 inline bool wa_axis_split()
 {
@@ -1609,10 +1637,10 @@ void launch_wirelength_pp(tdpg_session* s, double gamma, bool use_net_w, double*
         };
         int b0, nb;
         if (groups == 1) {
-            if (range(2, 5, b0, nb)) k_wa_axis_group<2, 5, 2><<<nb, 2 * kBlock, 0, st(1)>>>(b0, A, ctrl);
-            if (range(6, 8, b0, nb)) k_wa_axis_group<6, 8, 1><<<nb, 2 * kBlock, 0, st(2)>>>(b0, A, ctrl);
+            if (range(2, 5, b0, nb)) k_wa_axis_group<2, 5, 2><<<nb, 2 * kBlock, 0, st(1)>>>(b0, A, ctrl, 4 * wa_ahead());
+            if (range(6, 8, b0, nb)) k_wa_axis_group<6, 8, 1><<<nb, 2 * kBlock, 0, st(2)>>>(b0, A, ctrl, 2 * wa_ahead());
         } else {
-            if (range(2, 8, b0, nb)) k_wa_axis_group<2, 8, 1><<<nb, 2 * kBlock, 0, st(1)>>>(b0, A, ctrl);
+            if (range(2, 8, b0, nb)) k_wa_axis_group<2, 8, 1><<<nb, 2 * kBlock, 0, st(1)>>>(b0, A, ctrl, 2 * wa_ahead());
         }
         CK_LAUNCH();
     } else {
