@@ -1786,6 +1786,42 @@ void net_weights_record(tdpg_session* s, const Ctrl* ctrl)
     CK_LAUNCH();
 }
 
+// After a stable radix sort on the upper 32 bits of the endpoint keys: each run of equal upper halves among
+// the first nv entries (the violated endpoints) is re-sorted by the full key with a stable insertion sort by
+// the thread at its start, so the order is exactly the 64-bit stable sort's (slack, then pin).  Runs are a few
+// entries (the upper half keeps ~6 significant digits of the slack).
+__global__ void k_ep_fixup(const long long* __restrict__ nv_ptr, unsigned long long* __restrict__ keys,
+                           int* __restrict__ vals)
+{
+    const long long nv = *nv_ptr;
+    for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i + 1 < nv;
+         i += static_cast<long long>(gridDim.x) * kBlock) {
+        const unsigned hi = static_cast<unsigned>(keys[i] >> 32);
+        if ((i > 0 && static_cast<unsigned>(keys[i - 1] >> 32) == hi) || static_cast<unsigned>(keys[i + 1] >> 32) != hi)
+            continue; // not the start of a run of two or more
+        long long e = i + 2;
+        while (e < nv && static_cast<unsigned>(keys[e] >> 32) == hi) ++e;
+        for (long long j = i + 1; j < e; ++j) { // stable: only strictly greater keys move
+            const unsigned long long k = keys[j];
+            const int v = vals[j];
+            long long q = j - 1;
+            while (q >= i && keys[q] > k) keys[q + 1] = keys[q], vals[q + 1] = vals[q], --q;
+            keys[q + 1] = k, vals[q + 1] = v;
+        }
+    }
+}
+
+// TDPG_EP_SORT64=1: the endpoint sort over all 64 key bits (8 radix passes) instead of the upper 32 bits and
+// the run fix-up (4 passes + one kernel); A/B switch.
+bool ep_sort64()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_EP_SORT64");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // The endpoints in (slack, pin) order into sort_v1 (paths.cpp:77-87), from the keys sta_record left in
 // sort_k0 / sort_v0.  Readers take only the first (violated-count) entries: when few fail, compact them
 // stably and sort the smallest size class holding them; else sort every endpoint.  Capturable.
@@ -1796,9 +1832,17 @@ void sort_violated_endpoints(tdpg_session* s, const Ctrl* ctrl)
     CK_LAUNCH();
     switch_by_count(s, s->ep_nv.p, EP, [&](cudaStream_t st, long long n) {
         size_t b = s->cub_tmp.n;
+        const int lo_bit = ep_sort64() ? 0 : 32;
+        auto fixup = [&] {
+            if (lo_bit == 0) return;
+            k_ep_fixup<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(n, kBlock), 148 * 4)), kBlock, 0, st>>>(
+                s->ep_nv.p, s->sort_k1.p, s->sort_v1.p);
+            CK_LAUNCH();
+        };
         if (n >= EP) {
             CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, b, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p,
-                                               s->sort_v1.p, EP, 0, 64, st));
+                                               s->sort_v1.p, EP, lo_bit, 64, st));
+            fixup();
             return;
         }
         k_flag_keys<<<std::min<unsigned>(blocks_for(EP, kBlock), 148 * 4), kBlock, 0, st>>>(EP, s->sort_k0, s->ep_flag);
@@ -1811,7 +1855,8 @@ void sort_violated_endpoints(tdpg_session* s, const Ctrl* ctrl)
         CK_LAUNCH();
         b = s->cub_tmp.n;
         CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, b, s->ep_kc.p, s->sort_k1.p, s->ep_vc.p, s->sort_v1.p,
-                                           static_cast<int>(n), 0, 64, st));
+                                           static_cast<int>(n), lo_bit, 64, st));
+        fixup();
     });
 }
 
