@@ -1153,6 +1153,42 @@ void resolve_ties_dev(tdpg_session* s)
     s->ties_resolved = true;
 }
 
+// After a stable radix sort on the upper 32 bits of the endpoint keys: each run of equal upper halves among
+// the first nv entries (the violated endpoints) is re-sorted by the full key with a stable insertion sort by
+// the thread at its start, so the order is exactly the 64-bit stable sort's (slack, then pin).  Runs are a few
+// entries (the upper half keeps ~6 significant digits of the slack).
+__global__ void k_ep_fixup(const long long* __restrict__ nv_ptr, const double* __restrict__ nv_d,
+                           unsigned long long* __restrict__ keys, int* __restrict__ vals)
+{
+    const long long nv = nv_ptr ? *nv_ptr : static_cast<long long>(nv_d[2]); // (sta_out[2]: violated count)
+    for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i + 1 < nv;
+         i += static_cast<long long>(gridDim.x) * kBlock) {
+        const unsigned hi = static_cast<unsigned>(keys[i] >> 32);
+        if ((i > 0 && static_cast<unsigned>(keys[i - 1] >> 32) == hi) || static_cast<unsigned>(keys[i + 1] >> 32) != hi)
+            continue; // not the start of a run of two or more
+        long long e = i + 2;
+        while (e < nv && static_cast<unsigned>(keys[e] >> 32) == hi) ++e;
+        for (long long j = i + 1; j < e; ++j) { // stable: only strictly greater keys move
+            const unsigned long long k = keys[j];
+            const int v = vals[j];
+            long long q = j - 1;
+            while (q >= i && keys[q] > k) keys[q + 1] = keys[q], vals[q + 1] = vals[q], --q;
+            keys[q + 1] = k, vals[q + 1] = v;
+        }
+    }
+}
+
+// TDPG_EP_SORT64=1: the endpoint sort over all 64 key bits (8 radix passes) instead of the upper 32 bits and
+// the run fix-up (4 passes + one kernel); A/B switch.
+bool ep_sort64()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("TDPG_EP_SORT64");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // violated_endpoints (paths.cpp:77-87) of the current STA: (slack, pin) order in sort_v1; returns
 // how many endpoints violate.
 int sorted_violated(tdpg_session* s)
@@ -1175,8 +1211,14 @@ int sorted_violated(tdpg_session* s)
         cub::DeviceRadixSort::SortPairs(nullptr, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, s->EP,
                                         0, 64, s->st);
         void* tmp = cub_scratch(s, bytes);
+        const int lo_bit = ep_sort64() ? 0 : 32; // (upper halves, then the exact run fix-up)
         CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p, s->sort_v1.p, s->EP,
-                                           0, 64, s->st));
+                                           lo_bit, 64, s->st));
+        if (lo_bit) {
+            k_ep_fixup<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(s->EP, kBlock), 148 * 4)), kBlock, 0,
+                         s->st>>>(nullptr, out3, s->sort_k1.p, s->sort_v1.p);
+            CK_LAUNCH();
+        }
     }
     double h[3];
     CK(cudaMemcpyAsync(h, out3, sizeof h, cudaMemcpyDeviceToHost, s->st));
@@ -1236,8 +1278,14 @@ void extract_endpoint_dev(tdpg_session* s, int n)
                                                    s->sort_v0, s->part);
         k_sta_final<<<1, kBlock, 0, s->st>>>(nb, s->part, out3);
         size_t bytes = s->cub_tmp.n;
+        const int lo_bit = ep_sort64() ? 0 : 32; // (upper halves, then the exact run fix-up)
         CK(cub::DeviceRadixSort::SortPairs(s->cub_tmp.p, bytes, s->sort_k0.p, s->sort_k1.p, s->sort_v0.p,
-                                           s->sort_v1.p, EP, 0, 64, s->st));
+                                           s->sort_v1.p, EP, lo_bit, 64, s->st));
+        if (lo_bit) {
+            k_ep_fixup<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(EP, kBlock), 148 * 4)), kBlock, 0,
+                         s->st>>>(nullptr, out3, s->sort_k1.p, s->sort_v1.p);
+            CK_LAUNCH();
+        }
         CK(cudaMemsetAsync(s->pair_bits.p, 0, nbits * sizeof(unsigned), s->st));
         CK(cudaMemsetAsync(s->counters.p + 1, 0, sizeof(int), s->st));
         k_bt_walk<<<blocks_for(ub, kBlock), kBlock, 0, s->st>>>(
@@ -1786,42 +1834,6 @@ void net_weights_record(tdpg_session* s, const Ctrl* ctrl)
     CK_LAUNCH();
 }
 
-// After a stable radix sort on the upper 32 bits of the endpoint keys: each run of equal upper halves among
-// the first nv entries (the violated endpoints) is re-sorted by the full key with a stable insertion sort by
-// the thread at its start, so the order is exactly the 64-bit stable sort's (slack, then pin).  Runs are a few
-// entries (the upper half keeps ~6 significant digits of the slack).
-__global__ void k_ep_fixup(const long long* __restrict__ nv_ptr, unsigned long long* __restrict__ keys,
-                           int* __restrict__ vals)
-{
-    const long long nv = *nv_ptr;
-    for (long long i = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; i + 1 < nv;
-         i += static_cast<long long>(gridDim.x) * kBlock) {
-        const unsigned hi = static_cast<unsigned>(keys[i] >> 32);
-        if ((i > 0 && static_cast<unsigned>(keys[i - 1] >> 32) == hi) || static_cast<unsigned>(keys[i + 1] >> 32) != hi)
-            continue; // not the start of a run of two or more
-        long long e = i + 2;
-        while (e < nv && static_cast<unsigned>(keys[e] >> 32) == hi) ++e;
-        for (long long j = i + 1; j < e; ++j) { // stable: only strictly greater keys move
-            const unsigned long long k = keys[j];
-            const int v = vals[j];
-            long long q = j - 1;
-            while (q >= i && keys[q] > k) keys[q + 1] = keys[q], vals[q + 1] = vals[q], --q;
-            keys[q + 1] = k, vals[q + 1] = v;
-        }
-    }
-}
-
-// TDPG_EP_SORT64=1: the endpoint sort over all 64 key bits (8 radix passes) instead of the upper 32 bits and
-// the run fix-up (4 passes + one kernel); A/B switch.
-bool ep_sort64()
-{
-    static const bool on = [] {
-        const char* e = std::getenv("TDPG_EP_SORT64");
-        return e && std::atoi(e) != 0;
-    }();
-    return on;
-}
-
 // The endpoints in (slack, pin) order into sort_v1 (paths.cpp:77-87), from the keys sta_record left in
 // sort_k0 / sort_v0.  Readers take only the first (violated-count) entries: when few fail, compact them
 // stably and sort the smallest size class holding them; else sort every endpoint.  Capturable.
@@ -1836,7 +1848,7 @@ void sort_violated_endpoints(tdpg_session* s, const Ctrl* ctrl)
         auto fixup = [&] {
             if (lo_bit == 0) return;
             k_ep_fixup<<<std::max<unsigned>(1, std::min<unsigned>(blocks_for(n, kBlock), 148 * 4)), kBlock, 0, st>>>(
-                s->ep_nv.p, s->sort_k1.p, s->sort_v1.p);
+                s->ep_nv.p, nullptr, s->sort_k1.p, s->sort_v1.p);
             CK_LAUNCH();
         };
         if (n >= EP) {
