@@ -1171,10 +1171,12 @@ __global__ void __launch_bounds__(kFinBlock) k_fin_density(FinArgs a, Ctrl* ctrl
     const int it = ctrl->iter;
     const double lambda = a.sched ? a.sched[it].lambda : a.lambda_single;
     const double overflow = a.total_movable > 0.0 ? r[1] / a.total_movable : 0.0;
-    cur->lambda = lambda, cur->iter = it, cur->do_adam = 0, cur->live = 1;
+    cur->lambda = lambda, cur->iter = it, cur->do_adam = 0, cur->live = 1, cur->stop = 0;
     cur->density = r[0], cur->overflow = overflow;
-    if (ctrl->engaged && overflow <= a.stop_overflow) { // placer.cpp:459-462
-        ctrl->stopped = 1;
+    // placer.cpp:459-462.  The flag the other kernels read is raised by k_fin_terms, after this iteration's
+    // WA kernels: they run beside this kernel and must not see the stop before they have run.
+    if (ctrl->engaged && overflow <= a.stop_overflow) {
+        cur->stop = 1;
         return;
     }
     if (a.sched) {
@@ -1211,6 +1213,7 @@ __global__ void __launch_bounds__(kFinBlock) k_fin_terms(FinArgs a, Ctrl* ctrl, 
     }
     if (a.timing_row_clear) a.timing_row_clear[0] = 0.0;
     ctrl->rows = it + 1;
+    if (cur->stop) ctrl->stopped = 1;
 }
 
 // =====================================================================================
@@ -1272,23 +1275,20 @@ __device__ __forceinline__ double2 dens_grad5(int bx, int by, int sx_n, int sy_n
 
 // field = excess with fscale 2 (d sum excess^2, density.cpp:148-156) or the potential with fscale 1.
 // Cells of Grid::wide are skipped here (k_dens_grad_wide).
-template <bool EARLY>
 __global__ void __launch_bounds__(kBlock, 4) k_dens_grad(int n_mov, const int* __restrict__ perm,
                                                       const double2* __restrict__ xy_sp,
                                                       const double2* __restrict__ wh_sp, GridDev g,
                                                       const double* __restrict__ excess, double2* __restrict__ dgrad,
                                                       const Ctrl* __restrict__ ctrl, double fscale)
-{   // A programmatic dependent of the bins kernel.  The cell positions and sizes in spatial order were
-    // written by the scatter, which completed before the bins kernel started (it does not trigger early),
-    // so with EARLY they are loaded before pdl_wait(), overlapping the bins kernel; the excess field and
-    // the stop flag are read after it.
+{   // A programmatic dependent of the bins kernel: everything an earlier kernel of the iteration wrote (the
+    // scatter's spatial-order copies, the excess field, the stop flag) is read after pdl_wait() — a kernel
+    // may start once its primary's CTAs have exited, before their writes are guaranteed visible (loading
+    // the scatter's copies before the wait was measured to read stale data under compute-sanitizer).
     pdl_trigger();
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    double2 p = make_double2(0.0, 0.0), s = make_double2(0.0, 0.0);
-    if (EARLY && i < n_mov) p = xy_sp[i], s = wh_sp[i];
     pdl_wait();
+    const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n_mov) return;
-    if (!EARLY) p = xy_sp[i], s = wh_sp[i];
+    const double2 p = xy_sp[i], s = wh_sp[i];
     const bool stop = ctrl && ctrl->stopped;
     if (stop || s.x > g.wide_w || s.y > g.wide_h) return;
     double wx[kF5], dwx[kF5], wy[kF5], dwy[kF5];
@@ -1787,23 +1787,12 @@ CellArgs cell_args(tdpg_session* s, double2* d_cell, double2* m, double2* v, dou
     return a;
 }
 
-// TDPG_DGRAD_EARLY=0: the density gradient loads its cells after pdl_wait() (A/B switch).
-bool dens_grad_early()
-{
-    static const bool on = [] {
-        const char* e = std::getenv("TDPG_DGRAD_EARLY");
-        return !(e && std::atoi(e) == 0);
-    }();
-    return on;
-}
-
 void launch_dens_grad(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st)
 {
     const int n_mov = s->grid.n_movable;
     if (n_mov > 0) {
         const bool el = s->grid.model == 1;
-        CK(launch_pdl(dens_grad_early() ? k_dens_grad<true> : k_dens_grad<false>, blocks_for(n_mov, kBlock), kBlock, st,
-                      s->pdl_graph,
+        CK(launch_pdl(k_dens_grad, blocks_for(n_mov, kBlock), kBlock, st, s->pdl_graph,
                       n_mov, static_cast<const int*>(s->grid.perm.p), static_cast<const double2*>(s->grid.xy_sp.p),
                       static_cast<const double2*>(s->grid.wh_sp.p), grid_dev(s),
                       static_cast<const double*>(el ? s->grid.electro.psi.p : s->grid.excess.p), s->dgrad.p, ctrl,
@@ -2172,7 +2161,7 @@ void launch_dens_grad_part(tdpg_session* s, const Ctrl* ctrl, cudaStream_t st, i
     const bool el = s->grid.model == 1;
     const double* field = el ? s->grid.electro.psi.p : s->grid.excess.p;
     if (hi > lo) {
-        k_dens_grad<false><<<blocks_for(hi - lo, kBlock), kBlock, 0, st>>>(hi - lo, s->grid.perm.p + lo,
+        k_dens_grad<<<blocks_for(hi - lo, kBlock), kBlock, 0, st>>>(hi - lo, s->grid.perm.p + lo,
                                                                     s->grid.xy_sp.p + lo, s->grid.wh_sp.p + lo,
                                                                     grid_dev(s), field, s->dgrad, ctrl, el ? 1.0 : 2.0);
         CK_LAUNCH();

@@ -132,7 +132,8 @@ __device__ __forceinline__ bool axis5(double lo, double hi, double origin, doubl
 
 struct IterCur { // schedule values of the iteration being executed
     double lr, c1, c2, lambda;
-    int iter, do_adam, live, pad1; // live: the iteration ran (the engine was not already stopped)
+    int iter, do_adam, live, stop; // live: the iteration ran (the engine was not already stopped);
+                                   // stop: it met the stop condition (k_fin_terms raises ctrl->stopped)
     double density, overflow;      // the density terms (k_fin_density -> k_fin_terms)
 };
 
