@@ -130,6 +130,7 @@ struct tdpg_session {
     std::vector<uint8_t> h_cell_fixed, h_is_source, h_is_endpoint;
     std::vector<int> h_pin_cell, h_net_start, h_sources, h_endpoints, h_pin_net, h_pin_entry;
     std::vector<std::string> pin_names;
+    bool pin_names_blank = false; // names were given and all empty (error text prints them empty)
     std::vector<int> h_level, h_lvl_start, h_arc_from, h_arc_to, h_arc_kind, h_arc_owner; // (level / arcs: lazy)
     bool h_level_valid = false, h_arcs_valid = false;
     tdpg::DBuf<int> arc_from, arc_to, arc_kind, arc_owner; // arcs by id (timing_graph.cpp:60-77)
@@ -284,6 +285,9 @@ namespace tdpg {
 
 // session.cu
 void upload_positions(tdpg_session* s, const double* xy);
+// host <-> device copies of netlist-sized arrays through the process-wide pinned staging buffers (session.cu)
+void upload_bytes_staged(void* dst, const void* src, size_t bytes, cudaStream_t st);
+void download_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st);
 void host_pin_maps(tdpg_session* s);
 void refresh_fixed_baseline(tdpg_session* s);
 void build_graph_device(tdpg_session* s); // graph.cu

@@ -1844,7 +1844,7 @@ Terms evaluate_objective(tdpg_session* s, double gamma, double lambda, double be
     launch_cell_pass(s, ca, cur, nullptr);
     Terms t;
     CK(cudaMemcpyAsync(&t, terms, sizeof(Terms), cudaMemcpyDeviceToHost, s->st));
-    if (d_cell_host) s->d_cell.download(reinterpret_cast<double2*>(d_cell_host), s->C, s->st);
+    if (d_cell_host) download_bytes(d_cell_host, s->d_cell.p, sizeof(double2) * static_cast<size_t>(s->C), s->st);
     CK(cudaStreamSynchronize(s->st));
     return t;
 }

@@ -332,7 +332,9 @@ void build_graph_device(tdpg_session* s)
         CK(cudaMemcpyAsync(h_in_start.data(), s->in_start.p, sizeof(int) * (P + 1), cudaMemcpyDeviceToHost, st));
         if (A) CK(cudaMemcpyAsync(h_in_from.data(), s->in_from.p, sizeof(int) * A, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        auto name = [&](int p) { return s->pin_names.empty() ? "p" + std::to_string(p) : s->pin_names[p]; };
+        auto name = [&](int p) {
+            return s->pin_names.empty() ? (s->pin_names_blank ? std::string() : "p" + std::to_string(p)) : s->pin_names[p];
+        };
         int start = -1;
         for (int p = 0; p < P; ++p)
             if (h_indeg[p] > 0) start = p;
@@ -392,7 +394,8 @@ void build_graph_device(tdpg_session* s)
         CK(cudaStreamSynchronize(st));
         if (f != INT_MAX) {
             const int e = s->h_endpoints[f];
-            const std::string nm = s->pin_names.empty() ? "p" + std::to_string(e) : s->pin_names[e];
+            const std::string nm =
+                s->pin_names.empty() ? (s->pin_names_blank ? std::string() : "p" + std::to_string(e)) : s->pin_names[e];
             throw Error(TDPG_ERR_VALIDATION, "validation error: endpoint \"" + nm + "\" unreachable from every source");
         }
     }

@@ -213,7 +213,8 @@ __global__ void k_set_terminals(int P, const int* __restrict__ pin_cell, const d
 
 void upload_positions(tdpg_session* s, const double* xy)
 {
-    s->cell_xy.upload(reinterpret_cast<const double2*>(xy), s->C, s->st);
+    s->cell_xy.reserve(static_cast<size_t>(s->C));
+    upload_bytes_staged(s->cell_xy.p, xy, sizeof(double2) * static_cast<size_t>(s->C), s->st);
     s->sta_valid = false;
     s->pin_xy_external = false;
     refresh_fixed_baseline(s);
@@ -345,7 +346,7 @@ void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st)
     std::lock_guard<std::mutex> lock(S.mu);
     if (!S.buf[0]) {
         for (int k = 0; k < 2; ++k) {
-            CK(cudaHostAlloc(reinterpret_cast<void**>(&S.buf[k]), Stager::kChunk, cudaHostAllocDefault));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&S.buf[k]), Stager::kChunk, cudaHostAllocPortable));
             CK(cudaEventCreateWithFlags(&S.ev[k], cudaEventDisableTiming));
         }
     }
@@ -369,6 +370,54 @@ void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st)
         S.bytes += n;
     }
 }
+
+} // namespace
+
+namespace tdpg {
+
+// Device -> host counterpart of upload_bytes (stream-ordered on `st`, synchronous for the caller): each
+// 32 MB chunk lands in a pinned half by DMA and is copied out by several host threads while the next
+// chunk's DMA runs.  Small copies take the plain path (the caller synchronises).
+void download_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st)
+{
+    if (bytes == 0) return;
+    if (bytes < (size_t(4) << 20)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return;
+    }
+    Stager& S = stager();
+    std::lock_guard<std::mutex> lock(S.mu);
+    if (!S.buf[0]) {
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&S.buf[k]), Stager::kChunk, cudaHostAllocPortable));
+            CK(cudaEventCreateWithFlags(&S.ev[k], cudaEventDisableTiming));
+        }
+    }
+    const size_t nch = (bytes + Stager::kChunk - 1) / Stager::kChunk;
+    auto issue = [&](size_t c) {
+        const size_t off = c * Stager::kChunk, n = std::min(Stager::kChunk, bytes - off);
+        CK(cudaEventSynchronize(S.ev[c & 1])); // (the half's previous user is done)
+        CK(cudaMemcpyAsync(S.buf[c & 1], static_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(S.ev[c & 1], st));
+    };
+    issue(0);
+    for (size_t c = 0; c < nch; ++c) {
+        if (c + 1 < nch) issue(c + 1);
+        CK(cudaEventSynchronize(S.ev[c & 1]));
+        const size_t off = c * Stager::kChunk, n = std::min(Stager::kChunk, bytes - off);
+        char* to = static_cast<char*>(dst) + off;
+        const char* from = S.buf[c & 1];
+        par_for(static_cast<long long>(n), [&](long long lo, long long hi) { std::memcpy(to + lo, from + lo, hi - lo); },
+                size_t(4) << 20);
+    }
+}
+
+void upload_bytes_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) { upload_bytes(dst, src, bytes, st); }
+
+} // namespace tdpg
+
+namespace {
 
 template <typename T>
 void upload_fast(DBuf<T>& b, const T* h, size_t count, cudaStream_t st)
@@ -486,9 +535,15 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
     s->h_net_start.assign(d->net_start, d->net_start + N + 1);
     s->h_sources.assign(d->sources, d->sources + s->S);
     s->h_endpoints.assign(d->endpoints, d->endpoints + s->EP);
-    if (d->pin_names) {
-        s->pin_names.resize(P);
-        for (int p = 0; p < P; ++p) s->pin_names[p] = d->pin_names[p] ? d->pin_names[p] : "";
+    if (d->pin_names) { // (all blank: nothing stored, messages print the blank names)
+        bool any = false;
+        for (int p = 0; p < P && !any; ++p) any = d->pin_names[p] && d->pin_names[p][0];
+        if (any) {
+            s->pin_names.resize(P);
+            for (int p = 0; p < P; ++p) s->pin_names[p] = d->pin_names[p] ? d->pin_names[p] : "";
+        } else {
+            s->pin_names_blank = true;
+        }
     }
     const int* net_pins = d->net_pins;
     const double* pin_off = d->pin_off;
@@ -751,7 +806,7 @@ int tdpg_set_terminal_positions(tdpg_session* s, const double* xy)
 int tdpg_get_positions(tdpg_session* s, double* xy)
 {
     API_BEGIN
-    s->cell_xy.download(reinterpret_cast<double2*>(xy), s->C, s->st);
+    download_bytes(xy, s->cell_xy.p, sizeof(double2) * static_cast<size_t>(s->C), s->st);
     CK(cudaStreamSynchronize(s->st));
     API_END
 }

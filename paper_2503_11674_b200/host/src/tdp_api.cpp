@@ -62,16 +62,29 @@ struct FlatNetlist {
     FlatNetlist(const Netlist& nl, const DesignConstraints& c)
     {
         const size_t C = nl.cells.size(), P = nl.pins.size();
-        for (const Cell& cell : nl.cells)
-            cw.push_back(cell.width), ch.push_back(cell.height), cd.push_back(cell.delay), cf.push_back(cell.is_fixed);
-        for (const Pin& p : nl.pins) {
-            pcell.push_back(p.cell);
-            pt.push_back(p.terminal_pos.x), pt.push_back(p.terminal_pos.y);
-            po.push_back(p.offset.x), po.push_back(p.offset.y);
-            pd.push_back(p.dir == PinDir::Output ? 1 : 0);
-            pc.push_back(p.load_cap);
-            names.push_back(p.name);
+        cw.resize(C), ch.resize(C), cd.resize(C), cf.resize(C);
+        for (size_t i = 0; i < C; ++i) {
+            const Cell& cell = nl.cells[i];
+            cw[i] = cell.width, ch[i] = cell.height, cd[i] = cell.delay, cf[i] = cell.is_fixed;
         }
+        pcell.resize(P), pt.resize(2 * P), po.resize(2 * P), pd.resize(P), pc.resize(P);
+        bool named = false;
+        for (size_t i = 0; i < P; ++i) {
+            const Pin& p = nl.pins[i];
+            pcell[i] = p.cell;
+            pt[2 * i] = p.terminal_pos.x, pt[2 * i + 1] = p.terminal_pos.y;
+            po[2 * i] = p.offset.x, po[2 * i + 1] = p.offset.y;
+            pd[i] = p.dir == PinDir::Output ? 1 : 0;
+            pc[i] = p.load_cap;
+            named = named || !p.name.empty();
+        }
+        if (named) { // (names only feed error messages: skipped when the netlist has none)
+            names.reserve(P);
+            for (const Pin& p : nl.pins) names.push_back(p.name);
+        }
+        size_t E = 0;
+        for (const Net& n : nl.nets) E += 1 + n.sinks.size();
+        ns.reserve(nl.nets.size() + 1), np.reserve(E);
         ns.push_back(0);
         for (const Net& n : nl.nets) {
             np.push_back(n.driver);
@@ -90,6 +103,7 @@ struct FlatNetlist {
         view.endpoints = ep.data(), view.clock_period = c.clock_period > 0 ? c.clock_period : 1.0;
         view.r_unit = c.r_unit, view.c_unit = c.c_unit;
         view.core[0] = c.core.x_lo, view.core[1] = c.core.y_lo, view.core[2] = c.core.x_hi, view.core[3] = c.core.y_hi;
+        if (names.empty()) name_ptrs.assign(P, ""); // (all blank: the engine stores none)
         view.pin_names = name_ptrs.data();
     }
 };
@@ -862,18 +876,21 @@ ObjectiveResult objective_and_gradient(const Netlist& nl, const std::vector<Poin
         throw ValidationError("net weight count does not match net count");
     auto S = session(nl, core_only(grid.core()));
     set_core(S->s, grid.core());
-    const auto xy = flat_points(cell_pos);
-    ck(tdpg_set_positions(S->s, xy.data()));
+    if (cell_pos.size() != nl.cells.size()) throw ValidationError("cell position count does not match cell count");
+    // Point is two packed doubles: the positions go to the device and the gradient comes back in place,
+    // with no intermediate copies (the per-iteration host cost of a reference-style loop)
+    static_assert(sizeof(Point) == 2 * sizeof(double), "Point must be two packed doubles");
+    ck(tdpg_set_positions(S->s, reinterpret_cast<const double*>(cell_pos.data())));
     ck(tdpg_set_grid(S->s, grid.nx(), grid.ny(), grid.target_density()));
     ledger_upload(S->s, weights);
     double terms[6];
-    std::vector<double> d(2 * nl.cells.size());
-    ck(tdpg_objective(S->s, gamma, lambda, beta, kind == PairLossKind::Linear ? 1 : 0,
-                      net_weights.empty() ? nullptr : net_weights.data(), terms, d.data()));
     ObjectiveResult r;
+    r.d_cell.resize(nl.cells.size());
+    ck(tdpg_objective(S->s, gamma, lambda, beta, kind == PairLossKind::Linear ? 1 : 0,
+                      net_weights.empty() ? nullptr : net_weights.data(), terms,
+                      reinterpret_cast<double*>(r.d_cell.data())));
     r.value = terms[0], r.wl_term = terms[1], r.density_term = terms[2], r.pp_term = terms[3], r.hpwl = terms[4];
     r.overflow = terms[5];
-    r.d_cell = points(d);
     return r;
 }
 
