@@ -200,19 +200,16 @@ DesignConstraints core_only(const Rect& core)
     return c;
 }
 
-std::vector<double> flat_points(const std::vector<Point>& p)
-{
-    std::vector<double> v(2 * p.size());
-    for (std::size_t i = 0; i < p.size(); ++i) v[2 * i] = p[i].x, v[2 * i + 1] = p[i].y;
-    return v;
-}
+// Point is two packed doubles, so a std::vector<Point> is already the C-ABI's flat (x, y) array: the
+// engine reads the caller's positions in place and writes results straight into Point vectors.
+static_assert(sizeof(Point) == 2 * sizeof(double), "Point must be two packed doubles");
+struct FlatRef {
+    const double* p;
+    const double* data() const { return p; }
+};
+FlatRef flat_points(const std::vector<Point>& p) { return {reinterpret_cast<const double*>(p.data())}; }
+double* flat_out(std::vector<Point>& p) { return reinterpret_cast<double*>(p.data()); }
 
-std::vector<Point> points(const std::vector<double>& v)
-{
-    std::vector<Point> p(v.size() / 2);
-    for (std::size_t i = 0; i < p.size(); ++i) p[i] = Point{v[2 * i], v[2 * i + 1]};
-    return p;
-}
 
 // One-net scratch netlist of terminal pins at the given positions (pin 0 drives the rest).
 struct PointNet {
@@ -355,9 +352,9 @@ PinPositions pin_positions(const Netlist& nl, const std::vector<Point>& cell_pos
     auto S = session(nl, core_only({}));
     const auto xy = flat_points(cell_pos);
     ck(tdpg_set_positions(S->s, xy.data()));
-    std::vector<double> out(2 * nl.pins.size());
-    ck(tdpg_pin_positions(S->s, out.data()));
-    return points(out);
+    PinPositions out(nl.pins.size());
+    ck(tdpg_pin_positions(S->s, flat_out(out)));
+    return out;
 }
 
 // ---- timing graph ----------------------------------------------------------------------------------
@@ -633,9 +630,8 @@ DensityResult DensityGrid::evaluate(const Netlist& nl, const std::vector<Point>&
     ck(tdpg_set_positions(S->s, xy.data()));
     ck(tdpg_set_grid(S->s, nx_, ny_, target_density_));
     DensityResult r;
-    std::vector<double> d(2 * nl.cells.size());
-    ck(tdpg_density(S->s, &r.value, &r.overflow, d.data()));
-    r.d_cell = points(d);
+    r.d_cell.resize(nl.cells.size());
+    ck(tdpg_density(S->s, &r.value, &r.overflow, flat_out(r.d_cell)));
     return r;
 }
 
@@ -970,9 +966,8 @@ PlacementOutcome place_on(const std::shared_ptr<Sess>& S, const Design& design, 
     tdpg_set_round_callback(S->s, nullptr, nullptr);
     ck(rc);
     PlacementOutcome out;
-    std::vector<double> pos(2 * nl.cells.size());
-    ck(tdpg_get_positions(S->s, pos.data()));
-    out.positions = points(pos);
+    out.positions.resize(nl.cells.size());
+    ck(tdpg_get_positions(S->s, flat_out(out.positions)));
     for (int i = 0; i < n_rows; ++i) {
         const tdpg_trace_row& r = rows[static_cast<std::size_t>(i)];
         TraceRow t;
