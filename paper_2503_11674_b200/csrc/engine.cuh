@@ -53,8 +53,8 @@ struct Grid {
     double td = 0.0;
     double x0 = 0, y0 = 0, bw = 0, bh = 0, cap = 0, total_movable = 0;
     double scale = 1.0, inv_scale = 1.0; // fixed-point occupancy: q = rint(w * scale)
-    // limbs of the windowed scatter's shared accumulators: one footprint entry is below 2^(24 limbs), so
-    // 256 of them per block fit each 32-bit limb (2 from ~4K cells up, 3 otherwise)
+    // limbs of the windowed scatter's shared accumulators, so that 256 footprint entries per block fit each
+    // 32-bit limb: 2 when every entry is below 2^45 (designs from ~30K cells up), 3 otherwise (session.cu)
     int limbs = 3;
     bool has_fixed = false;
     DBuf<long long> acc;

@@ -257,8 +257,9 @@ void ensure_grid(tdpg_session* s, int nx, int ny, double td)
     const int k = std::min(60 - ex, 1000);
     g.scale = std::ldexp(1.0, k);
     g.inv_scale = std::ldexp(1.0, -k);
-    // an entry is area * wx * wy * scale with weights <= 1 (x2 margin): below 2^48 -> two 24-bit limbs
-    g.limbs = (2.0 * amax * g.scale < std::ldexp(1.0, 48)) ? 2 : 3;
+    // an entry is area * wx * wy * scale with weights <= 0.75 (x2 margin): below 2^45 -> two limbs (a 23-bit low
+    // part and a signed high part below 2^22, 256 of them per bin and block within int32), else three
+    g.limbs = (2.0 * amax * g.scale < std::ldexp(1.0, 45)) ? 2 : 3;
     const long long B = g.bins();
     g.acc.alloc(B);
     g.acc.zero(s->st);
