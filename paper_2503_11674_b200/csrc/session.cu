@@ -135,8 +135,10 @@ __global__ void k_entry_layout(int N, EntryLayout L, const int* __restrict__ ord
 }
 
 // Sink order of each net (pin_pairs.cpp:22-34 accumulates a driver's pair terms in ascending sink pin id):
-// rank of every sink by pin id (O(k^2) per net; nets are a handful of pins), the class nets' 3-bit slot words,
-// the generic nets' slot lists, and per sink its (net index, slot) and driver.
+// rank of every sink by pin id (O(k^2) per net, for nets of up to kRankOnDevice pins; the host sorts the
+// few larger ones), the class nets' 3-bit slot words, the generic nets' slot lists, and per sink its
+// (net index, slot) and driver.
+constexpr int kRankOnDevice = 256;
 __global__ void k_pair_tables(int N, int gen0, int gen1, const int* __restrict__ order,
                               const int* __restrict__ gen_start, const int* __restrict__ net_start,
                               const int* __restrict__ net_pins, uint32_t* __restrict__ ord, int* __restrict__ gen_ord,
@@ -150,9 +152,10 @@ __global__ void k_pair_tables(int N, int gen0, int gen1, const int* __restrict__
     uint32_t w = 0;
     for (int j = 1; j < k; ++j) {
         const int pj = net_pins[b0 + j];
+        pin_driver[pj] = drv;
+        if (k > kRankOnDevice) continue; // (a generic net: gen_ord from the host)
         int r = 0;
         for (int q = 1; q < k; ++q) r += net_pins[b0 + q] < pj ? 1 : 0; // (pins on a net are distinct)
-        pin_driver[pj] = drv;
         if (generic) {
             gen_ord[gen_start[i] + r] = j;
         } else {
@@ -636,6 +639,19 @@ int tdpg_session_create(const tdpg_netlist* d, tdpg_session** out)
                                                                 s->net_start, s->net_pins, s->pp_ord, s->wa_gen_ord,
                                                                 s->pin_loc, s->pin_driver);
         CK_LAUNCH();
+        for (int i = cnt[0]; i < cnt[1]; ++i) { // generic nets too large for the device rank loop
+            const int n = order[i], b0 = ns[n], k = ns[n + 1] - b0;
+            if (k <= kRankOnDevice) continue;
+            std::vector<std::pair<int, int>> sk;
+            sk.reserve(k - 1);
+            for (int j = 1; j < k; ++j) sk.emplace_back(net_pins[b0 + j], j);
+            std::sort(sk.begin(), sk.end());
+            std::vector<int> go(k - 1);
+            for (int q = 0; q + 1 < k; ++q) go[q] = sk[q].second;
+            CK(cudaMemcpyAsync(s->wa_gen_ord.p + gen_start[i], go.data(), sizeof(int) * (k - 1), cudaMemcpyHostToDevice,
+                               s->st));
+            CK(cudaStreamSynchronize(s->st)); // (go is a temporary)
+        }
         s->pp_mask.alloc(std::max(N, 1));
         s->pp_mask.zero(s->st);
         s->ppw_e.alloc(std::max(pos, 1));

@@ -135,3 +135,39 @@ def test_high_fanout_nets_generic_path():
     d.validate()
     xy = d.positions.copy()
     _objective_parity(d, xy, 16, 16, tol=1e-9)
+
+
+@pytest.mark.parametrize("fan", [40, 300])
+def test_huge_fanout_pairs_in_the_loop(fan):
+    """A net of `fan` sinks, every sink on its own violated path (source -> sink cell -> endpoint), so the
+    engine's fused pin-pair term carries one pair per sink on that net: the driver's terms are summed in
+    ascending sink pin id (the generic nets' order list; above 256 sinks it is sorted on the host at session
+    creation).  Placement trace against the oracle, timing rounds included."""
+    b = Builder((0, 0, 200, 200), 1.0, 0.01, 0.01)
+    rng = np.random.default_rng(fan)
+    s = b.terminal("S", (0, 100), OUT)
+    b.src.append(s)
+    sinks = []
+    for j in rng.permutation(fan):  # (sink pin ids not in net order)
+        c = b.cell(f"c{j}", 1.0, 1.0, 0.5, tuple(rng.uniform(0, 199, 2)))
+        i = b.pin(f"c{j}.i", c, IN, 0.2, (0.5, 0.5))
+        o = b.pin(f"c{j}.o", c, OUT, 0.0, (0.9, 0.9))
+        e = b.terminal(f"E{j}", tuple(rng.uniform(0, 200, 2)), IN, 0.3)
+        b.eps.append(e)
+        b.net(f"o{j}", o, [e])
+        sinks.append(i)
+    b.net("big", s, sinks)
+    d = b.finish()
+    d.validate()
+    o = Oracle(d)
+    d.clock_period = float(np.quantile(o.sta(d.positions)["arr"][d.endpoints], 0.3))  # most endpoints fail
+    s_, o = Session(d), Oracle(d)
+    cfg = {"max_iters": 25, "timing_start_iter": 3, "m": 4, "grid_nx": 8, "grid_ny": 8, "seed": 2}
+    ps, po = s_.place(cfg), o.place(cfg)
+    assert len(ps["ledger"][0]) > fan // 2  # pairs on the big net are in play
+    assert len(ps["trace"]) == len(po["trace"])
+    for rs, ro in zip(ps["trace"], po["trace"]):
+        assert abs(rs.hpwl - ro.hpwl) <= 1e-9 * ro.hpwl, (rs.iter, rs.hpwl, ro.hpwl)
+        assert abs(rs.pp_term - ro.pp_term) <= 1e-9 * max(1.0, abs(ro.pp_term)), (rs.iter, rs.pp_term, ro.pp_term)
+        if ro.has_timing:
+            assert abs(rs.tns - ro.tns) <= 1e-9 * max(1.0, abs(ro.tns)), (rs.iter, rs.tns, ro.tns)
