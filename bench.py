@@ -386,6 +386,8 @@ def traffic_for(d, grid, kernel):
 
 def maxr_dev(x, torch):
     import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(x)
     t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -407,7 +409,11 @@ def run_ours(args):
     from paper_2503_11674_b200.engine import Session
 
     mode = args.mode or ("partition" if world > 1 else "replicas")
-    partition = world > 1 and mode == "partition"
+    # (--mode partition at one GPU: the partitioned engine over a one-rank NCCL communicator, its all-reduces
+    # captured in the iteration graph as at N > 1 — the N = 1 point of the partitioned scaling curve)
+    partition = mode == "partition" and (world > 1 or args.mode == "partition")
+    if partition and world == 1:
+        os.environ["TDPG_COMM_WORLD1"] = "1"
     d, gen_s, source = load_or_make(args, make_design, 1 if partition else 1 + rank)  # partition: one design
     W, K = args.warmup, args.steps
     total_iters = W + K + 64
@@ -547,7 +553,7 @@ def run_ours(args):
         "scaling": "strong" if partition else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, d, world),
         "mode": ("nets and cells partitioned: NCCL all-reduces of the density grid and of the cell gradient inside "
-                 "the iteration graph" if partition else "replicas") if world > 1 else "single GPU",
+                 "the iteration graph" if partition else "replicas") if world > 1 or partition else "single GPU",
         "partition": comm,
         "timed_window": {"refreshes": refreshes, "refresh_ms_each": round(refresh_ms / max(refreshes, 1), 3),
                          "paths_extracted": paths_timed, "path_pins_extracted": st1["path_pins"] - st0["path_pins"],

@@ -269,6 +269,7 @@ struct tdpg_session {
 
     // partitioned multi-GPU mode (partition.cu): this rank's WA block range, NCCL communicator
     int part_rank = 0, part_world = 1, part_b0 = 0, part_b1 = 0;
+    bool part_comm1 = false; // a one-rank NCCL communicator drives the partitioned engine (TDPG_COMM_WORLD1 test)
     bool part_active = false; // WA launches honour the range only while the partitioned graph is recorded
     void* comm = nullptr; // ncclComm_t
 

@@ -130,7 +130,7 @@ void set_partition(tdpg_session* s, int rank, int world)
     const auto b = partition_bounds(wa_block_weights(s->N, s->h_net_start.data()), world);
     if (b.back() != s->n_wa_blocks && !(s->n_wa_blocks == 1 && b.back() == 0))
         throw Error(TDPG_ERR_INTERNAL, "partition plan does not match the WA block layout");
-    s->part_rank = rank, s->part_world = world;
+    s->part_rank = rank, s->part_world = world, s->part_comm1 = false;
     s->part_b0 = b[rank], s->part_b1 = world == 1 ? s->n_wa_blocks : b[rank + 1];
     engine_release(s); // the iteration graph depends on the partition: tdpg_engine_init again
 }
@@ -187,7 +187,11 @@ int tdpg_comm_init(tdpg_session* s, int32_t rank, int32_t world, const uint8_t i
     API_BEGIN
     set_partition(s, rank, world);
     comm_destroy(s);
-    if (world > 1) {
+    // TDPG_COMM_WORLD1=1: a one-rank communicator still drives the partitioned engine (its graph with the
+    // NCCL all-reduces captured in it), so that path runs on a single GPU (tests/test_partition_gpu.py)
+    const char* w1 = std::getenv("TDPG_COMM_WORLD1");
+    s->part_comm1 = world == 1 && w1 && std::atoi(w1) != 0;
+    if (world > 1 || s->part_comm1) {
         ncclUniqueId u;
         std::memcpy(&u, id, sizeof u);
         CK(cudaSetDevice(s->device));

@@ -616,8 +616,8 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->part.reserve(2 * E->nb_wa + E->nb_pp + 2 * E->nb_d + 8);
     E->part.zero(s->st);
     E->kernels_per_iter = 8 + (s->grid.n_wide > 0 ? 2 : 0); // (+ wide-cell scatter and density gradient)
-    if (s->part_world <= 1 && fin_split()) E->kernels_per_iter += 1; // (finalize in two halves)
-    E->partitioned = s->part_world > 1;
+    E->partitioned = s->part_world > 1 || s->part_comm1;
+    if (!E->partitioned && fin_split()) E->kernels_per_iter += 1; // (finalize in two halves)
     if (E->partitioned) { // this rank's slice of the spatial order (the density scatter / gradient share)
         const long long nm = s->grid.n_movable;
         E->mov_lo = static_cast<int>(nm * s->part_rank / s->part_world);

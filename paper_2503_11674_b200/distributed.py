@@ -29,7 +29,11 @@ def broadcast_unique_id(rank: int, make_id=engine.comm_unique_id) -> bytes:
 
 def init_partitioned(session: "engine.Session", rank: int, world: int) -> None:
     """Give `session` this rank's share of the nets and an NCCL communicator over all ranks."""
-    session.comm_init(rank, world, broadcast_unique_id(rank) if world > 1 else bytes(128))
+    if world > 1:
+        uid = broadcast_unique_id(rank)
+    else:  # (a one-rank communicator only when TDPG_COMM_WORLD1 asks for one: it needs a real id)
+        uid = engine.comm_unique_id() if os.environ.get("TDPG_COMM_WORLD1") else bytes(128)
+    session.comm_init(rank, world, uid)
 
 
 def max_over_ranks(value: float, device=None) -> float:

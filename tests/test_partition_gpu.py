@@ -71,3 +71,24 @@ def test_partitioned_requires_communicator(design):
     s.engine_init({"max_iters": 5, "grid_nx": 16, "grid_ny": 16})
     with pytest.raises(Exception, match="communicator"):
         s.iterate(1)
+
+
+def test_nccl_graph_path_one_rank(design, monkeypatch):
+    """The multi-GPU engine's own data path — NCCL all-reduces of the int64 density grid and the gradient
+    buffer captured inside the iteration graph — on one GPU with a one-rank communicator (TDPG_COMM_WORLD1):
+    the all-reduces are identities, so the run must reproduce the single-GPU engine (same fold order, same
+    density gradient addition) row for row."""
+    from paper_2503_11674_b200.engine import comm_unique_id
+    monkeypatch.setenv("TDPG_COMM_WORLD1", "1")
+    cfg = {"max_iters": 40, "timing_start_iter": 10, "m": 5, "grid_nx": 32, "grid_ny": 32, "seed": 3}
+    ref = Session(design).place(cfg)
+    s = Session(design)
+    s.comm_init(0, 1, comm_unique_id())
+    got = s.place(cfg)
+    assert len(got["trace"]) == len(ref["trace"]) == 40
+    assert any(r.has_timing and r.wns < 0 for r in ref["trace"])
+    for rg, rr in zip(got["trace"], ref["trace"]):
+        assert abs(rg.hpwl - rr.hpwl) <= 1e-9 * rr.hpwl, (rg.iter, rg.hpwl, rr.hpwl)
+        assert abs(rg.tns - rr.tns) <= 1e-9 * max(1.0, abs(rr.tns)), (rg.iter, rg.tns, rr.tns)
+    assert np.allclose(got["positions"], ref["positions"], rtol=0, atol=1e-9 * (design.core[2] - design.core[0]))
+    s.comm_bench(5)  # (the two collectives alone, on the communicator)
