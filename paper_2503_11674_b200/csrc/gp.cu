@@ -1183,7 +1183,8 @@ __global__ void __launch_bounds__(kFinBlock) k_fin_density(FinArgs a, Ctrl* ctrl
         cur->lr = a.sched[it].lr, cur->c1 = a.sched[it].c1, cur->c2 = a.sched[it].c2;
         cur->do_adam = 1;
     }
-    ctrl->iter = it + 1;
+    // (ctrl->iter advances in k_fin_terms: kernels beside this one — the partitioned engine's λ · density
+    // gradient fold — still read this iteration's index)
 }
 
 __global__ void __launch_bounds__(kFinBlock) k_fin_terms(FinArgs a, Ctrl* ctrl, const IterCur* cur)
@@ -1214,6 +1215,7 @@ __global__ void __launch_bounds__(kFinBlock) k_fin_terms(FinArgs a, Ctrl* ctrl, 
     if (a.timing_row_clear) a.timing_row_clear[0] = 0.0;
     ctrl->rows = it + 1;
     if (cur->stop) ctrl->stopped = 1;
+    else ctrl->iter = it + 1;
 }
 
 // =====================================================================================

@@ -266,6 +266,7 @@ bool fin_split()
 
 void capture_iteration(tdpg_session* s, Engine& E)
 {
+    const bool split = fin_split(); // (the finalize in two halves, both graph forms)
     if (E.gexec) cudaGraphExecDestroy(E.gexec), E.gexec = nullptr;
     double* part_wl = E.part.p;
     double* part_hp = part_wl + E.nb_wa;
@@ -309,6 +310,11 @@ void capture_iteration(tdpg_session* s, Engine& E)
                 comm_allreduce_i64(s, s->grid.acc.p, static_cast<size_t>(s->grid.bins()), E.br[0]);
             }
             launch_density_bins_ctrl(s, part_d, E.nb_d, E.ctrl);
+            if (split) { // the density half of the finalize beside the slice's density gradient (see below)
+                CK(cudaEventRecord(E.ev_bins, E.br[0]));
+                CK(cudaStreamWaitEvent(E.br[3], E.ev_bins, 0));
+                launch_fin_density(s, fa, E.ctrl, E.cur, E.br[3]);
+            }
             launch_dens_grad_part(s, E.ctrl, E.br[0], lo, hi);
             s->st = main;
             cudaStream_t wa_st[Engine::kBranches] = {main};
@@ -326,6 +332,17 @@ void capture_iteration(tdpg_session* s, Engine& E)
         };
         // B: terms from the reduced partials, cells from the reduced fold (density gradient included)
         auto record_b = [&] {
+            if (split) { // the terms half (reduced partials) beside the cell kernel
+                cudaStream_t main = s->st;
+                CK(cudaEventRecord(E.ev_fork, main));
+                CK(cudaStreamWaitEvent(E.br[4], E.ev_fork, 0));
+                launch_fin_terms(s, fp, E.ctrl, E.cur, E.br[4]);
+                CK(cudaEventRecord(E.ev_join[4], E.br[4]));
+                launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
+                             false, folded, true);
+                CK(cudaStreamWaitEvent(main, E.ev_join[4], 0));
+                return;
+            }
             launch_finalize(s, fp, E.ctrl, E.cur);
             launch_cells(s, nullptr, E.m, E.v, E.cfg.adam_beta1, E.cfg.adam_beta2, E.cfg.adam_eps, E.cur, E.ctrl,
                          false, folded, true);
@@ -347,7 +364,6 @@ void capture_iteration(tdpg_session* s, Engine& E)
         return;
     }
     s->pdl_graph = pdl_gp();
-    const bool split = fin_split();
     auto record = [&](bool sort) {
         // fork: density chain (scatter -> bins -> density gradient) on branch 0, the WA size classes
         // (+ fused pin pairs, dense ledger) on the main stream and branches 1..7; join -> finalize -> cells
@@ -617,7 +633,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     E->part.zero(s->st);
     E->kernels_per_iter = 8 + (s->grid.n_wide > 0 ? 2 : 0); // (+ wide-cell scatter and density gradient)
     E->partitioned = s->part_world > 1 || s->part_comm1;
-    if (!E->partitioned && fin_split()) E->kernels_per_iter += 1; // (finalize in two halves)
+    if (fin_split()) E->kernels_per_iter += 1; // (finalize in two halves)
     if (E->partitioned) { // this rank's slice of the spatial order (the density scatter / gradient share)
         const long long nm = s->grid.n_movable;
         E->mov_lo = static_cast<int>(nm * s->part_rank / s->part_world);

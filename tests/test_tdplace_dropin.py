@@ -113,6 +113,26 @@ def test_report_paths_topn_and_k():
         assert rep["unique_pin_pairs"] == ref["unique_pin_pairs"] and rep["unique_endpoints"] == ref["unique_endpoints"]
 
 
+def _ref_compare_isolated(dj, cfgs, attempts=2):
+    """The compiled reference's run_compare + compare_to_csv in a child process (the reference is third-party
+    test infrastructure: a crash inside it must not take the test session down; one retry)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import json, sys; sys.path.insert(0, %r)\n"
+            "from oracle.oracle import RefOracle\nfrom paper_2503_11674_b200.design import Design\n"
+            "a = json.loads(sys.stdin.read())\n"
+            "print(RefOracle(Design.from_json(a['design'])).compare(a['cfgs']), end='')\n") % root
+    payload = json.dumps({"design": dj, "cfgs": cfgs})
+    for _ in range(attempts):
+        r = subprocess.run([sys.executable, "-c", code], input=payload, capture_output=True, text=True, timeout=600)
+        if r.returncode == 0:
+            return r.stdout.splitlines()
+    raise AssertionError("reference compare failed: rc %d\n%s" % (r.returncode, r.stderr[-2000:]))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("parallel", [False, True])
 def test_compare_csv_against_reference(parallel):
@@ -127,7 +147,7 @@ def test_compare_csv_against_reference(parallel):
     cfgs = [dict(base, name="endpoint"), dict(base, name="endpoint_k3", k=3), dict(base, name="topn", extraction="topn"),
             dict(base, name="netw", net_weighting=True, beta=0.0)]
     ours = tdplace.compare_csv(dj, cfgs, parallel=parallel).splitlines()
-    ref = RefOracle(Design.from_json(dj)).compare(cfgs).splitlines()
+    ref = _ref_compare_isolated(dj, cfgs)
     assert ours[0] == ref[0] and len(ours) == len(ref) == 5
     for a, b in zip(ours[1:], ref[1:]):
         ra, rb = a.split(","), b.split(",")
