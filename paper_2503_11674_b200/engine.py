@@ -17,7 +17,7 @@ import numpy as np
 from .design import Design, TdpgConfig, TdpgNetlist, TdpgTraceRow, make_config
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtdpgpu.so")
+LIB_PATH = os.environ.get("TDPG_LIB") or os.path.join(HERE, "libtdpgpu.so")  # (TDPG_LIB: A/B of a variant build)
 
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
