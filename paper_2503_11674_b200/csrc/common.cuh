@@ -5,6 +5,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -96,6 +98,8 @@ struct DBuf {
         if (count) {
             CK(cudaMalloc(&p, count * sizeof(T)));
             ++dbuf_epoch();
+            static const bool trace = [] { const char* e = std::getenv("TDPG_TRACE_ALLOC"); return e && *e == '1'; }();
+            if (trace) std::fprintf(stderr, "dbuf alloc %zu x %zu B (epoch %llu)\n", count, sizeof(T), dbuf_epoch().load());
         }
     }
     // grow-only

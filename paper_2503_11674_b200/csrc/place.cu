@@ -136,8 +136,13 @@ struct Engine {
         double c[3];
         session_consts(s, c);
         if (!old_gexec || old_epoch != dbuf_epoch() || partitioned || old_sort_every != sort_every ||
-            !graph_cfg_equal(old_cfg, cfg) || std::memcmp(c, old_consts, sizeof c) != 0)
+            !graph_cfg_equal(old_cfg, cfg) || std::memcmp(c, old_consts, sizeof c) != 0) {
+            if (const char* e = std::getenv("TDPG_TRACE_INIT"); e && std::atoi(e) != 0)
+                std::fprintf(stderr, "engine_init graphs not adopted: old %d epoch %llu/%llu part %d sort %d/%d cfg %d consts %d\n",
+                             old_gexec != nullptr, (unsigned long long)old_epoch, dbuf_epoch().load(), partitioned, old_sort_every, sort_every,
+                             graph_cfg_equal(old_cfg, cfg), std::memcmp(c, old_consts, sizeof c) == 0);
             return false;
+        }
         std::swap(gexec, old_gexec), std::swap(gexec_sorted, old_gexec_sorted);
         std::swap(refresh_gexec, old_refresh), std::swap(sort_gexec, old_sort);
         refresh_lonly = old_lonly, epoch = old_epoch;
@@ -654,6 +659,11 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
     if (E->cfg.extraction == 0 && E->cfg.k > 1) kbest_refresh_reserve(s, E->cfg.k); // (the k-best refresh graph)
     s->ex_counts.zero(s->st); // (the refresh graph accumulates the run's path totals in [3], [4])
     place_tail_reserve(s); // (so a later run of the session finds every buffer where its graphs point)
+    if (cfg->lambda0 <= 0.0) { // lambda_auto's scratch (an allocation after the capture would re-capture)
+        const int nb_d = bins_blocks(s), nb = 148 * 2;
+        s->lam_scratch.reserve(2 * static_cast<size_t>(s->C) + 2 * nb_d + 64 + 2 * nb);
+        s->part.reserve(2 * wa_blocks(s) + pp_blocks(s) + 2 * nb_d + 64);
+    }
     s->pin_xy_external = false;
     sort_cells_spatial(s);
     tr.mark("reserve + sort");
@@ -667,7 +677,7 @@ void engine_init(tdpg_session* s, const tdpg_config* cfg, const uint8_t* pos_exp
         G.refresh_lonly = s->pins_stale, s->pins_stale = false; // (recorded, not run)
         tr.mark("refresh graph");
         G.sort_gexec = capture(s, [&] { sort_cells_spatial(s); });
-        G.epoch = dbuf_epoch(); // (an allocation by lambda_auto below re-captures at the first run)
+        G.epoch = dbuf_epoch();
         tr.mark("sort graph");
     } else {
         tr.mark("graphs adopted");

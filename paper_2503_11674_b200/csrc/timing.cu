@@ -1954,6 +1954,7 @@ void place_tail_reserve(tdpg_session* s)
     cub_scratch(s, bytes);
     s->part.reserve(2 * static_cast<size_t>(wa_blocks(s)) + 8);
     s->sta_out.reserve(4);
+    s->led_key.reserve(static_cast<size_t>(P) + 1), s->led_w.reserve(static_cast<size_t>(P) + 1); // (Q <= P)
 }
 
 // The dense ledger's pairs (weight > 0), compacted in any order (the sort below fixes it).
