@@ -175,7 +175,8 @@ int tdpg_set_density_model(tdpg_session* s, int32_t model);
 /* Last electrostatic evaluation's charge map rho and potential psi ([nx*ny], bin bx*ny + by). */
 int tdpg_density_fields(tdpg_session* s, double* rho, double* psi);
 /* Measurement aid (no reference counterpart): shared-memory atomics the density scatter issues at the
-   session's positions, lo_hi[0] = low-word, lo_hi[1] = high-word atomics. */
+   session's positions: lo_hi[0] = low-limb atomics (one per non-zero footprint entry), lo_hi[1] = upper-limb
+   atomics (Grid limbs - 1 per such entry). */
 int tdpg_density_atomics(tdpg_session* s, int64_t lo_hi[2]);
 
 /* ---- pin-pair ledger (PinPairWeights) ------------------------------- */

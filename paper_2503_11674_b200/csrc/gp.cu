@@ -1912,10 +1912,10 @@ int tdpg_wirelength(tdpg_session* s, double gamma, const double* net_w, double* 
 }
 
 // Shared-memory atomics the windowed scatter issues at the session's positions (measurement aid for the
-// roofline limiter): one 32-bit atomic per non-zero footprint entry of a five-bin cell, a second when the
-// entry's fixed-point value needs the high word (carries from the low word are not counted).
+// roofline limiter): per non-zero footprint entry of a five-bin cell one low-limb atomic ([0]) and
+// Grid::limbs - 1 upper-limb atomics ([1]), as k_density_scatter_limbs issues them.
 __global__ void k_count_scatter_atomics(int n_mov, const int* __restrict__ perm, const double2* __restrict__ cell_xy,
-                                        const double2* __restrict__ cell_wh, GridDev g,
+                                        const double2* __restrict__ cell_wh, GridDev g, int limbs,
                                         unsigned long long* __restrict__ out)
 {
     const int i = blockIdx.x * kBlock + threadIdx.x;
@@ -1933,7 +1933,7 @@ __global__ void k_count_scatter_atomics(int n_mov, const int* __restrict__ perm,
                 const double aw = area * wx[a];
                 for (int j = 0; j < kF5; ++j) {
                     const long long q = __double2ll_rn(aw * wy[j] * g.scale);
-                    lo += q != 0, hi += (static_cast<unsigned long long>(q) >> 32) != 0;
+                    lo += q != 0, hi += q != 0 ? limbs - 1 : 0;
                 }
             }
         }
@@ -1952,7 +1952,7 @@ int tdpg_density_atomics(tdpg_session* s, int64_t* lo_hi)
     const int n_mov = s->grid.n_movable;
     if (n_mov > 0)
         k_count_scatter_atomics<<<blocks_for(n_mov, kBlock), kBlock, 0, s->st>>>(n_mov, s->grid.perm, s->cell_xy,
-                                                                                s->cell_wh, grid_dev(s), out);
+                                                                                s->cell_wh, grid_dev(s), s->grid.limbs, out);
     CK_LAUNCH();
     unsigned long long h[2];
     out.download(h, 2, s->st);

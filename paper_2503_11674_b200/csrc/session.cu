@@ -339,11 +339,28 @@ Stager& stager()
     return *s;
 }
 
+// Page-locked (cudaHostAlloc'd or cudaHostRegister'ed) host memory: the DMA engines read / write it directly,
+// so the staging copy would only add a host memcpy.
+bool host_pinned(const void* p)
+{
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError(); // (clear the sticky-free query error)
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st)
 {
     if (bytes == 0) return;
-    if (bytes < (size_t(4) << 20)) {
+    if (bytes < (size_t(4) << 20)) { // (pageable: the driver stages it before returning)
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    if (host_pinned(src)) { // DMA straight from the caller's buffer, which it may reuse once we return
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
         return;
     }
     Stager& S = stager();
@@ -385,7 +402,7 @@ namespace tdpg {
 void download_bytes(void* dst, const void* src, size_t bytes, cudaStream_t st)
 {
     if (bytes == 0) return;
-    if (bytes < (size_t(4) << 20)) {
+    if (bytes < (size_t(4) << 20) || host_pinned(dst)) {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         return;

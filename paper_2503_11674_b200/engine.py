@@ -243,7 +243,7 @@ class Session:
         _check(self.lib.tdpg_set_density_model(self.h, int(m)))
 
     def density_atomics(self, nx, ny, td=0.6, xy=None):
-        """(low-word, high-word) shared-memory atomics of the density scatter at these positions."""
+        """(low-limb, upper-limb) shared-memory atomics of the density scatter at these positions."""
         self._pos(xy)
         _check(self.lib.tdpg_set_grid(self.h, nx, ny, td))
         out = np.zeros(2, np.int64)
