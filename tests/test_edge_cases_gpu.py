@@ -171,3 +171,27 @@ def test_huge_fanout_pairs_in_the_loop(fan):
         assert abs(rs.pp_term - ro.pp_term) <= 1e-9 * max(1.0, abs(ro.pp_term)), (rs.iter, rs.pp_term, ro.pp_term)
         if ro.has_timing:
             assert abs(rs.tns - ro.tns) <= 1e-9 * max(1.0, abs(ro.tns)), (rs.iter, rs.tns, ro.tns)
+
+
+def test_place_host_pinned_and_pageable_buffers_agree():
+    """tdpg_place through caller host buffers above the 4 MB staging threshold: page-locked buffers are DMA'd
+    directly, pageable ones go through the staging pair; both give the same bits, and a repeated call on the
+    session (which adopts the first call's graphs) reproduces them."""
+    import torch
+    d = generate(seed=2, cells=300_000, fail_frac=0.8, calibrate=False)
+    C = d.n_cells
+    assert 16 * C > 4 << 20
+    cfg = {"grid_nx": 256, "grid_ny": 256, "m": 5, "timing_start_iter": 0, "max_iters": 12, "seed": 1}
+    s = Session(d)
+    outs = []
+    for pinned in (True, False, True):
+        hin = torch.empty(2 * C, dtype=torch.float64, pin_memory=pinned)
+        hout = torch.full((2 * C,), np.nan, dtype=torch.float64, pin_memory=pinned)
+        hin.numpy()[:] = d.positions.reshape(-1)
+        rows, fin = s.place_host(cfg, hin.data_ptr(), hout.data_ptr())
+        assert rows == 12
+        outs.append((hout.numpy().copy(), fin))
+    for o, f in outs[1:]:
+        assert np.array_equal(o, outs[0][0])
+        assert f == outs[0][1]
+    assert not np.array_equal(outs[0][0], d.positions.reshape(-1))
