@@ -141,6 +141,10 @@ struct Engine {
                 std::fprintf(stderr, "engine_init graphs not adopted: old %d epoch %llu/%llu part %d sort %d/%d cfg %d consts %d\n",
                              old_gexec != nullptr, (unsigned long long)old_epoch, dbuf_epoch().load(), partitioned, old_sort_every, sort_every,
                              graph_cfg_equal(old_cfg, cfg), std::memcmp(c, old_consts, sizeof c) == 0);
+            // never adoptable now (this engine captures its own): freed here, in the call that re-captures
+            // anyway, rather than by this engine's destructor inside the next engine_init
+            for (cudaGraphExec_t* g : {&old_gexec, &old_gexec_sorted, &old_refresh, &old_sort})
+                if (*g) cudaGraphExecDestroy(*g), *g = nullptr;
             return false;
         }
         std::swap(gexec, old_gexec), std::swap(gexec_sorted, old_gexec_sorted);
