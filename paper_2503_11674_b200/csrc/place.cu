@@ -209,29 +209,21 @@ __global__ void k_l1_pair(int C, const double2* __restrict__ a, const double2* _
     if (threadIdx.x == 0) part[2 * blockIdx.x] = sa, part[2 * blockIdx.x + 1] = sb;
 }
 
-// lambda0 "auto": |grad WL|_1 / |grad D|_1 over movable cells (placer.cpp:388-402).
+// lambda0 "auto": |grad WL|_1 / |grad D|_1 over movable cells (placer.cpp:388-402).  One evaluation at
+// lambda = 0 leaves both: d_cell = fold + 0 * density gradient is the wirelength gradient, and the raw
+// density gradient in dgrad is what a lambda = 1 cell pass over zero entry gradients returns (0 + 1 * g),
+// so the two norms are bitwise those of two separate passes.
 double lambda_auto(tdpg_session* s, double gamma, int kind)
 {
     evaluate_objective(s, gamma, 0.0, 0.0, kind, false, nullptr);
-    // scratch in the session's jitter stream buffer (free after the jitter): [wl gradient | part | p2]
     const int nb_d = bins_blocks(s), nb = 148 * 2;
     s->lam_scratch.reserve(2 * static_cast<size_t>(s->C) + 2 * nb_d + 64 + 2 * nb);
-    double2* wl = reinterpret_cast<double2*>(s->lam_scratch.p);
-    double* part = reinterpret_cast<double*>(wl + s->C);
-    double* p2 = part + 2 * nb_d + 64;
-    CK(cudaMemcpyAsync(wl, s->d_cell.p, sizeof(double2) * s->C, cudaMemcpyDeviceToDevice, s->st));
-    // density-only gradient: zero entry gradients, lambda = 1
-    Terms* terms = reinterpret_cast<Terms*>(part + 2 * nb_d);
-    IterCur* cur = reinterpret_cast<IterCur*>(terms + 1);
-    launch_density(s, part, nb_d);
-    FinArgs fa{};
-    fa.part_d = part, fa.nb_d = nb_d, fa.total_movable = s->grid.total_movable, fa.lambda_single = 1.0;
-    fa.terms = terms;
-    launch_finalize(s, fa, nullptr, cur);
-    s->grad_e.zero(s->st, s->E_tot);
-    launch_cells(s, s->d_cell, nullptr, nullptr, 0, 0, 0, cur, nullptr);
-    k_l1_pair<<<nb, kBlock, 0, s->st>>>(s->C, wl, s->d_cell, s->cell_fixed, p2);
+    double* p2 = s->lam_scratch.p;
+    k_l1_pair<<<nb, kBlock, 0, s->st>>>(s->C, s->d_cell, s->dgrad, s->cell_fixed, p2);
     CK_LAUNCH();
+    // the loop expects zero entry gradients where its own kernels do not write (off-net pin slots; in a
+    // partitioned engine, the other ranks' nets)
+    s->grad_e.zero(s->st, s->E_tot);
     std::vector<double> h(2 * nb);
     CK(cudaMemcpyAsync(h.data(), p2, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
