@@ -266,6 +266,11 @@ struct tdpg_session {
     int n_free = -1;                   // cells that are not fixed (host count, lazily)
     tdpg::DBuf<double> lam_scratch;    // lambda_auto scratch
     tdpg::DBuf<uint8_t> jit_expl;
+    // jit_flag / jit_rank are a function of pos_explicit (cell_fixed is fixed per session): the host copy
+    // of the last pos_explicit (empty = none given) and the buffers it was computed into
+    std::vector<uint8_t> h_jit_expl;
+    bool jit_flags_ok = false, jit_expl_null = false;
+    const void* jit_flags_at[2] = {nullptr, nullptr};
 
     // partitioned multi-GPU mode (partition.cu): this rank's WA block range, NCCL communicator
     int part_rank = 0, part_world = 1, part_b0 = 0, part_b1 = 0;

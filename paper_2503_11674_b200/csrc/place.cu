@@ -546,14 +546,25 @@ void jitter_positions(tdpg_session* s, const tdpg_config* cfg, const uint8_t* po
 {
     const int C = s->C;
     s->jit_flag.reserve(C + 1), s->jit_rank.reserve(C + 1), s->jit_raw.reserve(2 * static_cast<size_t>(C) + 1);
-    const uint8_t* ex = nullptr;
-    if (pos_explicit) s->jit_expl.upload(pos_explicit, C, s->st), ex = s->jit_expl.p;
-    k_jit_flags<<<blocks_for(C + 1, kBlock), kBlock, 0, s->st>>>(C, s->cell_fixed, ex, s->jit_flag);
-    CK_LAUNCH();
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st);
-    void* tmp = cub_scratch(s, bytes);
-    CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st));
+    // which cells take a draw and their rank among them: recomputed only when pos_explicit changed
+    const bool same = s->jit_flags_ok && s->jit_flags_at[0] == s->jit_flag.p && s->jit_flags_at[1] == s->jit_rank.p &&
+                      (pos_explicit ? !s->jit_expl_null && s->h_jit_expl.size() == static_cast<size_t>(C) &&
+                                          std::memcmp(s->h_jit_expl.data(), pos_explicit, C) == 0
+                                    : s->jit_expl_null);
+    if (!same) {
+        const uint8_t* ex = nullptr;
+        if (pos_explicit) s->jit_expl.upload(pos_explicit, C, s->st), ex = s->jit_expl.p;
+        k_jit_flags<<<blocks_for(C + 1, kBlock), kBlock, 0, s->st>>>(C, s->cell_fixed, ex, s->jit_flag);
+        CK_LAUNCH();
+        size_t bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st);
+        void* tmp = cub_scratch(s, bytes);
+        CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, s->jit_flag.p, s->jit_rank.p, C + 1, s->st));
+        s->jit_expl_null = pos_explicit == nullptr;
+        if (pos_explicit) s->h_jit_expl.assign(pos_explicit, pos_explicit + C);
+        else s->h_jit_expl.clear();
+        s->jit_flags_at[0] = s->jit_flag.p, s->jit_flags_at[1] = s->jit_rank.p, s->jit_flags_ok = true;
+    }
     // the raw stream depends on the seed only: every free cell's two draws are generated once per seed
     // (explicitly placed cells only shorten the prefix used) and kept for the next run with that seed
     if (s->n_free < 0) {
